@@ -1,0 +1,148 @@
+/* hemul_gpu.h — C-ABI of the B200 HE Mul path (libhemul_gpu.so).
+ *
+ * The reference (/root/reference/proj, "hemul") has no FFI: its boundary is the
+ * C++ API in namespace hemul. Each entry point below replaces one reference
+ * interface, cited as file:line (paths relative to proj/core/):
+ *
+ *   hemul_gpu_create        Scheme::Scheme(const Params&)        include/hemul/heaan.hpp:74
+ *                           + make_params                        src/params.cpp:64-74
+ *   hemul_gpu_set_level     Scheme::warm_level(log_q, nullptr)   include/hemul/heaan.hpp:100
+ *                           (Scheme::level, tables only)         src/heaan.cpp:119-150
+ *   hemul_gpu_set_evk       Scheme::warm_level(log_q, &evk)      src/heaan.cpp:152-167
+ *   hemul_gpu_he_mul        Scheme::he_mul(c1, c2, evk)          include/hemul/heaan.hpp:91-92,
+ *                                                                src/heaan.cpp:339-410
+ *   hemul_gpu_rescale       Scheme::rescale(c)                   src/heaan.cpp:328-337
+ *   hemul_gpu_stage_ms      Scheme::timers (StageTimers)         include/hemul/counters.hpp:13,44-57
+ *   hemul_gpu_ntt / _crt /  ntt_forward / ntt_inverse            include/hemul/ntt.hpp:34-39
+ *   _icrt / _pointwise      crt_forward / icrt_reordered /       include/hemul/rns.hpp:62-85
+ *                           rns_pointwise_mul
+ *   hemul_gpu_level_info    PrimeSet / region{1,2}_prime_count   include/hemul/params.hpp:39-67
+ *
+ * Conventions
+ *  - Polynomials use the reference BigPoly layout (poly.hpp:15-26): n x limbs
+ *    u64, data[i*limbs + k], little-endian 64-bit limbs, limbs =
+ *    ceil(log_q/64), top limb masked. Batches are `batch` such polynomials
+ *    back to back.
+ *  - RNS matrices are prime-major, data[j*n + i] (rns.hpp:17-20 Layout::
+ *    prime_major); batches back to back.
+ *  - Every pointer may be host memory (pageable or pinned) or device memory
+ *    of the context's GPU; the library detects which with
+ *    cudaPointerGetAttributes and copies as needed on the context stream.
+ *  - No exceptions cross this boundary. Errors are status codes mirroring the
+ *    reference's exception kinds; hemul_gpu_last_error returns the message
+ *    (identical to the reference's what() string where one exists).
+ *  - A context is not thread safe (Scheme::he_mul is non-const, heaan.hpp:
+ *    91-92): use one per host thread or serialize.
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    computes returns HEMUL_E_CUDA.
+ */
+#ifndef HEMUL_GPU_H
+#define HEMUL_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hemul_gpu_ctx hemul_gpu_ctx;
+
+typedef enum {
+  HEMUL_OK = 0,
+  HEMUL_E_ARG = 1,               /* std::invalid_argument (bad size, layout, radix...) */
+  HEMUL_E_MODULUS_MISMATCH = 2,  /* "ciphertext modulus mismatch"   heaan.cpp:341-342 */
+  HEMUL_E_DEPTH = 3,             /* "multiplicative depth exhausted" heaan.cpp:344-345
+                                    "modulus exhausted; cannot rescale" heaan.cpp:329-330 */
+  HEMUL_E_CUDA = 4,              /* CUDA runtime / launch failure, or no device */
+  HEMUL_E_OOM = 5,               /* device allocation failed */
+  HEMUL_E_NO_EVK = 6             /* he_mul before set_evk at this level */
+} hemul_status;
+
+/* Stage buckets, same order as hemul::Stage (counters.hpp:13). */
+enum { HEMUL_STAGE_CRT = 0, HEMUL_STAGE_NTT, HEMUL_STAGE_INTT, HEMUL_STAGE_ICRT,
+       HEMUL_STAGE_EXTRA, HEMUL_STAGE_COUNT };
+
+/* make_params(log_p, depth, w64, log_n_override) (params.cpp:64-74) and a
+ * context on CUDA device `device`. log_n_override = 0 uses the security table
+ * (params.cpp:56-62). */
+hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_override,
+                              hemul_gpu_ctx **out);
+void hemul_gpu_destroy(hemul_gpu_ctx *ctx);
+const char *hemul_gpu_last_error(const hemul_gpu_ctx *ctx);
+/* {log_n, n, log_p, depth, log_q_max} */
+hemul_status hemul_gpu_params(const hemul_gpu_ctx *ctx, int out[5]);
+
+/* Build (or fetch from the 2-entry LRU, heaan.cpp:119-150) the tables of
+ * modulus log_q. */
+hemul_status hemul_gpu_set_level(hemul_gpu_ctx *ctx, int log_q);
+
+/* Cache the evaluation key's region-2 NTT forms at level log_q
+ * (heaan.cpp:152-167). evk polys: n x ceil(2 log_q_max / 64) limbs. evk_id
+ * identifies the key (the reference compares the EvalKey address,
+ * heaan.cpp:152; here the caller passes any stable id, 0 = always rebuild). */
+hemul_status hemul_gpu_set_evk(hemul_gpu_ctx *ctx, int log_q, const uint64_t *evk_ax,
+                               const uint64_t *evk_bx, uint64_t evk_id);
+
+/* batch independent HE Muls: out_b = rescale(relinearize(c1_b * c2_b))
+ * (heaan.cpp:339-410). Inputs n x ceil(log_q/64) limbs per poly; outputs
+ * n x ceil((log_q - log_p)/64). Checks run in the reference's order:
+ * c1_log_q != c2_log_q -> HEMUL_E_MODULUS_MISMATCH; log_q - log_p < log_p ->
+ * HEMUL_E_DEPTH. The evk must have been set at this level (or is set from
+ * evk_ax/evk_bx when those are non-null). */
+hemul_status hemul_gpu_he_mul(hemul_gpu_ctx *ctx, int c1_log_q, int c2_log_q, size_t batch,
+                              const uint64_t *c1_ax, const uint64_t *c1_bx,
+                              const uint64_t *c2_ax, const uint64_t *c2_bx,
+                              const uint64_t *evk_ax, const uint64_t *evk_bx, uint64_t evk_id,
+                              uint64_t *out_ax, uint64_t *out_bx);
+
+/* Scheme::rescale (heaan.cpp:328-337) on a batch: n x ceil(log_q/64) ->
+ * n x ceil((log_q - log_p)/64). */
+hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, const uint64_t *ax,
+                               const uint64_t *bx, uint64_t *out_ax, uint64_t *out_bx);
+
+/* Per-stage device milliseconds of the last he_mul call (CUDA events on the
+ * context stream), buckets as counters.hpp:13. Timing is only recorded when
+ * enabled (it inserts events between stages). */
+hemul_status hemul_gpu_enable_stage_timing(hemul_gpu_ctx *ctx, int on);
+hemul_status hemul_gpu_stage_ms(const hemul_gpu_ctx *ctx, double ms[HEMUL_STAGE_COUNT]);
+
+/* Region tables of level log_q: region 1 (products mod q) or 2 (key
+ * switching). Writes np and up to cap primes. */
+hemul_status hemul_gpu_level_info(hemul_gpu_ctx *ctx, int log_q, int region, int *np,
+                                  uint64_t *primes, int cap);
+
+/* ---- stage entry points (the reference's lower-level API) ---------------- */
+
+/* ntt_forward / ntt_inverse (ntt.cpp:153-197) in place over `rows` prime-major
+ * rows of n residues; row r is transformed mod prime (r % np) of the region. */
+hemul_status hemul_gpu_ntt(hemul_gpu_ctx *ctx, int log_q, int region, uint64_t *data, size_t rows,
+                           int inverse);
+/* crt_forward (rns.cpp:331-358): batch polys of n x ceil(in_bits/64) limbs ->
+ * batch x np x n residues. */
+hemul_status hemul_gpu_crt(hemul_gpu_ctx *ctx, int log_q, int region, int in_bits, size_t batch,
+                           const uint64_t *poly, uint64_t *rns);
+/* rns_pointwise_mul (rns.cpp:360-371) on batch x np x n. */
+hemul_status hemul_gpu_pointwise(hemul_gpu_ctx *ctx, int log_q, int region, size_t batch,
+                                 const uint64_t *a, const uint64_t *b, uint64_t *out);
+/* icrt_reordered (rns.cpp:395-415): batch x np x n -> batch polys mod the
+ * region target (2^log_q or 2^(log_q + log_q_max)). */
+hemul_status hemul_gpu_icrt(hemul_gpu_ctx *ctx, int log_q, int region, size_t batch,
+                            const uint64_t *rns, uint64_t *poly);
+
+/* Number of kernels this library launched since the context was created
+ * (the bench reports it as gpu_launches). */
+uint64_t hemul_gpu_launch_count(const hemul_gpu_ctx *ctx);
+
+/* ciphertext_digest (bench.cpp:35-47): FNV-1a 64 over log_q (8 bytes LE),
+ * then every word of ax, then every word of bx. Host buffers only. */
+uint64_t hemul_ciphertext_digest(int log_q, size_t words, const uint64_t *ax,
+                                 const uint64_t *bx);
+
+/* Ensures all work on the context stream finished. */
+hemul_status hemul_gpu_synchronize(hemul_gpu_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEMUL_GPU_H */

@@ -1,0 +1,752 @@
+// C-ABI implementation (include/hemul_gpu.h): context, level cache, evk
+// forms, and the HE Mul orchestration on one CUDA stream.
+//
+// Pipeline of one batched he_mul (reference: heaan.cpp:339-410), every box a
+// kernel of this library:
+//   region 1 (np1 primes, target 2^log_q)
+//     CRT x4 (ax1 bx1 ax2 bx2) -> fwd NTT (4B rows) -> tensor product
+//     (d0 = B1B2, d1 = A1B2 + A2B1, d2 = A1A2) -> iNTT (3B rows) -> iCRT (3B)
+//   region 2 (np2 primes, target 2^(log_q + log_Q))
+//     CRT(d2) -> fwd NTT -> evk product (cached evk forms) -> iNTT (2B rows)
+//     -> iCRT (2B)
+//   epilogue: out = R_logp(d + R_logQ(ks)) per component.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <list>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/hemul_gpu.h"
+#include "kernels.hpp"
+#include "level_tables.hpp"
+
+using namespace hemul_gpu;
+
+namespace {
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+  // grows (never shrinks); returns false on allocation failure
+  bool ensure(size_t want) {
+    if (want <= bytes) return true;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    if (cudaMalloc(&ptr, want) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    bytes = want;
+    return true;
+  }
+};
+
+struct RegionDev {
+  int np = 0;
+  int target_bits = 0;
+  DevBuf primes, tw, itw, btab, hat, big_p, half_p;
+  struct Crt {
+    int in_bits;
+    CrtWeights w;
+    std::unique_ptr<DevBuf> buf;
+  };
+  std::vector<Crt> crt;
+  IcrtTable icrt;
+  std::vector<uint64_t> host_primes;
+  const CrtWeights* weights(int bits) const {
+    for (const auto& c : crt)
+      if (c.in_bits == bits) return &c.w;
+    return nullptr;
+  }
+};
+
+struct Level {
+  int log_q = 0;
+  RegionDev r1, r2;
+  bool has_evk = false;
+  uint64_t evk_id = 0;
+  DevBuf evk_a, evk_b;  // np2 x n NTT forms
+};
+
+struct CudaFail : std::runtime_error {
+  hemul_status code;
+  CudaFail(hemul_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CudaFail(e == cudaErrorMemoryAllocation ? HEMUL_E_OOM : HEMUL_E_CUDA,
+                   std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename T>
+void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+  if (!b.ensure(v.size() * sizeof(T) + 16)) throw CudaFail(HEMUL_E_OOM, "device allocation failed");
+  check(cudaMemcpyAsync(b.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st),
+        "table upload");
+}
+
+}  // namespace
+
+struct hemul_gpu_ctx {
+  int device = 0;
+  int log_n = 0, n = 0, log_p = 0, depth = 0, log_q_max = 0;
+  cudaStream_t stream = nullptr;
+  std::list<std::unique_ptr<Level>> cache;  // most recent first, capacity 2
+  std::string err;
+  uint64_t launches = 0;
+  bool timing = false;
+  double stage_ms[HEMUL_STAGE_COUNT] = {};
+  struct Mark {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  // scratch
+  DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
+
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
+};
+
+namespace {
+
+hemul_status fail(hemul_gpu_ctx* c, hemul_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+template <typename F>
+hemul_status guarded(hemul_gpu_ctx* c, F&& f) {
+  try {
+    if (cudaSetDevice(c->device) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, HEMUL_E_CUDA, "cudaSetDevice failed");
+    }
+    return f();
+  } catch (const CudaFail& e) {
+    return fail(c, e.code, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(c, HEMUL_E_ARG, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(c, HEMUL_E_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(c, HEMUL_E_ARG, e.what());
+  }
+}
+
+// Stage timing scope (counters.hpp:58-76 ScopedStageTimer, on the device).
+struct StageScope {
+  hemul_gpu_ctx* c;
+  int stage;
+  cudaEvent_t a = nullptr;
+  StageScope(hemul_gpu_ctx* ctx, int s) : c(ctx), stage(s) {
+    if (c->timing) {
+      a = c->take_event();
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~StageScope() {
+    if (c->timing) {
+      cudaEvent_t b = c->take_event();
+      cudaEventRecord(b, c->stream);
+      c->marks.push_back({stage, a, b});
+    }
+  }
+};
+
+void fill_region(RegionDev& d, const RegionHost& h, int log_n, cudaStream_t st) {
+  d.np = h.np;
+  d.target_bits = h.target_bits;
+  d.host_primes = h.primes;
+  upload(d.primes, h.dev, st);
+  upload(d.tw, h.tw, st);
+  upload(d.itw, h.itw, st);
+  upload(d.btab, h.btab, st);
+  d.icrt.btab = d.btab.as<uint32_t>();
+  d.icrt.m_out = h.m_out;
+  d.icrt.m_pad = h.m_pad;
+  d.icrt.target_bits = h.target_bits;
+  upload(d.hat, h.hat_full, st);
+  upload(d.big_p, h.big_p, st);
+  upload(d.half_p, h.half_p, st);
+  d.icrt.hat = d.hat.as<uint64_t>();
+  d.icrt.big_p = d.big_p.as<uint64_t>();
+  d.icrt.half_p = d.half_p.as<uint64_t>();
+  d.icrt.p_limbs = h.p_limbs;
+  d.crt.clear();
+  for (const auto& c : h.crt) {
+    RegionDev::Crt dc;
+    dc.in_bits = c.in_bits;
+    dc.buf = std::make_unique<DevBuf>();
+    upload(*dc.buf, c.wtab, st);
+    dc.w.wtab = dc.buf->as<uint32_t>();
+    dc.w.chunks = c.chunks;
+    dc.w.np_pad = c.np_pad;
+    d.crt.push_back(std::move(dc));
+  }
+  (void)log_n;
+}
+
+int host_threads() {
+  const unsigned t = std::thread::hardware_concurrency();
+  return t ? int(t < 32 ? t : 32) : 1;
+}
+
+// Scheme::level (heaan.cpp:119-150): LRU of capacity 2 keyed by log_q.
+Level& get_level(hemul_gpu_ctx* c, int log_q) {
+  for (auto it = c->cache.begin(); it != c->cache.end(); ++it)
+    if ((*it)->log_q == log_q) {
+      c->cache.splice(c->cache.begin(), c->cache, it);
+      return *c->cache.front();
+    }
+  if (log_q <= 0 || log_q > c->log_q_max) throw std::invalid_argument("log_q out of range");
+  auto lv = std::make_unique<Level>();
+  lv->log_q = log_q;
+  const int th = host_threads();
+  RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th);
+  RegionHost h2 = build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th);
+  fill_region(lv->r1, h1, c->log_n, c->stream);
+  fill_region(lv->r2, h2, c->log_n, c->stream);
+  check(cudaStreamSynchronize(c->stream), "level upload");
+  c->cache.push_front(std::move(lv));
+  while (c->cache.size() > 2) c->cache.pop_back();
+  return *c->cache.front();
+}
+
+// Device view of a caller buffer: device pointers pass through, host
+// pointers are staged in `scratch` (at byte offset off).
+const uint64_t* to_device(hemul_gpu_ctx* c, const uint64_t* p, size_t words, DevBuf& scratch,
+                          size_t off_words) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
+    if (a.device != c->device) throw std::invalid_argument("device pointer on another GPU");
+    return p;
+  }
+  cudaGetLastError();
+  uint64_t* d = scratch.as<uint64_t>() + off_words;
+  check(cudaMemcpyAsync(d, p, words * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+  return d;
+}
+
+bool is_device(const hemul_gpu_ctx* c, const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
+    if (a.device != c->device) throw std::invalid_argument("device pointer on another GPU");
+    return true;
+  }
+  cudaGetLastError();
+  return false;
+}
+
+void ensure(DevBuf& b, size_t bytes) {
+  if (!b.ensure(bytes)) throw CudaFail(HEMUL_E_OOM, "device allocation failed");
+}
+
+int limbs_of(int bits) { return (bits + 63) / 64; }
+
+void set_evk_forms(hemul_gpu_ctx* c, Level& lv, const uint64_t* evk_ax, const uint64_t* evk_bx,
+                   uint64_t id) {
+  const size_t n = size_t(c->n);
+  const int Le = limbs_of(2 * c->log_q_max);
+  const RegionDev& r2 = lv.r2;
+  ensure(lv.evk_a, size_t(r2.np) * n * 8);
+  ensure(lv.evk_b, size_t(r2.np) * n * 8);
+  ensure(c->in, 2 * n * Le * 8);
+  const uint64_t* a = to_device(c, evk_ax, n * Le, c->in, 0);
+  const uint64_t* b = to_device(c, evk_bx, n * Le, c->in, n * Le);
+  const CrtWeights* w = r2.weights(2 * c->log_q_max);
+  int launches = 0;
+  check(crt_forward(a, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np,
+                    lv.evk_a.as<uint64_t>(), c->stream),
+        "evk CRT");
+  check(crt_forward(b, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np,
+                    lv.evk_b.as<uint64_t>(), c->stream),
+        "evk CRT");
+  c->launches += 2;
+  check(ntt_forward(lv.evk_a.as<uint64_t>(), r2.np, r2.np, c->log_n, r2.tw.as<Twiddle>(),
+                    r2.primes.as<DevPrime>(), c->stream, &launches),
+        "evk NTT");
+  check(ntt_forward(lv.evk_b.as<uint64_t>(), r2.np, r2.np, c->log_n, r2.tw.as<Twiddle>(),
+                    r2.primes.as<DevPrime>(), c->stream, &launches),
+        "evk NTT");
+  c->launches += launches;
+  check(cudaStreamSynchronize(c->stream), "evk forms");
+  lv.has_evk = true;
+  lv.evk_id = id;
+}
+
+void collect_timing(hemul_gpu_ctx* c) {
+  for (double& v : c->stage_ms) v = 0;
+  if (!c->timing) return;
+  check(cudaStreamSynchronize(c->stream), "timing sync");
+  for (auto& m : c->marks) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, m.a, m.b);
+    c->stage_ms[m.stage] += ms;
+    c->event_pool.push_back(m.a);
+    c->event_pool.push_back(m.b);
+  }
+  c->marks.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_override,
+                              hemul_gpu_ctx** out) {
+  if (!out) return HEMUL_E_ARG;
+  *out = nullptr;
+  if (log_p <= 0 || depth <= 0) return HEMUL_E_ARG;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return HEMUL_E_CUDA;
+  }
+  if (device < 0 || device >= count) return HEMUL_E_ARG;
+  auto c = std::make_unique<hemul_gpu_ctx>();
+  c->device = device;
+  c->log_p = log_p;
+  c->depth = depth;
+  c->log_q_max = log_p * depth;  // params.cpp:70
+  if (log_n_override) {
+    c->log_n = log_n_override;
+  } else {  // params.cpp:56-62
+    const int q = c->log_q_max;
+    if (q <= 300) c->log_n = 14;
+    else if (q <= 600) c->log_n = 15;
+    else if (q <= 1200) c->log_n = 16;
+    else if (q <= 2400) c->log_n = 17;
+    else return HEMUL_E_ARG;  // "modulus too large for security table"
+  }
+  if (c->log_n < 7 || c->log_n > 17) return HEMUL_E_ARG;
+  c->n = 1 << c->log_n;
+  if (cudaSetDevice(device) != cudaSuccess) return HEMUL_E_CUDA;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return HEMUL_E_CUDA;
+  if (ntt_setup_attributes() != cudaSuccess || crt_setup_attributes() != cudaSuccess ||
+      icrt_setup_attributes() != cudaSuccess)
+    return HEMUL_E_CUDA;
+  *out = c.release();
+  return HEMUL_OK;
+}
+
+void hemul_gpu_destroy(hemul_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& m : c->marks) {
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  c->cache.clear();
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* hemul_gpu_last_error(const hemul_gpu_ctx* c) { return c ? c->err.c_str() : ""; }
+
+hemul_status hemul_gpu_params(const hemul_gpu_ctx* c, int out[5]) {
+  if (!c || !out) return HEMUL_E_ARG;
+  out[0] = c->log_n;
+  out[1] = c->n;
+  out[2] = c->log_p;
+  out[3] = c->depth;
+  out[4] = c->log_q_max;
+  return HEMUL_OK;
+}
+
+hemul_status hemul_gpu_set_level(hemul_gpu_ctx* c, int log_q) {
+  if (!c) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    get_level(c, log_q);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_set_evk(hemul_gpu_ctx* c, int log_q, const uint64_t* evk_ax,
+                               const uint64_t* evk_bx, uint64_t evk_id) {
+  if (!c || !evk_ax || !evk_bx) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    Level& lv = get_level(c, log_q);
+    set_evk_forms(c, lv, evk_ax, evk_bx, evk_id);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_level_info(hemul_gpu_ctx* c, int log_q, int region, int* np,
+                                  uint64_t* primes, int cap) {
+  if (!c || (region != 1 && region != 2)) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    Level& lv = get_level(c, log_q);
+    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    if (np) *np = r.np;
+    for (int j = 0; j < r.np && j < cap && primes; ++j) primes[j] = r.host_primes[j];
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_enable_stage_timing(hemul_gpu_ctx* c, int on) {
+  if (!c) return HEMUL_E_ARG;
+  c->timing = on != 0;
+  return HEMUL_OK;
+}
+
+hemul_status hemul_gpu_stage_ms(const hemul_gpu_ctx* c, double ms[HEMUL_STAGE_COUNT]) {
+  if (!c || !ms) return HEMUL_E_ARG;
+  for (int i = 0; i < HEMUL_STAGE_COUNT; ++i) ms[i] = c->stage_ms[i];
+  return HEMUL_OK;
+}
+
+uint64_t hemul_gpu_launch_count(const hemul_gpu_ctx* c) { return c ? c->launches : 0; }
+
+hemul_status hemul_gpu_synchronize(hemul_gpu_ctx* c) {
+  if (!c) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    check(cudaStreamSynchronize(c->stream), "synchronize");
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size_t batch,
+                              const uint64_t* c1_ax, const uint64_t* c1_bx,
+                              const uint64_t* c2_ax, const uint64_t* c2_bx,
+                              const uint64_t* evk_ax, const uint64_t* evk_bx, uint64_t evk_id,
+                              uint64_t* out_ax, uint64_t* out_bx) {
+  if (!c) return HEMUL_E_ARG;
+  // heaan.cpp:341-345, same order and messages
+  if (c1_log_q != c2_log_q)
+    return fail(c, HEMUL_E_MODULUS_MISMATCH, "ciphertext modulus mismatch");
+  const int log_q = c1_log_q;
+  if (log_q - c->log_p < c->log_p)
+    return fail(c, HEMUL_E_DEPTH, "multiplicative depth exhausted");
+  if (batch == 0) return HEMUL_OK;
+  if (!c1_ax || !c1_bx || !c2_ax || !c2_bx || !out_ax || !out_bx)
+    return fail(c, HEMUL_E_ARG, "null buffer");
+  return guarded(c, [&]() -> hemul_status {
+    Level& lv = get_level(c, log_q);
+    if (evk_ax && evk_bx && (!lv.has_evk || evk_id == 0 || lv.evk_id != evk_id))
+      set_evk_forms(c, lv, evk_ax, evk_bx, evk_id);
+    if (!lv.has_evk) return fail(c, HEMUL_E_NO_EVK, "evaluation key not set for this level");
+    const size_t n = size_t(c->n);
+    const int log_n = c->log_n, log_Q = c->log_q_max, log_p = c->log_p;
+    const int L = limbs_of(log_q), L2 = limbs_of(log_q + log_Q), Lo = limbs_of(log_q - log_p);
+    const RegionDev& r1 = lv.r1;
+    const RegionDev& r2 = lv.r2;
+    const size_t B = batch;
+    const size_t poly_w = n * L;
+    const DevPrime* p1 = r1.primes.as<DevPrime>();
+    const DevPrime* p2 = r2.primes.as<DevPrime>();
+    c->marks.clear();
+    int launches = 0;
+    // ---- inputs ----------------------------------------------------------
+    ensure(c->in, 4 * B * poly_w * 8);
+    const uint64_t* in[4];
+    {
+      StageScope s(c, HEMUL_STAGE_EXTRA);
+      in[0] = to_device(c, c1_ax, B * poly_w, c->in, 0);
+      in[1] = to_device(c, c1_bx, B * poly_w, c->in, B * poly_w);
+      in[2] = to_device(c, c2_ax, B * poly_w, c->in, 2 * B * poly_w);
+      in[3] = to_device(c, c2_bx, B * poly_w, c->in, 3 * B * poly_w);
+    }
+    // ---- region 1 ---------------------------------------------------------
+    const size_t r1w = B * r1.np * n;  // one RNS operand
+    ensure(c->r1, 4 * r1w * 8);
+    uint64_t* R1 = c->r1.as<uint64_t>();
+    uint64_t* A1 = R1;
+    uint64_t* B1 = R1 + r1w;
+    uint64_t* A2 = R1 + 2 * r1w;
+    uint64_t* B2 = R1 + 3 * r1w;
+    const CrtWeights* w1 = r1.weights(log_q);
+    {
+      StageScope s(c, HEMUL_STAGE_CRT);
+      uint64_t* dst[4] = {A1, B1, A2, B2};
+      for (int t = 0; t < 4; ++t)
+        check(crt_forward(in[t], L, B, log_n, *w1, p1, r1.np, dst[t], c->stream), "CRT r1");
+      launches += 4;
+    }
+    {
+      StageScope s(c, HEMUL_STAGE_NTT);
+      check(ntt_forward(R1, 4 * B * r1.np, r1.np, log_n, r1.tw.as<Twiddle>(), p1, c->stream,
+                        &launches),
+            "NTT r1");
+    }
+    {
+      // pointwise products are booked under iCRT like rns.cpp:364
+      StageScope s(c, HEMUL_STAGE_ICRT);
+      // in place: d2 -> A1, d0 -> B1, d1 -> A2
+      check(tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream),
+            "tensor product");
+      ++launches;
+    }
+    {
+      StageScope s(c, HEMUL_STAGE_INTT);
+      check(ntt_inverse(R1, 3 * B * r1.np, r1.np, log_n, r1.itw.as<Twiddle>(), p1, c->stream,
+                        &launches),
+            "iNTT r1");
+    }
+    // d polys: [d2 | d0 | d1], each B x n x L
+    ensure(c->dpoly, 3 * B * poly_w * 8);
+    uint64_t* D = c->dpoly.as<uint64_t>();
+    uint64_t* d2 = D;
+    uint64_t* d0 = D + B * poly_w;
+    uint64_t* d1 = D + 2 * B * poly_w;
+    {
+      StageScope s(c, HEMUL_STAGE_ICRT);
+      check(icrt(R1, 3 * B, log_n, p1, r1.np, r1.icrt, D, c->stream), "iCRT r1");
+      ++launches;
+    }
+    // ---- region 2: ModUp, evk product, ModDown ----------------------------
+    const size_t r2w = B * r2.np * n;
+    ensure(c->r2, 2 * r2w * 8);
+    uint64_t* KA = c->r2.as<uint64_t>();
+    uint64_t* KB = KA + r2w;
+    {
+      StageScope s(c, HEMUL_STAGE_CRT);
+      check(crt_forward(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream),
+            "CRT r2");
+      ++launches;
+    }
+    {
+      StageScope s(c, HEMUL_STAGE_NTT);
+      check(ntt_forward(KA, B * r2.np, r2.np, log_n, r2.tw.as<Twiddle>(), p2, c->stream,
+                        &launches),
+            "NTT r2");
+    }
+    {
+      StageScope s(c, HEMUL_STAGE_ICRT);
+      check(evk_product(KA, lv.evk_a.as<uint64_t>(), lv.evk_b.as<uint64_t>(), KA, KB, B, r2.np,
+                        log_n, p2, c->stream),
+            "evk product");
+      ++launches;
+    }
+    {
+      StageScope s(c, HEMUL_STAGE_INTT);
+      check(ntt_inverse(KA, 2 * B * r2.np, r2.np, log_n, r2.itw.as<Twiddle>(), p2, c->stream,
+                        &launches),
+            "iNTT r2");
+    }
+    ensure(c->ks, 2 * B * n * L2 * 8);
+    uint64_t* KS = c->ks.as<uint64_t>();
+    {
+      StageScope s(c, HEMUL_STAGE_ICRT);
+      check(icrt(KA, 2 * B, log_n, p2, r2.np, r2.icrt, KS, c->stream), "iCRT r2");
+      ++launches;
+    }
+    // ---- epilogue ---------------------------------------------------------
+    const bool dev_out = is_device(c, out_ax) && is_device(c, out_bx);
+    uint64_t *oa = out_ax, *ob = out_bx;
+    if (!dev_out) {
+      ensure(c->outb, 2 * B * n * Lo * 8);
+      oa = c->outb.as<uint64_t>();
+      ob = oa + B * n * Lo;
+    }
+    {
+      StageScope s(c, HEMUL_STAGE_EXTRA);
+      check(keyswitch_epilogue(KS, d1, oa, B, log_n, log_q, log_Q, log_p, c->stream),
+            "epilogue ax");
+      check(keyswitch_epilogue(KS + B * n * L2, d0, ob, B, log_n, log_q, log_Q, log_p,
+                               c->stream),
+            "epilogue bx");
+      launches += 2;
+      if (!dev_out) {
+        check(cudaMemcpyAsync(out_ax, oa, B * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
+              "D2H");
+        check(cudaMemcpyAsync(out_bx, ob, B * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
+              "D2H");
+      }
+    }
+    c->launches += launches;
+    if (!dev_out) check(cudaStreamSynchronize(c->stream), "he_mul");
+    collect_timing(c);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_rescale(hemul_gpu_ctx* c, int log_q, size_t batch, const uint64_t* ax,
+                               const uint64_t* bx, uint64_t* out_ax, uint64_t* out_bx) {
+  if (!c) return HEMUL_E_ARG;
+  // heaan.cpp:329-330
+  if (log_q - c->log_p < c->log_p)
+    return fail(c, HEMUL_E_DEPTH, "modulus exhausted; cannot rescale");
+  if (batch == 0) return HEMUL_OK;
+  return guarded(c, [&]() -> hemul_status {
+    const size_t n = size_t(c->n);
+    const int L = limbs_of(log_q), Lo = limbs_of(log_q - c->log_p);
+    ensure(c->rescale_buf, 2 * batch * n * (L + Lo) * 8);
+    const uint64_t* a = to_device(c, ax, batch * n * L, c->rescale_buf, 0);
+    const uint64_t* b = to_device(c, bx, batch * n * L, c->rescale_buf, batch * n * L);
+    const bool dev_out = is_device(c, out_ax) && is_device(c, out_bx);
+    uint64_t* oa = dev_out ? out_ax : c->rescale_buf.as<uint64_t>() + 2 * batch * n * L;
+    uint64_t* ob = dev_out ? out_bx : oa + batch * n * Lo;
+    check(shift_right(a, oa, batch, c->log_n, log_q, c->log_p, c->stream), "rescale");
+    check(shift_right(b, ob, batch, c->log_n, log_q, c->log_p, c->stream), "rescale");
+    c->launches += 2;
+    if (!dev_out) {
+      check(cudaMemcpyAsync(out_ax, oa, batch * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
+            "D2H");
+      check(cudaMemcpyAsync(out_bx, ob, batch * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
+            "D2H");
+    }
+    check(cudaStreamSynchronize(c->stream), "rescale");
+    return HEMUL_OK;
+  });
+}
+
+uint64_t hemul_ciphertext_digest(int log_q, size_t words, const uint64_t* ax,
+                                 const uint64_t* bx) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](uint64_t v) {
+    for (int k = 0; k < 8; ++k) h = (h ^ ((v >> (8 * k)) & 0xff)) * 1099511628211ull;
+  };
+  mix(static_cast<uint64_t>(log_q));
+  for (size_t i = 0; i < words; ++i) mix(ax[i]);
+  for (size_t i = 0; i < words; ++i) mix(bx[i]);
+  return h;
+}
+
+// ---- stage entry points ------------------------------------------------------
+
+hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* data, size_t rows,
+                           int inverse) {
+  if (!c || !data || (region != 1 && region != 2)) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    Level& lv = get_level(c, log_q);
+    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const size_t words = rows * size_t(c->n);
+    const bool dev = is_device(c, data);
+    uint64_t* d = data;
+    if (!dev) {
+      ensure(c->r1, words * 8);
+      d = c->r1.as<uint64_t>();
+      check(cudaMemcpyAsync(d, data, words * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    }
+    int launches = 0;
+    if (inverse)
+      check(ntt_inverse(d, rows, r.np, c->log_n, r.itw.as<Twiddle>(), r.primes.as<DevPrime>(),
+                        c->stream, &launches),
+            "iNTT");
+    else
+      check(ntt_forward(d, rows, r.np, c->log_n, r.tw.as<Twiddle>(), r.primes.as<DevPrime>(),
+                        c->stream, &launches),
+            "NTT");
+    c->launches += launches;
+    if (!dev)
+      check(cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    check(cudaStreamSynchronize(c->stream), "ntt");
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_crt(hemul_gpu_ctx* c, int log_q, int region, int in_bits, size_t batch,
+                           const uint64_t* poly, uint64_t* rns) {
+  if (!c || !poly || !rns || (region != 1 && region != 2)) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    Level& lv = get_level(c, log_q);
+    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const CrtWeights* w = r.weights(in_bits);
+    if (!w) return fail(c, HEMUL_E_ARG, "no CRT table for this input width");
+    const size_t n = size_t(c->n);
+    const int L = limbs_of(in_bits);
+    ensure(c->in, batch * n * L * 8);
+    const uint64_t* src = to_device(c, poly, batch * n * L, c->in, 0);
+    const bool dev = is_device(c, rns);
+    uint64_t* dst = rns;
+    if (!dev) {
+      ensure(c->r1, batch * r.np * n * 8);
+      dst = c->r1.as<uint64_t>();
+    }
+    check(crt_forward(src, L, batch, c->log_n, *w, r.primes.as<DevPrime>(), r.np, dst,
+                      c->stream),
+          "CRT");
+    ++c->launches;
+    if (!dev)
+      check(cudaMemcpyAsync(rns, dst, batch * r.np * n * 8, cudaMemcpyDeviceToHost, c->stream),
+            "D2H");
+    check(cudaStreamSynchronize(c->stream), "crt");
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_pointwise(hemul_gpu_ctx* c, int log_q, int region, size_t batch,
+                                 const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  if (!c || !a || !b || !out || (region != 1 && region != 2)) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    Level& lv = get_level(c, log_q);
+    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const size_t words = batch * r.np * size_t(c->n);
+    ensure(c->r1, 3 * words * 8);
+    const uint64_t* da = to_device(c, a, words, c->r1, 0);
+    const uint64_t* db = to_device(c, b, words, c->r1, words);
+    const bool dev = is_device(c, out);
+    uint64_t* d = dev ? out : c->r1.as<uint64_t>() + 2 * words;
+    check(pointwise(da, db, d, batch, r.np, c->log_n, r.primes.as<DevPrime>(), c->stream),
+          "pointwise");
+    ++c->launches;
+    if (!dev) check(cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    check(cudaStreamSynchronize(c->stream), "pointwise");
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batch,
+                            const uint64_t* rns, uint64_t* poly) {
+  if (!c || !rns || !poly || (region != 1 && region != 2)) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    Level& lv = get_level(c, log_q);
+    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const size_t n = size_t(c->n);
+    const size_t words = batch * r.np * n;
+    const int TL = limbs_of(r.target_bits);
+    ensure(c->r1, words * 8);
+    const uint64_t* src = to_device(c, rns, words, c->r1, 0);
+    const bool dev = is_device(c, poly);
+    uint64_t* dst = poly;
+    if (!dev) {
+      ensure(c->ks, batch * n * TL * 8);
+      dst = c->ks.as<uint64_t>();
+    }
+    // arbitrary residues: enable the exact fix-up for |v| >= P/4
+    IcrtFlags flags;
+    flags.capacity = static_cast<unsigned>(batch * n);
+    ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
+    flags.count = c->flagbuf.as<unsigned>();
+    flags.ids = flags.count + 1;
+    check(icrt(src, batch, c->log_n, r.primes.as<DevPrime>(), r.np, r.icrt, dst, c->stream,
+               &flags),
+          "iCRT");
+    c->launches += 2;
+    if (!dev)
+      check(cudaMemcpyAsync(poly, dst, batch * n * TL * 8, cudaMemcpyDeviceToHost, c->stream),
+            "D2H");
+    check(cudaStreamSynchronize(c->stream), "icrt");
+    return HEMUL_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// Host-callable launchers of the sm_100a kernels (one .cu file per stage).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "device_tables.cuh"
+
+namespace hemul_gpu {
+
+// ---- NTT (ntt.cu) ----------------------------------------------------------
+cudaError_t ntt_setup_attributes();
+// rows = batch * np prime-major rows; row r uses prime r % np.
+cudaError_t ntt_forward(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* tw,
+                        const DevPrime* primes, cudaStream_t st, int* launches);
+cudaError_t ntt_inverse(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* itw,
+                        const DevPrime* primes, cudaStream_t st, int* launches);
+
+// ---- CRT (crt.cu) ----------------------------------------------------------
+// Weight table for one (prime set, input width): wtab[m * 2 * np_pad + 2 j + h]
+// = 30-bit half h of 2^(30 m) mod p_j, m < chunks = ceil(in_bits / 30).
+struct CrtWeights {
+  const uint32_t* wtab = nullptr;
+  int chunks = 0;
+  int np_pad = 0;  // multiple of kCrtPrimesPerTile
+};
+constexpr int kCrtPrimesPerTile = 16;
+cudaError_t crt_setup_attributes();
+// poly: batch x n x limbs; out: batch x np x n.
+cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n,
+                        const CrtWeights& w, const DevPrime* primes, int np, uint64_t* out,
+                        cudaStream_t st);
+
+// ---- iCRT (icrt.cu) --------------------------------------------------------
+// B table for the exact reconstruction mod 2^T: (2 np + 1) rows x m_pad
+// columns of 30-bit chunks (rows 2j: H_j mod 2^T, 2j+1: the same shifted up
+// one chunk, 2np: (-P) mod 2^T), m_out = ceil(T / 30) real columns.
+struct IcrtTable {
+  const uint32_t* btab = nullptr;
+  int m_out = 0;
+  int m_pad = 0;  // multiple of 16
+  int target_bits = 0;
+  // exact fallback (arbitrary residues): H_j = P/p_j, P, floor(P/2), each
+  // p_limbs words (H_j rows back to back)
+  const uint64_t* hat = nullptr;
+  const uint64_t* big_p = nullptr;
+  const uint64_t* half_p = nullptr;
+  int p_limbs = 0;
+};
+// Ambiguity list for icrt(): counter + coefficient ids whose fp64 quotient
+// lies within 1/4 of a half-integer, i.e. |v| >= P/4 — impossible inside
+// he_mul (slack >= 4 bits is asserted at level setup), possible for
+// arbitrary residues passed to the stage API. Those coefficients are
+// recomputed exactly by a fix-up kernel.
+struct IcrtFlags {
+  unsigned* count = nullptr;  // device counter, zeroed by icrt()
+  unsigned* ids = nullptr;    // capacity entries: b * n + i
+  unsigned capacity = 0;
+};
+cudaError_t icrt_setup_attributes();
+// rns: batch x np x n canonical residues; out: batch x n x ceil(T/64) limbs.
+// flags = nullptr: the caller guarantees |v| < P/4 (he_mul).
+cudaError_t icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* primes, int np,
+                 const IcrtTable& t, uint64_t* out, cudaStream_t st,
+                 const IcrtFlags* flags = nullptr);
+
+// ---- element-wise RNS and polynomial kernels (poly.cu) ---------------------
+// out = a * b mod p_j over batch x np x n.
+cudaError_t pointwise(const uint64_t* a, const uint64_t* b, uint64_t* out, size_t batch, int np,
+                      int log_n, const DevPrime* primes, cudaStream_t st);
+// Region-1 tensor product in the evaluation domain (heaan.cpp:372-394 with
+// the cross term as A1 B2 + A2 B1, bit-identical to the (a+b)(a'+b') form,
+// test_heaan.cpp:184-199): d0 = B1 B2, d2 = A1 A2, d1 = A1 B2 + A2 B1.
+cudaError_t tensor_product(const uint64_t* a1, const uint64_t* b1, const uint64_t* a2,
+                           const uint64_t* b2, uint64_t* d0, uint64_t* d1, uint64_t* d2,
+                           size_t batch, int np, int log_n, const DevPrime* primes,
+                           cudaStream_t st);
+// Region-2 evk inner product: ka = f * ea, kb = f * eb (evk forms shared by
+// the batch).
+cudaError_t evk_product(const uint64_t* f, const uint64_t* ea, const uint64_t* eb, uint64_t* ka,
+                        uint64_t* kb, size_t batch, int np, int log_n, const DevPrime* primes,
+                        cudaStream_t st);
+// out = R_logp( d + R_logQ(ks) mod 2^log_q ): ModDown shift, add and rescale
+// (poly.cpp:98-115, heaan.cpp:401-409). ks: n x ceil((log_q+log_Q)/64),
+// d: n x ceil(log_q/64), out: n x ceil((log_q-log_p)/64); batch of each.
+cudaError_t keyswitch_epilogue(const uint64_t* ks, const uint64_t* d, uint64_t* out, size_t batch,
+                               int log_n, int log_q, int log_Q, int log_p, cudaStream_t st);
+// Scheme::rescale on one poly batch (poly_shift_right, poly.cpp:98-115).
+cudaError_t shift_right(const uint64_t* a, uint64_t* out, size_t batch, int log_n, int log_q,
+                        int bits, cudaStream_t st);
+
+}  // namespace hemul_gpu

@@ -1,0 +1,280 @@
+// Host-side level tables: deterministic primes, twiddles, CRT weights and the
+// exact-iCRT table, built by the same rules as the reference so that every
+// intermediate residue matches (params.cpp:76-240, heaan.cpp:132-147).
+#include "level_tables.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+#include <thread>
+
+namespace hemul_gpu {
+
+namespace {
+
+using u128 = unsigned __int128;
+
+uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) { return uint64_t(u128(a) * b % m); }
+
+uint64_t powmod(uint64_t a, uint64_t e, uint64_t m) {
+  uint64_t r = 1 % m;
+  a %= m;
+  for (; e; e >>= 1) {
+    if (e & 1) r = mulmod(r, a, m);
+    a = mulmod(a, a, m);
+  }
+  return r;
+}
+
+// Miller-Rabin with the twelve prime bases below 40 (deterministic < 2^64),
+// as params.cpp:22-47 does.
+bool is_prime(uint64_t n) {
+  static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return false;
+  for (uint64_t b : bases)
+    if (n % b == 0) return n == b;
+  uint64_t d = n - 1;
+  int s = 0;
+  while ((d & 1) == 0) d >>= 1, ++s;
+  for (uint64_t b : bases) {
+    uint64_t x = powmod(b, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool witness = true;
+    for (int r = 1; r < s && witness; ++r) {
+      x = mulmod(x, x, n);
+      witness = x != n - 1;
+    }
+    if (witness) return false;
+  }
+  return true;
+}
+
+uint64_t shoup_q(uint64_t w, uint64_t p) { return uint64_t((u128(w) << 64) / p); }
+
+// little-endian natural number
+using Nat = std::vector<uint64_t>;
+
+void nat_mul_word(Nat& a, uint64_t w) {
+  uint64_t carry = 0;
+  for (auto& x : a) {
+    const u128 t = u128(x) * w + carry;
+    x = uint64_t(t);
+    carry = uint64_t(t >> 64);
+  }
+  if (carry) a.push_back(carry);
+}
+
+Nat nat_div_word(const Nat& a, uint64_t d, uint64_t* rem) {
+  Nat q(a.size());
+  u128 r = 0;
+  for (size_t k = a.size(); k-- > 0;) {
+    const u128 cur = (r << 64) | a[k];
+    q[k] = uint64_t(cur / d);
+    r = cur % d;
+  }
+  if (rem) *rem = uint64_t(r);
+  return q;
+}
+
+int nat_bits(const Nat& a) {
+  for (size_t k = a.size(); k-- > 0;)
+    if (a[k]) return int(k * 64 + 64 - __builtin_clzll(a[k]));
+  return 0;
+}
+
+// low `bits` bits of a as `limbs` words
+Nat nat_low(const Nat& a, int bits) {
+  const int limbs = (bits + 63) / 64;
+  Nat r(limbs, 0);
+  for (int k = 0; k < limbs && k < int(a.size()); ++k) r[k] = a[k];
+  if (bits % 64) r[limbs - 1] &= (uint64_t(1) << (bits % 64)) - 1;
+  return r;
+}
+
+// 2^bits - a  for 0 < a < 2^bits (two's complement in `bits` bits)
+Nat nat_neg_mod_pow2(const Nat& a, int bits) {
+  Nat r = nat_low(a, bits);
+  uint64_t borrow = 0;
+  for (auto& x : r) {  // 0 - r
+    const uint64_t v = 0 - x - borrow;
+    borrow = (x != 0) || borrow;
+    x = v;
+  }
+  if (bits % 64) r.back() &= (uint64_t(1) << (bits % 64)) - 1;
+  return r;
+}
+
+uint32_t chunk30(const Nat& a, int m) {
+  const int bit = 30 * m, k = bit / 64, off = bit % 64;
+  uint64_t v = k < int(a.size()) ? a[k] >> off : 0;
+  if (off > 34 && k + 1 < int(a.size())) v |= a[k + 1] << (64 - off);
+  return uint32_t(v) & 0x3fffffffu;
+}
+
+uint32_t bit_reverse(uint32_t i, int bits) {
+  uint32_t r = 0;
+  for (int b = 0; b < bits; ++b, i >>= 1) r = (r << 1) | (i & 1);
+  return r;
+}
+
+template <typename F>
+void parallel_for(int count, int threads, F&& f) {
+  threads = std::max(1, std::min(threads, count));
+  if (threads == 1) {
+    for (int i = 0; i < count; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      for (int i = t; i < count; i += threads) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+int prime_count(int bound_bits, int log_n) {
+  // ceil((bound + log_n) / 58): every w64 prime exceeds 2^57 (params.cpp:76-79)
+  return (bound_bits + log_n + 57) / 58;
+}
+
+void generate_primes(int count, int log_n, std::vector<uint64_t>& primes,
+                     std::vector<uint64_t>& roots) {
+  const uint64_t two_n = uint64_t(1) << (log_n + 1);
+  const uint64_t top = uint64_t(1) << 60, floor_ = uint64_t(1) << 57;
+  primes.clear();
+  roots.clear();
+  // the largest candidate = 1 (mod 2n) not above 2^60, then downward in 2n steps
+  for (uint64_t c = top - (top - 1) % two_n; int(primes.size()) < count; c -= two_n) {
+    if (c <= floor_) throw std::runtime_error("prime range exhausted for this ring degree");
+    if (!is_prime(c)) continue;
+    primes.push_back(c);
+    // smallest generator power of exact order 2n (params.cpp:49-54)
+    for (uint64_t g = 2;; ++g) {
+      const uint64_t psi = powmod(g, (c - 1) / two_n, c);
+      if (powmod(psi, two_n / 2, c) == c - 1) {
+        roots.push_back(psi);
+        break;
+      }
+    }
+  }
+}
+
+RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
+                        const std::vector<int>& crt_bits, int threads) {
+  RegionHost r;
+  r.region = region;
+  r.log_n = log_n;
+  const int n = 1 << log_n;
+  // prime count with the grow-until-bound loop of heaan.cpp:132-135 / 139-143
+  const int bound = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n + 1;
+  int count = region == 1 ? prime_count(2 * log_q, log_n)
+                          : prime_count(log_q + 2 * log_q_max, log_n);
+  Nat P;
+  for (;; ++count) {
+    generate_primes(count, log_n, r.primes, r.roots);
+    P.assign(1, 1);
+    for (uint64_t p : r.primes) nat_mul_word(P, p);
+    if (nat_bits(P) > bound) break;  // P >= 2^bound
+  }
+  r.np = count;
+  r.target_bits = region == 1 ? log_q : log_q + log_q_max;
+  // Largest |v| the iCRT must recover: region 1 carries d1 = A1 B2 + A2 B1,
+  // |v| < 2 n q^2; region 2 carries d2 * evk, |v| < n q Q^2.
+  const int vbits = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n;
+  r.slack_bits = (nat_bits(P) - 1) - 1 - vbits;
+  if (r.slack_bits < 4)
+    throw std::runtime_error("prime set leaves less than 4 bits of iCRT headroom");
+
+  // per-prime constants
+  r.dev.resize(count);
+  std::vector<Nat> hat(count);
+  for (int j = 0; j < count; ++j) {
+    const uint64_t p = r.primes[j];
+    DevPrime& d = r.dev[j];
+    d = DevPrime{};
+    d.p = p;
+    d.one_q = shoup_q(1, p);
+    d.beta = uint64_t((u128(1) << 64) % p);
+    d.beta_q = shoup_q(d.beta, p);
+    uint64_t hat_mod = 0;
+    hat[j] = nat_div_word(P, p, nullptr);
+    nat_div_word(hat[j], p, &hat_mod);
+    d.inv = powmod(hat_mod, p - 2, p);
+    d.inv_q = shoup_q(d.inv, p);
+    d.ninv = powmod(uint64_t(n) % p, p - 2, p);
+    d.ninv_q = shoup_q(d.ninv, p);
+    d.inv_p_dbl = 1.0 / double(p);
+  }
+
+  // twiddles: tw[j*n + i] = psi^rev(i), itw = psi^-rev(i) (params.cpp:151-180)
+  r.tw.resize(size_t(count) * n);
+  r.itw.resize(size_t(count) * n);
+  parallel_for(count, threads, [&](int j) {
+    const uint64_t p = r.primes[j], psi = r.roots[j];
+    const uint64_t psi_inv = powmod(psi, p - 2, p);
+    uint64_t pw = 1, ipw = 1;
+    for (int i = 0; i < n; ++i) {
+      const uint32_t k = bit_reverse(uint32_t(i), log_n);
+      r.tw[size_t(j) * n + k] = Twiddle{pw, shoup_q(pw, p)};
+      r.itw[size_t(j) * n + k] = Twiddle{ipw, shoup_q(ipw, p)};
+      pw = mulmod(pw, psi, p);
+      ipw = mulmod(ipw, psi_inv, p);
+    }
+    DevPrime& d = r.dev[j];
+    const uint64_t w1n = n > 1 ? mulmod(r.itw[size_t(j) * n + 1].w, d.ninv, p) : d.ninv;
+    d.w1n = w1n;
+    d.w1n_q = shoup_q(w1n, p);
+  });
+
+  // CRT weights: 30-bit halves of 2^(30 m) mod p_j
+  for (int bits : crt_bits) {
+    RegionHost::Crt c;
+    c.in_bits = bits;
+    c.chunks = (bits + 29) / 30;
+    c.np_pad = (count + 15) / 16 * 16;
+    c.wtab.assign(size_t(c.chunks) * 2 * c.np_pad, 0);
+    for (int j = 0; j < count; ++j) {
+      const uint64_t p = r.primes[j];
+      const uint64_t step = powmod(2, 30, p);
+      uint64_t u = 1 % p;
+      for (int m = 0; m < c.chunks; ++m) {
+        c.wtab[size_t(m) * 2 * c.np_pad + 2 * j] = uint32_t(u & 0x3fffffffu);
+        c.wtab[size_t(m) * 2 * c.np_pad + 2 * j + 1] = uint32_t(u >> 30);
+        u = mulmod(u, step, p);
+      }
+    }
+    r.crt.push_back(std::move(c));
+  }
+
+  // iCRT table: rows 2j = chunks of H_j mod 2^T, 2j+1 = the same one chunk
+  // up, 2np = chunks of (-P) mod 2^T
+  const int T = r.target_bits;
+  r.m_out = (T + 29) / 30;
+  r.m_pad = (r.m_out + 15) / 16 * 16;
+  const int K = 2 * count + 1;
+  r.btab.assign(size_t(K) * r.m_pad, 0);
+  for (int j = 0; j < count; ++j) {
+    const Nat h = nat_low(hat[j], T);
+    for (int m = 0; m < r.m_out; ++m) {
+      const uint32_t v = chunk30(h, m);
+      r.btab[size_t(2 * j) * r.m_pad + m] = v;
+      if (m + 1 < r.m_out) r.btab[size_t(2 * j + 1) * r.m_pad + m + 1] = v;
+    }
+  }
+  r.p_limbs = (nat_bits(P) + 63) / 64;
+  r.hat_full.assign(size_t(count) * r.p_limbs, 0);
+  for (int j = 0; j < count; ++j)
+    for (int k = 0; k < r.p_limbs && k < int(hat[j].size()); ++k)
+      r.hat_full[size_t(j) * r.p_limbs + k] = hat[j][k];
+  r.big_p.assign(r.p_limbs, 0);
+  r.half_p.assign(r.p_limbs, 0);
+  for (int k = 0; k < r.p_limbs && k < int(P.size()); ++k) r.big_p[k] = P[k];
+  for (int k = 0; k < r.p_limbs; ++k)
+    r.half_p[k] = (r.big_p[k] >> 1) | (k + 1 < r.p_limbs ? r.big_p[k + 1] << 63 : 0);
+  const Nat negP = nat_neg_mod_pow2(P, T);
+  for (int m = 0; m < r.m_out; ++m) r.btab[size_t(2 * count) * r.m_pad + m] = chunk30(negP, m);
+  return r;
+}
+
+}  // namespace hemul_gpu

@@ -1,0 +1,50 @@
+// Host-side construction of one level's tables (the B200 counterpart of
+// Scheme::Level, proj/core/src/heaan.cpp:104-112,119-150).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "device_tables.cuh"
+
+namespace hemul_gpu {
+
+// params.cpp:76-87
+int prime_count(int bound_bits, int log_n);
+// params.cpp:89-115 (w64): primes p = 1 mod 2n descending from 2^60, their
+// smallest-c primitive 2n-th roots. Throws std::runtime_error when exhausted.
+void generate_primes(int count, int log_n, std::vector<uint64_t>& primes,
+                     std::vector<uint64_t>& roots);
+
+struct RegionHost {
+  int region = 0;
+  int np = 0;
+  int log_n = 0;
+  int target_bits = 0;  // log_q (region 1) or log_q + log_Q (region 2)
+  int slack_bits = 0;   // log2(P) - log2(2 * max|v|), the iCRT headroom
+  std::vector<uint64_t> primes, roots;
+  std::vector<DevPrime> dev;         // np
+  std::vector<Twiddle> tw, itw;      // np * n each, ShoupPair tables
+  // CRT weights per input width (see kernels.hpp CrtWeights)
+  struct Crt {
+    int in_bits = 0, chunks = 0, np_pad = 0;
+    std::vector<uint32_t> wtab;
+  };
+  std::vector<Crt> crt;
+  // iCRT table (see kernels.hpp IcrtTable)
+  int m_out = 0, m_pad = 0;
+  std::vector<uint32_t> btab;
+  // exact iCRT fallback: H_j = P / p_j rows, P, floor(P / 2), p_limbs each
+  int p_limbs = 0;
+  std::vector<uint64_t> hat_full, big_p, half_p;
+};
+
+// Region 1 at modulus log_q: products mod 2^log_q (heaan.cpp:132-138).
+// Region 2: key switching, prime product >= 2^(log_q + 2 log_Q + log_n + 1),
+// target 2^(log_q + log_Q) (heaan.cpp:139-147). crt_bits lists the input
+// widths the region must convert (log_q; region 2 also 2 log_Q for the evk).
+// threads > 1 parallelises the twiddle tables.
+RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
+                        const std::vector<int>& crt_bits, int threads);
+
+}  // namespace hemul_gpu

@@ -1,0 +1,191 @@
+// Element-wise RNS products and big-integer polynomial epilogues (sm_100a).
+//
+// pointwise / tensor_product / evk_product:  rns_pointwise_mul
+//   (proj/core/src/rns.cpp:108-130, 360-371), one exact 64x64 -> 128 product
+//   reduced with two Shoup steps (the reference's reduce2, rns.cpp:14-19).
+// keyswitch_epilogue: poly_shift_right by log_Q (ModDown), poly_add with the
+//   region-1 term, poly_shift_right by log_p (rescale) — heaan.cpp:401-409,
+//   poly.cpp:46-70, 98-115 — fused into one pass per coefficient.
+// These kernels are HBM-bound; each coefficient's limbs are read once.
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+#include "modarith.cuh"
+
+namespace hemul_gpu {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mm(uint64_t a, uint64_t b, const DevPrime& pr) {
+  return mulmod(a, b, pr.p, pr.one_q, pr.beta, pr.beta_q);
+}
+
+__global__ void pointwise_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                 uint64_t* __restrict__ out, size_t total, int np, int log_n,
+                                 const DevPrime* __restrict__ primes) {
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>((idx >> log_n) % np);
+    out[idx] = mm(a[idx], b[idx], primes[j]);
+  }
+}
+
+__global__ void tensor_kernel(const uint64_t* a1, const uint64_t* b1,
+                              const uint64_t* a2, const uint64_t* b2,
+                              uint64_t* d0, uint64_t* d1,
+                              uint64_t* d2, size_t total, int np, int log_n,
+                              const DevPrime* __restrict__ primes) {
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const DevPrime pr = primes[(idx >> log_n) % np];
+    const uint64_t x1 = a1[idx], y1 = b1[idx], x2 = a2[idx], y2 = b2[idx];
+    d0[idx] = mm(y1, y2, pr);
+    d2[idx] = mm(x1, x2, pr);
+    d1[idx] = add_mod(mm(x1, y2, pr), mm(x2, y1, pr), pr.p);
+  }
+}
+
+__global__ void evk_kernel(const uint64_t* f, const uint64_t* __restrict__ ea,
+                           const uint64_t* __restrict__ eb, uint64_t* ka,
+                           uint64_t* __restrict__ kb, size_t total, int np, int log_n,
+                           const DevPrime* __restrict__ primes) {
+  const size_t per = size_t(np) << log_n;  // evk forms are shared by the batch
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const size_t e = idx % per;
+    const DevPrime pr = primes[e >> log_n];
+    const uint64_t x = f[idx];
+    ka[idx] = mm(x, ea[e], pr);
+    kb[idx] = mm(x, eb[e], pr);
+  }
+}
+
+constexpr int kMaxLimbs = 96;  // supports log_q + log_Q up to 6144 bits
+
+__device__ __forceinline__ uint64_t mask_of(int bits) {
+  return bits % 64 ? (uint64_t(1) << (bits % 64)) - 1 : ~uint64_t(0);
+}
+
+// s (len limbs) += 2^bit, then reduce mod 2^mod_bits (mod_bits <= 64 len).
+__device__ __forceinline__ void add_pow2_mod(uint64_t* s, int len, int bit, int mod_bits) {
+  uint64_t carry = uint64_t(1) << (bit % 64);
+  for (int k = bit / 64; k < len && carry; ++k) {
+    const uint64_t v = s[k] + carry;
+    carry = v < carry;
+    s[k] = v;
+  }
+  const int top = (mod_bits + 63) / 64;
+  if (top <= len) s[top - 1] &= mask_of(mod_bits);
+}
+
+// out[0..olen) = (s >> bits), s has len limbs.
+__device__ __forceinline__ void shr_limbs(const uint64_t* s, int len, int bits, uint64_t* out,
+                                          int olen) {
+  const int w = bits / 64, sh = bits % 64;
+  for (int k = 0; k < olen; ++k) {
+    const uint64_t lo = w + k < len ? s[w + k] : 0;
+    const uint64_t hi = w + k + 1 < len ? s[w + k + 1] : 0;
+    out[k] = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+  }
+}
+
+__global__ void keyswitch_epilogue_kernel(const uint64_t* __restrict__ ks,
+                                          const uint64_t* __restrict__ d,
+                                          uint64_t* __restrict__ out, size_t total, int log_q,
+                                          int log_Q, int log_p) {
+  const int L2 = (log_q + log_Q + 63) / 64, L = (log_q + 63) / 64;
+  const int Lo = (log_q - log_p + 63) / 64;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+       i += size_t(gridDim.x) * blockDim.x) {
+    uint64_t s[kMaxLimbs], t[kMaxLimbs];
+    const uint64_t* src = ks + i * L2;
+    for (int k = 0; k < L2; ++k) s[k] = src[k];
+    // R_logQ: (v + 2^(Q-1)) mod 2^(q+Q), >> Q   (poly.cpp:98-115)
+    add_pow2_mod(s, L2, log_Q - 1, log_q + log_Q);
+    shr_limbs(s, L2, log_Q, t, L);
+    t[L - 1] &= mask_of(log_q);
+    // + d mod 2^q   (poly.cpp:46-70)
+    const uint64_t* dd = d + i * L;
+    uint64_t carry = 0;
+    for (int k = 0; k < L; ++k) {
+      const uint64_t x = t[k] + carry;
+      const uint64_t c1 = x < carry;
+      const uint64_t y = x + dd[k];
+      carry = c1 + (y < x);
+      t[k] = y;
+    }
+    t[L - 1] &= mask_of(log_q);
+    // rescale R_logp   (heaan.cpp:328-337)
+    add_pow2_mod(t, L, log_p - 1, log_q);
+    uint64_t* o = out + i * Lo;
+    shr_limbs(t, L, log_p, s, Lo);
+    s[Lo - 1] &= mask_of(log_q - log_p);
+    for (int k = 0; k < Lo; ++k) o[k] = s[k];
+  }
+}
+
+__global__ void shift_right_kernel(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
+                                   size_t total, int log_q, int bits) {
+  const int L = (log_q + 63) / 64, Lo = (log_q - bits + 63) / 64;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+       i += size_t(gridDim.x) * blockDim.x) {
+    uint64_t s[kMaxLimbs], t[kMaxLimbs];
+    for (int k = 0; k < L; ++k) s[k] = a[i * L + k];
+    add_pow2_mod(s, L, bits - 1, log_q);
+    shr_limbs(s, L, bits, t, Lo);
+    t[Lo - 1] &= mask_of(log_q - bits);
+    for (int k = 0; k < Lo; ++k) out[i * Lo + k] = t[k];
+  }
+}
+
+unsigned grid_for(size_t total, int threads) {
+  size_t blocks = (total + threads - 1) / threads;
+  const size_t cap = 148 * 64;
+  return static_cast<unsigned>(blocks < cap ? blocks : cap);
+}
+
+}  // namespace
+
+cudaError_t pointwise(const uint64_t* a, const uint64_t* b, uint64_t* out, size_t batch, int np,
+                      int log_n, const DevPrime* primes, cudaStream_t st) {
+  const size_t total = (batch * np) << log_n;
+  pointwise_kernel<<<grid_for(total, 256), 256, 0, st>>>(a, b, out, total, np, log_n, primes);
+  return cudaGetLastError();
+}
+
+cudaError_t tensor_product(const uint64_t* a1, const uint64_t* b1, const uint64_t* a2,
+                           const uint64_t* b2, uint64_t* d0, uint64_t* d1, uint64_t* d2,
+                           size_t batch, int np, int log_n, const DevPrime* primes,
+                           cudaStream_t st) {
+  const size_t total = (batch * np) << log_n;
+  tensor_kernel<<<grid_for(total, 256), 256, 0, st>>>(a1, b1, a2, b2, d0, d1, d2, total, np,
+                                                      log_n, primes);
+  return cudaGetLastError();
+}
+
+cudaError_t evk_product(const uint64_t* f, const uint64_t* ea, const uint64_t* eb, uint64_t* ka,
+                        uint64_t* kb, size_t batch, int np, int log_n, const DevPrime* primes,
+                        cudaStream_t st) {
+  const size_t total = (batch * np) << log_n;
+  evk_kernel<<<grid_for(total, 256), 256, 0, st>>>(f, ea, eb, ka, kb, total, np, log_n, primes);
+  return cudaGetLastError();
+}
+
+cudaError_t keyswitch_epilogue(const uint64_t* ks, const uint64_t* d, uint64_t* out, size_t batch,
+                               int log_n, int log_q, int log_Q, int log_p, cudaStream_t st) {
+  if ((log_q + log_Q + 63) / 64 > kMaxLimbs) return cudaErrorInvalidValue;
+  const size_t total = batch << log_n;
+  keyswitch_epilogue_kernel<<<grid_for(total, 128), 128, 0, st>>>(ks, d, out, total, log_q,
+                                                                   log_Q, log_p);
+  return cudaGetLastError();
+}
+
+cudaError_t shift_right(const uint64_t* a, uint64_t* out, size_t batch, int log_n, int log_q,
+                        int bits, cudaStream_t st) {
+  if ((log_q + 63) / 64 > kMaxLimbs) return cudaErrorInvalidValue;
+  const size_t total = batch << log_n;
+  shift_right_kernel<<<grid_for(total, 128), 128, 0, st>>>(a, out, total, log_q, bits);
+  return cudaGetLastError();
+}
+
+}  // namespace hemul_gpu

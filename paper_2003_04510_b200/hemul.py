@@ -1,0 +1,323 @@
+"""Python mirror of the reference's HE Mul entry points over the C-ABI.
+
+The reference API is C++ (namespace ``hemul``, /root/reference/proj/core):
+``make_params`` (params.cpp:64-74), ``Scheme::warm_level`` / ``he_mul`` /
+``rescale`` (heaan.hpp:74-100, heaan.cpp:119-410) and the lower-level
+``ntt_forward`` / ``crt_forward`` / ``rns_pointwise_mul`` / ``icrt_reordered``
+(ntt.hpp:34-39, rns.hpp:62-85). This module binds ``libhemul_gpu.so``
+(include/hemul_gpu.h) with ctypes and keeps the reference's names, argument
+meaning and error kinds:
+
+* modulus mismatch      -> ``ValueError("ciphertext modulus mismatch")``
+  (std::invalid_argument, heaan.cpp:341-342)
+* depth exhausted       -> ``RuntimeError("multiplicative depth exhausted")``
+  (std::runtime_error, heaan.cpp:344-345)
+
+Arrays are numpy ``uint64`` (host) or torch ``uint64`` CUDA tensors (device;
+the call then stays on the device). Polynomials use the reference BigPoly
+layout (n, limbs) little-endian 64-bit limbs; a leading batch axis is allowed.
+
+There is no CPU fallback: importing works anywhere, but every computing call
+needs the CUDA library and a GPU and raises ``HemulGpuError`` otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Any
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhemul_gpu.so"
+
+HEMUL_OK = 0
+HEMUL_E_ARG = 1
+HEMUL_E_MODULUS_MISMATCH = 2
+HEMUL_E_DEPTH = 3
+HEMUL_E_CUDA = 4
+HEMUL_E_OOM = 5
+HEMUL_E_NO_EVK = 6
+
+STAGES = ("crt", "ntt", "intt", "icrt", "extra")  # counters.hpp:13
+
+
+class HemulGpuError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[status {status}] {message}")
+        self.status = status
+
+
+_lib: ctypes.CDLL | None = None
+
+_u64p = ctypes.c_void_p
+_SIGS = {
+    "hemul_gpu_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "hemul_gpu_destroy": (None, [ctypes.c_void_p]),
+    "hemul_gpu_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "hemul_gpu_params": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "hemul_gpu_set_level": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "hemul_gpu_set_evk": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _u64p, _u64p,
+                                         ctypes.c_uint64]),
+    "hemul_gpu_he_mul": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_size_t, _u64p, _u64p, _u64p, _u64p, _u64p,
+                                        _u64p, ctypes.c_uint64, _u64p, _u64p]),
+    "hemul_gpu_rescale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, _u64p,
+                                         _u64p, _u64p, _u64p]),
+    "hemul_gpu_enable_stage_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "hemul_gpu_stage_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    "hemul_gpu_level_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_int), _u64p, ctypes.c_int]),
+    "hemul_gpu_ntt": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u64p,
+                                     ctypes.c_size_t, ctypes.c_int]),
+    "hemul_gpu_crt": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_size_t, _u64p, _u64p]),
+    "hemul_gpu_pointwise": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_size_t, _u64p, _u64p, _u64p]),
+    "hemul_gpu_icrt": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_size_t, _u64p, _u64p]),
+    "hemul_gpu_launch_count": (ctypes.c_uint64, [ctypes.c_void_p]),
+    "hemul_gpu_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "hemul_ciphertext_digest": (ctypes.c_uint64, [ctypes.c_int, ctypes.c_size_t, _u64p, _u64p]),
+}
+
+
+def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load libhemul_gpu.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise HemulGpuError(HEMUL_E_CUDA, f"{p} missing: run `python -m paper_2003_04510_b200.build`")
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+@dataclass(frozen=True)
+class Params:
+    """make_params(log_p, depth, w64, log_n_override) (params.cpp:64-74)."""
+    log_p: int
+    depth: int
+    log_n_override: int = 0
+
+    @property
+    def log_q_max(self) -> int:
+        return self.log_p * self.depth
+
+    @property
+    def log_n(self) -> int:
+        if self.log_n_override:
+            return self.log_n_override
+        q = self.log_q_max
+        for bound, ln in ((300, 14), (600, 15), (1200, 16), (2400, 17)):
+            if q <= bound:
+                return ln
+        raise ValueError("modulus too large for security table")
+
+    @property
+    def n(self) -> int:
+        return 1 << self.log_n
+
+
+def make_params(log_p: int, depth: int, log_n_override: int = 0) -> Params:
+    return Params(log_p, depth, log_n_override)
+
+
+def limbs(bits: int) -> int:
+    return (bits + 63) // 64
+
+
+def _ptr(a: Any) -> int:
+    """Raw address of a numpy array or torch tensor (contiguous, uint64)."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.uint64 or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("expected a C-contiguous uint64 numpy array")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("expected a contiguous tensor")
+        return a.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(a)!r}")
+
+
+def _like(a: Any, shape: tuple[int, ...]):
+    if isinstance(a, np.ndarray):
+        return np.empty(shape, dtype=np.uint64)
+    import torch
+
+    return torch.empty(shape, dtype=torch.uint64, device=a.device)
+
+
+def _size(a: Any) -> int:
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+class Context:
+    """One device context = one reference ``Scheme`` (heaan.hpp:72-115) for
+    the GPU path: parameters, a 2-entry level LRU, cached evk forms."""
+
+    def __init__(self, params: Params, device: int = 0):
+        self._lib = load_library()
+        self.params = params
+        h = ctypes.c_void_p()
+        st = self._lib.hemul_gpu_create(device, params.log_p, params.depth,
+                                        params.log_n_override, ctypes.byref(h))
+        if st != HEMUL_OK:
+            raise HemulGpuError(st, "hemul_gpu_create failed (no usable CUDA device?)")
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.hemul_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- plumbing --------------------------------------------------------
+    def _check(self, st: int) -> None:
+        if st == HEMUL_OK:
+            return
+        msg = self._lib.hemul_gpu_last_error(self._h).decode()
+        if st == HEMUL_E_MODULUS_MISMATCH:
+            raise ValueError(msg)
+        if st == HEMUL_E_DEPTH:
+            raise RuntimeError(msg)
+        raise HemulGpuError(st, msg)
+
+    @property
+    def n(self) -> int:
+        return self.params.n
+
+    # -- Scheme-level API ------------------------------------------------
+    def warm_level(self, log_q: int, evk: tuple[Any, Any] | None = None, evk_id: int = 1) -> None:
+        """Scheme::warm_level (heaan.hpp:100): tables, and evk forms if given."""
+        if evk is None:
+            self._check(self._lib.hemul_gpu_set_level(self._h, log_q))
+        else:
+            ea, eb = evk
+            self._check(self._lib.hemul_gpu_set_evk(self._h, log_q, _ptr(ea), _ptr(eb), evk_id))
+
+    def he_mul(self, c1: tuple[Any, Any], c2: tuple[Any, Any], log_q: int,
+               c2_log_q: int | None = None, evk: tuple[Any, Any] | None = None,
+               evk_id: int = 1, out: tuple[Any, Any] | None = None):
+        """Scheme::he_mul (heaan.cpp:339-410) on (ax, bx) pairs. Inputs have
+        shape (n, limbs) or (batch, n, limbs); returns (ax, bx) at modulus
+        log_q - log_p."""
+        c2_log_q = log_q if c2_log_q is None else c2_log_q
+        p = self.params
+        if log_q != c2_log_q:
+            self._check(self._lib.hemul_gpu_he_mul(self._h, log_q, c2_log_q, 1, None, None, None,
+                                                   None, None, None, 0, None, None))
+        L, Lo = limbs(log_q), limbs(log_q - p.log_p)
+        per = self.n * L
+        total = _size(c1[0])
+        if total % per:
+            raise ValueError("ciphertext buffer is not a multiple of n x limbs")
+        batch = total // per
+        for a in (c1[1], c2[0], c2[1]):
+            if _size(a) != total:
+                raise ValueError("ciphertext components differ in size")
+        shape = (batch, self.n, Lo) if batch > 1 or getattr(c1[0], "ndim", 2) == 3 else (self.n, Lo)
+        if out is None:
+            out = (_like(c1[0], shape), _like(c1[0], shape))
+        ea = _ptr(evk[0]) if evk is not None else None
+        eb = _ptr(evk[1]) if evk is not None else None
+        self._check(self._lib.hemul_gpu_he_mul(
+            self._h, log_q, c2_log_q, batch, _ptr(c1[0]), _ptr(c1[1]), _ptr(c2[0]), _ptr(c2[1]),
+            ea, eb, evk_id if evk is not None else 0, _ptr(out[0]), _ptr(out[1])))
+        return out
+
+    def rescale(self, c: tuple[Any, Any], log_q: int):
+        """Scheme::rescale (heaan.cpp:328-337)."""
+        p = self.params
+        L, Lo = limbs(log_q), limbs(log_q - p.log_p)
+        batch = _size(c[0]) // (self.n * L)
+        shape = (batch, self.n, Lo) if batch > 1 else (self.n, Lo)
+        out = (_like(c[0], shape), _like(c[0], shape))
+        self._check(self._lib.hemul_gpu_rescale(self._h, log_q, batch, _ptr(c[0]), _ptr(c[1]),
+                                                _ptr(out[0]), _ptr(out[1])))
+        return out
+
+    # -- stage API (ntt.hpp / rns.hpp) -------------------------------------
+    def level_primes(self, log_q: int, region: int) -> np.ndarray:
+        np_ = ctypes.c_int()
+        self._check(self._lib.hemul_gpu_level_info(self._h, log_q, region, ctypes.byref(np_),
+                                                   None, 0))
+        buf = np.zeros(np_.value, dtype=np.uint64)
+        self._check(self._lib.hemul_gpu_level_info(self._h, log_q, region, ctypes.byref(np_),
+                                                   buf.ctypes.data, np_.value))
+        return buf
+
+    def ntt(self, data: Any, log_q: int, region: int, inverse: bool = False) -> None:
+        """In place over rows of n residues (row r uses prime r % np)."""
+        rows = _size(data) // self.n
+        self._check(self._lib.hemul_gpu_ntt(self._h, log_q, region, _ptr(data), rows, int(inverse)))
+
+    def crt(self, poly: Any, log_q: int, region: int, in_bits: int):
+        batch = _size(poly) // (self.n * limbs(in_bits))
+        np_ = len(self.level_primes(log_q, region))
+        out = _like(poly, (batch, np_, self.n) if batch > 1 else (np_, self.n))
+        self._check(self._lib.hemul_gpu_crt(self._h, log_q, region, in_bits, batch, _ptr(poly),
+                                            _ptr(out)))
+        return out
+
+    def pointwise(self, a: Any, b: Any, log_q: int, region: int):
+        np_ = len(self.level_primes(log_q, region))
+        batch = _size(a) // (np_ * self.n)
+        out = _like(a, tuple(a.shape))
+        self._check(self._lib.hemul_gpu_pointwise(self._h, log_q, region, batch, _ptr(a), _ptr(b),
+                                                  _ptr(out)))
+        return out
+
+    def icrt(self, rns: Any, log_q: int, region: int):
+        p = self.params
+        np_ = len(self.level_primes(log_q, region))
+        batch = _size(rns) // (np_ * self.n)
+        tbits = log_q if region == 1 else log_q + p.log_q_max
+        out = _like(rns, (batch, self.n, limbs(tbits)) if batch > 1 else (self.n, limbs(tbits)))
+        self._check(self._lib.hemul_gpu_icrt(self._h, log_q, region, batch, _ptr(rns), _ptr(out)))
+        return out
+
+    # -- instrumentation ---------------------------------------------------
+    def enable_stage_timing(self, on: bool = True) -> None:
+        self._check(self._lib.hemul_gpu_enable_stage_timing(self._h, int(on)))
+
+    def stage_ms(self) -> dict[str, float]:
+        buf = (ctypes.c_double * 5)()
+        self._check(self._lib.hemul_gpu_stage_ms(self._h, buf))
+        return dict(zip(STAGES, list(buf)))
+
+    def launch_count(self) -> int:
+        return int(self._lib.hemul_gpu_launch_count(self._h))
+
+    def synchronize(self) -> None:
+        self._check(self._lib.hemul_gpu_synchronize(self._h))
+
+
+def ciphertext_digest(log_q: int, ax: np.ndarray, bx: np.ndarray) -> int:
+    """FNV-1a 64 over log_q, ax words, bx words (bench.cpp:35-47)."""
+    ax = np.ascontiguousarray(ax, dtype=np.uint64)
+    bx = np.ascontiguousarray(bx, dtype=np.uint64)
+    if ax.size != bx.size:
+        raise ValueError("ax and bx differ in size")
+    return int(load_library().hemul_ciphertext_digest(log_q, ax.size, ax.ctypes.data,
+                                                      bx.ctypes.data))

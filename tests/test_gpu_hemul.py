@@ -1,0 +1,177 @@
+"""HE Mul (+ relinearize + rescale) on the GPU, bit-exact against the
+reference: golden fixtures, golden digests of the seed-7 bench protocol
+(bench.cpp:49-124) and the oracles. Restates test_heaan.cpp:129-199 and
+test_cli.cpp:141-170 (digest identity)."""
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle_lib import random_poly
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def _ctx(cfg):
+    from paper_2003_04510_b200.hemul import Context, make_params
+
+    return Context(make_params(*cfg))
+
+
+def _digest(log_q, ax, bx):
+    from paper_2003_04510_b200.hemul import ciphertext_digest
+
+    return ciphertext_digest(log_q, ax, bx)
+
+
+def test_s_bench_golden_fixture():
+    g = np.load(GOLDEN / "s_bench.npz")
+    digests = json.loads((GOLDEN / "digests.json").read_text())
+    ctx = _ctx((30, 4, 13))
+    q = int(g["log_q"])
+    oa, ob = ctx.he_mul((g["c1ax"], g["c1bx"]), (g["c2ax"], g["c2bx"]), q,
+                        evk=(g["evkax"], g["evkbx"]))
+    assert np.array_equal(oa, g["outax"])
+    assert np.array_equal(ob, g["outbx"])
+    assert f"{_digest(q - 30, oa, ob):016x}" == digests["S"]["digest"]
+
+
+def test_small_random_two_levels_golden():
+    g = np.load(GOLDEN / "small_random.npz")
+    cfg = tuple(int(v) for v in g["params"])
+    ctx = _ctx(cfg)
+    evk = (g["evkax"], g["evkbx"])
+    for lvl in (0, 1):
+        q = int(g[f"log_q_{lvl}"])
+        oa, ob = ctx.he_mul((g[f"c1ax_{lvl}"], g[f"c1bx_{lvl}"]),
+                            (g[f"c2ax_{lvl}"], g[f"c2bx_{lvl}"]), q, evk=evk)
+        assert np.array_equal(oa, g[f"outax_{lvl}"])
+        assert np.array_equal(ob, g[f"outbx_{lvl}"])
+
+
+@pytest.mark.parametrize("cfg", [(30, 4, 13), (30, 6, 11), (30, 10, 13), (20, 4, 10)])
+def test_random_inputs_every_level_vs_oracle(cfg, restated):
+    """Random residues at every level of the ladder (the level LRU evicts,
+    heaan.cpp:119-150) against the C restatement."""
+    ctx = _ctx(cfg)
+    p = ctx.params
+    rng = np.random.default_rng(sum(cfg))
+    evk = (random_poly(rng, p.n, 2 * p.log_q_max), random_poly(rng, p.n, 2 * p.log_q_max))
+    for log_q in range(p.log_q_max, 2 * p.log_p - 1, -p.log_p):
+        c1 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
+        c2 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
+        st, wa, wb = restated.he_mul(p.log_n, p.log_p, p.log_q_max, log_q, c1, c2, evk)
+        assert st == 0
+        oa, ob = ctx.he_mul(c1, c2, log_q, evk=evk)
+        assert np.array_equal(oa, wa), log_q
+        assert np.array_equal(ob, wb), log_q
+
+
+def test_edge_inputs_zero_and_all_ones(restated):
+    cfg = (30, 4, 10)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    q = p.log_q_max
+    rng = np.random.default_rng(1)
+    evk = (random_poly(rng, p.n, 2 * q), random_poly(rng, p.n, 2 * q))
+    ones = np.full((p.n, 2), np.uint64(0xFFFFFFFFFFFFFFFF))
+    ones[:, -1] &= np.uint64((1 << (q % 64)) - 1)
+    zero = np.zeros_like(ones)
+    for c1, c2 in [((zero, zero), (zero, zero)), ((ones, ones), (ones, ones)),
+                   ((ones, zero), (zero, ones))]:
+        st, wa, wb = restated.he_mul(p.log_n, p.log_p, q, q, c1, c2, evk)
+        oa, ob = ctx.he_mul(c1, c2, q, evk=evk)
+        assert np.array_equal(oa, wa) and np.array_equal(ob, wb)
+
+
+def test_batch_equals_singles(restated):
+    cfg = (30, 4, 12)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    q = p.log_q_max
+    rng = np.random.default_rng(9)
+    evk = (random_poly(rng, p.n, 2 * q), random_poly(rng, p.n, 2 * q))
+    B = 3
+    c1 = [np.stack([random_poly(rng, p.n, q) for _ in range(B)]) for _ in range(2)]
+    c2 = [np.stack([random_poly(rng, p.n, q) for _ in range(B)]) for _ in range(2)]
+    oa, ob = ctx.he_mul((c1[0], c1[1]), (c2[0], c2[1]), q, evk=evk)
+    assert oa.shape == (B, p.n, 2)
+    for b in range(B):
+        sa, sb = ctx.he_mul((c1[0][b], c1[1][b]), (c2[0][b], c2[1][b]), q, evk=evk)
+        assert np.array_equal(oa[b], sa) and np.array_equal(ob[b], sb)
+    st, wa, wb = restated.he_mul(p.log_n, p.log_p, q, q, (c1[0][1], c1[1][1]),
+                                 (c2[0][1], c2[1][1]), evk)
+    assert np.array_equal(oa[1], wa) and np.array_equal(ob[1], wb)
+
+
+def test_errors_match_reference_kinds():
+    """heaan.cpp:341-345: mismatch -> invalid_argument, depth -> runtime_error
+    (test_heaan.cpp:169-182)."""
+    ctx = _ctx((30, 4, 10))
+    p = ctx.params
+    z = np.zeros((p.n, 2), np.uint64)
+    with pytest.raises(ValueError, match="ciphertext modulus mismatch"):
+        ctx.he_mul((z, z), (z, z), 120, c2_log_q=90, evk=(np.zeros((p.n, 4), np.uint64),) * 2)
+    z1 = np.zeros((p.n, 1), np.uint64)
+    with pytest.raises(RuntimeError, match="multiplicative depth exhausted"):
+        ctx.he_mul((z1, z1), (z1, z1), 30, evk=(np.zeros((p.n, 4), np.uint64),) * 2)
+    with pytest.raises(RuntimeError, match="modulus exhausted; cannot rescale"):
+        ctx.rescale((z1, z1), 30)
+
+
+def test_rescale_matches_reference(reference):
+    cfg = (30, 4, 10)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    rng = np.random.default_rng(4)
+    a = random_poly(rng, p.n, 120)
+    b = random_poly(rng, p.n, 120)
+    oa, ob = ctx.rescale((a, b), 120)
+    assert np.array_equal(oa, reference.shift_right(p.n, 120, 30, a))
+    assert np.array_equal(ob, reference.shift_right(p.n, 120, 30, b))
+
+
+def test_device_resident_inputs_torch():
+    torch = pytest.importorskip("torch")
+    g = np.load(GOLDEN / "s_bench.npz")
+    ctx = _ctx((30, 4, 13))
+    q = int(g["log_q"])
+    dev = {k: torch.from_numpy(g[k]).cuda() for k in ("c1ax", "c1bx", "c2ax", "c2bx",
+                                                       "evkax", "evkbx")}
+    launches0 = ctx.launch_count()
+    oa, ob = ctx.he_mul((dev["c1ax"], dev["c1bx"]), (dev["c2ax"], dev["c2bx"]), q,
+                        evk=(dev["evkax"], dev["evkbx"]))
+    ctx.synchronize()
+    assert oa.is_cuda
+    assert np.array_equal(oa.cpu().numpy(), g["outax"])
+    assert np.array_equal(ob.cpu().numpy(), g["outbx"])
+    assert ctx.launch_count() > launches0
+
+
+def test_stage_timing_buckets():
+    g = np.load(GOLDEN / "s_bench.npz")
+    ctx = _ctx((30, 4, 13))
+    ctx.enable_stage_timing(True)
+    q = int(g["log_q"])
+    ctx.he_mul((g["c1ax"], g["c1bx"]), (g["c2ax"], g["c2bx"]), q, evk=(g["evkax"], g["evkbx"]))
+    ms = ctx.stage_ms()
+    assert set(ms) == {"crt", "ntt", "intt", "icrt", "extra"}
+    assert all(v > 0 for v in ms.values())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["logN14_logQ300", "M", "X"])
+def test_bench_protocol_digest_paper_scale(name, reference):
+    """Digest of he_mul on the reference's own seed-7 keys and ciphertexts
+    equals the reference's."""
+    d = json.loads((GOLDEN / "digests.json").read_text())[name]
+    cfg = tuple(d["params"])
+    inp = reference.bench_inputs(*cfg, seed=7)
+    ctx = _ctx(cfg)
+    q = inp["log_q_max"]
+    oa, ob = ctx.he_mul(inp["c1"], inp["c2"], q, evk=inp["evk"])
+    assert f"{_digest(q - cfg[0], oa, ob):016x}" == d["digest"]
