@@ -1,0 +1,444 @@
+"""HE Mul (+ relinearize + rescale) benchmark — BASELINE.json's metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config X|M|S]
+                    [--batch B] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1)
+
+One step = one batched call of the reference-facing entry point
+(hemul_gpu_he_mul, include/hemul_gpu.h == Scheme::he_mul, heaan.cpp:339-410)
+on B independent ciphertext pairs per GPU at the fresh modulus of the
+config (default X: N=2^17, logQ=2400 — the paper-scale point the metric is
+quoted on). Independent HE Muls shard by ciphertext across GPUs (weak
+scaling, replicated evk, no collective inside the timed region; NCCL only
+takes the max of the per-rank times and gathers result digests afterwards).
+
+Printed JSON (rank 0, one line):
+  value     whole-job HE Mul/s with inputs resident in HBM (device event time,
+            max over ranks)
+  latency_us  single HE Mul (batch 1) device latency on rank 0
+  e2e       the same metric through the C-ABI with pinned HOST buffers: every
+            step copies its inputs H2D and its outputs D2H inside the timed
+            region
+  roofline  dominant kernel class of the timed region: its algorithmic
+            integer work (32-bit IMAD-equivalent ops) / its
+            measured device time, against the IMAD.WIDE peak measured on this
+            device in this run (integer-bound path; MEASURED_PEAKS.json has
+            only HBM and bf16 peaks)
+  cpu_baseline  the reference CPU he_mul (oracle/_ref, compiled from the
+            reference sources) on this host's cores, 1 HE Mul sample
+--impl reference times that same reference CPU implementation as the whole
+arm (all host threads), on the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("HE Mul latency (µs) at N=2^17; batched HE Mul/s at 1/2/4/8 B200 vs CPU ref")
+CONFIGS = {  # make_params(log_p, depth, w64, log_n_override)
+    "X": (30, 80, 0),   # N=2^17, logQ=2400 (paper scale; BASELINE configs[3,4])
+    "M": (30, 40, 0),   # N=2^16, logQ=1200 (paper Table 7 point)
+    "S": (30, 4, 13),   # N=2^13, logQ=120
+}
+DEFAULT_BATCH = {"X": 8, "M": 16, "S": 64}
+
+
+def limbs(bits: int) -> int:
+    return (bits + 63) // 64
+
+
+# --------------------------------------------------------------------------
+# algorithmic integer work (32-bit IMAD-equivalent multiply-adds), DESIGN.md §4
+# --------------------------------------------------------------------------
+SHOUP_IMAD = 9    # 64-bit Shoup modmul: 3 (approx quotient) + 6 (remainder)
+MULMOD_IMAD = 26  # 64x64 product (8) + two Shoup reductions (2 x 9)
+
+
+def region_shapes(cfg, log_q):
+    from paper_2003_04510_b200.hemul import make_params
+
+    p = make_params(*cfg)
+    return p
+
+
+def work_per_step(p, np1: int, np2: int, B: int, log_q: int) -> dict[str, float]:
+    n, ln = p.n, p.log_n
+    s1 = ln if ln <= 11 else (ln + 1) // 2
+    s2 = ln - s1
+    m_in = math.ceil(log_q / 30)
+    m1 = math.ceil(log_q / 30)
+    m2 = math.ceil((log_q + p.log_q_max) / 30)
+    fwd_rows = 4 * B * np1 + B * np2
+    inv_rows = 3 * B * np1 + 2 * B * np2
+    bf = n // 2
+    return {
+        "crt": n * B * (4 * np1 + np2) * 2 * m_in,
+        "ntt_a": fwd_rows * bf * s1 * SHOUP_IMAD,
+        "ntt_b": fwd_rows * bf * s2 * SHOUP_IMAD,
+        "intt_b": inv_rows * bf * s2 * SHOUP_IMAD,
+        "intt_a": inv_rows * bf * s1 * SHOUP_IMAD + inv_rows * n * SHOUP_IMAD,
+        "tensor": n * B * np1 * 4 * MULMOD_IMAD,
+        "evk": n * B * np2 * 2 * MULMOD_IMAD,
+        "icrt": n * B * (3 * ((2 * np1 + 1) * m1 + np1 * SHOUP_IMAD)
+                         + 2 * ((2 * np2 + 1) * m2 + np2 * SHOUP_IMAD)),
+    }
+
+
+def reference_w_int(p, np1, np2, pl1, pl2, log_q):
+    """reference-algorithm IMAD slots per HE Mul (8 per 64x64
+    MAC, 16 per Shoup modmul)."""
+    n, ln = p.n, p.log_n
+    L = limbs(log_q)
+    mac = n * (6 * np1 * L + np2 * L + 3 * np1 + 2 * np2 + 3 * np1 * pl1 + 2 * np2 * pl2)
+    mod = (n * (18 * np1 + 3 * np2) + (n // 2) * ln * (6 * np1 + np2)
+           + 2 * n * (3 * np1 + 2 * np2) + (3 * np1 + 2 * np2) * ((n // 2) * ln + n)
+           + n * (3 * np1 + 2 * np2))
+    return 8 * mac + 16 * mod
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md)
+# --------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# reference CPU arm / baseline
+# --------------------------------------------------------------------------
+def reference_cpu(cfg, reps: int, threads: int, seed: int = 1):
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import REFERENCE_SO, Reference
+
+    if not REFERENCE_SO.exists():
+        return None, "oracle/_ref/libhemul_ref.so missing (build it where /root/reference exists)"
+    ref = Reference()
+    t0 = time.time()
+    ms, dig = ref.time_he_mul(*cfg, seed=seed, reps=reps, threads=threads, radix_log=1)
+    return {"ms": ms, "digest": f"{dig:016x}", "wall_s": time.time() - t0}, None
+
+
+def run_reference_arm(args, cfg, rank: int) -> None:
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # one step = one full HE Mul; warm-up steps run untimed
+    res, why = reference_cpu(cfg, reps=args.warmup + args.steps, threads=threads)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return
+    timed = res["ms"][args.warmup:]
+    ms = statistics.mean(timed)
+    value = 1000.0 / ms
+    from paper_2003_04510_b200.hemul import make_params
+
+    p = make_params(*cfg)
+    sample = (f"{args.steps} timed + {args.warmup} warm-up reference Scheme::he_mul calls "
+              f"(N=2^{p.log_n}, logQ={p.log_q_max}), random inputs, level warmed outside timing")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "HE Mul/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "latency_us": ms * 1000.0, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: HE Mul N=2^{p.log_n} logQ={p.log_q_max}",
+                   "batch_per_gpu": 1, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "HE Mul/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "HE Mul/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "digest": res["digest"],
+    }))
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="X", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="HE Muls per GPU per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency-reps", type=int, default=5)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    B = args.batch or DEFAULT_BATCH[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_04510_b200.hemul import Context, ciphertext_digest, make_params
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = make_params(*cfg)
+    ctx = Context(p, device=local)
+    # a dedicated (non-legacy) stream shared by torch and the library, so the
+    # CUDA events below bracket the library's kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    q = p.log_q_max
+    L, Lo, Le = limbs(q), limbs(q - p.log_p), limbs(2 * q)
+    n = p.n
+
+    # synthetic random ciphertexts and keys (SURVEY §8(d) throughput inputs),
+    # generated on the device, resident before timing; per-rank seeds
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000 + rank)
+
+    def rand_poly(batch, bits):
+        t = torch.randint(-(2**63), 2**63 - 1, (batch, n, limbs(bits)), generator=g,
+                          device="cuda", dtype=torch.int64)
+        if bits % 64:
+            t[..., -1] &= (1 << (bits % 64)) - 1
+        return t.view(torch.uint64)
+
+    c1 = (rand_poly(B, q), rand_poly(B, q))
+    c2 = (rand_poly(B, q), rand_poly(B, q))
+    evk = (rand_poly(1, 2 * q)[0].contiguous(), rand_poly(1, 2 * q)[0].contiguous())
+    out = (torch.empty((B, n, Lo), dtype=torch.uint64, device="cuda"),
+           torch.empty((B, n, Lo), dtype=torch.uint64, device="cuda"))
+    t0 = time.time()
+    ctx.warm_level(q, evk, evk_id=1)
+    level_s = time.time() - t0
+    np1, np2 = len(ctx.level_primes(q, 1)), len(ctx.level_primes(q, 2))
+
+    def step(b=B, o=out):
+        ctx.he_mul((c1[0][:b], c1[1][:b]), (c2[0][:b], c2[1][:b]), q, evk=evk, evk_id=1,
+                   out=(o[0][:b], o[1][:b]))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up ---------------------------------------------------------
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- headline timed region: device-resident inputs --------------------
+    ctx.enable_stage_timing(True)
+    ctx.reset_stats()
+    launches0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - launches0
+    kstats = ctx.kernel_stats()
+    ctx.enable_stage_timing(False)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = world * B * args.steps / (elapsed_ms / 1000.0)
+    ms_per_step = elapsed_ms / args.steps
+
+    # ---- single HE Mul latency (batch 1) ----------------------------------
+    lat = []
+    for _ in range(args.latency_reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step(1)
+        b.record(stream)
+        torch.cuda.synchronize()
+        lat.append(a.elapsed_time(b) * 1000.0)
+    latency_us = statistics.median(lat)
+
+    # ---- stage breakdown of one HE Mul (reference buckets) ----------------
+    ctx.enable_stage_timing(True)
+    step()
+    stage_ms = ctx.stage_ms()
+    ctx.enable_stage_timing(False)
+
+    # ---- e2e through the C-ABI with pinned host buffers --------------------
+    hc1 = tuple(x.cpu().pin_memory() for x in c1)
+    hc2 = tuple(x.cpu().pin_memory() for x in c2)
+    ho = tuple(torch.empty((B, n, Lo), dtype=torch.uint64).pin_memory() for _ in range(2))
+    nph = lambda t: t.numpy()  # noqa: E731 — pinned tensors viewed as host arrays
+
+    def e2e_step():
+        ctx.he_mul((nph(hc1[0]), nph(hc1[1])), (nph(hc2[0]), nph(hc2[1])), q, evk=evk,
+                   evk_id=1, out=(nph(ho[0]), nph(ho[1])))
+
+    e2e_step()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * B * e2e_steps / (e2e_ms / 1000.0)
+    if not torch.equal(ho[0], out[0].cpu()):
+        raise RuntimeError("e2e output differs from the device-resident output")
+
+    # ---- result digests gathered to rank 0 (after timing) ------------------
+    o0 = out[0][0].cpu().numpy(), out[1][0].cpu().numpy()
+    dig = ciphertext_digest(q - p.log_p, o0[0], o0[1])
+    digests = [dig]
+    if world > 1:
+        buf = [None] * world
+        dist.all_gather_object(buf, dig)
+        digests = buf
+
+    # ---- roofline of the dominant kernel class ----------------------------
+    imad_peak = ctx.imad_peak()
+    work = work_per_step(p, np1, np2, B, q)
+    per_class = {}
+    for k, (ms, cnt) in kstats.items():
+        if k in work and ms > 0:
+            per_class[k] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
+                            "tiops": work[k] / (ms / args.steps * 1e-3) / 1e12}
+    dom = max(per_class, key=lambda k: per_class[k]["ms_per_step"])
+    achieved = per_class[dom]["tiops"]
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
+    pl1 = pl2 = None
+    # reference-algorithm W_int over the measured step time
+    from math import ceil
+    # limbs of P1 / P2 (the reference's iCRT MAC width)
+    P1bits = sum(float(np.log2(float(x))) for x in ctx.level_primes(q, 1))
+    P2bits = sum(float(np.log2(float(x))) for x in ctx.level_primes(q, 2))
+    pl1, pl2 = ceil(P1bits / 64), ceil(P2bits / 64)
+    w_int = reference_w_int(p, np1, np2, pl1, pl2, q)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            res, why = reference_cpu(cfg, reps=1, threads=threads)
+            if res is not None:
+                v = 1000.0 / res["ms"][0]
+                cpu = {"value": v, "unit": "HE Mul/s", "cores": threads, "kind": "reference",
+                       "sample": f"1 reference Scheme::he_mul (N=2^{p.log_n}, logQ={q}) on "
+                                 f"{threads} threads, random inputs, level warmed outside timing",
+                       "latency_ms": res["ms"][0]}
+            else:
+                cpu = {"value": None, "unavailable": why}
+        line = {
+            "metric": METRIC, "value": value, "unit": "HE Mul/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "latency_us": latency_us, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: batched HE Mul+relin+rescale, "
+                                   f"N=2^{p.log_n}, logQ={q}, np1={np1}, np2={np2}",
+                       "batch_per_gpu": B, "global_batch": B * world,
+                       "parallelism": f"ciphertext-sharded x{world}, evk replicated",
+                       "l2": f"inputs {4 * B * n * L * 8 / 2**20:.0f} MiB per step > 126 MiB L2"},
+            "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": "HE Mul/s",
+                    "h2d_bytes_per_step": 4 * B * n * L * 8,
+                    "d2h_bytes_per_step": 2 * B * n * Lo * 8},
+            "roofline": {"bound": "imad", "kernel": dom, "achieved": achieved,
+                         "peak": imad_peak / 1e12, "unit": "TIOP/s (32-bit IMAD)",
+                         "frac": achieved / (imad_peak / 1e12), "traffic": traffic,
+                         "peak_source": "IMAD.WIDE.U32 probe on this device, this run"},
+            "he_mul_roofline": {"reference_w_int_imad_slots": w_int,
+                                "achieved_tslots": w_int * B / (ms_per_step * 1e-3) / 1e12,
+                                "frac_of_imad_peak": w_int * B / (ms_per_step * 1e-3) / imad_peak},
+            "kernels": per_class,
+            "stage_ms_one_call": stage_ms,
+            "level_setup_s": level_s,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "digests": [f"{d:016x}" for d in digests],
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -63,6 +63,11 @@ typedef enum {
 enum { HEMUL_STAGE_CRT = 0, HEMUL_STAGE_NTT, HEMUL_STAGE_INTT, HEMUL_STAGE_ICRT,
        HEMUL_STAGE_EXTRA, HEMUL_STAGE_COUNT };
 
+/* Kernel classes for per-launch device timing (hemul_gpu_kernel_stats). */
+enum { HEMUL_KCLASS_CRT = 0, HEMUL_KCLASS_NTT_A, HEMUL_KCLASS_NTT_B, HEMUL_KCLASS_INTT_B,
+       HEMUL_KCLASS_INTT_A, HEMUL_KCLASS_TENSOR, HEMUL_KCLASS_EVK, HEMUL_KCLASS_ICRT,
+       HEMUL_KCLASS_EPILOGUE, HEMUL_KCLASS_H2D, HEMUL_KCLASS_D2H, HEMUL_KCLASS_COUNT };
+
 /* make_params(log_p, depth, w64, log_n_override) (params.cpp:64-74) and a
  * context on CUDA device `device`. log_n_override = 0 uses the security table
  * (params.cpp:56-62). */
@@ -72,6 +77,11 @@ void hemul_gpu_destroy(hemul_gpu_ctx *ctx);
 const char *hemul_gpu_last_error(const hemul_gpu_ctx *ctx);
 /* {log_n, n, log_p, depth, log_q_max} */
 hemul_status hemul_gpu_params(const hemul_gpu_ctx *ctx, int out[5]);
+
+/* Launch everything on `stream` (a cudaStream_t of the context's device;
+ * NULL = the context's own stream). Lets a caller (e.g. PyTorch) order the
+ * library's kernels with its own work and time them with its own events. */
+hemul_status hemul_gpu_set_stream(hemul_gpu_ctx *ctx, void *stream);
 
 /* Build (or fetch from the 2-entry LRU, heaan.cpp:119-150) the tables of
  * modulus log_q. */
@@ -101,11 +111,21 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx *ctx, int c1_log_q, int c2_log_q, si
 hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, const uint64_t *ax,
                                const uint64_t *bx, uint64_t *out_ax, uint64_t *out_bx);
 
-/* Per-stage device milliseconds of the last he_mul call (CUDA events on the
- * context stream), buckets as counters.hpp:13. Timing is only recorded when
- * enabled (it inserts events between stages). */
+/* Device timing. When enabled every launch is bracketed by CUDA events on the
+ * context stream (read back lazily, so no extra host sync per call).
+ * stage_ms: per-stage milliseconds of the last he_mul call, buckets as
+ * counters.hpp:13 (pointwise booked under iCRT like rns.cpp:364).
+ * kernel_stats: cumulative milliseconds and launch counts per kernel class
+ * since the last reset_stats. */
 hemul_status hemul_gpu_enable_stage_timing(hemul_gpu_ctx *ctx, int on);
-hemul_status hemul_gpu_stage_ms(const hemul_gpu_ctx *ctx, double ms[HEMUL_STAGE_COUNT]);
+hemul_status hemul_gpu_stage_ms(hemul_gpu_ctx *ctx, double ms[HEMUL_STAGE_COUNT]);
+hemul_status hemul_gpu_kernel_stats(hemul_gpu_ctx *ctx, double ms[HEMUL_KCLASS_COUNT],
+                                    uint64_t launches[HEMUL_KCLASS_COUNT]);
+hemul_status hemul_gpu_reset_stats(hemul_gpu_ctx *ctx);
+
+/* Integer-pipe roofline denominator: measured IMAD.WIDE.U32 ops/s of the
+ * context's device (a short probe kernel). */
+hemul_status hemul_gpu_imad_peak(hemul_gpu_ctx *ctx, double *ops_per_s);
 
 /* Region tables of level log_q: region 1 (products mod q) or 2 (key
  * switching). Writes np and up to cap primes. */

@@ -11,6 +11,7 @@
 //   * expose the per-stage kernels (CRT / NTT / pointwise / iCRT) on the same
 //     level tables Scheme::level builds (proj/core/src/heaan.cpp:119-169),
 // so every GPU stage can be compared residue for residue.
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -226,6 +227,48 @@ int ref_run_bench(int log_p, int depth, int log_n_override, uint64_t seed,
       ms_out[6] = r.total_median_ms;
     }
     if (digest) *digest = r.result_digest;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
+// The CPU baseline: one Scheme, level + evk forms warmed outside the timing
+// (bench.cpp:68-69), then `reps` timed he_mul calls on random ciphertexts and
+// a random evk (uniform_bits, rng.hpp:30-41) at the fresh modulus.
+// ms_out[r] = wall milliseconds of rep r. Returns the output digest.
+int ref_time_he_mul(int log_p, int depth, int log_n_override, uint64_t seed, int reps,
+                    int threads, int radix_log, double* ms_out, uint64_t* digest) {
+  try {
+    const Params p = make_params(log_p, depth, WordSize::w64, log_n_override);
+    std::unique_ptr<ThreadPool> pool;
+    if (threads > 1) pool = std::make_unique<ThreadPool>(threads);
+    Scheme scheme(p, pool.get());
+    scheme.options().ntt.radix_log = radix_log > 0 ? radix_log : 1;
+    Rng rng(seed);
+    auto rnd = [&](int bits) {
+      BigPoly a = make_poly(p.n, bits, WordSize::w64);
+      for (int i = 0; i < p.n; ++i) poly_set(a, i, rng.uniform_bits(bits, WordSize::w64));
+      return a;
+    };
+    Ciphertext c1, c2;
+    c1.ax = rnd(p.log_q_max);
+    c1.bx = rnd(p.log_q_max);
+    c2.ax = rnd(p.log_q_max);
+    c2.bx = rnd(p.log_q_max);
+    c1.log_q = c2.log_q = p.log_q_max;
+    EvalKey evk;
+    evk.ax = rnd(2 * p.log_q_max);
+    evk.bx = rnd(2 * p.log_q_max);
+    scheme.warm_level(p.log_q_max, &evk);
+    Ciphertext out;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      out = scheme.he_mul(c1, c2, evk);
+      const auto t1 = std::chrono::steady_clock::now();
+      ms_out[r] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    }
+    if (digest) *digest = ciphertext_digest(out);
     return 0;
   } catch (const std::exception& e) {
     return fail(e, 1);

@@ -105,14 +105,19 @@ void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
 struct hemul_gpu_ctx {
   int device = 0;
   int log_n = 0, n = 0, log_p = 0, depth = 0, log_q_max = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // where every launch goes
+  cudaStream_t own_stream = nullptr;  // created by the context
   std::list<std::unique_ptr<Level>> cache;  // most recent first, capacity 2
   std::string err;
   uint64_t launches = 0;
   bool timing = false;
+  uint64_t call_id = 0;  // he_mul calls, to attribute stage times
   double stage_ms[HEMUL_STAGE_COUNT] = {};
+  double kclass_ms[HEMUL_KCLASS_COUNT] = {};
+  uint64_t kclass_launches[HEMUL_KCLASS_COUNT] = {};
   struct Mark {
-    int stage;
+    int stage, klass;
+    uint64_t call;
     cudaEvent_t a, b;
   };
   std::vector<Mark> marks;
@@ -158,25 +163,49 @@ hemul_status guarded(hemul_gpu_ctx* c, F&& f) {
   }
 }
 
-// Stage timing scope (counters.hpp:58-76 ScopedStageTimer, on the device).
-struct StageScope {
-  hemul_gpu_ctx* c;
-  int stage;
+// Runs one launch (or copy) f() on the context stream; with timing on, the
+// launch is bracketed by CUDA events and attributed to a reference stage
+// bucket (counters.hpp:13, ScopedStageTimer counters.hpp:58-76) and to a
+// kernel class. Events are read back lazily (flush_marks).
+template <typename F>
+void run(hemul_gpu_ctx* c, int stage, int klass, const char* what, F&& f) {
   cudaEvent_t a = nullptr;
-  StageScope(hemul_gpu_ctx* ctx, int s) : c(ctx), stage(s) {
-    if (c->timing) {
-      a = c->take_event();
-      cudaEventRecord(a, c->stream);
-    }
+  if (c->timing) {
+    a = c->take_event();
+    check(cudaEventRecord(a, c->stream), "event");
   }
-  ~StageScope() {
-    if (c->timing) {
-      cudaEvent_t b = c->take_event();
-      cudaEventRecord(b, c->stream);
-      c->marks.push_back({stage, a, b});
-    }
+  check(f(), what);
+  if (klass < HEMUL_KCLASS_H2D) ++c->launches;
+  if (c->timing) {
+    cudaEvent_t b = c->take_event();
+    check(cudaEventRecord(b, c->stream), "event");
+    c->marks.push_back({stage, klass, c->call_id, a, b});
   }
-};
+}
+
+// Reads back every pending event pair: stage times of the latest he_mul and
+// cumulative per-kernel-class times.
+void flush_marks(hemul_gpu_ctx* c) {
+  if (c->marks.empty()) return;
+  check(cudaStreamSynchronize(c->stream), "timing sync");
+  bool fresh = false;
+  for (auto& m : c->marks) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, m.a, m.b);
+    if (m.call == c->call_id) {
+      if (!fresh) {
+        for (double& v : c->stage_ms) v = 0;
+        fresh = true;
+      }
+      c->stage_ms[m.stage] += ms;
+    }
+    c->kclass_ms[m.klass] += ms;
+    ++c->kclass_launches[m.klass];
+    c->event_pool.push_back(m.a);
+    c->event_pool.push_back(m.b);
+  }
+  c->marks.clear();
+}
 
 void fill_region(RegionDev& d, const RegionHost& h, int log_n, cudaStream_t st) {
   d.np = h.np;
@@ -237,21 +266,6 @@ Level& get_level(hemul_gpu_ctx* c, int log_q) {
   return *c->cache.front();
 }
 
-// Device view of a caller buffer: device pointers pass through, host
-// pointers are staged in `scratch` (at byte offset off).
-const uint64_t* to_device(hemul_gpu_ctx* c, const uint64_t* p, size_t words, DevBuf& scratch,
-                          size_t off_words) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
-    if (a.device != c->device) throw std::invalid_argument("device pointer on another GPU");
-    return p;
-  }
-  cudaGetLastError();
-  uint64_t* d = scratch.as<uint64_t>() + off_words;
-  check(cudaMemcpyAsync(d, p, words * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
-  return d;
-}
-
 bool is_device(const hemul_gpu_ctx* c, const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
@@ -268,49 +282,78 @@ void ensure(DevBuf& b, size_t bytes) {
 
 int limbs_of(int bits) { return (bits + 63) / 64; }
 
+// Forward NTT of `rows` rows, one launch per memory pass.
+void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage) {
+  for (int pass = 0; pass < ntt_num_passes(c->log_n); ++pass)
+    run(c, stage, pass == 0 ? HEMUL_KCLASS_NTT_A : HEMUL_KCLASS_NTT_B, "NTT", [&] {
+      return ntt_forward_pass(pass, data, rows, r.np, c->log_n, r.tw.as<Twiddle>(),
+                              r.primes.as<DevPrime>(), c->stream);
+    });
+}
+
+void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage) {
+  const int passes = ntt_num_passes(c->log_n);
+  for (int pass = 0; pass < passes; ++pass)
+    run(c, stage, pass + 1 == passes ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B, "iNTT", [&] {
+      return ntt_inverse_pass(pass, data, rows, r.np, c->log_n, r.itw.as<Twiddle>(),
+                              r.primes.as<DevPrime>(), c->stream);
+    });
+}
+
+// Stages a caller buffer on the device when it is host memory.
+const uint64_t* stage_in(hemul_gpu_ctx* c, const uint64_t* p, size_t words, uint64_t* scratch) {
+  if (is_device(c, p)) return p;
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D",
+      [&] { return cudaMemcpyAsync(scratch, p, words * 8, cudaMemcpyHostToDevice, c->stream); });
+  return scratch;
+}
+
+// Scheme::level's evk transforms (heaan.cpp:152-167): CRT of the 2 log_Q-bit
+// key polys into the region-2 primes + forward NTT, kept on the device.
 void set_evk_forms(hemul_gpu_ctx* c, Level& lv, const uint64_t* evk_ax, const uint64_t* evk_bx,
                    uint64_t id) {
   const size_t n = size_t(c->n);
   const int Le = limbs_of(2 * c->log_q_max);
   const RegionDev& r2 = lv.r2;
-  ensure(lv.evk_a, size_t(r2.np) * n * 8);
-  ensure(lv.evk_b, size_t(r2.np) * n * 8);
+  ensure(lv.evk_a, 2 * size_t(r2.np) * n * 8);  // [evk_ax form | evk_bx form]
   ensure(c->in, 2 * n * Le * 8);
-  const uint64_t* a = to_device(c, evk_ax, n * Le, c->in, 0);
-  const uint64_t* b = to_device(c, evk_bx, n * Le, c->in, n * Le);
+  const uint64_t* a = stage_in(c, evk_ax, n * Le, c->in.as<uint64_t>());
+  const uint64_t* b = stage_in(c, evk_bx, n * Le, c->in.as<uint64_t>() + n * Le);
   const CrtWeights* w = r2.weights(2 * c->log_q_max);
-  int launches = 0;
-  check(crt_forward(a, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np,
-                    lv.evk_a.as<uint64_t>(), c->stream),
-        "evk CRT");
-  check(crt_forward(b, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np,
-                    lv.evk_b.as<uint64_t>(), c->stream),
-        "evk CRT");
-  c->launches += 2;
-  check(ntt_forward(lv.evk_a.as<uint64_t>(), r2.np, r2.np, c->log_n, r2.tw.as<Twiddle>(),
-                    r2.primes.as<DevPrime>(), c->stream, &launches),
-        "evk NTT");
-  check(ntt_forward(lv.evk_b.as<uint64_t>(), r2.np, r2.np, c->log_n, r2.tw.as<Twiddle>(),
-                    r2.primes.as<DevPrime>(), c->stream, &launches),
-        "evk NTT");
-  c->launches += launches;
+  uint64_t* fa = lv.evk_a.as<uint64_t>();
+  uint64_t* fb = fa + size_t(r2.np) * n;
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
+    return crt_forward(a, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np, fa, c->stream);
+  });
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
+    return crt_forward(b, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np, fb, c->stream);
+  });
+  ntt_fwd(c, r2, fa, 2 * size_t(r2.np), HEMUL_STAGE_EXTRA);
   check(cudaStreamSynchronize(c->stream), "evk forms");
   lv.has_evk = true;
   lv.evk_id = id;
 }
 
-void collect_timing(hemul_gpu_ctx* c) {
-  for (double& v : c->stage_ms) v = 0;
-  if (!c->timing) return;
-  check(cudaStreamSynchronize(c->stream), "timing sync");
-  for (auto& m : c->marks) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, m.a, m.b);
-    c->stage_ms[m.stage] += ms;
-    c->event_pool.push_back(m.a);
-    c->event_pool.push_back(m.b);
-  }
-  c->marks.clear();
+// Output buffers: the caller's device buffers, or scratch + D2H.
+struct OutPair {
+  uint64_t* a;
+  uint64_t* b;
+  bool device;
+};
+
+OutPair out_pair(hemul_gpu_ctx* c, uint64_t* oa, uint64_t* ob, size_t words, DevBuf& scratch) {
+  if (is_device(c, oa) && is_device(c, ob)) return {oa, ob, true};
+  ensure(scratch, 2 * words * 8);
+  return {scratch.as<uint64_t>(), scratch.as<uint64_t>() + words, false};
+}
+
+void copy_out(hemul_gpu_ctx* c, const OutPair& o, uint64_t* oa, uint64_t* ob, size_t words) {
+  if (o.device) return;
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
+      [&] { return cudaMemcpyAsync(oa, o.a, words * 8, cudaMemcpyDeviceToHost, c->stream); });
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
+      [&] { return cudaMemcpyAsync(ob, o.b, words * 8, cudaMemcpyDeviceToHost, c->stream); });
+  check(cudaStreamSynchronize(c->stream), "D2H");
 }
 
 }  // namespace
@@ -346,8 +389,9 @@ hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_overri
   if (c->log_n < 7 || c->log_n > 17) return HEMUL_E_ARG;
   c->n = 1 << c->log_n;
   if (cudaSetDevice(device) != cudaSuccess) return HEMUL_E_CUDA;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return HEMUL_E_CUDA;
+  c->stream = c->own_stream;
   if (ntt_setup_attributes() != cudaSuccess || crt_setup_attributes() != cudaSuccess ||
       icrt_setup_attributes() != cudaSuccess)
     return HEMUL_E_CUDA;
@@ -365,7 +409,7 @@ void hemul_gpu_destroy(hemul_gpu_ctx* c) {
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   c->cache.clear();
-  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->own_stream);
   delete c;
 }
 
@@ -379,6 +423,15 @@ hemul_status hemul_gpu_params(const hemul_gpu_ctx* c, int out[5]) {
   out[3] = c->depth;
   out[4] = c->log_q_max;
   return HEMUL_OK;
+}
+
+hemul_status hemul_gpu_set_stream(hemul_gpu_ctx* c, void* stream) {
+  if (!c) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    check(cudaStreamSynchronize(c->stream), "stream switch");
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    return HEMUL_OK;
+  });
 }
 
 hemul_status hemul_gpu_set_level(hemul_gpu_ctx* c, int log_q) {
@@ -417,10 +470,46 @@ hemul_status hemul_gpu_enable_stage_timing(hemul_gpu_ctx* c, int on) {
   return HEMUL_OK;
 }
 
-hemul_status hemul_gpu_stage_ms(const hemul_gpu_ctx* c, double ms[HEMUL_STAGE_COUNT]) {
+hemul_status hemul_gpu_stage_ms(hemul_gpu_ctx* c, double ms[HEMUL_STAGE_COUNT]) {
   if (!c || !ms) return HEMUL_E_ARG;
-  for (int i = 0; i < HEMUL_STAGE_COUNT; ++i) ms[i] = c->stage_ms[i];
-  return HEMUL_OK;
+  return guarded(c, [&] {
+    flush_marks(c);
+    for (int i = 0; i < HEMUL_STAGE_COUNT; ++i) ms[i] = c->stage_ms[i];
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_kernel_stats(hemul_gpu_ctx* c, double ms[HEMUL_KCLASS_COUNT],
+                                    uint64_t launches[HEMUL_KCLASS_COUNT]) {
+  if (!c) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    flush_marks(c);
+    for (int i = 0; i < HEMUL_KCLASS_COUNT; ++i) {
+      if (ms) ms[i] = c->kclass_ms[i];
+      if (launches) launches[i] = c->kclass_launches[i];
+    }
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_reset_stats(hemul_gpu_ctx* c) {
+  if (!c) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    flush_marks(c);
+    for (int i = 0; i < HEMUL_KCLASS_COUNT; ++i) {
+      c->kclass_ms[i] = 0;
+      c->kclass_launches[i] = 0;
+    }
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_imad_peak(hemul_gpu_ctx* c, double* ops_per_s) {
+  if (!c || !ops_per_s) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    check(imad_peak(ops_per_s, c->stream), "IMAD probe");
+    return HEMUL_OK;
+  });
 }
 
 uint64_t hemul_gpu_launch_count(const hemul_gpu_ctx* c) { return c ? c->launches : 0; }
@@ -462,19 +551,13 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     const size_t poly_w = n * L;
     const DevPrime* p1 = r1.primes.as<DevPrime>();
     const DevPrime* p2 = r2.primes.as<DevPrime>();
-    c->marks.clear();
-    int launches = 0;
+    ++c->call_id;
     // ---- inputs ----------------------------------------------------------
     ensure(c->in, 4 * B * poly_w * 8);
+    const uint64_t* src[4] = {c1_ax, c1_bx, c2_ax, c2_bx};
     const uint64_t* in[4];
-    {
-      StageScope s(c, HEMUL_STAGE_EXTRA);
-      in[0] = to_device(c, c1_ax, B * poly_w, c->in, 0);
-      in[1] = to_device(c, c1_bx, B * poly_w, c->in, B * poly_w);
-      in[2] = to_device(c, c2_ax, B * poly_w, c->in, 2 * B * poly_w);
-      in[3] = to_device(c, c2_bx, B * poly_w, c->in, 3 * B * poly_w);
-    }
-    // ---- region 1 ---------------------------------------------------------
+    for (int t = 0; t < 4; ++t) in[t] = stage_in(c, src[t], B * poly_w, c->in.as<uint64_t>() + t * B * poly_w);
+    // ---- region 1: d0 = bx1 bx2, d1 = ax1 bx2 + ax2 bx1, d2 = ax1 ax2 ---------
     const size_t r1w = B * r1.np * n;  // one RNS operand
     ensure(c->r1, 4 * r1w * 8);
     uint64_t* R1 = c->r1.as<uint64_t>();
@@ -483,107 +566,55 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     uint64_t* A2 = R1 + 2 * r1w;
     uint64_t* B2 = R1 + 3 * r1w;
     const CrtWeights* w1 = r1.weights(log_q);
-    {
-      StageScope s(c, HEMUL_STAGE_CRT);
-      uint64_t* dst[4] = {A1, B1, A2, B2};
-      for (int t = 0; t < 4; ++t)
-        check(crt_forward(in[t], L, B, log_n, *w1, p1, r1.np, dst[t], c->stream), "CRT r1");
-      launches += 4;
-    }
-    {
-      StageScope s(c, HEMUL_STAGE_NTT);
-      check(ntt_forward(R1, 4 * B * r1.np, r1.np, log_n, r1.tw.as<Twiddle>(), p1, c->stream,
-                        &launches),
-            "NTT r1");
-    }
-    {
-      // pointwise products are booked under iCRT like rns.cpp:364
-      StageScope s(c, HEMUL_STAGE_ICRT);
-      // in place: d2 -> A1, d0 -> B1, d1 -> A2
-      check(tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream),
-            "tensor product");
-      ++launches;
-    }
-    {
-      StageScope s(c, HEMUL_STAGE_INTT);
-      check(ntt_inverse(R1, 3 * B * r1.np, r1.np, log_n, r1.itw.as<Twiddle>(), p1, c->stream,
-                        &launches),
-            "iNTT r1");
-    }
+    uint64_t* dst[4] = {A1, B1, A2, B2};
+    for (int t = 0; t < 4; ++t)
+      run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
+        return crt_forward(in[t], L, B, log_n, *w1, p1, r1.np, dst[t], c->stream);
+      });
+    ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
+    // pointwise products are booked under iCRT like rns.cpp:364;
+    // in place: d2 -> A1, d0 -> B1, d1 -> A2
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "tensor product", [&] {
+      return tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
+    });
+    ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
     // d polys: [d2 | d0 | d1], each B x n x L
     ensure(c->dpoly, 3 * B * poly_w * 8);
     uint64_t* D = c->dpoly.as<uint64_t>();
     uint64_t* d2 = D;
     uint64_t* d0 = D + B * poly_w;
     uint64_t* d1 = D + 2 * B * poly_w;
-    {
-      StageScope s(c, HEMUL_STAGE_ICRT);
-      check(icrt(R1, 3 * B, log_n, p1, r1.np, r1.icrt, D, c->stream), "iCRT r1");
-      ++launches;
-    }
-    // ---- region 2: ModUp, evk product, ModDown ----------------------------
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1",
+        [&] { return icrt(R1, 3 * B, log_n, p1, r1.np, r1.icrt, D, c->stream); });
+    // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
     const size_t r2w = B * r2.np * n;
     ensure(c->r2, 2 * r2w * 8);
     uint64_t* KA = c->r2.as<uint64_t>();
     uint64_t* KB = KA + r2w;
-    {
-      StageScope s(c, HEMUL_STAGE_CRT);
-      check(crt_forward(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream),
-            "CRT r2");
-      ++launches;
-    }
-    {
-      StageScope s(c, HEMUL_STAGE_NTT);
-      check(ntt_forward(KA, B * r2.np, r2.np, log_n, r2.tw.as<Twiddle>(), p2, c->stream,
-                        &launches),
-            "NTT r2");
-    }
-    {
-      StageScope s(c, HEMUL_STAGE_ICRT);
-      check(evk_product(KA, lv.evk_a.as<uint64_t>(), lv.evk_b.as<uint64_t>(), KA, KB, B, r2.np,
-                        log_n, p2, c->stream),
-            "evk product");
-      ++launches;
-    }
-    {
-      StageScope s(c, HEMUL_STAGE_INTT);
-      check(ntt_inverse(KA, 2 * B * r2.np, r2.np, log_n, r2.itw.as<Twiddle>(), p2, c->stream,
-                        &launches),
-            "iNTT r2");
-    }
+    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2", [&] {
+      return crt_forward(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
+    });
+    ntt_fwd(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
+    const uint64_t* EA = lv.evk_a.as<uint64_t>();
+    const uint64_t* EB = EA + size_t(r2.np) * n;
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
+        [&] { return evk_product(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
+    ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
     ensure(c->ks, 2 * B * n * L2 * 8);
     uint64_t* KS = c->ks.as<uint64_t>();
-    {
-      StageScope s(c, HEMUL_STAGE_ICRT);
-      check(icrt(KA, 2 * B, log_n, p2, r2.np, r2.icrt, KS, c->stream), "iCRT r2");
-      ++launches;
-    }
-    // ---- epilogue ---------------------------------------------------------
-    const bool dev_out = is_device(c, out_ax) && is_device(c, out_bx);
-    uint64_t *oa = out_ax, *ob = out_bx;
-    if (!dev_out) {
-      ensure(c->outb, 2 * B * n * Lo * 8);
-      oa = c->outb.as<uint64_t>();
-      ob = oa + B * n * Lo;
-    }
-    {
-      StageScope s(c, HEMUL_STAGE_EXTRA);
-      check(keyswitch_epilogue(KS, d1, oa, B, log_n, log_q, log_Q, log_p, c->stream),
-            "epilogue ax");
-      check(keyswitch_epilogue(KS + B * n * L2, d0, ob, B, log_n, log_q, log_Q, log_p,
-                               c->stream),
-            "epilogue bx");
-      launches += 2;
-      if (!dev_out) {
-        check(cudaMemcpyAsync(out_ax, oa, B * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
-              "D2H");
-        check(cudaMemcpyAsync(out_bx, ob, B * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
-              "D2H");
-      }
-    }
-    c->launches += launches;
-    if (!dev_out) check(cudaStreamSynchronize(c->stream), "he_mul");
-    collect_timing(c);
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r2",
+        [&] { return icrt(KA, 2 * B, log_n, p2, r2.np, r2.icrt, KS, c->stream); });
+    // ---- epilogue: R_logp(d + R_logQ(ks)) ------------------------------------
+    const size_t ow = B * n * Lo;
+    const OutPair o = out_pair(c, out_ax, out_bx, ow, c->outb);
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "epilogue ax", [&] {
+      return keyswitch_epilogue(KS, d1, o.a, B, log_n, log_q, log_Q, log_p, c->stream);
+    });
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "epilogue bx", [&] {
+      return keyswitch_epilogue(KS + B * n * L2, d0, o.b, B, log_n, log_q, log_Q, log_p,
+                                c->stream);
+    });
+    copy_out(c, o, out_ax, out_bx, ow);
     return HEMUL_OK;
   });
 }
@@ -595,25 +626,21 @@ hemul_status hemul_gpu_rescale(hemul_gpu_ctx* c, int log_q, size_t batch, const 
   if (log_q - c->log_p < c->log_p)
     return fail(c, HEMUL_E_DEPTH, "modulus exhausted; cannot rescale");
   if (batch == 0) return HEMUL_OK;
+  if (!ax || !bx || !out_ax || !out_bx) return fail(c, HEMUL_E_ARG, "null buffer");
   return guarded(c, [&]() -> hemul_status {
     const size_t n = size_t(c->n);
     const int L = limbs_of(log_q), Lo = limbs_of(log_q - c->log_p);
-    ensure(c->rescale_buf, 2 * batch * n * (L + Lo) * 8);
-    const uint64_t* a = to_device(c, ax, batch * n * L, c->rescale_buf, 0);
-    const uint64_t* b = to_device(c, bx, batch * n * L, c->rescale_buf, batch * n * L);
-    const bool dev_out = is_device(c, out_ax) && is_device(c, out_bx);
-    uint64_t* oa = dev_out ? out_ax : c->rescale_buf.as<uint64_t>() + 2 * batch * n * L;
-    uint64_t* ob = dev_out ? out_bx : oa + batch * n * Lo;
-    check(shift_right(a, oa, batch, c->log_n, log_q, c->log_p, c->stream), "rescale");
-    check(shift_right(b, ob, batch, c->log_n, log_q, c->log_p, c->stream), "rescale");
-    c->launches += 2;
-    if (!dev_out) {
-      check(cudaMemcpyAsync(out_ax, oa, batch * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
-            "D2H");
-      check(cudaMemcpyAsync(out_bx, ob, batch * n * Lo * 8, cudaMemcpyDeviceToHost, c->stream),
-            "D2H");
-    }
-    check(cudaStreamSynchronize(c->stream), "rescale");
+    const size_t w = batch * n * L, ow = batch * n * Lo;
+    ensure(c->rescale_buf, 2 * w * 8);
+    const uint64_t* a = stage_in(c, ax, w, c->rescale_buf.as<uint64_t>());
+    const uint64_t* b = stage_in(c, bx, w, c->rescale_buf.as<uint64_t>() + w);
+    const OutPair o = out_pair(c, out_ax, out_bx, ow, c->outb);
+    for (int t = 0; t < 2; ++t)
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "rescale", [&] {
+        return shift_right(t ? b : a, t ? o.b : o.a, batch, c->log_n, log_q, c->log_p,
+                           c->stream);
+      });
+    copy_out(c, o, out_ax, out_bx, ow);
     return HEMUL_OK;
   });
 }
@@ -644,20 +671,16 @@ hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* da
     if (!dev) {
       ensure(c->r1, words * 8);
       d = c->r1.as<uint64_t>();
-      check(cudaMemcpyAsync(d, data, words * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+      stage_in(c, data, words, d);
     }
-    int launches = 0;
     if (inverse)
-      check(ntt_inverse(d, rows, r.np, c->log_n, r.itw.as<Twiddle>(), r.primes.as<DevPrime>(),
-                        c->stream, &launches),
-            "iNTT");
+      ntt_inv(c, r, d, rows, HEMUL_STAGE_INTT);
     else
-      check(ntt_forward(d, rows, r.np, c->log_n, r.tw.as<Twiddle>(), r.primes.as<DevPrime>(),
-                        c->stream, &launches),
-            "NTT");
-    c->launches += launches;
+      ntt_fwd(c, r, d, rows, HEMUL_STAGE_NTT);
     if (!dev)
-      check(cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDeviceToHost, c->stream);
+      });
     check(cudaStreamSynchronize(c->stream), "ntt");
     return HEMUL_OK;
   });
@@ -674,20 +697,22 @@ hemul_status hemul_gpu_crt(hemul_gpu_ctx* c, int log_q, int region, int in_bits,
     const size_t n = size_t(c->n);
     const int L = limbs_of(in_bits);
     ensure(c->in, batch * n * L * 8);
-    const uint64_t* src = to_device(c, poly, batch * n * L, c->in, 0);
+    const uint64_t* src = stage_in(c, poly, batch * n * L, c->in.as<uint64_t>());
     const bool dev = is_device(c, rns);
     uint64_t* dst = rns;
+    const size_t words = batch * r.np * n;
     if (!dev) {
-      ensure(c->r1, batch * r.np * n * 8);
+      ensure(c->r1, words * 8);
       dst = c->r1.as<uint64_t>();
     }
-    check(crt_forward(src, L, batch, c->log_n, *w, r.primes.as<DevPrime>(), r.np, dst,
-                      c->stream),
-          "CRT");
-    ++c->launches;
+    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT", [&] {
+      return crt_forward(src, L, batch, c->log_n, *w, r.primes.as<DevPrime>(), r.np, dst,
+                         c->stream);
+    });
     if (!dev)
-      check(cudaMemcpyAsync(rns, dst, batch * r.np * n * 8, cudaMemcpyDeviceToHost, c->stream),
-            "D2H");
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(rns, dst, words * 8, cudaMemcpyDeviceToHost, c->stream);
+      });
     check(cudaStreamSynchronize(c->stream), "crt");
     return HEMUL_OK;
   });
@@ -701,14 +726,17 @@ hemul_status hemul_gpu_pointwise(hemul_gpu_ctx* c, int log_q, int region, size_t
     const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
     const size_t words = batch * r.np * size_t(c->n);
     ensure(c->r1, 3 * words * 8);
-    const uint64_t* da = to_device(c, a, words, c->r1, 0);
-    const uint64_t* db = to_device(c, b, words, c->r1, words);
+    const uint64_t* da = stage_in(c, a, words, c->r1.as<uint64_t>());
+    const uint64_t* db = stage_in(c, b, words, c->r1.as<uint64_t>() + words);
     const bool dev = is_device(c, out);
     uint64_t* d = dev ? out : c->r1.as<uint64_t>() + 2 * words;
-    check(pointwise(da, db, d, batch, r.np, c->log_n, r.primes.as<DevPrime>(), c->stream),
-          "pointwise");
-    ++c->launches;
-    if (!dev) check(cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "pointwise", [&] {
+      return pointwise(da, db, d, batch, r.np, c->log_n, r.primes.as<DevPrime>(), c->stream);
+    });
+    if (!dev)
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDeviceToHost, c->stream);
+      });
     check(cudaStreamSynchronize(c->stream), "pointwise");
     return HEMUL_OK;
   });
@@ -724,7 +752,7 @@ hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batc
     const size_t words = batch * r.np * n;
     const int TL = limbs_of(r.target_bits);
     ensure(c->r1, words * 8);
-    const uint64_t* src = to_device(c, rns, words, c->r1, 0);
+    const uint64_t* src = stage_in(c, rns, words, c->r1.as<uint64_t>());
     const bool dev = is_device(c, poly);
     uint64_t* dst = poly;
     if (!dev) {
@@ -737,13 +765,15 @@ hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batc
     ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
     flags.count = c->flagbuf.as<unsigned>();
     flags.ids = flags.count + 1;
-    check(icrt(src, batch, c->log_n, r.primes.as<DevPrime>(), r.np, r.icrt, dst, c->stream,
-               &flags),
-          "iCRT");
-    c->launches += 2;
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT", [&] {
+      return icrt(src, batch, c->log_n, r.primes.as<DevPrime>(), r.np, r.icrt, dst, c->stream,
+                  &flags);
+    });
+    ++c->launches;  // the fix-up kernel
     if (!dev)
-      check(cudaMemcpyAsync(poly, dst, batch * n * TL * 8, cudaMemcpyDeviceToHost, c->stream),
-            "D2H");
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(poly, dst, batch * n * TL * 8, cudaMemcpyDeviceToHost, c->stream);
+      });
     check(cudaStreamSynchronize(c->stream), "icrt");
     return HEMUL_OK;
   });

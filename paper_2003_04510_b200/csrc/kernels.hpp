@@ -16,6 +16,19 @@ cudaError_t ntt_forward(uint64_t* data, size_t rows, int np, int log_n, const Tw
                         const DevPrime* primes, cudaStream_t st, int* launches);
 cudaError_t ntt_inverse(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* itw,
                         const DevPrime* primes, cudaStream_t st, int* launches);
+// The same transforms one memory pass at a time (for per-kernel timing):
+// forward pass 0 = levels [0, s1) on columns, pass 1 = levels [s1, logN) on
+// blocks; inverse pass 0 = levels [s1, logN), pass 1 = levels [0, s1) + n^-1.
+int ntt_num_passes(int log_n);
+cudaError_t ntt_forward_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
+                             const Twiddle* tw, const DevPrime* primes, cudaStream_t st);
+cudaError_t ntt_inverse_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
+                             const Twiddle* itw, const DevPrime* primes, cudaStream_t st);
+
+// ---- integer-pipe peak probe (probe.cu) ------------------------------------
+// Measured IMAD.WIDE.U32 throughput of this device in ops/s (a dependent-free
+// stream of mad.wide.u32, 148 x 8 CTAs), and the SM clock it ran at (kHz).
+cudaError_t imad_peak(double* ops_per_s, cudaStream_t st);
 
 // ---- CRT (crt.cu) ----------------------------------------------------------
 // Weight table for one (prime set, input width): wtab[m * 2 * np_pad + 2 j + h]

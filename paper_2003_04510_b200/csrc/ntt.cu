@@ -254,29 +254,47 @@ cudaError_t ntt_setup_attributes() {
                               64 * 1024);
 }
 
-cudaError_t ntt_forward(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* tw,
-                        const DevPrime* primes, cudaStream_t st, int* launches) {
+int ntt_num_passes(int log_n) {
   int s1, s2;
   split_levels(log_n, s1, s2);
-  cudaError_t e = launch_pass(false, data, tw, primes, np, rows, log_n, 0, s1, true, s2 == 0, st);
-  ++*launches;
-  if (e != cudaSuccess || s2 == 0) return e;
-  ++*launches;
+  return s2 == 0 ? 1 : 2;
+}
+
+cudaError_t ntt_forward_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
+                             const Twiddle* tw, const DevPrime* primes, cudaStream_t st) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  if (pass == 0) return launch_pass(false, data, tw, primes, np, rows, log_n, 0, s1, true, s2 == 0, st);
   return launch_pass(false, data, tw, primes, np, rows, log_n, s1, s2, false, true, st);
+}
+
+cudaError_t ntt_inverse_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
+                             const Twiddle* itw, const DevPrime* primes, cudaStream_t st) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  if (pass == 0 && s2 > 0)
+    return launch_pass(true, data, itw, primes, np, rows, log_n, s1, s2, false, false, st);
+  return launch_pass(true, data, itw, primes, np, rows, log_n, 0, s1, true, true, st);
+}
+
+cudaError_t ntt_forward(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* tw,
+                        const DevPrime* primes, cudaStream_t st, int* launches) {
+  for (int pass = 0; pass < ntt_num_passes(log_n); ++pass) {
+    cudaError_t e = ntt_forward_pass(pass, data, rows, np, log_n, tw, primes, st);
+    ++*launches;
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t ntt_inverse(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* itw,
                         const DevPrime* primes, cudaStream_t st, int* launches) {
-  int s1, s2;
-  split_levels(log_n, s1, s2);
-  cudaError_t e;
-  if (s2 > 0) {
-    e = launch_pass(true, data, itw, primes, np, rows, log_n, s1, s2, false, false, st);
+  for (int pass = 0; pass < ntt_num_passes(log_n); ++pass) {
+    cudaError_t e = ntt_inverse_pass(pass, data, rows, np, log_n, itw, primes, st);
     ++*launches;
     if (e != cudaSuccess) return e;
   }
-  ++*launches;
-  return launch_pass(true, data, itw, primes, np, rows, log_n, 0, s1, true, true, st);
+  return cudaSuccess;
 }
 
 }  // namespace hemul_gpu

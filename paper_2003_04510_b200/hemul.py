@@ -41,6 +41,8 @@ HEMUL_E_OOM = 5
 HEMUL_E_NO_EVK = 6
 
 STAGES = ("crt", "ntt", "intt", "icrt", "extra")  # counters.hpp:13
+KERNEL_CLASSES = ("crt", "ntt_a", "ntt_b", "intt_b", "intt_a", "tensor", "evk", "icrt",
+                  "epilogue", "h2d", "d2h")  # HEMUL_KCLASS_* in include/hemul_gpu.h
 
 
 class HemulGpuError(RuntimeError):
@@ -81,6 +83,11 @@ _SIGS = {
     "hemul_gpu_launch_count": (ctypes.c_uint64, [ctypes.c_void_p]),
     "hemul_gpu_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
     "hemul_ciphertext_digest": (ctypes.c_uint64, [ctypes.c_int, ctypes.c_size_t, _u64p, _u64p]),
+    "hemul_gpu_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "hemul_gpu_kernel_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(ctypes.c_uint64)]),
+    "hemul_gpu_reset_stats": (ctypes.c_int, [ctypes.c_void_p]),
+    "hemul_gpu_imad_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
 }
 
 
@@ -305,6 +312,27 @@ class Context:
         buf = (ctypes.c_double * 5)()
         self._check(self._lib.hemul_gpu_stage_ms(self._h, buf))
         return dict(zip(STAGES, list(buf)))
+
+    def kernel_stats(self) -> dict[str, tuple[float, int]]:
+        """Cumulative (ms, launches) per kernel class since reset_stats()."""
+        k = len(KERNEL_CLASSES)
+        ms = (ctypes.c_double * k)()
+        n = (ctypes.c_uint64 * k)()
+        self._check(self._lib.hemul_gpu_kernel_stats(self._h, ms, n))
+        return {name: (ms[i], int(n[i])) for i, name in enumerate(KERNEL_CLASSES)}
+
+    def reset_stats(self) -> None:
+        self._check(self._lib.hemul_gpu_reset_stats(self._h))
+
+    def set_stream(self, stream: int | None) -> None:
+        """Launch on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(self._lib.hemul_gpu_set_stream(self._h, stream))
+
+    def imad_peak(self) -> float:
+        """Measured IMAD.WIDE.U32 ops/s of this device."""
+        v = ctypes.c_double()
+        self._check(self._lib.hemul_gpu_imad_peak(self._h, ctypes.byref(v)))
+        return v.value
 
     def launch_count(self) -> int:
         return int(self._lib.hemul_gpu_launch_count(self._h))

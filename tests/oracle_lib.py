@@ -133,6 +133,7 @@ class Reference:
         L.ref_finish.argtypes = [_i, _i, _i, _i, _p, _p, _i]
         L.ref_pointwise.argtypes = [_i, _i, _i, _i, _p, _p, _p]
         L.ref_shift_right.argtypes = [_i, _i, _i, _p, _p]
+        L.ref_time_he_mul.argtypes = [_i, _i, _i, _u64, _i, _i, _i, _p, _p]
 
     def err(self):
         return self.lib.ref_last_error().decode()
@@ -185,6 +186,16 @@ class Reference:
 
     def digest(self, log_q, n, ax, bx):
         return int(self.lib.ref_digest(log_q, n, _ptr(ax), _ptr(bx)))
+
+    def time_he_mul(self, log_p, depth, log_n_override=0, seed=1, reps=1, threads=1,
+                    radix_log=1):
+        """Wall ms of `reps` warm he_mul calls on random inputs (+ digest)."""
+        ms = np.zeros(reps, np.float64)
+        dig = np.zeros(1, np.uint64)
+        st = self.lib.ref_time_he_mul(log_p, depth, log_n_override, seed, reps, threads,
+                                      radix_log, ms.ctypes.data, dig.ctypes.data)
+        assert st == 0, self.err()
+        return ms.tolist(), int(dig[0])
 
     def prepare(self, region, log_q, log_q_max, log_n, in_bits, poly, np_, stop_after_crt=False):
         out = np.zeros((np_, 1 << log_n), np.uint64)
