@@ -111,6 +111,13 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx *ctx, int c1_log_q, int c2_log_q, si
 hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, const uint64_t *ax,
                                const uint64_t *bx, uint64_t *out_ax, uint64_t *out_bx);
 
+/* Options. HEMUL_OPT_FORCE_EXACT = 1 routes every output coefficient of
+ * he_mul through the exact big-integer fix-up kernel that normally only
+ * handles the (probability 2^-64) coefficients whose truncated ModDown window
+ * is ambiguous — a test knob for that path; results are identical. */
+enum { HEMUL_OPT_FORCE_EXACT = 1 };
+hemul_status hemul_gpu_set_option(hemul_gpu_ctx *ctx, int option, int value);
+
 /* Device timing. When enabled every launch is bracketed by CUDA events on the
  * context stream (read back lazily, so no extra host sync per call).
  * stage_ms: per-stage milliseconds of the last he_mul call, buckets as

@@ -77,7 +77,9 @@ struct Level {
   RegionDev r1, r2;
   bool has_evk = false;
   uint64_t evk_id = 0;
-  DevBuf evk_a, evk_b;  // np2 x n NTT forms
+  DevBuf evk_a;  // 2 x np2 x n NTT forms (ax then bx)
+  DevBuf fin_btab;
+  Finisher fin;  // fused ModDown + add + rescale table (he_mul levels only)
 };
 
 struct CudaFail : std::runtime_error {
@@ -124,6 +126,7 @@ struct hemul_gpu_ctx {
   std::vector<cudaEvent_t> event_pool;
   // scratch
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
+  int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
 
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
@@ -260,6 +263,24 @@ Level& get_level(hemul_gpu_ctx* c, int log_q) {
   RegionHost h2 = build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th);
   fill_region(lv->r1, h1, c->log_n, c->stream);
   fill_region(lv->r2, h2, c->log_n, c->stream);
+  if (log_q - c->log_p >= c->log_p) {  // a level he_mul can run at
+    const FinisherHost fh = build_finisher(h1, h2, log_q, c->log_q_max, c->log_p);
+    upload(lv->fin_btab, fh.btab, c->stream);
+    Finisher& f = lv->fin;
+    f.btab = lv->fin_btab.as<uint32_t>();
+    f.cols = fh.cols;
+    f.cols_pad = fh.cols_pad;
+    f.k2 = fh.k2;
+    f.k1 = fh.k1;
+    f.base = fh.base;
+    f.half_q_bit = fh.half_q_bit;
+    f.half_p_bit = fh.half_p_bit;
+    f.out_bit = fh.out_bit;
+    f.out_bits = fh.out_bits;
+    f.log_q = log_q;
+    f.log_Q = c->log_q_max;
+    f.log_p = c->log_p;
+  }
   check(cudaStreamSynchronize(c->stream), "level upload");
   c->cache.push_front(std::move(lv));
   while (c->cache.size() > 2) c->cache.pop_back();
@@ -464,6 +485,17 @@ hemul_status hemul_gpu_level_info(hemul_gpu_ctx* c, int log_q, int region, int* 
   });
 }
 
+hemul_status hemul_gpu_set_option(hemul_gpu_ctx* c, int option, int value) {
+  if (!c) return HEMUL_E_ARG;
+  switch (option) {
+    case HEMUL_OPT_FORCE_EXACT:
+      c->force_exact = value != 0;
+      return HEMUL_OK;
+    default:
+      return fail(c, HEMUL_E_ARG, "unknown option");
+  }
+}
+
 hemul_status hemul_gpu_enable_stage_timing(hemul_gpu_ctx* c, int on) {
   if (!c) return HEMUL_E_ARG;
   c->timing = on != 0;
@@ -578,14 +610,12 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
       return tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
     });
     ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
-    // d polys: [d2 | d0 | d1], each B x n x L
-    ensure(c->dpoly, 3 * B * poly_w * 8);
-    uint64_t* D = c->dpoly.as<uint64_t>();
-    uint64_t* d2 = D;
-    uint64_t* d0 = D + B * poly_w;
-    uint64_t* d1 = D + 2 * B * poly_w;
+    // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
+    // and are reconstructed inside the finisher
+    ensure(c->dpoly, B * poly_w * 8);
+    uint64_t* d2 = c->dpoly.as<uint64_t>();
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1",
-        [&] { return icrt(R1, 3 * B, log_n, p1, r1.np, r1.icrt, D, c->stream); });
+        [&] { return icrt(A1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream); });
     // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
     const size_t r2w = B * r2.np * n;
     ensure(c->r2, 2 * r2w * 8);
@@ -600,20 +630,21 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
         [&] { return evk_product(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
     ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
-    ensure(c->ks, 2 * B * n * L2 * 8);
-    uint64_t* KS = c->ks.as<uint64_t>();
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r2",
-        [&] { return icrt(KA, 2 * B, log_n, p2, r2.np, r2.icrt, KS, c->stream); });
-    // ---- epilogue: R_logp(d + R_logQ(ks)) ------------------------------------
+    // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
+    // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
     const size_t ow = B * n * Lo;
     const OutPair o = out_pair(c, out_ax, out_bx, ow, c->outb);
-    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "epilogue ax", [&] {
-      return keyswitch_epilogue(KS, d1, o.a, B, log_n, log_q, log_Q, log_p, c->stream);
+    IcrtFlags flags;
+    flags.capacity = static_cast<unsigned>(2 * B * n);
+    ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
+    flags.count = c->flagbuf.as<unsigned>();
+    flags.ids = flags.count + 1;
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "finisher", [&] {
+      return finish_keyswitch(KA, A2 /* d1 */, B1 /* d0 */, B, log_n, p2, r2.np, p1, r1.np,
+                              lv.fin, r2.icrt, r1.icrt, o.a, o.b, flags, c->force_exact,
+                              c->stream);
     });
-    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "epilogue bx", [&] {
-      return keyswitch_epilogue(KS + B * n * L2, d0, o.b, B, log_n, log_q, log_Q, log_p,
-                                c->stream);
-    });
+    ++c->launches;  // the (normally empty) exact fix-up kernel
     copy_out(c, o, out_ax, out_bx, ow);
     return HEMUL_OK;
   });

@@ -133,7 +133,7 @@ size_t crt_smem(int limbs, int M) {
 
 cudaError_t crt_setup_attributes() {
   return cudaFuncSetAttribute(crt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+                              kMaxDynSmem);
 }
 
 cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n,

@@ -1,24 +1,26 @@
-// Exact inverse CRT: prime-major residues -> coefficients mod 2^T (sm_100a).
+// Exact inverse CRT and the fused key-switch finisher (sm_100a).
 //
-// Reference: icrt_reordered (proj/core/src/rns.cpp:132-190, 235-290, 395-415):
-//   t_j = x_j (P/p_j)^-1 mod p_j ; acc = sum_j t_j (P/p_j) ; fold below P ;
-//   centered lift (acc > floor(P/2) -> acc - P) ; reduce mod the target 2^T.
+// Reference: icrt_reordered (proj/core/src/rns.cpp:132-190, 235-290,
+// 395-415):  t_j = x_j (P/p_j)^-1 mod p_j ; acc = sum_j t_j (P/p_j) ; fold
+// below P ; centered lift (acc > floor(P/2) -> acc - P) ; reduce mod 2^T.
 //
 // B200 form (bit-identical):
-//   v = sum_j t_j H_j - k P with k = rint(sum_j t_j / p_j) computed in fp64.
-// sum_j t_j / p_j = k + v/P and the centered v satisfies |v|/P < 1/2 - 2^-s
-// (s = the level's slack, >= 4 bits is asserted at level setup), so fp64's
-// ~2^-45 error can never move the rounding. Then
-//   out = sum_j t_j (H_j mod 2^T) + k ((-P) mod 2^T)   mod 2^T,
-// so the MAC width is ceil(T/30) chunks instead of the limbs of P (40->80
-// chunks of 30 bits at region 1, N=2^16).
-// The accumulation is a small-K integer GEMM S[i][m] = sum_k A[k][i] B[k][m]
-// with A = {t_j low 30 bits, t_j high 30 bits, k} and B = {H_j chunks, H_j
-// chunks shifted one chunk up, (-P) chunks}; every product is one
-// IMAD.WIDE.U32 < 2^60, folded into 128 bits every 16 rows. A final carry
-// pass turns the 30-bit column sums into 64-bit limbs.
+//   v = sum_j t_j H_j - k P,  k = rint(sum_j t_j / p_j)  (fp64)
+// sum_j t_j / p_j = k + v/P with the centered |v|/P < 1/2 - 2^-s (s >= 4 is
+// asserted at level setup for every he_mul product), so fp64's ~2^-45 error
+// cannot move the rounding, and
+//   out = sum_j t_j (H_j mod 2^T) + k ((-P) mod 2^T)   mod 2^T.
+// With t_j = lo + 2^30 hi the sum is a small-K integer GEMM (igemm.cuh) of
+// A = {t_j lo, t_j hi, k} (30-bit) against B = 25-bit chunks of
+// {H_j, H_j 2^30, -P} mod 2^T, followed by one carry pass per coefficient.
+// Residues whose quotient is ambiguous (|v| >= P/4 — only arbitrary inputs
+// to the stage API) are flagged and recomputed exactly by the reference's
+// own big-integer algorithm in a fix-up kernel.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
+#include "igemm.cuh"
 #include "kernels.hpp"
 #include "modarith.cuh"
 
@@ -26,233 +28,402 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kCoefs = 32;   // coefficients per CTA
-constexpr int kKt = 16;      // B rows per shared-memory tile
+constexpr int kKT = 32;      // B rows per cp.async stage
+constexpr int kStages = 3;
+constexpr int kDigit = 25;   // B chunk width == output digit width
+constexpr uint32_t kDigitMask = (1u << kDigit) - 1;
+constexpr int kFixMaxLimbs = 136;
 
-// A CTA: 32 coefficients x m_pad chunks; lane -> (coef group = lane % 8,
-// chunk group = lane / 8 + 4 * warp); thread tile 4 coefs x 4 chunks.
-__global__ void __launch_bounds__(512) icrt_kernel(const uint64_t* __restrict__ rns,
-                                                  int log_n, const DevPrime* __restrict__ primes,
-                                                  int np, const uint32_t* __restrict__ btab,
-                                                  int m_out, int m_pad, int tbits,
-                                                  uint64_t* __restrict__ out, IcrtFlags flags) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const size_t n = size_t(1) << log_n;
-  const int b = blockIdx.y;
-  const size_t c0 = size_t(blockIdx.x) * kCoefs;
-  const int K = 2 * np + 1;
-  uint32_t* A = reinterpret_cast<uint32_t*>(smem);    // [K][kCoefs]
-  uint32_t* Bt = A + size_t(K) * kCoefs;              // [kKt][m_pad]
-  // ---- t_j = x_j * inv_j mod p_j, split in 30-bit halves ------------------
-  for (int idx = threadIdx.x; idx < np * kCoefs; idx += blockDim.x) {
-    const int j = idx / kCoefs, c = idx % kCoefs;
-    const DevPrime& pr = primes[j];
-    const uint64_t x = rns[(size_t(b) * np + j) * n + c0 + c];
+struct Seg {  // one RNS operand feeding A rows
+  const uint64_t* rns;  // [np][n] of this batch entry
+  const DevPrime* primes;
+  int np;
+};
+
+// A rows [row0, row0 + 2np + 1) for the CTA's 32 coefficients: the 30-bit
+// halves of t_j and the quotient k (warp w handles primes w, w+NW, ...; lane
+// = coefficient, so every x_j load is a coalesced 256-byte row segment).
+__device__ void build_rows(const Seg& s, size_t n, size_t c0, uint32_t* A, int row0,
+                           double* part, IcrtFlags flags, size_t id0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double acc = 0;
+  for (int j = warp; j < s.np; j += nw) {
+    const DevPrime& pr = s.primes[j];
+    const uint64_t x = s.rns[size_t(j) * n + c0 + lane];
     const uint64_t t = shoup_mul(x, pr.inv, pr.inv_q, pr.p);
-    A[(2 * j) * kCoefs + c] = static_cast<uint32_t>(t) & 0x3fffffffu;
-    A[(2 * j + 1) * kCoefs + c] = static_cast<uint32_t>(t >> 30);
+    A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
+    A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
+    acc += static_cast<double>(t) * pr.inv_p_dbl;
+  }
+  part[warp * 32 + lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double tot = 0;
+    for (int w = 0; w < nw; ++w) tot += part[w * 32 + lane];
+    const double k = rint(tot);
+    A[(row0 + 2 * s.np) * kGemmCoefs + lane] = static_cast<uint32_t>(k);
+    if (flags.count && fabs(tot - k) > 0.25) {
+      const unsigned slot = atomicAdd(flags.count, 1u);
+      if (slot < flags.capacity) flags.ids[slot] = static_cast<unsigned>(id0 + lane);
+    }
   }
   __syncthreads();
-  // ---- k = rint(sum_j t_j / p_j) ------------------------------------------
-  if (threadIdx.x < kCoefs) {
-    const int c = threadIdx.x;
-    double s = 0;
-    for (int j = 0; j < np; ++j) {
-      const uint64_t t = uint64_t(A[(2 * j) * kCoefs + c]) |
-                         (uint64_t(A[(2 * j + 1) * kCoefs + c]) << 30);
-      s += static_cast<double>(t) * primes[j].inv_p_dbl;
-    }
-    const double k = rint(s);
-    A[(2 * np) * kCoefs + c] = static_cast<uint32_t>(k);
-    if (flags.count && fabs(s - k) > 0.25) {
-      const unsigned slot = atomicAdd(flags.count, 1u);
-      if (slot < flags.capacity) flags.ids[slot] = unsigned(size_t(b) * n + c0 + c);
-    }
-  }
+}
+
+// Column sums of a GEMM tile -> S[c][col] (u64), columns < limit only.
+template <int NW>
+__device__ __forceinline__ void store_tile(uint64_t* S, int ld, int col0, int limit,
+                                           const uint64_t (&acc)[4][4]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cg = lane & 7;                        // coefficient group (4 coefs)
-  const int mg = (lane >> 3) + 4 * warp;          // chunk group (4 chunks)
-  const bool active = 4 * mg < m_pad;
-  uint64_t lo[4][4], hi[4][4];
+  const int cg = lane & 7, ng = lane >> 3;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) lo[i][q] = hi[i][q] = 0;
-  for (int kb = 0; kb < K; kb += kKt) {
-    const int ke = min(kb + kKt, K);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (ke - kb) * m_pad; idx += blockDim.x)
-      Bt[idx] = btab[size_t(kb) * m_pad + idx];
-    __syncthreads();
-    if (active) {
-      uint64_t acc[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[i][q] = 0;
-      for (int k = kb; k < ke; ++k) {
-        const uint4 a = *reinterpret_cast<const uint4*>(A + size_t(k) * kCoefs + 4 * cg);
-        const uint4 w = *reinterpret_cast<const uint4*>(Bt + size_t(k - kb) * m_pad + 4 * mg);
-        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[i][q] += wide(av[i], wv[q]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint64_t s = lo[i][q] + acc[i][q];
-          hi[i][q] += s < acc[i][q];
-          lo[i][q] = s;
-        }
+    for (int q = 0; q < 4; ++q) {
+      const int col = col0 + 16 * warp + 4 * ng + q;
+      if (col < limit) S[(4 * cg + i) * ld + col] = acc[i][q];
     }
-  }
-  __syncthreads();
-  // ---- column sums to shared memory, then a carry pass per coefficient ----
-  uint64_t* Slo = reinterpret_cast<uint64_t*>(smem);            // [kCoefs][m_pad]
-  uint32_t* Shi = reinterpret_cast<uint32_t*>(Slo + size_t(kCoefs) * m_pad);
-  if (active) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 4 * cg + i, m = 4 * mg + q;
-        Slo[size_t(c) * m_pad + m] = lo[i][q];
-        Shi[size_t(c) * m_pad + m] = static_cast<uint32_t>(hi[i][q]);
-      }
-  }
-  __syncthreads();
-  const int tl = (tbits + 63) / 64;
-  uint64_t* packed = reinterpret_cast<uint64_t*>(Shi + size_t(kCoefs) * m_pad);  // [kCoefs][tl]
-  if (threadIdx.x < kCoefs) {
-    const int c = threadIdx.x;
-    // carry = (chi:clo), 30-bit digit emitted each step, packed into limbs
-    uint64_t clo = 0, chi = 0, word = 0;
-    int fill = 0, limb = 0;
-    for (int m = 0; m < m_out; ++m) {
-      const uint64_t slo = Slo[size_t(c) * m_pad + m];
-      const uint64_t shi = Shi[size_t(c) * m_pad + m];
-      const uint64_t vlo = slo + clo;
-      const uint64_t vhi = shi + chi + (vlo < slo);
-      const uint64_t digit = vlo & 0x3fffffffu;
-      clo = (vlo >> 30) | (vhi << 34);
-      chi = vhi >> 30;
-      word |= digit << fill;
-      fill += 30;
-      if (fill >= 64) {
-        if (limb < tl) packed[size_t(c) * tl + limb] = word;
-        ++limb;
-        fill -= 64;
-        word = fill > 0 ? digit >> (30 - fill) : 0;
-      }
-    }
-    if (fill > 0 && limb < tl) packed[size_t(c) * tl + limb++] = word;
-    while (limb < tl) packed[size_t(c) * tl + limb++] = 0;
-    if (tbits % 64) packed[size_t(c) * tl + tl - 1] &= (uint64_t(1) << (tbits % 64)) - 1;
-  }
-  __syncthreads();
-  uint64_t* dst = out + (size_t(b) * n + c0) * tl;
-  for (int idx = threadIdx.x; idx < kCoefs * tl; idx += blockDim.x) dst[idx] = packed[idx];
 }
 
-// Exact reconstruction of the flagged coefficients, the reference's own
-// algorithm (rns.cpp:148-169, 192-233): acc = sum_j t_j H_j, fold below P,
-// centered lift, mod 2^T. One thread per flagged coefficient.
-constexpr int kFixMaxLimbs = 136;
+// bits [bit, bit + 64) of the digit string D (25-bit digits, ndig of them)
+__device__ __forceinline__ uint64_t digits_window(const uint32_t* D, int ndig, int bit) {
+  int m = bit / kDigit;
+  int pos = m * kDigit - bit;  // bit position in r where digit m starts (<= 0)
+  uint64_t r = 0;
+  for (; pos < 64 && m < ndig; ++m, pos += kDigit) {
+    const uint64_t d = D[m];
+    r |= pos >= 0 ? d << pos : d >> (-pos);
+  }
+  return r;
+}
+
+// One carry pass over a coefficient's column sums -> 25-bit digits, adding
+// 2^add0 and 2^add1 (the rounding halves; -1 = none) on the way.
+__device__ __forceinline__ void carry_pass(const uint64_t* S, uint32_t* D, int cols, int add0,
+                                           int add1) {
+  uint64_t carry = 0;
+  for (int m = 0; m < cols; ++m) {
+    uint64_t v = S[m] + carry;
+    if (add0 >= 0 && m == add0 / kDigit) v += uint64_t(1) << (add0 % kDigit);
+    if (add1 >= 0 && m == add1 / kDigit) v += uint64_t(1) << (add1 % kDigit);
+    D[m] = static_cast<uint32_t>(v) & kDigitMask;
+    carry = v >> kDigit;
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restrict__ rns,
+                                                       int log_n,
+                                                       const DevPrime* __restrict__ primes,
+                                                       int np, IcrtTable t,
+                                                       uint64_t* __restrict__ out,
+                                                       IcrtFlags flags) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const size_t n = size_t(1) << log_n;
+  const int b = blockIdx.y;
+  const size_t c0 = size_t(blockIdx.x) * kGemmCoefs;
+  const int K = 2 * np + 1;
+  constexpr int NC = 16 * NW;
+  uint32_t* A = reinterpret_cast<uint32_t*>(smem);                     // [K][32]
+  uint32_t* Bs = A + K * kGemmCoefs;                                   // cp.async ring
+  double* part = reinterpret_cast<double*>(Bs + kStages * kKT * NC);  // [NW][32]
+  uint64_t* S = reinterpret_cast<uint64_t*>(part + NW * 32);          // [32][m_pad]
+  uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * t.m_pad);  // [32][m_out]
+  const Seg seg{rns + size_t(b) * np * n, primes, np};
+  build_rows(seg, n, c0, A, 0, part, flags, size_t(b) * n + c0);
+  for (int col0 = 0; col0 < t.m_pad; col0 += NC) {
+    uint64_t acc[4][4] = {};
+    igemm_32xN<NW, kKT, kStages>(A, K, t.btab, t.m_pad, col0, Bs, acc);
+    store_tile<NW>(S, t.m_pad, col0, t.m_pad, acc);
+  }
+  __syncthreads();
+  if (threadIdx.x < kGemmCoefs)
+    carry_pass(S + threadIdx.x * t.m_pad, D + threadIdx.x * t.m_out, t.m_out, -1, -1);
+  __syncthreads();
+  const int tl = (t.target_bits + 63) / 64;
+  const uint64_t top = t.target_bits % 64 ? (uint64_t(1) << (t.target_bits % 64)) - 1 : ~0ull;
+  uint64_t* dst = out + (size_t(b) * n + c0) * tl;
+  for (int idx = threadIdx.x; idx < kGemmCoefs * tl; idx += blockDim.x) {
+    const int c = idx / tl, k = idx - c * tl;
+    uint64_t v = digits_window(D + c * t.m_out, t.m_out, 64 * k);
+    if (k == tl - 1) v &= top;
+    dst[idx] = v;
+  }
+}
+
+// Exact centered value mod 2^tbits (rns.cpp:148-169, 192-233), one thread.
+__device__ void exact_centered(const uint64_t* rns_b, size_t n, size_t i,
+                               const DevPrime* primes, int np, const IcrtTable& t, int tbits,
+                               uint64_t* o /* ceil(tbits/64) limbs */) {
+  const int pl = t.p_limbs, al = pl + 2;
+  uint64_t acc[kFixMaxLimbs];
+  for (int k = 0; k < al; ++k) acc[k] = 0;
+  for (int j = 0; j < np; ++j) {
+    const DevPrime& pr = primes[j];
+    const uint64_t tj = shoup_mul(rns_b[size_t(j) * n + i], pr.inv, pr.inv_q, pr.p);
+    const uint64_t* h = t.hat + size_t(j) * pl;
+    uint64_t carry = 0;
+    for (int k = 0; k < al; ++k) {
+      const uint64_t hk = k < pl ? h[k] : 0;
+      const uint64_t lo = tj * hk, hi = __umul64hi(tj, hk);
+      const uint64_t s1 = acc[k] + lo;
+      const uint64_t c1 = s1 < lo;
+      const uint64_t s2 = s1 + carry;
+      carry = hi + c1 + (s2 < s1);
+      acc[k] = s2;
+    }
+  }
+  auto cmp = [&](const uint64_t* x) {  // sign(acc - x)
+    for (int k = al - 1; k >= 0; --k) {
+      const uint64_t xk = k < pl ? x[k] : 0;
+      if (acc[k] != xk) return acc[k] > xk ? 1 : -1;
+    }
+    return 0;
+  };
+  while (cmp(t.big_p) >= 0) {
+    uint64_t borrow = 0;
+    for (int k = 0; k < al; ++k) {
+      const uint64_t xk = (k < pl ? t.big_p[k] : 0) + borrow;
+      const uint64_t nb = (xk < borrow) | (acc[k] < xk);
+      acc[k] -= xk;
+      borrow = nb;
+    }
+  }
+  const bool neg = cmp(t.half_p) > 0;  // acc > floor(P/2)
+  const int tl = (tbits + 63) / 64;
+  uint64_t borrow = 0;
+  for (int k = 0; k < tl; ++k) {
+    const uint64_t a = k < al ? acc[k] : 0;
+    if (neg) {
+      const uint64_t xk = (k < pl ? t.big_p[k] : 0) + borrow;
+      const uint64_t nb = (xk < borrow) | (a < xk);
+      o[k] = a - xk;
+      borrow = nb;
+    } else {
+      o[k] = a;
+    }
+  }
+  if (tbits % 64) o[tl - 1] &= (uint64_t(1) << (tbits % 64)) - 1;
+}
+
 __global__ void icrt_fixup_kernel(const uint64_t* __restrict__ rns, int log_n,
-                                  const DevPrime* __restrict__ primes, int np,
-                                  const uint64_t* __restrict__ hat, const uint64_t* __restrict__ P,
-                                  const uint64_t* __restrict__ halfP, int pl, int tbits,
+                                  const DevPrime* __restrict__ primes, int np, IcrtTable t,
                                   uint64_t* __restrict__ out, IcrtFlags flags) {
   const unsigned cnt = min(*flags.count, flags.capacity);
   const size_t n = size_t(1) << log_n;
-  const int tl = (tbits + 63) / 64;
-  const int al = pl + 2;
+  const int tl = (t.target_bits + 63) / 64;
   for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < cnt; f += gridDim.x * blockDim.x) {
     const size_t id = flags.ids[f];
     const size_t b = id / n, i = id % n;
-    uint64_t acc[kFixMaxLimbs];
-    for (int k = 0; k < al; ++k) acc[k] = 0;
-    for (int j = 0; j < np; ++j) {
-      const DevPrime& pr = primes[j];
-      const uint64_t t = shoup_mul(rns[(b * np + j) * n + i], pr.inv, pr.inv_q, pr.p);
-      const uint64_t* h = hat + size_t(j) * pl;
-      uint64_t carry = 0;
-      for (int k = 0; k < al; ++k) {
-        const uint64_t hk = k < pl ? h[k] : 0;
-        const uint64_t lo = t * hk, hi = __umul64hi(t, hk);
-        const uint64_t s1 = acc[k] + lo;
-        const uint64_t c1 = s1 < lo;
-        const uint64_t s2 = s1 + carry;
-        carry = hi + c1 + (s2 < s1);
-        acc[k] = s2;
-      }
-    }
-    auto geq = [&](const uint64_t* x) {  // acc >= x (x has pl limbs)
-      for (int k = al - 1; k >= 0; --k) {
-        const uint64_t xk = k < pl ? x[k] : 0;
-        if (acc[k] != xk) return acc[k] > xk;
-      }
-      return true;
-    };
-    while (geq(P)) {
-      uint64_t borrow = 0;
-      for (int k = 0; k < al; ++k) {
-        const uint64_t xk = (k < pl ? P[k] : 0) + borrow;
-        const uint64_t nb = (xk < borrow) | (acc[k] < xk);
-        acc[k] -= xk;
-        borrow = nb;
-      }
-    }
-    bool neg = geq(halfP);
-    if (neg) {  // acc > floor(P/2)  <=>  acc >= floor(P/2) + 1; equality impossible for odd P
-      bool eq = true;
-      for (int k = 0; k < al && eq; ++k) eq = acc[k] == (k < pl ? halfP[k] : 0);
-      neg = !eq;
-    }
-    uint64_t* o = out + (b * n + i) * tl;
-    uint64_t borrow = 0;
-    for (int k = 0; k < tl; ++k) {
-      const uint64_t a = k < al ? acc[k] : 0;
-      if (neg) {
-        const uint64_t xk = (k < pl ? P[k] : 0) + borrow;
-        const uint64_t nb = (xk < borrow) | (a < xk);
-        o[k] = a - xk;
-        borrow = nb;
-      } else {
-        o[k] = a;
-      }
-    }
-    if (tbits % 64) o[tl - 1] &= (uint64_t(1) << (tbits % 64)) - 1;
+    exact_centered(rns + b * np * n, n, i, primes, np, t, t.target_bits, out + (b * n + i) * tl);
   }
 }
 
-size_t icrt_smem(int np, int m_pad, int tbits) {
-  const int K = 2 * np + 1;
-  const size_t main = size_t(K) * kCoefs * 4 + size_t(kKt) * m_pad * 4;
-  const int tl = (tbits + 63) / 64;
-  const size_t epi = size_t(kCoefs) * m_pad * 12 + size_t(kCoefs) * tl * 8;
+// ---- fused key-switch finisher ----------------------------------------------
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) finish_kernel(
+    const uint64_t* __restrict__ ks, const uint64_t* __restrict__ d_ax,
+    const uint64_t* __restrict__ d_bx, int B, int log_n, const DevPrime* __restrict__ p2, int np2,
+    const DevPrime* __restrict__ p1, int np1, Finisher f, uint64_t* __restrict__ out_ax,
+    uint64_t* __restrict__ out_bx, IcrtFlags flags, int force_exact) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int flagged[kGemmCoefs];
+  const size_t n = size_t(1) << log_n;
+  const int bb = blockIdx.y;  // [0, B): ax, [B, 2B): bx
+  const bool is_bx = bb >= B;
+  const int b = is_bx ? bb - B : bb;
+  const size_t c0 = size_t(blockIdx.x) * kGemmCoefs;
+  const int K = f.k2 + f.k1;
+  constexpr int NC = 16 * NW;
+  uint32_t* A = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* Bs = A + K * kGemmCoefs;
+  double* part = reinterpret_cast<double*>(Bs + kStages * kKT * NC);
+  const Seg s2{ks + size_t(bb) * np2 * n, p2, np2};
+  const Seg s1{(is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, p1, np1};
+  const IcrtFlags none{};
+  build_rows(s2, n, c0, A, 0, part, none, 0);
+  build_rows(s1, n, c0, A, f.k2, part, none, 0);
+  uint64_t acc[4][4] = {};
+  igemm_32xN<NW, kKT, kStages>(A, K, f.btab, f.cols_pad, 0, Bs, acc);
+  // a single column tile (cols_pad <= 16 NW): S and the digits reuse A
+  uint64_t* S = reinterpret_cast<uint64_t*>(smem);                         // [32][cols_pad]
+  uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * f.cols_pad);  // [32][cols]
+  store_tile<NW>(S, f.cols_pad, 0, f.cols_pad, acc);
+  __syncthreads();
+  if (threadIdx.x < kGemmCoefs) {
+    const int c = threadIdx.x;
+    uint32_t* dc = D + c * f.cols;
+    carry_pass(S + c * f.cols_pad, dc, f.cols, f.half_q_bit, f.half_p_bit);
+    // exact unless the 64 bits below the output are all ones (kernels.hpp)
+    const bool amb = f.base > 0 && digits_window(dc, f.cols, f.out_bit - 64) == ~0ull;
+    if (amb || force_exact) {
+      const unsigned slot = atomicAdd(flags.count, 1u);
+      if (slot < flags.capacity) flags.ids[slot] = static_cast<unsigned>(size_t(bb) * n + c0 + c);
+    }
+    flagged[c] = amb || force_exact;
+  }
+  __syncthreads();
+  const int lo_l = (f.out_bits + 63) / 64;
+  const uint64_t top = f.out_bits % 64 ? (uint64_t(1) << (f.out_bits % 64)) - 1 : ~0ull;
+  uint64_t* dst = (is_bx ? out_bx : out_ax) + (size_t(b) * n + c0) * lo_l;
+  for (int idx = threadIdx.x; idx < kGemmCoefs * lo_l; idx += blockDim.x) {
+    const int c = idx / lo_l, k = idx - c * lo_l;
+    if (flagged[c]) continue;  // written by the fix-up kernel
+    uint64_t v = digits_window(D + c * f.cols, f.cols, f.out_bit + 64 * k);
+    if (k == lo_l - 1) v &= top;
+    dst[idx] = v;
+  }
+}
+
+// s (len limbs) += val * 2^bit, carries propagated, wraps mod 2^(64 len).
+__device__ __forceinline__ void add_shifted(uint64_t* s, int len, int bit, uint64_t val) {
+  const int w = bit / 64, sh = bit % 64;
+  uint64_t add[2] = {val << sh, sh ? val >> (64 - sh) : 0};
+  uint64_t carry = 0;
+  for (int k = w; k < len; ++k) {
+    const uint64_t a = k - w < 2 ? add[k - w] : 0;
+    const uint64_t s1 = s[k] + a;
+    const uint64_t c1 = s1 < a;
+    const uint64_t s2 = s1 + carry;
+    carry = c1 + (s2 < s1);
+    s[k] = s2;
+    if (k - w >= 1 && !carry) break;
+  }
+}
+
+// Exact recomputation of flagged finisher coefficients: X2 and X1 by the
+// reference algorithm, then bits [logQ+logp, logQ+logq) of
+// X2 + 2^(logQ-1) + 2^logQ (X1 + 2^(logp-1)) mod 2^(logq+logQ).
+__global__ void finish_fixup_kernel(const uint64_t* __restrict__ ks,
+                                    const uint64_t* __restrict__ d_ax,
+                                    const uint64_t* __restrict__ d_bx, int B, int log_n,
+                                    const DevPrime* __restrict__ p2, int np2,
+                                    const DevPrime* __restrict__ p1, int np1, Finisher f,
+                                    IcrtTable t2, IcrtTable t1, uint64_t* __restrict__ out_ax,
+                                    uint64_t* __restrict__ out_bx, IcrtFlags flags) {
+  const unsigned cnt = min(*flags.count, flags.capacity);
+  const size_t n = size_t(1) << log_n;
+  const int T2 = f.log_q + f.log_Q;
+  const int l2 = (T2 + 63) / 64, l1 = (f.log_q + 63) / 64;
+  const int lo_l = (f.out_bits + 63) / 64;
+  for (unsigned fi = blockIdx.x * blockDim.x + threadIdx.x; fi < cnt;
+       fi += gridDim.x * blockDim.x) {
+    const size_t id = flags.ids[fi];
+    const int bb = static_cast<int>(id / n);
+    const size_t i = id % n;
+    const bool is_bx = bb >= B;
+    const int b = is_bx ? bb - B : bb;
+    uint64_t x2[kFixMaxLimbs], x1[kFixMaxLimbs];
+    exact_centered(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2);
+    exact_centered((is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, n, i, p1, np1, t1, f.log_q, x1);
+    add_shifted(x2, l2, f.log_Q - 1, 1);
+    add_shifted(x1, l1, f.log_p - 1, 1);
+    for (int k = 0; k < l1; ++k) add_shifted(x2, l2, f.log_Q + 64 * k, x1[k]);
+    if (T2 % 64) x2[l2 - 1] &= (uint64_t(1) << (T2 % 64)) - 1;
+    uint64_t* o = (is_bx ? out_bx : out_ax) + (size_t(b) * n + i) * lo_l;
+    const int ob = f.log_Q + f.log_p;
+    for (int k = 0; k < lo_l; ++k) {
+      const int bit = ob + 64 * k, w = bit / 64, sh = bit % 64;
+      const uint64_t lo = w < l2 ? x2[w] : 0, hi = w + 1 < l2 ? x2[w + 1] : 0;
+      uint64_t v = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+      if (k == lo_l - 1 && f.out_bits % 64) v &= (uint64_t(1) << (f.out_bits % 64)) - 1;
+      o[k] = v;
+    }
+  }
+}
+
+template <int NW>
+size_t icrt_smem(int np, int m_pad) {
+  return size_t(2 * np + 1) * kGemmCoefs * 4 + size_t(kStages) * kKT * 16 * NW * 4 +
+         NW * 32 * 8 + size_t(kGemmCoefs) * m_pad * 12;
+}
+
+template <int NW>
+size_t finish_smem(const Finisher& f) {
+  const size_t main = size_t(f.k2 + f.k1) * kGemmCoefs * 4 +
+                      size_t(kStages) * kKT * 16 * NW * 4 + NW * 32 * 8;
+  const size_t epi = size_t(kGemmCoefs) * f.cols_pad * 8 + size_t(kGemmCoefs) * f.cols * 4;
   return main > epi ? main : epi;
+}
+
+template <int NW>
+cudaError_t launch_icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* primes,
+                        int np, const IcrtTable& t, uint64_t* out, cudaStream_t st,
+                        IcrtFlags f) {
+  const size_t n = size_t(1) << log_n;
+  dim3 grid(static_cast<unsigned>(n / kGemmCoefs), static_cast<unsigned>(batch));
+  icrt_kernel<NW><<<grid, NW * 32, icrt_smem<NW>(np, t.m_pad), st>>>(rns, log_n, primes, np, t,
+                                                                     out, f);
+  return cudaGetLastError();
+}
+
+template <int NW>
+cudaError_t launch_finish(const uint64_t* ks, const uint64_t* d_ax, const uint64_t* d_bx,
+                          size_t B, int log_n, const DevPrime* p2, int np2, const DevPrime* p1,
+                          int np1, const Finisher& f, uint64_t* out_ax, uint64_t* out_bx,
+                          const IcrtFlags& flags, int force_exact, cudaStream_t st) {
+  const size_t n = size_t(1) << log_n;
+  dim3 grid(static_cast<unsigned>(n / kGemmCoefs), static_cast<unsigned>(2 * B));
+  finish_kernel<NW><<<grid, NW * 32, finish_smem<NW>(f), st>>>(
+      ks, d_ax, d_bx, static_cast<int>(B), log_n, p2, np2, p1, np1, f, out_ax, out_bx, flags,
+      force_exact);
+  return cudaGetLastError();
+}
+
+// Warps per CTA for a table of cols_pad columns: every column tile must lie
+// inside the table rows (the cp.async loads read whole tiles), so NW divides
+// cols_pad / 16.
+int nw_for(int cols_pad) {
+  const int groups = cols_pad / 16;
+  for (int nw = 8; nw > 1; --nw)
+    if (groups % nw == 0) return nw;
+  return 1;
+}
+
+template <typename F>
+cudaError_t with_nw(int cols_pad, F&& f) {
+  switch (nw_for(cols_pad)) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    default: return f(std::integral_constant<int, 8>{});
+  }
+}
+
+template <int NW>
+cudaError_t set_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(icrt_kernel<NW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(finish_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kMaxDynSmem);
 }
 
 }  // namespace
 
 cudaError_t icrt_setup_attributes() {
-  return cudaFuncSetAttribute(icrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+  cudaError_t e;
+  if ((e = set_attrs<1>()) != cudaSuccess) return e;
+  if ((e = set_attrs<2>()) != cudaSuccess) return e;
+  if ((e = set_attrs<3>()) != cudaSuccess) return e;
+  if ((e = set_attrs<4>()) != cudaSuccess) return e;
+  if ((e = set_attrs<5>()) != cudaSuccess) return e;
+  if ((e = set_attrs<6>()) != cudaSuccess) return e;
+  if ((e = set_attrs<7>()) != cudaSuccess) return e;
+  return set_attrs<8>();
 }
+
+cudaError_t finisher_setup_attributes() { return cudaSuccess; }
 
 cudaError_t icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* primes, int np,
                  const IcrtTable& t, uint64_t* out, cudaStream_t st, const IcrtFlags* flags) {
   const size_t n = size_t(1) << log_n;
-  if (n < kCoefs) return cudaErrorInvalidValue;
-  int threads = 8 * (t.m_pad / 4);  // one thread per (coef group, chunk group)
-  threads = (threads + 31) / 32 * 32;
-  if (threads > 512) return cudaErrorInvalidValue;
-  dim3 grid(static_cast<unsigned>(n / kCoefs), static_cast<unsigned>(batch));
+  if (n < kGemmCoefs || 2 * np + 1 > kMaxGemmK) return cudaErrorInvalidValue;
   IcrtFlags f;
   if (flags) {
     if (t.p_limbs + 2 > kFixMaxLimbs) return cudaErrorInvalidValue;
@@ -260,12 +431,33 @@ cudaError_t icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* p
     cudaError_t e = cudaMemsetAsync(f.count, 0, sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
   }
-  icrt_kernel<<<grid, threads, icrt_smem(np, t.m_pad, t.target_bits), st>>>(
-      rns, log_n, primes, np, t.btab, t.m_out, t.m_pad, t.target_bits, out, f);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = with_nw(t.m_pad, [&](auto nw) {
+    return launch_icrt<decltype(nw)::value>(rns, batch, log_n, primes, np, t, out, st, f);
+  });
   if (e != cudaSuccess || !flags) return e;
-  icrt_fixup_kernel<<<64, 64, 0, st>>>(rns, log_n, primes, np, t.hat, t.big_p, t.half_p,
-                                       t.p_limbs, t.target_bits, out, f);
+  icrt_fixup_kernel<<<64, 64, 0, st>>>(rns, log_n, primes, np, t, out, f);
+  return cudaGetLastError();
+}
+
+cudaError_t finish_keyswitch(const uint64_t* ks, const uint64_t* d_ax, const uint64_t* d_bx,
+                             size_t B, int log_n, const DevPrime* p2, int np2,
+                             const DevPrime* p1, int np1, const Finisher& f,
+                             const IcrtTable& t2, const IcrtTable& t1, uint64_t* out_ax,
+                             uint64_t* out_bx, const IcrtFlags& flags, int force_exact,
+                             cudaStream_t st) {
+  const size_t n = size_t(1) << log_n;
+  if (n < kGemmCoefs || f.k2 + f.k1 > kMaxGemmK || f.cols_pad > 128 ||
+      t2.p_limbs + 2 > kFixMaxLimbs)
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(flags.count, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  e = with_nw(f.cols_pad, [&](auto nw) {
+    return launch_finish<decltype(nw)::value>(ks, d_ax, d_bx, B, log_n, p2, np2, p1, np1, f,
+                                              out_ax, out_bx, flags, force_exact, st);
+  });
+  if (e != cudaSuccess) return e;
+  finish_fixup_kernel<<<64, 64, 0, st>>>(ks, d_ax, d_bx, static_cast<int>(B), log_n, p2, np2, p1,
+                                         np1, f, t2, t1, out_ax, out_bx, flags);
   return cudaGetLastError();
 }
 

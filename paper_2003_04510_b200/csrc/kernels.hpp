@@ -9,6 +9,10 @@
 
 namespace hemul_gpu {
 
+// Opt-in dynamic shared memory cap we request (227 KB per CTA minus room for
+// static shared arrays).
+constexpr int kMaxDynSmem = 224 * 1024;
+
 // ---- NTT (ntt.cu) ----------------------------------------------------------
 cudaError_t ntt_setup_attributes();
 // rows = batch * np prime-major rows; row r uses prime r % np.
@@ -47,8 +51,8 @@ cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n
 
 // ---- iCRT (icrt.cu) --------------------------------------------------------
 // B table for the exact reconstruction mod 2^T: (2 np + 1) rows x m_pad
-// columns of 30-bit chunks (rows 2j: H_j mod 2^T, 2j+1: the same shifted up
-// one chunk, 2np: (-P) mod 2^T), m_out = ceil(T / 30) real columns.
+// columns of 25-bit chunks (rows 2j: H_j mod 2^T, 2j+1: H_j 2^30 mod 2^T,
+// 2np: (-P) mod 2^T), m_out = ceil(T / 25) real columns.
 struct IcrtTable {
   const uint32_t* btab = nullptr;
   int m_out = 0;
@@ -77,6 +81,35 @@ cudaError_t icrt_setup_attributes();
 cudaError_t icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* primes, int np,
                  const IcrtTable& t, uint64_t* out, cudaStream_t st,
                  const IcrtFlags* flags = nullptr);
+
+// Fused key-switch finisher (heaan.cpp:398-409 after the evk product): for
+// each coefficient one GEMM over the region-2 residues of ks (t_j halves + k)
+// and the region-1 residues of d evaluates
+//   V = X2 + 2^(logQ-1) + 2^logQ (X1 + 2^(logp-1)),
+//   X2 = ks-part mod 2^(logq+logQ), X1 = d mod 2^logq,
+// from bit `base` up, and writes out = bits [logQ+logp, logQ+logq) of V
+// = R_logp(d + R_logQ(ks)) — ModDown, the add and the rescale at once.
+// Region-2 rows are truncated below bit base = logQ - 125; the dropped part
+// is < 2^(base+68), so a coefficient is exact unless the 64 bits below the
+// output are all ones (probability 2^-64); such coefficients are flagged and
+// recomputed by an exact big-integer fix-up kernel (no approximation ever
+// reaches the output).
+struct Finisher {
+  const uint32_t* btab = nullptr;  // (k2 + k1) x cols_pad, 25-bit chunks
+  int cols = 0, cols_pad = 0, k2 = 0, k1 = 0, base = 0;
+  int half_q_bit = 0, half_p_bit = 0, out_bit = 0, out_bits = 0;
+  int log_q = 0, log_Q = 0, log_p = 0;
+};
+cudaError_t finisher_setup_attributes();
+// ks: 2B x np2 x n (B ax-batches then B bx-batches), d_ax / d_bx: B x np1 x n
+// (iNTT'd d1 / d0); out: B x n x ceil((logq-logp)/64) each.
+// force_exact != 0 routes every coefficient through the exact fix-up (test).
+cudaError_t finish_keyswitch(const uint64_t* ks, const uint64_t* d_ax, const uint64_t* d_bx,
+                             size_t B, int log_n, const DevPrime* p2, int np2,
+                             const DevPrime* p1, int np1, const Finisher& f,
+                             const IcrtTable& t2, const IcrtTable& t1, uint64_t* out_ax,
+                             uint64_t* out_bx, const IcrtFlags& flags, int force_exact,
+                             cudaStream_t st);
 
 // ---- element-wise RNS and polynomial kernels (poly.cu) ---------------------
 // out = a * b mod p_j over batch x np x n.

@@ -103,11 +103,28 @@ Nat nat_neg_mod_pow2(const Nat& a, int bits) {
   return r;
 }
 
-uint32_t chunk30(const Nat& a, int m) {
-  const int bit = 30 * m, k = bit / 64, off = bit % 64;
+// (a << s) mod 2^bits
+Nat nat_shl_low(const Nat& a, int s, int bits) {
+  const int limbs = (bits + 63) / 64;
+  Nat r(limbs, 0);
+  const int ws = s / 64, bs = s % 64;
+  for (int k = 0; k < limbs; ++k) {
+    const int src = k - ws;
+    uint64_t v = 0;
+    if (src >= 0 && src < int(a.size())) v = a[src] << bs;
+    if (bs && src - 1 >= 0 && src - 1 < int(a.size())) v |= a[src - 1] >> (64 - bs);
+    r[k] = v;
+  }
+  if (bits % 64) r[limbs - 1] &= (uint64_t(1) << (bits % 64)) - 1;
+  return r;
+}
+
+// bits [bit, bit + width) of a, width <= 32
+uint32_t bits_at(const Nat& a, int bit, int width) {
+  const int k = bit / 64, off = bit % 64;
   uint64_t v = k < int(a.size()) ? a[k] >> off : 0;
-  if (off > 34 && k + 1 < int(a.size())) v |= a[k + 1] << (64 - off);
-  return uint32_t(v) & 0x3fffffffu;
+  if (off + width > 64 && k + 1 < int(a.size())) v |= a[k + 1] << (64 - off);
+  return uint32_t(v & ((uint64_t(1) << width) - 1));
 }
 
 uint32_t bit_reverse(uint32_t i, int bits) {
@@ -247,21 +264,22 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
     r.crt.push_back(std::move(c));
   }
 
-  // iCRT table: rows 2j = chunks of H_j mod 2^T, 2j+1 = the same one chunk
-  // up, 2np = chunks of (-P) mod 2^T
+  // iCRT operands mod 2^T: H_j, H_j 2^30 (for the high 30-bit half of t_j)
+  // and (-P), then the 25-bit-chunk table rows of the same order
   const int T = r.target_bits;
-  r.m_out = (T + 29) / 30;
+  r.hat_t.resize(2 * count + 1);
+  for (int j = 0; j < count; ++j) {
+    r.hat_t[2 * j] = nat_low(hat[j], T);
+    r.hat_t[2 * j + 1] = nat_shl_low(hat[j], 30, T);
+  }
+  r.hat_t[2 * count] = nat_neg_mod_pow2(P, T);
+  r.m_out = (T + kChunkBits - 1) / kChunkBits;
   r.m_pad = (r.m_out + 15) / 16 * 16;
   const int K = 2 * count + 1;
   r.btab.assign(size_t(K) * r.m_pad, 0);
-  for (int j = 0; j < count; ++j) {
-    const Nat h = nat_low(hat[j], T);
-    for (int m = 0; m < r.m_out; ++m) {
-      const uint32_t v = chunk30(h, m);
-      r.btab[size_t(2 * j) * r.m_pad + m] = v;
-      if (m + 1 < r.m_out) r.btab[size_t(2 * j + 1) * r.m_pad + m + 1] = v;
-    }
-  }
+  for (int row = 0; row < K; ++row)
+    for (int m = 0; m < r.m_out; ++m)
+      r.btab[size_t(row) * r.m_pad + m] = bits_at(r.hat_t[row], kChunkBits * m, kChunkBits);
   r.p_limbs = (nat_bits(P) + 63) / 64;
   r.hat_full.assign(size_t(count) * r.p_limbs, 0);
   for (int j = 0; j < count; ++j)
@@ -272,9 +290,39 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   for (int k = 0; k < r.p_limbs && k < int(P.size()); ++k) r.big_p[k] = P[k];
   for (int k = 0; k < r.p_limbs; ++k)
     r.half_p[k] = (r.big_p[k] >> 1) | (k + 1 < r.p_limbs ? r.big_p[k + 1] << 63 : 0);
-  const Nat negP = nat_neg_mod_pow2(P, T);
-  for (int m = 0; m < r.m_out; ++m) r.btab[size_t(2 * count) * r.m_pad + m] = chunk30(negP, m);
   return r;
+}
+
+FinisherHost build_finisher(const RegionHost& r1, const RegionHost& r2, int log_q,
+                            int log_q_max, int log_p) {
+  // V = X2 + 2^logQ X1 (+ both rounding halves), evaluated from bit `base`
+  // up: region-2 rows are H_j-type values mod 2^(logq+logQ) truncated below
+  // base, region-1 rows are exact values mod 2^logq placed at bit logQ.
+  FinisherHost f;
+  const int T2 = log_q + log_q_max;
+  f.base = std::max(0, log_q_max - kFinisherGuardBits);
+  f.width = T2 - f.base;
+  f.cols = (f.width + kChunkBits - 1) / kChunkBits;
+  f.cols_pad = (f.cols + 15) / 16 * 16;
+  f.k2 = 2 * r2.np + 1;
+  f.k1 = 2 * r1.np + 1;
+  const int K = f.k2 + f.k1;
+  f.btab.assign(size_t(K) * f.cols_pad, 0);
+  for (int row = 0; row < f.k2; ++row)
+    for (int m = 0; m < f.cols; ++m)
+      f.btab[size_t(row) * f.cols_pad + m] =
+          bits_at(r2.hat_t[row], f.base + kChunkBits * m, kChunkBits);
+  const int shift = log_q_max - f.base;  // region-1 values sit at bit logQ
+  for (int row = 0; row < f.k1; ++row) {
+    const Nat v = nat_shl_low(r1.hat_t[row], shift, f.width);
+    for (int m = 0; m < f.cols; ++m)
+      f.btab[size_t(f.k2 + row) * f.cols_pad + m] = bits_at(v, kChunkBits * m, kChunkBits);
+  }
+  f.half_q_bit = log_q_max - 1 - f.base;
+  f.half_p_bit = log_q_max + log_p - 1 - f.base;
+  f.out_bit = log_q_max + log_p - f.base;
+  f.out_bits = log_q - log_p;
+  return f;
 }
 
 }  // namespace hemul_gpu

@@ -31,7 +31,9 @@ struct RegionHost {
     std::vector<uint32_t> wtab;
   };
   std::vector<Crt> crt;
-  // iCRT table (see kernels.hpp IcrtTable)
+  // iCRT operands mod 2^T, rows in A order: H_j, H_j 2^30, ..., (-P)
+  std::vector<std::vector<uint64_t>> hat_t;
+  // iCRT table (see kernels.hpp IcrtTable): hat_t rows in 25-bit chunks
   int m_out = 0, m_pad = 0;
   std::vector<uint32_t> btab;
   // exact iCRT fallback: H_j = P / p_j rows, P, floor(P / 2), p_limbs each
@@ -46,5 +48,20 @@ struct RegionHost {
 // threads > 1 parallelises the twiddle tables.
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
                         const std::vector<int>& crt_bits, int threads);
+
+// Chunk width of the iCRT GEMM's B operand (products 30 x 25 bits, see
+// igemm.cuh) and the fraction window kept below bit log_Q by the fused
+// key-switch finisher.
+constexpr int kChunkBits = 25;
+constexpr int kFinisherGuardBits = 125;
+
+// Table of the fused ModDown + add + rescale kernel (kernels.hpp Finisher).
+struct FinisherHost {
+  int base = 0, width = 0, cols = 0, cols_pad = 0, k2 = 0, k1 = 0;
+  int half_q_bit = 0, half_p_bit = 0, out_bit = 0, out_bits = 0;
+  std::vector<uint32_t> btab;  // (k2 + k1) x cols_pad
+};
+FinisherHost build_finisher(const RegionHost& r1, const RegionHost& r2, int log_q, int log_q_max,
+                            int log_p);
 
 }  // namespace hemul_gpu

@@ -7,16 +7,22 @@
 // then x n^-1 (folded here into level 0's butterfly).
 //
 // B200 mapping. One transform of n = 2^logN 64-bit residues is split into
-// two memory passes (2^s1 x 2^s2):
-//   pass A: levels [0, s1) on 2^s1-point columns at stride 2^s2, a CTA owns
+// two memory passes (2^s1 x 2^s2, s1 = ceil(logN/2)):
+//   pass A: levels [0, s1) on 2^s1-point columns at stride 2^s2; a CTA owns
 //           C adjacent columns (C x 8 B contiguous per global row);
 //   pass B: levels [s1, logN) on contiguous 2^s2-point blocks.
-// Inside a pass the block sits in shared memory and each thread runs radix-8
-// butterfly units (3 levels on 8 registers) between barriers, so shared
-// memory is touched once per 3 levels. Values stay lazy in [0, 4p) (forward)
-// or [0, 2p) (inverse) and are canonicalised at the end, so every output is
-// bit-identical to the reference's canonical residues (ntt.hpp:12-16, all
-// variants bit-identical, test_ntt.cpp:120-165).
+// Inside a pass the CTA's 4096 residues sit in shared memory and each thread
+// holds 8 of them in registers, running radix-8 butterfly units (3 levels)
+// between barriers, so shared memory is touched once per 3 levels. The pass
+// size S is a template parameter: every level group, unit and register index
+// is resolved at compile time (no local memory). Values stay lazy in [0, 4p)
+// (forward) / [0, 2p) (inverse) and are canonicalised at the end, so every
+// output is bit-identical to the reference's canonical residues (ntt.hpp:
+// 12-16, all variants bit-identical, test_ntt.cpp:120-165).
+//
+// Rows are visited prime-major (all batch rows of prime j back to back), so a
+// prime's twiddle table is streamed from HBM once per launch and re-read from
+// L2 by the other rows.
 #include <cuda_runtime.h>
 
 #include "device_tables.cuh"
@@ -26,6 +32,8 @@
 namespace hemul_gpu {
 
 namespace {
+
+constexpr int kPassElems = 4096;  // residues per CTA (32 KB of shared memory)
 
 // Lazy Cooley-Tukey butterfly: a, b in [0, 4p) -> [0, 4p) (Harvey).
 __device__ __forceinline__ void ct_bfly(uint64_t& a, uint64_t& b, const Twiddle w, uint64_t p2,
@@ -44,111 +52,106 @@ __device__ __forceinline__ void gs_bfly(uint64_t& a, uint64_t& b, const Twiddle 
   b = csub(shoup_mul_4p(u + p2 - v, w.w, w.wq, negp), p2);
 }
 
-struct PassGeom {
-  int S;        // levels in this pass
-  int st0;      // first global level
+struct PassArgs {
+  uint64_t* data;
+  const Twiddle* tw;
+  const DevPrime* primes;
+  int np;
   int log_n;
-  int tlast;    // element stride inside a sub-problem = n >> (st0 + S)
-  int C;        // sub-problems per CTA
-  bool strided; // pass A layout (columns) vs pass B (contiguous blocks)
+  int st0;        // first global level of the pass
+  int log_c;      // log2 of sub-problems per CTA
+  int rows_per_prime;
+  int last;       // final pass: canonicalise (fwd) / fold n^-1 (inv)
 };
 
-// Shared-memory slot of element e of the CTA's sub-problem c.
-__device__ __forceinline__ int sidx(const PassGeom& g, int e, int c) {
-  return g.strided ? e * g.C + c : (c << g.S) + e;
-}
-
-// Decomposes unit index `uid` of a level group (levels l..l+k-1) into
-// (sub-problem c, group h, offset u).
-__device__ __forceinline__ void unit_coords(const PassGeom& g, int l, int k, int uid, int& c,
-                                            int& h, int& u) {
-  const int ubits = g.S - l - k;  // log2 of units per group
-  if (g.strided) {
-    c = uid % g.C;
-    const int rest = uid / g.C;
-    u = rest & ((1 << ubits) - 1);
-    h = rest >> ubits;
-  } else {
-    u = uid & ((1 << ubits) - 1);
-    h = (uid >> ubits) & ((1 << l) - 1);
-    c = uid >> (ubits + l);
-  }
-}
-
-// One pass of a forward (INV=false) or inverse (INV=true) transform.
-// grid.x = CTA index within the row, grid.y = row (batch x prime).
-// LAST: this pass produces the final output (canonicalise / n^-1 fold).
-template <bool INV>
-__global__ void __launch_bounds__(512) ntt_pass_kernel(uint64_t* __restrict__ data,
-                                                      const Twiddle* __restrict__ tw,
-                                                      const DevPrime* __restrict__ primes, int np,
-                                                      PassGeom g, int last) {
+// One pass of S levels. STRIDED: pass A layout (sub-problems are columns at
+// stride tlast); else pass B (contiguous blocks of 2^S).
+template <int S, bool STRIDED, bool INV>
+__global__ void __launch_bounds__(512) ntt_pass_kernel(PassArgs a) {
   extern __shared__ uint64_t sbuf[];
-  const int row = blockIdx.y;
-  const int j = row % np;
-  const DevPrime pr = primes[j];
+  constexpr int NG = (S + 2) / 3;  // level groups
+  // prime-major traversal: blockIdx.y = j * rows_per_prime + b (row-major
+  // when the rows are not whole prime sets)
+  int j, row;
+  if (a.rows_per_prime) {
+    j = blockIdx.y / a.rows_per_prime;
+    row = (blockIdx.y - j * a.rows_per_prime) * a.np + j;
+  } else {
+    row = blockIdx.y;
+    j = row % a.np;
+  }
+  const DevPrime& pr = a.primes[j];
   const uint64_t p = pr.p, p2 = 2 * p, negp = 0 - p;
-  const size_t n = size_t(1) << g.log_n;
-  uint64_t* rowp = data + size_t(row) * n;
-  const Twiddle* twr = tw + size_t(j) * n;
-  const int elems = g.C << g.S;
-  // global offset of the CTA's first sub-problem
-  const int sp0 = blockIdx.x * g.C;
-  const int m0 = 1 << g.st0;
+  const size_t n = size_t(1) << a.log_n;
+  uint64_t* rowp = a.data + size_t(row) * n;
+  const Twiddle* twr = a.tw + size_t(j) * n;
+  const int C = 1 << a.log_c;
+  const int elems = C << S;
+  const int tlast = 1 << (a.log_n - a.st0 - S);
+  const int sp0 = blockIdx.x << a.log_c;  // first sub-problem of the CTA
+  const int m0 = 1 << a.st0;
+  const int T = blockDim.x;               // = elems / 8
   // ---- load ---------------------------------------------------------------
-  if (g.strided) {
-    // sub-problems sp0..sp0+C-1 are columns r (g = 0): element e at r + e*tlast
-    for (int idx = threadIdx.x; idx < elems; idx += blockDim.x) {
-      const int e = idx / g.C, c = idx % g.C;
-      sbuf[idx] = rowp[size_t(e) * g.tlast + sp0 + c];
+  if (STRIDED) {
+    for (int idx = threadIdx.x; idx < elems; idx += T) {
+      const int e = idx >> a.log_c, c = idx & (C - 1);
+      sbuf[idx] = rowp[size_t(e) * tlast + sp0 + c];
     }
   } else {
-    const uint64_t* src = rowp + (size_t(sp0) << g.S);
-    for (int idx = threadIdx.x; idx < elems; idx += blockDim.x) sbuf[idx] = src[idx];
+    const uint64_t* src = rowp + (size_t(sp0) << S);
+    for (int idx = threadIdx.x; idx < elems; idx += T) sbuf[idx] = src[idx];
   }
   __syncthreads();
-  // ---- level groups -------------------------------------------------------
-  // forward: l = 0, 3, 6, ... ; inverse walks the same groups in reverse order
-  int ngroups = (g.S + 2) / 3;
-  for (int gi = 0; gi < ngroups; ++gi) {
-    const int grp = INV ? ngroups - 1 - gi : gi;
-    const int l = grp * 3;
-    const int k = min(3, g.S - l);
-    const int units = elems >> k;
-    for (int uid = threadIdx.x; uid < units; uid += blockDim.x) {
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    const int grp = INV ? NG - 1 - gi : gi;
+    const int l = 3 * grp;
+    const int k = S - l < 3 ? S - l : 3;   // levels in this group
+    const int ubits = S - l - k;           // log2 of units per group
+    const int per = 8 >> k;                // units per thread
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q >= per) break;
+      const int uid = threadIdx.x + q * T;
       int c, h, u;
-      unit_coords(g, l, k, uid, c, h, u);
-      // sub-problem global group index (pass A: gsub = 0)
-      const int gsub = g.strided ? 0 : sp0 + c;
-      const int e0 = (h << (g.S - l)) + u;
-      const int stride = 1 << (g.S - l - k);
+      if (STRIDED) {
+        c = uid & (C - 1);
+        const int rest = uid >> a.log_c;
+        u = rest & ((1 << ubits) - 1);
+        h = rest >> ubits;
+      } else {
+        u = uid & ((1 << ubits) - 1);
+        h = (uid >> ubits) & ((1 << l) - 1);
+        c = uid >> (ubits + l);
+      }
+      const int gsub = STRIDED ? 0 : sp0 + c;
+      const int e0 = (h << (S - l)) + u;
+      const int stride = 1 << ubits;
       uint64_t x[8];
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        if (v < (1 << k)) x[v] = sbuf[sidx(g, e0 + v * stride, c)];
+        if (v < (1 << k)) {
+          const int e = e0 + v * stride;
+          x[v] = sbuf[STRIDED ? (e << a.log_c) + c : (c << S) + e];
+        }
       if (!INV) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           if (i < k) {
-            const int L = g.st0 + l + i;  // global level
             const int half = 1 << (k - i - 1);
+            const size_t tb = (size_t(m0 + gsub) << (l + i)) + (size_t(h) << i);
 #pragma unroll
-            for (int blk = 0; blk < 4; ++blk) {
+            for (int blk = 0; blk < 4; ++blk)
               if (blk < (1 << i)) {
-                const int hh = (h << i) + blk;  // group inside sub-problem at level l+i
-                const Twiddle w = twr[(size_t(m0) << (l + i)) + (size_t(gsub) << (l + i)) + hh];
-                (void)L;
+                const Twiddle w = twr[tb + blk];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  if (q < half) {
-                    const int a = blk * 2 * half + q;
-                    ct_bfly(x[a], x[a + half], w, p2, negp);
-                  }
+                for (int r = 0; r < 4; ++r)
+                  if (r < half)
+                    ct_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, p2, negp);
               }
-            }
           }
         }
-        if (last && grp == ngroups - 1) {
+        if (a.last && grp == NG - 1) {
 #pragma unroll
           for (int v = 0; v < 8; ++v)
             if (v < (1 << k)) x[v] = reduce_4p(x[v], p);
@@ -157,52 +160,52 @@ __global__ void __launch_bounds__(512) ntt_pass_kernel(uint64_t* __restrict__ da
 #pragma unroll
         for (int ii = 2; ii >= 0; --ii) {
           if (ii < k) {
-            const int L = g.st0 + l + ii;
             const int half = 1 << (k - ii - 1);
+            const int L = a.st0 + l + ii;
+            const size_t tb = (size_t(m0 + gsub) << (l + ii)) + (size_t(h) << ii);
 #pragma unroll
-            for (int blk = 0; blk < 4; ++blk) {
+            for (int blk = 0; blk < 4; ++blk)
               if (blk < (1 << ii)) {
-                const int hh = (h << ii) + blk;
-                if (L == 0 && last) {
-                  // level 0 of the inverse with n^-1 folded in: a' = (u+v) n^-1,
-                  // b' = (u-v) itw[1] n^-1, outputs canonical.
+                if (L == 0 && a.last) {
+                  // level 0 with n^-1 folded in: a' = (u+v) n^-1,
+                  // b' = (u-v) itw[1] n^-1, outputs canonical
 #pragma unroll
-                  for (int q = 0; q < 4; ++q)
-                    if (q < half) {
-                      const int a = blk * 2 * half + q;
-                      const uint64_t uu = x[a], vv = x[a + half];
-                      x[a] = shoup_mul(uu + vv, pr.ninv, pr.ninv_q, p);
-                      x[a + half] = shoup_mul(uu + p2 - vv, pr.w1n, pr.w1n_q, p);
+                  for (int r = 0; r < 4; ++r)
+                    if (r < half) {
+                      const int i0 = blk * 2 * half + r;
+                      const uint64_t uu = x[i0], vv = x[i0 + half];
+                      x[i0] = shoup_mul(uu + vv, pr.ninv, pr.ninv_q, p);
+                      x[i0 + half] = shoup_mul(uu + p2 - vv, pr.w1n, pr.w1n_q, p);
                     }
                 } else {
-                  const Twiddle w = twr[(size_t(m0) << (l + ii)) + (size_t(gsub) << (l + ii)) + hh];
+                  const Twiddle w = twr[tb + blk];
 #pragma unroll
-                  for (int q = 0; q < 4; ++q)
-                    if (q < half) {
-                      const int a = blk * 2 * half + q;
-                      gs_bfly(x[a], x[a + half], w, p2, negp);
-                    }
+                  for (int r = 0; r < 4; ++r)
+                    if (r < half)
+                      gs_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, p2, negp);
                 }
               }
-            }
           }
         }
       }
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        if (v < (1 << k)) sbuf[sidx(g, e0 + v * stride, c)] = x[v];
+        if (v < (1 << k)) {
+          const int e = e0 + v * stride;
+          sbuf[STRIDED ? (e << a.log_c) + c : (c << S) + e] = x[v];
+        }
     }
     __syncthreads();
   }
   // ---- store --------------------------------------------------------------
-  if (g.strided) {
-    for (int idx = threadIdx.x; idx < elems; idx += blockDim.x) {
-      const int e = idx / g.C, c = idx % g.C;
-      rowp[size_t(e) * g.tlast + sp0 + c] = sbuf[idx];
+  if (STRIDED) {
+    for (int idx = threadIdx.x; idx < elems; idx += T) {
+      const int e = idx >> a.log_c, c = idx & (C - 1);
+      rowp[size_t(e) * tlast + sp0 + c] = sbuf[idx];
     }
   } else {
-    uint64_t* dst = rowp + (size_t(sp0) << g.S);
-    for (int idx = threadIdx.x; idx < elems; idx += blockDim.x) dst[idx] = sbuf[idx];
+    uint64_t* dst = rowp + (size_t(sp0) << S);
+    for (int idx = threadIdx.x; idx < elems; idx += T) dst[idx] = sbuf[idx];
   }
 }
 
@@ -216,42 +219,76 @@ void split_levels(int log_n, int& s1, int& s2) {
   }
 }
 
+template <int S, bool STRIDED, bool INV>
+cudaError_t launch_s(const PassArgs& a, size_t rows, int C, cudaStream_t st) {
+  const int subproblems = STRIDED ? (1 << (a.log_n - a.st0 - S)) : (1 << a.st0);
+  dim3 grid(subproblems / C, static_cast<unsigned>(rows));
+  const int threads = (C << S) / 8;
+  ntt_pass_kernel<S, STRIDED, INV><<<grid, threads, sizeof(uint64_t) * (C << S), st>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool STRIDED, bool INV>
+cudaError_t launch_any(int S, const PassArgs& a, size_t rows, int C, cudaStream_t st) {
+  switch (S) {
+    case 3: return launch_s<3, STRIDED, INV>(a, rows, C, st);
+    case 4: return launch_s<4, STRIDED, INV>(a, rows, C, st);
+    case 5: return launch_s<5, STRIDED, INV>(a, rows, C, st);
+    case 6: return launch_s<6, STRIDED, INV>(a, rows, C, st);
+    case 7: return launch_s<7, STRIDED, INV>(a, rows, C, st);
+    case 8: return launch_s<8, STRIDED, INV>(a, rows, C, st);
+    case 9: return launch_s<9, STRIDED, INV>(a, rows, C, st);
+    case 10: return launch_s<10, STRIDED, INV>(a, rows, C, st);
+    case 11: return launch_s<11, STRIDED, INV>(a, rows, C, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_pass(bool inv, uint64_t* data, const Twiddle* tw, const DevPrime* primes, int np,
                         size_t rows, int log_n, int st0, int S, bool strided, bool last,
                         cudaStream_t st) {
-  PassGeom g;
-  g.S = S;
-  g.st0 = st0;
-  g.log_n = log_n;
-  g.tlast = 1 << (log_n - st0 - S);
-  g.strided = strided;
-  // aim at ~4096 elements (32 KB) per CTA
-  const int per = 1 << S;
-  const int subproblems = strided ? g.tlast : (1 << st0);
-  int C = per >= 4096 ? 1 : 4096 / per;
+  const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
+  PassArgs a{data, tw, primes, np, log_n, st0, 0, rpp, last ? 1 : 0};
+  const int subproblems = strided ? (1 << (log_n - st0 - S)) : (1 << st0);
+  int C = (1 << S) >= kPassElems ? 1 : kPassElems >> S;
   if (C > subproblems) C = subproblems;
-  g.C = C;
-  const int elems = C * per;
-  int threads = elems / 8;
-  if (threads < 32) threads = 32;
-  if (threads > 512) threads = 512;
-  dim3 grid(subproblems / C, static_cast<unsigned>(rows));
-  const size_t smem = sizeof(uint64_t) * elems;
-  if (inv)
-    ntt_pass_kernel<true><<<grid, threads, smem, st>>>(data, tw, primes, np, g, last);
-  else
-    ntt_pass_kernel<false><<<grid, threads, smem, st>>>(data, tw, primes, np, g, last);
-  return cudaGetLastError();
+  if ((C << S) / 8 > 512 || (C << S) < 8) return cudaErrorInvalidValue;
+  while ((1 << a.log_c) < C) ++a.log_c;
+  if (strided)
+    return inv ? launch_any<true, true>(S, a, rows, C, st)
+               : launch_any<true, false>(S, a, rows, C, st);
+  return inv ? launch_any<false, true>(S, a, rows, C, st)
+             : launch_any<false, false>(S, a, rows, C, st);
+}
+
+template <int S, bool STRIDED, bool INV>
+cudaError_t attr_s() {
+  return cudaFuncSetAttribute(ntt_pass_kernel<S, STRIDED, INV>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+}
+
+template <bool STRIDED, bool INV>
+cudaError_t attr_all() {
+  cudaError_t e = cudaSuccess;
+  if ((e = attr_s<3, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<4, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<5, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<6, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<7, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<8, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<9, STRIDED, INV>()) != cudaSuccess) return e;
+  if ((e = attr_s<10, STRIDED, INV>()) != cudaSuccess) return e;
+  return attr_s<11, STRIDED, INV>();
 }
 
 }  // namespace
 
 cudaError_t ntt_setup_attributes() {
-  cudaError_t e = cudaFuncSetAttribute(ntt_pass_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(ntt_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              64 * 1024);
+  cudaError_t e;
+  if ((e = attr_all<true, false>()) != cudaSuccess) return e;
+  if ((e = attr_all<true, true>()) != cudaSuccess) return e;
+  if ((e = attr_all<false, false>()) != cudaSuccess) return e;
+  return attr_all<false, true>();
 }
 
 int ntt_num_passes(int log_n) {
@@ -264,7 +301,8 @@ cudaError_t ntt_forward_pass(int pass, uint64_t* data, size_t rows, int np, int 
                              const Twiddle* tw, const DevPrime* primes, cudaStream_t st) {
   int s1, s2;
   split_levels(log_n, s1, s2);
-  if (pass == 0) return launch_pass(false, data, tw, primes, np, rows, log_n, 0, s1, true, s2 == 0, st);
+  if (pass == 0)
+    return launch_pass(false, data, tw, primes, np, rows, log_n, 0, s1, true, s2 == 0, st);
   return launch_pass(false, data, tw, primes, np, rows, log_n, s1, s2, false, true, st);
 }
 

@@ -88,7 +88,9 @@ _SIGS = {
                                               ctypes.POINTER(ctypes.c_uint64)]),
     "hemul_gpu_reset_stats": (ctypes.c_int, [ctypes.c_void_p]),
     "hemul_gpu_imad_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    "hemul_gpu_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
 }
+HEMUL_OPT_FORCE_EXACT = 1
 
 
 def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
@@ -323,6 +325,11 @@ class Context:
 
     def reset_stats(self) -> None:
         self._check(self._lib.hemul_gpu_reset_stats(self._h))
+
+    def set_force_exact(self, on: bool = True) -> None:
+        """Route every he_mul output coefficient through the exact big-integer
+        fix-up kernel (test knob for the rarely taken exact path)."""
+        self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_FORCE_EXACT, int(on)))
 
     def set_stream(self, stream: int | None) -> None:
         """Launch on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""

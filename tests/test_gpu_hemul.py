@@ -71,6 +71,23 @@ def test_random_inputs_every_level_vs_oracle(cfg, restated):
         assert np.array_equal(ob, wb), log_q
 
 
+@pytest.mark.parametrize("cfg", [(30, 4, 13), (30, 10, 12), (30, 6, 11)])
+def test_exact_fixup_path_matches(cfg, restated):
+    """The finisher's exact big-integer fix-up (normally taken with
+    probability 2^-64 per coefficient) forced on every coefficient."""
+    ctx = _ctx(cfg)
+    ctx.set_force_exact(True)
+    p = ctx.params
+    rng = np.random.default_rng(77)
+    evk = (random_poly(rng, p.n, 2 * p.log_q_max), random_poly(rng, p.n, 2 * p.log_q_max))
+    for log_q in (p.log_q_max, 2 * p.log_p):
+        c1 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
+        c2 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
+        st, wa, wb = restated.he_mul(p.log_n, p.log_p, p.log_q_max, log_q, c1, c2, evk)
+        oa, ob = ctx.he_mul(c1, c2, log_q, evk=evk)
+        assert np.array_equal(oa, wa) and np.array_equal(ob, wb), log_q
+
+
 def test_edge_inputs_zero_and_all_ones(restated):
     cfg = (30, 4, 10)
     ctx = _ctx(cfg)
