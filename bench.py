@@ -75,25 +75,28 @@ def region_shapes(cfg, log_q):
 
 
 def work_per_step(p, np1: int, np2: int, B: int, log_q: int) -> dict[str, float]:
+    """Integer work per step of each kernel class in 32-bit IMAD-equivalent
+    multiply-adds: GEMM products of the 25x30-bit CRT/iCRT
+    formulation, 9 per Shoup modmul, 26 per variable modmul."""
     n, ln = p.n, p.log_n
     s1 = ln if ln <= 11 else (ln + 1) // 2
     s2 = ln - s1
-    m_in = math.ceil(log_q / 30)
-    m1 = math.ceil(log_q / 30)
-    m2 = math.ceil((log_q + p.log_q_max) / 30)
+    chunks = math.ceil(log_q / 25)                      # 25-bit chunks of a ct poly
+    fin_cols = math.ceil((min(p.log_q_max, 125) + log_q) / 25)
     fwd_rows = 4 * B * np1 + B * np2
     inv_rows = 3 * B * np1 + 2 * B * np2
     bf = n // 2
     return {
-        "crt": n * B * (4 * np1 + np2) * 2 * m_in,
+        "crt": n * B * (4 * np1 + np2) * 2 * chunks,
         "ntt_a": fwd_rows * bf * s1 * SHOUP_IMAD,
         "ntt_b": fwd_rows * bf * s2 * SHOUP_IMAD,
         "intt_b": inv_rows * bf * s2 * SHOUP_IMAD,
         "intt_a": inv_rows * bf * s1 * SHOUP_IMAD + inv_rows * n * SHOUP_IMAD,
         "tensor": n * B * np1 * 4 * MULMOD_IMAD,
         "evk": n * B * np2 * 2 * MULMOD_IMAD,
-        "icrt": n * B * (3 * ((2 * np1 + 1) * m1 + np1 * SHOUP_IMAD)
-                         + 2 * ((2 * np2 + 1) * m2 + np2 * SHOUP_IMAD)),
+        "icrt": n * B * ((2 * np1 + 1) * chunks + np1 * SHOUP_IMAD),
+        "finish": n * 2 * B * ((2 * np2 + 2 * np1 + 2) * fin_cols
+                               + (np1 + np2) * SHOUP_IMAD),
     }
 
 

@@ -237,7 +237,7 @@ void fill_region(RegionDev& d, const RegionHost& h, int log_n, cudaStream_t st) 
     upload(*dc.buf, c.wtab, st);
     dc.w.wtab = dc.buf->as<uint32_t>();
     dc.w.chunks = c.chunks;
-    dc.w.np_pad = c.np_pad;
+    dc.w.ld = c.ld;
     d.crt.push_back(std::move(dc));
   }
   (void)log_n;
@@ -598,11 +598,10 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     uint64_t* A2 = R1 + 2 * r1w;
     uint64_t* B2 = R1 + 3 * r1w;
     const CrtWeights* w1 = r1.weights(log_q);
-    uint64_t* dst[4] = {A1, B1, A2, B2};
-    for (int t = 0; t < 4; ++t)
-      run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
-        return crt_forward(in[t], L, B, log_n, *w1, p1, r1.np, dst[t], c->stream);
-      });
+    // one launch: ax1 -> A1, bx1 -> B1, ax2 -> A2, bx2 -> B2 (R1 is [A1|B1|A2|B2])
+    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
+      return crt_forward_multi(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
+    });
     ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
     // pointwise products are booked under iCRT like rns.cpp:364;
     // in place: d2 -> A1, d0 -> B1, d1 -> A2
@@ -639,7 +638,7 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
     flags.count = c->flagbuf.as<unsigned>();
     flags.ids = flags.count + 1;
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "finisher", [&] {
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
       return finish_keyswitch(KA, A2 /* d1 */, B1 /* d0 */, B, log_n, p2, r2.np, p1, r1.np,
                               lv.fin, r2.icrt, r1.icrt, o.a, o.b, flags, c->force_exact,
                               c->stream);

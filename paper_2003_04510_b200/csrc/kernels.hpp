@@ -35,12 +35,13 @@ cudaError_t ntt_inverse_pass(int pass, uint64_t* data, size_t rows, int np, int 
 cudaError_t imad_peak(double* ops_per_s, cudaStream_t st);
 
 // ---- CRT (crt.cu) ----------------------------------------------------------
-// Weight table for one (prime set, input width): wtab[m * 2 * np_pad + 2 j + h]
-// = 30-bit half h of 2^(30 m) mod p_j, m < chunks = ceil(in_bits / 30).
+// Weight table for one (prime set, input width): wtab[m * ld + 2 j + h]
+// = 30-bit half h of 2^(25 m) mod p_j, m < chunks = ceil(in_bits / 25)
+// (the input is cut into 25-bit chunks: the iGEMM operand widths).
 struct CrtWeights {
   const uint32_t* wtab = nullptr;
   int chunks = 0;
-  int np_pad = 0;  // multiple of kCrtPrimesPerTile
+  int ld = 0;  // crt_cols_pad(2 np)
 };
 constexpr int kCrtPrimesPerTile = 16;
 cudaError_t crt_setup_attributes();
@@ -48,6 +49,11 @@ cudaError_t crt_setup_attributes();
 cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n,
                         const CrtWeights& w, const DevPrime* primes, int np, uint64_t* out,
                         cudaStream_t st);
+// Up to 4 independent inputs of `batch` polys each in one launch; input t
+// lands at out + t * batch * np * n.
+cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs, size_t batch,
+                              int log_n, const CrtWeights& w, const DevPrime* primes, int np,
+                              uint64_t* out, cudaStream_t st);
 
 // ---- iCRT (icrt.cu) --------------------------------------------------------
 // B table for the exact reconstruction mod 2^T: (2 np + 1) rows x m_pad

@@ -244,20 +244,20 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
     d.w1n_q = shoup_q(w1n, p);
   });
 
-  // CRT weights: 30-bit halves of 2^(30 m) mod p_j
+  // CRT weights: 30-bit halves of 2^(25 m) mod p_j (kernels.hpp CrtWeights)
   for (int bits : crt_bits) {
     RegionHost::Crt c;
     c.in_bits = bits;
-    c.chunks = (bits + 29) / 30;
-    c.np_pad = (count + 15) / 16 * 16;
-    c.wtab.assign(size_t(c.chunks) * 2 * c.np_pad, 0);
+    c.chunks = (bits + kChunkBits - 1) / kChunkBits;
+    c.ld = crt_cols_pad(2 * count);
+    c.wtab.assign(size_t(c.chunks) * c.ld, 0);
     for (int j = 0; j < count; ++j) {
       const uint64_t p = r.primes[j];
-      const uint64_t step = powmod(2, 30, p);
+      const uint64_t step = powmod(2, kChunkBits, p);
       uint64_t u = 1 % p;
       for (int m = 0; m < c.chunks; ++m) {
-        c.wtab[size_t(m) * 2 * c.np_pad + 2 * j] = uint32_t(u & 0x3fffffffu);
-        c.wtab[size_t(m) * 2 * c.np_pad + 2 * j + 1] = uint32_t(u >> 30);
+        c.wtab[size_t(m) * c.ld + 2 * j] = uint32_t(u & 0x3fffffffu);
+        c.wtab[size_t(m) * c.ld + 2 * j + 1] = uint32_t(u >> 30);
         u = mulmod(u, step, p);
       }
     }

@@ -27,7 +27,7 @@ struct RegionHost {
   std::vector<Twiddle> tw, itw;      // np * n each, ShoupPair tables
   // CRT weights per input width (see kernels.hpp CrtWeights)
   struct Crt {
-    int in_bits = 0, chunks = 0, np_pad = 0;
+    int in_bits = 0, chunks = 0, ld = 0;
     std::vector<uint32_t> wtab;
   };
   std::vector<Crt> crt;
@@ -54,6 +54,14 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
 // key-switch finisher.
 constexpr int kChunkBits = 25;
 constexpr int kFinisherGuardBits = 125;
+
+// CRT weight-table columns (2 np) padded for crt.cu's tiling: a multiple of
+// 16 up to 192 columns (one tile of <= 12 warps), else a multiple of 128
+// (tiles of 8 warps).
+inline int crt_cols_pad(int cols) {
+  const int c16 = (cols + 15) / 16 * 16;
+  return c16 <= 192 ? c16 : (cols + 127) / 128 * 128;
+}
 
 // Table of the fused ModDown + add + rescale kernel (kernels.hpp Finisher).
 struct FinisherHost {
