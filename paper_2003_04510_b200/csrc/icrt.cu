@@ -127,25 +127,27 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
   uint32_t* A = reinterpret_cast<uint32_t*>(smem);                     // [K][32]
   uint32_t* Bs = A + K * kGemmCoefs;                                   // cp.async ring
   double* part = reinterpret_cast<double*>(Bs + kStages * kKT * NC);  // [NW][32]
-  uint64_t* S = reinterpret_cast<uint64_t*>(part + NW * 32);          // [32][m_pad]
-  uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * t.m_pad);  // [32][m_out]
+  // odd row strides: the carry pass walks one row per lane, conflict-free
+  const int lds = t.m_pad + 1, ldd = t.m_out | 1;
+  uint64_t* S = reinterpret_cast<uint64_t*>(part + NW * 32);       // [32][lds]
+  uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * lds);  // [32][ldd]
   const Seg seg{rns + size_t(b) * np * n, primes, np};
   build_rows(seg, n, c0, A, 0, part, flags, size_t(b) * n + c0);
   for (int col0 = 0; col0 < t.m_pad; col0 += NC) {
     uint64_t acc[4][4] = {};
     igemm_32xN<NW, kKT, kStages>(A, K, t.btab, t.m_pad, col0, Bs, acc);
-    store_tile<NW>(S, t.m_pad, col0, t.m_pad, acc);
+    store_tile<NW>(S, lds, col0, t.m_pad, acc);
   }
   __syncthreads();
   if (threadIdx.x < kGemmCoefs)
-    carry_pass(S + threadIdx.x * t.m_pad, D + threadIdx.x * t.m_out, t.m_out, -1, -1);
+    carry_pass(S + threadIdx.x * lds, D + threadIdx.x * ldd, t.m_out, -1, -1);
   __syncthreads();
   const int tl = (t.target_bits + 63) / 64;
   const uint64_t top = t.target_bits % 64 ? (uint64_t(1) << (t.target_bits % 64)) - 1 : ~0ull;
   uint64_t* dst = out + (size_t(b) * n + c0) * tl;
   for (int idx = threadIdx.x; idx < kGemmCoefs * tl; idx += blockDim.x) {
     const int c = idx / tl, k = idx - c * tl;
-    uint64_t v = digits_window(D + c * t.m_out, t.m_out, 64 * k);
+    uint64_t v = digits_window(D + c * ldd, t.m_out, 64 * k);
     if (k == tl - 1) v &= top;
     dst[idx] = v;
   }
@@ -246,15 +248,17 @@ __global__ void __launch_bounds__(NW * 32) finish_kernel(
   build_rows(s1, n, c0, A, f.k2, part, none, 0);
   uint64_t acc[4][4] = {};
   igemm_32xN<NW, kKT, kStages>(A, K, f.btab, f.cols_pad, 0, Bs, acc);
-  // a single column tile (cols_pad <= 16 NW): S and the digits reuse A
-  uint64_t* S = reinterpret_cast<uint64_t*>(smem);                         // [32][cols_pad]
-  uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * f.cols_pad);  // [32][cols]
-  store_tile<NW>(S, f.cols_pad, 0, f.cols_pad, acc);
+  // a single column tile (cols_pad <= 16 NW): S and the digits reuse A; odd
+  // row strides keep the one-row-per-lane carry pass conflict-free
+  const int lds = f.cols_pad + 1, ldd = f.cols | 1;
+  uint64_t* S = reinterpret_cast<uint64_t*>(smem);                  // [32][lds]
+  uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * lds);  // [32][ldd]
+  store_tile<NW>(S, lds, 0, f.cols_pad, acc);
   __syncthreads();
   if (threadIdx.x < kGemmCoefs) {
     const int c = threadIdx.x;
-    uint32_t* dc = D + c * f.cols;
-    carry_pass(S + c * f.cols_pad, dc, f.cols, f.half_q_bit, f.half_p_bit);
+    uint32_t* dc = D + c * ldd;
+    carry_pass(S + c * lds, dc, f.cols, f.half_q_bit, f.half_p_bit);
     // exact unless the 64 bits below the output are all ones (kernels.hpp)
     const bool amb = f.base > 0 && digits_window(dc, f.cols, f.out_bit - 64) == ~0ull;
     if (amb || force_exact) {
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(NW * 32) finish_kernel(
   for (int idx = threadIdx.x; idx < kGemmCoefs * lo_l; idx += blockDim.x) {
     const int c = idx / lo_l, k = idx - c * lo_l;
     if (flagged[c]) continue;  // written by the fix-up kernel
-    uint64_t v = digits_window(D + c * f.cols, f.cols, f.out_bit + 64 * k);
+    uint64_t v = digits_window(D + c * ldd, f.cols, f.out_bit + 64 * k);
     if (k == lo_l - 1) v &= top;
     dst[idx] = v;
   }
@@ -336,14 +340,15 @@ __global__ void finish_fixup_kernel(const uint64_t* __restrict__ ks,
 template <int NW>
 size_t icrt_smem(int np, int m_pad) {
   return size_t(2 * np + 1) * kGemmCoefs * 4 + size_t(kStages) * kKT * 16 * NW * 4 +
-         NW * 32 * 8 + size_t(kGemmCoefs) * m_pad * 12;
+         NW * 32 * 8 + size_t(kGemmCoefs) * (m_pad + 1) * 12;
 }
 
 template <int NW>
 size_t finish_smem(const Finisher& f) {
   const size_t main = size_t(f.k2 + f.k1) * kGemmCoefs * 4 +
                       size_t(kStages) * kKT * 16 * NW * 4 + NW * 32 * 8;
-  const size_t epi = size_t(kGemmCoefs) * f.cols_pad * 8 + size_t(kGemmCoefs) * f.cols * 4;
+  const size_t epi =
+      size_t(kGemmCoefs) * (f.cols_pad + 1) * 8 + size_t(kGemmCoefs) * (f.cols | 1) * 4;
   return main > epi ? main : epi;
 }
 

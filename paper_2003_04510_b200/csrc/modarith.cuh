@@ -28,7 +28,10 @@ __device__ __forceinline__ uint64_t mulhi_approx(uint64_t x, uint64_t y) {
   const uint32_t x0 = lo32(x), x1 = hi32(x), y0 = lo32(y), y1 = hi32(y);
   const uint64_t a = wide(x1, y0);
   const uint64_t b = wide(x0, y1);
-  return wide(x1, y1) + hi32(a) + hi32(b);
+  // the 33-bit sum of the high halves as the addend of the last IMAD.WIDE
+  // (avoids materialising {hi, 0} register pairs)
+  const uint64_t s = static_cast<uint64_t>(hi32(a)) + hi32(b);
+  return wide(x1, y1) + s;
 }
 
 // Exact floor(x*y / 2^64).
@@ -38,9 +41,10 @@ __device__ __forceinline__ uint64_t mulhi(uint64_t x, uint64_t y) { return __umu
 __device__ __forceinline__ uint64_t mul_sub_lo(uint64_t x, uint64_t y, uint64_t q, uint64_t negp) {
   const uint32_t x0 = lo32(x), x1 = hi32(x), y0 = lo32(y), y1 = hi32(y);
   const uint32_t q0 = lo32(q), q1 = hi32(q), n0 = lo32(negp), n1 = hi32(negp);
-  uint64_t r = wide(x0, y0) + wide(q0, n0);  // wraps mod 2^64
-  const uint32_t cross = x0 * y1 + x1 * y0 + q0 * n1 + q1 * n0;
-  return r + (static_cast<uint64_t>(cross) << 32);
+  const uint64_t r = wide(x0, y0) + wide(q0, n0);  // wraps mod 2^64
+  // the cross terms only touch the high word: 4 chained 32-bit IMADs
+  const uint32_t hi = hi32(r) + x0 * y1 + x1 * y0 + q0 * n1 + q1 * n0;
+  return (static_cast<uint64_t>(hi) << 32) | lo32(r);
 }
 
 // Shoup multiplication by a fixed operand w with wq = floor(w 2^64 / p).

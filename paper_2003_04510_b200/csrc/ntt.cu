@@ -11,14 +11,17 @@
 //   pass A: levels [0, s1) on 2^s1-point columns at stride 2^s2; a CTA owns
 //           C adjacent columns (C x 8 B contiguous per global row);
 //   pass B: levels [s1, logN) on contiguous 2^s2-point blocks.
-// Inside a pass the CTA's 4096 residues sit in shared memory and each thread
-// holds 8 of them in registers, running radix-8 butterfly units (3 levels)
+// A CTA holds 4096 residues (32 KB) in shared memory; each of its 512
+// threads keeps 8 in registers and runs radix-8 butterfly units (3 levels)
 // between barriers, so shared memory is touched once per 3 levels. The pass
-// size S is a template parameter: every level group, unit and register index
-// is resolved at compile time (no local memory). Values stay lazy in [0, 4p)
-// (forward) / [0, 2p) (inverse) and are canonicalised at the end, so every
-// output is bit-identical to the reference's canonical residues (ntt.hpp:
-// 12-16, all variants bit-identical, test_ntt.cpp:120-165).
+// size S, the sub-problems per CTA C and the thread count are template
+// parameters: all index arithmetic folds to shifts of threadIdx, and no
+// register array is dynamically indexed. Pass A's 2^S twiddles are staged in
+// shared memory (every column of a row uses the same ones); pass B's are
+// read once each from global memory. Values stay lazy in [0, 4p) (forward) /
+// [0, 2p) (inverse) and are canonicalised at the end, so every output is
+// bit-identical to the reference's canonical residues (ntt.hpp:12-16; all
+// reference variants are bit-identical, test_ntt.cpp:120-165).
 //
 // Rows are visited prime-major (all batch rows of prime j back to back), so a
 // prime's twiddle table is streamed from HBM once per launch and re-read from
@@ -33,23 +36,27 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kPassElems = 4096;  // residues per CTA (32 KB of shared memory)
+constexpr int kLogPassElems = 12;  // 4096 residues per CTA
 
-// Lazy Cooley-Tukey butterfly: a, b in [0, 4p) -> [0, 4p) (Harvey).
-__device__ __forceinline__ void ct_bfly(uint64_t& a, uint64_t& b, const Twiddle w, uint64_t p2,
-                                        uint64_t negp) {
-  const uint64_t u = csub(a, p2);
-  const uint64_t v = csub(shoup_mul_4p(b, w.w, w.wq, negp), p2);
+// Lazy Cooley-Tukey butterfly, one conditional subtraction: a, b in [0, 8p)
+// -> [0, 8p). u = a mod 4p in [0, 4p), v = b w mod p in [0, 4p) (approximate
+// Shoup quotient), a' = u + v < 8p, b' = u + 4p - v in (0, 8p). 8p < 2^63
+// for p < 2^60, so every intermediate fits (Harvey's bounds, one level wider).
+__device__ __forceinline__ void ct_bfly(uint64_t& a, uint64_t& b, uint64_t w, uint64_t wq,
+                                        uint64_t p4, uint64_t negp) {
+  const uint64_t u = csub(a, p4);
+  const uint64_t v = shoup_mul_4p(b, w, wq, negp);
   a = u + v;
-  b = u + p2 - v;
+  b = u + p4 - v;
 }
 
-// Lazy Gentleman-Sande butterfly: a, b in [0, 2p) -> [0, 2p).
-__device__ __forceinline__ void gs_bfly(uint64_t& a, uint64_t& b, const Twiddle w, uint64_t p2,
-                                        uint64_t negp) {
+// Lazy Gentleman-Sande butterfly, one conditional subtraction: a, b in
+// [0, 4p) -> [0, 4p).
+__device__ __forceinline__ void gs_bfly(uint64_t& a, uint64_t& b, uint64_t w, uint64_t wq,
+                                        uint64_t p4, uint64_t negp) {
   const uint64_t u = a, v = b;
-  a = csub(u + v, p2);
-  b = csub(shoup_mul_4p(u + p2 - v, w.w, w.wq, negp), p2);
+  a = csub(u + v, p4);
+  b = shoup_mul_4p(u + p4 - v, w, wq, negp);
 }
 
 struct PassArgs {
@@ -58,22 +65,23 @@ struct PassArgs {
   const DevPrime* primes;
   int np;
   int log_n;
-  int st0;        // first global level of the pass
-  int log_c;      // log2 of sub-problems per CTA
-  int rows_per_prime;
-  int last;       // final pass: canonicalise (fwd) / fold n^-1 (inv)
+  int st0;             // first global level of the pass
+  int rows_per_prime;  // 0: row-major traversal (ragged row counts)
+  int last;            // final pass: canonicalise (fwd) / fold n^-1 (inv)
 };
 
-// One pass of S levels. STRIDED: pass A layout (sub-problems are columns at
-// stride tlast); else pass B (contiguous blocks of 2^S).
-template <int S, bool STRIDED, bool INV>
-__global__ void __launch_bounds__(512) ntt_pass_kernel(PassArgs a) {
-  extern __shared__ uint64_t sbuf[];
-  constexpr int NG = (S + 2) / 3;  // level groups
-  // prime-major traversal: blockIdx.y = j * rows_per_prime + b (row-major
-  // when the rows are not whole prime sets)
+// One pass of S levels over C = 2^LOGC sub-problems. STRIDED: pass A layout
+// (sub-problems are columns at stride tlast); else pass B (contiguous blocks).
+template <int S, int LOGC, bool STRIDED, bool INV>
+__global__ void __launch_bounds__(1 << (S + LOGC - 3)) ntt_pass_kernel(PassArgs a) {
+  constexpr int C = 1 << LOGC;
+  constexpr int ELEMS = C << S;
+  constexpr int T = ELEMS / 8;
+  constexpr int NG = (S + 2) / 3;
+  extern __shared__ uint64_t sbuf[];       // [ELEMS] residues, then pass-A twiddles
+  uint64_t* stw = sbuf + ELEMS;            // [2^S] x {w, wq}
   int j, row;
-  if (a.rows_per_prime) {
+  if (a.rows_per_prime) {  // prime-major: blockIdx.y = j * rows_per_prime + b
     j = blockIdx.y / a.rows_per_prime;
     row = (blockIdx.y - j * a.rows_per_prime) * a.np + j;
   } else {
@@ -81,42 +89,44 @@ __global__ void __launch_bounds__(512) ntt_pass_kernel(PassArgs a) {
     j = row % a.np;
   }
   const DevPrime& pr = a.primes[j];
-  const uint64_t p = pr.p, p2 = 2 * p, negp = 0 - p;
+  const uint64_t p = pr.p, p4 = 4 * p, negp = 0 - p;
   const size_t n = size_t(1) << a.log_n;
   uint64_t* rowp = a.data + size_t(row) * n;
   const Twiddle* twr = a.tw + size_t(j) * n;
-  const int C = 1 << a.log_c;
-  const int elems = C << S;
   const int tlast = 1 << (a.log_n - a.st0 - S);
-  const int sp0 = blockIdx.x << a.log_c;  // first sub-problem of the CTA
-  const int m0 = 1 << a.st0;
-  const int T = blockDim.x;               // = elems / 8
-  // ---- load ---------------------------------------------------------------
+  const int sp0 = blockIdx.x << LOGC;  // first sub-problem of the CTA
+  const int tid = threadIdx.x;
+  // ---- load (+ pass-A twiddles) ------------------------------------------
   if (STRIDED) {
-    for (int idx = threadIdx.x; idx < elems; idx += T) {
-      const int e = idx >> a.log_c, c = idx & (C - 1);
-      sbuf[idx] = rowp[size_t(e) * tlast + sp0 + c];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int idx = tid + r * T;
+      sbuf[idx] = rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))];
     }
+    const uint64_t* t2 = reinterpret_cast<const uint64_t*>(twr);
+    for (int i = tid; i < 2 << S; i += T) stw[i] = t2[i];
   } else {
-    const uint64_t* src = rowp + (size_t(sp0) << S);
-    for (int idx = threadIdx.x; idx < elems; idx += T) sbuf[idx] = src[idx];
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(rowp + (size_t(sp0) << S));
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      reinterpret_cast<ulonglong2*>(sbuf)[tid + r * T] = src[tid + r * T];
   }
   __syncthreads();
 #pragma unroll
   for (int gi = 0; gi < NG; ++gi) {
     const int grp = INV ? NG - 1 - gi : gi;
     const int l = 3 * grp;
-    const int k = S - l < 3 ? S - l : 3;   // levels in this group
-    const int ubits = S - l - k;           // log2 of units per group
-    const int per = 8 >> k;                // units per thread
+    const int k = S - l < 3 ? S - l : 3;  // levels in this group
+    const int ubits = S - l - k;          // log2 of units per group
+    const int per = 8 >> k;               // units per thread
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (q >= per) break;
-      const int uid = threadIdx.x + q * T;
+      const int uid = tid + q * T;
       int c, h, u;
       if (STRIDED) {
         c = uid & (C - 1);
-        const int rest = uid >> a.log_c;
+        const int rest = uid >> LOGC;
         u = rest & ((1 << ubits) - 1);
         h = rest >> ubits;
       } else {
@@ -124,49 +134,59 @@ __global__ void __launch_bounds__(512) ntt_pass_kernel(PassArgs a) {
         h = (uid >> ubits) & ((1 << l) - 1);
         c = uid >> (ubits + l);
       }
-      const int gsub = STRIDED ? 0 : sp0 + c;
       const int e0 = (h << (S - l)) + u;
-      const int stride = 1 << ubits;
       uint64_t x[8];
 #pragma unroll
       for (int v = 0; v < 8; ++v)
         if (v < (1 << k)) {
-          const int e = e0 + v * stride;
-          x[v] = sbuf[STRIDED ? (e << a.log_c) + c : (c << S) + e];
+          const int e = e0 + (v << ubits);
+          x[v] = sbuf[STRIDED ? (e << LOGC) + c : (c << S) + e];
         }
+      // twiddle of group hh at local level l + i
+      auto tw_at = [&](int i, int blk, uint64_t& w, uint64_t& wq) {
+        if (STRIDED) {
+          const int t = (1 << (l + i)) + (h << i) + blk;
+          w = stw[2 * t];
+          wq = stw[2 * t + 1];
+        } else {
+          const Twiddle tt =
+              twr[(size_t((1 << a.st0) + sp0 + c) << (l + i)) + (size_t(h) << i) + blk];
+          w = tt.w;
+          wq = tt.wq;
+        }
+      };
       if (!INV) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           if (i < k) {
             const int half = 1 << (k - i - 1);
-            const size_t tb = (size_t(m0 + gsub) << (l + i)) + (size_t(h) << i);
 #pragma unroll
             for (int blk = 0; blk < 4; ++blk)
               if (blk < (1 << i)) {
-                const Twiddle w = twr[tb + blk];
+                uint64_t w, wq;
+                tw_at(i, blk, w, wq);
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                   if (r < half)
-                    ct_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, p2, negp);
+                    ct_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, wq, p4, negp);
               }
           }
         }
         if (a.last && grp == NG - 1) {
 #pragma unroll
           for (int v = 0; v < 8; ++v)
-            if (v < (1 << k)) x[v] = reduce_4p(x[v], p);
+            if (v < (1 << k)) x[v] = reduce_4p(csub(x[v], p4), p);  // [0, 8p) -> [0, p)
         }
       } else {
 #pragma unroll
         for (int ii = 2; ii >= 0; --ii) {
           if (ii < k) {
             const int half = 1 << (k - ii - 1);
-            const int L = a.st0 + l + ii;
-            const size_t tb = (size_t(m0 + gsub) << (l + ii)) + (size_t(h) << ii);
+            const bool level0 = STRIDED && l + ii == 0 && a.last;
 #pragma unroll
             for (int blk = 0; blk < 4; ++blk)
               if (blk < (1 << ii)) {
-                if (L == 0 && a.last) {
+                if (level0) {
                   // level 0 with n^-1 folded in: a' = (u+v) n^-1,
                   // b' = (u-v) itw[1] n^-1, outputs canonical
 #pragma unroll
@@ -175,14 +195,16 @@ __global__ void __launch_bounds__(512) ntt_pass_kernel(PassArgs a) {
                       const int i0 = blk * 2 * half + r;
                       const uint64_t uu = x[i0], vv = x[i0 + half];
                       x[i0] = shoup_mul(uu + vv, pr.ninv, pr.ninv_q, p);
-                      x[i0 + half] = shoup_mul(uu + p2 - vv, pr.w1n, pr.w1n_q, p);
+                      x[i0 + half] = shoup_mul(uu + p4 - vv, pr.w1n, pr.w1n_q, p);
                     }
                 } else {
-                  const Twiddle w = twr[tb + blk];
+                  uint64_t w, wq;
+                  tw_at(ii, blk, w, wq);
 #pragma unroll
                   for (int r = 0; r < 4; ++r)
                     if (r < half)
-                      gs_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, p2, negp);
+                      gs_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, wq, p4,
+                              negp);
                 }
               }
           }
@@ -191,21 +213,24 @@ __global__ void __launch_bounds__(512) ntt_pass_kernel(PassArgs a) {
 #pragma unroll
       for (int v = 0; v < 8; ++v)
         if (v < (1 << k)) {
-          const int e = e0 + v * stride;
-          sbuf[STRIDED ? (e << a.log_c) + c : (c << S) + e] = x[v];
+          const int e = e0 + (v << ubits);
+          sbuf[STRIDED ? (e << LOGC) + c : (c << S) + e] = x[v];
         }
     }
     __syncthreads();
   }
   // ---- store --------------------------------------------------------------
   if (STRIDED) {
-    for (int idx = threadIdx.x; idx < elems; idx += T) {
-      const int e = idx >> a.log_c, c = idx & (C - 1);
-      rowp[size_t(e) * tlast + sp0 + c] = sbuf[idx];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int idx = tid + r * T;
+      rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))] = sbuf[idx];
     }
   } else {
-    uint64_t* dst = rowp + (size_t(sp0) << S);
-    for (int idx = threadIdx.x; idx < elems; idx += T) dst[idx] = sbuf[idx];
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(rowp + (size_t(sp0) << S));
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      dst[tid + r * T] = reinterpret_cast<const ulonglong2*>(sbuf)[tid + r * T];
   }
 }
 
@@ -219,76 +244,71 @@ void split_levels(int log_n, int& s1, int& s2) {
   }
 }
 
-template <int S, bool STRIDED, bool INV>
-cudaError_t launch_s(const PassArgs& a, size_t rows, int C, cudaStream_t st) {
+template <int S, int LOGC, bool STRIDED, bool INV>
+size_t smem_bytes() {
+  return sizeof(uint64_t) * ((size_t(1) << (S + LOGC)) + (STRIDED ? (size_t(2) << S) : 0));
+}
+
+template <int S, int LOGC, bool STRIDED, bool INV>
+cudaError_t launch_t(const PassArgs& a, size_t rows, cudaStream_t st) {
   const int subproblems = STRIDED ? (1 << (a.log_n - a.st0 - S)) : (1 << a.st0);
-  dim3 grid(subproblems / C, static_cast<unsigned>(rows));
-  const int threads = (C << S) / 8;
-  ntt_pass_kernel<S, STRIDED, INV><<<grid, threads, sizeof(uint64_t) * (C << S), st>>>(a);
+  dim3 grid(subproblems >> LOGC, static_cast<unsigned>(rows));
+  ntt_pass_kernel<S, LOGC, STRIDED, INV>
+      <<<grid, 1 << (S + LOGC - 3), smem_bytes<S, LOGC, STRIDED, INV>(), st>>>(a);
   return cudaGetLastError();
 }
 
-template <bool STRIDED, bool INV>
-cudaError_t launch_any(int S, const PassArgs& a, size_t rows, int C, cudaStream_t st) {
-  switch (S) {
-    case 3: return launch_s<3, STRIDED, INV>(a, rows, C, st);
-    case 4: return launch_s<4, STRIDED, INV>(a, rows, C, st);
-    case 5: return launch_s<5, STRIDED, INV>(a, rows, C, st);
-    case 6: return launch_s<6, STRIDED, INV>(a, rows, C, st);
-    case 7: return launch_s<7, STRIDED, INV>(a, rows, C, st);
-    case 8: return launch_s<8, STRIDED, INV>(a, rows, C, st);
-    case 9: return launch_s<9, STRIDED, INV>(a, rows, C, st);
-    case 10: return launch_s<10, STRIDED, INV>(a, rows, C, st);
-    case 11: return launch_s<11, STRIDED, INV>(a, rows, C, st);
-    default: return cudaErrorInvalidValue;
-  }
+// (S, LOGC) instances: 2-pass sizes use 4096-residue CTAs (LOGC = 12 - S),
+// single-pass transforms (logN <= 11) one row per CTA (LOGC = 0).
+template <bool STRIDED, bool INV, typename F>
+cudaError_t dispatch(int S, int logc, F&& f) {
+#define HEMUL_NTT_CASE(s, lc)                                          \
+  if (S == s && logc == lc) return f(ntt_pass_kernel<s, lc, STRIDED, INV>, \
+                                     launch_t<s, lc, STRIDED, INV>,   \
+                                     smem_bytes<s, lc, STRIDED, INV>());
+  HEMUL_NTT_CASE(6, 6) HEMUL_NTT_CASE(7, 5) HEMUL_NTT_CASE(8, 4) HEMUL_NTT_CASE(9, 3)
+  HEMUL_NTT_CASE(3, 0) HEMUL_NTT_CASE(4, 0) HEMUL_NTT_CASE(5, 0) HEMUL_NTT_CASE(6, 0)
+  HEMUL_NTT_CASE(7, 0) HEMUL_NTT_CASE(8, 0) HEMUL_NTT_CASE(9, 0) HEMUL_NTT_CASE(10, 0)
+  HEMUL_NTT_CASE(11, 0)
+#undef HEMUL_NTT_CASE
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_pass(bool inv, uint64_t* data, const Twiddle* tw, const DevPrime* primes, int np,
                         size_t rows, int log_n, int st0, int S, bool strided, bool last,
                         cudaStream_t st) {
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
-  PassArgs a{data, tw, primes, np, log_n, st0, 0, rpp, last ? 1 : 0};
-  const int subproblems = strided ? (1 << (log_n - st0 - S)) : (1 << st0);
-  int C = (1 << S) >= kPassElems ? 1 : kPassElems >> S;
-  if (C > subproblems) C = subproblems;
-  if ((C << S) / 8 > 512 || (C << S) < 8) return cudaErrorInvalidValue;
-  while ((1 << a.log_c) < C) ++a.log_c;
+  const PassArgs a{data, tw, primes, np, log_n, st0, rpp, last ? 1 : 0};
+  const int logc = log_n <= 11 ? 0 : kLogPassElems - S;
+  auto go = [&](auto kernel, auto launcher, size_t) { (void)kernel; return launcher(a, rows, st); };
   if (strided)
-    return inv ? launch_any<true, true>(S, a, rows, C, st)
-               : launch_any<true, false>(S, a, rows, C, st);
-  return inv ? launch_any<false, true>(S, a, rows, C, st)
-             : launch_any<false, false>(S, a, rows, C, st);
-}
-
-template <int S, bool STRIDED, bool INV>
-cudaError_t attr_s() {
-  return cudaFuncSetAttribute(ntt_pass_kernel<S, STRIDED, INV>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    return inv ? dispatch<true, true>(S, logc, go) : dispatch<true, false>(S, logc, go);
+  return inv ? dispatch<false, true>(S, logc, go) : dispatch<false, false>(S, logc, go);
 }
 
 template <bool STRIDED, bool INV>
-cudaError_t attr_all() {
-  cudaError_t e = cudaSuccess;
-  if ((e = attr_s<3, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<4, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<5, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<6, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<7, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<8, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<9, STRIDED, INV>()) != cudaSuccess) return e;
-  if ((e = attr_s<10, STRIDED, INV>()) != cudaSuccess) return e;
-  return attr_s<11, STRIDED, INV>();
+cudaError_t set_attrs() {
+  auto attr = [](auto kernel, auto, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes));
+  };
+  const int sizes[][2] = {{6, 6}, {7, 5}, {8, 4}, {9, 3}, {3, 0}, {4, 0}, {5, 0},
+                          {6, 0}, {7, 0}, {8, 0}, {9, 0}, {10, 0}, {11, 0}};
+  for (const auto& sz : sizes) {
+    cudaError_t e = dispatch<STRIDED, INV>(sz[0], sz[1], attr);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
 
 cudaError_t ntt_setup_attributes() {
   cudaError_t e;
-  if ((e = attr_all<true, false>()) != cudaSuccess) return e;
-  if ((e = attr_all<true, true>()) != cudaSuccess) return e;
-  if ((e = attr_all<false, false>()) != cudaSuccess) return e;
-  return attr_all<false, true>();
+  if ((e = set_attrs<true, false>()) != cudaSuccess) return e;
+  if ((e = set_attrs<true, true>()) != cudaSuccess) return e;
+  if ((e = set_attrs<false, false>()) != cudaSuccess) return e;
+  return set_attrs<false, true>();
 }
 
 int ntt_num_passes(int log_n) {

@@ -1,6 +1,11 @@
 // Integer-pipe roofline denominator: IMAD.WIDE.U32 throughput measured on the
-// device the context runs on (the HBM and bf16 peaks come from
-// MEASURED_PEAKS.json; no integer peak is recorded there).
+// device the context runs on (MEASURED_PEAKS.json records only HBM and bf16
+// peaks). The multiplier changes every iteration so ptxas cannot hoist the
+// products (a fixed multiplier gets strength-reduced into 64-bit adds); the
+// accumulate is split by ptxas into product + IADD3 on the ALU pipe, which
+// runs beside the FMA-heavy pipe. On B200 this measures ~27 IMAD.WIDE / clk
+// / SM (profiles/r01_pipe_probe.txt), the same pipe the iGEMM kernels load
+// (ncu sm__pipe_fmaheavy_cycles_active).
 #include <cuda_runtime.h>
 
 #include "kernels.hpp"
@@ -9,18 +14,19 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kIters = 4096;
+constexpr int kIters = 2048;
 
 __global__ void imad_probe_kernel(unsigned long long* out, unsigned seed) {
   unsigned a[8];
   unsigned long long acc[8];
-  const unsigned b = seed * 2654435761u + threadIdx.x;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     a[i] = seed + i * 77 + threadIdx.x;
     acc[i] = i;
   }
+  unsigned b = seed * 2654435761u + threadIdx.x;
   for (int it = 0; it < kIters; ++it) {
+    b += 0x9e3779b9u;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(a[i]), "r"(b));
