@@ -242,6 +242,7 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
+    from paper_2003_04510_b200.dist import gather_to_rank0, max_over_ranks
     from paper_2003_04510_b200.hemul import Context, ciphertext_digest, make_params
 
     torch.cuda.set_device(local)
@@ -311,10 +312,7 @@ def main() -> None:
     launches = ctx.launch_count() - launches0
     kstats = ctx.kernel_stats()
     ctx.enable_stage_timing(False)
-    if world > 1:
-        t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms = max_over_ranks(elapsed_ms, device="cuda")
     value = world * B * args.steps / (elapsed_ms / 1000.0)
     ms_per_step = elapsed_ms / args.steps
 
@@ -356,10 +354,7 @@ def main() -> None:
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms, device="cuda")
     e2e_value = world * B * e2e_steps / (e2e_ms / 1000.0)
     if not torch.equal(ho[0], out[0].cpu()):
         raise RuntimeError("e2e output differs from the device-resident output")
@@ -367,11 +362,7 @@ def main() -> None:
     # ---- result digests gathered to rank 0 (after timing) ------------------
     o0 = out[0][0].cpu().numpy(), out[1][0].cpu().numpy()
     dig = ciphertext_digest(q - p.log_p, o0[0], o0[1])
-    digests = [dig]
-    if world > 1:
-        buf = [None] * world
-        dist.all_gather_object(buf, dig)
-        digests = buf
+    digests = gather_to_rank0(dig) or []
 
     # ---- roofline of the dominant kernel class ----------------------------
     imad_peak = ctx.imad_peak()
