@@ -94,6 +94,10 @@ def work_per_step(p, np1: int, np2: int, B: int, log_q: int) -> dict[str, float]
         "intt_a": inv_rows * bf * s1 * SHOUP_IMAD + inv_rows * n * SHOUP_IMAD,
         "tensor": n * B * np1 * 4 * MULMOD_IMAD,
         "evk": n * B * np2 * 2 * MULMOD_IMAD,
+        "mid_r1": (4 * B * np1 * bf * s2 + 3 * B * np1 * bf * s2) * SHOUP_IMAD
+                  + n * B * np1 * 4 * MULMOD_IMAD,
+        "mid_r2": (B * np2 * bf * s2 + 2 * B * np2 * bf * s2) * SHOUP_IMAD
+                  + n * B * np2 * 2 * MULMOD_IMAD,
         "icrt": n * B * ((2 * np1 + 1) * chunks + np1 * SHOUP_IMAD),
         "finish": n * 2 * B * ((2 * np2 + 2 * np1 + 2) * fin_cols
                                + (np1 + np2) * SHOUP_IMAD),

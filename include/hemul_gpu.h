@@ -66,8 +66,8 @@ enum { HEMUL_STAGE_CRT = 0, HEMUL_STAGE_NTT, HEMUL_STAGE_INTT, HEMUL_STAGE_ICRT,
 /* Kernel classes for per-launch device timing (hemul_gpu_kernel_stats). */
 enum { HEMUL_KCLASS_CRT = 0, HEMUL_KCLASS_NTT_A, HEMUL_KCLASS_NTT_B, HEMUL_KCLASS_INTT_B,
        HEMUL_KCLASS_INTT_A, HEMUL_KCLASS_TENSOR, HEMUL_KCLASS_EVK, HEMUL_KCLASS_ICRT,
-       HEMUL_KCLASS_FINISH, HEMUL_KCLASS_EPILOGUE, HEMUL_KCLASS_H2D, HEMUL_KCLASS_D2H,
-       HEMUL_KCLASS_COUNT };
+       HEMUL_KCLASS_FINISH, HEMUL_KCLASS_MID_R1, HEMUL_KCLASS_MID_R2, HEMUL_KCLASS_EPILOGUE,
+       HEMUL_KCLASS_H2D, HEMUL_KCLASS_D2H, HEMUL_KCLASS_COUNT };
 
 /* make_params(log_p, depth, w64, log_n_override) (params.cpp:64-74) and a
  * context on CUDA device `device`. log_n_override = 0 uses the security table

@@ -303,19 +303,24 @@ void ensure(DevBuf& b, size_t bytes) {
 
 int limbs_of(int bits) { return (bits + 63) / 64; }
 
-// Forward NTT of `rows` rows, one launch per memory pass.
-void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage) {
-  for (int pass = 0; pass < ntt_num_passes(c->log_n); ++pass)
+// Forward NTT of `rows` rows, one launch per memory pass (only the first
+// `passes` of them when a fused middle pass follows).
+void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage,
+             int passes = 2) {
+  const int total = ntt_num_passes(c->log_n);
+  for (int pass = 0; pass < total && pass < passes; ++pass)
     run(c, stage, pass == 0 ? HEMUL_KCLASS_NTT_A : HEMUL_KCLASS_NTT_B, "NTT", [&] {
       return ntt_forward_pass(pass, data, rows, r.np, c->log_n, r.tw.as<Twiddle>(),
                               r.primes.as<DevPrime>(), c->stream);
     });
 }
 
-void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage) {
-  const int passes = ntt_num_passes(c->log_n);
-  for (int pass = 0; pass < passes; ++pass)
-    run(c, stage, pass + 1 == passes ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B, "iNTT", [&] {
+// Inverse NTT; passes = 1 runs only the final pass (after a fused middle pass).
+void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage,
+             int passes = 2) {
+  const int total = ntt_num_passes(c->log_n);
+  for (int pass = total > passes ? total - passes : 0; pass < total; ++pass)
+    run(c, stage, pass + 1 == total ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B, "iNTT", [&] {
       return ntt_inverse_pass(pass, data, rows, r.np, c->log_n, r.itw.as<Twiddle>(),
                               r.primes.as<DevPrime>(), c->stream);
     });
@@ -602,13 +607,25 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
       return crt_forward_multi(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
     });
-    ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
-    // pointwise products are booked under iCRT like rns.cpp:364;
     // in place: d2 -> A1, d0 -> B1, d1 -> A2
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "tensor product", [&] {
-      return tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
-    });
-    ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
+    const bool mid = ntt_has_mid(log_n);
+    if (mid) {
+      // forward pass A, then one fused pass: forward pass B + tensor product +
+      // inverse pass B, then inverse pass A
+      ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT, 1);
+      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R1, "NTT mid r1", [&] {
+        return ntt_mid_tensor(A1, B1, A2, B2, B, r1.np, log_n, r1.tw.as<Twiddle>(),
+                              r1.itw.as<Twiddle>(), p1, c->stream);
+      });
+      ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT, 1);
+    } else {
+      ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
+      // pointwise products are booked under iCRT like rns.cpp:364
+      run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "tensor product", [&] {
+        return tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
+      });
+      ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
+    }
     // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
     // and are reconstructed inside the finisher
     ensure(c->dpoly, B * poly_w * 8);
@@ -623,12 +640,21 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2", [&] {
       return crt_forward(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
     });
-    ntt_fwd(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
     const uint64_t* EA = lv.evk_a.as<uint64_t>();
     const uint64_t* EB = EA + size_t(r2.np) * n;
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
-        [&] { return evk_product(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
-    ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
+    if (mid) {
+      ntt_fwd(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT, 1);
+      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R2, "NTT mid r2", [&] {
+        return ntt_mid_evk(KA, EA, EB, KA, KB, B, r2.np, log_n, r2.tw.as<Twiddle>(),
+                           r2.itw.as<Twiddle>(), p2, c->stream);
+      });
+      ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1);
+    } else {
+      ntt_fwd(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
+      run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
+          [&] { return evk_product(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
+      ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
+    }
     // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
     // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
     const size_t ow = B * n * Lo;

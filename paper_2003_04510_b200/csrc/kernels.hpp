@@ -29,6 +29,20 @@ cudaError_t ntt_forward_pass(int pass, uint64_t* data, size_t rows, int np, int 
 cudaError_t ntt_inverse_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
                              const Twiddle* itw, const DevPrime* primes, cudaStream_t st);
 
+// Fused middle pass (two-pass sizes, logN 12..17): forward levels
+// [s1, logN) of every operand + the evaluation-domain product + inverse
+// levels [s1, logN) of the products, one read and one write per block.
+// Inputs come out of forward pass 0, outputs go into inverse pass 1.
+bool ntt_has_mid(int log_n);
+// Region 1: A1 B1 A2 B2 -> d2 (over A1), d0 (over B1), d1 = A1B2 + A2B1 (over A2).
+cudaError_t ntt_mid_tensor(uint64_t* A1, uint64_t* B1, uint64_t* A2, uint64_t* B2, size_t batch,
+                           int np, int log_n, const Twiddle* tw, const Twiddle* itw,
+                           const DevPrime* primes, cudaStream_t st);
+// Region 2: F -> F evk_a (KA), F evk_b (KB); KA may alias F.
+cudaError_t ntt_mid_evk(uint64_t* F, const uint64_t* ea, const uint64_t* eb, uint64_t* KA,
+                        uint64_t* KB, size_t batch, int np, int log_n, const Twiddle* tw,
+                        const Twiddle* itw, const DevPrime* primes, cudaStream_t st);
+
 // ---- integer-pipe peak probe (probe.cu) ------------------------------------
 // Measured IMAD.WIDE.U32 throughput of this device in ops/s (a dependent-free
 // stream of mad.wide.u32, 148 x 8 CTAs), and the SM clock it ran at (kHz).

@@ -234,6 +234,167 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3)) ntt_pass_kernel(PassArgs 
   }
 }
 
+// ---- fused middle pass: forward levels [s1, logN) + product + inverse ------
+//
+// The evaluation-domain product of the reference (pm_pointwise,
+// polymul.cpp:22-27 / rns_pointwise_mul rns.cpp:108-130, 360-371) sits
+// between the last forward levels and the first inverse levels, and both
+// act on the same contiguous 2^s2-point blocks. One CTA therefore loads a
+// block of every operand once, finishes the forward transforms, multiplies,
+// runs the first inverse levels and stores only the products' blocks:
+//   OP_TENSOR (region 1): A1 B1 A2 B2 -> d2 = A1A2, d0 = B1B2,
+//                         d1 = A1B2 + A2B1 (written over A1, B1, A2)
+//   OP_EVK    (region 2): F, evk_a, evk_b -> F evk_a, F evk_b
+// Each twiddle is loaded once per unit and reused for every operand.
+enum { OP_TENSOR = 0, OP_EVK = 1 };
+
+template <int S, int LOGC, int NOPS, bool INV>
+__device__ __forceinline__ void block_group(uint64_t* sb, int grp, int sp0, int m0,
+                                            const Twiddle* twr, uint64_t p4, uint64_t negp) {
+  constexpr int C = 1 << LOGC;
+  constexpr int T = (C << S) / 8;
+  constexpr int OPS = C << S;  // residues per operand in shared memory
+  const int l = 3 * grp;
+  const int k = S - l < 3 ? S - l : 3;
+  const int ubits = S - l - k;
+  const int per = 8 >> k;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q >= per) break;
+    const int uid = threadIdx.x + q * T;
+    const int u = uid & ((1 << ubits) - 1);
+    const int h = (uid >> ubits) & ((1 << l) - 1);
+    const int c = uid >> (ubits + l);
+    const int e0 = (c << S) + (h << (S - l)) + u;
+    uint64_t w[7], wq[7];
+    const size_t g = size_t(m0 + sp0 + c);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (i < k)
+#pragma unroll
+        for (int blk = 0; blk < 4; ++blk)
+          if (blk < (1 << i)) {
+            const Twiddle t = twr[(g << (l + i)) + (size_t(h) << i) + blk];
+            w[(1 << i) - 1 + blk] = t.w;
+            wq[(1 << i) - 1 + blk] = t.wq;
+          }
+#pragma unroll
+    for (int op = 0; op < NOPS; ++op) {
+      uint64_t x[8];
+      uint64_t* base = sb + op * OPS + e0;
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        if (v < (1 << k)) x[v] = base[v << ubits];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int i = INV ? 2 - s : s;
+        if (i < k) {
+          const int half = 1 << (k - i - 1);
+#pragma unroll
+          for (int blk = 0; blk < 4; ++blk)
+            if (blk < (1 << i))
+#pragma unroll
+              for (int r = 0; r < 4; ++r)
+                if (r < half) {
+                  const int a = blk * 2 * half + r;
+                  if (INV)
+                    gs_bfly(x[a], x[a + half], w[(1 << i) - 1 + blk], wq[(1 << i) - 1 + blk], p4,
+                            negp);
+                  else
+                    ct_bfly(x[a], x[a + half], w[(1 << i) - 1 + blk], wq[(1 << i) - 1 + blk], p4,
+                            negp);
+                }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        if (v < (1 << k)) base[v << ubits] = x[v];
+    }
+  }
+}
+
+struct MidArgs {
+  uint64_t* in[4];          // operand rows (batch x np x n each)
+  const uint64_t* evk[2];   // OP_EVK: evk forms, np x n each (shared by the batch)
+  uint64_t* out[3];         // product rows (batch x np x n each)
+  const Twiddle* tw;
+  const Twiddle* itw;
+  const DevPrime* primes;
+  int np, log_n, s1, rows_per_prime;
+};
+
+template <int S, int LOGC, int OP>
+__global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs a) {
+  constexpr int C = 1 << LOGC;
+  constexpr int ELEMS = C << S;
+  constexpr int T = ELEMS / 8;
+  constexpr int NG = (S + 2) / 3;
+  constexpr int NIN = OP == OP_TENSOR ? 4 : 1;
+  constexpr int NOUT = OP == OP_TENSOR ? 3 : 2;
+  extern __shared__ uint64_t sb[];  // NIN operands, products reuse the slots
+  const int j = blockIdx.y / a.rows_per_prime;
+  const int b = blockIdx.y - j * a.rows_per_prime;
+  const DevPrime& pr = a.primes[j];
+  const uint64_t p = pr.p, p4 = 4 * p, negp = 0 - p;
+  const size_t n = size_t(1) << a.log_n;
+  const size_t row_off = (size_t(b) * a.np + j) * n;
+  const int sp0 = blockIdx.x << LOGC;
+  const size_t blk_off = size_t(sp0) << S;
+  const int m0 = 1 << a.s1;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int op = 0; op < NIN; ++op) {
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(a.in[op] + row_off + blk_off);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      reinterpret_cast<ulonglong2*>(sb + op * ELEMS)[tid + r * T] = src[tid + r * T];
+  }
+  __syncthreads();
+  const Twiddle* twr = a.tw + size_t(j) * n;
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    block_group<S, LOGC, NIN, false>(sb, gi, sp0, m0, twr, p4, negp);
+    __syncthreads();
+  }
+  // evaluation-domain products (values in [0, 8p): 64-bit products < 2^126)
+  const uint64_t one_q = pr.one_q, beta = pr.beta, beta_q = pr.beta_q;
+  const uint64_t* ea = OP == OP_EVK ? a.evk[0] + size_t(j) * n + blk_off : nullptr;
+  const uint64_t* eb = OP == OP_EVK ? a.evk[1] + size_t(j) * n + blk_off : nullptr;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int e = tid + r * T;
+    if (OP == OP_TENSOR) {
+      const uint64_t x1 = sb[e], y1 = sb[ELEMS + e], x2 = sb[2 * ELEMS + e],
+                     y2 = sb[3 * ELEMS + e];
+      const uint64_t d2 = mulmod(x1, x2, p, one_q, beta, beta_q);
+      const uint64_t d0 = mulmod(y1, y2, p, one_q, beta, beta_q);
+      const uint64_t d1 = add_mod(mulmod(x1, y2, p, one_q, beta, beta_q),
+                                  mulmod(x2, y1, p, one_q, beta, beta_q), p);
+      sb[e] = d2;
+      sb[ELEMS + e] = d0;
+      sb[2 * ELEMS + e] = d1;
+    } else {
+      const uint64_t f = sb[e];
+      sb[e] = mulmod(f, ea[e], p, one_q, beta, beta_q);
+      sb[ELEMS + e] = mulmod(f, eb[e], p, one_q, beta, beta_q);
+    }
+  }
+  __syncthreads();
+  const Twiddle* itwr = a.itw + size_t(j) * n;
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    block_group<S, LOGC, NOUT, true>(sb, NG - 1 - gi, sp0, m0, itwr, p4, negp);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int op = 0; op < NOUT; ++op) {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(a.out[op] + row_off + blk_off);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      dst[tid + r * T] = reinterpret_cast<const ulonglong2*>(sb + op * ELEMS)[tid + r * T];
+  }
+}
+
 void split_levels(int log_n, int& s1, int& s2) {
   if (log_n <= 11) {
     s1 = log_n;
@@ -309,6 +470,90 @@ cudaError_t ntt_setup_attributes() {
   if ((e = set_attrs<true, true>()) != cudaSuccess) return e;
   if ((e = set_attrs<false, false>()) != cudaSuccess) return e;
   return set_attrs<false, true>();
+}
+
+namespace {
+
+constexpr int kMidLogElems = 11;  // residues per operand per CTA (2048)
+
+template <int S, int OP>
+cudaError_t launch_mid(const MidArgs& a, size_t rows, cudaStream_t st) {
+  constexpr int LOGC = kMidLogElems - S;
+  constexpr int NSLOT = OP == OP_TENSOR ? 4 : 2;
+  const size_t smem = sizeof(uint64_t) * NSLOT * (size_t(1) << kMidLogElems);
+  static bool attr = false;  // one-time opt-in above 48 KB
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ntt_mid_kernel<S, LOGC, OP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((1 << a.s1) >> LOGC, static_cast<unsigned>(rows));
+  ntt_mid_kernel<S, LOGC, OP><<<grid, (1 << kMidLogElems) / 8, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int OP>
+cudaError_t launch_mid_any(const MidArgs& a, int s2, size_t rows, cudaStream_t st) {
+  switch (s2) {
+    case 6: return launch_mid<6, OP>(a, rows, st);
+    case 7: return launch_mid<7, OP>(a, rows, st);
+    case 8: return launch_mid<8, OP>(a, rows, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+bool ntt_has_mid(int log_n) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  return s2 >= 6 && s2 <= 8;
+}
+
+cudaError_t ntt_mid_tensor(uint64_t* A1, uint64_t* B1, uint64_t* A2, uint64_t* B2, size_t batch,
+                           int np, int log_n, const Twiddle* tw, const Twiddle* itw,
+                           const DevPrime* primes, cudaStream_t st) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  MidArgs a{};
+  a.in[0] = A1;
+  a.in[1] = B1;
+  a.in[2] = A2;
+  a.in[3] = B2;
+  a.out[0] = A1;  // d2
+  a.out[1] = B1;  // d0
+  a.out[2] = A2;  // d1
+  a.tw = tw;
+  a.itw = itw;
+  a.primes = primes;
+  a.np = np;
+  a.log_n = log_n;
+  a.s1 = s1;
+  a.rows_per_prime = static_cast<int>(batch);
+  return launch_mid_any<OP_TENSOR>(a, s2, batch * np, st);
+}
+
+cudaError_t ntt_mid_evk(uint64_t* F, const uint64_t* ea, const uint64_t* eb, uint64_t* KA,
+                        uint64_t* KB, size_t batch, int np, int log_n, const Twiddle* tw,
+                        const Twiddle* itw, const DevPrime* primes, cudaStream_t st) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  MidArgs a{};
+  a.in[0] = F;
+  a.evk[0] = ea;
+  a.evk[1] = eb;
+  a.out[0] = KA;
+  a.out[1] = KB;
+  a.tw = tw;
+  a.itw = itw;
+  a.primes = primes;
+  a.np = np;
+  a.log_n = log_n;
+  a.s1 = s1;
+  a.rows_per_prime = static_cast<int>(batch);
+  return launch_mid_any<OP_EVK>(a, s2, batch * np, st);
 }
 
 int ntt_num_passes(int log_n) {

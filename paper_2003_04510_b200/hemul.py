@@ -42,7 +42,8 @@ HEMUL_E_NO_EVK = 6
 
 STAGES = ("crt", "ntt", "intt", "icrt", "extra")  # counters.hpp:13
 KERNEL_CLASSES = ("crt", "ntt_a", "ntt_b", "intt_b", "intt_a", "tensor", "evk", "icrt",
-                  "finish", "epilogue", "h2d", "d2h")  # HEMUL_KCLASS_* in include/hemul_gpu.h
+                  "finish", "mid_r1", "mid_r2", "epilogue", "h2d",
+                  "d2h")  # HEMUL_KCLASS_* in include/hemul_gpu.h
 
 
 class HemulGpuError(RuntimeError):
