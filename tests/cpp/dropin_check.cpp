@@ -1,0 +1,150 @@
+// Drop-in check: code written against the reference's C++ API (namespace
+// hemul, include/hemul/*.hpp) compiled against libhemul_gpu.so.
+//
+//   dropin_check keys  <log_p> <depth> <log_n> <seed> <out_prefix>   (CPU only)
+//       bench-protocol keygen/encode/encrypt (bench.cpp:60-67); writes
+//       c1ax c1bx c2ax c2bx evkax evkbx as raw little-endian u64 files
+//   dropin_check bench <log_p> <depth> <log_n> <seed> <reps>          (GPU)
+//       run_he_mul_bench; prints "digest <hex>" and the table
+//   dropin_check ladder <log_p> <depth> <log_n> <seed>                (GPU)
+//       test_heaan.cpp:143-167: he_mul down the modulus chain, decrypting
+//       and decoding after each step; prints "max_err <e>"; exit 1 on > 1e-3
+//   dropin_check errors                                                (GPU)
+//       test_heaan.cpp:169-182: modulus mismatch / exhausted depth throw
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "hemul/bench.hpp"
+#include "hemul/heaan.hpp"
+
+using namespace hemul;
+
+namespace {
+
+Message random_message(int slots, Rng& rng) {
+  Message m;
+  m.slots.resize(slots);
+  for (auto& s : m.slots) {
+    const double re = static_cast<double>(rng.next() >> 11) * 0x1p-53 * 2 - 1;
+    const double im = static_cast<double>(rng.next() >> 11) * 0x1p-53 * 2 - 1;
+    s = {re, im};
+  }
+  return m;
+}
+
+double max_err(const Message& a, const Message& b) {
+  double e = 0;
+  for (size_t i = 0; i < a.slots.size(); ++i) e = std::max(e, std::abs(a.slots[i] - b.slots[i]));
+  return e;
+}
+
+void write_poly(const std::string& path, const BigPoly& p) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot write " + path);
+  std::fwrite(p.data.data(), sizeof(uint64_t), p.data.size(), f);
+  std::fclose(f);
+}
+
+int cmd_keys(int log_p, int depth, int log_n, uint64_t seed, const std::string& out) {
+  const Params p = make_params(log_p, depth, WordSize::w64, log_n);
+  Scheme sch(p);
+  Rng rng(seed);
+  const int ns = std::min(64, p.n / 2);
+  const KeySet keys = sch.keygen(rng);
+  const Plaintext t1 = sch.encode(random_message(ns, rng));
+  const Plaintext t2 = sch.encode(random_message(ns, rng));
+  const Ciphertext c1 = sch.encrypt(t1, keys.pk, rng);
+  const Ciphertext c2 = sch.encrypt(t2, keys.pk, rng);
+  write_poly(out + "c1ax", c1.ax);
+  write_poly(out + "c1bx", c1.bx);
+  write_poly(out + "c2ax", c2.ax);
+  write_poly(out + "c2bx", c2.bx);
+  write_poly(out + "evkax", keys.evk.ax);
+  write_poly(out + "evkbx", keys.evk.bx);
+  return 0;
+}
+
+int cmd_bench(int log_p, int depth, int log_n, uint64_t seed, int reps) {
+  BenchConfig cfg;
+  cfg.seed = seed;
+  cfg.reps = reps;
+  const BenchReport r = run_he_mul_bench(make_params(log_p, depth, WordSize::w64, log_n), cfg, nullptr);
+  std::printf("digest %016llx\n%s", static_cast<unsigned long long>(r.result_digest),
+              bench_table(r).c_str());
+  return 0;
+}
+
+int cmd_ladder(int log_p, int depth, int log_n, uint64_t seed) {
+  const Params p = make_params(log_p, depth, WordSize::w64, log_n);
+  Scheme sch(p);
+  Rng rng(seed);
+  const KeySet keys = sch.keygen(rng);
+  Message want = random_message(8, rng);
+  Ciphertext acc = sch.encrypt(sch.encode(want), keys.pk, rng);
+  double worst = 0;
+  for (int step = 0; step < depth - 2; ++step) {
+    const Message m = random_message(8, rng);
+    Ciphertext c = sch.encrypt(sch.encode(m), keys.pk, rng);
+    if (c.log_q > acc.log_q) {  // align moduli before multiplying
+      c.ax = poly_mod_down(c.ax, acc.log_q);
+      c.bx = poly_mod_down(c.bx, acc.log_q);
+      c.log_q = acc.log_q;
+    }
+    acc = sch.he_mul(acc, c, keys.evk);
+    for (size_t i = 0; i < want.slots.size(); ++i) want.slots[i] *= m.slots[i];
+    worst = std::max(worst, max_err(sch.decode(sch.decrypt(acc, keys.sk)), want));
+  }
+  std::printf("max_err %.3e final_log_q %d\n", worst, acc.log_q);
+  return worst < 1e-3 && acc.log_q == p.log_q_max - (depth - 2) * p.log_p ? 0 : 1;
+}
+
+int cmd_errors() {
+  const Params p = make_params(30, 4, WordSize::w64, 10);
+  Scheme sch(p);
+  Rng rng(8);
+  const KeySet keys = sch.keygen(rng);
+  const Message m = random_message(4, rng);
+  const Ciphertext c1 = sch.encrypt(sch.encode(m), keys.pk, rng);
+  const Ciphertext c2 = sch.encrypt(sch.encode(m), keys.pk, rng);
+  const Ciphertext d1 = sch.he_mul(c1, c2, keys.evk);
+  int fails = 0;
+  try {
+    sch.he_mul(d1, c1, keys.evk);
+    ++fails;
+  } catch (const std::invalid_argument&) {
+  }
+  const Ciphertext d2 = sch.he_mul(d1, d1, keys.evk);
+  const Ciphertext d3 = sch.he_mul(d2, d2, keys.evk);
+  try {
+    sch.he_mul(d3, d3, keys.evk);
+    ++fails;
+  } catch (const std::runtime_error&) {
+  }
+  std::printf("error checks %s\n", fails ? "FAILED" : "ok");
+  return fails;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  try {
+    const std::string cmd = argc > 1 ? argv[1] : "";
+    auto arg = [&](int i) { return std::atoi(argv[i]); };
+    if (cmd == "keys" && argc == 7)
+      return cmd_keys(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10), argv[6]);
+    if (cmd == "bench" && argc == 7)
+      return cmd_bench(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10), arg(6));
+    if (cmd == "ladder" && argc == 6)
+      return cmd_ladder(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10));
+    if (cmd == "errors") return cmd_errors();
+    std::fprintf(stderr, "usage: see the header of tests/cpp/dropin_check.cpp\n");
+    return 2;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 3;
+  }
+}
