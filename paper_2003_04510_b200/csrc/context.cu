@@ -109,6 +109,8 @@ struct hemul_gpu_ctx {
   int log_n = 0, n = 0, log_p = 0, depth = 0, log_q_max = 0;
   cudaStream_t stream = nullptr;      // where every launch goes
   cudaStream_t own_stream = nullptr;  // created by the context
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the host-buffer pipeline
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
   std::list<std::unique_ptr<Level>> cache;  // most recent first, capacity 2
   std::string err;
   uint64_t launches = 0;
@@ -171,19 +173,24 @@ hemul_status guarded(hemul_gpu_ctx* c, F&& f) {
 // bucket (counters.hpp:13, ScopedStageTimer counters.hpp:58-76) and to a
 // kernel class. Events are read back lazily (flush_marks).
 template <typename F>
-void run(hemul_gpu_ctx* c, int stage, int klass, const char* what, F&& f) {
+void run_on(hemul_gpu_ctx* c, cudaStream_t st, int stage, int klass, const char* what, F&& f) {
   cudaEvent_t a = nullptr;
   if (c->timing) {
     a = c->take_event();
-    check(cudaEventRecord(a, c->stream), "event");
+    check(cudaEventRecord(a, st), "event");
   }
   check(f(), what);
   if (klass < HEMUL_KCLASS_H2D) ++c->launches;
   if (c->timing) {
     cudaEvent_t b = c->take_event();
-    check(cudaEventRecord(b, c->stream), "event");
+    check(cudaEventRecord(b, st), "event");
     c->marks.push_back({stage, klass, c->call_id, a, b});
   }
+}
+
+template <typename F>
+void run(hemul_gpu_ctx* c, int stage, int klass, const char* what, F&& f) {
+  run_on(c, c->stream, stage, klass, what, f);
 }
 
 // Reads back every pending event pair: stage times of the latest he_mul and
@@ -194,6 +201,7 @@ void flush_marks(hemul_gpu_ctx* c) {
   bool fresh = false;
   for (auto& m : c->marks) {
     float ms = 0;
+    cudaEventSynchronize(m.b);  // copies run on their own streams
     cudaEventElapsedTime(&ms, m.a, m.b);
     if (m.call == c->call_id) {
       if (!fresh) {
@@ -382,6 +390,12 @@ void copy_out(hemul_gpu_ctx* c, const OutPair& o, uint64_t* oa, uint64_t* ob, si
   check(cudaStreamSynchronize(c->stream), "D2H");
 }
 
+void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
+                   const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx);
+void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
+                      const uint64_t* const src[4], bool dev_in, uint64_t* out_ax,
+                      uint64_t* out_bx, bool dev_out);
+
 }  // namespace
 
 extern "C" {
@@ -418,6 +432,14 @@ hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_overri
   if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return HEMUL_E_CUDA;
   c->stream = c->own_stream;
+  if (cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess)
+    return HEMUL_E_CUDA;
+  for (int s = 0; s < 2; ++s)
+    if (cudaEventCreateWithFlags(&c->ev_h2d[s], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_comp[s], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventDisableTiming) != cudaSuccess)
+      return HEMUL_E_CUDA;
   if (ntt_setup_attributes() != cudaSuccess || crt_setup_attributes() != cudaSuccess ||
       icrt_setup_attributes() != cudaSuccess)
     return HEMUL_E_CUDA;
@@ -435,6 +457,15 @@ void hemul_gpu_destroy(hemul_gpu_ctx* c) {
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   c->cache.clear();
+  cudaStreamSynchronize(c->h2d);
+  cudaStreamSynchronize(c->d2h);
+  for (int s = 0; s < 2; ++s) {
+    cudaEventDestroy(c->ev_h2d[s]);
+    cudaEventDestroy(c->ev_comp[s]);
+    cudaEventDestroy(c->ev_d2h[s]);
+  }
+  cudaStreamDestroy(c->h2d);
+  cudaStreamDestroy(c->d2h);
   cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -579,21 +610,63 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     if (evk_ax && evk_bx && (!lv.has_evk || evk_id == 0 || lv.evk_id != evk_id))
       set_evk_forms(c, lv, evk_ax, evk_bx, evk_id);
     if (!lv.has_evk) return fail(c, HEMUL_E_NO_EVK, "evaluation key not set for this level");
+    ++c->call_id;
+    const uint64_t* src[4] = {c1_ax, c1_bx, c2_ax, c2_bx};
+    bool dev_in = true;
+    for (const uint64_t* s : src) dev_in = dev_in && is_device(c, s);
+    const bool dev_out = is_device(c, out_ax) && is_device(c, out_bx);
+    if (dev_in && dev_out) {
+      he_mul_device(c, lv, log_q, batch, src, out_ax, out_bx);
+      return HEMUL_OK;
+    }
+    he_mul_pipelined(c, lv, log_q, batch, src, dev_in, out_ax, out_bx, dev_out);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_rescale(hemul_gpu_ctx* c, int log_q, size_t batch, const uint64_t* ax,
+                               const uint64_t* bx, uint64_t* out_ax, uint64_t* out_bx) {
+  if (!c) return HEMUL_E_ARG;
+  // heaan.cpp:329-330
+  if (log_q - c->log_p < c->log_p)
+    return fail(c, HEMUL_E_DEPTH, "modulus exhausted; cannot rescale");
+  if (batch == 0) return HEMUL_OK;
+  if (!ax || !bx || !out_ax || !out_bx) return fail(c, HEMUL_E_ARG, "null buffer");
+  return guarded(c, [&]() -> hemul_status {
     const size_t n = size_t(c->n);
-    const int log_n = c->log_n, log_Q = c->log_q_max, log_p = c->log_p;
-    const int L = limbs_of(log_q), L2 = limbs_of(log_q + log_Q), Lo = limbs_of(log_q - log_p);
+    const int L = limbs_of(log_q), Lo = limbs_of(log_q - c->log_p);
+    const size_t w = batch * n * L, ow = batch * n * Lo;
+    ensure(c->rescale_buf, 2 * w * 8);
+    const uint64_t* a = stage_in(c, ax, w, c->rescale_buf.as<uint64_t>());
+    const uint64_t* b = stage_in(c, bx, w, c->rescale_buf.as<uint64_t>() + w);
+    const OutPair o = out_pair(c, out_ax, out_bx, ow, c->outb);
+    for (int t = 0; t < 2; ++t)
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "rescale", [&] {
+        return shift_right(t ? b : a, t ? o.b : o.a, batch, c->log_n, log_q, c->log_p,
+                           c->stream);
+      });
+    copy_out(c, o, out_ax, out_bx, ow);
+    return HEMUL_OK;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// One batched HE Mul on device buffers, every launch on c->stream.
+void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
+                   const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx) {
+  {
+    const size_t n = size_t(c->n);
+    const int log_n = c->log_n;
+    const int L = limbs_of(log_q);
     const RegionDev& r1 = lv.r1;
     const RegionDev& r2 = lv.r2;
     const size_t B = batch;
     const size_t poly_w = n * L;
     const DevPrime* p1 = r1.primes.as<DevPrime>();
     const DevPrime* p2 = r2.primes.as<DevPrime>();
-    ++c->call_id;
-    // ---- inputs ----------------------------------------------------------
-    ensure(c->in, 4 * B * poly_w * 8);
-    const uint64_t* src[4] = {c1_ax, c1_bx, c2_ax, c2_bx};
-    const uint64_t* in[4];
-    for (int t = 0; t < 4; ++t) in[t] = stage_in(c, src[t], B * poly_w, c->in.as<uint64_t>() + t * B * poly_w);
     // ---- region 1: d0 = bx1 bx2, d1 = ax1 bx2 + ax2 bx1, d2 = ax1 ax2 ---------
     const size_t r1w = B * r1.np * n;  // one RNS operand
     ensure(c->r1, 4 * r1w * 8);
@@ -657,8 +730,6 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     }
     // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
     // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
-    const size_t ow = B * n * Lo;
-    const OutPair o = out_pair(c, out_ax, out_bx, ow, c->outb);
     IcrtFlags flags;
     flags.capacity = static_cast<unsigned>(2 * B * n);
     ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
@@ -666,40 +737,76 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     flags.ids = flags.count + 1;
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
       return finish_keyswitch(KA, A2 /* d1 */, B1 /* d0 */, B, log_n, p2, r2.np, p1, r1.np,
-                              lv.fin, r2.icrt, r1.icrt, o.a, o.b, flags, c->force_exact,
+                              lv.fin, r2.icrt, r1.icrt, out_ax, out_bx, flags, c->force_exact,
                               c->stream);
     });
     ++c->launches;  // the (normally empty) exact fix-up kernel
-    copy_out(c, o, out_ax, out_bx, ow);
-    return HEMUL_OK;
-  });
+  }
 }
 
-hemul_status hemul_gpu_rescale(hemul_gpu_ctx* c, int log_q, size_t batch, const uint64_t* ax,
-                               const uint64_t* bx, uint64_t* out_ax, uint64_t* out_bx) {
-  if (!c) return HEMUL_E_ARG;
-  // heaan.cpp:329-330
-  if (log_q - c->log_p < c->log_p)
-    return fail(c, HEMUL_E_DEPTH, "modulus exhausted; cannot rescale");
-  if (batch == 0) return HEMUL_OK;
-  if (!ax || !bx || !out_ax || !out_bx) return fail(c, HEMUL_E_ARG, "null buffer");
-  return guarded(c, [&]() -> hemul_status {
-    const size_t n = size_t(c->n);
-    const int L = limbs_of(log_q), Lo = limbs_of(log_q - c->log_p);
-    const size_t w = batch * n * L, ow = batch * n * Lo;
-    ensure(c->rescale_buf, 2 * w * 8);
-    const uint64_t* a = stage_in(c, ax, w, c->rescale_buf.as<uint64_t>());
-    const uint64_t* b = stage_in(c, bx, w, c->rescale_buf.as<uint64_t>() + w);
-    const OutPair o = out_pair(c, out_ax, out_bx, ow, c->outb);
-    for (int t = 0; t < 2; ++t)
-      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "rescale", [&] {
-        return shift_right(t ? b : a, t ? o.b : o.a, batch, c->log_n, log_q, c->log_p,
-                           c->stream);
+// Host buffers: the batch runs in chunks through double-buffered device
+// staging so that the H2D copy of chunk k+1 and the D2H copy of chunk k-1
+// (two copy streams) overlap the kernels of chunk k (compute stream).
+void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
+                      const uint64_t* const src[4], bool dev_in, uint64_t* out_ax,
+                      uint64_t* out_bx, bool dev_out) {
+  const size_t n = size_t(c->n);
+  const size_t poly_w = n * limbs_of(log_q), out_w = n * limbs_of(log_q - c->log_p);
+  const size_t chunk = batch <= 1 ? 1 : (batch + 3) / 4;
+  const size_t chunks = (batch + chunk - 1) / chunk;
+  ensure(c->in, 2 * 4 * chunk * poly_w * 8);
+  ensure(c->outb, 2 * 2 * chunk * out_w * 8);
+  uint64_t* in_slot[2] = {c->in.as<uint64_t>(), c->in.as<uint64_t>() + 4 * chunk * poly_w};
+  uint64_t* out_slot[2] = {c->outb.as<uint64_t>(), c->outb.as<uint64_t>() + 2 * chunk * out_w};
+  for (size_t k = 0; k < chunks; ++k) {
+    const size_t b0 = k * chunk, bc = std::min(chunk, batch - b0);
+    const int s = static_cast<int>(k & 1);
+    // inputs: wait until chunk k-2 (same slot) finished computing
+    if (k >= 2) check(cudaStreamWaitEvent(c->h2d, c->ev_comp[s], 0), "wait");
+    const uint64_t* in[4];
+    for (int t = 0; t < 4; ++t) {
+      if (dev_in) {
+        in[t] = src[t] + b0 * poly_w;
+      } else {
+        uint64_t* d = in_slot[s] + t * chunk * poly_w;
+        run_on(c, c->h2d, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D", [&] {
+          return cudaMemcpyAsync(d, src[t] + b0 * poly_w, bc * poly_w * 8,
+                                 cudaMemcpyHostToDevice, c->h2d);
+        });
+        in[t] = d;
+      }
+    }
+    check(cudaEventRecord(c->ev_h2d[s], c->h2d), "event");
+    check(cudaStreamWaitEvent(c->stream, c->ev_h2d[s], 0), "wait");
+    // outputs: wait until chunk k-2's results left the slot
+    if (k >= 2 && !dev_out) check(cudaStreamWaitEvent(c->stream, c->ev_d2h[s], 0), "wait");
+    uint64_t* oa = dev_out ? out_ax + b0 * out_w : out_slot[s];
+    uint64_t* ob = dev_out ? out_bx + b0 * out_w : out_slot[s] + chunk * out_w;
+    he_mul_device(c, lv, log_q, bc, in, oa, ob);
+    check(cudaEventRecord(c->ev_comp[s], c->stream), "event");
+    if (!dev_out) {
+      check(cudaStreamWaitEvent(c->d2h, c->ev_comp[s], 0), "wait");
+      run_on(c, c->d2h, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(out_ax + b0 * out_w, oa, bc * out_w * 8, cudaMemcpyDeviceToHost,
+                               c->d2h);
       });
-    copy_out(c, o, out_ax, out_bx, ow);
-    return HEMUL_OK;
-  });
+      run_on(c, c->d2h, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(out_bx + b0 * out_w, ob, bc * out_w * 8, cudaMemcpyDeviceToHost,
+                               c->d2h);
+      });
+      check(cudaEventRecord(c->ev_d2h[s], c->d2h), "event");
+    }
+  }
+  // the call returns with the results in place (like the synchronous reference)
+  check(cudaStreamSynchronize(dev_out ? c->stream : c->d2h), "he_mul");
+  check(cudaStreamSynchronize(c->stream), "he_mul");
+  // later work on the caller's stream must see the copies done
+  if (!dev_out) check(cudaStreamWaitEvent(c->stream, c->ev_d2h[(chunks - 1) & 1], 0), "wait");
 }
+
+}  // namespace
+
+extern "C" {
 
 uint64_t hemul_ciphertext_digest(int log_q, size_t words, const uint64_t* ax,
                                  const uint64_t* bx) {
