@@ -26,7 +26,7 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kKT = 32;
+constexpr int kKT = 32;  // B rows per cp.async stage
 constexpr int kStages = 3;
 
 struct Inputs {
@@ -49,7 +49,11 @@ __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limb
   uint32_t* Bs = A + K * kGemmCoefs;                                        // ring
   uint64_t* raw = reinterpret_cast<uint64_t*>(Bs + kStages * kKT * NC);    // [32][limbs]
   const uint64_t* src = in.p[t] + (size_t(b) * n + c0) * limbs;
-  for (int idx = threadIdx.x; idx < kGemmCoefs * limbs; idx += blockDim.x) raw[idx] = src[idx];
+  // the CTA's limbs are one contiguous run: 16-byte cp.async copies
+  for (int idx = threadIdx.x; idx < kGemmCoefs * limbs / 2; idx += blockDim.x)
+    cp_async16(raw + 2 * idx, src + 2 * idx);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   for (int idx = threadIdx.x; idx < kGemmCoefs * K; idx += blockDim.x) {
     const int m = idx >> 5, c = idx & 31;

@@ -47,13 +47,34 @@ __device__ void build_rows(const Seg& s, size_t n, size_t c0, uint32_t* A, int r
                            double* part, IcrtFlags flags, size_t id0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double acc = 0;
-  for (int j = warp; j < s.np; j += nw) {
-    const DevPrime& pr = s.primes[j];
-    const uint64_t x = s.rns[size_t(j) * n + c0 + lane];
-    const uint64_t t = shoup_mul(x, pr.inv, pr.inv_q, pr.p);
-    A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
-    A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
-    acc += static_cast<double>(t) * pr.inv_p_dbl;
+  // batches of kBatch rows: all loads of a batch are issued before any use,
+  // so a warp keeps kBatch HBM requests in flight instead of one
+  constexpr int kBatch = 8;
+  for (int j0 = warp; j0 < s.np; j0 += kBatch * nw) {
+    uint64_t x[kBatch], inv[kBatch], inv_q[kBatch], p[kBatch];
+    double ip[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int j = j0 + u * nw;
+      if (j < s.np) {
+        x[u] = __ldcs(s.rns + size_t(j) * n + c0 + lane);  // streamed once
+        const DevPrime& pr = s.primes[j];
+        inv[u] = pr.inv;
+        inv_q[u] = pr.inv_q;
+        p[u] = pr.p;
+        ip[u] = pr.inv_p_dbl;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int j = j0 + u * nw;
+      if (j < s.np) {
+        const uint64_t t = shoup_mul(x[u], inv[u], inv_q[u], p[u]);
+        A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
+        A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
+        acc += static_cast<double>(t) * ip[u];
+      }
+    }
   }
   part[warp * 32 + lane] = acc;
   __syncthreads();
@@ -97,18 +118,58 @@ __device__ __forceinline__ uint64_t digits_window(const uint32_t* D, int ndig, i
   return r;
 }
 
-// One carry pass over a coefficient's column sums -> 25-bit digits, adding
-// 2^add0 and 2^add1 (the rounding halves; -1 = none) on the way.
-__device__ __forceinline__ void carry_pass(const uint64_t* S, uint32_t* D, int cols, int add0,
-                                           int add1) {
+// Carry pass of columns [m0, m1) of one coefficient's column sums -> 25-bit
+// digits, adding 2^add0 and 2^add1 (the rounding halves; -1 = none) on the
+// way; returns the carry out (S_m < 2^64 and carries < 2^40, so v fits).
+__device__ __forceinline__ uint64_t carry_pass(const uint64_t* S, uint32_t* D, int m0, int m1,
+                                               int add0, int add1) {
   uint64_t carry = 0;
-  for (int m = 0; m < cols; ++m) {
+  for (int m = m0; m < m1; ++m) {
     uint64_t v = S[m] + carry;
     if (add0 >= 0 && m == add0 / kDigit) v += uint64_t(1) << (add0 % kDigit);
     if (add1 >= 0 && m == add1 / kDigit) v += uint64_t(1) << (add1 % kDigit);
     D[m] = static_cast<uint32_t>(v) & kDigitMask;
     carry = v >> kDigit;
   }
+  return carry;
+}
+
+// Digits of all 32 coefficients of the CTA. With >= 128 threads each
+// coefficient's columns are cut into 4 segments carried in parallel; one
+// thread per coefficient then ripples each segment's carry into the next
+// (a carry < 2^41 changes ~2 digits unless they are all ones). co: 128 u64.
+__device__ void carry_digits(const uint64_t* S, int lds, uint32_t* D, int ldd, int cols,
+                             int add0, int add1, uint64_t* co) {
+  constexpr int kSeg = 4;
+  if (blockDim.x < kGemmCoefs * kSeg) {
+    if (threadIdx.x < kGemmCoefs)
+      carry_pass(S + threadIdx.x * lds, D + threadIdx.x * ldd, 0, cols, add0, add1);
+    __syncthreads();
+    return;
+  }
+  const int len = (cols + kSeg - 1) / kSeg;
+  if (threadIdx.x < kGemmCoefs * kSeg) {
+    const int c = threadIdx.x & 31, g = threadIdx.x >> 5;  // a warp per segment
+    const int m0 = g * len, m1 = min(cols, m0 + len);
+    co[g * 32 + c] =
+        m0 < m1 ? carry_pass(S + c * lds, D + c * ldd, m0, m1, add0, add1) : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGemmCoefs) {
+    const int c = threadIdx.x;
+    uint32_t* dc = D + c * ldd;
+    uint64_t cin = 0;
+    for (int g = 0; g < kSeg; ++g) {
+      const int m0 = g * len, m1 = min(cols, m0 + len);
+      for (int m = m0; m < m1 && cin; ++m) {
+        const uint64_t v = dc[m] + cin;
+        dc[m] = static_cast<uint32_t>(v) & kDigitMask;
+        cin = v >> kDigit;
+      }
+      cin += co[g * 32 + c];
+    }
+  }
+  __syncthreads();
 }
 
 template <int NW>
@@ -139,9 +200,7 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
     store_tile<NW>(S, lds, col0, t.m_pad, acc);
   }
   __syncthreads();
-  if (threadIdx.x < kGemmCoefs)
-    carry_pass(S + threadIdx.x * lds, D + threadIdx.x * ldd, t.m_out, -1, -1);
-  __syncthreads();
+  carry_digits(S, lds, D, ldd, t.m_out, -1, -1, reinterpret_cast<uint64_t*>(part));
   const int tl = (t.target_bits + 63) / 64;
   const uint64_t top = t.target_bits % 64 ? (uint64_t(1) << (t.target_bits % 64)) - 1 : ~0ull;
   uint64_t* dst = out + (size_t(b) * n + c0) * tl;
@@ -255,10 +314,11 @@ __global__ void __launch_bounds__(NW * 32) finish_kernel(
   uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * lds);  // [32][ldd]
   store_tile<NW>(S, lds, 0, f.cols_pad, acc);
   __syncthreads();
+  carry_digits(S, lds, D, ldd, f.cols, f.half_q_bit, f.half_p_bit,
+               reinterpret_cast<uint64_t*>(part));
   if (threadIdx.x < kGemmCoefs) {
     const int c = threadIdx.x;
     uint32_t* dc = D + c * ldd;
-    carry_pass(S + c * lds, dc, f.cols, f.half_q_bit, f.half_p_bit);
     // exact unless the 64 bits below the output are all ones (kernels.hpp)
     const bool amb = f.base > 0 && digits_window(dc, f.cols, f.out_bit - 64) == ~0ull;
     if (amb || force_exact) {
