@@ -1,0 +1,20 @@
+#!/bin/bash
+# ncu evidence for the X workload (run on the GPU box via gpurun, one GPU).
+# 1) launch list of a short bench (per-launch device times, cold & serialised)
+# 2) --set full capture of one launch of each he_mul kernel class
+set -u
+OUT=${1:-gpurun_out}
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --latency-reps 1"
+mkdir -p $OUT
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_X.csv $CMD > /dev/null 2>&1
+prof() {  # class kernel-regex launch-skip
+  ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o $OUT/prof_$1 $CMD > /dev/null 2>&1
+}
+prof crt crt_kernel 2
+prof ntt_a ntt_pass_kernel 2
+prof mid_r1 ntt_mid_kernel 0
+prof intt_a ntt_pass_kernel 3
+prof icrt icrt_kernel 0
+prof mid_r2 ntt_mid_kernel 1
+prof finish finish_kernel 0
+ls -la $OUT
