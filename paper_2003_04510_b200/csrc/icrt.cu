@@ -30,6 +30,11 @@ namespace {
 
 constexpr int kKT = 32;      // B rows per cp.async stage
 constexpr int kStages = 3;
+// the finisher: a smaller ring and <= 96 registers so 3 CTAs share an SM
+// (one CTA's prologue / carry pass overlaps the others' IMAD.WIDE loops)
+constexpr int kFinKT = 16;
+constexpr int kFinStages = 2;
+constexpr int kFinMinBlocks = 3;
 constexpr int kDigit = 25;   // B chunk width == output digit width
 constexpr uint32_t kDigitMask = (1u << kDigit) - 1;
 constexpr int kFixMaxLimbs = 136;
@@ -40,41 +45,35 @@ struct Seg {  // one RNS operand feeding A rows
   int np;
 };
 
-// A rows [row0, row0 + 2np + 1) for the CTA's 32 coefficients: the 30-bit
-// halves of t_j and the quotient k (warp w handles primes w, w+NW, ...; lane
-// = coefficient, so every x_j load is a coalesced 256-byte row segment).
-__device__ void build_rows(const Seg& s, size_t n, size_t c0, uint32_t* A, int row0,
-                           double* part, IcrtFlags flags, size_t id0) {
+// Stage the CTA's residues x_j (32 coefficients, 256 contiguous bytes per
+// prime) straight into the A rows they become: x row j occupies exactly the
+// bytes of A rows row0+2j and row0+2j+1, so every row is one batch of
+// 16-byte cp.async copies with all of them in flight at once. Commits a
+// cp.async group; build_rows waits for it.
+__device__ void stage_rows(const Seg& s, size_t n, size_t c0, uint32_t* A, int row0) {
+  uint64_t* dst = reinterpret_cast<uint64_t*>(A + row0 * kGemmCoefs);
+  for (int idx = threadIdx.x; idx < s.np * 16; idx += blockDim.x) {
+    const int j = idx >> 4, c = 2 * (idx & 15);
+    cp_async16(dst + 32 * j + c, s.rns + size_t(j) * n + c0 + c);
+  }
+}
+
+// A rows [row0, row0 + 2np + 1) for the CTA's 32 coefficients, in place over
+// the staged x rows: the 30-bit halves of t_j = x_j (P/p_j)^-1 mod p_j and
+// the quotient k (warp w converts primes w, w+NW, ...; lane = coefficient).
+__device__ void build_rows(const Seg& s, uint32_t* A, int row0, double* part, IcrtFlags flags,
+                           size_t id0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double acc = 0;
-  // batches of kBatch rows: all loads of a batch are issued before any use,
-  // so a warp keeps kBatch HBM requests in flight instead of one
-  constexpr int kBatch = 8;
-  for (int j0 = warp; j0 < s.np; j0 += kBatch * nw) {
-    uint64_t x[kBatch], inv[kBatch], inv_q[kBatch], p[kBatch];
-    double ip[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int j = j0 + u * nw;
-      if (j < s.np) {
-        x[u] = __ldcs(s.rns + size_t(j) * n + c0 + lane);  // streamed once
-        const DevPrime& pr = s.primes[j];
-        inv[u] = pr.inv;
-        inv_q[u] = pr.inv_q;
-        p[u] = pr.p;
-        ip[u] = pr.inv_p_dbl;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int j = j0 + u * nw;
-      if (j < s.np) {
-        const uint64_t t = shoup_mul(x[u], inv[u], inv_q[u], p[u]);
-        A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
-        A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
-        acc += static_cast<double>(t) * ip[u];
-      }
-    }
+  const uint64_t* xs = reinterpret_cast<const uint64_t*>(A + row0 * kGemmCoefs);
+  for (int j = warp; j < s.np; j += nw) {
+    const DevPrime& pr = s.primes[j];
+    const uint64_t x = xs[32 * j + lane];
+    __syncwarp();  // the whole row is read before any lane overwrites it
+    const uint64_t t = shoup_mul(x, pr.inv, pr.inv_q, pr.p);
+    A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
+    A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
+    acc += static_cast<double>(t) * pr.inv_p_dbl;
   }
   part[warp * 32 + lane] = acc;
   __syncthreads();
@@ -193,7 +192,11 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
   uint64_t* S = reinterpret_cast<uint64_t*>(part + NW * 32);       // [32][lds]
   uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * lds);  // [32][ldd]
   const Seg seg{rns + size_t(b) * np * n, primes, np};
-  build_rows(seg, n, c0, A, 0, part, flags, size_t(b) * n + c0);
+  stage_rows(seg, n, c0, A, 0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  build_rows(seg, A, 0, part, flags, size_t(b) * n + c0);
   for (int col0 = 0; col0 < t.m_pad; col0 += NC) {
     uint64_t acc[4][4] = {};
     igemm_32xN<NW, kKT, kStages>(A, K, t.btab, t.m_pad, col0, Bs, acc);
@@ -283,7 +286,7 @@ __global__ void icrt_fixup_kernel(const uint64_t* __restrict__ rns, int log_n,
 // ---- fused key-switch finisher ----------------------------------------------
 
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) finish_kernel(
+__global__ void __launch_bounds__(NW * 32, kFinMinBlocks) finish_kernel(
     const uint64_t* __restrict__ ks, const uint64_t* __restrict__ d_ax,
     const uint64_t* __restrict__ d_bx, int B, int log_n, const DevPrime* __restrict__ p2, int np2,
     const DevPrime* __restrict__ p1, int np1, Finisher f, uint64_t* __restrict__ out_ax,
@@ -299,14 +302,19 @@ __global__ void __launch_bounds__(NW * 32) finish_kernel(
   constexpr int NC = 16 * NW;
   uint32_t* A = reinterpret_cast<uint32_t*>(smem);
   uint32_t* Bs = A + K * kGemmCoefs;
-  double* part = reinterpret_cast<double*>(Bs + kStages * kKT * NC);
+  double* part = reinterpret_cast<double*>(Bs + kFinStages * kFinKT * NC);
   const Seg s2{ks + size_t(bb) * np2 * n, p2, np2};
   const Seg s1{(is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, p1, np1};
   const IcrtFlags none{};
-  build_rows(s2, n, c0, A, 0, part, none, 0);
-  build_rows(s1, n, c0, A, f.k2, part, none, 0);
+  stage_rows(s2, n, c0, A, 0);
+  stage_rows(s1, n, c0, A, f.k2);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  build_rows(s2, A, 0, part, none, 0);
+  build_rows(s1, A, f.k2, part, none, 0);
   uint64_t acc[4][4] = {};
-  igemm_32xN<NW, kKT, kStages>(A, K, f.btab, f.cols_pad, 0, Bs, acc);
+  igemm_32xN<NW, kFinKT, kFinStages>(A, K, f.btab, f.cols_pad, 0, Bs, acc);
   // a single column tile (cols_pad <= 16 NW): S and the digits reuse A; odd
   // row strides keep the one-row-per-lane carry pass conflict-free
   const int lds = f.cols_pad + 1, ldd = f.cols | 1;
@@ -406,7 +414,7 @@ size_t icrt_smem(int np, int m_pad) {
 template <int NW>
 size_t finish_smem(const Finisher& f) {
   const size_t main = size_t(f.k2 + f.k1) * kGemmCoefs * 4 +
-                      size_t(kStages) * kKT * 16 * NW * 4 + NW * 32 * 8;
+                      size_t(kFinStages) * kFinKT * 16 * NW * 4 + NW * 32 * 8;
   const size_t epi =
       size_t(kGemmCoefs) * (f.cols_pad + 1) * 8 + size_t(kGemmCoefs) * (f.cols | 1) * 4;
   return main > epi ? main : epi;
