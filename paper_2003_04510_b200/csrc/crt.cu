@@ -63,10 +63,11 @@ __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limb
     if (off > 39 && k + 1 < limbs) v |= l[k + 1] << (64 - off);
     A[idx] = static_cast<uint32_t>(v) & 0x1ffffffu;
   }
-  // (igemm_32xN synchronises before touching A)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cg = lane & 7, ng = lane >> 3;
   uint64_t* obase = out + size_t(t) * B * np * n + size_t(b) * np * n + c0 + 4 * cg;
+  // (igemm_32xN synchronises before touching A; the CTA-wide ring measured
+  // faster than per-warp rings here: 11 warps share each 704-byte B row)
   for (int col0 = 0; col0 < w.ld; col0 += NC) {
     uint64_t acc[4][4] = {};
     igemm_32xN<NW, kKT, kStages>(A, K, w.wtab, w.ld, col0, Bs, acc);

@@ -197,10 +197,11 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
   cp_async_wait<0>();
   __syncthreads();
   build_rows(seg, A, 0, part, flags, size_t(b) * n + c0);
+  uint32_t* Bw = Bs + (threadIdx.x >> 5) * kStages * kKT * 16;  // private B ring
   for (int col0 = 0; col0 < t.m_pad; col0 += NC) {
     uint64_t acc[4][4] = {};
-    igemm_32xN<NW, kKT, kStages>(A, K, t.btab, t.m_pad, col0, Bs, acc);
-    store_tile<NW>(S, lds, col0, t.m_pad, acc);
+    igemm_32x16_warp<kKT, kStages>(A, K, t.btab, t.m_pad, col0, Bw, acc);
+    store_tile<NW>(S, lds, col0, t.m_pad, acc);  // S does not alias A here
   }
   __syncthreads();
   carry_digits(S, lds, D, ldd, t.m_out, -1, -1, reinterpret_cast<uint64_t*>(part));
@@ -314,7 +315,9 @@ __global__ void __launch_bounds__(NW * 32, kFinMinBlocks) finish_kernel(
   build_rows(s2, A, 0, part, none, 0);
   build_rows(s1, A, f.k2, part, none, 0);
   uint64_t acc[4][4] = {};
-  igemm_32xN<NW, kFinKT, kFinStages>(A, K, f.btab, f.cols_pad, 0, Bs, acc);
+  igemm_32x16_warp<kFinKT, kFinStages>(A, K, f.btab, f.cols_pad, 0,
+                                       Bs + (threadIdx.x >> 5) * kFinStages * kFinKT * 16, acc);
+  __syncthreads();  // every warp is done with A before S overwrites it
   // a single column tile (cols_pad <= 16 NW): S and the digits reuse A; odd
   // row strides keep the one-row-per-lane carry pass conflict-free
   const int lds = f.cols_pad + 1, ldd = f.cols | 1;

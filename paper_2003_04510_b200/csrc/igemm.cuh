@@ -99,4 +99,63 @@ __device__ __forceinline__ void igemm_32xN(const uint32_t* __restrict__ As, int 
   __syncthreads();
 }
 
+// The same product with no CTA-wide barrier in the K loop: a warp only ever
+// reads its own 16 B columns, so each warp streams them through a private
+// cp.async ring (STAGES x KT rows x 64 bytes at Bw) and synchronises with
+// __syncwarp. Warps then run their IMAD.WIDE loops at their own pace instead
+// of meeting at a __syncthreads every tile. A (all K rows) must be complete
+// and visible (one __syncthreads) before the call; col0 is the CTA tile's
+// first column (the warp uses col0 + 16 * warp).
+template <int KT, int STAGES>
+__device__ __forceinline__ void igemm_32x16_warp(const uint32_t* __restrict__ As, int K,
+                                                 const uint32_t* __restrict__ Bg, int ldb,
+                                                 int col0, uint32_t* __restrict__ Bw,
+                                                 uint64_t (&acc)[4][4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cg = lane & 7, ng = lane >> 3;
+  const int colw = col0 + 16 * warp;
+  const int tiles = (K + KT - 1) / KT;
+  auto load = [&](int t) {
+    if (t < tiles) {
+      const int k0 = t * KT;
+      const int rows = min(KT, K - k0);
+      uint32_t* dst = Bw + (t % STAGES) * KT * 16;
+      for (int idx = lane; idx < rows * 4; idx += 32) {
+        const int r = idx >> 2, c = idx & 3;
+        cp_async16(dst + r * 16 + 4 * c, Bg + size_t(k0 + r) * ldb + colw + 4 * c);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) load(s);
+  const uint32_t* a_ptr = As + 4 * cg;
+  for (int t = 0; t < tiles; ++t) {
+    cp_async_wait<STAGES - 2>();
+    __syncwarp();
+    load(t + STAGES - 1);
+    const int k0 = t * KT;
+    const int rows = min(KT, K - k0);
+    const uint32_t* bt = Bw + (t % STAGES) * KT * 16 + 4 * ng;
+    const uint32_t* at = a_ptr + k0 * kGemmCoefs;
+    auto step = [&](int r) {
+      const uint4 a = *reinterpret_cast<const uint4*>(at + r * kGemmCoefs);
+      const uint4 b = *reinterpret_cast<const uint4*>(bt + r * 16);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] += static_cast<uint64_t>(av[i]) * bv[q];
+    };
+    if (rows == KT) {
+#pragma unroll 8
+      for (int r = 0; r < KT; ++r) step(r);
+    } else {
+      for (int r = 0; r < rows; ++r) step(r);
+    }
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+}
+
 }  // namespace hemul_gpu
