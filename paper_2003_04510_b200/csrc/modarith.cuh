@@ -25,13 +25,28 @@ __device__ __forceinline__ uint64_t wide(uint32_t a, uint32_t b) {
 // carries of the two cross terms' low halves are dropped (cf. word.hpp:45-51
 // approx_mulhi, which drops lo*lo the same way). 3 IMAD.WIDE + 1 add.
 __device__ __forceinline__ uint64_t mulhi_approx(uint64_t x, uint64_t y) {
-  const uint32_t x0 = lo32(x), x1 = hi32(x), y0 = lo32(y), y1 = hi32(y);
-  const uint64_t a = wide(x1, y0);
-  const uint64_t b = wide(x0, y1);
-  // the 33-bit sum of the high halves as the addend of the last IMAD.WIDE
-  // (avoids materialising {hi, 0} register pairs)
-  const uint64_t s = static_cast<uint64_t>(hi32(a)) + hi32(b);
-  return wide(x1, y1) + s;
+  // x1 y1 + hi(x1 y0) + hi(x0 y1): the 33-bit sum of the two high halves is
+  // formed with one add/addc pair and fed as the 64-bit addend of the last
+  // IMAD.WIDE (written in PTX so no {hi, 0} register pairs get materialised
+  // with moves on the FMA pipe)
+  uint64_t q;
+  asm("{\n\t"
+      ".reg .u32 x0, x1, y0, y1, al, ah, bl, bh, sl, sh;\n\t"
+      ".reg .u64 a, b, s;\n\t"
+      "mov.b64 {x0, x1}, %1;\n\t"
+      "mov.b64 {y0, y1}, %2;\n\t"
+      "mul.wide.u32 a, x1, y0;\n\t"
+      "mul.wide.u32 b, x0, y1;\n\t"
+      "mov.b64 {al, ah}, a;\n\t"
+      "mov.b64 {bl, bh}, b;\n\t"
+      "add.cc.u32 sl, ah, bh;\n\t"
+      "addc.u32 sh, 0, 0;\n\t"
+      "mov.b64 s, {sl, sh};\n\t"
+      "mad.wide.u32 %0, x1, y1, s;\n\t"
+      "}"
+      : "=l"(q)
+      : "l"(x), "l"(y));
+  return q;
 }
 
 // Exact floor(x*y / 2^64).
@@ -39,12 +54,27 @@ __device__ __forceinline__ uint64_t mulhi(uint64_t x, uint64_t y) { return __umu
 
 // x*y + q*(2^64 - p) mod 2^64 == x*y - q*p mod 2^64, in 2 IMAD.WIDE + 4 IMAD.
 __device__ __forceinline__ uint64_t mul_sub_lo(uint64_t x, uint64_t y, uint64_t q, uint64_t negp) {
-  const uint32_t x0 = lo32(x), x1 = hi32(x), y0 = lo32(y), y1 = hi32(y);
-  const uint32_t q0 = lo32(q), q1 = hi32(q), n0 = lo32(negp), n1 = hi32(negp);
-  const uint64_t r = wide(x0, y0) + wide(q0, n0);  // wraps mod 2^64
-  // the cross terms only touch the high word: 4 chained 32-bit IMADs
-  const uint32_t hi = hi32(r) + x0 * y1 + x1 * y0 + q0 * n1 + q1 * n0;
-  return (static_cast<uint64_t>(hi) << 32) | lo32(r);
+  // lo64(x0 y0 + q0 n0) then the four cross terms on the high word only
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 x0, x1, y0, y1, q0, q1, n0, n1, rl, rh;\n\t"
+      ".reg .u64 t;\n\t"
+      "mov.b64 {x0, x1}, %1;\n\t"
+      "mov.b64 {y0, y1}, %2;\n\t"
+      "mov.b64 {q0, q1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\t"
+      "mul.wide.u32 t, x0, y0;\n\t"
+      "mad.wide.u32 t, q0, n0, t;\n\t"
+      "mov.b64 {rl, rh}, t;\n\t"
+      "mad.lo.u32 rh, x0, y1, rh;\n\t"
+      "mad.lo.u32 rh, x1, y0, rh;\n\t"
+      "mad.lo.u32 rh, q0, n1, rh;\n\t"
+      "mad.lo.u32 rh, q1, n0, rh;\n\t"
+      "mov.b64 %0, {rl, rh};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(x), "l"(y), "l"(q), "l"(negp));
+  return r;
 }
 
 // Shoup multiplication by a fixed operand w with wq = floor(w 2^64 / p).

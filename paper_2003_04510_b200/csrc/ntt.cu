@@ -73,7 +73,8 @@ struct PassArgs {
 // One pass of S levels over C = 2^LOGC sub-problems. STRIDED: pass A layout
 // (sub-problems are columns at stride tlast); else pass B (contiguous blocks).
 template <int S, int LOGC, bool STRIDED, bool INV>
-__global__ void __launch_bounds__(1 << (S + LOGC - 3)) ntt_pass_kernel(PassArgs a) {
+// at least 2 CTAs (1024 threads) per SM: <= 64 registers per thread
+__global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassArgs a) {
   constexpr int C = 1 << LOGC;
   constexpr int ELEMS = C << S;
   constexpr int T = ELEMS / 8;
