@@ -95,6 +95,104 @@ __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limb
   }
 }
 
+// ---- persistent variant: the CTA's weight columns stay in shared memory ---
+//
+// The weight table is the same for every coefficient, so a persistent CTA
+// loads its column tile (K x 16 NW words) once and then walks coefficient
+// tiles, double-buffering each tile's limbs with cp.async so the next tile's
+// HBM reads overlap this tile's IMAD.WIDE loop. grid = (CTAs per column
+// tile, column tiles).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) crt_persistent_kernel(
+    Inputs in, int count, int B, int limbs, int log_n, CrtWeights w,
+    const DevPrime* __restrict__ primes, int np, uint64_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NC = 16 * NW;
+  const size_t n = size_t(1) << log_n;
+  const int K = w.chunks;
+  const int col0 = blockIdx.y * NC;
+  uint32_t* Bsm = reinterpret_cast<uint32_t*>(smem);       // [K][NC]
+  uint32_t* A = Bsm + K * NC;                                // [K][32]
+  uint64_t* raw = reinterpret_cast<uint64_t*>(A + K * kGemmCoefs);  // [2][32 * limbs]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cg = lane & 7, ng = lane >> 3;
+  const int coef_tiles = static_cast<int>(n / kGemmCoefs);
+  const int tiles = count * B * coef_tiles;
+  const int rawsz = kGemmCoefs * limbs;
+  // weight tile, once
+  for (int idx = tid; idx < K * (NC / 4); idx += NW * 32) {
+    const int k = idx / (NC / 4), c = idx - k * (NC / 4);
+    cp_async16(Bsm + k * NC + 4 * c, w.wtab + size_t(k) * w.ld + col0 + 4 * c);
+  }
+  auto fetch = [&](int tile, uint64_t* dst) {
+    const int ct = tile % coef_tiles, bt = tile / coef_tiles;  // bt = t * B + b
+    const int t = bt / B, b = bt - t * B;
+    const uint64_t* src = in.p[t] + (size_t(b) * n + size_t(ct) * kGemmCoefs) * limbs;
+    for (int idx = tid; idx < rawsz / 2; idx += NW * 32) cp_async16(dst + 2 * idx, src + 2 * idx);
+  };
+  int tile = blockIdx.x;
+  if (tile < tiles) fetch(tile, raw);
+  cp_async_commit();
+  for (int it = 0; tile < tiles; tile += gridDim.x, ++it) {
+    uint64_t* cur = raw + (it & 1) * rawsz;
+    cp_async_wait<0>();
+    __syncthreads();  // limbs of this tile (and the weights) are in; A is free
+    if (tile + gridDim.x < tiles) fetch(tile + gridDim.x, raw + ((it + 1) & 1) * rawsz);
+    cp_async_commit();
+    for (int idx = tid; idx < kGemmCoefs * K; idx += NW * 32) {
+      const int m = idx >> 5, c = idx & 31;
+      const int bit = 25 * m, k = bit >> 6, off = bit & 63;
+      const uint64_t* l = cur + c * limbs;
+      uint64_t v = k < limbs ? l[k] >> off : 0;
+      if (off > 39 && k + 1 < limbs) v |= l[k + 1] << (64 - off);
+      A[idx] = static_cast<uint32_t>(v) & 0x1ffffffu;
+    }
+    __syncthreads();
+    uint64_t acc[4][4] = {};
+    const uint32_t* ap = A + 4 * cg;
+    const uint32_t* bp = Bsm + 16 * warp + 4 * ng;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      const uint4 a = *reinterpret_cast<const uint4*>(ap + k * kGemmCoefs);
+      const uint4 b = *reinterpret_cast<const uint4*>(bp + k * NC);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] += static_cast<uint64_t>(av[i]) * bv[q];
+    }
+    const int ct = tile % coef_tiles, bt = tile / coef_tiles;
+    uint64_t* obase = out + size_t(bt) * np * n + size_t(ct) * kGemmCoefs + 4 * cg;
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const int j = (col0 + 16 * warp + 4 * ng) / 2 + pp;
+      if (j >= np) continue;
+      const DevPrime& pr = primes[j];
+      const uint64_t negp = 0 - pr.p;
+      uint64_t r[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t x = acc[i][2 * pp], y = acc[i][2 * pp + 1];
+        const uint64_t vlo = x + (y << 30);
+        const uint64_t vhi = (y >> 34) + (vlo < x);
+        const uint64_t r0 = shoup_mul_4p(vlo, 1, pr.one_q, negp);
+        const uint64_t r1 = shoup_mul_4p(vhi, pr.beta, pr.beta_q, negp);
+        r[i] = reduce_4p(csub(r0 + r1, 4 * pr.p), pr.p);
+      }
+      uint64_t* dst = obase + size_t(j) * n;
+      reinterpret_cast<ulonglong2*>(dst)[0] = make_ulonglong2(r[0], r[1]);
+      reinterpret_cast<ulonglong2*>(dst)[1] = make_ulonglong2(r[2], r[3]);
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int NW>
+size_t crt_persistent_smem(int limbs, int K) {
+  return size_t(K) * 16 * NW * 4 + size_t(K) * kGemmCoefs * 4 +
+         2 * size_t(kGemmCoefs) * limbs * 8;
+}
+
 int nw_for(int ld) { return ld <= 192 ? ld / 16 : 8; }
 
 template <int NW>
@@ -138,7 +236,11 @@ cudaError_t with_nw(int nw, F&& f) {
 cudaError_t crt_setup_attributes() {
   for (int nw = 1; nw <= 12; ++nw) {
     cudaError_t e = with_nw(nw, [](auto v) {
-      return cudaFuncSetAttribute(crt_kernel<decltype(v)::value>,
+      cudaError_t e2 = cudaFuncSetAttribute(crt_kernel<decltype(v)::value>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kMaxDynSmem);
+      if (e2 != cudaSuccess) return e2;
+      return cudaFuncSetAttribute(crt_persistent_kernel<decltype(v)::value>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (e != cudaSuccess) return e;
@@ -153,8 +255,24 @@ cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs
   if (count < 1 || count > 4 || n < kGemmCoefs || w.chunks > kMaxGemmK) return cudaErrorInvalidValue;
   Inputs in{};
   for (int t = 0; t < count; ++t) in.p[t] = polys[t];
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   return with_nw(nw_for(w.ld), [&](auto v) {
-    return launch<decltype(v)::value>(in, count, limbs, batch, log_n, w, primes, np, out, st);
+    constexpr int NW = decltype(v)::value;
+    const size_t psmem = crt_persistent_smem<NW>(limbs, w.chunks);
+    if (psmem <= 110 * 1024) {  // 2 persistent CTAs per SM
+      const int col_tiles = w.ld / (16 * NW);
+      const int tiles = static_cast<int>(count * batch * (n / kGemmCoefs));
+      const int per = std::max(1, std::min(tiles, 2 * sms / col_tiles));
+      crt_persistent_kernel<NW><<<dim3(per, col_tiles), NW * 32, psmem, st>>>(
+          in, count, static_cast<int>(batch), limbs, log_n, w, primes, np, out);
+      return cudaGetLastError();
+    }
+    return launch<NW>(in, count, limbs, batch, log_n, w, primes, np, out, st);
   });
 }
 
