@@ -115,8 +115,14 @@ hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, cons
 /* Options. HEMUL_OPT_FORCE_EXACT = 1 routes every output coefficient of
  * he_mul through the exact big-integer fix-up kernel that normally only
  * handles the (probability 2^-64) coefficients whose truncated ModDown window
- * is ambiguous — a test knob for that path; results are identical. */
-enum { HEMUL_OPT_FORCE_EXACT = 1 };
+ * is ambiguous — a test knob for that path; results are identical.
+ * HEMUL_OPT_BASIS selects the RNS prime basis he_mul computes in: 32 (the
+ * default) = primes p = 1 mod 2n below 2^30 with 32-bit residues, 64 = the
+ * reference's own w64 primes (params.cpp:89-115). The product is exact in
+ * either basis, so the ciphertexts are bit-identical; the 30-bit basis falls
+ * back to 64 when a ring degree has too few such primes. Changing it
+ * invalidates cached evk forms (pass the evk to the next he_mul). */
+enum { HEMUL_OPT_FORCE_EXACT = 1, HEMUL_OPT_BASIS = 2 };
 hemul_status hemul_gpu_set_option(hemul_gpu_ctx *ctx, int option, int value);
 
 /* Device timing. When enabled every launch is bracketed by CUDA events on the
@@ -136,7 +142,9 @@ hemul_status hemul_gpu_reset_stats(hemul_gpu_ctx *ctx);
 hemul_status hemul_gpu_imad_peak(hemul_gpu_ctx *ctx, double *ops_per_s);
 
 /* Region tables of level log_q: region 1 (products mod q) or 2 (key
- * switching). Writes np and up to cap primes. */
+ * switching) in the reference's w64 basis, as the stage entry points use
+ * them; region -1 / -2: the basis he_mul runs in (HEMUL_OPT_BASIS). Writes
+ * np and up to cap primes. */
 hemul_status hemul_gpu_level_info(hemul_gpu_ctx *ctx, int log_q, int region, int *np,
                                   uint64_t *primes, int cap);
 

@@ -53,7 +53,10 @@ struct DevBuf {
   }
 };
 
+// One region's device tables in one basis (word 64: the reference's w64
+// primes, F64; word 32: the B200 30-bit basis, F32).
 struct RegionDev {
+  int word = 64;
   int np = 0;
   int target_bits = 0;
   DevBuf primes, tw, itw, btab, hat, big_p, half_p;
@@ -70,16 +73,35 @@ struct RegionDev {
       if (c.in_bits == bits) return &c.w;
     return nullptr;
   }
+  template <class F>
+  const typename F::Prime* P() const {
+    return primes.as<const typename F::Prime>();
+  }
+  template <class F>
+  const typename F::Tw* TW() const {
+    return tw.as<const typename F::Tw>();
+  }
+  template <class F>
+  const typename F::Tw* ITW() const {
+    return itw.as<const typename F::Tw>();
+  }
+};
+
+// Both regions of a level in one basis, and the fused finisher's table.
+struct Basis {
+  std::unique_ptr<RegionDev> r1, r2;
+  bool has_fin = false;
+  DevBuf fin_btab;
+  Finisher fin;  // fused ModDown + add + rescale table (he_mul levels only)
 };
 
 struct Level {
   int log_q = 0;
-  RegionDev r1, r2;
+  Basis basis[2];  // [0]: w64 reference primes, [1]: 30-bit basis
   bool has_evk = false;
+  int evk_word = 0;  // basis of the cached evk forms
   uint64_t evk_id = 0;
   DevBuf evk_a;  // 2 x np2 x n NTT forms (ax then bx)
-  DevBuf fin_btab;
-  Finisher fin;  // fused ModDown + add + rescale table (he_mul levels only)
 };
 
 struct CudaFail : std::runtime_error {
@@ -129,6 +151,7 @@ struct hemul_gpu_ctx {
   // scratch
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
+  int basis = 32;       // HEMUL_OPT_BASIS: he_mul prime basis (32 or 64)
 
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
@@ -218,13 +241,20 @@ void flush_marks(hemul_gpu_ctx* c) {
   c->marks.clear();
 }
 
-void fill_region(RegionDev& d, const RegionHost& h, int log_n, cudaStream_t st) {
+void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
+  d.word = h.word;
   d.np = h.np;
   d.target_bits = h.target_bits;
   d.host_primes = h.primes;
-  upload(d.primes, h.dev, st);
-  upload(d.tw, h.tw, st);
-  upload(d.itw, h.itw, st);
+  if (h.word == 64) {
+    upload(d.primes, h.dev, st);
+    upload(d.tw, h.tw, st);
+    upload(d.itw, h.itw, st);
+  } else {
+    upload(d.primes, h.dev32, st);
+    upload(d.tw, h.tw32, st);
+    upload(d.itw, h.itw32, st);
+  }
   upload(d.btab, h.btab, st);
   d.icrt.btab = d.btab.as<uint32_t>();
   d.icrt.m_out = h.m_out;
@@ -248,7 +278,6 @@ void fill_region(RegionDev& d, const RegionHost& h, int log_n, cudaStream_t st) 
     dc.w.ld = c.ld;
     d.crt.push_back(std::move(dc));
   }
-  (void)log_n;
 }
 
 int host_threads() {
@@ -256,7 +285,8 @@ int host_threads() {
   return t ? int(t < 32 ? t : 32) : 1;
 }
 
-// Scheme::level (heaan.cpp:119-150): LRU of capacity 2 keyed by log_q.
+// Scheme::level (heaan.cpp:119-150): LRU of capacity 2 keyed by log_q. The
+// tables of each basis are built on first use (get_basis).
 Level& get_level(hemul_gpu_ctx* c, int log_q) {
   for (auto it = c->cache.begin(); it != c->cache.end(); ++it)
     if ((*it)->log_q == log_q) {
@@ -266,16 +296,31 @@ Level& get_level(hemul_gpu_ctx* c, int log_q) {
   if (log_q <= 0 || log_q > c->log_q_max) throw std::invalid_argument("log_q out of range");
   auto lv = std::make_unique<Level>();
   lv->log_q = log_q;
+  c->cache.push_front(std::move(lv));
+  while (c->cache.size() > 2) c->cache.pop_back();
+  return *c->cache.front();
+}
+
+// Regions 1 and 2 of a level in basis `word` (64 or 32), plus the finisher
+// table when he_mul can run at this level. Throws std::runtime_error when
+// the 30-bit basis has too few primes for the ring degree.
+Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
+  Basis& b = lv.basis[word == 64 ? 0 : 1];
+  if (b.r1) return b;
+  const int log_q = lv.log_q;
   const int th = host_threads();
-  RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th);
-  RegionHost h2 = build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th);
-  fill_region(lv->r1, h1, c->log_n, c->stream);
-  fill_region(lv->r2, h2, c->log_n, c->stream);
+  RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th, word);
+  RegionHost h2 =
+      build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th, word);
+  auto r1 = std::make_unique<RegionDev>();
+  auto r2 = std::make_unique<RegionDev>();
+  fill_region(*r1, h1, c->stream);
+  fill_region(*r2, h2, c->stream);
   if (log_q - c->log_p >= c->log_p) {  // a level he_mul can run at
     const FinisherHost fh = build_finisher(h1, h2, log_q, c->log_q_max, c->log_p);
-    upload(lv->fin_btab, fh.btab, c->stream);
-    Finisher& f = lv->fin;
-    f.btab = lv->fin_btab.as<uint32_t>();
+    upload(b.fin_btab, fh.btab, c->stream);
+    Finisher& f = b.fin;
+    f.btab = b.fin_btab.as<uint32_t>();
     f.cols = fh.cols;
     f.cols_pad = fh.cols_pad;
     f.k2 = fh.k2;
@@ -288,11 +333,24 @@ Level& get_level(hemul_gpu_ctx* c, int log_q) {
     f.log_q = log_q;
     f.log_Q = c->log_q_max;
     f.log_p = c->log_p;
+    b.has_fin = true;
   }
   check(cudaStreamSynchronize(c->stream), "level upload");
-  c->cache.push_front(std::move(lv));
-  while (c->cache.size() > 2) c->cache.pop_back();
-  return *c->cache.front();
+  b.r1 = std::move(r1);
+  b.r2 = std::move(r2);
+  return b;
+}
+
+// The basis he_mul runs in: the context's choice, or the reference's w64
+// primes when the 30-bit basis cannot cover the level (fields.cuh).
+int mul_word(hemul_gpu_ctx* c, Level& lv) {
+  if (c->basis == 64) return 64;
+  try {
+    get_basis(c, lv, 32);
+    return 32;
+  } catch (const std::runtime_error&) {
+    return 64;
+  }
 }
 
 bool is_device(const hemul_gpu_ctx* c, const void* p) {
@@ -313,24 +371,26 @@ int limbs_of(int bits) { return (bits + 63) / 64; }
 
 // Forward NTT of `rows` rows, one launch per memory pass (only the first
 // `passes` of them when a fused middle pass follows).
-void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage,
+template <class F>
+void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t rows, int stage,
              int passes = 2) {
   const int total = ntt_num_passes(c->log_n);
   for (int pass = 0; pass < total && pass < passes; ++pass)
     run(c, stage, pass == 0 ? HEMUL_KCLASS_NTT_A : HEMUL_KCLASS_NTT_B, "NTT", [&] {
-      return ntt_forward_pass(pass, data, rows, r.np, c->log_n, r.tw.as<Twiddle>(),
-                              r.primes.as<DevPrime>(), c->stream);
+      return ntt_forward_pass<F>(pass, data, rows, r.np, c->log_n, r.TW<F>(), r.P<F>(),
+                                 c->stream);
     });
 }
 
 // Inverse NTT; passes = 1 runs only the final pass (after a fused middle pass).
-void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, uint64_t* data, size_t rows, int stage,
+template <class F>
+void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t rows, int stage,
              int passes = 2) {
   const int total = ntt_num_passes(c->log_n);
   for (int pass = total > passes ? total - passes : 0; pass < total; ++pass)
     run(c, stage, pass + 1 == total ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B, "iNTT", [&] {
-      return ntt_inverse_pass(pass, data, rows, r.np, c->log_n, r.itw.as<Twiddle>(),
-                              r.primes.as<DevPrime>(), c->stream);
+      return ntt_inverse_pass<F>(pass, data, rows, r.np, c->log_n, r.ITW<F>(), r.P<F>(),
+                                 c->stream);
     });
 }
 
@@ -343,28 +403,43 @@ const uint64_t* stage_in(hemul_gpu_ctx* c, const uint64_t* p, size_t words, uint
 }
 
 // Scheme::level's evk transforms (heaan.cpp:152-167): CRT of the 2 log_Q-bit
-// key polys into the region-2 primes + forward NTT, kept on the device.
+// key polys into the region-2 primes of the he_mul basis + forward NTT,
+// kept on the device.
+template <class F>
+void evk_forms(hemul_gpu_ctx* c, Level& lv, const RegionDev& r2, const uint64_t* a,
+               const uint64_t* b) {
+  using W = typename F::W;
+  const size_t n = size_t(c->n);
+  ensure(lv.evk_a, 2 * size_t(r2.np) * n * sizeof(W));  // [evk_ax form | evk_bx form]
+  const CrtWeights* w = r2.weights(2 * c->log_q_max);
+  W* fa = lv.evk_a.as<W>();
+  W* fb = fa + size_t(r2.np) * n;
+  const int Le = limbs_of(2 * c->log_q_max);
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
+    return crt_forward<F>(a, Le, 1, c->log_n, *w, r2.P<F>(), r2.np, fa, c->stream);
+  });
+  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
+    return crt_forward<F>(b, Le, 1, c->log_n, *w, r2.P<F>(), r2.np, fb, c->stream);
+  });
+  ntt_fwd<F>(c, r2, fa, 2 * size_t(r2.np), HEMUL_STAGE_EXTRA);
+}
+
 void set_evk_forms(hemul_gpu_ctx* c, Level& lv, const uint64_t* evk_ax, const uint64_t* evk_bx,
                    uint64_t id) {
   const size_t n = size_t(c->n);
   const int Le = limbs_of(2 * c->log_q_max);
-  const RegionDev& r2 = lv.r2;
-  ensure(lv.evk_a, 2 * size_t(r2.np) * n * 8);  // [evk_ax form | evk_bx form]
+  const int word = mul_word(c, lv);
+  const RegionDev& r2 = *get_basis(c, lv, word).r2;
   ensure(c->in, 2 * n * Le * 8);
   const uint64_t* a = stage_in(c, evk_ax, n * Le, c->in.as<uint64_t>());
   const uint64_t* b = stage_in(c, evk_bx, n * Le, c->in.as<uint64_t>() + n * Le);
-  const CrtWeights* w = r2.weights(2 * c->log_q_max);
-  uint64_t* fa = lv.evk_a.as<uint64_t>();
-  uint64_t* fb = fa + size_t(r2.np) * n;
-  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
-    return crt_forward(a, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np, fa, c->stream);
-  });
-  run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
-    return crt_forward(b, Le, 1, c->log_n, *w, r2.primes.as<DevPrime>(), r2.np, fb, c->stream);
-  });
-  ntt_fwd(c, r2, fa, 2 * size_t(r2.np), HEMUL_STAGE_EXTRA);
+  if (word == 64)
+    evk_forms<F64>(c, lv, r2, a, b);
+  else
+    evk_forms<F32>(c, lv, r2, a, b);
   check(cudaStreamSynchronize(c->stream), "evk forms");
   lv.has_evk = true;
+  lv.evk_word = word;
   lv.evk_id = id;
 }
 
@@ -390,8 +465,11 @@ void copy_out(hemul_gpu_ctx* c, const OutPair& o, uint64_t* oa, uint64_t* ob, si
   check(cudaStreamSynchronize(c->stream), "D2H");
 }
 
+template <class F>
 void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                    const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx);
+void he_mul_any(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
+                const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx);
 void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                       const uint64_t* const src[4], bool dev_in, uint64_t* out_ax,
                       uint64_t* out_bx, bool dev_out);
@@ -494,7 +572,8 @@ hemul_status hemul_gpu_set_stream(hemul_gpu_ctx* c, void* stream) {
 hemul_status hemul_gpu_set_level(hemul_gpu_ctx* c, int log_q) {
   if (!c) return HEMUL_E_ARG;
   return guarded(c, [&] {
-    get_level(c, log_q);
+    Level& lv = get_level(c, log_q);
+    get_basis(c, lv, mul_word(c, lv));
     return HEMUL_OK;
   });
 }
@@ -511,10 +590,11 @@ hemul_status hemul_gpu_set_evk(hemul_gpu_ctx* c, int log_q, const uint64_t* evk_
 
 hemul_status hemul_gpu_level_info(hemul_gpu_ctx* c, int log_q, int region, int* np,
                                   uint64_t* primes, int cap) {
-  if (!c || (region != 1 && region != 2)) return HEMUL_E_ARG;
+  if (!c || (region != 1 && region != 2 && region != -1 && region != -2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
     Level& lv = get_level(c, log_q);
-    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const Basis& b = get_basis(c, lv, region > 0 ? 64 : mul_word(c, lv));
+    const RegionDev& r = region == 1 || region == -1 ? *b.r1 : *b.r2;
     if (np) *np = r.np;
     for (int j = 0; j < r.np && j < cap && primes; ++j) primes[j] = r.host_primes[j];
     return HEMUL_OK;
@@ -526,6 +606,10 @@ hemul_status hemul_gpu_set_option(hemul_gpu_ctx* c, int option, int value) {
   switch (option) {
     case HEMUL_OPT_FORCE_EXACT:
       c->force_exact = value != 0;
+      return HEMUL_OK;
+    case HEMUL_OPT_BASIS:
+      if (value != 32 && value != 64) return fail(c, HEMUL_E_ARG, "basis must be 32 or 64");
+      c->basis = value;
       return HEMUL_OK;
     default:
       return fail(c, HEMUL_E_ARG, "unknown option");
@@ -607,16 +691,19 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
     return fail(c, HEMUL_E_ARG, "null buffer");
   return guarded(c, [&]() -> hemul_status {
     Level& lv = get_level(c, log_q);
-    if (evk_ax && evk_bx && (!lv.has_evk || evk_id == 0 || lv.evk_id != evk_id))
+    const int word = mul_word(c, lv);
+    if (evk_ax && evk_bx &&
+        (!lv.has_evk || evk_id == 0 || lv.evk_id != evk_id || lv.evk_word != word))
       set_evk_forms(c, lv, evk_ax, evk_bx, evk_id);
-    if (!lv.has_evk) return fail(c, HEMUL_E_NO_EVK, "evaluation key not set for this level");
+    if (!lv.has_evk || lv.evk_word != word)
+      return fail(c, HEMUL_E_NO_EVK, "evaluation key not set for this level");
     ++c->call_id;
     const uint64_t* src[4] = {c1_ax, c1_bx, c2_ax, c2_bx};
     bool dev_in = true;
     for (const uint64_t* s : src) dev_in = dev_in && is_device(c, s);
     const bool dev_out = is_device(c, out_ax) && is_device(c, out_bx);
     if (dev_in && dev_out) {
-      he_mul_device(c, lv, log_q, batch, src, out_ax, out_bx);
+      he_mul_any(c, lv, log_q, batch, src, out_ax, out_bx);
       return HEMUL_OK;
     }
     he_mul_pipelined(c, lv, log_q, batch, src, dev_in, out_ax, out_bx, dev_out);
@@ -654,94 +741,104 @@ hemul_status hemul_gpu_rescale(hemul_gpu_ctx* c, int log_q, size_t batch, const 
 
 namespace {
 
-// One batched HE Mul on device buffers, every launch on c->stream.
+// One batched HE Mul on device buffers, every launch on c->stream, in the
+// prime basis of field F (fields.cuh).
+template <class F>
 void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                    const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx) {
-  {
-    const size_t n = size_t(c->n);
-    const int log_n = c->log_n;
-    const int L = limbs_of(log_q);
-    const RegionDev& r1 = lv.r1;
-    const RegionDev& r2 = lv.r2;
-    const size_t B = batch;
-    const size_t poly_w = n * L;
-    const DevPrime* p1 = r1.primes.as<DevPrime>();
-    const DevPrime* p2 = r2.primes.as<DevPrime>();
-    // ---- region 1: d0 = bx1 bx2, d1 = ax1 bx2 + ax2 bx1, d2 = ax1 ax2 ---------
-    const size_t r1w = B * r1.np * n;  // one RNS operand
-    ensure(c->r1, 4 * r1w * 8);
-    uint64_t* R1 = c->r1.as<uint64_t>();
-    uint64_t* A1 = R1;
-    uint64_t* B1 = R1 + r1w;
-    uint64_t* A2 = R1 + 2 * r1w;
-    uint64_t* B2 = R1 + 3 * r1w;
-    const CrtWeights* w1 = r1.weights(log_q);
-    // one launch: ax1 -> A1, bx1 -> B1, ax2 -> A2, bx2 -> B2 (R1 is [A1|B1|A2|B2])
-    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
-      return crt_forward_multi(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
+  using W = typename F::W;
+  const size_t n = size_t(c->n);
+  const int log_n = c->log_n;
+  const int L = limbs_of(log_q);
+  const Basis& bs = get_basis(c, lv, sizeof(W) == 8 ? 64 : 32);
+  const RegionDev& r1 = *bs.r1;
+  const RegionDev& r2 = *bs.r2;
+  const size_t B = batch;
+  const size_t poly_w = n * L;
+  const typename F::Prime* p1 = r1.P<F>();
+  const typename F::Prime* p2 = r2.P<F>();
+  // ---- region 1: d0 = bx1 bx2, d1 = ax1 bx2 + ax2 bx1, d2 = ax1 ax2 ---------
+  const size_t r1w = B * r1.np * n;  // one RNS operand
+  ensure(c->r1, 4 * r1w * sizeof(W));
+  W* R1 = c->r1.as<W>();
+  W* A1 = R1;
+  W* B1 = R1 + r1w;
+  W* A2 = R1 + 2 * r1w;
+  W* B2 = R1 + 3 * r1w;
+  const CrtWeights* w1 = r1.weights(log_q);
+  // one launch: ax1 -> A1, bx1 -> B1, ax2 -> A2, bx2 -> B2 (R1 is [A1|B1|A2|B2])
+  run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
+    return crt_forward_multi<F>(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
+  });
+  // in place: d2 -> A1, d0 -> B1, d1 -> A2
+  const bool mid = ntt_has_mid(log_n);
+  if (mid) {
+    // forward pass A, then one fused pass: forward pass B + tensor product +
+    // inverse pass B, then inverse pass A
+    ntt_fwd<F>(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT, 1);
+    run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R1, "NTT mid r1", [&] {
+      return ntt_mid_tensor<F>(A1, B1, A2, B2, B, r1.np, log_n, r1.TW<F>(), r1.ITW<F>(), p1,
+                               c->stream);
     });
-    // in place: d2 -> A1, d0 -> B1, d1 -> A2
-    const bool mid = ntt_has_mid(log_n);
-    if (mid) {
-      // forward pass A, then one fused pass: forward pass B + tensor product +
-      // inverse pass B, then inverse pass A
-      ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT, 1);
-      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R1, "NTT mid r1", [&] {
-        return ntt_mid_tensor(A1, B1, A2, B2, B, r1.np, log_n, r1.tw.as<Twiddle>(),
-                              r1.itw.as<Twiddle>(), p1, c->stream);
-      });
-      ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT, 1);
-    } else {
-      ntt_fwd(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
-      // pointwise products are booked under iCRT like rns.cpp:364
-      run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "tensor product", [&] {
-        return tensor_product(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
-      });
-      ntt_inv(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
-    }
-    // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
-    // and are reconstructed inside the finisher
-    ensure(c->dpoly, B * poly_w * 8);
-    uint64_t* d2 = c->dpoly.as<uint64_t>();
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1",
-        [&] { return icrt(A1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream); });
-    // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
-    const size_t r2w = B * r2.np * n;
-    ensure(c->r2, 2 * r2w * 8);
-    uint64_t* KA = c->r2.as<uint64_t>();
-    uint64_t* KB = KA + r2w;
-    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2", [&] {
-      return crt_forward(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
+    ntt_inv<F>(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT, 1);
+  } else {
+    ntt_fwd<F>(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
+    // pointwise products are booked under iCRT like rns.cpp:364
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "tensor product", [&] {
+      return tensor_product<F>(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
     });
-    const uint64_t* EA = lv.evk_a.as<uint64_t>();
-    const uint64_t* EB = EA + size_t(r2.np) * n;
-    if (mid) {
-      ntt_fwd(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT, 1);
-      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R2, "NTT mid r2", [&] {
-        return ntt_mid_evk(KA, EA, EB, KA, KB, B, r2.np, log_n, r2.tw.as<Twiddle>(),
-                           r2.itw.as<Twiddle>(), p2, c->stream);
-      });
-      ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1);
-    } else {
-      ntt_fwd(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
-      run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
-          [&] { return evk_product(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
-      ntt_inv(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
-    }
-    // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
-    // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
-    IcrtFlags flags;
-    flags.capacity = static_cast<unsigned>(2 * B * n);
-    ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
-    flags.count = c->flagbuf.as<unsigned>();
-    flags.ids = flags.count + 1;
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
-      return finish_keyswitch(KA, A2 /* d1 */, B1 /* d0 */, B, log_n, p2, r2.np, p1, r1.np,
-                              lv.fin, r2.icrt, r1.icrt, out_ax, out_bx, flags, c->force_exact,
-                              c->stream);
-    });
-    ++c->launches;  // the (normally empty) exact fix-up kernel
+    ntt_inv<F>(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
   }
+  // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
+  // and are reconstructed inside the finisher
+  ensure(c->dpoly, B * poly_w * 8);
+  uint64_t* d2 = c->dpoly.as<uint64_t>();
+  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1",
+      [&] { return icrt<F>(A1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream); });
+  // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
+  const size_t r2w = B * r2.np * n;
+  ensure(c->r2, 2 * r2w * sizeof(W));
+  W* KA = c->r2.as<W>();
+  W* KB = KA + r2w;
+  run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2", [&] {
+    return crt_forward<F>(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
+  });
+  const W* EA = lv.evk_a.as<W>();
+  const W* EB = EA + size_t(r2.np) * n;
+  if (mid) {
+    ntt_fwd<F>(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT, 1);
+    run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R2, "NTT mid r2", [&] {
+      return ntt_mid_evk<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, r2.TW<F>(), r2.ITW<F>(), p2,
+                            c->stream);
+    });
+    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1);
+  } else {
+    ntt_fwd<F>(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
+        [&] { return evk_product<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
+    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
+  }
+  // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
+  // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
+  IcrtFlags flags;
+  flags.capacity = static_cast<unsigned>(2 * B * n);
+  ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
+  flags.count = c->flagbuf.as<unsigned>();
+  flags.ids = flags.count + 1;
+  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
+    return finish_keyswitch<F>(KA, A2 /* d1 */, B1 /* d0 */, B, log_n, p2, r2.np, p1, r1.np,
+                               bs.fin, r2.icrt, r1.icrt, out_ax, out_bx, flags, c->force_exact,
+                               c->stream);
+  });
+  ++c->launches;  // the (normally empty) exact fix-up kernel
+}
+
+void he_mul_any(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
+                const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx) {
+  if (lv.evk_word == 64)
+    he_mul_device<F64>(c, lv, log_q, batch, in, out_ax, out_bx);
+  else
+    he_mul_device<F32>(c, lv, log_q, batch, in, out_ax, out_bx);
 }
 
 // Host buffers: the batch runs in chunks through double-buffered device
@@ -782,7 +879,7 @@ void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
     if (k >= 2 && !dev_out) check(cudaStreamWaitEvent(c->stream, c->ev_d2h[s], 0), "wait");
     uint64_t* oa = dev_out ? out_ax + b0 * out_w : out_slot[s];
     uint64_t* ob = dev_out ? out_bx + b0 * out_w : out_slot[s] + chunk * out_w;
-    he_mul_device(c, lv, log_q, bc, in, oa, ob);
+    he_mul_any(c, lv, log_q, bc, in, oa, ob);
     check(cudaEventRecord(c->ev_comp[s], c->stream), "event");
     if (!dev_out) {
       check(cudaStreamWaitEvent(c->d2h, c->ev_comp[s], 0), "wait");
@@ -827,7 +924,8 @@ hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* da
   if (!c || !data || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
     Level& lv = get_level(c, log_q);
-    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
+    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
     const size_t words = rows * size_t(c->n);
     const bool dev = is_device(c, data);
     uint64_t* d = data;
@@ -837,9 +935,9 @@ hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* da
       stage_in(c, data, words, d);
     }
     if (inverse)
-      ntt_inv(c, r, d, rows, HEMUL_STAGE_INTT);
+      ntt_inv<F64>(c, r, d, rows, HEMUL_STAGE_INTT);
     else
-      ntt_fwd(c, r, d, rows, HEMUL_STAGE_NTT);
+      ntt_fwd<F64>(c, r, d, rows, HEMUL_STAGE_NTT);
     if (!dev)
       run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
         return cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDeviceToHost, c->stream);
@@ -854,7 +952,8 @@ hemul_status hemul_gpu_crt(hemul_gpu_ctx* c, int log_q, int region, int in_bits,
   if (!c || !poly || !rns || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&]() -> hemul_status {
     Level& lv = get_level(c, log_q);
-    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
+    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
     const CrtWeights* w = r.weights(in_bits);
     if (!w) return fail(c, HEMUL_E_ARG, "no CRT table for this input width");
     const size_t n = size_t(c->n);
@@ -869,8 +968,7 @@ hemul_status hemul_gpu_crt(hemul_gpu_ctx* c, int log_q, int region, int in_bits,
       dst = c->r1.as<uint64_t>();
     }
     run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT", [&] {
-      return crt_forward(src, L, batch, c->log_n, *w, r.primes.as<DevPrime>(), r.np, dst,
-                         c->stream);
+      return crt_forward<F64>(src, L, batch, c->log_n, *w, r.P<F64>(), r.np, dst, c->stream);
     });
     if (!dev)
       run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
@@ -886,7 +984,8 @@ hemul_status hemul_gpu_pointwise(hemul_gpu_ctx* c, int log_q, int region, size_t
   if (!c || !a || !b || !out || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
     Level& lv = get_level(c, log_q);
-    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
+    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
     const size_t words = batch * r.np * size_t(c->n);
     ensure(c->r1, 3 * words * 8);
     const uint64_t* da = stage_in(c, a, words, c->r1.as<uint64_t>());
@@ -910,7 +1009,8 @@ hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batc
   if (!c || !rns || !poly || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
     Level& lv = get_level(c, log_q);
-    const RegionDev& r = region == 1 ? lv.r1 : lv.r2;
+    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
+    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
     const size_t n = size_t(c->n);
     const size_t words = batch * r.np * n;
     const int TL = limbs_of(r.target_bits);
@@ -929,8 +1029,7 @@ hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batc
     flags.count = c->flagbuf.as<unsigned>();
     flags.ids = flags.count + 1;
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT", [&] {
-      return icrt(src, batch, c->log_n, r.primes.as<DevPrime>(), r.np, r.icrt, dst, c->stream,
-                  &flags);
+      return icrt<F64>(src, batch, c->log_n, r.P<F64>(), r.np, r.icrt, dst, c->stream, &flags);
     });
     ++c->launches;  // the fix-up kernel
     if (!dev)

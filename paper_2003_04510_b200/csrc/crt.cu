@@ -18,9 +18,9 @@
 
 #include <type_traits>
 
+#include "fields.cuh"
 #include "igemm.cuh"
 #include "kernels.hpp"
-#include "modarith.cuh"
 
 namespace hemul_gpu {
 
@@ -33,11 +33,56 @@ struct Inputs {
   const uint64_t* p[4];
 };
 
-template <int NW>
+// Residues of the thread's 4 coefficients x 4 accumulator columns. F64: the
+// column pair (2j, 2j+1) holds the 30-bit halves of prime j's weights,
+// V = X + 2^30 Y reduced with two Shoup steps. F32: column j is prime j,
+// one 64 -> 32 reduction. obase points at coefficient 4 cg of prime 0.
+template <class F>
+__device__ __forceinline__ void crt_store(const uint64_t (&acc)[4][4], int col,
+                                          const typename F::Prime* __restrict__ primes, int np,
+                                          size_t n, typename F::W* obase) {
+  if constexpr (F::kCrtColsPerPrime == 2) {
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const int j = col / 2 + pp;
+      if (j >= np) continue;
+      const DevPrime& pr = primes[j];
+      const uint64_t negp = 0 - pr.p;
+      uint64_t r[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t x = acc[i][2 * pp], y = acc[i][2 * pp + 1];
+        const uint64_t vlo = x + (y << 30);
+        const uint64_t vhi = (y >> 34) + (vlo < x);
+        const uint64_t r0 = shoup_mul_4p(vlo, 1, pr.one_q, negp);
+        const uint64_t r1 = shoup_mul_4p(vhi, pr.beta, pr.beta_q, negp);
+        r[i] = reduce_4p(csub(r0 + r1, 4 * pr.p), pr.p);
+      }
+      uint64_t* dst = obase + size_t(j) * n;
+      reinterpret_cast<ulonglong2*>(dst)[0] = make_ulonglong2(r[0], r[1]);
+      reinterpret_cast<ulonglong2*>(dst)[1] = make_ulonglong2(r[2], r[3]);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = col + q;
+      if (j >= np) continue;
+      const DevPrime32& pr = primes[j];
+      const uint32_t negp = 0u - pr.p;
+      uint32_t r[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        r[i] = csub32(reduce64_32(acc[i][q], pr.p, negp, pr.one_q, pr.beta, pr.beta_q), pr.p);
+      *reinterpret_cast<uint4*>(obase + size_t(j) * n) = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+  }
+}
+
+template <class F, int NW>
 __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limbs, int log_n,
                                                       CrtWeights w,
-                                                      const DevPrime* __restrict__ primes,
-                                                      int np, uint64_t* __restrict__ out) {
+                                                      const typename F::Prime* __restrict__ primes,
+                                                      int np, typename F::W* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NC = 16 * NW;
   const size_t n = size_t(1) << log_n;
@@ -65,33 +110,13 @@ __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limb
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cg = lane & 7, ng = lane >> 3;
-  uint64_t* obase = out + size_t(t) * B * np * n + size_t(b) * np * n + c0 + 4 * cg;
+  typename F::W* obase = out + size_t(t) * B * np * n + size_t(b) * np * n + c0 + 4 * cg;
   // (igemm_32xN synchronises before touching A; the CTA-wide ring measured
   // faster than per-warp rings here: 11 warps share each 704-byte B row)
   for (int col0 = 0; col0 < w.ld; col0 += NC) {
     uint64_t acc[4][4] = {};
     igemm_32xN<NW, kKT, kStages>(A, K, w.wtab, w.ld, col0, Bs, acc);
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      const int j = (col0 + 16 * warp + 4 * ng) / 2 + pp;
-      if (j >= np) continue;
-      const DevPrime& pr = primes[j];
-      const uint64_t negp = 0 - pr.p;
-      uint64_t r[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        // V = X + 2^30 Y, X, Y < 2^64
-        const uint64_t x = acc[i][2 * pp], y = acc[i][2 * pp + 1];
-        const uint64_t vlo = x + (y << 30);
-        const uint64_t vhi = (y >> 34) + (vlo < x);
-        const uint64_t r0 = shoup_mul_4p(vlo, 1, pr.one_q, negp);
-        const uint64_t r1 = shoup_mul_4p(vhi, pr.beta, pr.beta_q, negp);
-        r[i] = reduce_4p(csub(r0 + r1, 4 * pr.p), pr.p);
-      }
-      uint64_t* dst = obase + size_t(j) * n;
-      reinterpret_cast<ulonglong2*>(dst)[0] = make_ulonglong2(r[0], r[1]);
-      reinterpret_cast<ulonglong2*>(dst)[1] = make_ulonglong2(r[2], r[3]);
-    }
+    crt_store<F>(acc, col0 + 16 * warp + 4 * ng, primes, np, n, obase);
   }
 }
 
@@ -102,10 +127,10 @@ __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limb
 // tiles, double-buffering each tile's limbs with cp.async so the next tile's
 // HBM reads overlap this tile's IMAD.WIDE loop. grid = (CTAs per column
 // tile, column tiles).
-template <int NW>
+template <class F, int NW>
 __global__ void __launch_bounds__(NW * 32) crt_persistent_kernel(
     Inputs in, int count, int B, int limbs, int log_n, CrtWeights w,
-    const DevPrime* __restrict__ primes, int np, uint64_t* __restrict__ out) {
+    const typename F::Prime* __restrict__ primes, int np, typename F::W* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NC = 16 * NW;
   const size_t n = size_t(1) << log_n;
@@ -162,27 +187,8 @@ __global__ void __launch_bounds__(NW * 32) crt_persistent_kernel(
         for (int q = 0; q < 4; ++q) acc[i][q] += static_cast<uint64_t>(av[i]) * bv[q];
     }
     const int ct = tile % coef_tiles, bt = tile / coef_tiles;
-    uint64_t* obase = out + size_t(bt) * np * n + size_t(ct) * kGemmCoefs + 4 * cg;
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      const int j = (col0 + 16 * warp + 4 * ng) / 2 + pp;
-      if (j >= np) continue;
-      const DevPrime& pr = primes[j];
-      const uint64_t negp = 0 - pr.p;
-      uint64_t r[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint64_t x = acc[i][2 * pp], y = acc[i][2 * pp + 1];
-        const uint64_t vlo = x + (y << 30);
-        const uint64_t vhi = (y >> 34) + (vlo < x);
-        const uint64_t r0 = shoup_mul_4p(vlo, 1, pr.one_q, negp);
-        const uint64_t r1 = shoup_mul_4p(vhi, pr.beta, pr.beta_q, negp);
-        r[i] = reduce_4p(csub(r0 + r1, 4 * pr.p), pr.p);
-      }
-      uint64_t* dst = obase + size_t(j) * n;
-      reinterpret_cast<ulonglong2*>(dst)[0] = make_ulonglong2(r[0], r[1]);
-      reinterpret_cast<ulonglong2*>(dst)[1] = make_ulonglong2(r[2], r[3]);
-    }
+    typename F::W* obase = out + size_t(bt) * np * n + size_t(ct) * kGemmCoefs + 4 * cg;
+    crt_store<F>(acc, col0 + 16 * warp + 4 * ng, primes, np, n, obase);
   }
   cp_async_wait<0>();
 }
@@ -201,13 +207,13 @@ size_t crt_smem(int limbs, int K) {
          size_t(kGemmCoefs) * limbs * 8;
 }
 
-template <int NW>
+template <class F, int NW>
 cudaError_t launch(const Inputs& in, int count, int limbs, size_t batch, int log_n,
-                   const CrtWeights& w, const DevPrime* primes, int np, uint64_t* out,
-                   cudaStream_t st) {
+                   const CrtWeights& w, const typename F::Prime* primes, int np,
+                   typename F::W* out, cudaStream_t st) {
   const size_t n = size_t(1) << log_n;
   dim3 grid(static_cast<unsigned>(n / kGemmCoefs), static_cast<unsigned>(count * batch));
-  crt_kernel<NW><<<grid, NW * 32, crt_smem<NW>(limbs, w.chunks), st>>>(
+  crt_kernel<F, NW><<<grid, NW * 32, crt_smem<NW>(limbs, w.chunks), st>>>(
       in, static_cast<int>(batch), limbs, log_n, w, primes, np, out);
   return cudaGetLastError();
 }
@@ -231,16 +237,15 @@ cudaError_t with_nw(int nw, F&& f) {
   }
 }
 
-}  // namespace
-
-cudaError_t crt_setup_attributes() {
+template <class F>
+cudaError_t crt_attrs() {
   for (int nw = 1; nw <= 12; ++nw) {
     cudaError_t e = with_nw(nw, [](auto v) {
-      cudaError_t e2 = cudaFuncSetAttribute(crt_kernel<decltype(v)::value>,
+      cudaError_t e2 = cudaFuncSetAttribute(crt_kernel<F, decltype(v)::value>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kMaxDynSmem);
       if (e2 != cudaSuccess) return e2;
-      return cudaFuncSetAttribute(crt_persistent_kernel<decltype(v)::value>,
+      return cudaFuncSetAttribute(crt_persistent_kernel<F, decltype(v)::value>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (e != cudaSuccess) return e;
@@ -248,9 +253,17 @@ cudaError_t crt_setup_attributes() {
   return cudaSuccess;
 }
 
+}  // namespace
+
+cudaError_t crt_setup_attributes() {
+  cudaError_t e = crt_attrs<F64>();
+  return e != cudaSuccess ? e : crt_attrs<F32>();
+}
+
+template <class F>
 cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs, size_t batch,
-                              int log_n, const CrtWeights& w, const DevPrime* primes, int np,
-                              uint64_t* out, cudaStream_t st) {
+                              int log_n, const CrtWeights& w, const typename F::Prime* primes,
+                              int np, typename F::W* out, cudaStream_t st) {
   const size_t n = size_t(1) << log_n;
   if (count < 1 || count > 4 || n < kGemmCoefs || w.chunks > kMaxGemmK) return cudaErrorInvalidValue;
   Inputs in{};
@@ -268,18 +281,29 @@ cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs
       const int col_tiles = w.ld / (16 * NW);
       const int tiles = static_cast<int>(count * batch * (n / kGemmCoefs));
       const int per = std::max(1, std::min(tiles, 2 * sms / col_tiles));
-      crt_persistent_kernel<NW><<<dim3(per, col_tiles), NW * 32, psmem, st>>>(
+      crt_persistent_kernel<F, NW><<<dim3(per, col_tiles), NW * 32, psmem, st>>>(
           in, count, static_cast<int>(batch), limbs, log_n, w, primes, np, out);
       return cudaGetLastError();
     }
-    return launch<NW>(in, count, limbs, batch, log_n, w, primes, np, out, st);
+    return launch<F, NW>(in, count, limbs, batch, log_n, w, primes, np, out, st);
   });
 }
 
+template <class F>
 cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n,
-                        const CrtWeights& w, const DevPrime* primes, int np, uint64_t* out,
-                        cudaStream_t st) {
-  return crt_forward_multi(&poly, 1, limbs, batch, log_n, w, primes, np, out, st);
+                        const CrtWeights& w, const typename F::Prime* primes, int np,
+                        typename F::W* out, cudaStream_t st) {
+  return crt_forward_multi<F>(&poly, 1, limbs, batch, log_n, w, primes, np, out, st);
 }
+
+#define HEMUL_CRT_INSTANTIATE(F)                                                              \
+  template cudaError_t crt_forward_multi<F>(const uint64_t* const*, int, int, size_t, int,    \
+                                            const CrtWeights&, const F::Prime*, int, F::W*,   \
+                                            cudaStream_t);                                    \
+  template cudaError_t crt_forward<F>(const uint64_t*, int, size_t, int, const CrtWeights&,   \
+                                      const F::Prime*, int, F::W*, cudaStream_t);
+HEMUL_CRT_INSTANTIATE(F64)
+HEMUL_CRT_INSTANTIATE(F32)
+#undef HEMUL_CRT_INSTANTIATE
 
 }  // namespace hemul_gpu

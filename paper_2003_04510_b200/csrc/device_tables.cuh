@@ -31,4 +31,25 @@ struct Twiddle {
   uint64_t w, wq;
 };
 
+// One prime of the B200 30-bit basis (fields.cuh F32); Shoup quotients are
+// floor(w 2^32 / p). No reference counterpart: the HE Mul result does not
+// depend on the basis (see fields.cuh).
+struct DevPrime32 {
+  uint32_t p;
+  uint32_t one_q;   // floor(2^32 / p)
+  uint32_t beta;    // 2^32 mod p
+  uint32_t beta_q;  // floor(beta 2^32 / p)
+  uint32_t inv, inv_q;    // (P / p)^-1 mod p
+  uint32_t ninv, ninv_q;  // n^-1 mod p
+  uint32_t w1n, w1n_q;    // itw[1] n^-1
+  uint32_t pad[2];
+  double inv_p_dbl;       // 1 / p
+  double pad2;
+};
+static_assert(sizeof(DevPrime32) == 64, "DevPrime32 layout");
+
+struct Twiddle32 {
+  uint32_t w, wq;
+};
+
 }  // namespace hemul_gpu

@@ -20,9 +20,9 @@
 
 #include <type_traits>
 
+#include "fields.cuh"
 #include "igemm.cuh"
 #include "kernels.hpp"
-#include "modarith.cuh"
 
 namespace hemul_gpu {
 
@@ -39,40 +39,53 @@ constexpr int kDigit = 25;   // B chunk width == output digit width
 constexpr uint32_t kDigitMask = (1u << kDigit) - 1;
 constexpr int kFixMaxLimbs = 136;
 
+template <class F>
 struct Seg {  // one RNS operand feeding A rows
-  const uint64_t* rns;  // [np][n] of this batch entry
-  const DevPrime* primes;
+  const typename F::W* rns;  // [np][n] of this batch entry
+  const typename F::Prime* primes;
   int np;
 };
 
-// Stage the CTA's residues x_j (32 coefficients, 256 contiguous bytes per
-// prime) straight into the A rows they become: x row j occupies exactly the
-// bytes of A rows row0+2j and row0+2j+1, so every row is one batch of
-// 16-byte cp.async copies with all of them in flight at once. Commits a
-// cp.async group; build_rows waits for it.
-__device__ void stage_rows(const Seg& s, size_t n, size_t c0, uint32_t* A, int row0) {
-  uint64_t* dst = reinterpret_cast<uint64_t*>(A + row0 * kGemmCoefs);
-  for (int idx = threadIdx.x; idx < s.np * 16; idx += blockDim.x) {
-    const int j = idx >> 4, c = 2 * (idx & 15);
+// Stage the CTA's residues x_j (32 coefficients, 32 sizeof(W) contiguous
+// bytes per prime) straight into the A rows they become: x row j occupies
+// exactly the bytes of A rows row0 + R j .. row0 + R j + R - 1 (R =
+// F::kRowsPerPrime), so every row is one batch of 16-byte cp.async copies
+// with all of them in flight at once. The caller commits the group.
+template <class F>
+__device__ void stage_rows(const Seg<F>& s, size_t n, size_t c0, uint32_t* A, int row0) {
+  using W = typename F::W;
+  constexpr int CP = 2 * int(sizeof(W));   // 16-byte chunks per prime row
+  constexpr int EPC = 16 / int(sizeof(W));  // residues per chunk
+  W* dst = reinterpret_cast<W*>(A + row0 * kGemmCoefs);
+  for (int idx = threadIdx.x; idx < s.np * CP; idx += blockDim.x) {
+    const int j = idx / CP, c = EPC * (idx % CP);
     cp_async16(dst + 32 * j + c, s.rns + size_t(j) * n + c0 + c);
   }
 }
 
-// A rows [row0, row0 + 2np + 1) for the CTA's 32 coefficients, in place over
-// the staged x rows: the 30-bit halves of t_j = x_j (P/p_j)^-1 mod p_j and
-// the quotient k (warp w converts primes w, w+NW, ...; lane = coefficient).
-__device__ void build_rows(const Seg& s, uint32_t* A, int row0, double* part, IcrtFlags flags,
+// A rows [row0, row0 + R np + 1) for the CTA's 32 coefficients, in place
+// over the staged x rows: t_j = x_j (P/p_j)^-1 mod p_j (F64: its two 30-bit
+// halves; F32: t_j < 2^30 itself) and the quotient k (warp w converts primes
+// w, w+NW, ...; lane = coefficient).
+template <class F>
+__device__ void build_rows(const Seg<F>& s, uint32_t* A, int row0, double* part, IcrtFlags flags,
                            size_t id0) {
+  using W = typename F::W;
+  constexpr int R = F::kRowsPerPrime;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double acc = 0;
-  const uint64_t* xs = reinterpret_cast<const uint64_t*>(A + row0 * kGemmCoefs);
+  const W* xs = reinterpret_cast<const W*>(A + row0 * kGemmCoefs);
   for (int j = warp; j < s.np; j += nw) {
-    const DevPrime& pr = s.primes[j];
-    const uint64_t x = xs[32 * j + lane];
+    const typename F::Prime& pr = s.primes[j];
+    const W x = xs[32 * j + lane];
     __syncwarp();  // the whole row is read before any lane overwrites it
-    const uint64_t t = shoup_mul(x, pr.inv, pr.inv_q, pr.p);
-    A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
-    A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
+    const uint64_t t = F::hat_inv(x, pr);
+    if (R == 2) {
+      A[(row0 + 2 * j) * kGemmCoefs + lane] = static_cast<uint32_t>(t) & 0x3fffffffu;
+      A[(row0 + 2 * j + 1) * kGemmCoefs + lane] = static_cast<uint32_t>(t >> 30);
+    } else {
+      A[(row0 + j) * kGemmCoefs + lane] = static_cast<uint32_t>(t);
+    }
     acc += static_cast<double>(t) * pr.inv_p_dbl;
   }
   part[warp * 32 + lane] = acc;
@@ -81,7 +94,7 @@ __device__ void build_rows(const Seg& s, uint32_t* A, int row0, double* part, Ic
     double tot = 0;
     for (int w = 0; w < nw; ++w) tot += part[w * 32 + lane];
     const double k = rint(tot);
-    A[(row0 + 2 * s.np) * kGemmCoefs + lane] = static_cast<uint32_t>(k);
+    A[(row0 + R * s.np) * kGemmCoefs + lane] = static_cast<uint32_t>(k);
     if (flags.count && fabs(tot - k) > 0.25) {
       const unsigned slot = atomicAdd(flags.count, 1u);
       if (slot < flags.capacity) flags.ids[slot] = static_cast<unsigned>(id0 + lane);
@@ -171,10 +184,10 @@ __device__ void carry_digits(const uint64_t* S, int lds, uint32_t* D, int ldd, i
   __syncthreads();
 }
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restrict__ rns,
+template <class F, int NW>
+__global__ void __launch_bounds__(NW * 32) icrt_kernel(const typename F::W* __restrict__ rns,
                                                        int log_n,
-                                                       const DevPrime* __restrict__ primes,
+                                                       const typename F::Prime* __restrict__ primes,
                                                        int np, IcrtTable t,
                                                        uint64_t* __restrict__ out,
                                                        IcrtFlags flags) {
@@ -182,7 +195,7 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
   const size_t n = size_t(1) << log_n;
   const int b = blockIdx.y;
   const size_t c0 = size_t(blockIdx.x) * kGemmCoefs;
-  const int K = 2 * np + 1;
+  const int K = F::kRowsPerPrime * np + 1;
   constexpr int NC = 16 * NW;
   uint32_t* A = reinterpret_cast<uint32_t*>(smem);                     // [K][32]
   uint32_t* Bs = A + K * kGemmCoefs;                                   // cp.async ring
@@ -191,7 +204,7 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
   const int lds = t.m_pad + 1, ldd = t.m_out | 1;
   uint64_t* S = reinterpret_cast<uint64_t*>(part + NW * 32);       // [32][lds]
   uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * lds);  // [32][ldd]
-  const Seg seg{rns + size_t(b) * np * n, primes, np};
+  const Seg<F> seg{rns + size_t(b) * np * n, primes, np};
   stage_rows(seg, n, c0, A, 0);
   cp_async_commit();
   cp_async_wait<0>();
@@ -217,15 +230,15 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const uint64_t* __restric
 }
 
 // Exact centered value mod 2^tbits (rns.cpp:148-169, 192-233), one thread.
-__device__ void exact_centered(const uint64_t* rns_b, size_t n, size_t i,
-                               const DevPrime* primes, int np, const IcrtTable& t, int tbits,
-                               uint64_t* o /* ceil(tbits/64) limbs */) {
+template <class F>
+__device__ void exact_centered(const typename F::W* rns_b, size_t n, size_t i,
+                               const typename F::Prime* primes, int np, const IcrtTable& t,
+                               int tbits, uint64_t* o /* ceil(tbits/64) limbs */) {
   const int pl = t.p_limbs, al = pl + 2;
   uint64_t acc[kFixMaxLimbs];
   for (int k = 0; k < al; ++k) acc[k] = 0;
   for (int j = 0; j < np; ++j) {
-    const DevPrime& pr = primes[j];
-    const uint64_t tj = shoup_mul(rns_b[size_t(j) * n + i], pr.inv, pr.inv_q, pr.p);
+    const uint64_t tj = F::hat_inv(rns_b[size_t(j) * n + i], primes[j]);
     const uint64_t* h = t.hat + size_t(j) * pl;
     uint64_t carry = 0;
     for (int k = 0; k < al; ++k) {
@@ -271,27 +284,29 @@ __device__ void exact_centered(const uint64_t* rns_b, size_t n, size_t i,
   if (tbits % 64) o[tl - 1] &= (uint64_t(1) << (tbits % 64)) - 1;
 }
 
-__global__ void icrt_fixup_kernel(const uint64_t* __restrict__ rns, int log_n,
-                                  const DevPrime* __restrict__ primes, int np, IcrtTable t,
-                                  uint64_t* __restrict__ out, IcrtFlags flags) {
+template <class F>
+__global__ void icrt_fixup_kernel(const typename F::W* __restrict__ rns, int log_n,
+                                  const typename F::Prime* __restrict__ primes, int np,
+                                  IcrtTable t, uint64_t* __restrict__ out, IcrtFlags flags) {
   const unsigned cnt = min(*flags.count, flags.capacity);
   const size_t n = size_t(1) << log_n;
   const int tl = (t.target_bits + 63) / 64;
   for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < cnt; f += gridDim.x * blockDim.x) {
     const size_t id = flags.ids[f];
     const size_t b = id / n, i = id % n;
-    exact_centered(rns + b * np * n, n, i, primes, np, t, t.target_bits, out + (b * n + i) * tl);
+    exact_centered<F>(rns + b * np * n, n, i, primes, np, t, t.target_bits, out + (b * n + i) * tl);
   }
 }
 
 // ---- fused key-switch finisher ----------------------------------------------
 
-template <int NW>
+template <class F, int NW>
 __global__ void __launch_bounds__(NW * 32, kFinMinBlocks) finish_kernel(
-    const uint64_t* __restrict__ ks, const uint64_t* __restrict__ d_ax,
-    const uint64_t* __restrict__ d_bx, int B, int log_n, const DevPrime* __restrict__ p2, int np2,
-    const DevPrime* __restrict__ p1, int np1, Finisher f, uint64_t* __restrict__ out_ax,
-    uint64_t* __restrict__ out_bx, IcrtFlags flags, int force_exact) {
+    const typename F::W* __restrict__ ks, const typename F::W* __restrict__ d_ax,
+    const typename F::W* __restrict__ d_bx, int B, int log_n,
+    const typename F::Prime* __restrict__ p2, int np2, const typename F::Prime* __restrict__ p1,
+    int np1, Finisher f, uint64_t* __restrict__ out_ax, uint64_t* __restrict__ out_bx,
+    IcrtFlags flags, int force_exact) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int flagged[kGemmCoefs];
   const size_t n = size_t(1) << log_n;
@@ -304,8 +319,8 @@ __global__ void __launch_bounds__(NW * 32, kFinMinBlocks) finish_kernel(
   uint32_t* A = reinterpret_cast<uint32_t*>(smem);
   uint32_t* Bs = A + K * kGemmCoefs;
   double* part = reinterpret_cast<double*>(Bs + kFinStages * kFinKT * NC);
-  const Seg s2{ks + size_t(bb) * np2 * n, p2, np2};
-  const Seg s1{(is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, p1, np1};
+  const Seg<F> s2{ks + size_t(bb) * np2 * n, p2, np2};
+  const Seg<F> s1{(is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, p1, np1};
   const IcrtFlags none{};
   stage_rows(s2, n, c0, A, 0);
   stage_rows(s1, n, c0, A, f.k2);
@@ -370,11 +385,12 @@ __device__ __forceinline__ void add_shifted(uint64_t* s, int len, int bit, uint6
 // Exact recomputation of flagged finisher coefficients: X2 and X1 by the
 // reference algorithm, then bits [logQ+logp, logQ+logq) of
 // X2 + 2^(logQ-1) + 2^logQ (X1 + 2^(logp-1)) mod 2^(logq+logQ).
-__global__ void finish_fixup_kernel(const uint64_t* __restrict__ ks,
-                                    const uint64_t* __restrict__ d_ax,
-                                    const uint64_t* __restrict__ d_bx, int B, int log_n,
-                                    const DevPrime* __restrict__ p2, int np2,
-                                    const DevPrime* __restrict__ p1, int np1, Finisher f,
+template <class F>
+__global__ void finish_fixup_kernel(const typename F::W* __restrict__ ks,
+                                    const typename F::W* __restrict__ d_ax,
+                                    const typename F::W* __restrict__ d_bx, int B, int log_n,
+                                    const typename F::Prime* __restrict__ p2, int np2,
+                                    const typename F::Prime* __restrict__ p1, int np1, Finisher f,
                                     IcrtTable t2, IcrtTable t1, uint64_t* __restrict__ out_ax,
                                     uint64_t* __restrict__ out_bx, IcrtFlags flags) {
   const unsigned cnt = min(*flags.count, flags.capacity);
@@ -390,8 +406,9 @@ __global__ void finish_fixup_kernel(const uint64_t* __restrict__ ks,
     const bool is_bx = bb >= B;
     const int b = is_bx ? bb - B : bb;
     uint64_t x2[kFixMaxLimbs], x1[kFixMaxLimbs];
-    exact_centered(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2);
-    exact_centered((is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, n, i, p1, np1, t1, f.log_q, x1);
+    exact_centered<F>(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2);
+    exact_centered<F>((is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, n, i, p1, np1, t1, f.log_q,
+                      x1);
     add_shifted(x2, l2, f.log_Q - 1, 1);
     add_shifted(x1, l1, f.log_p - 1, 1);
     for (int k = 0; k < l1; ++k) add_shifted(x2, l2, f.log_Q + 64 * k, x1[k]);
@@ -408,9 +425,9 @@ __global__ void finish_fixup_kernel(const uint64_t* __restrict__ ks,
   }
 }
 
-template <int NW>
+template <class F, int NW>
 size_t icrt_smem(int np, int m_pad) {
-  return size_t(2 * np + 1) * kGemmCoefs * 4 + size_t(kStages) * kKT * 16 * NW * 4 +
+  return size_t(F::kRowsPerPrime * np + 1) * kGemmCoefs * 4 + size_t(kStages) * kKT * 16 * NW * 4 +
          NW * 32 * 8 + size_t(kGemmCoefs) * (m_pad + 1) * 12;
 }
 
@@ -423,25 +440,26 @@ size_t finish_smem(const Finisher& f) {
   return main > epi ? main : epi;
 }
 
-template <int NW>
-cudaError_t launch_icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* primes,
-                        int np, const IcrtTable& t, uint64_t* out, cudaStream_t st,
-                        IcrtFlags f) {
+template <class F, int NW>
+cudaError_t launch_icrt(const typename F::W* rns, size_t batch, int log_n,
+                        const typename F::Prime* primes, int np, const IcrtTable& t,
+                        uint64_t* out, cudaStream_t st, IcrtFlags f) {
   const size_t n = size_t(1) << log_n;
   dim3 grid(static_cast<unsigned>(n / kGemmCoefs), static_cast<unsigned>(batch));
-  icrt_kernel<NW><<<grid, NW * 32, icrt_smem<NW>(np, t.m_pad), st>>>(rns, log_n, primes, np, t,
-                                                                     out, f);
+  icrt_kernel<F, NW><<<grid, NW * 32, icrt_smem<F, NW>(np, t.m_pad), st>>>(rns, log_n, primes,
+                                                                           np, t, out, f);
   return cudaGetLastError();
 }
 
-template <int NW>
-cudaError_t launch_finish(const uint64_t* ks, const uint64_t* d_ax, const uint64_t* d_bx,
-                          size_t B, int log_n, const DevPrime* p2, int np2, const DevPrime* p1,
+template <class F, int NW>
+cudaError_t launch_finish(const typename F::W* ks, const typename F::W* d_ax,
+                          const typename F::W* d_bx, size_t B, int log_n,
+                          const typename F::Prime* p2, int np2, const typename F::Prime* p1,
                           int np1, const Finisher& f, uint64_t* out_ax, uint64_t* out_bx,
                           const IcrtFlags& flags, int force_exact, cudaStream_t st) {
   const size_t n = size_t(1) << log_n;
   dim3 grid(static_cast<unsigned>(n / kGemmCoefs), static_cast<unsigned>(2 * B));
-  finish_kernel<NW><<<grid, NW * 32, finish_smem<NW>(f), st>>>(
+  finish_kernel<F, NW><<<grid, NW * 32, finish_smem<NW>(f), st>>>(
       ks, d_ax, d_bx, static_cast<int>(B), log_n, p2, np2, p1, np1, f, out_ax, out_bx, flags,
       force_exact);
   return cudaGetLastError();
@@ -471,35 +489,43 @@ cudaError_t with_nw(int cols_pad, F&& f) {
   }
 }
 
-template <int NW>
+template <class F, int NW>
 cudaError_t set_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(icrt_kernel<NW>,
+  cudaError_t e = cudaFuncSetAttribute(icrt_kernel<F, NW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(finish_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(finish_kernel<F, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kMaxDynSmem);
+}
+
+template <class F>
+cudaError_t set_all_attrs() {
+  cudaError_t e;
+  if ((e = set_attrs<F, 1>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, 2>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, 3>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, 4>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, 5>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, 6>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, 7>()) != cudaSuccess) return e;
+  return set_attrs<F, 8>();
 }
 
 }  // namespace
 
 cudaError_t icrt_setup_attributes() {
-  cudaError_t e;
-  if ((e = set_attrs<1>()) != cudaSuccess) return e;
-  if ((e = set_attrs<2>()) != cudaSuccess) return e;
-  if ((e = set_attrs<3>()) != cudaSuccess) return e;
-  if ((e = set_attrs<4>()) != cudaSuccess) return e;
-  if ((e = set_attrs<5>()) != cudaSuccess) return e;
-  if ((e = set_attrs<6>()) != cudaSuccess) return e;
-  if ((e = set_attrs<7>()) != cudaSuccess) return e;
-  return set_attrs<8>();
+  cudaError_t e = set_all_attrs<F64>();
+  return e != cudaSuccess ? e : set_all_attrs<F32>();
 }
 
 cudaError_t finisher_setup_attributes() { return cudaSuccess; }
 
-cudaError_t icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* primes, int np,
-                 const IcrtTable& t, uint64_t* out, cudaStream_t st, const IcrtFlags* flags) {
+template <class F>
+cudaError_t icrt(const typename F::W* rns, size_t batch, int log_n,
+                 const typename F::Prime* primes, int np, const IcrtTable& t, uint64_t* out,
+                 cudaStream_t st, const IcrtFlags* flags) {
   const size_t n = size_t(1) << log_n;
-  if (n < kGemmCoefs || 2 * np + 1 > kMaxGemmK) return cudaErrorInvalidValue;
+  if (n < kGemmCoefs || F::kRowsPerPrime * np + 1 > kMaxGemmK) return cudaErrorInvalidValue;
   IcrtFlags f;
   if (flags) {
     if (t.p_limbs + 2 > kFixMaxLimbs) return cudaErrorInvalidValue;
@@ -508,16 +534,18 @@ cudaError_t icrt(const uint64_t* rns, size_t batch, int log_n, const DevPrime* p
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = with_nw(t.m_pad, [&](auto nw) {
-    return launch_icrt<decltype(nw)::value>(rns, batch, log_n, primes, np, t, out, st, f);
+    return launch_icrt<F, decltype(nw)::value>(rns, batch, log_n, primes, np, t, out, st, f);
   });
   if (e != cudaSuccess || !flags) return e;
-  icrt_fixup_kernel<<<64, 64, 0, st>>>(rns, log_n, primes, np, t, out, f);
+  icrt_fixup_kernel<F><<<64, 64, 0, st>>>(rns, log_n, primes, np, t, out, f);
   return cudaGetLastError();
 }
 
-cudaError_t finish_keyswitch(const uint64_t* ks, const uint64_t* d_ax, const uint64_t* d_bx,
-                             size_t B, int log_n, const DevPrime* p2, int np2,
-                             const DevPrime* p1, int np1, const Finisher& f,
+template <class F>
+cudaError_t finish_keyswitch(const typename F::W* ks, const typename F::W* d_ax,
+                             const typename F::W* d_bx, size_t B, int log_n,
+                             const typename F::Prime* p2, int np2, const typename F::Prime* p1,
+                             int np1, const Finisher& f,
                              const IcrtTable& t2, const IcrtTable& t1, uint64_t* out_ax,
                              uint64_t* out_bx, const IcrtFlags& flags, int force_exact,
                              cudaStream_t st) {
@@ -528,13 +556,25 @@ cudaError_t finish_keyswitch(const uint64_t* ks, const uint64_t* d_ax, const uin
   cudaError_t e = cudaMemsetAsync(flags.count, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   e = with_nw(f.cols_pad, [&](auto nw) {
-    return launch_finish<decltype(nw)::value>(ks, d_ax, d_bx, B, log_n, p2, np2, p1, np1, f,
+    return launch_finish<F, decltype(nw)::value>(ks, d_ax, d_bx, B, log_n, p2, np2, p1, np1, f,
                                               out_ax, out_bx, flags, force_exact, st);
   });
   if (e != cudaSuccess) return e;
-  finish_fixup_kernel<<<64, 64, 0, st>>>(ks, d_ax, d_bx, static_cast<int>(B), log_n, p2, np2, p1,
+  finish_fixup_kernel<F><<<64, 64, 0, st>>>(ks, d_ax, d_bx, static_cast<int>(B), log_n, p2, np2, p1,
                                          np1, f, t2, t1, out_ax, out_bx, flags);
   return cudaGetLastError();
 }
+
+#define HEMUL_ICRT_INSTANTIATE(F)                                                             \
+  template cudaError_t icrt<F>(const F::W*, size_t, int, const F::Prime*, int,                \
+                               const IcrtTable&, uint64_t*, cudaStream_t, const IcrtFlags*);  \
+  template cudaError_t finish_keyswitch<F>(const F::W*, const F::W*, const F::W*, size_t, int, \
+                                           const F::Prime*, int, const F::Prime*, int,         \
+                                           const Finisher&, const IcrtTable&,                  \
+                                           const IcrtTable&, uint64_t*, uint64_t*,             \
+                                           const IcrtFlags&, int, cudaStream_t);
+HEMUL_ICRT_INSTANTIATE(F64)
+HEMUL_ICRT_INSTANTIATE(F32)
+#undef HEMUL_ICRT_INSTANTIATE
 
 }  // namespace hemul_gpu

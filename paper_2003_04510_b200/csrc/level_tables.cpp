@@ -49,6 +49,15 @@ bool is_prime(uint64_t n) {
 }
 
 uint64_t shoup_q(uint64_t w, uint64_t p) { return uint64_t((u128(w) << 64) / p); }
+uint32_t shoup_q32(uint64_t w, uint64_t p) { return uint32_t((w << 32) / p); }
+
+// smallest generator power of exact order 2n (params.cpp:49-54)
+uint64_t min_root(uint64_t p, uint64_t two_n) {
+  for (uint64_t g = 2;; ++g) {
+    const uint64_t psi = powmod(g, (p - 1) / two_n, p);
+    if (powmod(psi, two_n / 2, p) == p - 1) return psi;
+  }
+}
 
 // little-endian natural number
 using Nat = std::vector<uint64_t>;
@@ -166,116 +175,180 @@ void generate_primes(int count, int log_n, std::vector<uint64_t>& primes,
     if (c <= floor_) throw std::runtime_error("prime range exhausted for this ring degree");
     if (!is_prime(c)) continue;
     primes.push_back(c);
-    // smallest generator power of exact order 2n (params.cpp:49-54)
-    for (uint64_t g = 2;; ++g) {
-      const uint64_t psi = powmod(g, (c - 1) / two_n, c);
-      if (powmod(psi, two_n / 2, c) == c - 1) {
-        roots.push_back(psi);
-        break;
-      }
-    }
+    roots.push_back(min_root(c, two_n));
+  }
+}
+
+void generate_primes30(int count, int log_n, std::vector<uint64_t>& primes,
+                       std::vector<uint64_t>& roots) {
+  const uint64_t two_n = uint64_t(1) << (log_n + 1);
+  const uint64_t top = (uint64_t(1) << kPrime30Bits) - 1, floor_ = uint64_t(1) << 20;
+  primes.clear();
+  roots.clear();
+  for (uint64_t c = top - (top - 1) % two_n; int(primes.size()) < count; c -= two_n) {
+    if (c <= floor_ || c < two_n)
+      throw std::runtime_error("30-bit prime range exhausted for this ring degree");
+    if (!is_prime(c)) continue;
+    primes.push_back(c);
+    roots.push_back(min_root(c, two_n));
   }
 }
 
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
-                        const std::vector<int>& crt_bits, int threads) {
+                        const std::vector<int>& crt_bits, int threads, int word) {
   RegionHost r;
   r.region = region;
   r.log_n = log_n;
+  r.word = word;
   const int n = 1 << log_n;
-  // prime count with the grow-until-bound loop of heaan.cpp:132-135 / 139-143
-  const int bound = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n + 1;
-  int count = region == 1 ? prime_count(2 * log_q, log_n)
-                          : prime_count(log_q + 2 * log_q_max, log_n);
-  Nat P;
-  for (;; ++count) {
-    generate_primes(count, log_n, r.primes, r.roots);
-    P.assign(1, 1);
-    for (uint64_t p : r.primes) nat_mul_word(P, p);
-    if (nat_bits(P) > bound) break;  // P >= 2^bound
-  }
-  r.np = count;
-  r.target_bits = region == 1 ? log_q : log_q + log_q_max;
   // Largest |v| the iCRT must recover: region 1 carries d1 = A1 B2 + A2 B1,
   // |v| < 2 n q^2; region 2 carries d2 * evk, |v| < n q Q^2.
   const int vbits = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n;
+  Nat P;
+  int count;
+  if (word == 64) {
+    // prime count with the grow-until-bound loop of heaan.cpp:132-135 / 139-143
+    const int bound = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n + 1;
+    count = region == 1 ? prime_count(2 * log_q, log_n) : prime_count(log_q + 2 * log_q_max, log_n);
+    for (;; ++count) {
+      generate_primes(count, log_n, r.primes, r.roots);
+      P.assign(1, 1);
+      for (uint64_t p : r.primes) nat_mul_word(P, p);
+      if (nat_bits(P) > bound) break;  // P >= 2^bound
+    }
+  } else {
+    // the B200 basis: the fewest 30-bit primes that leave the iCRT headroom
+    count = (vbits + 2 + kMinSlackBits) / kPrime30Bits;
+    for (;; ++count) {
+      generate_primes30(count, log_n, r.primes, r.roots);
+      P.assign(1, 1);
+      for (uint64_t p : r.primes) nat_mul_word(P, p);
+      if ((nat_bits(P) - 1) - 1 - vbits >= kMinSlackBits) break;
+    }
+  }
+  r.np = count;
+  r.target_bits = region == 1 ? log_q : log_q + log_q_max;
   r.slack_bits = (nat_bits(P) - 1) - 1 - vbits;
-  if (r.slack_bits < 4)
+  if (r.slack_bits < kMinSlackBits)
     throw std::runtime_error("prime set leaves less than 4 bits of iCRT headroom");
 
   // per-prime constants
-  r.dev.resize(count);
   std::vector<Nat> hat(count);
+  std::vector<uint64_t> inv(count), ninv(count);
   for (int j = 0; j < count; ++j) {
     const uint64_t p = r.primes[j];
-    DevPrime& d = r.dev[j];
-    d = DevPrime{};
-    d.p = p;
-    d.one_q = shoup_q(1, p);
-    d.beta = uint64_t((u128(1) << 64) % p);
-    d.beta_q = shoup_q(d.beta, p);
     uint64_t hat_mod = 0;
     hat[j] = nat_div_word(P, p, nullptr);
     nat_div_word(hat[j], p, &hat_mod);
-    d.inv = powmod(hat_mod, p - 2, p);
-    d.inv_q = shoup_q(d.inv, p);
-    d.ninv = powmod(uint64_t(n) % p, p - 2, p);
-    d.ninv_q = shoup_q(d.ninv, p);
-    d.inv_p_dbl = 1.0 / double(p);
+    inv[j] = powmod(hat_mod, p - 2, p);
+    ninv[j] = powmod(uint64_t(n) % p, p - 2, p);
+  }
+  if (word == 64) {
+    r.dev.resize(count);
+    for (int j = 0; j < count; ++j) {
+      const uint64_t p = r.primes[j];
+      DevPrime& d = r.dev[j];
+      d = DevPrime{};
+      d.p = p;
+      d.one_q = shoup_q(1, p);
+      d.beta = uint64_t((u128(1) << 64) % p);
+      d.beta_q = shoup_q(d.beta, p);
+      d.inv = inv[j];
+      d.inv_q = shoup_q(d.inv, p);
+      d.ninv = ninv[j];
+      d.ninv_q = shoup_q(d.ninv, p);
+      d.inv_p_dbl = 1.0 / double(p);
+    }
+    r.tw.resize(size_t(count) * n);
+    r.itw.resize(size_t(count) * n);
+  } else {
+    r.dev32.resize(count);
+    for (int j = 0; j < count; ++j) {
+      const uint64_t p = r.primes[j];
+      DevPrime32& d = r.dev32[j];
+      d = DevPrime32{};
+      d.p = uint32_t(p);
+      d.one_q = shoup_q32(1, p);
+      d.beta = uint32_t((uint64_t(1) << 32) % p);
+      d.beta_q = shoup_q32(d.beta, p);
+      d.inv = uint32_t(inv[j]);
+      d.inv_q = shoup_q32(inv[j], p);
+      d.ninv = uint32_t(ninv[j]);
+      d.ninv_q = shoup_q32(ninv[j], p);
+      d.inv_p_dbl = 1.0 / double(p);
+    }
+    r.tw32.resize(size_t(count) * n);
+    r.itw32.resize(size_t(count) * n);
   }
 
   // twiddles: tw[j*n + i] = psi^rev(i), itw = psi^-rev(i) (params.cpp:151-180)
-  r.tw.resize(size_t(count) * n);
-  r.itw.resize(size_t(count) * n);
   parallel_for(count, threads, [&](int j) {
     const uint64_t p = r.primes[j], psi = r.roots[j];
     const uint64_t psi_inv = powmod(psi, p - 2, p);
-    uint64_t pw = 1, ipw = 1;
+    uint64_t pw = 1, ipw = 1, itw1 = 1;
     for (int i = 0; i < n; ++i) {
       const uint32_t k = bit_reverse(uint32_t(i), log_n);
-      r.tw[size_t(j) * n + k] = Twiddle{pw, shoup_q(pw, p)};
-      r.itw[size_t(j) * n + k] = Twiddle{ipw, shoup_q(ipw, p)};
+      if (k == 1) itw1 = ipw;
+      if (word == 64) {
+        r.tw[size_t(j) * n + k] = Twiddle{pw, shoup_q(pw, p)};
+        r.itw[size_t(j) * n + k] = Twiddle{ipw, shoup_q(ipw, p)};
+      } else {
+        r.tw32[size_t(j) * n + k] = Twiddle32{uint32_t(pw), shoup_q32(pw, p)};
+        r.itw32[size_t(j) * n + k] = Twiddle32{uint32_t(ipw), shoup_q32(ipw, p)};
+      }
       pw = mulmod(pw, psi, p);
       ipw = mulmod(ipw, psi_inv, p);
     }
-    DevPrime& d = r.dev[j];
-    const uint64_t w1n = n > 1 ? mulmod(r.itw[size_t(j) * n + 1].w, d.ninv, p) : d.ninv;
-    d.w1n = w1n;
-    d.w1n_q = shoup_q(w1n, p);
+    const uint64_t w1n = n > 1 ? mulmod(itw1, ninv[j], p) : ninv[j];
+    if (word == 64) {
+      r.dev[j].w1n = w1n;
+      r.dev[j].w1n_q = shoup_q(w1n, p);
+    } else {
+      r.dev32[j].w1n = uint32_t(w1n);
+      r.dev32[j].w1n_q = shoup_q32(w1n, p);
+    }
   });
 
-  // CRT weights: 30-bit halves of 2^(25 m) mod p_j (kernels.hpp CrtWeights)
+  // CRT weights of 2^(25 m) mod p_j (kernels.hpp CrtWeights): w64 as two
+  // 30-bit halves, the 30-bit basis as one column
+  const int wcols = word == 64 ? 2 : 1;
   for (int bits : crt_bits) {
     RegionHost::Crt c;
     c.in_bits = bits;
     c.chunks = (bits + kChunkBits - 1) / kChunkBits;
-    c.ld = crt_cols_pad(2 * count);
+    c.ld = crt_cols_pad(wcols * count);
     c.wtab.assign(size_t(c.chunks) * c.ld, 0);
     for (int j = 0; j < count; ++j) {
       const uint64_t p = r.primes[j];
       const uint64_t step = powmod(2, kChunkBits, p);
       uint64_t u = 1 % p;
       for (int m = 0; m < c.chunks; ++m) {
-        c.wtab[size_t(m) * c.ld + 2 * j] = uint32_t(u & 0x3fffffffu);
-        c.wtab[size_t(m) * c.ld + 2 * j + 1] = uint32_t(u >> 30);
+        if (wcols == 2) {
+          c.wtab[size_t(m) * c.ld + 2 * j] = uint32_t(u & 0x3fffffffu);
+          c.wtab[size_t(m) * c.ld + 2 * j + 1] = uint32_t(u >> 30);
+        } else {
+          c.wtab[size_t(m) * c.ld + j] = uint32_t(u);
+        }
         u = mulmod(u, step, p);
       }
     }
     r.crt.push_back(std::move(c));
   }
 
-  // iCRT operands mod 2^T: H_j, H_j 2^30 (for the high 30-bit half of t_j)
-  // and (-P), then the 25-bit-chunk table rows of the same order
+  // iCRT operands mod 2^T in A-row order: w64 H_j, H_j 2^30 (the two 30-bit
+  // halves of t_j), the 30-bit basis H_j; then (-P). Then the 25-bit-chunk
+  // table rows of the same order.
   const int T = r.target_bits;
-  r.hat_t.resize(2 * count + 1);
+  const int R = word == 64 ? 2 : 1;
+  r.hat_t.resize(R * count + 1);
   for (int j = 0; j < count; ++j) {
-    r.hat_t[2 * j] = nat_low(hat[j], T);
-    r.hat_t[2 * j + 1] = nat_shl_low(hat[j], 30, T);
+    r.hat_t[R * j] = nat_low(hat[j], T);
+    if (R == 2) r.hat_t[2 * j + 1] = nat_shl_low(hat[j], 30, T);
   }
-  r.hat_t[2 * count] = nat_neg_mod_pow2(P, T);
+  r.hat_t[R * count] = nat_neg_mod_pow2(P, T);
   r.m_out = (T + kChunkBits - 1) / kChunkBits;
   r.m_pad = (r.m_out + 15) / 16 * 16;
-  const int K = 2 * count + 1;
+  const int K = R * count + 1;
   r.btab.assign(size_t(K) * r.m_pad, 0);
   for (int row = 0; row < K; ++row)
     for (int m = 0; m < r.m_out; ++m)
@@ -304,8 +377,8 @@ FinisherHost build_finisher(const RegionHost& r1, const RegionHost& r2, int log_
   f.width = T2 - f.base;
   f.cols = (f.width + kChunkBits - 1) / kChunkBits;
   f.cols_pad = (f.cols + 15) / 16 * 16;
-  f.k2 = 2 * r2.np + 1;
-  f.k1 = 2 * r1.np + 1;
+  f.k2 = static_cast<int>(r2.hat_t.size());
+  f.k1 = static_cast<int>(r1.hat_t.size());
   const int K = f.k2 + f.k1;
   f.btab.assign(size_t(K) * f.cols_pad, 0);
   for (int row = 0; row < f.k2; ++row)

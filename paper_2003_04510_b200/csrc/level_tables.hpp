@@ -15,23 +15,32 @@ int prime_count(int bound_bits, int log_n);
 // smallest-c primitive 2n-th roots. Throws std::runtime_error when exhausted.
 void generate_primes(int count, int log_n, std::vector<uint64_t>& primes,
                      std::vector<uint64_t>& roots);
+// The B200 basis (fields.cuh F32): the same rule below 2^30.
+constexpr int kPrime30Bits = 30;
+void generate_primes30(int count, int log_n, std::vector<uint64_t>& primes,
+                       std::vector<uint64_t>& roots);
+// iCRT headroom every he_mul region keeps (icrt.cu: fp64 quotient argument)
+constexpr int kMinSlackBits = 4;
 
 struct RegionHost {
   int region = 0;
+  int word = 64;  // 64: reference w64 primes (F64), 32: 30-bit basis (F32)
   int np = 0;
   int log_n = 0;
   int target_bits = 0;  // log_q (region 1) or log_q + log_Q (region 2)
   int slack_bits = 0;   // log2(P) - log2(2 * max|v|), the iCRT headroom
   std::vector<uint64_t> primes, roots;
-  std::vector<DevPrime> dev;         // np
-  std::vector<Twiddle> tw, itw;      // np * n each, ShoupPair tables
+  std::vector<DevPrime> dev;         // np (word 64)
+  std::vector<Twiddle> tw, itw;      // np * n each, ShoupPair tables (word 64)
+  std::vector<DevPrime32> dev32;     // np (word 32)
+  std::vector<Twiddle32> tw32, itw32;  // np * n each (word 32)
   // CRT weights per input width (see kernels.hpp CrtWeights)
   struct Crt {
     int in_bits = 0, chunks = 0, ld = 0;
     std::vector<uint32_t> wtab;
   };
   std::vector<Crt> crt;
-  // iCRT operands mod 2^T, rows in A order: H_j, H_j 2^30, ..., (-P)
+  // iCRT operands mod 2^T, rows in A order: H_j[, H_j 2^30], ..., (-P)
   std::vector<std::vector<uint64_t>> hat_t;
   // iCRT table (see kernels.hpp IcrtTable): hat_t rows in 25-bit chunks
   int m_out = 0, m_pad = 0;
@@ -45,9 +54,11 @@ struct RegionHost {
 // Region 2: key switching, prime product >= 2^(log_q + 2 log_Q + log_n + 1),
 // target 2^(log_q + log_Q) (heaan.cpp:139-147). crt_bits lists the input
 // widths the region must convert (log_q; region 2 also 2 log_Q for the evk).
-// threads > 1 parallelises the twiddle tables.
+// threads > 1 parallelises the twiddle tables. word 64: the reference's
+// primes and prime count; word 32: the fewest 30-bit primes with
+// kMinSlackBits of iCRT headroom.
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
-                        const std::vector<int>& crt_bits, int threads);
+                        const std::vector<int>& crt_bits, int threads, int word = 64);
 
 // Chunk width of the iCRT GEMM's B operand (products 30 x 25 bits, see
 // igemm.cuh) and the fraction window kept below bit log_Q by the fused

@@ -29,8 +29,8 @@
 #include <cuda_runtime.h>
 
 #include "device_tables.cuh"
+#include "fields.cuh"
 #include "kernels.hpp"
-#include "modarith.cuh"
 
 namespace hemul_gpu {
 
@@ -38,31 +38,49 @@ namespace {
 
 constexpr int kLogPassElems = 12;  // 4096 residues per CTA
 
-// Lazy Cooley-Tukey butterfly, one conditional subtraction: a, b in [0, 8p)
-// -> [0, 8p). u = a mod 4p in [0, 4p), v = b w mod p in [0, 4p) (approximate
-// Shoup quotient), a' = u + v < 8p, b' = u + 4p - v in (0, 8p). 8p < 2^63
-// for p < 2^60, so every intermediate fits (Harvey's bounds, one level wider).
-__device__ __forceinline__ void ct_bfly(uint64_t& a, uint64_t& b, uint64_t w, uint64_t wq,
-                                        uint64_t p4, uint64_t negp) {
-  const uint64_t u = csub(a, p4);
-  const uint64_t v = shoup_mul_4p(b, w, wq, negp);
-  a = u + v;
-  b = u + p4 - v;
+// Shared-memory slot of residue index i. In every radix-8 group a warp's 32
+// lanes take the lowest five index bits that are not the group's butterfly
+// (v) bits, so whenever the three v bits sit below bit 5 the lanes spill into
+// bits 5..7 and, with 32-bit residues, land in the same banks. XOR-ing bits
+// 5, 6, 7 into the bank bits with the masks 31, 21, 25 makes the lanes' banks
+// distinct for every position of the v bits (any group of 1..3 levels, any
+// pass layout). The map is linear, so swz(base + off) = swz(base) ^ swz(off)
+// for disjoint bit fields and compile-time offsets fold into immediates.
+// 64-bit residues keep the identity layout.
+template <class W>
+__host__ __device__ constexpr int swz(int i) {
+  return sizeof(W) != 4 ? i
+                        : i ^ (((i >> 5) & 1) * 31) ^ (((i >> 6) & 1) * 21) ^ (((i >> 7) & 1) * 25);
 }
 
-// Lazy Gentleman-Sande butterfly, one conditional subtraction: a, b in
-// [0, 4p) -> [0, 4p).
-__device__ __forceinline__ void gs_bfly(uint64_t& a, uint64_t& b, uint64_t w, uint64_t wq,
-                                        uint64_t p4, uint64_t negp) {
-  const uint64_t u = a, v = b;
-  a = csub(u + v, p4);
-  b = shoup_mul_4p(u + p4 - v, w, wq, negp);
+// 16-byte vector r of a contiguous block <-> swizzled shared slots
+template <class W>
+__device__ __forceinline__ void put_vec(W* sb, uint4* sv, int r, uint4 v) {
+  if constexpr (sizeof(W) == 4) {
+    const int e = swz<W>(4 * r);
+    sb[e] = v.x;
+    sb[e ^ 1] = v.y;
+    sb[e ^ 2] = v.z;
+    sb[e ^ 3] = v.w;
+  } else {
+    sv[r] = v;
+  }
+}
+template <class W>
+__device__ __forceinline__ uint4 get_vec(const W* sb, const uint4* sv, int r) {
+  if constexpr (sizeof(W) == 4) {
+    const int e = swz<W>(4 * r);
+    return make_uint4(sb[e], sb[e ^ 1], sb[e ^ 2], sb[e ^ 3]);
+  } else {
+    return sv[r];
+  }
 }
 
+template <class F>
 struct PassArgs {
-  uint64_t* data;
-  const Twiddle* tw;
-  const DevPrime* primes;
+  typename F::W* data;
+  const typename F::Tw* tw;
+  const typename F::Prime* primes;
   int np;
   int log_n;
   int st0;             // first global level of the pass
@@ -72,15 +90,19 @@ struct PassArgs {
 
 // One pass of S levels over C = 2^LOGC sub-problems. STRIDED: pass A layout
 // (sub-problems are columns at stride tlast); else pass B (contiguous blocks).
-template <int S, int LOGC, bool STRIDED, bool INV>
+template <class F, int S, int LOGC, bool STRIDED, bool INV>
 // at least 2 CTAs (1024 threads) per SM: <= 64 registers per thread
-__global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassArgs<F> a) {
+  using W = typename F::W;
+  using Tw = typename F::Tw;
   constexpr int C = 1 << LOGC;
   constexpr int ELEMS = C << S;
   constexpr int T = ELEMS / 8;
   constexpr int NG = (S + 2) / 3;
-  extern __shared__ uint64_t sbuf[];       // [ELEMS] residues, then pass-A twiddles
-  uint64_t* stw = sbuf + ELEMS;            // [2^S] x {w, wq}
+  constexpr int VPT = ELEMS * int(sizeof(W)) / 16 / T;  // 16-byte vectors per thread
+  extern __shared__ uint4 smem_raw[];
+  W* sbuf = reinterpret_cast<W*>(smem_raw);  // [ELEMS] residues, then pass-A twiddles
+  W* stw = sbuf + ELEMS;                     // [2^S] x {w, wq}
   int j, row;
   if (a.rows_per_prime) {  // prime-major: blockIdx.y = j * rows_per_prime + b
     j = blockIdx.y / a.rows_per_prime;
@@ -89,11 +111,11 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
     row = blockIdx.y;
     j = row % a.np;
   }
-  const DevPrime& pr = a.primes[j];
-  const uint64_t p = pr.p, p4 = 4 * p, negp = 0 - p;
+  const typename F::Prime& pr = a.primes[j];
+  const typename F::Mod md(pr);
   const size_t n = size_t(1) << a.log_n;
-  uint64_t* rowp = a.data + size_t(row) * n;
-  const Twiddle* twr = a.tw + size_t(j) * n;
+  W* rowp = a.data + size_t(row) * n;
+  const Tw* twr = a.tw + size_t(j) * n;
   const int tlast = 1 << (a.log_n - a.st0 - S);
   const int sp0 = blockIdx.x << LOGC;  // first sub-problem of the CTA
   const int tid = threadIdx.x;
@@ -102,15 +124,14 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int idx = tid + r * T;
-      sbuf[idx] = rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))];
+      sbuf[swz<W>(idx)] = rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))];
     }
-    const uint64_t* t2 = reinterpret_cast<const uint64_t*>(twr);
+    const W* t2 = reinterpret_cast<const W*>(twr);
     for (int i = tid; i < 2 << S; i += T) stw[i] = t2[i];
   } else {
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(rowp + (size_t(sp0) << S));
+    const uint4* src = reinterpret_cast<const uint4*>(rowp + (size_t(sp0) << S));
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      reinterpret_cast<ulonglong2*>(sbuf)[tid + r * T] = src[tid + r * T];
+    for (int r = 0; r < VPT; ++r) put_vec(sbuf, smem_raw, tid + r * T, src[tid + r * T]);
   }
   __syncthreads();
 #pragma unroll
@@ -136,21 +157,19 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
         c = uid >> (ubits + l);
       }
       const int e0 = (h << (S - l)) + u;
-      uint64_t x[8];
+      W x[8];
+      const int sbase = swz<W>(STRIDED ? (e0 << LOGC) + c : (c << S) + e0);
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        if (v < (1 << k)) {
-          const int e = e0 + (v << ubits);
-          x[v] = sbuf[STRIDED ? (e << LOGC) + c : (c << S) + e];
-        }
+        if (v < (1 << k)) x[v] = sbuf[sbase ^ swz<W>((v << ubits) << (STRIDED ? LOGC : 0))];
       // twiddle of group hh at local level l + i
-      auto tw_at = [&](int i, int blk, uint64_t& w, uint64_t& wq) {
+      auto tw_at = [&](int i, int blk, W& w, W& wq) {
         if (STRIDED) {
           const int t = (1 << (l + i)) + (h << i) + blk;
           w = stw[2 * t];
           wq = stw[2 * t + 1];
         } else {
-          const Twiddle tt =
+          const Tw tt =
               twr[(size_t((1 << a.st0) + sp0 + c) << (l + i)) + (size_t(h) << i) + blk];
           w = tt.w;
           wq = tt.wq;
@@ -164,19 +183,18 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
 #pragma unroll
             for (int blk = 0; blk < 4; ++blk)
               if (blk < (1 << i)) {
-                uint64_t w, wq;
+                W w, wq;
                 tw_at(i, blk, w, wq);
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
-                  if (r < half)
-                    ct_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, wq, p4, negp);
+                  if (r < half) F::ct(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, wq, md);
               }
           }
         }
         if (a.last && grp == NG - 1) {
 #pragma unroll
           for (int v = 0; v < 8; ++v)
-            if (v < (1 << k)) x[v] = reduce_4p(csub(x[v], p4), p);  // [0, 8p) -> [0, p)
+            if (v < (1 << k)) x[v] = F::fwd_canon(x[v], md);
         }
       } else {
 #pragma unroll
@@ -194,18 +212,14 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
                   for (int r = 0; r < 4; ++r)
                     if (r < half) {
                       const int i0 = blk * 2 * half + r;
-                      const uint64_t uu = x[i0], vv = x[i0 + half];
-                      x[i0] = shoup_mul(uu + vv, pr.ninv, pr.ninv_q, p);
-                      x[i0 + half] = shoup_mul(uu + p4 - vv, pr.w1n, pr.w1n_q, p);
+                      F::inv_level0(x[i0], x[i0 + half], pr, md);
                     }
                 } else {
-                  uint64_t w, wq;
+                  W w, wq;
                   tw_at(ii, blk, w, wq);
 #pragma unroll
                   for (int r = 0; r < 4; ++r)
-                    if (r < half)
-                      gs_bfly(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, wq, p4,
-                              negp);
+                    if (r < half) F::gs(x[blk * 2 * half + r], x[blk * 2 * half + r + half], w, wq, md);
                 }
               }
           }
@@ -213,10 +227,7 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
       }
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        if (v < (1 << k)) {
-          const int e = e0 + (v << ubits);
-          sbuf[STRIDED ? (e << LOGC) + c : (c << S) + e] = x[v];
-        }
+        if (v < (1 << k)) sbuf[sbase ^ swz<W>((v << ubits) << (STRIDED ? LOGC : 0))] = x[v];
     }
     __syncthreads();
   }
@@ -225,13 +236,12 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int idx = tid + r * T;
-      rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))] = sbuf[idx];
+      rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))] = sbuf[swz<W>(idx)];
     }
   } else {
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(rowp + (size_t(sp0) << S));
+    uint4* dst = reinterpret_cast<uint4*>(rowp + (size_t(sp0) << S));
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      dst[tid + r * T] = reinterpret_cast<const ulonglong2*>(sbuf)[tid + r * T];
+    for (int r = 0; r < VPT; ++r) dst[tid + r * T] = get_vec(sbuf, smem_raw, tid + r * T);
   }
 }
 
@@ -249,9 +259,11 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
 // Each twiddle is loaded once per unit and reused for every operand.
 enum { OP_TENSOR = 0, OP_EVK = 1 };
 
-template <int S, int LOGC, int NOPS, bool INV>
-__device__ __forceinline__ void block_group(uint64_t* sb, int grp, int sp0, int m0,
-                                            const Twiddle* twr, uint64_t p4, uint64_t negp) {
+template <class F, int S, int LOGC, int NOPS, bool INV>
+__device__ __forceinline__ void block_group(typename F::W* sb, int grp, int sp0, int m0,
+                                            const typename F::Tw* twr,
+                                            const typename F::Mod& md) {
+  using W = typename F::W;
   constexpr int C = 1 << LOGC;
   constexpr int T = (C << S) / 8;
   constexpr int OPS = C << S;  // residues per operand in shared memory
@@ -267,7 +279,7 @@ __device__ __forceinline__ void block_group(uint64_t* sb, int grp, int sp0, int 
     const int h = (uid >> ubits) & ((1 << l) - 1);
     const int c = uid >> (ubits + l);
     const int e0 = (c << S) + (h << (S - l)) + u;
-    uint64_t w[7], wq[7];
+    W w[7], wq[7];
     const size_t g = size_t(m0 + sp0 + c);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -275,17 +287,18 @@ __device__ __forceinline__ void block_group(uint64_t* sb, int grp, int sp0, int 
 #pragma unroll
         for (int blk = 0; blk < 4; ++blk)
           if (blk < (1 << i)) {
-            const Twiddle t = twr[(g << (l + i)) + (size_t(h) << i) + blk];
+            const typename F::Tw t = twr[(g << (l + i)) + (size_t(h) << i) + blk];
             w[(1 << i) - 1 + blk] = t.w;
             wq[(1 << i) - 1 + blk] = t.wq;
           }
 #pragma unroll
+    const int sbase = swz<W>(e0);
     for (int op = 0; op < NOPS; ++op) {
-      uint64_t x[8];
-      uint64_t* base = sb + op * OPS + e0;
+      W x[8];
+      W* base = sb + op * OPS;  // OPS is a multiple of 256: slots swizzle alike
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        if (v < (1 << k)) x[v] = base[v << ubits];
+        if (v < (1 << k)) x[v] = base[sbase ^ swz<W>(v << ubits)];
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
         const int i = INV ? 2 - s : s;
@@ -299,44 +312,48 @@ __device__ __forceinline__ void block_group(uint64_t* sb, int grp, int sp0, int 
                 if (r < half) {
                   const int a = blk * 2 * half + r;
                   if (INV)
-                    gs_bfly(x[a], x[a + half], w[(1 << i) - 1 + blk], wq[(1 << i) - 1 + blk], p4,
-                            negp);
+                    F::gs(x[a], x[a + half], w[(1 << i) - 1 + blk], wq[(1 << i) - 1 + blk], md);
                   else
-                    ct_bfly(x[a], x[a + half], w[(1 << i) - 1 + blk], wq[(1 << i) - 1 + blk], p4,
-                            negp);
+                    F::ct(x[a], x[a + half], w[(1 << i) - 1 + blk], wq[(1 << i) - 1 + blk], md);
                 }
         }
       }
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        if (v < (1 << k)) base[v << ubits] = x[v];
+        if (v < (1 << k)) base[sbase ^ swz<W>(v << ubits)] = x[v];
     }
   }
 }
 
+template <class F>
 struct MidArgs {
-  uint64_t* in[4];          // operand rows (batch x np x n each)
-  const uint64_t* evk[2];   // OP_EVK: evk forms, np x n each (shared by the batch)
-  uint64_t* out[3];         // product rows (batch x np x n each)
-  const Twiddle* tw;
-  const Twiddle* itw;
-  const DevPrime* primes;
+  using W = typename F::W;
+  W* in[4];          // operand rows (batch x np x n each)
+  const W* evk[2];   // OP_EVK: evk forms, np x n each (shared by the batch)
+  W* out[3];         // product rows (batch x np x n each)
+  const typename F::Tw* tw;
+  const typename F::Tw* itw;
+  const typename F::Prime* primes;
   int np, log_n, s1, rows_per_prime;
 };
 
-template <int S, int LOGC, int OP>
-__global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs a) {
+template <class F, int S, int LOGC, int OP>
+__global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs<F> a) {
+  using W = typename F::W;
   constexpr int C = 1 << LOGC;
   constexpr int ELEMS = C << S;
   constexpr int T = ELEMS / 8;
   constexpr int NG = (S + 2) / 3;
   constexpr int NIN = OP == OP_TENSOR ? 4 : 1;
   constexpr int NOUT = OP == OP_TENSOR ? 3 : 2;
-  extern __shared__ uint64_t sb[];  // NIN operands, products reuse the slots
+  constexpr int VPT = ELEMS * int(sizeof(W)) / 16 / T;  // 16-byte vectors per thread
+  constexpr int VOP = ELEMS * int(sizeof(W)) / 16;      // 16-byte vectors per operand
+  extern __shared__ uint4 smem_raw[];
+  W* sb = reinterpret_cast<W*>(smem_raw);  // NIN operands, products reuse the slots
   const int j = blockIdx.y / a.rows_per_prime;
   const int b = blockIdx.y - j * a.rows_per_prime;
-  const DevPrime& pr = a.primes[j];
-  const uint64_t p = pr.p, p4 = 4 * p, negp = 0 - p;
+  const typename F::Prime& pr = a.primes[j];
+  const typename F::Mod md(pr);
   const size_t n = size_t(1) << a.log_n;
   const size_t row_off = (size_t(b) * a.np + j) * n;
   const int sp0 = blockIdx.x << LOGC;
@@ -345,54 +362,48 @@ __global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs 
   const int tid = threadIdx.x;
 #pragma unroll
   for (int op = 0; op < NIN; ++op) {
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(a.in[op] + row_off + blk_off);
+    const uint4* src = reinterpret_cast<const uint4*>(a.in[op] + row_off + blk_off);
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      reinterpret_cast<ulonglong2*>(sb + op * ELEMS)[tid + r * T] = src[tid + r * T];
+    for (int r = 0; r < VPT; ++r)
+      put_vec(sb + op * ELEMS, smem_raw + op * VOP, tid + r * T, src[tid + r * T]);
   }
   __syncthreads();
-  const Twiddle* twr = a.tw + size_t(j) * n;
+  const typename F::Tw* twr = a.tw + size_t(j) * n;
 #pragma unroll
   for (int gi = 0; gi < NG; ++gi) {
-    block_group<S, LOGC, NIN, false>(sb, gi, sp0, m0, twr, p4, negp);
+    block_group<F, S, LOGC, NIN, false>(sb, gi, sp0, m0, twr, md);
     __syncthreads();
   }
-  // evaluation-domain products (values in [0, 8p): 64-bit products < 2^126)
-  const uint64_t one_q = pr.one_q, beta = pr.beta, beta_q = pr.beta_q;
-  const uint64_t* ea = OP == OP_EVK ? a.evk[0] + size_t(j) * n + blk_off : nullptr;
-  const uint64_t* eb = OP == OP_EVK ? a.evk[1] + size_t(j) * n + blk_off : nullptr;
+  // evaluation-domain products of forward-domain (lazy) values
+  const W* ea = OP == OP_EVK ? a.evk[0] + size_t(j) * n + blk_off : nullptr;
+  const W* eb = OP == OP_EVK ? a.evk[1] + size_t(j) * n + blk_off : nullptr;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const int e = tid + r * T;
+    const int i = tid + r * T, e = swz<W>(i);
     if (OP == OP_TENSOR) {
-      const uint64_t x1 = sb[e], y1 = sb[ELEMS + e], x2 = sb[2 * ELEMS + e],
-                     y2 = sb[3 * ELEMS + e];
-      const uint64_t d2 = mulmod(x1, x2, p, one_q, beta, beta_q);
-      const uint64_t d0 = mulmod(y1, y2, p, one_q, beta, beta_q);
-      const uint64_t d1 = add_mod(mulmod(x1, y2, p, one_q, beta, beta_q),
-                                  mulmod(x2, y1, p, one_q, beta, beta_q), p);
-      sb[e] = d2;
-      sb[ELEMS + e] = d0;
-      sb[2 * ELEMS + e] = d1;
+      const W x1 = sb[e], y1 = sb[ELEMS + e], x2 = sb[2 * ELEMS + e], y2 = sb[3 * ELEMS + e];
+      sb[e] = F::mul(x1, x2, pr);                      // d2
+      sb[ELEMS + e] = F::mul(y1, y2, pr);              // d0
+      sb[2 * ELEMS + e] = F::mul_add2(x1, y2, x2, y1, pr);  // d1
     } else {
-      const uint64_t f = sb[e];
-      sb[e] = mulmod(f, ea[e], p, one_q, beta, beta_q);
-      sb[ELEMS + e] = mulmod(f, eb[e], p, one_q, beta, beta_q);
+      const W f = sb[e];
+      sb[e] = F::mul(f, ea[i], pr);
+      sb[ELEMS + e] = F::mul(f, eb[i], pr);
     }
   }
   __syncthreads();
-  const Twiddle* itwr = a.itw + size_t(j) * n;
+  const typename F::Tw* itwr = a.itw + size_t(j) * n;
 #pragma unroll
   for (int gi = 0; gi < NG; ++gi) {
-    block_group<S, LOGC, NOUT, true>(sb, NG - 1 - gi, sp0, m0, itwr, p4, negp);
+    block_group<F, S, LOGC, NOUT, true>(sb, NG - 1 - gi, sp0, m0, itwr, md);
     __syncthreads();
   }
 #pragma unroll
   for (int op = 0; op < NOUT; ++op) {
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(a.out[op] + row_off + blk_off);
+    uint4* dst = reinterpret_cast<uint4*>(a.out[op] + row_off + blk_off);
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      dst[tid + r * T] = reinterpret_cast<const ulonglong2*>(sb + op * ELEMS)[tid + r * T];
+    for (int r = 0; r < VPT; ++r)
+      dst[tid + r * T] = get_vec(sb + op * ELEMS, smem_raw + op * VOP, tid + r * T);
   }
 }
 
@@ -406,28 +417,29 @@ void split_levels(int log_n, int& s1, int& s2) {
   }
 }
 
-template <int S, int LOGC, bool STRIDED, bool INV>
+template <class F, int S, int LOGC, bool STRIDED, bool INV>
 size_t smem_bytes() {
-  return sizeof(uint64_t) * ((size_t(1) << (S + LOGC)) + (STRIDED ? (size_t(2) << S) : 0));
+  return sizeof(typename F::W) *
+         ((size_t(1) << (S + LOGC)) + (STRIDED ? (size_t(2) << S) : 0));
 }
 
-template <int S, int LOGC, bool STRIDED, bool INV>
-cudaError_t launch_t(const PassArgs& a, size_t rows, cudaStream_t st) {
+template <class F, int S, int LOGC, bool STRIDED, bool INV>
+cudaError_t launch_t(const PassArgs<F>& a, size_t rows, cudaStream_t st) {
   const int subproblems = STRIDED ? (1 << (a.log_n - a.st0 - S)) : (1 << a.st0);
   dim3 grid(subproblems >> LOGC, static_cast<unsigned>(rows));
-  ntt_pass_kernel<S, LOGC, STRIDED, INV>
-      <<<grid, 1 << (S + LOGC - 3), smem_bytes<S, LOGC, STRIDED, INV>(), st>>>(a);
+  ntt_pass_kernel<F, S, LOGC, STRIDED, INV>
+      <<<grid, 1 << (S + LOGC - 3), smem_bytes<F, S, LOGC, STRIDED, INV>(), st>>>(a);
   return cudaGetLastError();
 }
 
 // (S, LOGC) instances: 2-pass sizes use 4096-residue CTAs (LOGC = 12 - S),
 // single-pass transforms (logN <= 11) one row per CTA (LOGC = 0).
-template <bool STRIDED, bool INV, typename F>
-cudaError_t dispatch(int S, int logc, F&& f) {
-#define HEMUL_NTT_CASE(s, lc)                                          \
-  if (S == s && logc == lc) return f(ntt_pass_kernel<s, lc, STRIDED, INV>, \
-                                     launch_t<s, lc, STRIDED, INV>,   \
-                                     smem_bytes<s, lc, STRIDED, INV>());
+template <class F, bool STRIDED, bool INV, typename Fn>
+cudaError_t dispatch(int S, int logc, Fn&& f) {
+#define HEMUL_NTT_CASE(s, lc)                                                  \
+  if (S == s && logc == lc) return f(ntt_pass_kernel<F, s, lc, STRIDED, INV>,  \
+                                     launch_t<F, s, lc, STRIDED, INV>,         \
+                                     smem_bytes<F, s, lc, STRIDED, INV>());
   HEMUL_NTT_CASE(6, 6) HEMUL_NTT_CASE(7, 5) HEMUL_NTT_CASE(8, 4) HEMUL_NTT_CASE(9, 3)
   HEMUL_NTT_CASE(3, 0) HEMUL_NTT_CASE(4, 0) HEMUL_NTT_CASE(5, 0) HEMUL_NTT_CASE(6, 0)
   HEMUL_NTT_CASE(7, 0) HEMUL_NTT_CASE(8, 0) HEMUL_NTT_CASE(9, 0) HEMUL_NTT_CASE(10, 0)
@@ -436,19 +448,20 @@ cudaError_t dispatch(int S, int logc, F&& f) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_pass(bool inv, uint64_t* data, const Twiddle* tw, const DevPrime* primes, int np,
-                        size_t rows, int log_n, int st0, int S, bool strided, bool last,
-                        cudaStream_t st) {
+template <class F>
+cudaError_t launch_pass(bool inv, typename F::W* data, const typename F::Tw* tw,
+                        const typename F::Prime* primes, int np, size_t rows, int log_n, int st0,
+                        int S, bool strided, bool last, cudaStream_t st) {
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
-  const PassArgs a{data, tw, primes, np, log_n, st0, rpp, last ? 1 : 0};
+  const PassArgs<F> a{data, tw, primes, np, log_n, st0, rpp, last ? 1 : 0};
   const int logc = log_n <= 11 ? 0 : kLogPassElems - S;
   auto go = [&](auto kernel, auto launcher, size_t) { (void)kernel; return launcher(a, rows, st); };
   if (strided)
-    return inv ? dispatch<true, true>(S, logc, go) : dispatch<true, false>(S, logc, go);
-  return inv ? dispatch<false, true>(S, logc, go) : dispatch<false, false>(S, logc, go);
+    return inv ? dispatch<F, true, true>(S, logc, go) : dispatch<F, true, false>(S, logc, go);
+  return inv ? dispatch<F, false, true>(S, logc, go) : dispatch<F, false, false>(S, logc, go);
 }
 
-template <bool STRIDED, bool INV>
+template <class F, bool STRIDED, bool INV>
 cudaError_t set_attrs() {
   auto attr = [](auto kernel, auto, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -457,50 +470,57 @@ cudaError_t set_attrs() {
   const int sizes[][2] = {{6, 6}, {7, 5}, {8, 4}, {9, 3}, {3, 0}, {4, 0}, {5, 0},
                           {6, 0}, {7, 0}, {8, 0}, {9, 0}, {10, 0}, {11, 0}};
   for (const auto& sz : sizes) {
-    cudaError_t e = dispatch<STRIDED, INV>(sz[0], sz[1], attr);
+    cudaError_t e = dispatch<F, STRIDED, INV>(sz[0], sz[1], attr);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
+template <class F>
+cudaError_t set_all_attrs() {
+  cudaError_t e;
+  if ((e = set_attrs<F, true, false>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, true, true>()) != cudaSuccess) return e;
+  if ((e = set_attrs<F, false, false>()) != cudaSuccess) return e;
+  return set_attrs<F, false, true>();
+}
+
 }  // namespace
 
 cudaError_t ntt_setup_attributes() {
-  cudaError_t e;
-  if ((e = set_attrs<true, false>()) != cudaSuccess) return e;
-  if ((e = set_attrs<true, true>()) != cudaSuccess) return e;
-  if ((e = set_attrs<false, false>()) != cudaSuccess) return e;
-  return set_attrs<false, true>();
+  cudaError_t e = set_all_attrs<F64>();
+  if (e != cudaSuccess) return e;
+  return set_all_attrs<F32>();
 }
 
 namespace {
 
 constexpr int kMidLogElems = 11;  // residues per operand per CTA (2048)
 
-template <int S, int OP>
-cudaError_t launch_mid(const MidArgs& a, size_t rows, cudaStream_t st) {
+template <class F, int S, int OP>
+cudaError_t launch_mid(const MidArgs<F>& a, size_t rows, cudaStream_t st) {
   constexpr int LOGC = kMidLogElems - S;
   constexpr int NSLOT = OP == OP_TENSOR ? 4 : 2;
-  const size_t smem = sizeof(uint64_t) * NSLOT * (size_t(1) << kMidLogElems);
+  const size_t smem = sizeof(typename F::W) * NSLOT * (size_t(1) << kMidLogElems);
   static bool attr = false;  // one-time opt-in above 48 KB
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ntt_mid_kernel<S, LOGC, OP>,
+    cudaError_t e = cudaFuncSetAttribute(ntt_mid_kernel<F, S, LOGC, OP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((1 << a.s1) >> LOGC, static_cast<unsigned>(rows));
-  ntt_mid_kernel<S, LOGC, OP><<<grid, (1 << kMidLogElems) / 8, smem, st>>>(a);
+  ntt_mid_kernel<F, S, LOGC, OP><<<grid, (1 << kMidLogElems) / 8, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int OP>
-cudaError_t launch_mid_any(const MidArgs& a, int s2, size_t rows, cudaStream_t st) {
+template <class F, int OP>
+cudaError_t launch_mid_any(const MidArgs<F>& a, int s2, size_t rows, cudaStream_t st) {
   switch (s2) {
-    case 6: return launch_mid<6, OP>(a, rows, st);
-    case 7: return launch_mid<7, OP>(a, rows, st);
-    case 8: return launch_mid<8, OP>(a, rows, st);
+    case 6: return launch_mid<F, 6, OP>(a, rows, st);
+    case 7: return launch_mid<F, 7, OP>(a, rows, st);
+    case 8: return launch_mid<F, 8, OP>(a, rows, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -513,12 +533,14 @@ bool ntt_has_mid(int log_n) {
   return s2 >= 6 && s2 <= 8;
 }
 
-cudaError_t ntt_mid_tensor(uint64_t* A1, uint64_t* B1, uint64_t* A2, uint64_t* B2, size_t batch,
-                           int np, int log_n, const Twiddle* tw, const Twiddle* itw,
-                           const DevPrime* primes, cudaStream_t st) {
+template <class F>
+cudaError_t ntt_mid_tensor(typename F::W* A1, typename F::W* B1, typename F::W* A2,
+                           typename F::W* B2, size_t batch, int np, int log_n,
+                           const typename F::Tw* tw, const typename F::Tw* itw,
+                           const typename F::Prime* primes, cudaStream_t st) {
   int s1, s2;
   split_levels(log_n, s1, s2);
-  MidArgs a{};
+  MidArgs<F> a{};
   a.in[0] = A1;
   a.in[1] = B1;
   a.in[2] = A2;
@@ -533,16 +555,18 @@ cudaError_t ntt_mid_tensor(uint64_t* A1, uint64_t* B1, uint64_t* A2, uint64_t* B
   a.log_n = log_n;
   a.s1 = s1;
   a.rows_per_prime = static_cast<int>(batch);
-  return launch_mid_any<OP_TENSOR>(a, s2, batch * np, st);
+  return launch_mid_any<F, OP_TENSOR>(a, s2, batch * np, st);
 }
 
-cudaError_t ntt_mid_evk(uint64_t* F, const uint64_t* ea, const uint64_t* eb, uint64_t* KA,
-                        uint64_t* KB, size_t batch, int np, int log_n, const Twiddle* tw,
-                        const Twiddle* itw, const DevPrime* primes, cudaStream_t st) {
+template <class F>
+cudaError_t ntt_mid_evk(typename F::W* Fin, const typename F::W* ea, const typename F::W* eb,
+                        typename F::W* KA, typename F::W* KB, size_t batch, int np, int log_n,
+                        const typename F::Tw* tw, const typename F::Tw* itw,
+                        const typename F::Prime* primes, cudaStream_t st) {
   int s1, s2;
   split_levels(log_n, s1, s2);
-  MidArgs a{};
-  a.in[0] = F;
+  MidArgs<F> a{};
+  a.in[0] = Fin;
   a.evk[0] = ea;
   a.evk[1] = eb;
   a.out[0] = KA;
@@ -554,7 +578,7 @@ cudaError_t ntt_mid_evk(uint64_t* F, const uint64_t* ea, const uint64_t* eb, uin
   a.log_n = log_n;
   a.s1 = s1;
   a.rows_per_prime = static_cast<int>(batch);
-  return launch_mid_any<OP_EVK>(a, s2, batch * np, st);
+  return launch_mid_any<F, OP_EVK>(a, s2, batch * np, st);
 }
 
 int ntt_num_passes(int log_n) {
@@ -563,42 +587,41 @@ int ntt_num_passes(int log_n) {
   return s2 == 0 ? 1 : 2;
 }
 
-cudaError_t ntt_forward_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
-                             const Twiddle* tw, const DevPrime* primes, cudaStream_t st) {
+template <class F>
+cudaError_t ntt_forward_pass(int pass, typename F::W* data, size_t rows, int np, int log_n,
+                             const typename F::Tw* tw, const typename F::Prime* primes,
+                             cudaStream_t st) {
   int s1, s2;
   split_levels(log_n, s1, s2);
   if (pass == 0)
-    return launch_pass(false, data, tw, primes, np, rows, log_n, 0, s1, true, s2 == 0, st);
-  return launch_pass(false, data, tw, primes, np, rows, log_n, s1, s2, false, true, st);
+    return launch_pass<F>(false, data, tw, primes, np, rows, log_n, 0, s1, true, s2 == 0, st);
+  return launch_pass<F>(false, data, tw, primes, np, rows, log_n, s1, s2, false, true, st);
 }
 
-cudaError_t ntt_inverse_pass(int pass, uint64_t* data, size_t rows, int np, int log_n,
-                             const Twiddle* itw, const DevPrime* primes, cudaStream_t st) {
+template <class F>
+cudaError_t ntt_inverse_pass(int pass, typename F::W* data, size_t rows, int np, int log_n,
+                             const typename F::Tw* itw, const typename F::Prime* primes,
+                             cudaStream_t st) {
   int s1, s2;
   split_levels(log_n, s1, s2);
   if (pass == 0 && s2 > 0)
-    return launch_pass(true, data, itw, primes, np, rows, log_n, s1, s2, false, false, st);
-  return launch_pass(true, data, itw, primes, np, rows, log_n, 0, s1, true, true, st);
+    return launch_pass<F>(true, data, itw, primes, np, rows, log_n, s1, s2, false, false, st);
+  return launch_pass<F>(true, data, itw, primes, np, rows, log_n, 0, s1, true, true, st);
 }
 
-cudaError_t ntt_forward(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* tw,
-                        const DevPrime* primes, cudaStream_t st, int* launches) {
-  for (int pass = 0; pass < ntt_num_passes(log_n); ++pass) {
-    cudaError_t e = ntt_forward_pass(pass, data, rows, np, log_n, tw, primes, st);
-    ++*launches;
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
-
-cudaError_t ntt_inverse(uint64_t* data, size_t rows, int np, int log_n, const Twiddle* itw,
-                        const DevPrime* primes, cudaStream_t st, int* launches) {
-  for (int pass = 0; pass < ntt_num_passes(log_n); ++pass) {
-    cudaError_t e = ntt_inverse_pass(pass, data, rows, np, log_n, itw, primes, st);
-    ++*launches;
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
+#define HEMUL_NTT_INSTANTIATE(F)                                                              \
+  template cudaError_t ntt_mid_tensor<F>(F::W*, F::W*, F::W*, F::W*, size_t, int, int,        \
+                                         const F::Tw*, const F::Tw*, const F::Prime*,         \
+                                         cudaStream_t);                                       \
+  template cudaError_t ntt_mid_evk<F>(F::W*, const F::W*, const F::W*, F::W*, F::W*, size_t,  \
+                                      int, int, const F::Tw*, const F::Tw*, const F::Prime*,  \
+                                      cudaStream_t);                                          \
+  template cudaError_t ntt_forward_pass<F>(int, F::W*, size_t, int, int, const F::Tw*,        \
+                                           const F::Prime*, cudaStream_t);                    \
+  template cudaError_t ntt_inverse_pass<F>(int, F::W*, size_t, int, int, const F::Tw*,        \
+                                           const F::Prime*, cudaStream_t);
+HEMUL_NTT_INSTANTIATE(F64)
+HEMUL_NTT_INSTANTIATE(F32)
+#undef HEMUL_NTT_INSTANTIATE
 
 }  // namespace hemul_gpu

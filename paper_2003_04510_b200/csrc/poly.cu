@@ -9,8 +9,8 @@
 // These kernels are HBM-bound; each coefficient's limbs are read once.
 #include <cuda_runtime.h>
 
+#include "fields.cuh"
 #include "kernels.hpp"
-#include "modarith.cuh"
 
 namespace hemul_gpu {
 
@@ -30,33 +30,37 @@ __global__ void pointwise_kernel(const uint64_t* __restrict__ a, const uint64_t*
   }
 }
 
-__global__ void tensor_kernel(const uint64_t* a1, const uint64_t* b1,
-                              const uint64_t* a2, const uint64_t* b2,
-                              uint64_t* d0, uint64_t* d1,
-                              uint64_t* d2, size_t total, int np, int log_n,
-                              const DevPrime* __restrict__ primes) {
+// The products of the unfused path (logN < 12): forward-domain inputs,
+// inverse-domain outputs (F64 canonical, F32 in [0, 2p), fields.cuh).
+template <class F>
+__global__ void tensor_kernel(const typename F::W* a1, const typename F::W* b1,
+                              const typename F::W* a2, const typename F::W* b2,
+                              typename F::W* d0, typename F::W* d1, typename F::W* d2,
+                              size_t total, int np, int log_n,
+                              const typename F::Prime* __restrict__ primes) {
   for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
        idx += size_t(gridDim.x) * blockDim.x) {
-    const DevPrime pr = primes[(idx >> log_n) % np];
-    const uint64_t x1 = a1[idx], y1 = b1[idx], x2 = a2[idx], y2 = b2[idx];
-    d0[idx] = mm(y1, y2, pr);
-    d2[idx] = mm(x1, x2, pr);
-    d1[idx] = add_mod(mm(x1, y2, pr), mm(x2, y1, pr), pr.p);
+    const typename F::Prime pr = primes[(idx >> log_n) % np];
+    const typename F::W x1 = a1[idx], y1 = b1[idx], x2 = a2[idx], y2 = b2[idx];
+    d0[idx] = F::mul(y1, y2, pr);
+    d2[idx] = F::mul(x1, x2, pr);
+    d1[idx] = F::mul_add2(x1, y2, x2, y1, pr);
   }
 }
 
-__global__ void evk_kernel(const uint64_t* f, const uint64_t* __restrict__ ea,
-                           const uint64_t* __restrict__ eb, uint64_t* ka,
-                           uint64_t* __restrict__ kb, size_t total, int np, int log_n,
-                           const DevPrime* __restrict__ primes) {
+template <class F>
+__global__ void evk_kernel(const typename F::W* f, const typename F::W* __restrict__ ea,
+                           const typename F::W* __restrict__ eb, typename F::W* ka,
+                           typename F::W* __restrict__ kb, size_t total, int np, int log_n,
+                           const typename F::Prime* __restrict__ primes) {
   const size_t per = size_t(np) << log_n;  // evk forms are shared by the batch
   for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
        idx += size_t(gridDim.x) * blockDim.x) {
     const size_t e = idx % per;
-    const DevPrime pr = primes[e >> log_n];
-    const uint64_t x = f[idx];
-    ka[idx] = mm(x, ea[e], pr);
-    kb[idx] = mm(x, eb[e], pr);
+    const typename F::Prime pr = primes[e >> log_n];
+    const typename F::W x = f[idx];
+    ka[idx] = F::mul(x, ea[e], pr);
+    kb[idx] = F::mul(x, eb[e], pr);
   }
 }
 
@@ -153,23 +157,36 @@ cudaError_t pointwise(const uint64_t* a, const uint64_t* b, uint64_t* out, size_
   return cudaGetLastError();
 }
 
-cudaError_t tensor_product(const uint64_t* a1, const uint64_t* b1, const uint64_t* a2,
-                           const uint64_t* b2, uint64_t* d0, uint64_t* d1, uint64_t* d2,
-                           size_t batch, int np, int log_n, const DevPrime* primes,
-                           cudaStream_t st) {
+template <class F>
+cudaError_t tensor_product(const typename F::W* a1, const typename F::W* b1,
+                           const typename F::W* a2, const typename F::W* b2, typename F::W* d0,
+                           typename F::W* d1, typename F::W* d2, size_t batch, int np,
+                           int log_n, const typename F::Prime* primes, cudaStream_t st) {
   const size_t total = (batch * np) << log_n;
-  tensor_kernel<<<grid_for(total, 256), 256, 0, st>>>(a1, b1, a2, b2, d0, d1, d2, total, np,
-                                                      log_n, primes);
+  tensor_kernel<F><<<grid_for(total, 256), 256, 0, st>>>(a1, b1, a2, b2, d0, d1, d2, total, np,
+                                                         log_n, primes);
   return cudaGetLastError();
 }
 
-cudaError_t evk_product(const uint64_t* f, const uint64_t* ea, const uint64_t* eb, uint64_t* ka,
-                        uint64_t* kb, size_t batch, int np, int log_n, const DevPrime* primes,
-                        cudaStream_t st) {
+template <class F>
+cudaError_t evk_product(const typename F::W* f, const typename F::W* ea, const typename F::W* eb,
+                        typename F::W* ka, typename F::W* kb, size_t batch, int np, int log_n,
+                        const typename F::Prime* primes, cudaStream_t st) {
   const size_t total = (batch * np) << log_n;
-  evk_kernel<<<grid_for(total, 256), 256, 0, st>>>(f, ea, eb, ka, kb, total, np, log_n, primes);
+  evk_kernel<F><<<grid_for(total, 256), 256, 0, st>>>(f, ea, eb, ka, kb, total, np, log_n,
+                                                      primes);
   return cudaGetLastError();
 }
+
+#define HEMUL_POLY_INSTANTIATE(F)                                                             \
+  template cudaError_t tensor_product<F>(const F::W*, const F::W*, const F::W*, const F::W*,  \
+                                         F::W*, F::W*, F::W*, size_t, int, int,               \
+                                         const F::Prime*, cudaStream_t);                      \
+  template cudaError_t evk_product<F>(const F::W*, const F::W*, const F::W*, F::W*, F::W*,    \
+                                      size_t, int, int, const F::Prime*, cudaStream_t);
+HEMUL_POLY_INSTANTIATE(F64)
+HEMUL_POLY_INSTANTIATE(F32)
+#undef HEMUL_POLY_INSTANTIATE
 
 cudaError_t keyswitch_epilogue(const uint64_t* ks, const uint64_t* d, uint64_t* out, size_t batch,
                                int log_n, int log_q, int log_Q, int log_p, cudaStream_t st) {

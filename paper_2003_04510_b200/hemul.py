@@ -92,6 +92,7 @@ _SIGS = {
     "hemul_gpu_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
 }
 HEMUL_OPT_FORCE_EXACT = 1
+HEMUL_OPT_BASIS = 2
 
 
 def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
@@ -331,6 +332,19 @@ class Context:
         """Route every he_mul output coefficient through the exact big-integer
         fix-up kernel (test knob for the rarely taken exact path)."""
         self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_FORCE_EXACT, int(on)))
+
+    def set_basis(self, word: int) -> None:
+        """RNS basis he_mul computes in: 32 (30-bit primes, default) or 64 (the
+        reference's w64 primes). Bit-identical results; pass the evk to the
+        next he_mul after switching."""
+        self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_BASIS, int(word)))
+
+    def mul_basis(self, log_q: int) -> tuple[int, int, int]:
+        """(word, np1, np2) of the basis he_mul uses at level log_q."""
+        p1 = self.level_primes(log_q, -1)
+        p2 = self.level_primes(log_q, -2)
+        word = 32 if int(p1.max()) < (1 << 30) else 64
+        return word, len(p1), len(p2)
 
     def set_stream(self, stream: int | None) -> None:
         """Launch on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""

@@ -16,10 +16,15 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-def _ctx(cfg):
+BASES = [32, 64]  # he_mul prime bases (HEMUL_OPT_BASIS): results must not depend on it
+
+
+def _ctx(cfg, basis=32):
     from paper_2003_04510_b200.hemul import Context, make_params
 
-    return Context(make_params(*cfg))
+    ctx = Context(make_params(*cfg))
+    ctx.set_basis(basis)
+    return ctx
 
 
 def _digest(log_q, ax, bx):
@@ -53,11 +58,13 @@ def test_small_random_two_levels_golden():
         assert np.array_equal(ob, g[f"outbx_{lvl}"])
 
 
+@pytest.mark.parametrize("basis", BASES)
 @pytest.mark.parametrize("cfg", [(30, 4, 13), (30, 6, 11), (30, 10, 13), (20, 4, 10)])
-def test_random_inputs_every_level_vs_oracle(cfg, restated):
+def test_random_inputs_every_level_vs_oracle(cfg, basis, restated):
     """Random residues at every level of the ladder (the level LRU evicts,
     heaan.cpp:119-150) against the C restatement."""
-    ctx = _ctx(cfg)
+    ctx = _ctx(cfg, basis)
+    assert ctx.mul_basis(ctx.params.log_q_max)[0] == basis
     p = ctx.params
     rng = np.random.default_rng(sum(cfg))
     evk = (random_poly(rng, p.n, 2 * p.log_q_max), random_poly(rng, p.n, 2 * p.log_q_max))
@@ -71,11 +78,12 @@ def test_random_inputs_every_level_vs_oracle(cfg, restated):
         assert np.array_equal(ob, wb), log_q
 
 
+@pytest.mark.parametrize("basis", BASES)
 @pytest.mark.parametrize("cfg", [(30, 4, 13), (30, 10, 12), (30, 6, 11)])
-def test_exact_fixup_path_matches(cfg, restated):
+def test_exact_fixup_path_matches(cfg, basis, restated):
     """The finisher's exact big-integer fix-up (normally taken with
     probability 2^-64 per coefficient) forced on every coefficient."""
-    ctx = _ctx(cfg)
+    ctx = _ctx(cfg, basis)
     ctx.set_force_exact(True)
     p = ctx.params
     rng = np.random.default_rng(77)
@@ -88,9 +96,10 @@ def test_exact_fixup_path_matches(cfg, restated):
         assert np.array_equal(oa, wa) and np.array_equal(ob, wb), log_q
 
 
-def test_edge_inputs_zero_and_all_ones(restated):
+@pytest.mark.parametrize("basis", BASES)
+def test_edge_inputs_zero_and_all_ones(basis, restated):
     cfg = (30, 4, 10)
-    ctx = _ctx(cfg)
+    ctx = _ctx(cfg, basis)
     p = ctx.params
     q = p.log_q_max
     rng = np.random.default_rng(1)
@@ -105,9 +114,10 @@ def test_edge_inputs_zero_and_all_ones(restated):
         assert np.array_equal(oa, wa) and np.array_equal(ob, wb)
 
 
-def test_batch_equals_singles(restated):
+@pytest.mark.parametrize("basis", BASES)
+def test_batch_equals_singles(basis, restated):
     cfg = (30, 4, 12)
-    ctx = _ctx(cfg)
+    ctx = _ctx(cfg, basis)
     p = ctx.params
     q = p.log_q_max
     rng = np.random.default_rng(9)
@@ -180,15 +190,33 @@ def test_stage_timing_buckets():
     assert all(v > 0 for v in ms.values())
 
 
+def test_basis_switch_and_counts():
+    """The 30-bit basis covers every ring degree the parameter table allows;
+    switching bases re-derives the evk forms and gives the same ciphertext."""
+    g = np.load(GOLDEN / "s_bench.npz")
+    ctx = _ctx((30, 4, 13), 32)
+    q = int(g["log_q"])
+    word, np1, np2 = ctx.mul_basis(q)
+    assert word == 32 and np1 > len(ctx.level_primes(q, 1)) and np2 > len(ctx.level_primes(q, 2))
+    evk = (g["evkax"], g["evkbx"])
+    outs = []
+    for basis in (32, 64, 32):
+        ctx.set_basis(basis)
+        outs.append(ctx.he_mul((g["c1ax"], g["c1bx"]), (g["c2ax"], g["c2bx"]), q, evk=evk))
+    for oa, ob in outs:
+        assert np.array_equal(oa, g["outax"]) and np.array_equal(ob, g["outbx"])
+
+
 @pytest.mark.slow
+@pytest.mark.parametrize("basis", BASES)
 @pytest.mark.parametrize("name", ["logN14_logQ300", "M", "X"])
-def test_bench_protocol_digest_paper_scale(name, reference):
+def test_bench_protocol_digest_paper_scale(name, basis, reference):
     """Digest of he_mul on the reference's own seed-7 keys and ciphertexts
     equals the reference's."""
     d = json.loads((GOLDEN / "digests.json").read_text())[name]
     cfg = tuple(d["params"])
     inp = reference.bench_inputs(*cfg, seed=7)
-    ctx = _ctx(cfg)
+    ctx = _ctx(cfg, basis)
     q = inp["log_q_max"]
     oa, ob = ctx.he_mul(inp["c1"], inp["c2"], q, evk=inp["evk"])
     assert f"{_digest(q - cfg[0], oa, ob):016x}" == d["digest"]
