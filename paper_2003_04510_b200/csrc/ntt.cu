@@ -6,27 +6,30 @@
 // Inverse = Gentleman-Sande from the last level back to level 0 with itw,
 // then x n^-1 (folded here into level 0's butterfly).
 //
-// B200 mapping. One transform of n = 2^logN 64-bit residues is split into
-// two memory passes (2^s1 x 2^s2, s1 = ceil(logN/2)):
+// B200 mapping. One transform of n = 2^logN residues is split into two
+// memory passes (2^s1 x 2^s2, s1 = ceil(logN/2)):
 //   pass A: levels [0, s1) on 2^s1-point columns at stride 2^s2; a CTA owns
-//           C adjacent columns (C x 8 B contiguous per global row);
+//           C adjacent columns (C residues contiguous per global row);
 //   pass B: levels [s1, logN) on contiguous 2^s2-point blocks.
-// A CTA holds 4096 residues (32 KB) in shared memory; each of its 512
-// threads keeps 8 in registers and runs radix-8 butterfly units (3 levels)
-// between barriers, so shared memory is touched once per 3 levels. The pass
-// size S, the sub-problems per CTA C and the thread count are template
-// parameters: all index arithmetic folds to shifts of threadIdx, and no
-// register array is dynamically indexed. Pass A's 2^S twiddles are staged in
-// shared memory (every column of a row uses the same ones); pass B's are
-// read once each from global memory. Values stay lazy in [0, 4p) (forward) /
-// [0, 2p) (inverse) and are canonicalised at the end, so every output is
-// bit-identical to the reference's canonical residues (ntt.hpp:12-16; all
-// reference variants are bit-identical, test_ntt.cpp:120-165).
+// A CTA holds 2^LP residues in shared memory (F64: 4096 x 8 B, 8 per
+// thread; F32: 8192 x 4 B, 16 per thread — the Geo table below) and runs
+// radix-8 butterfly units (3 levels) in registers between barriers, so
+// shared memory is touched once per 3 levels. The pass size S, the
+// sub-problems per CTA C and the thread count are template parameters: all
+// index arithmetic folds to shifts of threadIdx, and no register array is
+// dynamically indexed. Pass A's 2^S twiddles are staged in shared memory
+// (every column of a row uses the same ones); pass B's are read once each
+// from global memory. Values stay lazy (fields.cuh) and are canonicalised at
+// the end, so every output is bit-identical to the reference's canonical
+// residues (ntt.hpp:12-16; all reference variants are bit-identical,
+// test_ntt.cpp:120-165).
 //
 // Rows are visited prime-major (all batch rows of prime j back to back), so a
 // prime's twiddle table is streamed from HBM once per launch and re-read from
 // L2 by the other rows.
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "device_tables.cuh"
 #include "fields.cuh"
@@ -36,7 +39,6 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kLogPassElems = 12;  // 4096 residues per CTA
 
 // Shared-memory slot of residue index i. In every radix-8 group a warp's 32
 // lanes take the lowest five index bits that are not the group's butterfly
@@ -90,14 +92,14 @@ struct PassArgs {
 
 // One pass of S levels over C = 2^LOGC sub-problems. STRIDED: pass A layout
 // (sub-problems are columns at stride tlast); else pass B (contiguous blocks).
-template <class F, int S, int LOGC, bool STRIDED, bool INV>
-// at least 2 CTAs (1024 threads) per SM: <= 64 registers per thread
-__global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassArgs<F> a) {
+template <class F, int S, int LOGC, int LOGT, int MINB, bool STRIDED, bool INV>
+__global__ void __launch_bounds__(1 << LOGT, MINB) ntt_pass_kernel(PassArgs<F> a) {
   using W = typename F::W;
   using Tw = typename F::Tw;
   constexpr int C = 1 << LOGC;
   constexpr int ELEMS = C << S;
-  constexpr int T = ELEMS / 8;
+  constexpr int T = 1 << LOGT;
+  constexpr int EPT = ELEMS / T;  // residues per thread (8 or 16)
   constexpr int NG = (S + 2) / 3;
   constexpr int VPT = ELEMS * int(sizeof(W)) / 16 / T;  // 16-byte vectors per thread
   extern __shared__ uint4 smem_raw[];
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
   // ---- load (+ pass-A twiddles) ------------------------------------------
   if (STRIDED) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < EPT; ++r) {
       const int idx = tid + r * T;
       sbuf[swz<W>(idx)] = rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))];
     }
@@ -140,9 +142,9 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
     const int l = 3 * grp;
     const int k = S - l < 3 ? S - l : 3;  // levels in this group
     const int ubits = S - l - k;          // log2 of units per group
-    const int per = 8 >> k;               // units per thread
+    const int per = EPT >> k;             // units per thread
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < EPT / 2; ++q) {
       if (q >= per) break;
       const int uid = tid + q * T;
       int c, h, u;
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
   // ---- store --------------------------------------------------------------
   if (STRIDED) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < EPT; ++r) {
       const int idx = tid + r * T;
       rowp[size_t(idx >> LOGC) * tlast + sp0 + (idx & (C - 1))] = sbuf[swz<W>(idx)];
     }
@@ -259,20 +261,21 @@ __global__ void __launch_bounds__(1 << (S + LOGC - 3), 2) ntt_pass_kernel(PassAr
 // Each twiddle is loaded once per unit and reused for every operand.
 enum { OP_TENSOR = 0, OP_EVK = 1 };
 
-template <class F, int S, int LOGC, int NOPS, bool INV>
+template <class F, int S, int LOGC, int LOGT, int NOPS, bool INV>
 __device__ __forceinline__ void block_group(typename F::W* sb, int grp, int sp0, int m0,
                                             const typename F::Tw* twr,
                                             const typename F::Mod& md) {
   using W = typename F::W;
   constexpr int C = 1 << LOGC;
-  constexpr int T = (C << S) / 8;
+  constexpr int T = 1 << LOGT;
   constexpr int OPS = C << S;  // residues per operand in shared memory
+  constexpr int EPT = OPS / T;
   const int l = 3 * grp;
   const int k = S - l < 3 ? S - l : 3;
   const int ubits = S - l - k;
-  const int per = 8 >> k;
+  const int per = EPT >> k;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < EPT / 2; ++q) {
     if (q >= per) break;
     const int uid = threadIdx.x + q * T;
     const int u = uid & ((1 << ubits) - 1);
@@ -337,12 +340,13 @@ struct MidArgs {
   int np, log_n, s1, rows_per_prime;
 };
 
-template <class F, int S, int LOGC, int OP>
-__global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs<F> a) {
+template <class F, int S, int LOGC, int LOGT, int OP>
+__global__ void __launch_bounds__(1 << LOGT) ntt_mid_kernel(MidArgs<F> a) {
   using W = typename F::W;
   constexpr int C = 1 << LOGC;
   constexpr int ELEMS = C << S;
-  constexpr int T = ELEMS / 8;
+  constexpr int T = 1 << LOGT;
+  constexpr int EPT = ELEMS / T;
   constexpr int NG = (S + 2) / 3;
   constexpr int NIN = OP == OP_TENSOR ? 4 : 1;
   constexpr int NOUT = OP == OP_TENSOR ? 3 : 2;
@@ -371,14 +375,14 @@ __global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs<
   const typename F::Tw* twr = a.tw + size_t(j) * n;
 #pragma unroll
   for (int gi = 0; gi < NG; ++gi) {
-    block_group<F, S, LOGC, NIN, false>(sb, gi, sp0, m0, twr, md);
+    block_group<F, S, LOGC, LOGT, NIN, false>(sb, gi, sp0, m0, twr, md);
     __syncthreads();
   }
   // evaluation-domain products of forward-domain (lazy) values
   const W* ea = OP == OP_EVK ? a.evk[0] + size_t(j) * n + blk_off : nullptr;
   const W* eb = OP == OP_EVK ? a.evk[1] + size_t(j) * n + blk_off : nullptr;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < EPT; ++r) {
     const int i = tid + r * T, e = swz<W>(i);
     if (OP == OP_TENSOR) {
       const W x1 = sb[e], y1 = sb[ELEMS + e], x2 = sb[2 * ELEMS + e], y2 = sb[3 * ELEMS + e];
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__((1 << (S + LOGC)) / 8) ntt_mid_kernel(MidArgs<
   const typename F::Tw* itwr = a.itw + size_t(j) * n;
 #pragma unroll
   for (int gi = 0; gi < NG; ++gi) {
-    block_group<F, S, LOGC, NOUT, true>(sb, NG - 1 - gi, sp0, m0, itwr, md);
+    block_group<F, S, LOGC, LOGT, NOUT, true>(sb, NG - 1 - gi, sp0, m0, itwr, md);
     __syncthreads();
   }
 #pragma unroll
@@ -417,35 +421,60 @@ void split_levels(int log_n, int& s1, int& s2) {
   }
 }
 
-template <class F, int S, int LOGC, bool STRIDED, bool INV>
-size_t smem_bytes() {
-  return sizeof(typename F::W) *
-         ((size_t(1) << (S + LOGC)) + (STRIDED ? (size_t(2) << S) : 0));
+template <class F, int S, int LOGC>
+size_t smem_bytes(bool strided) {
+  return sizeof(typename F::W) * ((size_t(1) << (S + LOGC)) + (strided ? (size_t(2) << S) : 0));
 }
 
-template <class F, int S, int LOGC, bool STRIDED, bool INV>
+template <class F, int S, int LOGC, int LOGT, int MINB, bool STRIDED, bool INV>
 cudaError_t launch_t(const PassArgs<F>& a, size_t rows, cudaStream_t st) {
   const int subproblems = STRIDED ? (1 << (a.log_n - a.st0 - S)) : (1 << a.st0);
   dim3 grid(subproblems >> LOGC, static_cast<unsigned>(rows));
-  ntt_pass_kernel<F, S, LOGC, STRIDED, INV>
-      <<<grid, 1 << (S + LOGC - 3), smem_bytes<F, S, LOGC, STRIDED, INV>(), st>>>(a);
+  ntt_pass_kernel<F, S, LOGC, LOGT, MINB, STRIDED, INV>
+      <<<grid, 1 << LOGT, smem_bytes<F, S, LOGC>(STRIDED), st>>>(a);
   return cudaGetLastError();
 }
 
-// (S, LOGC) instances: 2-pass sizes use 4096-residue CTAs (LOGC = 12 - S),
-// single-pass transforms (logN <= 11) one row per CTA (LOGC = 0).
+// Pass geometry of a field: two-pass sizes put 2^LP residues in a CTA,
+// 2^LOGEPT per thread, with MINB resident CTAs per SM; single-pass
+// transforms (logN <= 11) one row per CTA, 8 residues per thread.
+template <int LP_, int LOGEPT_, int MINB_>
+struct Geo {
+  static constexpr int LP = LP_, LOGEPT = LOGEPT_, MINB = MINB_;
+};
+
+template <class F, class G, bool STRIDED, bool INV, typename Fn>
+cudaError_t dispatch_geo(int S, int logc, Fn&& f) {
+#define HEMUL_NTT_CASE2(s)                                                                   \
+  if constexpr (G::LP - s >= 0)                                                             \
+    if (S == s && logc == G::LP - s)                                                        \
+      return f(ntt_pass_kernel<F, s, G::LP - s, G::LP - G::LOGEPT, G::MINB, STRIDED, INV>,  \
+               launch_t<F, s, G::LP - s, G::LP - G::LOGEPT, G::MINB, STRIDED, INV>,         \
+               smem_bytes<F, s, G::LP - s>(STRIDED));
+#define HEMUL_NTT_CASE1(s)                                                              \
+  if (S == s && logc == 0)                                                             \
+    return f(ntt_pass_kernel<F, s, 0, s - 3, 2, STRIDED, INV>,                          \
+             launch_t<F, s, 0, s - 3, 2, STRIDED, INV>, smem_bytes<F, s, 0>(STRIDED));
+  HEMUL_NTT_CASE2(6) HEMUL_NTT_CASE2(7) HEMUL_NTT_CASE2(8) HEMUL_NTT_CASE2(9)
+  HEMUL_NTT_CASE1(3) HEMUL_NTT_CASE1(4) HEMUL_NTT_CASE1(5) HEMUL_NTT_CASE1(6)
+  HEMUL_NTT_CASE1(7) HEMUL_NTT_CASE1(8) HEMUL_NTT_CASE1(9) HEMUL_NTT_CASE1(10)
+  HEMUL_NTT_CASE1(11)
+#undef HEMUL_NTT_CASE1
+#undef HEMUL_NTT_CASE2
+  return cudaErrorInvalidValue;
+}
+
+// Measured on B200 at N=2^17 (30-bit basis): 8192 residues x 16 per thread
+// beat 4096 x 8 (ntt_a 3.47 -> 2.85 ms, intt_a 3.90 -> 3.17 ms per step) and
+// the 3-CTA / 1024-thread / 16384-residue variants.
+using GeoF64 = Geo<12, 3, 2>;
+using GeoF32 = Geo<13, 4, 2>;
+template <class F>
+using GeoOf = typename std::conditional<sizeof(typename F::W) == 8, GeoF64, GeoF32>::type;
+
 template <class F, bool STRIDED, bool INV, typename Fn>
 cudaError_t dispatch(int S, int logc, Fn&& f) {
-#define HEMUL_NTT_CASE(s, lc)                                                  \
-  if (S == s && logc == lc) return f(ntt_pass_kernel<F, s, lc, STRIDED, INV>,  \
-                                     launch_t<F, s, lc, STRIDED, INV>,         \
-                                     smem_bytes<F, s, lc, STRIDED, INV>());
-  HEMUL_NTT_CASE(6, 6) HEMUL_NTT_CASE(7, 5) HEMUL_NTT_CASE(8, 4) HEMUL_NTT_CASE(9, 3)
-  HEMUL_NTT_CASE(3, 0) HEMUL_NTT_CASE(4, 0) HEMUL_NTT_CASE(5, 0) HEMUL_NTT_CASE(6, 0)
-  HEMUL_NTT_CASE(7, 0) HEMUL_NTT_CASE(8, 0) HEMUL_NTT_CASE(9, 0) HEMUL_NTT_CASE(10, 0)
-  HEMUL_NTT_CASE(11, 0)
-#undef HEMUL_NTT_CASE
-  return cudaErrorInvalidValue;
+  return dispatch_geo<F, GeoOf<F>, STRIDED, INV>(S, logc, f);
 }
 
 template <class F>
@@ -454,7 +483,7 @@ cudaError_t launch_pass(bool inv, typename F::W* data, const typename F::Tw* tw,
                         int S, bool strided, bool last, cudaStream_t st) {
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
   const PassArgs<F> a{data, tw, primes, np, log_n, st0, rpp, last ? 1 : 0};
-  const int logc = log_n <= 11 ? 0 : kLogPassElems - S;
+  const int logc = log_n <= 11 ? 0 : GeoOf<F>::LP - S;
   auto go = [&](auto kernel, auto launcher, size_t) { (void)kernel; return launcher(a, rows, st); };
   if (strided)
     return inv ? dispatch<F, true, true>(S, logc, go) : dispatch<F, true, false>(S, logc, go);
@@ -467,10 +496,13 @@ cudaError_t set_attrs() {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bytes));
   };
-  const int sizes[][2] = {{6, 6}, {7, 5}, {8, 4}, {9, 3}, {3, 0}, {4, 0}, {5, 0},
-                          {6, 0}, {7, 0}, {8, 0}, {9, 0}, {10, 0}, {11, 0}};
-  for (const auto& sz : sizes) {
-    cudaError_t e = dispatch<F, STRIDED, INV>(sz[0], sz[1], attr);
+  const int lp = GeoOf<F>::LP;
+  for (int s = 6; s <= 9; ++s) {
+    cudaError_t e = dispatch<F, STRIDED, INV>(s, lp - s, attr);
+    if (e != cudaSuccess) return e;
+  }
+  for (int s = 3; s <= 11; ++s) {
+    cudaError_t e = dispatch<F, STRIDED, INV>(s, 0, attr);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -495,24 +527,34 @@ cudaError_t ntt_setup_attributes() {
 
 namespace {
 
-constexpr int kMidLogElems = 11;  // residues per operand per CTA (2048)
-
-template <class F, int S, int OP>
-cudaError_t launch_mid(const MidArgs<F>& a, size_t rows, cudaStream_t st) {
-  constexpr int LOGC = kMidLogElems - S;
+// Middle-pass geometry: 2^LM residues per operand per CTA, 2^LOGT threads.
+template <int LM_, int LOGT_>
+struct MidGeo {
+  static constexpr int LM = LM_, LOGT = LOGT_;
+};
+template <class F, class G, int S, int OP>
+cudaError_t launch_mid_g(const MidArgs<F>& a, size_t rows, cudaStream_t st) {
+  constexpr int LOGC = G::LM - S;
   constexpr int NSLOT = OP == OP_TENSOR ? 4 : 2;
-  const size_t smem = sizeof(typename F::W) * NSLOT * (size_t(1) << kMidLogElems);
+  const size_t smem = sizeof(typename F::W) * NSLOT * (size_t(1) << G::LM);
   static bool attr = false;  // one-time opt-in above 48 KB
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ntt_mid_kernel<F, S, LOGC, OP>,
+    cudaError_t e = cudaFuncSetAttribute(ntt_mid_kernel<F, S, LOGC, G::LOGT, OP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((1 << a.s1) >> LOGC, static_cast<unsigned>(rows));
-  ntt_mid_kernel<F, S, LOGC, OP><<<grid, (1 << kMidLogElems) / 8, smem, st>>>(a);
+  ntt_mid_kernel<F, S, LOGC, G::LOGT, OP><<<grid, 1 << G::LOGT, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <class F, int S, int OP>
+cudaError_t launch_mid(const MidArgs<F>& a, size_t rows, cudaStream_t st) {
+  // 2048 residues per operand, 8 per thread: measured faster on B200 for
+  // both fields than 4096 x 16 / 2048 x 16 / 4096 x 8
+  return launch_mid_g<F, MidGeo<11, 8>, S, OP>(a, rows, st);
 }
 
 template <class F, int OP>
