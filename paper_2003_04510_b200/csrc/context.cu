@@ -57,6 +57,7 @@ struct DevBuf {
 // primes, F64; word 32: the B200 30-bit basis, F32).
 struct RegionDev {
   int word = 64;
+  int split_h = 0;  // region 1 operands split at bit h (level_tables.hpp)
   int np = 0;
   int target_bits = 0;
   DevBuf primes, tw, itw, btab, hat, big_p, half_p;
@@ -243,6 +244,7 @@ void flush_marks(hemul_gpu_ctx* c) {
 
 void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
   d.word = h.word;
+  d.split_h = h.split_h;
   d.np = h.np;
   d.target_bits = h.target_bits;
   d.host_primes = h.primes;
@@ -309,7 +311,9 @@ Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
   if (b.r1) return b;
   const int log_q = lv.log_q;
   const int th = host_threads();
-  RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th, word);
+  // the 30-bit basis splits region-1 operands in halves (h = ceil(log_q / 2))
+  const int split_h = word == 32 ? (log_q + 1) / 2 : 0;
+  RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th, word, split_h);
   RegionHost h2 =
       build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th, word);
   auto r1 = std::make_unique<RegionDev>();
@@ -333,6 +337,7 @@ Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
     f.log_q = log_q;
     f.log_Q = c->log_q_max;
     f.log_p = c->log_p;
+    f.split_h = split_h;
     b.has_fin = true;
   }
   check(cudaStreamSynchronize(c->stream), "level upload");
@@ -758,43 +763,70 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   const typename F::Prime* p1 = r1.P<F>();
   const typename F::Prime* p2 = r2.P<F>();
   // ---- region 1: d0 = bx1 bx2, d1 = ax1 bx2 + ax2 bx1, d2 = ax1 ax2 ---------
-  const size_t r1w = B * r1.np * n;  // one RNS operand
-  ensure(c->r1, 4 * r1w * sizeof(W));
+  // F64: one RNS operand per input, products d2 (slot 0), d0 (1), d1 (2).
+  // F32: every input split at bit h (level_tables.hpp split_h): slots
+  // x1 X1 y1 Y1 x2 X2 y2 Y2, products d2 = (0, 1), d0 = (2, 3), d1 = (4, 5)
+  // as (c0, c1) with d = c0 + 2^h c1 mod 2^log_q.
+  constexpr bool kSplit = sizeof(W) == 4;
+  constexpr int kInSlots = kSplit ? 8 : 4, kOutSlots = kSplit ? 6 : 3;
+  const int h = r1.split_h;
+  const size_t r1w = B * r1.np * n;  // one RNS operand slot
+  ensure(c->r1, kInSlots * r1w * sizeof(W));
   W* R1 = c->r1.as<W>();
-  W* A1 = R1;
-  W* B1 = R1 + r1w;
-  W* A2 = R1 + 2 * r1w;
-  W* B2 = R1 + 3 * r1w;
-  const CrtWeights* w1 = r1.weights(log_q);
-  // one launch: ax1 -> A1, bx1 -> B1, ax2 -> A2, bx2 -> B2 (R1 is [A1|B1|A2|B2])
-  run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
-    return crt_forward_multi<F>(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
-  });
-  // in place: d2 -> A1, d0 -> B1, d1 -> A2
+  const CrtWeights* w1 = r1.weights(kSplit ? h : log_q);
+  if constexpr (kSplit) {
+    const uint64_t* polys[8];
+    int bit0[8], bits[8];
+    for (int t = 0; t < 8; ++t) {
+      polys[t] = in[t / 2];
+      bit0[t] = (t & 1) ? h : 0;
+      bits[t] = (t & 1) ? log_q - h : h;
+    }
+    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
+      return crt_forward_multi<F>(polys, 8, L, B, log_n, *w1, p1, r1.np, R1, c->stream, bit0,
+                                  bits);
+    });
+  } else {
+    // one launch: ax1 -> A1, bx1 -> B1, ax2 -> A2, bx2 -> B2 (R1 is [A1|B1|A2|B2])
+    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
+      return crt_forward_multi<F>(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
+    });
+  }
   const bool mid = ntt_has_mid(log_n);
   if (mid) {
     // forward pass A, then one fused pass: forward pass B + tensor product +
     // inverse pass B, then inverse pass A
-    ntt_fwd<F>(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT, 1);
+    ntt_fwd<F>(c, r1, R1, kInSlots * B * r1.np, HEMUL_STAGE_NTT, 1);
     run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R1, "NTT mid r1", [&] {
-      return ntt_mid_tensor<F>(A1, B1, A2, B2, B, r1.np, log_n, r1.TW<F>(), r1.ITW<F>(), p1,
-                               c->stream);
+      if constexpr (kSplit)
+        return ntt_mid_tensor_split(R1, B, r1.np, log_n, r1.TW<F>(), r1.ITW<F>(), p1, c->stream);
+      else  // in place: d2 -> A1, d0 -> B1, d1 -> A2
+        return ntt_mid_tensor<F>(R1, R1 + r1w, R1 + 2 * r1w, R1 + 3 * r1w, B, r1.np, log_n,
+                                 r1.TW<F>(), r1.ITW<F>(), p1, c->stream);
     });
-    ntt_inv<F>(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT, 1);
+    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 1);
   } else {
-    ntt_fwd<F>(c, r1, R1, 4 * B * r1.np, HEMUL_STAGE_NTT);
+    ntt_fwd<F>(c, r1, R1, kInSlots * B * r1.np, HEMUL_STAGE_NTT);
     // pointwise products are booked under iCRT like rns.cpp:364
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "tensor product", [&] {
-      return tensor_product<F>(A1, B1, A2, B2, B1, A2, A1, B, r1.np, log_n, p1, c->stream);
+      if constexpr (kSplit)
+        return tensor_split_product(R1, B, r1.np, log_n, p1, c->stream);
+      else
+        return tensor_product<F>(R1, R1 + r1w, R1 + 2 * r1w, R1 + 3 * r1w, R1 + r1w,
+                                 R1 + 2 * r1w, R1, B, r1.np, log_n, p1, c->stream);
     });
-    ntt_inv<F>(c, r1, R1, 3 * B * r1.np, HEMUL_STAGE_INTT);
+    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT);
   }
   // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
   // and are reconstructed inside the finisher
   ensure(c->dpoly, B * poly_w * 8);
   uint64_t* d2 = c->dpoly.as<uint64_t>();
-  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1",
-      [&] { return icrt<F>(A1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream); });
+  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1", [&] {
+    return icrt<F>(R1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream, nullptr,
+                   kSplit ? R1 + r1w : nullptr);
+  });
+  const W* D1 = R1 + (kSplit ? 4 : 2) * r1w;  // d1 (c0)
+  const W* D0 = R1 + (kSplit ? 2 : 1) * r1w;  // d0 (c0)
   // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
   const size_t r2w = B * r2.np * n;
   ensure(c->r2, 2 * r2w * sizeof(W));
@@ -825,10 +857,11 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
   flags.count = c->flagbuf.as<unsigned>();
   flags.ids = flags.count + 1;
+  Finisher fin = bs.fin;
+  fin.hi_off = kSplit ? r1w : 0;
   run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
-    return finish_keyswitch<F>(KA, A2 /* d1 */, B1 /* d0 */, B, log_n, p2, r2.np, p1, r1.np,
-                               bs.fin, r2.icrt, r1.icrt, out_ax, out_bx, flags, c->force_exact,
-                               c->stream);
+    return finish_keyswitch<F>(KA, D1, D0, B, log_n, p2, r2.np, p1, r1.np, fin, r2.icrt,
+                               r1.icrt, out_ax, out_bx, flags, c->force_exact, c->stream);
   });
   ++c->launches;  // the (normally empty) exact fix-up kernel
 }

@@ -29,9 +29,26 @@ namespace {
 constexpr int kKT = 32;  // B rows per cp.async stage
 constexpr int kStages = 3;
 
+constexpr int kMaxCrtInputs = 8;
+
+// Input t: polys p[t], converting bits [bit0[t], bit0[t] + bits[t]) of each
+// coefficient (the halves of a split operand, context.cu).
 struct Inputs {
-  const uint64_t* p[4];
+  const uint64_t* p[kMaxCrtInputs];
+  int bit0[kMaxCrtInputs];
+  int bits[kMaxCrtInputs];
 };
+
+// 25-bit chunk m of one coefficient's field (limbs l)
+__device__ __forceinline__ uint32_t chunk_of(const uint64_t* l, int limbs, int bit0, int bits,
+                                             int m) {
+  const int lim = bits - 25 * m;
+  if (lim <= 0) return 0;
+  const int bit = bit0 + 25 * m, k = bit >> 6, off = bit & 63;
+  uint64_t v = k < limbs ? l[k] >> off : 0;
+  if (off > 39 && k + 1 < limbs) v |= l[k + 1] << (64 - off);
+  return static_cast<uint32_t>(v) & (lim >= 25 ? 0x1ffffffu : (1u << lim) - 1);
+}
 
 // Residues of the thread's 4 coefficients x 4 accumulator columns. F64: the
 // column pair (2j, 2j+1) holds the 30-bit halves of prime j's weights,
@@ -102,11 +119,7 @@ __global__ void __launch_bounds__(NW * 32) crt_kernel(Inputs in, int B, int limb
   __syncthreads();
   for (int idx = threadIdx.x; idx < kGemmCoefs * K; idx += blockDim.x) {
     const int m = idx >> 5, c = idx & 31;
-    const int bit = 25 * m, k = bit >> 6, off = bit & 63;
-    const uint64_t* l = raw + c * limbs;
-    uint64_t v = k < limbs ? l[k] >> off : 0;
-    if (off > 39 && k + 1 < limbs) v |= l[k + 1] << (64 - off);
-    A[idx] = static_cast<uint32_t>(v) & 0x1ffffffu;
+    A[idx] = chunk_of(raw + c * limbs, limbs, in.bit0[t], in.bits[t], m);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cg = lane & 7, ng = lane >> 3;
@@ -164,13 +177,10 @@ __global__ void __launch_bounds__(NW * 32) crt_persistent_kernel(
     __syncthreads();  // limbs of this tile (and the weights) are in; A is free
     if (tile + gridDim.x < tiles) fetch(tile + gridDim.x, raw + ((it + 1) & 1) * rawsz);
     cp_async_commit();
+    const int tin = tile / coef_tiles / B;  // input of this tile
     for (int idx = tid; idx < kGemmCoefs * K; idx += NW * 32) {
       const int m = idx >> 5, c = idx & 31;
-      const int bit = 25 * m, k = bit >> 6, off = bit & 63;
-      const uint64_t* l = cur + c * limbs;
-      uint64_t v = k < limbs ? l[k] >> off : 0;
-      if (off > 39 && k + 1 < limbs) v |= l[k + 1] << (64 - off);
-      A[idx] = static_cast<uint32_t>(v) & 0x1ffffffu;
+      A[idx] = chunk_of(cur + c * limbs, limbs, in.bit0[tin], in.bits[tin], m);
     }
     __syncthreads();
     uint64_t acc[4][4] = {};
@@ -263,11 +273,17 @@ cudaError_t crt_setup_attributes() {
 template <class F>
 cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs, size_t batch,
                               int log_n, const CrtWeights& w, const typename F::Prime* primes,
-                              int np, typename F::W* out, cudaStream_t st) {
+                              int np, typename F::W* out, cudaStream_t st, const int* bit0,
+                              const int* bits) {
   const size_t n = size_t(1) << log_n;
-  if (count < 1 || count > 4 || n < kGemmCoefs || w.chunks > kMaxGemmK) return cudaErrorInvalidValue;
+  if (count < 1 || count > kMaxCrtInputs || n < kGemmCoefs || w.chunks > kMaxGemmK)
+    return cudaErrorInvalidValue;
   Inputs in{};
-  for (int t = 0; t < count; ++t) in.p[t] = polys[t];
+  for (int t = 0; t < count; ++t) {
+    in.p[t] = polys[t];
+    in.bit0[t] = bit0 ? bit0[t] : 0;
+    in.bits[t] = bits ? bits[t] : 25 * w.chunks;
+  }
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -293,13 +309,14 @@ template <class F>
 cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n,
                         const CrtWeights& w, const typename F::Prime* primes, int np,
                         typename F::W* out, cudaStream_t st) {
-  return crt_forward_multi<F>(&poly, 1, limbs, batch, log_n, w, primes, np, out, st);
+  return crt_forward_multi<F>(&poly, 1, limbs, batch, log_n, w, primes, np, out, st, nullptr,
+                              nullptr);
 }
 
 #define HEMUL_CRT_INSTANTIATE(F)                                                              \
   template cudaError_t crt_forward_multi<F>(const uint64_t* const*, int, int, size_t, int,    \
                                             const CrtWeights&, const F::Prime*, int, F::W*,   \
-                                            cudaStream_t);                                    \
+                                            cudaStream_t, const int*, const int*);            \
   template cudaError_t crt_forward<F>(const uint64_t*, int, size_t, int, const CrtWeights&,   \
                                       const F::Prime*, int, F::W*, cudaStream_t);
 HEMUL_CRT_INSTANTIATE(F64)

@@ -139,6 +139,25 @@ struct F32 {
   static __device__ __forceinline__ W hat_inv(W x, const Prime& pr) {
     return csub32(shoup32(x, pr.inv, pr.inv_q, 0u - pr.p), pr.p);
   }
+  // Split tensor product (context.cu, level_tables.hpp split_h): v = the
+  // halves x1 X1 y1 Y1 x2 X2 y2 Y2 of ax1 bx1 ax2 bx2 (forward domain, lazy)
+  // -> d2 = (x1x2, x1X2 + X1x2), d0 = (y1y2, y1Y2 + Y1y2),
+  //    d1 = (x1y2 + x2y1, x1Y2 + X1y2 + x2Y1 + X2y1) in v[0..5].
+  // Inputs are reduced to [0, p) first: a sum of four products < 4 p^2 < 2^62.
+  static __device__ __forceinline__ void tensor_split(W (&v)[8], const Prime& pr) {
+    const Mod m(pr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m);
+    auto P = [](W a, W b) { return static_cast<uint64_t>(a) * b; };
+    auto R = [&](uint64_t z) { return reduce64_32(z, pr.p, m.negp, pr.one_q, pr.beta, pr.beta_q); };
+    const W x1 = v[0], X1 = v[1], y1 = v[2], Y1 = v[3], x2 = v[4], X2 = v[5], y2 = v[6], Y2 = v[7];
+    v[0] = R(P(x1, x2));
+    v[1] = R(P(x1, X2) + P(X1, x2));
+    v[2] = R(P(y1, y2));
+    v[3] = R(P(y1, Y2) + P(Y1, y2));
+    v[4] = R(P(x1, y2) + P(x2, y1));
+    v[5] = R(P(x1, Y2) + P(X1, y2) + P(x2, Y1) + P(X2, y1));
+  }
 };
 
 }  // namespace hemul_gpu

@@ -184,8 +184,12 @@ __device__ void carry_digits(const uint64_t* S, int lds, uint32_t* D, int ldd, i
   __syncthreads();
 }
 
+// rns_hi (split region 1): a second operand c1 of the same primes whose
+// rows follow c0's; the table's second half holds the rows times 2^h, so the
+// GEMM yields c0 + 2^h c1 mod 2^T.
 template <class F, int NW>
 __global__ void __launch_bounds__(NW * 32) icrt_kernel(const typename F::W* __restrict__ rns,
+                                                       const typename F::W* __restrict__ rns_hi,
                                                        int log_n,
                                                        const typename F::Prime* __restrict__ primes,
                                                        int np, IcrtTable t,
@@ -195,7 +199,8 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const typename F::W* __re
   const size_t n = size_t(1) << log_n;
   const int b = blockIdx.y;
   const size_t c0 = size_t(blockIdx.x) * kGemmCoefs;
-  const int K = F::kRowsPerPrime * np + 1;
+  const int seg_rows = F::kRowsPerPrime * np + 1;
+  const int K = rns_hi ? 2 * seg_rows : seg_rows;
   constexpr int NC = 16 * NW;
   uint32_t* A = reinterpret_cast<uint32_t*>(smem);                     // [K][32]
   uint32_t* Bs = A + K * kGemmCoefs;                                   // cp.async ring
@@ -205,11 +210,14 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const typename F::W* __re
   uint64_t* S = reinterpret_cast<uint64_t*>(part + NW * 32);       // [32][lds]
   uint32_t* D = reinterpret_cast<uint32_t*>(S + kGemmCoefs * lds);  // [32][ldd]
   const Seg<F> seg{rns + size_t(b) * np * n, primes, np};
+  const Seg<F> seg_hi{rns_hi ? rns_hi + size_t(b) * np * n : nullptr, primes, np};
   stage_rows(seg, n, c0, A, 0);
+  if (rns_hi) stage_rows(seg_hi, n, c0, A, seg_rows);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   build_rows(seg, A, 0, part, flags, size_t(b) * n + c0);
+  if (rns_hi) build_rows(seg_hi, A, seg_rows, part, IcrtFlags{}, 0);
   uint32_t* Bw = Bs + (threadIdx.x >> 5) * kStages * kKT * 16;  // private B ring
   for (int col0 = 0; col0 < t.m_pad; col0 += NC) {
     uint64_t acc[4][4] = {};
@@ -321,14 +329,19 @@ __global__ void __launch_bounds__(NW * 32, kFinMinBlocks) finish_kernel(
   double* part = reinterpret_cast<double*>(Bs + kFinStages * kFinKT * NC);
   const Seg<F> s2{ks + size_t(bb) * np2 * n, p2, np2};
   const Seg<F> s1{(is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, p1, np1};
+  // split region 1: the high product c1 sits hi_off residues after c0
+  const Seg<F> s1h{s1.rns + f.hi_off, p1, np1};
+  const int seg1 = F::kRowsPerPrime * np1 + 1;
   const IcrtFlags none{};
   stage_rows(s2, n, c0, A, 0);
   stage_rows(s1, n, c0, A, f.k2);
+  if (f.hi_off) stage_rows(s1h, n, c0, A, f.k2 + seg1);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   build_rows(s2, A, 0, part, none, 0);
   build_rows(s1, A, f.k2, part, none, 0);
+  if (f.hi_off) build_rows(s1h, A, f.k2 + seg1, part, none, 0);
   uint64_t acc[4][4] = {};
   igemm_32x16_warp<kFinKT, kFinStages>(A, K, f.btab, f.cols_pad, 0,
                                        Bs + (threadIdx.x >> 5) * kFinStages * kFinKT * 16, acc);
@@ -407,8 +420,14 @@ __global__ void finish_fixup_kernel(const typename F::W* __restrict__ ks,
     const int b = is_bx ? bb - B : bb;
     uint64_t x2[kFixMaxLimbs], x1[kFixMaxLimbs];
     exact_centered<F>(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2);
-    exact_centered<F>((is_bx ? d_bx : d_ax) + size_t(b) * np1 * n, n, i, p1, np1, t1, f.log_q,
-                      x1);
+    const typename F::W* d1p = (is_bx ? d_bx : d_ax) + size_t(b) * np1 * n;
+    exact_centered<F>(d1p, n, i, p1, np1, t1, f.log_q, x1);
+    if (f.hi_off) {  // split: x1 = c0 + 2^h c1 mod 2^logq
+      uint64_t x1h[kFixMaxLimbs];
+      exact_centered<F>(d1p + f.hi_off, n, i, p1, np1, t1, f.log_q, x1h);
+      for (int k = 0; k < l1; ++k) add_shifted(x1, l1, f.split_h + 64 * k, x1h[k]);
+      if (f.log_q % 64) x1[l1 - 1] &= (uint64_t(1) << (f.log_q % 64)) - 1;
+    }
     add_shifted(x2, l2, f.log_Q - 1, 1);
     add_shifted(x1, l1, f.log_p - 1, 1);
     for (int k = 0; k < l1; ++k) add_shifted(x2, l2, f.log_Q + 64 * k, x1[k]);
@@ -426,8 +445,8 @@ __global__ void finish_fixup_kernel(const typename F::W* __restrict__ ks,
 }
 
 template <class F, int NW>
-size_t icrt_smem(int np, int m_pad) {
-  return size_t(F::kRowsPerPrime * np + 1) * kGemmCoefs * 4 + size_t(kStages) * kKT * 16 * NW * 4 +
+size_t icrt_smem(int K, int m_pad) {
+  return size_t(K) * kGemmCoefs * 4 + size_t(kStages) * kKT * 16 * NW * 4 +
          NW * 32 * 8 + size_t(kGemmCoefs) * (m_pad + 1) * 12;
 }
 
@@ -441,13 +460,14 @@ size_t finish_smem(const Finisher& f) {
 }
 
 template <class F, int NW>
-cudaError_t launch_icrt(const typename F::W* rns, size_t batch, int log_n,
-                        const typename F::Prime* primes, int np, const IcrtTable& t,
+cudaError_t launch_icrt(const typename F::W* rns, const typename F::W* rns_hi, size_t batch,
+                        int log_n, const typename F::Prime* primes, int np, const IcrtTable& t,
                         uint64_t* out, cudaStream_t st, IcrtFlags f) {
   const size_t n = size_t(1) << log_n;
+  const int K = (F::kRowsPerPrime * np + 1) * (rns_hi ? 2 : 1);
   dim3 grid(static_cast<unsigned>(n / kGemmCoefs), static_cast<unsigned>(batch));
-  icrt_kernel<F, NW><<<grid, NW * 32, icrt_smem<F, NW>(np, t.m_pad), st>>>(rns, log_n, primes,
-                                                                           np, t, out, f);
+  icrt_kernel<F, NW><<<grid, NW * 32, icrt_smem<F, NW>(K, t.m_pad), st>>>(rns, rns_hi, log_n,
+                                                                          primes, np, t, out, f);
   return cudaGetLastError();
 }
 
@@ -523,9 +543,10 @@ cudaError_t finisher_setup_attributes() { return cudaSuccess; }
 template <class F>
 cudaError_t icrt(const typename F::W* rns, size_t batch, int log_n,
                  const typename F::Prime* primes, int np, const IcrtTable& t, uint64_t* out,
-                 cudaStream_t st, const IcrtFlags* flags) {
+                 cudaStream_t st, const IcrtFlags* flags, const typename F::W* rns_hi) {
   const size_t n = size_t(1) << log_n;
-  if (n < kGemmCoefs || F::kRowsPerPrime * np + 1 > kMaxGemmK) return cudaErrorInvalidValue;
+  const int K = (F::kRowsPerPrime * np + 1) * (rns_hi ? 2 : 1);
+  if (n < kGemmCoefs || K > kMaxGemmK || (flags && rns_hi)) return cudaErrorInvalidValue;
   IcrtFlags f;
   if (flags) {
     if (t.p_limbs + 2 > kFixMaxLimbs) return cudaErrorInvalidValue;
@@ -534,7 +555,7 @@ cudaError_t icrt(const typename F::W* rns, size_t batch, int log_n,
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = with_nw(t.m_pad, [&](auto nw) {
-    return launch_icrt<F, decltype(nw)::value>(rns, batch, log_n, primes, np, t, out, st, f);
+    return launch_icrt<F, decltype(nw)::value>(rns, rns_hi, batch, log_n, primes, np, t, out, st, f);
   });
   if (e != cudaSuccess || !flags) return e;
   icrt_fixup_kernel<F><<<64, 64, 0, st>>>(rns, log_n, primes, np, t, out, f);
@@ -567,7 +588,8 @@ cudaError_t finish_keyswitch(const typename F::W* ks, const typename F::W* d_ax,
 
 #define HEMUL_ICRT_INSTANTIATE(F)                                                             \
   template cudaError_t icrt<F>(const F::W*, size_t, int, const F::Prime*, int,                \
-                               const IcrtTable&, uint64_t*, cudaStream_t, const IcrtFlags*);  \
+                               const IcrtTable&, uint64_t*, cudaStream_t, const IcrtFlags*,   \
+                               const F::W*);                                                  \
   template cudaError_t finish_keyswitch<F>(const F::W*, const F::W*, const F::W*, size_t, int, \
                                            const F::Prime*, int, const F::Prime*, int,         \
                                            const Finisher&, const IcrtTable&,                  \

@@ -43,6 +43,11 @@ cudaError_t ntt_mid_tensor(typename F::W* A1, typename F::W* B1, typename F::W* 
                            typename F::W* B2, size_t batch, int np, int log_n,
                            const typename F::Tw* tw, const typename F::Tw* itw,
                            const typename F::Prime* primes, cudaStream_t st);
+// Split region 1 (F32::tensor_split): R1 = 8 slots of batch x np x n (the
+// halves x1 X1 y1 Y1 x2 X2 y2 Y2); the six half products land in slots 0..5.
+cudaError_t ntt_mid_tensor_split(uint32_t* R1, size_t batch, int np, int log_n,
+                                 const Twiddle32* tw, const Twiddle32* itw,
+                                 const DevPrime32* primes, cudaStream_t st);
 // Region 2: F -> F evk_a (KA), F evk_b (KB); KA may alias F.
 template <class F>
 cudaError_t ntt_mid_evk(typename F::W* Fin, const typename F::W* ea, const typename F::W* eb,
@@ -72,12 +77,14 @@ template <class F>
 cudaError_t crt_forward(const uint64_t* poly, int limbs, size_t batch, int log_n,
                         const CrtWeights& w, const typename F::Prime* primes, int np,
                         typename F::W* out, cudaStream_t st);
-// Up to 4 independent inputs of `batch` polys each in one launch; input t
-// lands at out + t * batch * np * n.
+// Up to 8 independent inputs of `batch` polys each in one launch; input t
+// lands at out + t * batch * np * n and converts bits [bit0[t], bit0[t] +
+// bits[t]) of its coefficients (null arrays: bit 0, the table's width).
 template <class F>
 cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs, size_t batch,
                               int log_n, const CrtWeights& w, const typename F::Prime* primes,
-                              int np, typename F::W* out, cudaStream_t st);
+                              int np, typename F::W* out, cudaStream_t st,
+                              const int* bit0 = nullptr, const int* bits = nullptr);
 
 // ---- iCRT (icrt.cu) --------------------------------------------------------
 // B table for the exact reconstruction mod 2^T: (R np + 1) rows x m_pad
@@ -109,10 +116,13 @@ struct IcrtFlags {
 cudaError_t icrt_setup_attributes();
 // rns: batch x np x n canonical residues; out: batch x n x ceil(T/64) limbs.
 // flags = nullptr: the caller guarantees |v| < P/4 (he_mul).
+// rns_hi (split region 1, no flags): out = c0 + 2^h c1 mod 2^T for c0 = rns,
+// c1 = rns_hi, with the table of a split region (level_tables.hpp).
 template <class F>
 cudaError_t icrt(const typename F::W* rns, size_t batch, int log_n,
                  const typename F::Prime* primes, int np, const IcrtTable& t, uint64_t* out,
-                 cudaStream_t st, const IcrtFlags* flags = nullptr);
+                 cudaStream_t st, const IcrtFlags* flags = nullptr,
+                 const typename F::W* rns_hi = nullptr);
 
 // Fused key-switch finisher (heaan.cpp:398-409 after the evk product): for
 // each coefficient one GEMM over the region-2 residues of ks (t_j halves + k)
@@ -131,6 +141,10 @@ struct Finisher {
   int cols = 0, cols_pad = 0, k2 = 0, k1 = 0, base = 0;
   int half_q_bit = 0, half_p_bit = 0, out_bit = 0, out_bits = 0;
   int log_q = 0, log_Q = 0, log_p = 0;
+  // split region 1 (level_tables.hpp): d = c0 + 2^split_h c1, c1 stored
+  // hi_off residues after c0; hi_off = 0: unsplit
+  int split_h = 0;
+  size_t hi_off = 0;
 };
 cudaError_t finisher_setup_attributes();
 // ks: 2B x np2 x n (B ax-batches then B bx-batches), d_ax / d_bx: B x np1 x n
@@ -157,6 +171,10 @@ cudaError_t tensor_product(const typename F::W* a1, const typename F::W* b1,
                            const typename F::W* a2, const typename F::W* b2, typename F::W* d0,
                            typename F::W* d1, typename F::W* d2, size_t batch, int np,
                            int log_n, const typename F::Prime* primes, cudaStream_t st);
+// Split region 1 (F32::tensor_split) for the unfused path: r1 = 8 slots of
+// batch x np x n; the six half products land in slots 0..5.
+cudaError_t tensor_split_product(uint32_t* r1, size_t batch, int np, int log_n,
+                                 const DevPrime32* primes, cudaStream_t st);
 // Region-2 evk inner product: ka = f * ea, kb = f * eb (evk forms shared by
 // the batch).
 template <class F>

@@ -195,15 +195,19 @@ void generate_primes30(int count, int log_n, std::vector<uint64_t>& primes,
 }
 
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
-                        const std::vector<int>& crt_bits, int threads, int word) {
+                        const std::vector<int>& crt_bits, int threads, int word, int split_h) {
   RegionHost r;
   r.region = region;
   r.log_n = log_n;
   r.word = word;
   const int n = 1 << log_n;
+  const int h = region == 1 ? split_h : 0;
+  r.split_h = h;
   // Largest |v| the iCRT must recover: region 1 carries d1 = A1 B2 + A2 B1,
-  // |v| < 2 n q^2; region 2 carries d2 * evk, |v| < n q Q^2.
-  const int vbits = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n;
+  // |v| < 2 n q^2 (split: the high product sums four h-bit x h-bit
+  // products, |v| < 4 n 2^(2h)); region 2 carries d2 * evk, |v| < n q Q^2.
+  const int vbits = region == 2 ? log_q + 2 * log_q_max + log_n
+                                : (h ? 2 * h + log_n + 2 : 2 * log_q + log_n + 1);
   Nat P;
   int count;
   if (word == 64) {
@@ -312,7 +316,9 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   // CRT weights of 2^(25 m) mod p_j (kernels.hpp CrtWeights): w64 as two
   // 30-bit halves, the 30-bit basis as one column
   const int wcols = word == 64 ? 2 : 1;
-  for (int bits : crt_bits) {
+  std::vector<int> in_bits = crt_bits;
+  if (h) in_bits = {h};  // both halves of a split input use the low half's table
+  for (int bits : in_bits) {
     RegionHost::Crt c;
     c.in_bits = bits;
     c.chunks = (bits + kChunkBits - 1) / kChunkBits;
@@ -340,15 +346,18 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   // table rows of the same order.
   const int T = r.target_bits;
   const int R = word == 64 ? 2 : 1;
-  r.hat_t.resize(R * count + 1);
+  const int seg = R * count + 1;  // A rows of one RNS operand
+  r.hat_t.resize(h ? 2 * seg : seg);
   for (int j = 0; j < count; ++j) {
     r.hat_t[R * j] = nat_low(hat[j], T);
     if (R == 2) r.hat_t[2 * j + 1] = nat_shl_low(hat[j], 30, T);
   }
   r.hat_t[R * count] = nat_neg_mod_pow2(P, T);
+  // split: the high product c1 enters as 2^h c1 (a b = c0 + 2^h c1 mod 2^T)
+  for (int row = 0; h && row < seg; ++row) r.hat_t[seg + row] = nat_shl_low(r.hat_t[row], h, T);
   r.m_out = (T + kChunkBits - 1) / kChunkBits;
   r.m_pad = (r.m_out + 15) / 16 * 16;
-  const int K = R * count + 1;
+  const int K = static_cast<int>(r.hat_t.size());
   r.btab.assign(size_t(K) * r.m_pad, 0);
   for (int row = 0; row < K; ++row)
     for (int m = 0; m < r.m_out; ++m)

@@ -25,6 +25,7 @@ constexpr int kMinSlackBits = 4;
 struct RegionHost {
   int region = 0;
   int word = 64;  // 64: reference w64 primes (F64), 32: 30-bit basis (F32)
+  int split_h = 0;  // region 1 split into h-bit halves (0: unsplit)
   int np = 0;
   int log_n = 0;
   int target_bits = 0;  // log_q (region 1) or log_q + log_Q (region 2)
@@ -41,6 +42,7 @@ struct RegionHost {
   };
   std::vector<Crt> crt;
   // iCRT operands mod 2^T, rows in A order: H_j[, H_j 2^30], ..., (-P)
+  // (split: then the same rows times 2^h)
   std::vector<std::vector<uint64_t>> hat_t;
   // iCRT table (see kernels.hpp IcrtTable): hat_t rows in 25-bit chunks
   int m_out = 0, m_pad = 0;
@@ -57,8 +59,14 @@ struct RegionHost {
 // threads > 1 parallelises the twiddle tables. word 64: the reference's
 // primes and prime count; word 32: the fewest 30-bit primes with
 // kMinSlackBits of iCRT headroom.
+// split_h > 0 (region 1): the operands are cut at bit h (h >= log_q / 2),
+// a = a0 + 2^h a1, so a b mod 2^log_q = c0 + 2^h c1 with c0 = a0 b0 and
+// c1 = a0 b1 + a1 b0 (2^(2h) = 0 mod 2^log_q); the basis only has to hold
+// h-bit x h-bit products, the CRT table converts h-bit halves, and the iCRT
+// table has the rows of c0 followed by the rows of c1 shifted by h.
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
-                        const std::vector<int>& crt_bits, int threads, int word = 64);
+                        const std::vector<int>& crt_bits, int threads, int word = 64,
+                        int split_h = 0);
 
 // Chunk width of the iCRT GEMM's B operand (products 30 x 25 bits, see
 // igemm.cuh) and the fraction window kept below bit log_Q by the fused

@@ -258,8 +258,11 @@ __global__ void __launch_bounds__(1 << LOGT, MINB) ntt_pass_kernel(PassArgs<F> a
 //   OP_TENSOR (region 1): A1 B1 A2 B2 -> d2 = A1A2, d0 = B1B2,
 //                         d1 = A1B2 + A2B1 (written over A1, B1, A2)
 //   OP_EVK    (region 2): F, evk_a, evk_b -> F evk_a, F evk_b
+//   OP_TENSOR2 (split region 1, F32): the eight halves x1 X1 y1 Y1 x2 X2 y2
+//                         Y2 -> the six half products of F32::tensor_split
+//                         (written over the first six)
 // Each twiddle is loaded once per unit and reused for every operand.
-enum { OP_TENSOR = 0, OP_EVK = 1 };
+enum { OP_TENSOR = 0, OP_EVK = 1, OP_TENSOR2 = 2 };
 
 template <class F, int S, int LOGC, int LOGT, int NOPS, bool INV>
 __device__ __forceinline__ void block_group(typename F::W* sb, int grp, int sp0, int m0,
@@ -331,9 +334,9 @@ __device__ __forceinline__ void block_group(typename F::W* sb, int grp, int sp0,
 template <class F>
 struct MidArgs {
   using W = typename F::W;
-  W* in[4];          // operand rows (batch x np x n each)
+  W* in[8];          // operand rows (batch x np x n each)
   const W* evk[2];   // OP_EVK: evk forms, np x n each (shared by the batch)
-  W* out[3];         // product rows (batch x np x n each)
+  W* out[6];         // product rows (batch x np x n each)
   const typename F::Tw* tw;
   const typename F::Tw* itw;
   const typename F::Prime* primes;
@@ -348,8 +351,8 @@ __global__ void __launch_bounds__(1 << LOGT) ntt_mid_kernel(MidArgs<F> a) {
   constexpr int T = 1 << LOGT;
   constexpr int EPT = ELEMS / T;
   constexpr int NG = (S + 2) / 3;
-  constexpr int NIN = OP == OP_TENSOR ? 4 : 1;
-  constexpr int NOUT = OP == OP_TENSOR ? 3 : 2;
+  constexpr int NIN = OP == OP_TENSOR ? 4 : OP == OP_TENSOR2 ? 8 : 1;
+  constexpr int NOUT = OP == OP_TENSOR ? 3 : OP == OP_TENSOR2 ? 6 : 2;
   constexpr int VPT = ELEMS * int(sizeof(W)) / 16 / T;  // 16-byte vectors per thread
   constexpr int VOP = ELEMS * int(sizeof(W)) / 16;      // 16-byte vectors per operand
   extern __shared__ uint4 smem_raw[];
@@ -384,7 +387,14 @@ __global__ void __launch_bounds__(1 << LOGT) ntt_mid_kernel(MidArgs<F> a) {
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int i = tid + r * T, e = swz<W>(i);
-    if (OP == OP_TENSOR) {
+    if constexpr (OP == OP_TENSOR2) {
+      W v[8];
+#pragma unroll
+      for (int op = 0; op < 8; ++op) v[op] = sb[op * ELEMS + e];
+      F::tensor_split(v, pr);
+#pragma unroll
+      for (int op = 0; op < 6; ++op) sb[op * ELEMS + e] = v[op];
+    } else if (OP == OP_TENSOR) {
       const W x1 = sb[e], y1 = sb[ELEMS + e], x2 = sb[2 * ELEMS + e], y2 = sb[3 * ELEMS + e];
       sb[e] = F::mul(x1, x2, pr);                      // d2
       sb[ELEMS + e] = F::mul(y1, y2, pr);              // d0
@@ -472,9 +482,18 @@ using GeoF32 = Geo<13, 4, 2>;
 template <class F>
 using GeoOf = typename std::conditional<sizeof(typename F::W) == 8, GeoF64, GeoF32>::type;
 
+// A CTA cannot hold more than a whole row: logN = 12 rows use 4096-residue
+// CTAs whatever the field.
+using GeoSmall = Geo<12, 3, 2>;
+template <class F>
+int pass_lp(int log_n) {
+  return log_n < GeoOf<F>::LP ? GeoSmall::LP : GeoOf<F>::LP;
+}
+
 template <class F, bool STRIDED, bool INV, typename Fn>
-cudaError_t dispatch(int S, int logc, Fn&& f) {
-  return dispatch_geo<F, GeoOf<F>, STRIDED, INV>(S, logc, f);
+cudaError_t dispatch(int S, int logc, int lp, Fn&& f) {
+  if (lp == GeoOf<F>::LP) return dispatch_geo<F, GeoOf<F>, STRIDED, INV>(S, logc, f);
+  return dispatch_geo<F, GeoSmall, STRIDED, INV>(S, logc, f);
 }
 
 template <class F>
@@ -483,11 +502,14 @@ cudaError_t launch_pass(bool inv, typename F::W* data, const typename F::Tw* tw,
                         int S, bool strided, bool last, cudaStream_t st) {
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
   const PassArgs<F> a{data, tw, primes, np, log_n, st0, rpp, last ? 1 : 0};
-  const int logc = log_n <= 11 ? 0 : GeoOf<F>::LP - S;
+  const int lp = pass_lp<F>(log_n);
+  const int logc = log_n <= 11 ? 0 : lp - S;
   auto go = [&](auto kernel, auto launcher, size_t) { (void)kernel; return launcher(a, rows, st); };
   if (strided)
-    return inv ? dispatch<F, true, true>(S, logc, go) : dispatch<F, true, false>(S, logc, go);
-  return inv ? dispatch<F, false, true>(S, logc, go) : dispatch<F, false, false>(S, logc, go);
+    return inv ? dispatch<F, true, true>(S, logc, lp, go)
+               : dispatch<F, true, false>(S, logc, lp, go);
+  return inv ? dispatch<F, false, true>(S, logc, lp, go)
+             : dispatch<F, false, false>(S, logc, lp, go);
 }
 
 template <class F, bool STRIDED, bool INV>
@@ -496,13 +518,13 @@ cudaError_t set_attrs() {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(bytes));
   };
-  const int lp = GeoOf<F>::LP;
-  for (int s = 6; s <= 9; ++s) {
-    cudaError_t e = dispatch<F, STRIDED, INV>(s, lp - s, attr);
-    if (e != cudaSuccess) return e;
-  }
+  for (int lp : {GeoOf<F>::LP, GeoSmall::LP})
+    for (int s = 6; s <= 9; ++s) {
+      cudaError_t e = dispatch<F, STRIDED, INV>(s, lp - s, lp, attr);
+      if (e != cudaSuccess) return e;
+    }
   for (int s = 3; s <= 11; ++s) {
-    cudaError_t e = dispatch<F, STRIDED, INV>(s, 0, attr);
+    cudaError_t e = dispatch<F, STRIDED, INV>(s, 0, GeoOf<F>::LP, attr);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -535,7 +557,7 @@ struct MidGeo {
 template <class F, class G, int S, int OP>
 cudaError_t launch_mid_g(const MidArgs<F>& a, size_t rows, cudaStream_t st) {
   constexpr int LOGC = G::LM - S;
-  constexpr int NSLOT = OP == OP_TENSOR ? 4 : 2;
+  constexpr int NSLOT = OP == OP_TENSOR ? 4 : OP == OP_TENSOR2 ? 8 : 2;
   const size_t smem = sizeof(typename F::W) * NSLOT * (size_t(1) << G::LM);
   static bool attr = false;  // one-time opt-in above 48 KB
   if (!attr) {
@@ -598,6 +620,25 @@ cudaError_t ntt_mid_tensor(typename F::W* A1, typename F::W* B1, typename F::W* 
   a.s1 = s1;
   a.rows_per_prime = static_cast<int>(batch);
   return launch_mid_any<F, OP_TENSOR>(a, s2, batch * np, st);
+}
+
+cudaError_t ntt_mid_tensor_split(uint32_t* R1, size_t batch, int np, int log_n,
+                                 const Twiddle32* tw, const Twiddle32* itw,
+                                 const DevPrime32* primes, cudaStream_t st) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  MidArgs<F32> a{};
+  const size_t slot = batch * size_t(np) << log_n;
+  for (int op = 0; op < 8; ++op) a.in[op] = R1 + op * slot;
+  for (int op = 0; op < 6; ++op) a.out[op] = R1 + op * slot;
+  a.tw = tw;
+  a.itw = itw;
+  a.primes = primes;
+  a.np = np;
+  a.log_n = log_n;
+  a.s1 = s1;
+  a.rows_per_prime = static_cast<int>(batch);
+  return launch_mid_any<F32, OP_TENSOR2>(a, s2, batch * np, st);
 }
 
 template <class F>

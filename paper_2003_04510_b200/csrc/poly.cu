@@ -48,6 +48,21 @@ __global__ void tensor_kernel(const typename F::W* a1, const typename F::W* b1,
   }
 }
 
+// split region 1 (F32::tensor_split): 8 operand slots -> slots 0..5
+__global__ void tensor_split_kernel(uint32_t* __restrict__ r1, size_t slot, int np, int log_n,
+                                    const DevPrime32* __restrict__ primes) {
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < slot;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const DevPrime32 pr = primes[(idx >> log_n) % np];
+    uint32_t v[8];
+#pragma unroll
+    for (int op = 0; op < 8; ++op) v[op] = r1[op * slot + idx];
+    F32::tensor_split(v, pr);
+#pragma unroll
+    for (int op = 0; op < 6; ++op) r1[op * slot + idx] = v[op];
+  }
+}
+
 template <class F>
 __global__ void evk_kernel(const typename F::W* f, const typename F::W* __restrict__ ea,
                            const typename F::W* __restrict__ eb, typename F::W* ka,
@@ -165,6 +180,13 @@ cudaError_t tensor_product(const typename F::W* a1, const typename F::W* b1,
   const size_t total = (batch * np) << log_n;
   tensor_kernel<F><<<grid_for(total, 256), 256, 0, st>>>(a1, b1, a2, b2, d0, d1, d2, total, np,
                                                          log_n, primes);
+  return cudaGetLastError();
+}
+
+cudaError_t tensor_split_product(uint32_t* r1, size_t batch, int np, int log_n,
+                                 const DevPrime32* primes, cudaStream_t st) {
+  const size_t slot = (batch * np) << log_n;
+  tensor_split_kernel<<<grid_for(slot, 256), 256, 0, st>>>(r1, slot, np, log_n, primes);
   return cudaGetLastError();
 }
 
