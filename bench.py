@@ -61,59 +61,58 @@ def limbs(bits: int) -> int:
 
 
 # --------------------------------------------------------------------------
-# algorithmic integer work (32-bit IMAD-equivalent multiply-adds), DESIGN.md §4
+# algorithmic work per kernel class
 # --------------------------------------------------------------------------
-SHOUP_IMAD = 9    # 64-bit Shoup modmul: 3 (approx quotient) + 6 (remainder)
-MULMOD_IMAD = 26  # 64x64 product (8) + two Shoup reductions (2 x 9)
+GEMM_CLASSES = ("crt", "icrt", "finish")     # bound: IMAD.WIDE.U32 issue
+NTT_CLASSES = ("ntt_a", "ntt_b", "intt_b", "intt_a", "mid_r1", "mid_r2", "tensor", "evk")
 
 
-def region_shapes(cfg, log_q):
-    from paper_2003_04510_b200.hemul import make_params
-
-    p = make_params(*cfg)
-    return p
-
-
-def work_per_step(p, np1: int, np2: int, B: int, log_q: int) -> dict[str, float]:
-    """Integer work per step of each kernel class in 32-bit IMAD-equivalent
-    multiply-adds: GEMM products of the 25x30-bit CRT/iCRT
-    formulation, 9 per Shoup modmul, 26 per variable modmul."""
+def kernel_model(p, word: int, np1: int, np2: int, B: int, log_q: int) -> dict[str, dict]:
+    """Per kernel class and step: `products` = the algorithmic inner-product
+    terms of the integer GEMMs (one IMAD.WIDE.U32 each: 25-bit chunk x
+    30-bit operand), `bytes` = the HBM bytes the kernel must move (each
+    operand read once, each result written once), `butterflies` = NTT
+    butterflies. word 32: the 30-bit basis with split region 1 (np1 primes
+    per half product); word 64: the reference's w64 basis."""
     n, ln = p.n, p.log_n
     s1 = ln if ln <= 11 else (ln + 1) // 2
     s2 = ln - s1
-    chunks = math.ceil(log_q / 25)                      # 25-bit chunks of a ct poly
-    fin_cols = math.ceil((min(p.log_q_max, 125) + log_q) / 25)
-    fwd_rows = 4 * B * np1 + B * np2
-    inv_rows = 3 * B * np1 + 2 * B * np2
-    bf = n // 2
-    return {
-        "crt": n * B * (4 * np1 + np2) * 2 * chunks,
-        "ntt_a": fwd_rows * bf * s1 * SHOUP_IMAD,
-        "ntt_b": fwd_rows * bf * s2 * SHOUP_IMAD,
-        "intt_b": inv_rows * bf * s2 * SHOUP_IMAD,
-        "intt_a": inv_rows * bf * s1 * SHOUP_IMAD + inv_rows * n * SHOUP_IMAD,
-        "tensor": n * B * np1 * 4 * MULMOD_IMAD,
-        "evk": n * B * np2 * 2 * MULMOD_IMAD,
-        "mid_r1": (4 * B * np1 * bf * s2 + 3 * B * np1 * bf * s2) * SHOUP_IMAD
-                  + n * B * np1 * 4 * MULMOD_IMAD,
-        "mid_r2": (B * np2 * bf * s2 + 2 * B * np2 * bf * s2) * SHOUP_IMAD
-                  + n * B * np2 * 2 * MULMOD_IMAD,
-        "icrt": n * B * ((2 * np1 + 1) * chunks + np1 * SHOUP_IMAD),
-        "finish": n * 2 * B * ((2 * np2 + 2 * np1 + 2) * fin_cols
-                               + (np1 + np2) * SHOUP_IMAD),
-    }
-
-
-def reference_w_int(p, np1, np2, pl1, pl2, log_q):
-    """reference-algorithm IMAD slots per HE Mul (8 per 64x64
-    MAC, 16 per Shoup modmul)."""
-    n, ln = p.n, p.log_n
     L = limbs(log_q)
-    mac = n * (6 * np1 * L + np2 * L + 3 * np1 + 2 * np2 + 3 * np1 * pl1 + 2 * np2 * pl2)
-    mod = (n * (18 * np1 + 3 * np2) + (n // 2) * ln * (6 * np1 + np2)
-           + 2 * n * (3 * np1 + 2 * np2) + (3 * np1 + 2 * np2) * ((n // 2) * ln + n)
-           + n * (3 * np1 + 2 * np2))
-    return 8 * mac + 16 * mod
+    kq = math.ceil(log_q / 25)
+    fin_cols = math.ceil((min(p.log_q_max, 125) + log_q) / 25)
+    rb = n * word // 8                       # bytes of one RNS row
+    if word == 32:
+        h = (log_q + 1) // 2
+        in1, out1, R = 8, 6, 1
+        crt_products = n * B * (8 * math.ceil(h / 25) * np1 + kq * np2)
+    else:
+        in1, out1, R = 4, 3, 2
+        crt_products = n * B * (4 * np1 + np2) * 2 * kq
+    k1 = (R * np1 + 1) * (2 if word == 32 else 1)
+    k2 = R * np2 + 1
+    fwd_rows = in1 * B * np1 + B * np2
+    inv_rows = out1 * B * np1 + 2 * B * np2
+    bf = n // 2
+    m = {
+        "crt": {"products": crt_products,
+                "bytes": 5 * B * n * L * 8 + fwd_rows * rb},
+        "icrt": {"products": n * B * k1 * kq,
+                 "bytes": (2 if word == 32 else 1) * B * np1 * rb + B * n * L * 8},
+        "finish": {"products": n * 2 * B * (k2 + k1) * fin_cols,
+                   "bytes": 2 * B * np2 * rb + (out1 - 2) * B * np1 * rb
+                            + 2 * B * n * limbs(log_q - p.log_p) * 8},
+        "ntt_a": {"butterflies": fwd_rows * bf * s1, "bytes": 2 * fwd_rows * rb},
+        "intt_a": {"butterflies": inv_rows * bf * s1, "bytes": 2 * inv_rows * rb},
+        "ntt_b": {"butterflies": fwd_rows * bf * s2, "bytes": 2 * fwd_rows * rb},
+        "intt_b": {"butterflies": inv_rows * bf * s2, "bytes": 2 * inv_rows * rb},
+        "mid_r1": {"butterflies": (in1 + out1) * B * np1 * bf * s2,
+                   "bytes": (in1 + out1) * B * np1 * rb},
+        "mid_r2": {"butterflies": 3 * B * np2 * bf * s2,
+                   "bytes": 3 * B * np2 * rb + 2 * np2 * rb},
+        "tensor": {"bytes": (in1 + out1) * B * np1 * rb},
+        "evk": {"bytes": 3 * B * np2 * rb + 2 * np2 * rb},
+    }
+    return m
 
 
 # --------------------------------------------------------------------------
@@ -232,6 +231,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--latency-reps", type=int, default=5)
+    ap.add_argument("--basis", type=int, default=32, choices=[32, 64],
+                    help="RNS basis of he_mul (HEMUL_OPT_BASIS); results are identical")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     B = args.batch or DEFAULT_BATCH[args.config]
@@ -259,6 +260,7 @@ def main() -> None:
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_basis(args.basis)
     q = p.log_q_max
     L, Lo, Le = limbs(q), limbs(q - p.log_p), limbs(2 * q)
     n = p.n
@@ -283,7 +285,7 @@ def main() -> None:
     t0 = time.time()
     ctx.warm_level(q, evk, evk_id=1)
     level_s = time.time() - t0
-    np1, np2 = len(ctx.level_primes(q, 1)), len(ctx.level_primes(q, 2))
+    word, np1, np2 = ctx.mul_basis(q)   # the RNS basis he_mul runs in
 
     def step(b=B, o=out):
         ctx.he_mul((c1[0][:b], c1[1][:b]), (c2[0][:b], c2[1][:b]), q, evk=evk, evk_id=1,
@@ -368,28 +370,44 @@ def main() -> None:
     dig = ciphertext_digest(q - p.log_p, o0[0], o0[1])
     digests = gather_to_rank0(dig) or []
 
-    # ---- roofline of the dominant kernel class ----------------------------
+    # ---- roofline: GEMM kernels vs the IMAD.WIDE probe, NTT kernels vs HBM --
     imad_peak = ctx.imad_peak()
-    work = work_per_step(p, np1, np2, B, q)
+    peaks = {}
+    pfile = ROOT / "MEASURED_PEAKS.json"
+    if pfile.exists():
+        peaks = json.loads(pfile.read_text())
+    hbm_peak = peaks.get("hbm_gbs")
+    model = kernel_model(p, word, np1, np2, B, q)
     per_class = {}
     for k, (ms, cnt) in kstats.items():
-        if k in work and ms > 0:
-            per_class[k] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
-                            "tiops": work[k] / (ms / args.steps * 1e-3) / 1e12}
+        if k not in model or ms <= 0:
+            continue
+        sec = ms / args.steps * 1e-3
+        mk = model[k]
+        e = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
+             "hbm_gbs": mk["bytes"] / sec / 1e9}
+        if hbm_peak:
+            e["hbm_frac"] = e["hbm_gbs"] / hbm_peak
+        if "products" in mk:
+            e["tiops"] = mk["products"] / sec / 1e12
+            e["imad_frac"] = e["tiops"] / (imad_peak / 1e12)
+        if "butterflies" in mk:
+            e["gbutterflies_s"] = mk["butterflies"] / sec / 1e9
+        per_class[k] = e
     dom = max(per_class, key=lambda k: per_class[k]["ms_per_step"])
-    achieved = per_class[dom]["tiops"]
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
-    pl1 = pl2 = None
-    # reference-algorithm W_int over the measured step time
-    from math import ceil
-    # limbs of P1 / P2 (the reference's iCRT MAC width)
-    P1bits = sum(float(np.log2(float(x))) for x in ctx.level_primes(q, 1))
-    P2bits = sum(float(np.log2(float(x))) for x in ctx.level_primes(q, 2))
-    pl1, pl2 = ceil(P1bits / 64), ceil(P2bits / 64)
-    w_int = reference_w_int(p, np1, np2, pl1, pl2, q)
+    if "tiops" in per_class[dom]:
+        roof = {"bound": "imad", "kernel": dom, "achieved": per_class[dom]["tiops"],
+                "peak": imad_peak / 1e12, "unit": "TIOP/s (IMAD.WIDE.U32 products)",
+                "frac": per_class[dom]["imad_frac"], "traffic": traffic,
+                "peak_source": "IMAD.WIDE.U32 probe on this device, this run"}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": per_class[dom]["hbm_gbs"],
+                "peak": hbm_peak, "unit": "GB/s", "frac": per_class[dom].get("hbm_frac"),
+                "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
     if rank == 0:
         cpu = None
@@ -408,9 +426,11 @@ def main() -> None:
             "metric": METRIC, "value": value, "unit": "HE Mul/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "latency_us": latency_us, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "u32" if word == 32 else "u64",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: batched HE Mul+relin+rescale, "
-                                   f"N=2^{p.log_n}, logQ={q}, np1={np1}, np2={np2}",
+                                   f"N=2^{p.log_n}, logQ={q}, basis {word}-bit: np1={np1}"
+                                   f"{' per half product' if word == 32 else ''}, np2={np2}",
                        "batch_per_gpu": B, "global_batch": B * world,
                        "parallelism": f"ciphertext-sharded x{world}, evk replicated",
                        "l2": f"inputs {4 * B * n * L * 8 / 2**20:.0f} MiB per step > 126 MiB L2"},
@@ -418,13 +438,7 @@ def main() -> None:
             "e2e": {"value": e2e_value, "unit": "HE Mul/s",
                     "h2d_bytes_per_step": 4 * B * n * L * 8,
                     "d2h_bytes_per_step": 2 * B * n * Lo * 8},
-            "roofline": {"bound": "imad", "kernel": dom, "achieved": achieved,
-                         "peak": imad_peak / 1e12, "unit": "TIOP/s (32-bit IMAD)",
-                         "frac": achieved / (imad_peak / 1e12), "traffic": traffic,
-                         "peak_source": "IMAD.WIDE.U32 probe on this device, this run"},
-            "he_mul_roofline": {"reference_w_int_imad_slots": w_int,
-                                "achieved_tslots": w_int * B / (ms_per_step * 1e-3) / 1e12,
-                                "frac_of_imad_peak": w_int * B / (ms_per_step * 1e-3) / imad_peak},
+            "roofline": roof,
             "kernels": per_class,
             "stage_ms_one_call": stage_ms,
             "level_setup_s": level_s,

@@ -293,10 +293,15 @@ cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs
   return with_nw(nw_for(w.ld), [&](auto v) {
     constexpr int NW = decltype(v)::value;
     const size_t psmem = crt_persistent_smem<NW>(limbs, w.chunks);
-    if (psmem <= 110 * 1024) {  // 2 persistent CTAs per SM
+    int resident = 0;  // persistent CTAs per SM at this shared-memory size
+    if (psmem <= 110 * 1024 &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, crt_persistent_kernel<F, NW>,
+                                                      NW * 32, psmem) != cudaSuccess)
+      return cudaGetLastError();
+    if (resident >= 2) {
       const int col_tiles = w.ld / (16 * NW);
       const int tiles = static_cast<int>(count * batch * (n / kGemmCoefs));
-      const int per = std::max(1, std::min(tiles, 2 * sms / col_tiles));
+      const int per = std::max(1, std::min(tiles, resident * sms / col_tiles));
       crt_persistent_kernel<F, NW><<<dim3(per, col_tiles), NW * 32, psmem, st>>>(
           in, count, static_cast<int>(batch), limbs, log_n, w, primes, np, out);
       return cudaGetLastError();

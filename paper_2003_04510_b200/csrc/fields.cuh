@@ -11,11 +11,14 @@
 //        IMAD.HI + two IMAD instead of five IMAD.WIDE + four IMAD.
 //
 // Every field exposes the same lazy-reduction contract to the kernels:
-//   ct()   Cooley-Tukey butterfly, closed on [0, F::kFwdBound p)
-//   gs()   Gentleman-Sande butterfly, closed on [0, F::kInvBound p)
+//   ct()   Cooley-Tukey butterfly, closed on the forward domain
+//          (F64: [0, 8p), F32: [0, 4p))
+//   gs()   Gentleman-Sande butterfly, closed on the inverse domain
+//          (F64: [0, 4p), F32: [0, 2p))
 //   fwd_canon()  forward-domain value -> [0, p)
 //   inv_level0() last inverse level with n^-1 folded in, outputs in [0, p)
 //   mul(), mul_add2()  products of forward-domain values -> inverse domain
+//   hat_inv()    t_j = x (P/p_j)^-1 mod p_j in [0, p) (the iCRT A rows)
 #pragma once
 #include <cstdint>
 

@@ -63,21 +63,21 @@ def main() -> None:
     ap.add_argument("--title", default="ncu --set full, one launch per kernel")
     args = ap.parse_args()
     lines = [f"# {args.title}", "",
-             "| kernel | ms | DRAM read MB | DRAM write MB | FMA-heavy % | ALU % | LSU % | issue % "
+             "| class | kernel | ms | DRAM read MB | DRAM write MB | FMA-heavy % | ALU % | LSU % | issue % "
              "| occupancy % | smem conflicts / wavefronts | regs | grid x block |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = json.loads(args.traffic.read_text()) if args.traffic and args.traffic.exists() else {}
     for rep in args.reports:
         r = read(rep)
         name = r["kernel"].split("(")[0].split("::")[-1]
+        key = rep.stem.split("prof_", 1)[-1]  # report named prof_<bench kernel class>.ncu-rep
         lines.append(
-            f"| `{name}` | {r.get('duration', 0):.3f} | {r.get('dram_read', 0) / 1e6:.1f} | "
+            f"| {key} | `{name}` | {r.get('duration', 0):.3f} | {r.get('dram_read', 0) / 1e6:.1f} | "
             f"{r.get('dram_write', 0) / 1e6:.1f} | {r.get('fmaheavy_pct', 0):.1f} | "
             f"{r.get('alu_pct', 0):.1f} | {r.get('lsu_pct', 0):.1f} | {r.get('issue_pct', 0):.1f} | "
             f"{r.get('occupancy_pct', 0):.1f} | {r.get('smem_conflicts', 0):.3g} / "
             f"{r.get('smem_wavefronts', 0):.3g} | {int(r.get('regs', 0))} | "
             f"{int(r.get('grid', 0))} x {int(r.get('block', 0))} |")
-        key = rep.stem.split("prof_", 1)[-1]  # report named prof_<bench kernel class>.ncu-rep
         traffic.setdefault(args.config, {})[key] = r.get("dram_read", 0) + r.get("dram_write", 0)
     args.out.write_text("\n".join(lines) + "\n")
     if args.traffic:

@@ -1,7 +1,8 @@
 #!/bin/bash
 # ncu evidence for the X workload (run on the GPU box via gpurun, one GPU).
 # 1) launch list of a short bench (per-launch device times, cold & serialised)
-# 2) --set full capture of one launch of each he_mul kernel class
+# 2) --set full capture of one launch of each he_mul kernel class, summarised
+#    on the box (reports are large) into $OUT/ncu_summary_X.md + traffic.json
 set -u
 OUT=${1:-gpurun_out}
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --latency-reps 1"
@@ -10,11 +11,16 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 prof() {  # class kernel-regex launch-skip
   ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o $OUT/prof_$1 $CMD > /dev/null 2>&1
 }
-prof crt crt_kernel 2
+# launch order: warm_level (evk CRT x2, NTT fwd A+B), then per step
+# crt r1, ntt A, mid r1, intt A, icrt, crt r2, ntt A, mid r2, intt A, finish
+prof crt crt_persistent_kernel 2
+prof crt_r2 crt_persistent_kernel 3
 prof ntt_a ntt_pass_kernel 2
 prof mid_r1 ntt_mid_kernel 0
 prof intt_a ntt_pass_kernel 3
 prof icrt icrt_kernel 0
 prof mid_r2 ntt_mid_kernel 1
 prof finish finish_kernel 0
-ls -la $OUT
+python tools/ncu_summary.py $OUT/prof_*.ncu-rep --out $OUT/ncu_summary_X.md --traffic $OUT/traffic.json --config X
+for f in $OUT/prof_*.ncu-rep; do python tools/ncu_keys.py $f; done > $OUT/ncu_keys_X.txt
+rm -f $OUT/prof_*.ncu-rep
