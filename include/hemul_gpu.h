@@ -121,8 +121,12 @@ hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, cons
  * reference's own w64 primes (params.cpp:89-115). The product is exact in
  * either basis, so the ciphertexts are bit-identical; the 30-bit basis falls
  * back to 64 when a ring degree has too few such primes. Changing it
- * invalidates cached evk forms (pass the evk to the next he_mul). */
-enum { HEMUL_OPT_FORCE_EXACT = 1, HEMUL_OPT_BASIS = 2 };
+ * invalidates cached evk forms (pass the evk to the next he_mul).
+ * HEMUL_OPT_TENSOR_CORES (default 1): in the 30-bit basis the big-integer
+ * base conversions run as exact u8 x u8 -> s32 GEMMs on the tcgen05 tensor
+ * cores; 0 selects the IMAD.WIDE integer-pipe kernels. Results are
+ * bit-identical either way. */
+enum { HEMUL_OPT_FORCE_EXACT = 1, HEMUL_OPT_BASIS = 2, HEMUL_OPT_TENSOR_CORES = 3 };
 hemul_status hemul_gpu_set_option(hemul_gpu_ctx *ctx, int option, int value);
 
 /* Device timing. When enabled every launch is bracketed by CUDA events on the

@@ -67,11 +67,22 @@ struct RegionDev {
     std::unique_ptr<DevBuf> buf;
   };
   std::vector<Crt> crt;
+  struct CrtTc {
+    int bit0, bits;
+    CrtTcTable tab;
+    std::unique_ptr<DevBuf> buf;
+  };
+  std::vector<CrtTc> crt_tc;  // int8 tensor-core CRT tables (30-bit basis)
   IcrtTable icrt;
   std::vector<uint64_t> host_primes;
   const CrtWeights* weights(int bits) const {
     for (const auto& c : crt)
       if (c.in_bits == bits) return &c.w;
+    return nullptr;
+  }
+  const CrtTcTable* tc_table(int bit0, int bits) const {
+    for (const auto& c : crt_tc)
+      if (c.bit0 == bit0 && c.bits == bits && crt_tc_supported(c.tab)) return &c.tab;
     return nullptr;
   }
   template <class F>
@@ -153,6 +164,7 @@ struct hemul_gpu_ctx {
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
   int basis = 32;       // HEMUL_OPT_BASIS: he_mul prime basis (32 or 64)
+  int tensor_cores = 1;  // HEMUL_OPT_TENSOR_CORES: int8 tcgen05 base conversions
 
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
@@ -280,6 +292,22 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
     dc.w.ld = c.ld;
     d.crt.push_back(std::move(dc));
   }
+  d.crt_tc.clear();
+  for (const auto& t : h.crt_tc) {
+    RegionDev::CrtTc dt;
+    dt.bit0 = t.bit0;
+    dt.bits = t.bits;
+    dt.buf = std::make_unique<DevBuf>();
+    upload(*dt.buf, t.btab, st);
+    dt.tab.btab = dt.buf->as<uint8_t>();
+    dt.tab.kpad = t.kpad;
+    dt.tab.col_tile = t.col_tile;
+    dt.tab.ncol_tiles = t.ncol_tiles;
+    dt.tab.primes_per_tile = t.primes_per_tile;
+    dt.tab.limb0 = t.limb0;
+    dt.tab.end_bit = t.end_bit;
+    d.crt_tc.push_back(std::move(dt));
+  }
 }
 
 int host_threads() {
@@ -312,7 +340,7 @@ Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
   const int log_q = lv.log_q;
   const int th = host_threads();
   // the 30-bit basis splits region-1 operands in halves (h = ceil(log_q / 2))
-  const int split_h = word == 32 ? (log_q + 1) / 2 : 0;
+  const int split_h = word == 32 ? split_point(log_q) : 0;
   RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th, word, split_h);
   RegionHost h2 =
       build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th, word);
@@ -524,6 +552,7 @@ hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_overri
         cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventDisableTiming) != cudaSuccess)
       return HEMUL_E_CUDA;
   if (ntt_setup_attributes() != cudaSuccess || crt_setup_attributes() != cudaSuccess ||
+      crt_tc_setup_attributes() != cudaSuccess ||
       icrt_setup_attributes() != cudaSuccess)
     return HEMUL_E_CUDA;
   *out = c.release();
@@ -611,6 +640,9 @@ hemul_status hemul_gpu_set_option(hemul_gpu_ctx* c, int option, int value) {
   switch (option) {
     case HEMUL_OPT_FORCE_EXACT:
       c->force_exact = value != 0;
+      return HEMUL_OK;
+    case HEMUL_OPT_TENSOR_CORES:
+      c->tensor_cores = value != 0;
       return HEMUL_OK;
     case HEMUL_OPT_BASIS:
       if (value != 32 && value != 64) return fail(c, HEMUL_E_ARG, "basis must be 32 or 64");
@@ -782,10 +814,20 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       bit0[t] = (t & 1) ? h : 0;
       bits[t] = (t & 1) ? log_q - h : h;
     }
-    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
-      return crt_forward_multi<F>(polys, 8, L, B, log_n, *w1, p1, r1.np, R1, c->stream, bit0,
-                                  bits);
-    });
+    const CrtTcTable* tlo = c->tensor_cores ? r1.tc_table(0, h) : nullptr;
+    const CrtTcTable* thi = c->tensor_cores ? r1.tc_table(h, log_q - h) : nullptr;
+    if (tlo && thi) {
+      CrtTcTable tabs[8];
+      for (int t = 0; t < 8; ++t) tabs[t] = (t & 1) ? *thi : *tlo;
+      run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1 (tensor cores)", [&] {
+        return crt_forward_tc(polys, tabs, 8, L, B, log_n, p1, r1.np, R1, c->stream);
+      });
+    } else {
+      run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
+        return crt_forward_multi<F>(polys, 8, L, B, log_n, *w1, p1, r1.np, R1, c->stream, bit0,
+                                    bits);
+      });
+    }
   } else {
     // one launch: ax1 -> A1, bx1 -> B1, ax2 -> A2, bx2 -> B2 (R1 is [A1|B1|A2|B2])
     run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
@@ -832,9 +874,21 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   ensure(c->r2, 2 * r2w * sizeof(W));
   W* KA = c->r2.as<W>();
   W* KB = KA + r2w;
-  run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2", [&] {
-    return crt_forward<F>(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
-  });
+  bool r2_done = false;
+  if constexpr (kSplit) {
+    if (const CrtTcTable* t2 = c->tensor_cores ? r2.tc_table(0, log_q) : nullptr) {
+      const uint64_t* d2c = d2;
+      run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2 (tensor cores)", [&] {
+        return crt_forward_tc(&d2c, t2, 1, L, B, log_n, p2, r2.np, KA, c->stream);
+      });
+      r2_done = true;
+    }
+  }
+  if (!r2_done) {
+    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2", [&] {
+      return crt_forward<F>(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
+    });
+  }
   const W* EA = lv.evk_a.as<W>();
   const W* EB = EA + size_t(r2.np) * n;
   if (mid) {

@@ -29,7 +29,7 @@ namespace {
 constexpr int kKT = 32;  // B rows per cp.async stage
 constexpr int kStages = 3;
 
-constexpr int kMaxCrtInputs = 8;
+
 
 // Input t: polys p[t], converting bits [bit0[t], bit0[t] + bits[t]) of each
 // coefficient (the halves of a split operand, context.cu).

@@ -71,6 +71,7 @@ struct CrtWeights {
   int ld = 0;  // crt_cols_pad(np * F::kCrtColsPerPrime)
 };
 constexpr int kCrtPrimesPerTile = 16;
+constexpr int kMaxCrtInputs = 8;  // inputs of one multi-input CRT launch
 cudaError_t crt_setup_attributes();
 // poly: batch x n x limbs; out: batch x np x n canonical residues.
 template <class F>
@@ -85,6 +86,31 @@ cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs
                               int log_n, const CrtWeights& w, const typename F::Prime* primes,
                               int np, typename F::W* out, cudaStream_t st,
                               const int* bit0 = nullptr, const int* bits = nullptr);
+
+// ---- CRT on the int8 tensor cores (crt_tc.cu, 30-bit basis only) ----------
+// One input field: bits [bit0, bit0 + bits) of each coefficient, bit0 % 8 = 0.
+// The GEMM reads kpad bytes per coefficient starting at limb limb0 (byte
+// offset d = bit0 / 8 - 8 limb0 inside it); bits >= end_bit (= bit0 + bits,
+// relative to the coefficient) are cleared on load.
+// btab: [ncol_tiles * col_tile][kpad] u8, row 4 jj + b of column tile ct =
+// byte b of 2^(8 (k - d)) mod p_j, j = ct * primes_per_tile + jj, for
+// d <= k < d + ceil(bits / 8), else 0 (level_tables.cpp build_crt_tc).
+struct CrtTcTable {
+  const uint8_t* btab = nullptr;
+  int kpad = 0;             // multiple of 32
+  int col_tile = 0;         // multiple of 16, <= 256 (4 x primes_per_tile, padded)
+  int ncol_tiles = 0;
+  int primes_per_tile = 0;
+  int limb0 = 0;
+  int end_bit = 0;
+};
+cudaError_t crt_tc_setup_attributes();
+bool crt_tc_supported(const CrtTcTable& tab);
+// Up to 8 inputs (same layout and column tiling, own tables); input t lands
+// at out + t * batch * np * n as canonical residues (crt_forward_multi).
+cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs, int count,
+                           int limbs, size_t batch, int log_n, const DevPrime32* primes, int np,
+                           uint32_t* out, cudaStream_t st);
 
 // ---- iCRT (icrt.cu) --------------------------------------------------------
 // B table for the exact reconstruction mod 2^T: (R np + 1) rows x m_pad

@@ -340,6 +340,15 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
     }
     r.crt.push_back(std::move(c));
   }
+  if (word == 32) {
+    // tensor-core CRT fields: region 1 the two halves, region 2 the ModUp input
+    std::vector<std::pair<int, int>> fields;
+    if (h && h % 8 == 0)
+      fields = {{0, h}, {h, log_q - h}};
+    else if (region == 2)
+      fields = {{0, log_q}};
+    for (auto [b0, nb] : fields) r.crt_tc.push_back(build_crt_tc(r.primes, b0, nb));
+  }
 
   // iCRT operands mod 2^T in A-row order: w64 H_j, H_j 2^30 (the two 30-bit
   // halves of t_j), the 30-bit basis H_j; then (-P). Then the 25-bit-chunk
@@ -373,6 +382,39 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   for (int k = 0; k < r.p_limbs; ++k)
     r.half_p[k] = (r.big_p[k] >> 1) | (k + 1 < r.p_limbs ? r.big_p[k + 1] << 63 : 0);
   return r;
+}
+
+RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, int bits) {
+  RegionHost::CrtTc t;
+  const int np = static_cast<int>(primes.size());
+  t.bit0 = bit0;
+  t.bits = bits;
+  const int byte0 = bit0 / 8, nbytes = (bits + 7) / 8;
+  t.limb0 = byte0 / 8;
+  const int d = byte0 - 8 * t.limb0;
+  t.kpad = (d + nbytes + 31) / 32 * 32;
+  t.end_bit = bit0 + bits;
+  // shared memory of crt_tc.cu: col_tile x K + 2 stages x 128 x K (K rounded
+  // to 128-byte atom columns) + 1 KB alignment, within kMaxDynSmem (224 KB)
+  const int kc = (t.kpad + 127) / 128 * 128;
+  for (t.ncol_tiles = (4 * np + 255) / 256;; ++t.ncol_tiles) {
+    t.primes_per_tile = (np + t.ncol_tiles - 1) / t.ncol_tiles;
+    t.col_tile = (4 * t.primes_per_tile + 15) / 16 * 16;
+    if (t.col_tile * kc + 2 * 128 * kc + 1024 <= 224 * 1024 || t.col_tile <= 16) break;
+  }
+  t.btab.assign(size_t(t.ncol_tiles) * t.col_tile * t.kpad, 0);
+  for (int j = 0; j < np; ++j) {
+    const int ct = j / t.primes_per_tile, jj = j - ct * t.primes_per_tile;
+    const uint64_t p = primes[j];
+    const uint64_t step = powmod(2, 8, p);
+    uint64_t u = 1 % p;
+    for (int k = d; k < d + nbytes; ++k) {
+      for (int b = 0; b < 4; ++b)
+        t.btab[(size_t(ct) * t.col_tile + 4 * jj + b) * t.kpad + k] = uint8_t(u >> (8 * b));
+      u = mulmod(u, step, p);
+    }
+  }
+  return t;
 }
 
 FinisherHost build_finisher(const RegionHost& r1, const RegionHost& r2, int log_q,

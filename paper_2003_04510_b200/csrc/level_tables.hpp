@@ -41,6 +41,14 @@ struct RegionHost {
     std::vector<uint32_t> wtab;
   };
   std::vector<Crt> crt;
+  // int8 tensor-core CRT tables (word 32; kernels.hpp CrtTcTable), one per
+  // input field [bit0, bit0 + bits)
+  struct CrtTc {
+    int bit0 = 0, bits = 0;
+    int kpad = 0, col_tile = 0, ncol_tiles = 0, primes_per_tile = 0, limb0 = 0, end_bit = 0;
+    std::vector<uint8_t> btab;
+  };
+  std::vector<CrtTc> crt_tc;
   // iCRT operands mod 2^T, rows in A order: H_j[, H_j 2^30], ..., (-P)
   // (split: then the same rows times 2^h)
   std::vector<std::vector<uint64_t>> hat_t;
@@ -67,6 +75,18 @@ struct RegionHost {
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
                         const std::vector<int>& crt_bits, int threads, int word = 64,
                         int split_h = 0);
+
+// Tensor-core CRT table of field [bit0, bit0 + bits) (bit0 % 8 == 0) for the
+// region's primes: column tiling chosen so that the weight tile and two
+// 128-coefficient A stages fit in shared memory (crt_tc.cu).
+RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, int bits);
+// Split point of the 30-bit basis' region 1: ceil(log_q / 2) rounded up to a
+// byte (the tensor-core CRT reads whole bytes), or ceil(log_q / 2) when that
+// leaves no high half.
+inline int split_point(int log_q) {
+  const int h = (log_q + 1) / 2, h8 = (h + 7) / 8 * 8;
+  return h8 < log_q ? h8 : h;
+}
 
 // Chunk width of the iCRT GEMM's B operand (products 30 x 25 bits, see
 // igemm.cuh) and the fraction window kept below bit log_Q by the fused

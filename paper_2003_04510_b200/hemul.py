@@ -93,6 +93,7 @@ _SIGS = {
 }
 HEMUL_OPT_FORCE_EXACT = 1
 HEMUL_OPT_BASIS = 2
+HEMUL_OPT_TENSOR_CORES = 3
 
 
 def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
@@ -338,6 +339,12 @@ class Context:
         reference's w64 primes). Bit-identical results; pass the evk to the
         next he_mul after switching."""
         self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_BASIS, int(word)))
+
+    def set_tensor_cores(self, on: bool = True) -> None:
+        """30-bit basis: run the big-integer base conversions as exact int8
+        GEMMs on the tcgen05 tensor cores (default) or on the IMAD.WIDE
+        integer pipe. Bit-identical results."""
+        self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_TENSOR_CORES, int(on)))
 
     def mul_basis(self, log_q: int) -> tuple[int, int, int]:
         """(word, np1, np2) of the basis he_mul uses at level log_q."""

@@ -16,14 +16,21 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-BASES = [32, 64]  # he_mul prime bases (HEMUL_OPT_BASIS): results must not depend on it
+# he_mul engines: prime basis (HEMUL_OPT_BASIS) x base-conversion engine
+# (HEMUL_OPT_TENSOR_CORES, 30-bit basis only); results must not depend on them
+BASES = ["32tc", "32imad", "64"]
 
 
-def _ctx(cfg, basis=32):
+def _word(basis) -> int:
+    return int(str(basis)[:2])
+
+
+def _ctx(cfg, basis="32tc"):
     from paper_2003_04510_b200.hemul import Context, make_params
 
     ctx = Context(make_params(*cfg))
-    ctx.set_basis(basis)
+    ctx.set_basis(_word(basis))
+    ctx.set_tensor_cores(str(basis).endswith("tc"))
     return ctx
 
 
@@ -64,7 +71,7 @@ def test_random_inputs_every_level_vs_oracle(cfg, basis, restated):
     """Random residues at every level of the ladder (the level LRU evicts,
     heaan.cpp:119-150) against the C restatement."""
     ctx = _ctx(cfg, basis)
-    assert ctx.mul_basis(ctx.params.log_q_max)[0] == basis
+    assert ctx.mul_basis(ctx.params.log_q_max)[0] == _word(basis)
     p = ctx.params
     rng = np.random.default_rng(sum(cfg))
     evk = (random_poly(rng, p.n, 2 * p.log_q_max), random_poly(rng, p.n, 2 * p.log_q_max))
