@@ -1,0 +1,454 @@
+// Exact inverse CRT and the fused key-switch finisher on the int8 tensor
+// cores (sm_100a tcgen05, 30-bit basis).
+//
+// Reference: icrt_reordered (proj/core/src/rns.cpp:132-190, 235-290,
+// 395-415) and the ModDown / add / rescale tail of Scheme::he_mul
+// (heaan.cpp:398-409, poly.cpp:98-115). As in icrt.cu (the IMAD.WIDE form),
+// every RNS operand ("segment") of a coefficient is reconstructed as
+//   v = sum_j t_j H_j + k (-P),  t_j = x_j (P/p_j)^-1 mod p_j,
+//   k = round(sum_j t_j / p_j)   (exact: >= 4 bits of slack, level_tables.cpp)
+// and the kernel evaluates, per coefficient, the big integer
+//   V = sum_segments sum_rows a_row V_row     (mod 2^T, from bit base8 up)
+// whose rows V_row are the segment's H_j / -P already shifted to their place
+// in the output (region-1 rows at bit logQ for the finisher; the split high
+// product at 2^h), so that one pass gives d2 (iCRT) or
+// R_logp(d + R_logQ(ks)) (finisher).
+//
+// Tensor-core form: with a_row = sum_b a_{row,b} 2^(8b) (bytes) and
+// V_row = sum_e v_{row,e} 2^(8e),
+//   D[i][m] = sum_{row,b} a_{row,b}(i) * v_{row, m + m0 - b}      (u8 x u8 -> s32)
+//   V = sum_m D[i][m] 2^(8 (m + m0))
+// i.e. a GEMM of the coefficients' byte planes (A, M = 128 coefficients,
+// K = 4 bytes per row) against a constant table B[m][K] of shifted row bytes
+// (level_tables.cpp build_bigint_tc). D < K 2^16 < 2^27 is exact in s32; the
+// epilogue carries the columns into 32-bit digits and extracts the output
+// window. Columns below m0 (the finisher's bits under logQ - 125) are
+// dropped: the truncation error is < 2^(8 m0 + 19), far below the 64 guard
+// bits the ambiguity check inspects, exactly as in the IMAD finisher
+// (kernels.hpp Finisher).
+//
+// Persistent warp-specialised CTA (one per SM, 512 TMEM columns):
+//   warp 4      TMA: B chunks (64 K-bytes x n_cols rows, 64-byte swizzle)
+//   warp 5      MMA issue: 2 k-steps x 2 MMAs (N = n_cols / 2 each) per chunk
+//   warps 6-9   producers: cp.async of the t_j rows (6-stage private ring; the
+//               inverse NTT already scaled x_j by (P/p_j)^-1, context.cu
+//               ntt_inv to_t), fixed-point sum_j umulhi(t_j, 2^55 / p_j) for k,
+//               byte planes written MN-major (128-byte swizzle); the last
+//               chunk of a tile carries the k bytes
+//   warps 0-3   epilogue: TMEM columns -> 32-bit digits -> output limbs
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "fields.cuh"
+#include "igemm.cuh"
+#include "kernels.hpp"
+#include "tc.cuh"
+
+namespace hemul_gpu {
+
+namespace {
+
+constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
+constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
+constexpr int kSlots = kChunk / 4;   // row slots (4-byte residues) per chunk
+constexpr int kEpiWarps = 4;
+constexpr int kTmaWarp = 4, kMmaWarp = 5, kProd0 = 6, kProdWarps = 4;
+constexpr int kThreads = 32 * (kProd0 + kProdWarps);
+constexpr int kSA = 8;               // A (byte plane) stages
+constexpr int kSB = 4;               // B (table) stages
+constexpr int kSR = 6;               // raw t stages (producer-private cp.async ring)
+constexpr int kLag = kSR - 1;        // producer prefetch distance in chunks
+constexpr int kABytes = kChunk * kRows;          // 8 KB
+constexpr int kRawBytes = kSlots * kRows * 4;    // 8 KB
+constexpr int kMaxSeg = 3;
+
+struct Params {
+  BigTcSeg seg[kMaxSeg];
+  int nseg, B, entries, log_n;
+  int n_cols, k_bytes, k_slot, rows_total;
+  BigTcOut o;
+  uint32_t s8, s16, s24;  // 2^8, 2^16, 2^24 (arguments: kept as IMAD.WIDE)
+};
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void producer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kProdWarps * 32) : "memory");
+}
+
+// MN-major, 128-byte swizzle A tile (M = 128): K row kk, bytes m .. m + 3
+__device__ __forceinline__ uint32_t a_off(uint32_t kk, uint32_t m) {
+  return (kk >> 3) * 1024 + (kk & 7) * 128 + ((((m >> 4) ^ kk) & 7) << 4) + (m & 15);
+}
+
+__device__ __forceinline__ const uint32_t* seg_rows(const BigTcSeg& s, int e, int B, size_t n) {
+  const int b = e % B, hi = e / B;
+  return s.base + size_t(b) * s.estride + (hi ? s.half_off : 0);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    bigint_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params P) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t a_full[kSA], a_empty[kSA], b_full[kSB], b_empty[kSB];
+  __shared__ __align__(8) uint64_t t_full, t_empty;
+  __shared__ uint32_t tmem_base;
+  // 1024-byte aligned by pointer arithmetic on the shared array (an integer
+  // round trip would lose the state space: generic LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_addr(smem_raw) & 1023u)) & 1023u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t n = size_t(1) << P.log_n;
+  const int N = P.n_cols, NH = N / 2;
+  const uint32_t b_bytes = uint32_t(N) * kChunk;
+  uint8_t* sB = smem;                                  // kSB x [N][64] (SW64 K-major)
+  uint8_t* sA = sB + kSB * b_bytes;                    // kSA x [64 K][128 M] (SW128 MN-major)
+  uint8_t* sR = sA + kSA * kABytes;                    // kSR x [16 rows][128] u32
+  uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);  // [4][3][128]
+  uint32_t* mu_tab = xbuf + kProdWarps * kMaxSeg * kRows;                // [rows]
+  const int C = P.k_bytes / kChunk;                    // chunks per tile (last: k bytes)
+  const int tiles_per_entry = static_cast<int>(n / kRows);
+  const int tiles = P.entries * tiles_per_entry;
+  const int my_tiles = tiles > int(blockIdx.x) ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int total = my_tiles * C;                      // this CTA's chunk sequence
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSA; ++s) {
+      tc::mbar_init(&a_full[s], kProdWarps * 32);
+      tc::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < kSB; ++s) {
+      tc::mbar_init(&b_full[s], 1);
+      tc::mbar_init(&b_empty[s], 1);
+    }
+    tc::mbar_init(&t_full, 1);
+    tc::mbar_init(&t_empty, kEpiWarps * 32);
+    tc::mbar_fence_init();
+  }
+  // floor(2^55 / p) of every A row (the fixed-point k quotient)
+  for (int g = threadIdx.x; g < P.rows_total; g += kThreads) {
+    const int s = (g >= P.seg[1].slot0) + (g >= P.seg[2].slot0);
+    const int j = g - P.seg[s].slot0;
+    mu_tab[g] = j < P.seg[s].np ? P.seg[s].primes[j].pad[0] : 0u;  // 0: padding row
+  }
+  if (warp == kTmaWarp) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == kTmaWarp) {
+    // ---- B chunks by TMA -------------------------------------------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      for (int q = 0, c = 0; q < total; ++q) {
+        const int s = q % kSB;
+        tc::mbar_wait(&b_empty[s], ((q / kSB) & 1) ^ 1);
+        mbar_expect_tx(&b_full[s], b_bytes);
+        const uint32_t dst = tc::smem_addr(sB + s * b_bytes);
+        tma_load_2d(dst, &tmap, c * kChunk, 0, &b_full[s]);
+        tma_load_2d(dst + NH * kChunk, &tmap, c * kChunk, NH, &b_full[s]);
+        if (++c == C) c = 0;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---- MMA issue -------------------------------------------------------
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_u8(kRows, NH, 1, 0);
+      for (int q = 0, c = 0, it = 0; q < total; ++q) {
+        if (c == 0) tc::mbar_wait(&t_empty, (it & 1) ^ 1);
+        tc::mbar_wait(&b_full[q % kSB], (q / kSB) & 1);
+        tc::mbar_wait(&a_full[q % kSA], (q / kSA) & 1);
+        tc::fence_async_smem();
+        tc::fence_after();
+        const uint32_t a0 = tc::smem_addr(sA + (q % kSA) * kABytes);
+        const uint32_t b0 = tc::smem_addr(sB + (q % kSB) * b_bytes);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t ad = tc::smem_desc(a0 + ks * 4096, 8192, 1024, tc::kSw128);
+          const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
+          tc::mma_u8(tmem, ad, tc::smem_desc(b0 + ks * 32, 16, 512, tc::kSw64), idesc, acc);
+          tc::mma_u8(tmem + NH, ad, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
+                     idesc, acc);
+        }
+        tc::mma_commit(&b_empty[q % kSB]);
+        tc::mma_commit(&a_empty[q % kSA]);
+        if (++c == C) {
+          tc::mma_commit(&t_full);
+          c = 0;
+          ++it;
+        }
+      }
+    }
+  } else if (warp >= kProd0) {
+    // ---- producers ---------------------------------------------------------
+    const int pw = warp - kProd0;
+    const int slot_lo = 4 * pw;  // this warp's 4 row slots of every chunk
+    const int pt = threadIdx.x - 32 * kProd0;  // 0..127
+    // fixed point sum_j t_j / p_j 2^23 of the 4 coefficients per segment:
+    // umulhi(t_j, floor(2^55 / p_j)) per row (each term < 2^23, low by < 1;
+    // <= 511 rows per segment keep the sum below 2^32)
+    uint32_t F[kMaxSeg][4];
+#pragma unroll
+    for (int s = 0; s < kMaxSeg; ++s)
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) F[s][c4] = 0;
+    // raw t of the next chunk to issue: row slots slot_lo..+3, coefficients
+    // 4 lane..+3. Segments start on chunk boundaries (build_bigint), so a
+    // chunk reads 4 consecutive rows of one segment; chunks are issued in
+    // sequence and the tile's segment row pointers are updated incrementally.
+    const int sl1 = P.seg[1].slot0, sl2 = P.seg[2].slot0;
+    const int np0 = P.seg[0].np, np1 = P.seg[1].np, np2 = P.seg[2].np;
+    int is_q = 0, is_c = 0, is_tl = 0;
+    const uint32_t *rb0 = nullptr, *rb1 = nullptr, *rb2 = nullptr;
+    auto set_tile = [&](int tl) {
+      const int tile = blockIdx.x + tl * gridDim.x;
+      const int e = tile / tiles_per_entry;
+      const size_t off = size_t(tile - e * tiles_per_entry) * kRows + 4 * lane;
+      rb0 = seg_rows(P.seg[0], e, P.B, n) + off;
+      rb1 = P.nseg > 1 ? seg_rows(P.seg[1], e, P.B, n) + off : rb0;
+      rb2 = P.nseg > 2 ? seg_rows(P.seg[2], e, P.B, n) + off : rb0;
+    };
+    if (total > 0) set_tile(0);
+    auto issue = [&]() {
+      if (is_q < total && is_c != C - 1) {
+        const int g0 = kSlots * is_c + slot_lo;  // first of my 4 row slots
+        const int s = (g0 >= sl1) + (g0 >= sl2);
+        const int j0 = g0 - (s == 2 ? sl2 : s == 1 ? sl1 : 0);
+        const int npn = s == 2 ? np2 : s == 1 ? np1 : np0;
+        const uint32_t* src = (s == 2 ? rb2 : s == 1 ? rb1 : rb0) + size_t(j0) * n;
+        const uint32_t dst0 =
+            tc::smem_addr(sR + (is_q % kSR) * kRawBytes + slot_lo * kRows * 4 + 16 * lane);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (j0 + i < npn) tc::cp_async16z(dst0 + i * kRows * 4, src + size_t(i) * n, 16);
+      }
+      cp_async_commit();
+      ++is_q;
+      if (++is_c == C) {
+        is_c = 0;
+        if (++is_tl < my_tiles) set_tile(is_tl);
+      }
+    };
+    for (int q = 0; q < kLag; ++q) issue();
+    for (int q = 0, c = 0; q < total; ++q) {
+      issue();
+      cp_async_wait<kLag>();  // this thread's copies of chunk q have landed
+      const int sa = q % kSA;
+      tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
+      uint8_t* A = sA + sa * kABytes;
+      if (c != C - 1) {
+        const uint8_t* R = sR + (q % kSR) * kRawBytes + slot_lo * kRows * 4 + 16 * lane;
+        const int g0 = kSlots * c + slot_lo;
+        const int s = (g0 >= sl1) + (g0 >= sl2);  // one segment per chunk (warp-uniform)
+        const int j0 = g0 - (s == 2 ? sl2 : s == 1 ? sl1 : 0);
+        const int npn = s == 2 ? np2 : s == 1 ? np1 : np0;
+        uint32_t f[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (j0 + i < npn) {  // warp-uniform (padding rows have zero B rows)
+            // t_j of 4 coefficients (the inverse NTT folded (P/p_j)^-1 in)
+            const uint4 x = *reinterpret_cast<const uint4*>(R + i * kRows * 4);
+            const uint32_t t0 = x.x, t1 = x.y, t2 = x.z, t3 = x.w;
+            const uint32_t mu = mu_tab[g0 + i];
+            f[0] += __umulhi(t0, mu);
+            f[1] += __umulhi(t1, mu);
+            f[2] += __umulhi(t2, mu);
+            f[3] += __umulhi(t3, mu);
+            // byte planes of the 4 coefficients (K rows 4 slot + b)
+            const uint32_t lo01 = __byte_perm(t0, t1, 0x5140), lo23 = __byte_perm(t2, t3, 0x5140);
+            const uint32_t hi01 = __byte_perm(t0, t1, 0x7362), hi23 = __byte_perm(t2, t3, 0x7362);
+            const uint32_t kk = 4 * (slot_lo + i);
+            *reinterpret_cast<uint32_t*>(A + a_off(kk, 4 * lane)) = __byte_perm(lo01, lo23, 0x5410);
+            *reinterpret_cast<uint32_t*>(A + a_off(kk + 1, 4 * lane)) = __byte_perm(lo01, lo23, 0x7632);
+            *reinterpret_cast<uint32_t*>(A + a_off(kk + 2, 4 * lane)) = __byte_perm(hi01, hi23, 0x5410);
+            *reinterpret_cast<uint32_t*>(A + a_off(kk + 3, 4 * lane)) = __byte_perm(hi01, hi23, 0x7632);
+          }
+        }
+#pragma unroll
+        for (int ss = 0; ss < kMaxSeg; ++ss)
+          if (ss == s)
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) F[ss][c4] += f[c4];
+      } else {
+        // k chunk: k_s = round(sum_j t_j / p_j) per segment, bytes 2 s, 2 s + 1
+#pragma unroll
+        for (int s = 0; s < kMaxSeg; ++s)
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            xbuf[(pw * kMaxSeg + s) * kRows + 4 * lane + c4] = F[s][c4];
+            F[s][c4] = 0;
+          }
+        producer_sync();
+        for (int s = 0; s < P.nseg; ++s) {
+          uint32_t tot = 0;
+#pragma unroll
+          for (int w = 0; w < kProdWarps; ++w) tot += xbuf[(w * kMaxSeg + s) * kRows + pt];
+          const uint32_t k = (tot + (1u << 22)) >> 23;
+          A[a_off(2 * s, pt)] = static_cast<uint8_t>(k);
+          A[a_off(2 * s + 1, pt)] = static_cast<uint8_t>(k >> 8);
+        }
+        A[a_off(6, pt)] = 1;  // constant row: the window's rounding constants
+        producer_sync();
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&a_full[sa]);
+      if (++c == C) c = 0;
+    }
+    cp_async_wait<0>();
+  } else {
+    // ---- epilogue: lane = coefficient i0 + 32 warp + lane -----------------------
+    // Column sums -> 32-bit digits d_h = (sum_{c<4} D[4h+c] 2^(8c) + carry) mod
+    // 2^32. Output limb j (j = 0 is the guard limb below out_bit when the
+    // ambiguity check is on) = bits [B0 + 64 j, +64) = e_{q+2j} | e_{q+2j+1} << 32
+    // with e_h = (d_{h+1}:d_h) >> S, B0 = 32 q + S. Digits 0..q only carry;
+    // then every 4 digits (one 16-column TMEM load) complete two limbs.
+    // (The rounding constants enter through a constant A row, build_bigint.)
+    const BigTcOut& o = P.o;
+    const int H = N / 4;
+    const int kst = (o.check_amb || o.force_exact) ? -1 : 0;
+    const int B0 = o.out_bit + 64 * kst;
+    const int S = B0 & 31, q = B0 >> 5;
+    const int L = o.out_limbs, nl = L - kst;
+    const uint64_t top = o.out_bits % 64 ? (uint64_t(1) << (o.out_bits % 64)) - 1 : ~0ull;
+    const uint32_t taddr0 = tmem + (uint32_t(32 * warp) << 16);
+    auto digit = [&](const uint32_t* v, int h, uint64_t& carry) -> uint32_t {
+      uint64_t z = carry;
+      if (h < H) {  // warp-uniform
+        z += v[0];
+        z += uint64_t(v[1]) * P.s8;
+        z += uint64_t(v[2]) * P.s16;
+        z += uint64_t(v[3]) * P.s24;
+      }
+      carry = z >> 32;
+      return static_cast<uint32_t>(z);
+    };
+    for (int it = 0; it < my_tiles; ++it) {
+      const int tile = blockIdx.x + it * gridDim.x;
+      const int e = tile / tiles_per_entry;
+      const size_t i = size_t(tile - e * tiles_per_entry) * kRows + 32 * warp + lane;
+      const int eb = e % P.B;
+      uint64_t* dst = (e < P.B ? o.out0 : o.out1) + (size_t(eb) * n + i) * L;
+      tc::mbar_wait_sleep<128>(&t_full, it & 1);
+      tc::fence_after();
+      uint64_t carry = 0;
+      uint32_t dprev = 0;
+      // digits 0 .. q: carry only
+      for (int h0 = 0; h0 <= q; h0 += 4) {
+        uint32_t v[16];
+        tc::tmem_ld16(taddr0 + 4 * h0, v);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (h0 + c <= q) dprev = digit(v + 4 * c, h0 + c, carry);
+      }
+      bool skip = false;
+      for (int j = 0; j < nl; j += 2) {
+        const int h = q + 1 + 2 * j;  // digits h .. h + 3 -> limbs j, j + 1
+        uint32_t v[16];
+        if (4 * h < N) {
+          tc::tmem_ld16(taddr0 + 4 * h, v);
+          tc::tmem_wait_ld();
+        }
+        const uint32_t d0 = digit(v, h, carry), d1 = digit(v + 4, h + 1, carry);
+        const uint32_t d2 = digit(v + 8, h + 2, carry), d3 = digit(v + 12, h + 3, carry);
+        const uint64_t l0 = __funnelshift_r(dprev, d0, S) |
+                            (uint64_t(__funnelshift_r(d0, d1, S)) << 32);
+        const uint64_t l1 = __funnelshift_r(d1, d2, S) |
+                            (uint64_t(__funnelshift_r(d2, d3, S)) << 32);
+        dprev = d3;
+        const int k0 = j + kst;
+        if (k0 < 0) {
+          // guard limb: exact unless its 64 bits are all ones (kernels.hpp Finisher)
+          skip = (o.check_amb && l0 == ~0ull) || o.force_exact;
+          if (skip) {
+            const unsigned slot = atomicAdd(o.flags.count, 1u);
+            if (slot < o.flags.capacity) o.flags.ids[slot] = static_cast<unsigned>(size_t(e) * n + i);
+          }
+        } else if (!skip) {
+          dst[k0] = k0 == L - 1 ? l0 & top : l0;
+        }
+        if (!skip && k0 + 1 < L) dst[k0 + 1] = k0 + 1 == L - 1 ? l1 & top : l1;
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&t_empty);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == kTmaWarp) tc::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+constexpr int kMaxRows = 1024;  // A rows (residues) per coefficient
+
+size_t bigint_tc_smem(int n_cols) {
+  return size_t(kSB) * n_cols * kChunk + size_t(kSA) * kABytes + size_t(kSR) * kRawBytes +
+         size_t(kProdWarps) * kMaxSeg * kRows * 4 + kMaxRows * 4 + 1024;
+}
+
+cudaError_t bigint_tc_setup_attributes() {
+  return cudaFuncSetAttribute(bigint_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kMaxDynSmem);
+}
+
+cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, int B, int log_n,
+                      const BigTcOut& o, cudaStream_t st) {
+  const size_t n = size_t(1) << log_n;
+  if (!t.tmap || t.nseg < 1 || t.nseg > kMaxSeg || n < size_t(kRows) || t.n_cols % 32 ||
+      t.n_cols > 480 || t.k_bytes % kChunk || bigint_tc_smem(t.n_cols) > size_t(kMaxDynSmem))
+    return cudaErrorInvalidValue;
+  if ((o.check_amb || o.force_exact) && !o.flags.count) return cudaErrorInvalidValue;
+  if (t.k_slot > kMaxRows) return cudaErrorInvalidValue;
+  for (int s2 = 0; s2 < t.nseg; ++s2)
+    if (t.np[s2] > 511) return cudaErrorInvalidValue;  // fixed-point k sum < 2^32
+  Params P{};
+  for (int s = 0; s < kMaxSeg; ++s) {
+    if (s < t.nseg) {
+      P.seg[s] = segs[s];
+      P.seg[s].slot0 = t.slot0[s];
+      P.seg[s].np = t.np[s];
+    } else {
+      P.seg[s].slot0 = 1 << 30;  // never selected
+    }
+  }
+  P.nseg = t.nseg;
+  P.B = B;
+  P.entries = entries;
+  P.log_n = log_n;
+  P.n_cols = t.n_cols;
+  P.k_bytes = t.k_bytes;
+  P.k_slot = t.k_slot;
+  P.rows_total = t.slot0[t.nseg - 1] + t.np[t.nseg - 1];  // real rows; padding up to k_slot
+  P.o = o;
+  P.s8 = 1u << 8;
+  P.s16 = 1u << 16;
+  P.s24 = 1u << 24;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = entries * static_cast<int>(n / kRows);
+  const int grid = tiles < sms ? tiles : sms;
+  if (o.check_amb || o.force_exact) {
+    cudaError_t e = cudaMemsetAsync(o.flags.count, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+  }
+  bigint_tc_kernel<<<grid, kThreads, bigint_tc_smem(t.n_cols), st>>>(
+      *static_cast<const CUtensorMap*>(t.tmap), P);
+  return cudaGetLastError();
+}
+
+}  // namespace hemul_gpu

@@ -10,6 +10,8 @@
 //     CRT(d2) -> fwd NTT -> evk product (cached evk forms) -> iNTT (2B rows)
 //     -> iCRT (2B)
 //   epilogue: out = R_logp(d + R_logQ(ks)) per component.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -61,6 +63,7 @@ struct RegionDev {
   int np = 0;
   int target_bits = 0;
   DevBuf primes, tw, itw, btab, hat, big_p, half_p;
+  DevBuf primes_t;  // word 32: inverse NTT constants that output t_j (level_tables.hpp)
   struct Crt {
     int in_bits;
     CrtWeights w;
@@ -99,12 +102,22 @@ struct RegionDev {
   }
 };
 
+// A tensor-core iCRT / finisher table on the device, with its TMA map.
+struct BigTcDev {
+  DevBuf btab;
+  alignas(64) CUtensorMap tmap;
+  BigTcTable t;
+  int out_bit = 0, out_bits = 0;
+};
+
 // Both regions of a level in one basis, and the fused finisher's table.
 struct Basis {
   std::unique_ptr<RegionDev> r1, r2;
   bool has_fin = false;
   DevBuf fin_btab;
   Finisher fin;  // fused ModDown + add + rescale table (he_mul levels only)
+  // int8 tensor-core forms (30-bit split basis): iCRT of d2 and the finisher
+  std::unique_ptr<BigTcDev> icrt_tc, fin_tc;
 };
 
 struct Level {
@@ -266,6 +279,7 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
     upload(d.itw, h.itw, st);
   } else {
     upload(d.primes, h.dev32, st);
+    upload(d.primes_t, h.dev32_t, st);
     upload(d.tw, h.tw32, st);
     upload(d.itw, h.itw32, st);
   }
@@ -308,6 +322,53 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
     dt.tab.end_bit = t.end_bit;
     d.crt_tc.push_back(std::move(dt));
   }
+}
+
+// 2-D TMA map of a u8 table [rows][inner] with boxes of box_inner x box_rows
+// and 64-byte swizzle (bigint_tc.cu's B operand). The driver entry point is
+// resolved through the runtime (no libcuda link).
+void make_tmap_u8(CUtensorMap* m, const void* g, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                  uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !fn)
+      throw CudaFail(HEMUL_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {inner, rows};
+  const cuuint64_t strides[1] = {inner};
+  const cuuint32_t box[2] = {box_inner, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(g), dims, strides,
+                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaFail(HEMUL_E_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
+std::unique_ptr<BigTcDev> upload_bigint(const BigTcHost& h, cudaStream_t st) {
+  if (h.n_cols > 480 || bigint_tc_smem(h.n_cols) > size_t(kMaxDynSmem)) return nullptr;
+  auto d = std::make_unique<BigTcDev>();
+  upload(d->btab, h.btab, st);
+  make_tmap_u8(&d->tmap, d->btab.ptr, uint64_t(h.k_bytes), uint64_t(h.n_cols), 64,
+               uint32_t(h.n_cols / 2));
+  BigTcTable& t = d->t;
+  t.btab = d->btab.as<uint8_t>();
+  t.tmap = &d->tmap;
+  t.n_cols = h.n_cols;
+  t.k_bytes = h.k_bytes;
+  t.k_slot = h.k_slot;
+  t.nseg = h.nseg;
+  for (int s = 0; s < 3; ++s) {
+    t.slot0[s] = h.slot0[s];
+    t.np[s] = h.np[s];
+  }
+  d->out_bit = h.out_bit;
+  d->out_bits = h.out_bits;
+  return d;
 }
 
 int host_threads() {
@@ -367,7 +428,10 @@ Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
     f.log_p = c->log_p;
     f.split_h = split_h;
     b.has_fin = true;
+    if (word == 32 && split_h % 8 == 0)
+      b.fin_tc = upload_bigint(build_finisher_tc(h1, h2, log_q, c->log_q_max, c->log_p), c->stream);
   }
+  if (word == 32 && split_h % 8 == 0) b.icrt_tc = upload_bigint(build_icrt_tc(h1), c->stream);
   check(cudaStreamSynchronize(c->stream), "level upload");
   b.r1 = std::move(r1);
   b.r2 = std::move(r2);
@@ -416,14 +480,17 @@ void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t r
 }
 
 // Inverse NTT; passes = 1 runs only the final pass (after a fused middle pass).
+// to_t (30-bit basis): the last level scales by n^-1 (P/p_j)^-1, giving the
+// tensor-core iCRT / finisher operand t_j instead of x_j.
 template <class F>
 void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t rows, int stage,
-             int passes = 2) {
+             int passes = 2, bool to_t = false) {
   const int total = ntt_num_passes(c->log_n);
+  const typename F::Prime* pr =
+      to_t ? r.primes_t.as<const typename F::Prime>() : r.P<F>();
   for (int pass = total > passes ? total - passes : 0; pass < total; ++pass)
     run(c, stage, pass + 1 == total ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B, "iNTT", [&] {
-      return ntt_inverse_pass<F>(pass, data, rows, r.np, c->log_n, r.ITW<F>(), r.P<F>(),
-                                 c->stream);
+      return ntt_inverse_pass<F>(pass, data, rows, r.np, c->log_n, r.ITW<F>(), pr, c->stream);
     });
 }
 
@@ -552,7 +619,7 @@ hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_overri
         cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventDisableTiming) != cudaSuccess)
       return HEMUL_E_CUDA;
   if (ntt_setup_attributes() != cudaSuccess || crt_setup_attributes() != cudaSuccess ||
-      crt_tc_setup_attributes() != cudaSuccess ||
+      crt_tc_setup_attributes() != cudaSuccess || bigint_tc_setup_attributes() != cudaSuccess ||
       icrt_setup_attributes() != cudaSuccess)
     return HEMUL_E_CUDA;
   *out = c.release();
@@ -834,6 +901,10 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       return crt_forward_multi<F>(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
     });
   }
+  // int8 tensor-core iCRT + finisher (30-bit split basis): the inverse NTTs
+  // feeding them output t_j directly
+  bool tc_big = false;
+  if constexpr (kSplit) tc_big = c->tensor_cores && bs.icrt_tc && bs.fin_tc;
   const bool mid = ntt_has_mid(log_n);
   if (mid) {
     // forward pass A, then one fused pass: forward pass B + tensor product +
@@ -846,7 +917,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
         return ntt_mid_tensor<F>(R1, R1 + r1w, R1 + 2 * r1w, R1 + 3 * r1w, B, r1.np, log_n,
                                  r1.TW<F>(), r1.ITW<F>(), p1, c->stream);
     });
-    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 1);
+    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 1, tc_big);
   } else {
     ntt_fwd<F>(c, r1, R1, kInSlots * B * r1.np, HEMUL_STAGE_NTT);
     // pointwise products are booked under iCRT like rns.cpp:364
@@ -857,16 +928,39 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
         return tensor_product<F>(R1, R1 + r1w, R1 + 2 * r1w, R1 + 3 * r1w, R1 + r1w,
                                  R1 + 2 * r1w, R1, B, r1.np, log_n, p1, c->stream);
     });
-    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT);
+    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 2, tc_big);
   }
   // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
   // and are reconstructed inside the finisher
   ensure(c->dpoly, B * poly_w * 8);
   uint64_t* d2 = c->dpoly.as<uint64_t>();
-  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1", [&] {
-    return icrt<F>(R1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream, nullptr,
-                   kSplit ? R1 + r1w : nullptr);
-  });
+  bool icrt_done = false;
+  if constexpr (kSplit) {
+    if (tc_big) {
+      const BigTcDev& T = *bs.icrt_tc;
+      BigTcSeg segs[2];
+      for (int h2 = 0; h2 < 2; ++h2) {
+        segs[h2].base = R1 + h2 * r1w;
+        segs[h2].estride = static_cast<long long>(r1.np) * n;
+        segs[h2].primes = p1;
+      }
+      BigTcOut o;
+      o.out0 = o.out1 = d2;
+      o.out_limbs = L;
+      o.out_bit = T.out_bit;
+      o.out_bits = T.out_bits;
+      run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1 (tensor cores)", [&] {
+        return bigint_tc(T.t, segs, static_cast<int>(B), static_cast<int>(B), log_n, o, c->stream);
+      });
+      icrt_done = true;
+    }
+  }
+  if (!icrt_done) {
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1", [&] {
+      return icrt<F>(R1, B, log_n, p1, r1.np, r1.icrt, d2, c->stream, nullptr,
+                     kSplit ? R1 + r1w : nullptr);
+    });
+  }
   const W* D1 = R1 + (kSplit ? 4 : 2) * r1w;  // d1 (c0)
   const W* D0 = R1 + (kSplit ? 2 : 1) * r1w;  // d0 (c0)
   // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
@@ -897,12 +991,12 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       return ntt_mid_evk<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, r2.TW<F>(), r2.ITW<F>(), p2,
                             c->stream);
     });
-    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1);
+    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1, tc_big);
   } else {
     ntt_fwd<F>(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",
         [&] { return evk_product<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
-    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT);
+    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 2, tc_big);
   }
   // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
   // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
@@ -913,10 +1007,48 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   flags.ids = flags.count + 1;
   Finisher fin = bs.fin;
   fin.hi_off = kSplit ? r1w : 0;
-  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
-    return finish_keyswitch<F>(KA, D1, D0, B, log_n, p2, r2.np, p1, r1.np, fin, r2.icrt,
-                               r1.icrt, out_ax, out_bx, flags, c->force_exact, c->stream);
-  });
+  bool fin_done = false;
+  if constexpr (kSplit) {
+    if (tc_big) {
+      const BigTcDev& T = *bs.fin_tc;
+      BigTcSeg segs[3];
+      segs[0].base = KA;  // entries e < B: ks_a (KA), e >= B: ks_b (KB = KA + B np2 n)
+      segs[0].estride = static_cast<long long>(r2.np) * n;
+      segs[0].half_off = static_cast<long long>(r2w);
+      segs[0].primes = p2;
+      for (int h2 = 0; h2 < 2; ++h2) {  // d1 (ax) / d0 (bx), c0 then c1 = c0 + r1w
+        segs[1 + h2].base = D1 + h2 * r1w;
+        segs[1 + h2].estride = static_cast<long long>(r1.np) * n;
+        segs[1 + h2].half_off = static_cast<long long>(D0 - D1);
+        segs[1 + h2].primes = p1;
+      }
+      BigTcOut o;
+      o.out0 = out_ax;
+      o.out1 = out_bx;
+      o.out_limbs = limbs_of(log_q - c->log_p);
+      o.out_bit = T.out_bit;
+      o.out_bits = T.out_bits;
+      o.check_amb = 1;
+      o.force_exact = c->force_exact;
+      o.flags = flags;
+      run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher (tensor cores)", [&] {
+        cudaError_t e = bigint_tc(T.t, segs, static_cast<int>(2 * B), static_cast<int>(B), log_n, o,
+                                  c->stream);
+        if (e != cudaSuccess) return e;
+        Finisher ft = fin;
+        ft.t_inputs = 1;
+        return finish_fixup<F32>(KA, D1, D0, B, log_n, p2, r2.np, p1, r1.np, ft, r2.icrt,
+                                 r1.icrt, out_ax, out_bx, flags, c->stream);
+      });
+      fin_done = true;
+    }
+  }
+  if (!fin_done) {
+    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher", [&] {
+      return finish_keyswitch<F>(KA, D1, D0, B, log_n, p2, r2.np, p1, r1.np, fin, r2.icrt,
+                                 r1.icrt, out_ax, out_bx, flags, c->force_exact, c->stream);
+    });
+  }
   ++c->launches;  // the (normally empty) exact fix-up kernel
 }
 

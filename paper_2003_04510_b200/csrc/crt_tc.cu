@@ -91,8 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t a_full[kMaxStages], a_empty[kMaxStages], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base;
   __shared__ uint4 eprimes[kMaxTilePrimes];  // {p, one_q, beta, beta_q} of the tile's primes
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_addr(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t n = size_t(1) << log_n;
   const int kpad = tab.kpad;                  // K bytes the MMAs read (multiple of 32)
@@ -166,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // cp.async (zero-filled past the field); the stage's barrier completes
       // when every producer thread's copies have landed
       const int pt = threadIdx.x - 32 * (kMmaWarp + 1);
-      tc::mbar_wait(&a_empty[s], ((it / stages) & 1) ^ 1);
+      tc::mbar_wait_sleep<32>(&a_empty[s], ((it / stages) & 1) ^ 1);
       uint8_t* dstA = sA + s * a_bytes;
       const uint64_t* base = in.p[t] + (size_t(b) * n + i0) * limbs;
       const int chunks = kpad / 16;  // 16-byte chunks per row
@@ -219,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       // ---- epilogue: lane quadrant warp % 4 (coefficient i0 + 32 (warp % 4)
       // + lane), prime groups split between the two warps of a quadrant
-      tc::mbar_wait(&t_full[acc], (it >> 1) & 1);
+      tc::mbar_wait_sleep<64>(&t_full[acc], (it >> 1) & 1);
       tc::fence_after();
       const int quad = warp & 3, part = warp >> 2;  // part < kEpiWarps / 4
       const uint32_t taddr = tmem + acc * 256 + (uint32_t(32 * quad) << 16);

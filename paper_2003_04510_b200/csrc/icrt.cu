@@ -238,15 +238,19 @@ __global__ void __launch_bounds__(NW * 32) icrt_kernel(const typename F::W* __re
 }
 
 // Exact centered value mod 2^tbits (rns.cpp:148-169, 192-233), one thread.
+// t_inputs: the residues already are t_j = x_j (P/p_j)^-1 (the inverse NTT
+// folded the factor in, bigint_tc.cu)
 template <class F>
 __device__ void exact_centered(const typename F::W* rns_b, size_t n, size_t i,
                                const typename F::Prime* primes, int np, const IcrtTable& t,
-                               int tbits, uint64_t* o /* ceil(tbits/64) limbs */) {
+                               int tbits, uint64_t* o /* ceil(tbits/64) limbs */,
+                               bool t_inputs = false) {
   const int pl = t.p_limbs, al = pl + 2;
   uint64_t acc[kFixMaxLimbs];
   for (int k = 0; k < al; ++k) acc[k] = 0;
   for (int j = 0; j < np; ++j) {
-    const uint64_t tj = F::hat_inv(rns_b[size_t(j) * n + i], primes[j]);
+    const uint64_t xj = rns_b[size_t(j) * n + i];
+    const uint64_t tj = t_inputs ? xj : F::hat_inv(xj, primes[j]);
     const uint64_t* h = t.hat + size_t(j) * pl;
     uint64_t carry = 0;
     for (int k = 0; k < al; ++k) {
@@ -419,12 +423,12 @@ __global__ void finish_fixup_kernel(const typename F::W* __restrict__ ks,
     const bool is_bx = bb >= B;
     const int b = is_bx ? bb - B : bb;
     uint64_t x2[kFixMaxLimbs], x1[kFixMaxLimbs];
-    exact_centered<F>(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2);
+    exact_centered<F>(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2, f.t_inputs);
     const typename F::W* d1p = (is_bx ? d_bx : d_ax) + size_t(b) * np1 * n;
-    exact_centered<F>(d1p, n, i, p1, np1, t1, f.log_q, x1);
+    exact_centered<F>(d1p, n, i, p1, np1, t1, f.log_q, x1, f.t_inputs);
     if (f.hi_off) {  // split: x1 = c0 + 2^h c1 mod 2^logq
       uint64_t x1h[kFixMaxLimbs];
-      exact_centered<F>(d1p + f.hi_off, n, i, p1, np1, t1, f.log_q, x1h);
+      exact_centered<F>(d1p + f.hi_off, n, i, p1, np1, t1, f.log_q, x1h, f.t_inputs);
       for (int k = 0; k < l1; ++k) add_shifted(x1, l1, f.split_h + 64 * k, x1h[k]);
       if (f.log_q % 64) x1[l1 - 1] &= (uint64_t(1) << (f.log_q % 64)) - 1;
     }
@@ -585,6 +589,22 @@ cudaError_t finish_keyswitch(const typename F::W* ks, const typename F::W* d_ax,
                                          np1, f, t2, t1, out_ax, out_bx, flags);
   return cudaGetLastError();
 }
+
+template <class F>
+cudaError_t finish_fixup(const typename F::W* ks, const typename F::W* d_ax,
+                         const typename F::W* d_bx, size_t B, int log_n,
+                         const typename F::Prime* p2, int np2, const typename F::Prime* p1,
+                         int np1, const Finisher& f, const IcrtTable& t2, const IcrtTable& t1,
+                         uint64_t* out_ax, uint64_t* out_bx, const IcrtFlags& flags,
+                         cudaStream_t st) {
+  finish_fixup_kernel<F><<<64, 64, 0, st>>>(ks, d_ax, d_bx, static_cast<int>(B), log_n, p2, np2, p1,
+                                         np1, f, t2, t1, out_ax, out_bx, flags);
+  return cudaGetLastError();
+}
+template cudaError_t finish_fixup<F32>(const uint32_t*, const uint32_t*, const uint32_t*, size_t,
+                                       int, const DevPrime32*, int, const DevPrime32*, int,
+                                       const Finisher&, const IcrtTable&, const IcrtTable&,
+                                       uint64_t*, uint64_t*, const IcrtFlags&, cudaStream_t);
 
 #define HEMUL_ICRT_INSTANTIATE(F)                                                             \
   template cudaError_t icrt<F>(const F::W*, size_t, int, const F::Prime*, int,                \

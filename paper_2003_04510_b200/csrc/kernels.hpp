@@ -171,6 +171,7 @@ struct Finisher {
   // hi_off residues after c0; hi_off = 0: unsplit
   int split_h = 0;
   size_t hi_off = 0;
+  int t_inputs = 0;  // residues are t_j already (tensor-core path, bigint_tc.cu)
 };
 cudaError_t finisher_setup_attributes();
 // ks: 2B x np2 x n (B ax-batches then B bx-batches), d_ax / d_bx: B x np1 x n
@@ -184,6 +185,55 @@ cudaError_t finish_keyswitch(const typename F::W* ks, const typename F::W* d_ax,
                              const IcrtTable& t2, const IcrtTable& t1, uint64_t* out_ax,
                              uint64_t* out_bx, const IcrtFlags& flags, int force_exact,
                              cudaStream_t st);
+
+// ---- iCRT / key-switch finisher on the int8 tensor cores (bigint_tc.cu) -----
+// One RNS operand feeding the GEMM's A rows: entry e (< entries) reads
+// rows j < np at base + (e % B) * estride + (e >= B ? half_off : 0) + j * n.
+struct BigTcSeg {
+  const uint32_t* base = nullptr;
+  long long estride = 0, half_off = 0;
+  const DevPrime32* primes = nullptr;  // pad[0] = floor(2^55 / p) (the k quotient)
+  int np = 0;
+  int slot0 = 0;  // set from the table
+};
+// Constant GEMM operand (level_tables.cpp build_bigint_tc): btab [n_cols][k_bytes]
+// u8, column m <-> 2^(8 (m + m0)) of the window; segment s's row j occupies
+// K bytes 4 (slot0[s] + j) .. +3, the k quotients bytes 4 k_slot + 2 s, +1.
+// tmap: host pointer to the CUtensorMap of btab (box 64 x n_cols / 2, 64-byte
+// swizzle), built by the context.
+struct BigTcTable {
+  const uint8_t* btab = nullptr;
+  const void* tmap = nullptr;
+  int n_cols = 0;   // multiple of 32, <= 480 (16-column TMEM reads past the end)
+  int k_bytes = 0;  // multiple of 64
+  int k_slot = 0;
+  int nseg = 0;
+  int slot0[3] = {0, 0, 0}, np[3] = {0, 0, 0};
+};
+// Output window: limbs of bits [out_bit, out_bit + out_bits) of the window
+// value (rounding constants included by the table) to out0 (entries < B) / out1 (>= B),
+// n x out_limbs per entry. check_amb: coefficients whose 64 bits below
+// out_bit are all ones (truncated window, p = 2^-64) and, with force_exact,
+// every coefficient, are listed in flags and left to the exact fix-up.
+struct BigTcOut {
+  uint64_t* out0 = nullptr;
+  uint64_t* out1 = nullptr;
+  int out_limbs = 0, out_bit = 0, out_bits = 0;
+  int check_amb = 0, force_exact = 0;
+  IcrtFlags flags;
+};
+cudaError_t bigint_tc_setup_attributes();
+size_t bigint_tc_smem(int n_cols);
+cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, int B, int log_n,
+                      const BigTcOut& o, cudaStream_t st);
+// Exact fix-up of flagged finisher coefficients (icrt.cu finish_fixup_kernel).
+template <class F>
+cudaError_t finish_fixup(const typename F::W* ks, const typename F::W* d_ax,
+                         const typename F::W* d_bx, size_t B, int log_n,
+                         const typename F::Prime* p2, int np2, const typename F::Prime* p1,
+                         int np1, const Finisher& f, const IcrtTable& t2, const IcrtTable& t1,
+                         uint64_t* out_ax, uint64_t* out_bx, const IcrtFlags& flags,
+                         cudaStream_t st);
 
 // ---- element-wise RNS and polynomial kernels (poly.cu) ---------------------
 // out = a * b mod p_j over batch x np x n.

@@ -280,6 +280,7 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
       d.ninv = uint32_t(ninv[j]);
       d.ninv_q = shoup_q32(ninv[j], p);
       d.inv_p_dbl = 1.0 / double(p);
+      d.pad[0] = uint32_t((u128(1) << 55) / p);  // bigint_tc.cu: fixed-point k quotient
     }
     r.tw32.resize(size_t(count) * n);
     r.itw32.resize(size_t(count) * n);
@@ -312,6 +313,19 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
       r.dev32[j].w1n_q = shoup_q32(w1n, p);
     }
   });
+
+  if (word == 32) {
+    r.dev32_t = r.dev32;
+    for (int j = 0; j < count; ++j) {
+      const uint64_t p = r.primes[j];
+      DevPrime32& d = r.dev32_t[j];
+      const uint64_t nt = mulmod(d.ninv, inv[j], p), wt = mulmod(d.w1n, inv[j], p);
+      d.ninv = uint32_t(nt);
+      d.ninv_q = shoup_q32(nt, p);
+      d.w1n = uint32_t(wt);
+      d.w1n_q = shoup_q32(wt, p);
+    }
+  }
 
   // CRT weights of 2^(25 m) mod p_j (kernels.hpp CrtWeights): w64 as two
   // 30-bit halves, the 30-bit basis as one column
@@ -414,6 +428,81 @@ RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, in
       u = mulmod(u, step, p);
     }
   }
+  return t;
+}
+
+namespace {
+
+uint8_t nat_byte(const Nat& v, long e) {
+  if (e < 0 || size_t(e / 8) >= v.size()) return 0;
+  return uint8_t(v[e / 8] >> (8 * (e % 8)));
+}
+
+// segs[s] = {rows V_j..., k row V_k}; values < 2^T. The A operand carries a
+// constant 1 at K byte 4 k_slot + 6: its row adds `round` (< 2^T) to every
+// coefficient (the finisher's rounding halves).
+BigTcHost build_bigint(const std::vector<std::vector<Nat>>& segs, int T, int base8,
+                       const Nat& round) {
+  BigTcHost t;
+  t.nseg = static_cast<int>(segs.size());
+  t.base8 = base8;
+  // every segment starts on a 16-row (64-byte) chunk: a chunk's rows belong to
+  // one segment (padding rows have zero B rows)
+  int slot = 0;
+  for (int s = 0; s < t.nseg; ++s) {
+    t.slot0[s] = slot;
+    t.np[s] = static_cast<int>(segs[s].size()) - 1;
+    slot += (t.np[s] + 15) / 16 * 16;
+  }
+  t.k_slot = slot;
+  t.k_bytes = 4 * t.k_slot + 64;
+  t.n_cols = ((T - base8 + 7) / 8 + 31) / 32 * 32;
+  const long m0 = base8 / 8;
+  t.btab.assign(size_t(t.n_cols) * t.k_bytes, 0);
+  for (int s = 0; s < t.nseg; ++s) {
+    for (int j = 0; j <= t.np[s]; ++j) {
+      const Nat& v = segs[s][j];
+      const bool krow = j == t.np[s];
+      const int kb0 = krow ? 4 * t.k_slot + 2 * s : 4 * (t.slot0[s] + j);
+      const int nb = krow ? 2 : 4;  // k < 2^16, t < 2^32
+      for (int m = 0; m < t.n_cols; ++m)
+        for (int b = 0; b < nb; ++b)
+          t.btab[size_t(m) * t.k_bytes + kb0 + b] = nat_byte(v, m + m0 - b);
+    }
+  }
+  for (int m = 0; m < t.n_cols; ++m) t.btab[size_t(m) * t.k_bytes + 4 * t.k_slot + 6] = nat_byte(round, m + m0);
+  return t;
+}
+
+}  // namespace
+
+BigTcHost build_icrt_tc(const RegionHost& r1) {
+  const int np = r1.np, T = r1.target_bits;
+  std::vector<std::vector<Nat>> segs(2);
+  for (int h = 0; h < 2; ++h)
+    for (int j = 0; j <= np; ++j) segs[h].push_back(r1.hat_t[size_t(h) * (np + 1) + j]);
+  BigTcHost t = build_bigint(segs, T, 0, Nat{});
+  t.out_bit = 0;
+  t.out_bits = T;
+  return t;
+}
+
+BigTcHost build_finisher_tc(const RegionHost& r1, const RegionHost& r2, int log_q, int log_q_max,
+                            int log_p) {
+  const int T2 = log_q + log_q_max;
+  const int base8 = std::max(0, log_q_max - kFinisherGuardBits) / 8 * 8;
+  std::vector<std::vector<Nat>> segs(3);
+  for (int j = 0; j <= r2.np; ++j) segs[0].push_back(r2.hat_t[j]);
+  for (int h = 0; h < 2; ++h)
+    for (int j = 0; j <= r1.np; ++j)
+      segs[1 + h].push_back(nat_shl_low(r1.hat_t[size_t(h) * (r1.np + 1) + j], log_q_max, T2));
+  // rounding halves of R_logQ and R_logp: 2^(logQ-1) + 2^(logQ+logp-1)
+  Nat round(size_t((T2 + 63) / 64), 0);
+  round[(log_q_max - 1) / 64] |= uint64_t(1) << ((log_q_max - 1) % 64);
+  round[(log_q_max + log_p - 1) / 64] |= uint64_t(1) << ((log_q_max + log_p - 1) % 64);
+  BigTcHost t = build_bigint(segs, T2, base8, round);
+  t.out_bit = log_q_max + log_p - base8;
+  t.out_bits = log_q - log_p;
   return t;
 }
 

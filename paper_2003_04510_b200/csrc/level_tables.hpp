@@ -34,6 +34,10 @@ struct RegionHost {
   std::vector<DevPrime> dev;         // np (word 64)
   std::vector<Twiddle> tw, itw;      // np * n each, ShoupPair tables (word 64)
   std::vector<DevPrime32> dev32;     // np (word 32)
+  // word 32: the same with ninv, w1n pre-multiplied by (P/p_j)^-1, so that
+  // the last inverse-NTT level outputs t_j = x_j (P/p_j)^-1 directly (the
+  // operand of the tensor-core iCRT / finisher, bigint_tc.cu)
+  std::vector<DevPrime32> dev32_t;
   std::vector<Twiddle32> tw32, itw32;  // np * n each (word 32)
   // CRT weights per input width (see kernels.hpp CrtWeights)
   struct Crt {
@@ -101,6 +105,22 @@ inline int crt_cols_pad(int cols) {
   const int c16 = (cols + 15) / 16 * 16;
   return c16 <= 192 ? c16 : (cols + 127) / 128 * 128;
 }
+
+// Constant operand of the tensor-core iCRT / finisher GEMM (kernels.hpp
+// BigTcTable): segments of rows V (< 2^T) with their k rows (-P), the window
+// starting at bit base8 (multiple of 8).
+struct BigTcHost {
+  int n_cols = 0, k_bytes = 0, k_slot = 0, nseg = 0, base8 = 0;
+  int slot0[3] = {0, 0, 0}, np[3] = {0, 0, 0};
+  // output window (relative to base8); rounding constants are a table row
+  int out_bit = 0, out_bits = 0;
+  std::vector<uint8_t> btab;  // [n_cols][k_bytes]
+};
+// iCRT of a split region 1 (d = c0 + 2^h c1 mod 2^log_q, exact from bit 0).
+BigTcHost build_icrt_tc(const RegionHost& r1);
+// Fused ModDown + add + rescale (same window as build_finisher).
+BigTcHost build_finisher_tc(const RegionHost& r1, const RegionHost& r2, int log_q, int log_q_max,
+                            int log_p);
 
 // Table of the fused ModDown + add + rescale kernel (kernels.hpp Finisher).
 struct FinisherHost {

@@ -26,18 +26,35 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                    smem_addr(bar))
                : "memory");
 }
-// Blocks until the phase with the given parity has completed. try_wait
-// suspends the thread until the phase completes or the time hint (ns)
-// elapses, so the retry loop spins rarely.
+// Blocks until the phase with the given parity has completed (tight retry:
+// for the roles on the critical path).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity), "n"(1000000)
+      "r"(parity)
       : "memory");
+}
+// The same with a nanosleep back-off between probes, for warps that wait
+// long (epilogue, producers ahead of the MMA) and would otherwise take issue
+// slots from the warps they share a scheduler with.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+template <int kSleepNs>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(kSleepNs);
 }
 
 // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
