@@ -19,11 +19,11 @@ Printed JSON (rank 0, one line):
   e2e       the same metric through the C-ABI with pinned HOST buffers: every
             step copies its inputs H2D and its outputs D2H inside the timed
             region
-  roofline  dominant kernel class of the timed region: its algorithmic
-            integer work (32-bit IMAD-equivalent ops) / its
-            measured device time, against the IMAD.WIDE peak measured on this
-            device in this run (integer-bound path; MEASURED_PEAKS.json has
-            only HBM and bf16 peaks)
+  roofline  dominant kernel class of the timed region against its bound:
+            NTT passes = HBM bytes vs MEASURED_PEAKS.json; base-conversion
+            GEMMs = algorithmic u8 MACs vs the int8 tensor-core peak measured
+            on this device in this run (tcgen05 probe; or IMAD.WIDE products
+            vs the IMAD probe with --engine imad). `kernels` lists every class.
   cpu_baseline  the reference CPU he_mul (oracle/_ref, compiled from the
             reference sources) on this host's cores, 1 HE Mul sample
 --impl reference times that same reference CPU implementation as the whole
@@ -63,17 +63,28 @@ def limbs(bits: int) -> int:
 # --------------------------------------------------------------------------
 # algorithmic work per kernel class
 # --------------------------------------------------------------------------
-GEMM_CLASSES = ("crt", "icrt", "finish")     # bound: IMAD.WIDE.U32 issue
+GEMM_CLASSES = ("crt", "icrt", "finish")     # bound: int8 tensor cores (or IMAD.WIDE.U32)
 NTT_CLASSES = ("ntt_a", "ntt_b", "intt_b", "intt_a", "mid_r1", "mid_r2", "tensor", "evk")
 
 
-def kernel_model(p, word: int, np1: int, np2: int, B: int, log_q: int) -> dict[str, dict]:
+def split_point(log_q: int) -> int:
+    """level_tables.hpp split_point: ceil(log_q/2) rounded up to a byte."""
+    h = (log_q + 1) // 2
+    h8 = (h + 7) // 8 * 8
+    return h8 if h8 < log_q else h
+
+
+def kernel_model(p, word: int, np1: int, np2: int, B: int, log_q: int,
+                 tensor: bool = False) -> dict[str, dict]:
     """Per kernel class and step: `products` = the algorithmic inner-product
-    terms of the integer GEMMs (one IMAD.WIDE.U32 each: 25-bit chunk x
-    30-bit operand), `bytes` = the HBM bytes the kernel must move (each
-    operand read once, each result written once), `butterflies` = NTT
-    butterflies. word 32: the 30-bit basis with split region 1 (np1 primes
-    per half product); word 64: the reference's w64 basis."""
+    terms of the integer GEMMs on the IMAD pipe (one IMAD.WIDE.U32 each:
+    25-bit chunk x 30-bit operand), or with `tensor` (30-bit basis, int8
+    tensor cores) `macs` = the algorithmic u8 x u8 multiply-accumulates
+    (byte planes x bytes; padding not counted); `bytes` = the
+    HBM bytes the kernel must move (each operand read once, each result
+    written once); `butterflies` = NTT butterflies. word 32: the 30-bit
+    basis with split region 1 (np1 primes per half product); word 64: the
+    reference's w64 basis."""
     n, ln = p.n, p.log_n
     s1 = ln if ln <= 11 else (ln + 1) // 2
     s2 = ln - s1
@@ -93,6 +104,13 @@ def kernel_model(p, word: int, np1: int, np2: int, B: int, log_q: int) -> dict[s
     fwd_rows = in1 * B * np1 + B * np2
     inv_rows = out1 * B * np1 + 2 * B * np2
     bf = n // 2
+    if tensor and word == 32:
+        h = split_point(log_q)
+        T2 = log_q + p.log_q_max
+        base8 = max(0, p.log_q_max - 125) // 8 * 8
+        crt_macs = n * B * (8 * math.ceil(h / 8) * 4 * np1 + math.ceil(log_q / 8) * 4 * np2)
+        icrt_macs = n * B * (4 * 2 * np1 + 7) * math.ceil(log_q / 8)
+        fin_macs = n * 2 * B * (4 * (np2 + 2 * np1) + 7) * math.ceil((T2 - base8) / 8)
     m = {
         "crt": {"products": crt_products,
                 "bytes": 5 * B * n * L * 8 + fwd_rows * rb},
@@ -112,6 +130,10 @@ def kernel_model(p, word: int, np1: int, np2: int, B: int, log_q: int) -> dict[s
         "tensor": {"bytes": (in1 + out1) * B * np1 * rb},
         "evk": {"bytes": 3 * B * np2 * rb + 2 * np2 * rb},
     }
+    if tensor and word == 32:
+        for k, v in (("crt", crt_macs), ("icrt", icrt_macs), ("finish", fin_macs)):
+            del m[k]["products"]
+            m[k]["macs"] = v
     return m
 
 
@@ -233,6 +255,9 @@ def main() -> None:
     ap.add_argument("--latency-reps", type=int, default=5)
     ap.add_argument("--basis", type=int, default=32, choices=[32, 64],
                     help="RNS basis of he_mul (HEMUL_OPT_BASIS); results are identical")
+    ap.add_argument("--engine", default="tc", choices=["tc", "imad"],
+                    help="30-bit basis base conversions on the int8 tensor cores (tc) or the "
+                         "IMAD.WIDE pipe (HEMUL_OPT_TENSOR_CORES); results are identical")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     B = args.batch or DEFAULT_BATCH[args.config]
@@ -261,6 +286,7 @@ def main() -> None:
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_basis(args.basis)
+    ctx.set_tensor_cores(args.engine == "tc")
     q = p.log_q_max
     L, Lo, Le = limbs(q), limbs(q - p.log_p), limbs(2 * q)
     n = p.n
@@ -370,14 +396,17 @@ def main() -> None:
     dig = ciphertext_digest(q - p.log_p, o0[0], o0[1])
     digests = gather_to_rank0(dig) or []
 
-    # ---- roofline: GEMM kernels vs the IMAD.WIDE probe, NTT kernels vs HBM --
+    # ---- roofline: GEMM kernels vs the int8 tensor-core / IMAD.WIDE probes
+    # measured on this device in this run, NTT kernels vs HBM
     imad_peak = ctx.imad_peak()
+    tc_peak = ctx.tc_peak()
+    tensor = args.engine == "tc" and word == 32
     peaks = {}
     pfile = ROOT / "MEASURED_PEAKS.json"
     if pfile.exists():
         peaks = json.loads(pfile.read_text())
     hbm_peak = peaks.get("hbm_gbs")
-    model = kernel_model(p, word, np1, np2, B, q)
+    model = kernel_model(p, word, np1, np2, B, q, tensor=tensor)
     per_class = {}
     for k, (ms, cnt) in kstats.items():
         if k not in model or ms <= 0:
@@ -391,6 +420,9 @@ def main() -> None:
         if "products" in mk:
             e["tiops"] = mk["products"] / sec / 1e12
             e["imad_frac"] = e["tiops"] / (imad_peak / 1e12)
+        if "macs" in mk:
+            e["tensor_tops"] = 2 * mk["macs"] / sec / 1e12
+            e["tensor_frac"] = e["tensor_tops"] / (tc_peak / 1e12)
         if "butterflies" in mk:
             e["gbutterflies_s"] = mk["butterflies"] / sec / 1e9
         per_class[k] = e
@@ -399,7 +431,12 @@ def main() -> None:
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
-    if "tiops" in per_class[dom]:
+    if "tensor_tops" in per_class[dom]:
+        roof = {"bound": "tensor", "kernel": dom, "achieved": per_class[dom]["tensor_tops"],
+                "peak": tc_peak / 1e12, "unit": "TOP/s (int8, dense)",
+                "frac": per_class[dom]["tensor_frac"], "traffic": traffic,
+                "peak_source": "tcgen05.mma kind::i8 probe on this device, this run"}
+    elif "tiops" in per_class[dom]:
         roof = {"bound": "imad", "kernel": dom, "achieved": per_class[dom]["tiops"],
                 "peak": imad_peak / 1e12, "unit": "TIOP/s (IMAD.WIDE.U32 products)",
                 "frac": per_class[dom]["imad_frac"], "traffic": traffic,
@@ -440,6 +477,9 @@ def main() -> None:
                     "d2h_bytes_per_step": 2 * B * n * Lo * 8},
             "roofline": roof,
             "kernels": per_class,
+            "engine": "int8 tensor cores (tcgen05)" if tensor else "IMAD.WIDE integer pipe",
+            "peaks": {"tensor_int8_tops": tc_peak / 1e12, "imad_wide_tops": imad_peak / 1e12,
+                      "hbm_gbs": hbm_peak},
             "stage_ms_one_call": stage_ms,
             "level_setup_s": level_s,
             "clocks": clocks.summary(),

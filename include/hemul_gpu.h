@@ -144,6 +144,10 @@ hemul_status hemul_gpu_reset_stats(hemul_gpu_ctx *ctx);
 /* Integer-pipe roofline denominator: measured IMAD.WIDE.U32 ops/s of the
  * context's device (a short probe kernel). */
 hemul_status hemul_gpu_imad_peak(hemul_gpu_ctx *ctx, double *ops_per_s);
+/* Tensor-core roofline denominator: measured dense int8 ops/s (2 per u8 x u8
+ * MAC) of tcgen05.mma kind::i8 on the context's device, the engine of the
+ * 30-bit basis' CRT / iCRT / finisher GEMMs (HEMUL_OPT_TENSOR_CORES). */
+hemul_status hemul_gpu_tc_peak(hemul_gpu_ctx *ctx, double *ops_per_s);
 
 /* Region tables of level log_q: region 1 (products mod q) or 2 (key
  * switching) in the reference's w64 basis, as the stage entry points use

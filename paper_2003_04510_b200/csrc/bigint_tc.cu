@@ -52,11 +52,13 @@ constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
 constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
 constexpr int kSlots = kChunk / 4;   // row slots (4-byte residues) per chunk
 constexpr int kEpiWarps = 4;
-constexpr int kTmaWarp = 4, kMmaWarp = 5, kProd0 = 6, kProdWarps = 4;
-constexpr int kThreads = 32 * (kProd0 + kProdWarps);
-constexpr int kSA = 8;               // A (byte plane) stages
-constexpr int kSB = 4;               // B (table) stages
-constexpr int kSR = 6;               // raw t stages (producer-private cp.async ring)
+constexpr int kTmaWarp = 4, kMmaWarp = 5, kProd0 = 6, kProdWarps = 8;
+constexpr int kRawWarp = kProd0 + kProdWarps;  // TMA of the t rows
+constexpr int kProdRows = kSlots / kProdWarps;  // row slots per producer warp and chunk
+constexpr int kThreads = 32 * (kRawWarp + 1);
+constexpr int kSA = 3;               // A (byte plane) stages
+constexpr int kSB = 6;               // B (table) stages
+constexpr int kSR = 6;               // raw t stages (TMA, kRawWarp)
 constexpr int kLag = kSR - 1;        // producer prefetch distance in chunks
 constexpr int kABytes = kChunk * kRows;          // 8 KB
 constexpr int kRawBytes = kSlots * kRows * 4;    // 8 KB
@@ -92,16 +94,18 @@ __device__ __forceinline__ uint32_t a_off(uint32_t kk, uint32_t m) {
   return (kk >> 3) * 1024 + (kk & 7) * 128 + ((((m >> 4) ^ kk) & 7) << 4) + (m & 15);
 }
 
-__device__ __forceinline__ const uint32_t* seg_rows(const BigTcSeg& s, int e, int B, size_t n) {
+// row (in the segment's tensor map) of residue row j of entry e
+__device__ __forceinline__ int seg_row(const BigTcSeg& s, int e, int B, int j) {
   const int b = e % B, hi = e / B;
-  return s.base + size_t(b) * s.estride + (hi ? s.half_off : 0);
+  return s.row0 + b * s.erows + (hi ? s.half_rows : 0) + j;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    bigint_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params P) {
+    bigint_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap rmap0,
+                     const __grid_constant__ CUtensorMap rmap1, Params P) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t a_full[kSA], a_empty[kSA], b_full[kSB], b_empty[kSB];
-  __shared__ __align__(8) uint64_t t_full, t_empty;
+  __shared__ __align__(8) uint64_t t_full[2], blk_free[3], r_full[kSR], r_empty[kSR];
   __shared__ uint32_t tmem_base;
   // 1024-byte aligned by pointer arithmetic on the shared array (an integer
   // round trip would lose the state space: generic LD/ST instead of LDS/STS)
@@ -130,8 +134,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&b_full[s], 1);
       tc::mbar_init(&b_empty[s], 1);
     }
-    tc::mbar_init(&t_full, 1);
-    tc::mbar_init(&t_empty, kEpiWarps * 32);
+    for (int s = 0; s < kSR; ++s) {
+      tc::mbar_init(&r_full[s], 1);
+      tc::mbar_init(&r_empty[s], kProdWarps);
+    }
+    for (int a = 0; a < 2; ++a) tc::mbar_init(&t_full[a], 1);
+    for (int b = 0; b < 3; ++b) tc::mbar_init(&blk_free[b], kEpiWarps * 32);
     tc::mbar_fence_init();
   }
   // floor(2^55 / p) of every A row (the fixed-point k quotient)
@@ -145,9 +153,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
+  // TMEM: the accumulator is two column blocks of NH (low / high columns).
+  // With 3 NH <= 512 the blocks rotate through three slots, tile t using
+  // slots (2t mod 3, 2t+1 mod 3): the MMAs of tile t+1 need only the low
+  // block of tile t, which the epilogue releases half way through.
+  const int nslots = 3 * NH <= 512 ? 3 : 2;
+  auto slot_lo = [&](int t) { return nslots == 3 ? (2 * t) % 3 : 0; };
+  auto slot_hi = [&](int t) { return nslots == 3 ? (2 * t + 1) % 3 : 1; };
 
   if (warp == kTmaWarp) {
-    // ---- B chunks by TMA -------------------------------------------------
+    // ---- TMA: B chunks (table) -------------------------------------------
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       for (int q = 0, c = 0; q < total; ++q) {
@@ -160,12 +175,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++c == C) c = 0;
       }
     }
+  } else if (warp == kRawWarp) {
+    // ---- TMA: the t rows of each chunk (kSR stages ahead of the producers)
+    if (lane == 0) {
+      for (int tl = 0, qr = 0; tl < my_tiles; ++tl) {
+        const int tile = blockIdx.x + tl * gridDim.x;
+        const int e = tile / tiles_per_entry;
+        const int i0 = (tile - e * tiles_per_entry) * kRows;
+        for (int c = 0; c < C - 1; ++c, ++qr) {
+          // rows 16 c .. 16 c + 15 of one segment (segments start on chunks;
+          // rows past the segment read neighbours or zero-filled OOB, unused)
+          const int g0 = kSlots * c;
+          const int sg = (g0 >= P.seg[1].slot0) + (g0 >= P.seg[2].slot0);
+          const BigTcSeg& S = P.seg[sg];
+          const int r = qr % kSR;
+          tc::mbar_wait(&r_empty[r], ((qr / kSR) & 1) ^ 1);
+          mbar_expect_tx(&r_full[r], kRawBytes);
+          tma_load_2d(tc::smem_addr(sR + r * kRawBytes), S.map ? &rmap1 : &rmap0, i0,
+                      seg_row(S, e, P.B, g0 - S.slot0), &r_full[r]);
+        }
+      }
+    }
   } else if (warp == kMmaWarp) {
     // ---- MMA issue -------------------------------------------------------
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_u8(kRows, NH, 1, 0);
+      int uses[3] = {0, 0, 0};
+      uint32_t dlo = 0, dhi = 0;
       for (int q = 0, c = 0, it = 0; q < total; ++q) {
-        if (c == 0) tc::mbar_wait(&t_empty, (it & 1) ^ 1);
+        if (c == 0) {  // a new tile: its two TMEM blocks must be drained
+          const int bl = slot_lo(it), bh = slot_hi(it);
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            if ((b == bl || b == bh) && uses[b]++ > 0)
+              tc::mbar_wait(&blk_free[b], (uses[b] - 2) & 1);
+          dlo = tmem + bl * NH;
+          dhi = tmem + bh * NH;
+        }
         tc::mbar_wait(&b_full[q % kSB], (q / kSB) & 1);
         tc::mbar_wait(&a_full[q % kSA], (q / kSA) & 1);
         tc::fence_async_smem();
@@ -176,14 +222,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ks = 0; ks < 2; ++ks) {
           const uint64_t ad = tc::smem_desc(a0 + ks * 4096, 8192, 1024, tc::kSw128);
           const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
-          tc::mma_u8(tmem, ad, tc::smem_desc(b0 + ks * 32, 16, 512, tc::kSw64), idesc, acc);
-          tc::mma_u8(tmem + NH, ad, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
+          tc::mma_u8(dlo, ad, tc::smem_desc(b0 + ks * 32, 16, 512, tc::kSw64), idesc, acc);
+          tc::mma_u8(dhi, ad, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
                      idesc, acc);
         }
         tc::mma_commit(&b_empty[q % kSB]);
         tc::mma_commit(&a_empty[q % kSA]);
         if (++c == C) {
-          tc::mma_commit(&t_full);
+          tc::mma_commit(&t_full[it & 1]);
           c = 0;
           ++it;
         }
@@ -192,8 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= kProd0) {
     // ---- producers ---------------------------------------------------------
     const int pw = warp - kProd0;
-    const int slot_lo = 4 * pw;  // this warp's 4 row slots of every chunk
-    const int pt = threadIdx.x - 32 * kProd0;  // 0..127
+    const int slot_lo = kProdRows * pw;  // this warp's row slots of every chunk
+    const int pt = threadIdx.x - 32 * kProd0;  // 0 .. 32 kProdWarps - 1
     // fixed point sum_j t_j / p_j 2^23 of the 4 coefficients per segment:
     // umulhi(t_j, floor(2^55 / p_j)) per row (each term < 2^23, low by < 1;
     // <= 511 rows per segment keep the sum below 2^32)
@@ -202,59 +248,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kMaxSeg; ++s)
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) F[s][c4] = 0;
-    // raw t of the next chunk to issue: row slots slot_lo..+3, coefficients
-    // 4 lane..+3. Segments start on chunk boundaries (build_bigint), so a
-    // chunk reads 4 consecutive rows of one segment; chunks are issued in
-    // sequence and the tile's segment row pointers are updated incrementally.
     const int sl1 = P.seg[1].slot0, sl2 = P.seg[2].slot0;
     const int np0 = P.seg[0].np, np1 = P.seg[1].np, np2 = P.seg[2].np;
-    int is_q = 0, is_c = 0, is_tl = 0;
-    const uint32_t *rb0 = nullptr, *rb1 = nullptr, *rb2 = nullptr;
-    auto set_tile = [&](int tl) {
-      const int tile = blockIdx.x + tl * gridDim.x;
-      const int e = tile / tiles_per_entry;
-      const size_t off = size_t(tile - e * tiles_per_entry) * kRows + 4 * lane;
-      rb0 = seg_rows(P.seg[0], e, P.B, n) + off;
-      rb1 = P.nseg > 1 ? seg_rows(P.seg[1], e, P.B, n) + off : rb0;
-      rb2 = P.nseg > 2 ? seg_rows(P.seg[2], e, P.B, n) + off : rb0;
-    };
-    if (total > 0) set_tile(0);
-    auto issue = [&]() {
-      if (is_q < total && is_c != C - 1) {
-        const int g0 = kSlots * is_c + slot_lo;  // first of my 4 row slots
-        const int s = (g0 >= sl1) + (g0 >= sl2);
-        const int j0 = g0 - (s == 2 ? sl2 : s == 1 ? sl1 : 0);
-        const int npn = s == 2 ? np2 : s == 1 ? np1 : np0;
-        const uint32_t* src = (s == 2 ? rb2 : s == 1 ? rb1 : rb0) + size_t(j0) * n;
-        const uint32_t dst0 =
-            tc::smem_addr(sR + (is_q % kSR) * kRawBytes + slot_lo * kRows * 4 + 16 * lane);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (j0 + i < npn) tc::cp_async16z(dst0 + i * kRows * 4, src + size_t(i) * n, 16);
-      }
-      cp_async_commit();
-      ++is_q;
-      if (++is_c == C) {
-        is_c = 0;
-        if (++is_tl < my_tiles) set_tile(is_tl);
-      }
-    };
-    for (int q = 0; q < kLag; ++q) issue();
-    for (int q = 0, c = 0; q < total; ++q) {
-      issue();
-      cp_async_wait<kLag>();  // this thread's copies of chunk q have landed
+    for (int q = 0, c = 0, qr = 0; q < total; ++q) {
       const int sa = q % kSA;
       tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
       uint8_t* A = sA + sa * kABytes;
       if (c != C - 1) {
-        const uint8_t* R = sR + (q % kSR) * kRawBytes + slot_lo * kRows * 4 + 16 * lane;
+        const int r = qr % kSR;
+        tc::mbar_wait_sleep<32>(&r_full[r], (qr / kSR) & 1);
+        const uint8_t* R = sR + r * kRawBytes + slot_lo * kRows * 4 + 16 * lane;
         const int g0 = kSlots * c + slot_lo;
         const int s = (g0 >= sl1) + (g0 >= sl2);  // one segment per chunk (warp-uniform)
         const int j0 = g0 - (s == 2 ? sl2 : s == 1 ? sl1 : 0);
         const int npn = s == 2 ? np2 : s == 1 ? np1 : np0;
         uint32_t f[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < kProdRows; ++i) {
           if (j0 + i < npn) {  // warp-uniform (padding rows have zero B rows)
             // t_j of 4 coefficients (the inverse NTT folded (P/p_j)^-1 in)
             const uint4 x = *reinterpret_cast<const uint4*>(R + i * kRows * 4);
@@ -274,6 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<uint32_t*>(A + a_off(kk + 3, 4 * lane)) = __byte_perm(hi01, hi23, 0x7632);
           }
         }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&r_empty[r]);  // this warp's rows are read
+        ++qr;
 #pragma unroll
         for (int ss = 0; ss < kMaxSeg; ++ss)
           if (ss == s)
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             F[s][c4] = 0;
           }
         producer_sync();
-        for (int s = 0; s < P.nseg; ++s) {
+        for (int s = 0; s < P.nseg && pt < kRows; ++s) {
           uint32_t tot = 0;
 #pragma unroll
           for (int w = 0; w < kProdWarps; ++w) tot += xbuf[(w * kMaxSeg + s) * kRows + pt];
@@ -297,14 +310,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           A[a_off(2 * s, pt)] = static_cast<uint8_t>(k);
           A[a_off(2 * s + 1, pt)] = static_cast<uint8_t>(k >> 8);
         }
-        A[a_off(6, pt)] = 1;  // constant row: the window's rounding constants
+        if (pt < kRows) A[a_off(6, pt)] = 1;  // constant row: the window's rounding constants
         producer_sync();
       }
       tc::fence_async_smem();
       tc::mbar_arrive(&a_full[sa]);
       if (++c == C) c = 0;
     }
-    cp_async_wait<0>();
   } else {
     // ---- epilogue: lane = coefficient i0 + 32 warp + lane -----------------------
     // Column sums -> 32-bit digits d_h = (sum_{c<4} D[4h+c] 2^(8c) + carry) mod
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int S = B0 & 31, q = B0 >> 5;
     const int L = o.out_limbs, nl = L - kst;
     const uint64_t top = o.out_bits % 64 ? (uint64_t(1) << (o.out_bits % 64)) - 1 : ~0ull;
-    const uint32_t taddr0 = tmem + (uint32_t(32 * warp) << 16);
+    const uint32_t lane_base = tmem + (uint32_t(32 * warp) << 16);
     auto digit = [&](const uint32_t* v, int h, uint64_t& carry) -> uint32_t {
       uint64_t z = carry;
       if (h < H) {  // warp-uniform
@@ -338,15 +350,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const size_t i = size_t(tile - e * tiles_per_entry) * kRows + 32 * warp + lane;
       const int eb = e % P.B;
       uint64_t* dst = (e < P.B ? o.out0 : o.out1) + (size_t(eb) * n + i) * L;
-      tc::mbar_wait_sleep<128>(&t_full, it & 1);
+      tc::mbar_wait_sleep<128>(&t_full[it & 1], (it >> 1) & 1);
       tc::fence_after();
+      const int bl = slot_lo(it), bh = slot_hi(it);
+      const uint32_t alo = lane_base + bl * NH, ahi = lane_base + bh * NH - NH;
+      bool lo_held = true;
+      // 16 columns from col (multiple of 4); the low block is handed back to
+      // the MMA as soon as every column below NH has been read
+      auto load16 = [&](int col, uint32_t (&v)[16]) {
+        if (col + 16 <= NH) {
+          tc::tmem_ld16(alo + col, v);
+        } else if (col >= NH) {
+          tc::tmem_ld16(ahi + col, v);
+        } else {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            const int cc = col + 4 * d;
+            tc::tmem_ld4((cc < NH ? alo : ahi) + cc, *reinterpret_cast<uint32_t(*)[4]>(v + 4 * d));
+          }
+        }
+        tc::tmem_wait_ld();
+        if (lo_held && col + 16 >= NH) {
+          tc::fence_before();
+          tc::mbar_arrive(&blk_free[bl]);
+          lo_held = false;
+        }
+      };
       uint64_t carry = 0;
       uint32_t dprev = 0;
       // digits 0 .. q: carry only
       for (int h0 = 0; h0 <= q; h0 += 4) {
         uint32_t v[16];
-        tc::tmem_ld16(taddr0 + 4 * h0, v);
-        tc::tmem_wait_ld();
+        load16(4 * h0, v);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           if (h0 + c <= q) dprev = digit(v + 4 * c, h0 + c, carry);
@@ -355,10 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nl; j += 2) {
         const int h = q + 1 + 2 * j;  // digits h .. h + 3 -> limbs j, j + 1
         uint32_t v[16];
-        if (4 * h < N) {
-          tc::tmem_ld16(taddr0 + 4 * h, v);
-          tc::tmem_wait_ld();
-        }
+        if (4 * h < N) load16(4 * h, v);
         const uint32_t d0 = digit(v, h, carry), d1 = digit(v + 4, h + 1, carry);
         const uint32_t d2 = digit(v + 8, h + 2, carry), d3 = digit(v + 12, h + 3, carry);
         const uint64_t l0 = __funnelshift_r(dprev, d0, S) |
@@ -380,7 +412,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!skip && k0 + 1 < L) dst[k0 + 1] = k0 + 1 == L - 1 ? l1 & top : l1;
       }
       tc::fence_before();
-      tc::mbar_arrive(&t_empty);
+      if (lo_held) tc::mbar_arrive(&blk_free[bl]);
+      tc::mbar_arrive(&blk_free[bh]);
     }
   }
   tc::fence_before();
@@ -403,9 +436,9 @@ cudaError_t bigint_tc_setup_attributes() {
 }
 
 cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, int B, int log_n,
-                      const BigTcOut& o, cudaStream_t st) {
+                      const BigTcOut& o, const void* const* rmaps, cudaStream_t st) {
   const size_t n = size_t(1) << log_n;
-  if (!t.tmap || t.nseg < 1 || t.nseg > kMaxSeg || n < size_t(kRows) || t.n_cols % 32 ||
+  if (!t.tmap || !rmaps || !rmaps[0] || !rmaps[1] || t.nseg < 1 || t.nseg > kMaxSeg || n < size_t(kRows) || t.n_cols % 32 ||
       t.n_cols > 480 || t.k_bytes % kChunk || bigint_tc_smem(t.n_cols) > size_t(kMaxDynSmem))
     return cudaErrorInvalidValue;
   if ((o.check_amb || o.force_exact) && !o.flags.count) return cudaErrorInvalidValue;
@@ -447,7 +480,8 @@ cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, in
     if (e != cudaSuccess) return e;
   }
   bigint_tc_kernel<<<grid, kThreads, bigint_tc_smem(t.n_cols), st>>>(
-      *static_cast<const CUtensorMap*>(t.tmap), P);
+      *static_cast<const CUtensorMap*>(t.tmap), *static_cast<const CUtensorMap*>(rmaps[0]),
+      *static_cast<const CUtensorMap*>(rmaps[1]), P);
   return cudaGetLastError();
 }
 

@@ -327,8 +327,7 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
 // 2-D TMA map of a u8 table [rows][inner] with boxes of box_inner x box_rows
 // and 64-byte swizzle (bigint_tc.cu's B operand). The driver entry point is
 // resolved through the runtime (no libcuda link).
-void make_tmap_u8(CUtensorMap* m, const void* g, uint64_t inner, uint64_t rows, uint32_t box_inner,
-                  uint32_t box_rows) {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -339,6 +338,12 @@ void make_tmap_u8(CUtensorMap* m, const void* g, uint64_t inner, uint64_t rows, 
       throw CudaFail(HEMUL_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return encode;
+}
+
+void make_tmap_u8(CUtensorMap* m, const void* g, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                  uint32_t box_rows) {
+  const auto encode = tmap_encoder();
   const cuuint64_t dims[2] = {inner, rows};
   const cuuint64_t strides[1] = {inner};
   const cuuint32_t box[2] = {box_inner, box_rows};
@@ -347,6 +352,20 @@ void make_tmap_u8(CUtensorMap* m, const void* g, uint64_t inner, uint64_t rows, 
                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaFail(HEMUL_E_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
+// 2-D TMA map of a u32 residue array [rows][n], boxes of 128 residues x 16
+// rows, no swizzle (bigint_tc.cu's t rows).
+void make_raw_tmap(CUtensorMap* m, const uint32_t* g, uint64_t n, uint64_t rows) {
+  const cuuint64_t dims[2] = {n, rows};
+  const cuuint64_t strides[1] = {n * 4};
+  const cuuint32_t box[2] = {128, 16};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = tmap_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(g),
+                                    dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaFail(HEMUL_E_CUDA, "cuTensorMapEncodeTiled (t rows) failed");
 }
 
 std::unique_ptr<BigTcDev> upload_bigint(const BigTcHost& h, cudaStream_t st) {
@@ -768,6 +787,14 @@ hemul_status hemul_gpu_imad_peak(hemul_gpu_ctx* c, double* ops_per_s) {
   });
 }
 
+hemul_status hemul_gpu_tc_peak(hemul_gpu_ctx* c, double* ops_per_s) {
+  if (!c || !ops_per_s) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    check(tc_peak(ops_per_s, c->stream), "tensor-core probe");
+    return HEMUL_OK;
+  });
+}
+
 uint64_t hemul_gpu_launch_count(const hemul_gpu_ctx* c) { return c ? c->launches : 0; }
 
 hemul_status hemul_gpu_synchronize(hemul_gpu_ctx* c) {
@@ -938,10 +965,14 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   if constexpr (kSplit) {
     if (tc_big) {
       const BigTcDev& T = *bs.icrt_tc;
+      // t rows: R1 = 8 slots of B x np1 rows; d2 = (slot 0, slot 1)
+      alignas(64) CUtensorMap rmap;
+      make_raw_tmap(&rmap, R1, n, uint64_t(kInSlots) * B * r1.np);
+      const void* rmaps[2] = {&rmap, &rmap};
       BigTcSeg segs[2];
       for (int h2 = 0; h2 < 2; ++h2) {
-        segs[h2].base = R1 + h2 * r1w;
-        segs[h2].estride = static_cast<long long>(r1.np) * n;
+        segs[h2].row0 = h2 * static_cast<int>(B) * r1.np;
+        segs[h2].erows = r1.np;
         segs[h2].primes = p1;
       }
       BigTcOut o;
@@ -950,7 +981,8 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       o.out_bit = T.out_bit;
       o.out_bits = T.out_bits;
       run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1 (tensor cores)", [&] {
-        return bigint_tc(T.t, segs, static_cast<int>(B), static_cast<int>(B), log_n, o, c->stream);
+        return bigint_tc(T.t, segs, static_cast<int>(B), static_cast<int>(B), log_n, o, rmaps,
+                         c->stream);
       });
       icrt_done = true;
     }
@@ -1011,15 +1043,23 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   if constexpr (kSplit) {
     if (tc_big) {
       const BigTcDev& T = *bs.fin_tc;
+      // t rows: map 0 = KA|KB (2B x np2 rows: entries e < B ks_a, e >= B
+      // ks_b), map 1 = R1 slots (d1 = slots 4, 5 for ax; d0 = slots 2, 3 for bx)
+      alignas(64) CUtensorMap rmap2, rmap1;
+      make_raw_tmap(&rmap2, KA, n, 2 * uint64_t(B) * r2.np);
+      make_raw_tmap(&rmap1, R1, n, uint64_t(kInSlots) * B * r1.np);
+      const void* rmaps[2] = {&rmap2, &rmap1};
+      const int Bi = static_cast<int>(B);
       BigTcSeg segs[3];
-      segs[0].base = KA;  // entries e < B: ks_a (KA), e >= B: ks_b (KB = KA + B np2 n)
-      segs[0].estride = static_cast<long long>(r2.np) * n;
-      segs[0].half_off = static_cast<long long>(r2w);
+      segs[0].map = 0;
+      segs[0].erows = r2.np;
+      segs[0].half_rows = Bi * r2.np;
       segs[0].primes = p2;
-      for (int h2 = 0; h2 < 2; ++h2) {  // d1 (ax) / d0 (bx), c0 then c1 = c0 + r1w
-        segs[1 + h2].base = D1 + h2 * r1w;
-        segs[1 + h2].estride = static_cast<long long>(r1.np) * n;
-        segs[1 + h2].half_off = static_cast<long long>(D0 - D1);
+      for (int h2 = 0; h2 < 2; ++h2) {  // c0 then c1 (the next slot)
+        segs[1 + h2].map = 1;
+        segs[1 + h2].row0 = (4 + h2) * Bi * r1.np;
+        segs[1 + h2].erows = r1.np;
+        segs[1 + h2].half_rows = -2 * Bi * r1.np;
         segs[1 + h2].primes = p1;
       }
       BigTcOut o;
@@ -1033,7 +1073,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       o.flags = flags;
       run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher (tensor cores)", [&] {
         cudaError_t e = bigint_tc(T.t, segs, static_cast<int>(2 * B), static_cast<int>(B), log_n, o,
-                                  c->stream);
+                                  rmaps, c->stream);
         if (e != cudaSuccess) return e;
         Finisher ft = fin;
         ft.t_inputs = 1;

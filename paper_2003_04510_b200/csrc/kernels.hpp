@@ -59,6 +59,8 @@ cudaError_t ntt_mid_evk(typename F::W* Fin, const typename F::W* ea, const typen
 // Measured IMAD.WIDE.U32 throughput of this device in ops/s (a dependent-free
 // stream of mad.wide.u32, 148 x 8 CTAs), and the SM clock it ran at (kHz).
 cudaError_t imad_peak(double* ops_per_s, cudaStream_t st);
+// Dense int8 tensor-core ops/s (2 per u8 MAC) of tcgen05.mma kind::i8 on this device.
+cudaError_t tc_peak(double* ops_per_s, cudaStream_t st);
 
 // ---- CRT (crt.cu) ----------------------------------------------------------
 // Weight table for one (prime set, input width), m < chunks = ceil(in_bits /
@@ -187,11 +189,12 @@ cudaError_t finish_keyswitch(const typename F::W* ks, const typename F::W* d_ax,
                              cudaStream_t st);
 
 // ---- iCRT / key-switch finisher on the int8 tensor cores (bigint_tc.cu) -----
-// One RNS operand feeding the GEMM's A rows: entry e (< entries) reads
-// rows j < np at base + (e % B) * estride + (e >= B ? half_off : 0) + j * n.
+// One RNS operand feeding the GEMM's A rows (t_j residues, prime-major rows
+// of n): entry e (< entries) reads rows row0 + (e % B) erows + (e >= B ?
+// half_rows : 0) + j (j < np) of raw tensor map `map` (bigint_tc's rmaps).
 struct BigTcSeg {
-  const uint32_t* base = nullptr;
-  long long estride = 0, half_off = 0;
+  int map = 0;
+  int row0 = 0, erows = 0, half_rows = 0;
   const DevPrime32* primes = nullptr;  // pad[0] = floor(2^55 / p) (the k quotient)
   int np = 0;
   int slot0 = 0;  // set from the table
@@ -224,8 +227,10 @@ struct BigTcOut {
 };
 cudaError_t bigint_tc_setup_attributes();
 size_t bigint_tc_smem(int n_cols);
+// rmaps[2]: host pointers to CUtensorMaps of u32 residue arrays [rows][n]
+// (box 128 x 16, no swizzle; make_raw_tmap).
 cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, int B, int log_n,
-                      const BigTcOut& o, cudaStream_t st);
+                      const BigTcOut& o, const void* const* rmaps, cudaStream_t st);
 // Exact fix-up of flagged finisher coefficients (icrt.cu finish_fixup_kernel).
 template <class F>
 cudaError_t finish_fixup(const typename F::W* ks, const typename F::W* d_ax,

@@ -89,6 +89,7 @@ _SIGS = {
                                               ctypes.POINTER(ctypes.c_uint64)]),
     "hemul_gpu_reset_stats": (ctypes.c_int, [ctypes.c_void_p]),
     "hemul_gpu_imad_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    "hemul_gpu_tc_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "hemul_gpu_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
 }
 HEMUL_OPT_FORCE_EXACT = 1
@@ -361,6 +362,12 @@ class Context:
         """Measured IMAD.WIDE.U32 ops/s of this device."""
         v = ctypes.c_double()
         self._check(self._lib.hemul_gpu_imad_peak(self._h, ctypes.byref(v)))
+        return v.value
+
+    def tc_peak(self) -> float:
+        """Measured dense int8 tensor-core ops/s (tcgen05.mma kind::i8) of this device."""
+        v = ctypes.c_double()
+        self._check(self._lib.hemul_gpu_tc_peak(self._h, ctypes.byref(v)))
         return v.value
 
     def launch_count(self) -> int:

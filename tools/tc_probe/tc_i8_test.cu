@@ -176,6 +176,55 @@ __global__ void mma_rate(int iters, int32_t* sink) {
   if (threadIdx.x < 32) tc::tmem_dealloc<512>(tbase);
 }
 
+// throughput of one layout / shape: a_mn (A MN-major SW128, M=128), b_sw
+// (B K-major swizzle 128 or 64), N per MMA, two MMAs per k-step (N each)
+__global__ void mma_rate2(int iters, int a_mn, int b_sw, int N, int32_t* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < 64 * 1024; i += blockDim.x) smem[i] = uint8_t(i * 7);
+  tc::fence_async_smem();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = tmem_base;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = tc::smem_addr(smem), b0 = a0 + 16384;
+    const uint32_t idesc = tc::idesc_u8(128, N, a_mn, 0);
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const uint64_t ad = a_mn ? tc::smem_desc(a0 + s * 4096, 8192, 1024, tc::kSw128)
+                                 : tc::kmaj_sw128_desc(a0, s, 128);
+        const uint64_t bd0 = b_sw == 64 ? tc::smem_desc(b0 + s * 32, 16, 512, tc::kSw64)
+                                        : tc::kmaj_sw128_desc(b0, s, N);
+        const uint64_t bd1 = b_sw == 64 ? tc::smem_desc(b0 + N * 64 + s * 32, 16, 512, tc::kSw64)
+                                        : tc::kmaj_sw128_desc(b0 + N * 128, s, N);
+        tc::mma_u8(tbase, ad, bd0, idesc, 1);
+        tc::mma_u8(tbase + N, ad, bd1, idesc, 1);
+      }
+    tc::mma_commit(&bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after();
+  if (threadIdx.x < 32) {
+    uint32_t r[4];
+    tc::tmem_ld4(tbase, r);
+    tc::tmem_wait_ld();
+    if (threadIdx.x == 0) sink[blockIdx.x] = r[0];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc<512>(tbase);
+}
+
 int main(int argc, char** argv) {
   const char* names[] = {"A,B K-major SW128", "A,B K-major interleave", "A,B K-major interleave (LBO/SBO swapped)",
                          "A MN-major SW128 / B K SW128", "A MN-major SW128 (LBO/SBO swapped) / B K SW128",
@@ -200,6 +249,22 @@ int main(int argc, char** argv) {
   cudaEventElapsedTime(&ms, e0, e1);
   const double ops = 2.0 * sms * iters * 4 * 128.0 * 256 * 32;
   printf("int8 MMA rate: %.1f TOPS dense (%d SMs, %.3f ms)\n", ops / (ms * 1e-3) / 1e12, sms, ms);
+  CK(cudaFuncSetAttribute(mma_rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  const int cfgs[][3] = {{0, 128, 256}, {1, 128, 256}, {0, 128, 160}, {1, 128, 160},
+                         {0, 64, 160}, {1, 64, 160}, {1, 64, 128}, {1, 64, 240}};
+  for (const auto& cf : cfgs) {
+    mma_rate2<<<sms, 128, 100 * 1024>>>(16, cf[0], cf[1], cf[2], sink);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    mma_rate2<<<sms, 128, 100 * 1024>>>(4096, cf[0], cf[1], cf[2], sink);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms2 = 0;
+    cudaEventElapsedTime(&ms2, e0, e1);
+    const double ops2 = 2.0 * sms * 4096 * 4 * 128.0 * cf[2] * 32;
+    printf("rate A %s, B K-major SW%d, N=%d x2: %.1f TOPS\n", cf[0] ? "MN-major" : "K-major", cf[1],
+           cf[2], ops2 / (ms2 * 1e-3) / 1e12);
+  }
   const int Ns[] = {256, 176, 80, 16};
   const int Ks[] = {32, 160, 320};
   srand(12345);
