@@ -32,6 +32,8 @@ METRICS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_pct",
 }
 
 # ncu reports these in scaled units; normalise to bytes / milliseconds
@@ -47,8 +49,10 @@ def read(rep: Path) -> dict:
     hdr, units, vals = rows[0], rows[1], rows[2]
     res = {"kernel": vals[hdr.index("Kernel Name")]}
     for m, key in METRICS.items():
-        if m in hdr:
-            i = hdr.index(m)
+        # some sections prefix their metrics (e.g. "TPC.TriageCompute.")
+        idx = [i for i, h in enumerate(hdr) if h == m or h.endswith("." + m)]
+        if idx:
+            i = idx[0]
             v = float(vals[i].replace(",", ""))
             res[key] = v * UNIT.get(units[i], 1.0)
     return res
@@ -63,9 +67,9 @@ def main() -> None:
     ap.add_argument("--title", default="ncu --set full, one launch per kernel")
     args = ap.parse_args()
     lines = [f"# {args.title}", "",
-             "| class | kernel | ms | DRAM read MB | DRAM write MB | FMA-heavy % | ALU % | LSU % | issue % "
-             "| occupancy % | smem conflicts / wavefronts | regs | grid x block |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "| class | kernel | ms | DRAM read MB | DRAM write MB | tensor % | L2 % | FMA-heavy % | ALU % "
+             "| LSU % | issue % | occupancy % | smem conflicts / wavefronts | regs | grid x block |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = json.loads(args.traffic.read_text()) if args.traffic and args.traffic.exists() else {}
     for rep in args.reports:
         r = read(rep)
@@ -73,7 +77,8 @@ def main() -> None:
         key = rep.stem.split("prof_", 1)[-1]  # report named prof_<bench kernel class>.ncu-rep
         lines.append(
             f"| {key} | `{name}` | {r.get('duration', 0):.3f} | {r.get('dram_read', 0) / 1e6:.1f} | "
-            f"{r.get('dram_write', 0) / 1e6:.1f} | {r.get('fmaheavy_pct', 0):.1f} | "
+            f"{r.get('dram_write', 0) / 1e6:.1f} | {r.get('tensor_pct', 0):.1f} | "
+            f"{r.get('l2_pct', 0):.1f} | {r.get('fmaheavy_pct', 0):.1f} | "
             f"{r.get('alu_pct', 0):.1f} | {r.get('lsu_pct', 0):.1f} | {r.get('issue_pct', 0):.1f} | "
             f"{r.get('occupancy_pct', 0):.1f} | {r.get('smem_conflicts', 0):.3g} / "
             f"{r.get('smem_wavefronts', 0):.3g} | {int(r.get('regs', 0))} | "
