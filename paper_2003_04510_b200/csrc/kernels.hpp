@@ -32,6 +32,13 @@ cudaError_t ntt_inverse_pass(int pass, typename F::W* data, size_t rows, int np,
                              const typename F::Tw* itw, const typename F::Prime* primes,
                              cudaStream_t st);
 
+// 30-bit basis pass A (strided levels [0, S), ntt_col.cu): one warp per
+// column, shuffles for the lane levels; used by ntt_forward_pass /
+// ntt_inverse_pass when supported (S = 6..9, >= 16 columns).
+bool ntt_col_supported(int log_n, int S);
+cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
+                         const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st);
+
 // Fused middle pass (two-pass sizes, logN 12..17): forward levels
 // [s1, logN) of every operand + the evaluation-domain product + inverse
 // levels [s1, logN) of the products, one read and one write per block.

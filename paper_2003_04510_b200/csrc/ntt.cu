@@ -500,6 +500,12 @@ template <class F>
 cudaError_t launch_pass(bool inv, typename F::W* data, const typename F::Tw* tw,
                         const typename F::Prime* primes, int np, size_t rows, int log_n, int st0,
                         int S, bool strided, bool last, cudaStream_t st) {
+  if constexpr (sizeof(typename F::W) == 4) {
+    // 30-bit basis pass A (forward first pass / inverse last pass): the
+    // warp-per-column kernel (ntt_col.cu)
+    if (strided && st0 == 0 && log_n >= 12 && last == inv && ntt_col_supported(log_n, S))
+      return ntt_col_pass(inv, data, rows, np, log_n, S, tw, primes, st);
+  }
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
   const PassArgs<F> a{data, tw, primes, np, log_n, st0, rpp, last ? 1 : 0};
   const int lp = pass_lp<F>(log_n);

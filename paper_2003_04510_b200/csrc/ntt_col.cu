@@ -1,0 +1,284 @@
+// Strided NTT pass A (levels [0, S) on 2^S-point columns) for the 30-bit
+// basis, one warp per column (sm_100a).
+//
+// Reference: ntt_forward / ntt_inverse (proj/core/src/ntt.cpp:59-137,
+// 153-197); pass structure as in ntt.cu (pass A = the first forward levels /
+// the last inverse levels, n^-1 folded into inverse level 0). Values stay in
+// the same lazy ranges as F32::ct / F32::gs (fields.cuh), so the outputs are
+// identical to ntt.cu's pass A.
+//
+// Layout. A CTA loads 16 adjacent columns (16 consecutive residues of every
+// one of the 2^S rows: coalesced 64-byte segments) into shared memory, column
+// x at x * CS + f(y), f(y) = y + y / 32, CS = 2 (mod 32): the cooperative
+// load / store, and both register layouts below, are bank-conflict free. Each
+// warp then transforms its column alone (only __syncwarp), with EPT = 2^S / 32
+// residues per lane:
+//   layout H: lane l holds y = l + 32 r (r < EPT): the top R = log2(EPT) bits
+//             of y live in registers -> levels 0 .. R-1 in registers, their
+//             twiddles uniform across the warp (broadcast reads);
+//   layout L: lane l holds y = EPT l + r: the low R bits in registers ->
+//             levels S-R .. S-1 in registers;
+//   levels R .. S-R-1 pair lanes: one __shfl_xor per residue and level.
+// The forward pass runs H, shuffles, L; the inverse the mirror image.
+// Compared with the radix-8 CTA-wide kernel this drops the 3 CTA barriers
+// and most index arithmetic: every shared address is a per-thread base plus
+// a compile-time offset. 256-thread CTAs (each warp takes two of the 16
+// columns in turn), 5 per SM: the pass is bound by how much HBM traffic is in
+// flight, and more independent CTAs keep more of it going (2 x 512 threads:
+// 2.84 / 3.17 ms per step forward / inverse at X, 5 x 256: 2.30 / 2.49).
+#include <cuda_runtime.h>
+
+#include "fields.cuh"
+#include "kernels.hpp"
+
+namespace hemul_gpu {
+
+namespace {
+
+constexpr int kCols = 16;     // columns per CTA (64-byte row segments)
+constexpr int kWarps = 8;     // each warp transforms kCols / kWarps columns in turn
+constexpr int kThreads = 32 * kWarps;
+
+template <int S>
+struct ColGeo {
+  static constexpr int EPT = (1 << S) / 32;
+  static constexpr int R = S - 5;                 // log2(EPT)
+  static_assert(EPT >= 4, "16-byte cooperative load: >= 4 residues per thread");
+  static constexpr int NSH = S - 2 * R;           // shuffle levels
+  // column stride: >= f(2^S) and = 2 (mod 32)
+  static constexpr int CS = ((1 << S) + (1 << (S - 5)) + 29) / 32 * 32 + 2;
+};
+
+__device__ __forceinline__ int padf(int y) { return y + (y >> 5); }
+
+struct ColArgs {
+  uint32_t* data;
+  const Twiddle32* tw;
+  const DevPrime32* primes;
+  int np, log_n, rows_per_prime;
+};
+
+// Harvey CT / GS butterflies (fields.cuh F32::ct, F32::gs)
+__device__ __forceinline__ void ct(uint32_t& a, uint32_t& b, uint32_t w, uint32_t wq, uint32_t p2,
+                                   uint32_t negp) {
+  const uint32_t u = csub32(a, p2);
+  const uint32_t v = shoup32(b, w, wq, negp);
+  a = u + v;
+  b = u + p2 - v;
+}
+__device__ __forceinline__ void gs(uint32_t& a, uint32_t& b, uint32_t w, uint32_t wq, uint32_t p2,
+                                   uint32_t negp) {
+  const uint32_t u = a, v = b;
+  a = csub32(u + v, p2);
+  b = shoup32(u + p2 - v, w, wq, negp);
+}
+
+template <int S, bool INV>
+__global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
+  using G = ColGeo<S>;
+  constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH, CS = G::CS;
+  extern __shared__ uint32_t smem[];
+  uint32_t* col = smem;                        // [kCols][CS]
+  uint32_t* stw = smem + kCols * CS;           // [2^S] x {w, wq}
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int j, row;
+  if (a.rows_per_prime) {  // prime-major traversal (ntt.cu PassArgs)
+    j = blockIdx.y / a.rows_per_prime;
+    row = (blockIdx.y - j * a.rows_per_prime) * a.np + j;
+  } else {
+    row = blockIdx.y;
+    j = row % a.np;
+  }
+  const DevPrime32& pr = a.primes[j];
+  const uint32_t p = pr.p, p2 = 2 * p, negp = 0u - p;
+  const size_t n = size_t(1) << a.log_n;
+  const int tlast = 1 << (a.log_n - S);
+  uint32_t* rowp = a.data + size_t(row) * n + size_t(blockIdx.x) * kCols;
+  // ---- cooperative load: 16-byte vectors, thread -> (columns 4 (tid % 4)
+  // .. +3, rows tid / 4 + 128 r) ------------------------------------------------
+  {
+    constexpr int RS = kThreads / 4;  // rows per sweep
+    const int x4 = 4 * (tid & 3), y0 = tid >> 2;
+    const uint4* src = reinterpret_cast<const uint4*>(rowp + size_t(y0) * tlast + x4);
+    const size_t step = size_t(RS) * tlast / 4;
+#pragma unroll
+    for (int r = 0; r < (1 << S) / RS; ++r) {
+      const uint4 q = src[r * step];
+      const int fy = padf(y0 + RS * r);
+      col[x4 * CS + fy] = q.x;
+      col[(x4 + 1) * CS + fy] = q.y;
+      col[(x4 + 2) * CS + fy] = q.z;
+      col[(x4 + 3) * CS + fy] = q.w;
+    }
+    const uint32_t* t2 = reinterpret_cast<const uint32_t*>(a.tw + size_t(j) * n);
+    for (int i = tid; i < 2 << S; i += kThreads) stw[i] = t2[i];
+  }
+  __syncthreads();
+  for (int cw = warp; cw < kCols; cw += kWarps) {
+  uint32_t* mc = col + cw * CS;
+  uint32_t v[EPT];
+  auto tw = [&](int idx, uint32_t& w, uint32_t& wq) {
+    w = stw[2 * idx];
+    wq = stw[2 * idx + 1];
+  };
+  if (!INV) {
+    // ---- layout H: y = lane + 32 r; levels 0 .. R-1 ----------------------
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(lane + 32 * r)];
+#pragma unroll
+    for (int L = 0; L < R; ++L) {
+      const int half = EPT >> (L + 1);
+#pragma unroll
+      for (int blk = 0; blk < (1 << L); ++blk) {
+        uint32_t w, wq;
+        tw((1 << L) + blk, w, wq);  // group y >> (S - L) = blk: uniform
+#pragma unroll
+        for (int rr = 0; rr < half; ++rr)
+          ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) mc[padf(lane + 32 * r)] = v[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(EPT * lane + r)];
+    // ---- lane levels R .. S-R-1 (layout L: y = EPT lane + r) -------------
+#pragma unroll
+    for (int L = R; L < R + NSH; ++L) {
+      const int lb = S - 1 - L - R;  // lane bit of the pair
+      const bool upper = (lane >> lb) & 1;
+      uint32_t w, wq;
+      tw((1 << L) + (lane >> (S - L - R)), w, wq);
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lb);
+        const uint32_t top = upper ? o : v[r], bot = upper ? v[r] : o;
+        const uint32_t u = csub32(top, p2);
+        const uint32_t t = shoup32(bot, w, wq, negp);
+        v[r] = upper ? u + p2 - t : u + t;
+      }
+    }
+    // ---- register levels S-R .. S-1 --------------------------------------
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int L = S - R + i, half = EPT >> (i + 1);
+#pragma unroll
+      for (int blk = 0; blk < (1 << i); ++blk) {
+        uint32_t w, wq;
+        tw((1 << L) + (lane << i) + blk, w, wq);
+#pragma unroll
+        for (int rr = 0; rr < half; ++rr)
+          ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) mc[padf(EPT * lane + r)] = v[r];
+  } else {
+    // ---- layout L: levels S-1 .. S-R in registers --------------------------
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(EPT * lane + r)];
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      const int L = S - R + i, half = EPT >> (i + 1);
+#pragma unroll
+      for (int blk = 0; blk < (1 << i); ++blk) {
+        uint32_t w, wq;
+        tw((1 << L) + (lane << i) + blk, w, wq);
+#pragma unroll
+        for (int rr = 0; rr < half; ++rr)
+          gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+      }
+    }
+    // ---- lane levels S-R-1 .. R ------------------------------------------
+#pragma unroll
+    for (int L = R + NSH - 1; L >= R; --L) {
+      const int lb = S - 1 - L - R;
+      const bool upper = (lane >> lb) & 1;
+      uint32_t w, wq;
+      tw((1 << L) + (lane >> (S - L - R)), w, wq);
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lb);
+        const uint32_t top = upper ? o : v[r], bot = upper ? v[r] : o;
+        v[r] = upper ? shoup32(top + p2 - bot, w, wq, negp) : csub32(top + bot, p2);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) mc[padf(EPT * lane + r)] = v[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(lane + 32 * r)];
+    // ---- layout H: levels R-1 .. 1, then level 0 with n^-1 folded ---------
+#pragma unroll
+    for (int L = R - 1; L >= 1; --L) {
+      const int half = EPT >> (L + 1);
+#pragma unroll
+      for (int blk = 0; blk < (1 << L); ++blk) {
+        uint32_t w, wq;
+        tw((1 << L) + blk, w, wq);
+#pragma unroll
+        for (int rr = 0; rr < half; ++rr)
+          gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < EPT / 2; ++rr) {
+      // a' = (u+v) n^-1, b' = (u-v) itw[1] n^-1, canonical (F32::inv_level0)
+      const uint32_t u = v[rr], w2 = v[rr + EPT / 2];
+      v[rr] = csub32(shoup32(u + w2, pr.ninv, pr.ninv_q, negp), p);
+      v[rr + EPT / 2] = csub32(shoup32(u + p2 - w2, pr.w1n, pr.w1n_q, negp), p);
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) mc[padf(lane + 32 * r)] = v[r];
+  }
+  }
+  __syncthreads();
+  // ---- cooperative store ------------------------------------------------
+  {
+    constexpr int RS = kThreads / 4;
+    const int x4 = 4 * (tid & 3), y0 = tid >> 2;
+    uint4* dst = reinterpret_cast<uint4*>(rowp + size_t(y0) * tlast + x4);
+    const size_t step = size_t(RS) * tlast / 4;
+#pragma unroll
+    for (int r = 0; r < (1 << S) / RS; ++r) {
+      const int fy = padf(y0 + RS * r);
+      dst[r * step] = make_uint4(col[x4 * CS + fy], col[(x4 + 1) * CS + fy],
+                                 col[(x4 + 2) * CS + fy], col[(x4 + 3) * CS + fy]);
+    }
+  }
+}
+
+template <int S, bool INV>
+cudaError_t launch_col(const ColArgs& a, size_t rows, cudaStream_t st) {
+  const size_t smem = (size_t(kCols) * ColGeo<S>::CS + (size_t(2) << S)) * 4;
+  const int cols = 1 << (a.log_n - S);
+  dim3 grid(static_cast<unsigned>(cols / kCols), static_cast<unsigned>(rows));
+  ntt_col_kernel<S, INV><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Pass A of the 30-bit basis through the column kernel: forward levels
+// [0, S) (not the last pass) or inverse levels [S-1, 0] with n^-1 (the last
+// pass); S = the pass-A level count of ntt.cu (7..9), n / 2^S >= 16 columns.
+bool ntt_col_supported(int log_n, int S) {
+  return S >= 7 && S <= 9 && log_n - S >= 4;
+}
+
+cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
+                         const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st) {
+  if (!ntt_col_supported(log_n, S)) return cudaErrorInvalidValue;
+  const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
+  const ColArgs a{data, tw, primes, np, log_n, rpp};
+  switch (S * 2 + (inv ? 1 : 0)) {
+    case 14: return launch_col<7, false>(a, rows, st);
+    case 15: return launch_col<7, true>(a, rows, st);
+    case 16: return launch_col<8, false>(a, rows, st);
+    case 17: return launch_col<8, true>(a, rows, st);
+    case 18: return launch_col<9, false>(a, rows, st);
+    default: return launch_col<9, true>(a, rows, st);
+  }
+}
+
+}  // namespace hemul_gpu
