@@ -39,6 +39,16 @@ bool ntt_col_supported(int log_n, int S);
 cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
                          const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st);
 
+// 30-bit basis fused middle pass with one warp per contiguous block
+// (ntt_blk.cu); used by ntt_mid_tensor_split / ntt_mid_evk when supported.
+bool ntt_blk_supported(int log_n);
+cudaError_t ntt_blk_tensor_split(uint32_t* R1, size_t batch, int np, int log_n,
+                                 const Twiddle32* tw, const Twiddle32* itw,
+                                 const DevPrime32* primes, cudaStream_t st);
+cudaError_t ntt_blk_evk(uint32_t* Fin, const uint32_t* ea, const uint32_t* eb, uint32_t* KA,
+                        uint32_t* KB, size_t batch, int np, int log_n, const Twiddle32* tw,
+                        const Twiddle32* itw, const DevPrime32* primes, cudaStream_t st);
+
 // Fused middle pass (two-pass sizes, logN 12..17): forward levels
 // [s1, logN) of every operand + the evaluation-domain product + inverse
 // levels [s1, logN) of the products, one read and one write per block.

@@ -631,6 +631,8 @@ cudaError_t ntt_mid_tensor(typename F::W* A1, typename F::W* B1, typename F::W* 
 cudaError_t ntt_mid_tensor_split(uint32_t* R1, size_t batch, int np, int log_n,
                                  const Twiddle32* tw, const Twiddle32* itw,
                                  const DevPrime32* primes, cudaStream_t st) {
+  if (ntt_blk_supported(log_n))  // warp-per-block form (ntt_blk.cu)
+    return ntt_blk_tensor_split(R1, batch, np, log_n, tw, itw, primes, st);
   int s1, s2;
   split_levels(log_n, s1, s2);
   MidArgs<F32> a{};
@@ -652,6 +654,10 @@ cudaError_t ntt_mid_evk(typename F::W* Fin, const typename F::W* ea, const typen
                         typename F::W* KA, typename F::W* KB, size_t batch, int np, int log_n,
                         const typename F::Tw* tw, const typename F::Tw* itw,
                         const typename F::Prime* primes, cudaStream_t st) {
+  if constexpr (sizeof(typename F::W) == 4) {
+    if (ntt_blk_supported(log_n))  // warp-per-block form (ntt_blk.cu)
+      return ntt_blk_evk(Fin, ea, eb, KA, KB, batch, np, log_n, tw, itw, primes, st);
+  }
   int s1, s2;
   split_levels(log_n, s1, s2);
   MidArgs<F> a{};

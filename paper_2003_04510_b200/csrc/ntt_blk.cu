@@ -1,0 +1,340 @@
+// Fused NTT middle pass for the 30-bit basis, one warp per contiguous block
+// (sm_100a): forward levels [s1, logN) of every operand, the evaluation-
+// domain product, inverse levels [logN-1, s1) of every product.
+//
+// Reference: ntt_forward / ntt_inverse (proj/core/src/ntt.cpp:59-137,
+// 153-197) and the pointwise products pm_pointwise / rns_pointwise_mul
+// (polymul.cpp:22-27, rns.cpp:108-130); the same computation as ntt.cu's
+// ntt_mid_kernel (OP_TENSOR2 / OP_EVK) with the same lazy ranges, so the
+// results are identical.
+//
+// A warp owns one 2^S-point block (S = logN - s1) of one row for all
+// operands: its loads and stores are coalesced 128-byte rows of the block,
+// its twiddles ((2^s1 + block) 2^L + group, shared by every operand) sit in
+// registers, and the three register / shuffle / register level groups of
+// ntt_col.cu run between __syncwarp exchanges through the warp's own padded
+// shared-memory slots. No CTA barrier at all: warps progress independently,
+// so the HBM traffic of one warp overlaps the arithmetic of the others.
+#include <cuda_runtime.h>
+
+#include "fields.cuh"
+#include "kernels.hpp"
+
+namespace hemul_gpu {
+
+namespace {
+
+constexpr int kWarps = 4;  // blocks (warps) per CTA
+constexpr int kTensor2 = 0, kEvk = 1;
+
+__device__ __forceinline__ int padf(int y) { return y + (y >> 5); }
+
+struct BlkArgs {
+  const uint32_t* in[8];   // operand rows (batch x np x n each)
+  const uint32_t* evk[2];  // kEvk: evk NTT forms, np x n each
+  uint32_t* out[6];        // product rows
+  const Twiddle32* tw;
+  const Twiddle32* itw;
+  const DevPrime32* primes;
+  int np, log_n, s1, rows_per_prime;
+};
+
+template <int S>
+struct BlkGeo {
+  static constexpr int EPT = (1 << S) / 32;
+  static constexpr int R = S - 5;
+  static constexpr int NSH = S - 2 * R;
+  static constexpr int NH = EPT - 1;  // twiddles of R register levels
+  static constexpr int BS = (1 << S) + (1 << (S - 5));  // padded slot (words)
+};
+
+__device__ __forceinline__ Twiddle32 ldtw(const Twiddle32* p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return Twiddle32{v.x, v.y};
+}
+
+// The block's twiddles at levels s1 + L: index (gbase << L) + group
+template <int S>
+struct BlkTw {
+  using G = BlkGeo<S>;
+  uint32_t hw[G::NH], hq[G::NH];      // layout H levels 0 .. R-1 (uniform)
+  uint32_t sw[G::NSH], sq[G::NSH];    // lane levels R .. S-R-1
+  uint32_t lw[G::NH], lq[G::NH];      // layout L levels S-R .. S-1
+  __device__ __forceinline__ void load(const Twiddle32* t, uint32_t gbase, int lane) {
+    constexpr int R = G::R, NSH = G::NSH;
+#pragma unroll
+    for (int L = 0; L < R; ++L)
+#pragma unroll
+      for (int b = 0; b < (1 << L); ++b) {
+        const Twiddle32 x = ldtw(t + (size_t(gbase) << L) + b);
+        hw[(1 << L) - 1 + b] = x.w;
+        hq[(1 << L) - 1 + b] = x.wq;
+      }
+#pragma unroll
+    for (int k = 0; k < NSH; ++k) {
+      const int L = R + k;
+      const Twiddle32 x = ldtw(t + (size_t(gbase) << L) + (lane >> (S - L - R)));
+      sw[k] = x.w;
+      sq[k] = x.wq;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int L = S - R + i;
+#pragma unroll
+      for (int b = 0; b < (1 << i); ++b) {
+        const Twiddle32 x = ldtw(t + (size_t(gbase) << L) + (size_t(lane) << i) + b);
+        lw[(1 << i) - 1 + b] = x.w;
+        lq[(1 << i) - 1 + b] = x.wq;
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ void ct(uint32_t& a, uint32_t& b, uint32_t w, uint32_t wq, uint32_t p2,
+                                   uint32_t negp) {
+  const uint32_t u = csub32(a, p2);
+  const uint32_t v = shoup32(b, w, wq, negp);
+  a = u + v;
+  b = u + p2 - v;
+}
+__device__ __forceinline__ void gs(uint32_t& a, uint32_t& b, uint32_t w, uint32_t wq, uint32_t p2,
+                                   uint32_t negp) {
+  const uint32_t u = a, v = b;
+  a = csub32(u + v, p2);
+  b = shoup32(u + p2 - v, w, wq, negp);
+}
+
+// Forward levels of one operand: v in layout H (y = lane + 32 r) on entry,
+// layout L (y = EPT lane + r) on exit; slot = the warp's scratch slot.
+template <int S>
+__device__ __forceinline__ void fwd(uint32_t (&v)[BlkGeo<S>::EPT], const BlkTw<S>& T,
+                                    uint32_t* slot, int lane, uint32_t p2, uint32_t negp) {
+  using G = BlkGeo<S>;
+  constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH;
+#pragma unroll
+  for (int L = 0; L < R; ++L) {
+    const int half = EPT >> (L + 1);
+#pragma unroll
+    for (int b = 0; b < (1 << L); ++b)
+#pragma unroll
+      for (int rr = 0; rr < half; ++rr)
+        ct(v[b * 2 * half + rr], v[b * 2 * half + rr + half], T.hw[(1 << L) - 1 + b],
+           T.hq[(1 << L) - 1 + b], p2, negp);
+  }
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) slot[padf(lane + 32 * r)] = v[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) v[r] = slot[padf(EPT * lane + r)];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < NSH; ++k) {
+    const int lb = S - 1 - (R + k) - R;
+    const bool upper = (lane >> lb) & 1;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lb);
+      const uint32_t top = upper ? o : v[r], bot = upper ? v[r] : o;
+      const uint32_t u = csub32(top, p2);
+      const uint32_t t = shoup32(bot, T.sw[k], T.sq[k], negp);
+      v[r] = upper ? u + p2 - t : u + t;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int half = EPT >> (i + 1);
+#pragma unroll
+    for (int b = 0; b < (1 << i); ++b)
+#pragma unroll
+      for (int rr = 0; rr < half; ++rr)
+        ct(v[b * 2 * half + rr], v[b * 2 * half + rr + half], T.lw[(1 << i) - 1 + b],
+           T.lq[(1 << i) - 1 + b], p2, negp);
+  }
+}
+
+// Inverse levels (mirror of fwd): layout L on entry, layout H on exit.
+template <int S>
+__device__ __forceinline__ void inv(uint32_t (&v)[BlkGeo<S>::EPT], const BlkTw<S>& T,
+                                    uint32_t* slot, int lane, uint32_t p2, uint32_t negp) {
+  using G = BlkGeo<S>;
+  constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH;
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    const int half = EPT >> (i + 1);
+#pragma unroll
+    for (int b = 0; b < (1 << i); ++b)
+#pragma unroll
+      for (int rr = 0; rr < half; ++rr)
+        gs(v[b * 2 * half + rr], v[b * 2 * half + rr + half], T.lw[(1 << i) - 1 + b],
+           T.lq[(1 << i) - 1 + b], p2, negp);
+  }
+#pragma unroll
+  for (int k = NSH - 1; k >= 0; --k) {
+    const int lb = S - 1 - (R + k) - R;
+    const bool upper = (lane >> lb) & 1;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lb);
+      const uint32_t top = upper ? o : v[r], bot = upper ? v[r] : o;
+      v[r] = upper ? shoup32(top + p2 - bot, T.sw[k], T.sq[k], negp) : csub32(top + bot, p2);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) slot[padf(EPT * lane + r)] = v[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) v[r] = slot[padf(lane + 32 * r)];
+  __syncwarp();
+#pragma unroll
+  for (int L = R - 1; L >= 0; --L) {
+    const int half = EPT >> (L + 1);
+#pragma unroll
+    for (int b = 0; b < (1 << L); ++b)
+#pragma unroll
+      for (int rr = 0; rr < half; ++rr)
+        gs(v[b * 2 * half + rr], v[b * 2 * half + rr + half], T.hw[(1 << L) - 1 + b],
+           T.hq[(1 << L) - 1 + b], p2, negp);
+  }
+}
+
+template <int S, int OP>
+__global__ void __launch_bounds__(32 * kWarps) ntt_blk_kernel(BlkArgs a) {
+  using G = BlkGeo<S>;
+  constexpr int EPT = G::EPT, BS = G::BS;
+  constexpr int NIN = OP == kTensor2 ? 8 : 1, NOUT = OP == kTensor2 ? 6 : 2;
+  constexpr int NSLOT = NIN > NOUT ? NIN : NOUT;
+  extern __shared__ uint32_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* slots = smem + warp * NSLOT * BS;
+  const int j = blockIdx.y / a.rows_per_prime;
+  const int bt = blockIdx.y - j * a.rows_per_prime;
+  const DevPrime32& pr = a.primes[j];
+  const uint32_t p2 = 2 * pr.p, negp = 0u - pr.p;
+  const size_t n = size_t(1) << a.log_n;
+  const int block = blockIdx.x * kWarps + warp;
+  const uint32_t gbase = (1u << a.s1) + block;
+  const size_t off = (size_t(bt) * a.np + j) * n + (size_t(block) << S) + lane;
+  BlkTw<S> T;
+  T.load(a.tw + size_t(j) * n, gbase, lane);
+  // ---- forward levels of every operand; results parked in layout L. The
+  // next operand's rows are loaded while this one is transformed. ----------
+  uint32_t nx[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) nx[r] = a.in[0][off + 32 * r];
+#pragma unroll 1
+  for (int o = 0; o < NIN; ++o) {
+    uint32_t v[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = nx[r];
+    if (o + 1 < NIN) {
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) nx[r] = a.in[o + 1][off + 32 * r];
+    }
+    fwd<S>(v, T, slots + o * BS, lane, p2, negp);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) slots[o * BS + padf(EPT * lane + r)] = v[r];
+  }
+  // ---- products at this lane's own positions (no exchange needed) -------
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int e = padf(EPT * lane + r);
+    if constexpr (OP == kTensor2) {
+      uint32_t x[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) x[o] = slots[o * BS + e];
+      F32::tensor_split(x, pr);
+#pragma unroll
+      for (int o = 0; o < 6; ++o) slots[o * BS + e] = x[o];
+    } else {
+      const size_t ei = size_t(j) * n + (size_t(block) << S) + EPT * lane + r;
+      const uint32_t f = slots[e];
+      slots[e] = F32::mul(f, __ldg(a.evk[0] + ei), pr);
+      slots[BS + e] = F32::mul(f, __ldg(a.evk[1] + ei), pr);
+    }
+  }
+  // ---- inverse levels of every product ------------------------------------
+  T.load(a.itw + size_t(j) * n, gbase, lane);
+#pragma unroll 1
+  for (int o = 0; o < NOUT; ++o) {
+    uint32_t v[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = slots[o * BS + padf(EPT * lane + r)];
+    inv<S>(v, T, slots + o * BS, lane, p2, negp);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) a.out[o][off + 32 * r] = v[r];
+  }
+}
+
+template <int S, int OP>
+cudaError_t launch_blk(const BlkArgs& a, size_t rows, cudaStream_t st) {
+  constexpr int NSLOT = OP == kTensor2 ? 8 : 2;
+  const size_t smem = size_t(kWarps) * NSLOT * BlkGeo<S>::BS * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(ntt_blk_kernel<S, OP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(static_cast<unsigned>((1 << a.s1) / kWarps), static_cast<unsigned>(rows));
+  ntt_blk_kernel<S, OP><<<grid, 32 * kWarps, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int OP>
+cudaError_t launch_blk_any(const BlkArgs& a, int S, size_t rows, cudaStream_t st) {
+  switch (S) {
+    case 6: return launch_blk<6, OP>(a, rows, st);
+    case 7: return launch_blk<7, OP>(a, rows, st);
+    default: return launch_blk<8, OP>(a, rows, st);
+  }
+}
+
+}  // namespace
+
+bool ntt_blk_supported(int log_n) {
+  if (log_n < 12 || log_n > 17) return false;
+  const int s1 = (log_n + 1) / 2, s2 = log_n - s1;
+  return s2 >= 6 && s2 <= 8 && (1 << s1) % kWarps == 0;
+}
+
+cudaError_t ntt_blk_tensor_split(uint32_t* R1, size_t batch, int np, int log_n,
+                                 const Twiddle32* tw, const Twiddle32* itw,
+                                 const DevPrime32* primes, cudaStream_t st) {
+  if (!ntt_blk_supported(log_n)) return cudaErrorInvalidValue;
+  const int s1 = (log_n + 1) / 2;
+  BlkArgs a{};
+  const size_t slot = batch * size_t(np) << log_n;
+  for (int o = 0; o < 8; ++o) a.in[o] = R1 + o * slot;
+  for (int o = 0; o < 6; ++o) a.out[o] = R1 + o * slot;
+  a.tw = tw;
+  a.itw = itw;
+  a.primes = primes;
+  a.np = np;
+  a.log_n = log_n;
+  a.s1 = s1;
+  a.rows_per_prime = static_cast<int>(batch);
+  return launch_blk_any<kTensor2>(a, log_n - s1, batch * np, st);
+}
+
+cudaError_t ntt_blk_evk(uint32_t* Fin, const uint32_t* ea, const uint32_t* eb, uint32_t* KA,
+                        uint32_t* KB, size_t batch, int np, int log_n, const Twiddle32* tw,
+                        const Twiddle32* itw, const DevPrime32* primes, cudaStream_t st) {
+  if (!ntt_blk_supported(log_n)) return cudaErrorInvalidValue;
+  const int s1 = (log_n + 1) / 2;
+  BlkArgs a{};
+  a.in[0] = Fin;
+  a.evk[0] = ea;
+  a.evk[1] = eb;
+  a.out[0] = KA;
+  a.out[1] = KB;
+  a.tw = tw;
+  a.itw = itw;
+  a.primes = primes;
+  a.np = np;
+  a.log_n = log_n;
+  a.s1 = s1;
+  a.rows_per_prime = static_cast<int>(batch);
+  return launch_blk_any<kEvk>(a, log_n - s1, batch * np, st);
+}
+
+}  // namespace hemul_gpu

@@ -73,54 +73,18 @@ __device__ __forceinline__ void gs(uint32_t& a, uint32_t& b, uint32_t w, uint32_
   b = shoup32(u + p2 - v, w, wq, negp);
 }
 
+// One warp transforms one padded column mc (see the layout notes above).
 template <int S, bool INV>
-__global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
+__device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* stw,
+                                                 const DevPrime32& pr, int lane) {
   using G = ColGeo<S>;
-  constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH, CS = G::CS;
-  extern __shared__ uint32_t smem[];
-  uint32_t* col = smem;                        // [kCols][CS]
-  uint32_t* stw = smem + kCols * CS;           // [2^S] x {w, wq}
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  int j, row;
-  if (a.rows_per_prime) {  // prime-major traversal (ntt.cu PassArgs)
-    j = blockIdx.y / a.rows_per_prime;
-    row = (blockIdx.y - j * a.rows_per_prime) * a.np + j;
-  } else {
-    row = blockIdx.y;
-    j = row % a.np;
-  }
-  const DevPrime32& pr = a.primes[j];
+  constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH;
   const uint32_t p = pr.p, p2 = 2 * p, negp = 0u - p;
-  const size_t n = size_t(1) << a.log_n;
-  const int tlast = 1 << (a.log_n - S);
-  uint32_t* rowp = a.data + size_t(row) * n + size_t(blockIdx.x) * kCols;
-  // ---- cooperative load: 16-byte vectors, thread -> (columns 4 (tid % 4)
-  // .. +3, rows tid / 4 + 128 r) ------------------------------------------------
-  {
-    constexpr int RS = kThreads / 4;  // rows per sweep
-    const int x4 = 4 * (tid & 3), y0 = tid >> 2;
-    const uint4* src = reinterpret_cast<const uint4*>(rowp + size_t(y0) * tlast + x4);
-    const size_t step = size_t(RS) * tlast / 4;
-#pragma unroll
-    for (int r = 0; r < (1 << S) / RS; ++r) {
-      const uint4 q = src[r * step];
-      const int fy = padf(y0 + RS * r);
-      col[x4 * CS + fy] = q.x;
-      col[(x4 + 1) * CS + fy] = q.y;
-      col[(x4 + 2) * CS + fy] = q.z;
-      col[(x4 + 3) * CS + fy] = q.w;
-    }
-    const uint32_t* t2 = reinterpret_cast<const uint32_t*>(a.tw + size_t(j) * n);
-    for (int i = tid; i < 2 << S; i += kThreads) stw[i] = t2[i];
-  }
-  __syncthreads();
-  for (int cw = warp; cw < kCols; cw += kWarps) {
-  uint32_t* mc = col + cw * CS;
-  uint32_t v[EPT];
   auto tw = [&](int idx, uint32_t& w, uint32_t& wq) {
     w = stw[2 * idx];
     wq = stw[2 * idx + 1];
   };
+  uint32_t v[EPT];
   if (!INV) {
     // ---- layout H: y = lane + 32 r; levels 0 .. R-1 ----------------------
 #pragma unroll
@@ -231,7 +195,48 @@ __global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
 #pragma unroll
     for (int r = 0; r < EPT; ++r) mc[padf(lane + 32 * r)] = v[r];
   }
+}
+
+template <int S, bool INV>
+__global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
+  constexpr int CS = ColGeo<S>::CS;
+  extern __shared__ uint32_t smem[];
+  uint32_t* col = smem;                        // [kCols][CS]
+  uint32_t* stw = smem + kCols * CS;           // [2^S] x {w, wq}
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int j, row;
+  if (a.rows_per_prime) {  // prime-major traversal (ntt.cu PassArgs)
+    j = blockIdx.y / a.rows_per_prime;
+    row = (blockIdx.y - j * a.rows_per_prime) * a.np + j;
+  } else {
+    row = blockIdx.y;
+    j = row % a.np;
   }
+  const DevPrime32& pr = a.primes[j];
+  const size_t n = size_t(1) << a.log_n;
+  const int tlast = 1 << (a.log_n - S);
+  uint32_t* rowp = a.data + size_t(row) * n + size_t(blockIdx.x) * kCols;
+  // ---- cooperative load: 16-byte vectors, thread -> (columns 4 (tid % 4)
+  // .. +3, rows tid / 4 + 128 r) ------------------------------------------------
+  {
+    constexpr int RS = kThreads / 4;  // rows per sweep
+    const int x4 = 4 * (tid & 3), y0 = tid >> 2;
+    const uint4* src = reinterpret_cast<const uint4*>(rowp + size_t(y0) * tlast + x4);
+    const size_t step = size_t(RS) * tlast / 4;
+#pragma unroll
+    for (int r = 0; r < (1 << S) / RS; ++r) {
+      const uint4 q = src[r * step];
+      const int fy = padf(y0 + RS * r);
+      col[x4 * CS + fy] = q.x;
+      col[(x4 + 1) * CS + fy] = q.y;
+      col[(x4 + 2) * CS + fy] = q.z;
+      col[(x4 + 3) * CS + fy] = q.w;
+    }
+    const uint32_t* t2 = reinterpret_cast<const uint32_t*>(a.tw + size_t(j) * n);
+    for (int i = tid; i < 2 << S; i += kThreads) stw[i] = t2[i];
+  }
+  __syncthreads();
+  for (int cw = warp; cw < kCols; cw += kWarps) column_transform<S, INV>(col + cw * CS, stw, pr, lane);
   __syncthreads();
   // ---- cooperative store ------------------------------------------------
   {
