@@ -73,6 +73,17 @@ __device__ __forceinline__ void gs(uint32_t& a, uint32_t& b, uint32_t w, uint32_
   b = shoup32(u + p2 - v, w, wq, negp);
 }
 
+// Shared twiddle slot of table entry t (level L = floor(log2 t)). Layout-L
+// levels (L >= S - R = 5) are read by lane l at t = 2^L + l 2^i + blk
+// (i = L - 5): stored lane-minor instead (2^L + blk 32 + l) so those reads
+// are bank-conflict free; w and wq live in separate arrays.
+template <int S>
+__device__ __forceinline__ int twiddle_slot(int t) {
+  if (t < 32) return t;
+  const int L = 31 - __clz(t), i = L - 5, within = t - (1 << L);
+  return (1 << L) + (within & ((1 << i) - 1)) * 32 + (within >> i);
+}
+
 // One warp transforms one padded column mc (see the layout notes above).
 template <int S, bool INV>
 __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* stw,
@@ -81,8 +92,8 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
   constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH;
   const uint32_t p = pr.p, p2 = 2 * p, negp = 0u - p;
   auto tw = [&](int idx, uint32_t& w, uint32_t& wq) {
-    w = stw[2 * idx];
-    wq = stw[2 * idx + 1];
+    w = stw[idx];
+    wq = stw[(1 << S) + idx];
   };
   uint32_t v[EPT];
   if (!INV) {
@@ -129,7 +140,7 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
 #pragma unroll
       for (int blk = 0; blk < (1 << i); ++blk) {
         uint32_t w, wq;
-        tw((1 << L) + (lane << i) + blk, w, wq);
+        tw((1 << L) + blk * 32 + lane, w, wq);  // permuted (twiddle_slot)
 #pragma unroll
         for (int rr = 0; rr < half; ++rr)
           ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
@@ -147,7 +158,7 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
 #pragma unroll
       for (int blk = 0; blk < (1 << i); ++blk) {
         uint32_t w, wq;
-        tw((1 << L) + (lane << i) + blk, w, wq);
+        tw((1 << L) + blk * 32 + lane, w, wq);  // permuted (twiddle_slot)
 #pragma unroll
         for (int rr = 0; rr < half; ++rr)
           gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
@@ -202,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
   constexpr int CS = ColGeo<S>::CS;
   extern __shared__ uint32_t smem[];
   uint32_t* col = smem;                        // [kCols][CS]
-  uint32_t* stw = smem + kCols * CS;           // [2^S] x {w, wq}
+  uint32_t* stw = smem + kCols * CS;           // w[2^S] then wq[2^S] (twiddle_slot order)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int j, row;
   if (a.rows_per_prime) {  // prime-major traversal (ntt.cu PassArgs)
@@ -233,7 +244,11 @@ __global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
       col[(x4 + 3) * CS + fy] = q.w;
     }
     const uint32_t* t2 = reinterpret_cast<const uint32_t*>(a.tw + size_t(j) * n);
-    for (int i = tid; i < 2 << S; i += kThreads) stw[i] = t2[i];
+    for (int i = tid; i < 1 << S; i += kThreads) {
+      const int pos = twiddle_slot<S>(i);
+      stw[pos] = t2[2 * i];
+      stw[(1 << S) + pos] = t2[2 * i + 1];
+    }
   }
   __syncthreads();
   for (int cw = warp; cw < kCols; cw += kWarps) column_transform<S, INV>(col + cw * CS, stw, pr, lane);
