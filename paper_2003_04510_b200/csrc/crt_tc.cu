@@ -9,7 +9,8 @@
 // bytes), the weights u_{j,k} = 2^(8k) mod p_j (< 2^30) are cut into four
 // byte planes, and one u8 x u8 -> s32 tensor-core GEMM gives
 //   D[i][4j+b] = sum_k a_{i,k} byte_b(u_{j,k})        (< K 2^16: exact)
-//   a_i mod p_j = (D0 + 2^8 D1 + 2^16 D2 + 2^24 D3) mod p_j   (epilogue)
+//   a_i mod p_j = (D0 + 2^8 D1 + 2^16 D2 + 2^24 D3) 2^-32 mod p_j  (epilogue;
+//   the weights carry 2^32: one Montgomery step)
 // with no carries anywhere. A coefficient costs K x 4 np MACs on a
 // 4.1 POPS pipe instead of ceil(bits/25) x np IMAD.WIDE on a 8 T/s pipe.
 //
@@ -62,35 +63,44 @@ __device__ __forceinline__ uint32_t limb_bytes(int l, int limbs, int end_bit) {
   return lim <= 0 ? 0u : lim >= 64 ? 8u : uint32_t((lim + 7) >> 3);
 }
 
-// Plane shifts passed as kernel arguments: ptxas then keeps the three
-// IMAD.WIDE (a known power of two would be strength-reduced into a longer
-// shift/add/carry sequence).
-struct PlaneShifts {
-  uint32_t s8, s16, s24;  // 2^8, 2^16, 2^24
-};
+// (d0 + 2^8 d1 + 2^16 d2 + 2^24 d3) 2^-32 mod p, lazy in [0, 2p) (inside the
+// forward NTT's input domain [0, 4p), fields.cuh F32::ct), for plane sums
+// d_b < 2^26. The table weights carry the factor 2^32 (build_crt_tc), so this
+// is a mod p. z = d0 + ... < 2^51 is assembled in two 32-bit words with a
+// carry chain (ALU pipe), then one Montgomery step: m = zl (-p^-1) mod 2^32,
+// (z + m p) / 2^32 = zh + umulhi(m, p) + (zl != 0) < p + 2^19 + 1 < 2p.
+__device__ __forceinline__ uint32_t planes_mont(uint32_t d0, uint32_t d1, uint32_t d2,
+                                                uint32_t d3, uint32_t p, uint32_t pinv) {
+  uint32_t zl, zh;
+  asm("{\n\t.reg .u32 a1, a2, a3, h1, h2, h3;\n\t"
+      "shl.b32 a1, %2, 8;\n\tshr.u32 h1, %2, 24;\n\t"
+      "shl.b32 a2, %3, 16;\n\tshr.u32 h2, %3, 16;\n\t"
+      "shl.b32 a3, %4, 24;\n\tshr.u32 h3, %4, 8;\n\t"
+      "add.cc.u32 %0, %5, a1;\n\taddc.u32 %1, h1, h2;\n\t"
+      "add.cc.u32 %0, %0, a2;\n\taddc.u32 %1, %1, h3;\n\t"
+      "add.cc.u32 %0, %0, a3;\n\taddc.u32 %1, %1, 0;\n\t}"
+      : "=r"(zl), "=r"(zh)
+      : "r"(d1), "r"(d2), "r"(d3), "r"(d0));
+  const uint32_t m = zl * pinv;
+  return zh + __umulhi(m, p) + (zl != 0u);
+}
 
-// (d0 + 2^8 d1 + 2^16 d2 + 2^24 d3) mod p, lazy in [0, 4p) (the forward
-// NTT's input domain, fields.cuh F32::ct), for plane sums d_b < 2^26:
-// z < 2^51 by three IMAD.WIDE, then zl + zh (2^32 mod p) by two Shoup steps.
-__device__ __forceinline__ uint32_t planes_mod(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
-                                               const uint4& pr, const PlaneShifts& sh) {
-  uint64_t z = d0;
-  z += uint64_t(d1) * sh.s8;
-  z += uint64_t(d2) * sh.s16;
-  z += uint64_t(d3) * sh.s24;
-  const uint32_t zl = static_cast<uint32_t>(z), zh = static_cast<uint32_t>(z >> 32);
-  const uint32_t negp = 0u - pr.x;  // pr = {p, floor(2^32/p), 2^32 mod p, its Shoup quotient}
-  return shoup32(zh, pr.z, pr.w, negp) + (zl + __umulhi(zl, pr.y) * negp);
+// -p^-1 mod 2^32 (p odd): Newton, 5 steps from inv = p (correct to 3 bits)
+__device__ __forceinline__ uint32_t neg_inv32(uint32_t p) {
+  uint32_t inv = p;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+  return 0u - inv;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     crt_tc_kernel(TcInputs in, int count, int B, int limbs, int log_n, CrtTcTable tab,
                   const DevPrime32* __restrict__ primes, int np, uint32_t* __restrict__ out,
-                  int stages, PlaneShifts sh) {
+                  int stages) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t a_full[kMaxStages], a_empty[kMaxStages], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ uint4 eprimes[kMaxTilePrimes];  // {p, one_q, beta, beta_q} of the tile's primes
+  __shared__ uint2 eprimes[kMaxTilePrimes];  // {p, -p^-1 mod 2^32} of the tile's primes
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_addr(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t n = size_t(1) << log_n;
@@ -121,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int j = threadIdx.x; j < pcount; j += kThreads) {
     const DevPrime32& pr = primes[jbase + j];
-    eprimes[j] = make_uint4(pr.p, pr.one_q, pr.beta, pr.beta_q);
+    eprimes[j] = make_uint2(pr.p, neg_inv32(pr.p));
   }
   if (warp == kMmaWarp) tc::tmem_alloc<512>(&tmem_base);
   tc::fence_before();
@@ -237,9 +247,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int jn = min((g + 1 < g1) ? 8 : 4, pcount - 4 * g);  // primes in this pair
 #pragma unroll
         for (int q = 0; q < 8; ++q, op += n)
-          if (q < jn)
-            *op = planes_mod(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], eprimes[4 * g + q],
-                             sh);
+          if (q < jn) {
+            const uint2 e = eprimes[4 * g + q];
+            *op = planes_mont(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], e.x, e.y);
+          }
       }
       tc::fence_before();
       tc::mbar_arrive(&t_empty[acc]);
@@ -311,8 +322,7 @@ cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs,
   const int per_ct = std::max(1, sms / tab.ncol_tiles);
   const int grid = per_ct * tab.ncol_tiles;
   crt_tc_kernel<<<grid, kThreads, smem, st>>>(in, count, static_cast<int>(batch), limbs, log_n,
-                                              tab, primes, np, out, stages,
-                                              PlaneShifts{1u << 8, 1u << 16, 1u << 24});
+                                              tab, primes, np, out, stages);
   return cudaGetLastError();
 }
 

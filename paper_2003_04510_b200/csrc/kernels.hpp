@@ -112,7 +112,7 @@ cudaError_t crt_forward_multi(const uint64_t* const* polys, int count, int limbs
 // offset d = bit0 / 8 - 8 limb0 inside it); bits >= end_bit (= bit0 + bits,
 // relative to the coefficient) are cleared on load.
 // btab: [ncol_tiles * col_tile][kpad] u8, row 4 jj + b of column tile ct =
-// byte b of 2^(8 (k - d)) mod p_j, j = ct * primes_per_tile + jj, for
+// byte b of 2^(8 (k - d) + 32) mod p_j (Montgomery), j = ct * primes_per_tile + jj, for
 // d <= k < d + ceil(bits / 8), else 0 (level_tables.cpp build_crt_tc).
 struct CrtTcTable {
   const uint8_t* btab = nullptr;

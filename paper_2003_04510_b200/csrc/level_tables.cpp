@@ -421,7 +421,7 @@ RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, in
     const int ct = j / t.primes_per_tile, jj = j - ct * t.primes_per_tile;
     const uint64_t p = primes[j];
     const uint64_t step = powmod(2, 8, p);
-    uint64_t u = 1 % p;
+    uint64_t u = powmod(2, 32, p);  // Montgomery factor: crt_tc.cu planes_mont
     for (int k = d; k < d + nbytes; ++k) {
       for (int b = 0; b < 4; ++b)
         t.btab[(size_t(ct) * t.col_tile + 4 * jj + b) * t.kpad + k] = uint8_t(u >> (8 * b));
