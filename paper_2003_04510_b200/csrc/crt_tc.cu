@@ -48,7 +48,8 @@ constexpr int kMaxTilePrimes = 64;
 
 struct TcInputs {
   const uint64_t* p[kMaxCrtInputs];
-  const uint8_t* btab[kMaxCrtInputs];
+  const uint8_t* btab[2];       // the (at most two) distinct weight tables
+  int slot[kMaxCrtInputs];      // input t's table
   int limb0[kMaxCrtInputs];
   int end_bit[kMaxCrtInputs];
   int aligned16[kMaxCrtInputs];  // rows and the field start 16-byte aligned
@@ -96,7 +97,7 @@ __device__ __forceinline__ uint32_t neg_inv32(uint32_t p) {
 __global__ void __launch_bounds__(kThreads, 1)
     crt_tc_kernel(TcInputs in, int count, int B, int limbs, int log_n, CrtTcTable tab,
                   const DevPrime32* __restrict__ primes, int np, uint32_t* __restrict__ out,
-                  int stages) {
+                  int stages, int nslots) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t a_full[kMaxStages], a_empty[kMaxStages], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base;
@@ -110,11 +111,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cta_in_ct = blockIdx.x / tab.ncol_tiles;
   const int ctas_per_ct = gridDim.x / tab.ncol_tiles;
   const int col_tile = tab.col_tile;
-  uint8_t* sB = smem;                                   // [col_tile][kcols]
-  uint8_t* sA = smem + size_t(col_tile) * kcols;        // stages x [128][kcols]
+  uint8_t* sB = smem;                                   // nslots x [col_tile][kcols]
+  const uint32_t b_bytes = uint32_t(col_tile) * kcols;
+  uint8_t* sA = smem + size_t(nslots) * b_bytes;        // stages x [128][kcols]
   const uint32_t a_bytes = kRows * kcols;
   const int tiles_per_poly = static_cast<int>(n / kRows);
-  const int tiles = count * B * tiles_per_poly;
   const int jbase = ct * tab.primes_per_tile;
   const int pcount = min(tab.primes_per_tile, np - jbase);
 
@@ -139,34 +140,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
-  // Tiles are walked in input order; the resident weight tile is reloaded
-  // (by every warp, between two CTA barriers) when the input changes.
-  int cur_in = -1;
-  int it = 0;  // local tile counter (ring / accumulator phases)
-  // tile = (t * B + b) * tiles_per_poly + ci, advanced without divisions
-  const int poly_tiles = B * tiles_per_poly;
-  int t = cta_in_ct / poly_tiles, rem = cta_in_ct - t * poly_tiles;
-  int b = rem / tiles_per_poly, ci = rem - b * tiles_per_poly;
-  const int step_t = ctas_per_ct / poly_tiles, step_r = ctas_per_ct - step_t * poly_tiles;
-  const int step_b = step_r / tiles_per_poly, step_c = step_r - step_b * tiles_per_poly;
-  for (int tile = cta_in_ct; tile < tiles; tile += ctas_per_ct) {
-    if (t != cur_in) {
-      // every role has finished its part of the previous tile here, and the
-      // epilogue has seen its accumulator: no MMA reads sB any more
-      __syncthreads();
-      const uint8_t* g = in.btab[t] + size_t(ct) * col_tile * kpad;
-      const int chunks = kpad / 16;
-      for (int idx = threadIdx.x; idx < col_tile * chunks; idx += kThreads) {
-        const int r = idx / chunks, c = idx - r * chunks;
-        tc::cp_async16z(tc::smem_addr(sB + tc::kmaj_sw128(r, 16 * c, col_tile)),
-                        g + size_t(r) * kpad + 16 * c, 16);
-      }
-      cp_async_commit();
-      cp_async_wait<0>();
-      tc::fence_async_smem();
-      __syncthreads();
-      cur_in = t;
+  // Both weight tables (the low and high halves' of split region 1, or the
+  // one of region 2) stay resident. A CTA walks coefficient blocks (batch
+  // entry b, 128 coefficients at ci) and converts every input's field of the
+  // block in turn, so the halves of one poly read the same rows back to back.
+  for (int sl = 0; sl < nslots; ++sl) {
+    const uint8_t* g = in.btab[sl] + size_t(ct) * col_tile * kpad;
+    const int chunks = kpad / 16;
+    for (int idx = threadIdx.x; idx < col_tile * chunks; idx += kThreads) {
+      const int r = idx / chunks, c = idx - r * chunks;
+      tc::cp_async16z(tc::smem_addr(sB + sl * b_bytes + tc::kmaj_sw128(r, 16 * c, col_tile)),
+                      g + size_t(r) * kpad + 16 * c, 16);
     }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  tc::fence_async_smem();
+  __syncthreads();
+  int it = 0;  // local tile counter (ring / accumulator phases)
+  const int poly_tiles = B * tiles_per_poly;
+  int b = cta_in_ct / tiles_per_poly, ci = cta_in_ct - b * tiles_per_poly;
+  const int step_b = ctas_per_ct / tiles_per_poly, step_c = ctas_per_ct - step_b * tiles_per_poly;
+  for (int blk = cta_in_ct; blk < poly_tiles; blk += ctas_per_ct) {
+  for (int t = 0; t < count; ++t) {
     const size_t i0 = size_t(ci) * kRows;
     const int s = it % stages;
     const int acc = it & 1;
@@ -215,7 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_async_smem();  // cp.async (generic proxy) data -> tensor core
         tc::mbar_wait(&t_empty[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after();
-        const uint32_t a0 = tc::smem_addr(sA + s * a_bytes), b0 = tc::smem_addr(sB);
+        const uint32_t a0 = tc::smem_addr(sA + s * a_bytes);
+        const uint32_t b0 = tc::smem_addr(sB + in.slot[t] * b_bytes);
         const uint32_t idesc = tc::idesc_u8(kRows, col_tile, 0, 0);
         const uint32_t d = tmem + acc * 256;
         for (int k = 0; k < kpad / 32; ++k)
@@ -256,11 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_arrive(&t_empty[acc]);
     }
     ++it;
+  }
     ci += step_c;
     b += step_b;
-    t += step_t;
     if (ci >= tiles_per_poly) ci -= tiles_per_poly, ++b;
-    if (b >= B) b -= B, ++t;
   }
   cp_async_wait<0>();
   tc::fence_before();
@@ -270,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t crt_tc_smem(const CrtTcTable& tab, int* stages) {
+size_t crt_tc_smem(const CrtTcTable& tab, int* stages, int nslots = 1) {
   const size_t kc = round128(tab.kpad);
-  const size_t b = size_t(tab.col_tile) * kc, a = kRows * kc;
+  const size_t b = size_t(nslots) * tab.col_tile * kc, a = kRows * kc;
   const size_t cap = kMaxDynSmem - 1024;
   int s = kMaxStages;
   while (s > 2 && b + s * a > cap) --s;
@@ -299,12 +295,19 @@ cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs,
   if (count < 1 || count > kMaxCrtInputs || n < size_t(kRows)) return cudaErrorInvalidValue;
   TcInputs in{};
   CrtTcTable tab = tabs[0];
+  int nslots = 0;
   for (int t = 0; t < count; ++t) {
     if (tabs[t].kpad != tab.kpad || tabs[t].col_tile != tab.col_tile ||
         tabs[t].ncol_tiles != tab.ncol_tiles || !crt_tc_supported(tabs[t]))
       return cudaErrorInvalidValue;
     in.p[t] = polys[t];
-    in.btab[t] = tabs[t].btab;
+    int sl = 0;
+    while (sl < nslots && in.btab[sl] != tabs[t].btab) ++sl;
+    if (sl == nslots) {
+      if (nslots == 2) return cudaErrorInvalidValue;  // at most two distinct tables
+      in.btab[nslots++] = tabs[t].btab;
+    }
+    in.slot[t] = sl;
     in.limb0[t] = tabs[t].limb0;
     in.end_bit[t] = tabs[t].end_bit;
     in.aligned16[t] = limbs % 2 == 0 && tabs[t].limb0 % 2 == 0 &&
@@ -318,11 +321,12 @@ cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int stages = 0;
-  const size_t smem = crt_tc_smem(tab, &stages);
+  const size_t smem = crt_tc_smem(tab, &stages, nslots);
+  if (smem > size_t(kMaxDynSmem)) return cudaErrorInvalidValue;
   const int per_ct = std::max(1, sms / tab.ncol_tiles);
   const int grid = per_ct * tab.ncol_tiles;
   crt_tc_kernel<<<grid, kThreads, smem, st>>>(in, count, static_cast<int>(batch), limbs, log_n,
-                                              tab, primes, np, out, stages);
+                                              tab, primes, np, out, stages, nslots);
   return cudaGetLastError();
 }
 
