@@ -1109,7 +1109,9 @@ void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                       uint64_t* out_bx, bool dev_out) {
   const size_t n = size_t(c->n);
   const size_t poly_w = n * limbs_of(log_q), out_w = n * limbs_of(log_q - c->log_p);
-  const size_t chunk = batch <= 1 ? 1 : (batch + 3) / 4;
+  // 8 chunks: the copies dominate (PCIe moves ~240 MB per HE Mul at X), so
+  // small chunks shorten the un-overlapped first H2D and last compute + D2H
+  const size_t chunk = batch <= 1 ? 1 : (batch + 7) / 8;
   const size_t chunks = (batch + chunk - 1) / chunk;
   ensure(c->in, 2 * 4 * chunk * poly_w * 8);
   ensure(c->outb, 2 * 2 * chunk * out_w * 8);

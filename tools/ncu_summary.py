@@ -50,11 +50,13 @@ def read(rep: Path) -> dict:
     res = {"kernel": vals[hdr.index("Kernel Name")]}
     for m, key in METRICS.items():
         # some sections prefix their metrics (e.g. "TPC.TriageCompute.")
-        idx = [i for i, h in enumerate(hdr) if h == m or h.endswith("." + m)]
-        if idx:
-            i = idx[0]
-            v = float(vals[i].replace(",", ""))
+        for i in [i for i, h in enumerate(hdr) if h == m or h.endswith("." + m)]:
+            try:
+                v = float(vals[i].replace(",", ""))
+            except ValueError:
+                continue
             res[key] = v * UNIT.get(units[i], 1.0)
+            break
     return res
 
 

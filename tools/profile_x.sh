@@ -11,18 +11,19 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 prof() {  # class kernel-regex launch-skip
   ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o $OUT/prof_$1 $CMD > /dev/null 2>&1
 }
-# launch order per he_mul (30-bit basis, tensor-core engine): crt_tc r1, ntt A,
-# mid r1, intt A, bigint_tc (iCRT), crt_tc r2, ntt A, mid r2, intt A,
-# bigint_tc (finisher), fix-up. warm_level runs the evk CRT (IMAD kernel) and
-# NTT passes first.
+# launch order per he_mul (30-bit basis, tensor-core engine): crt_tc r1,
+# ntt_col (fwd A), ntt_blk (mid r1), ntt_col (inv A), bigint_tc (iCRT), crt_tc
+# r2, ntt_col, ntt_blk (mid r2), ntt_col, bigint_tc (finisher), fix-up.
+# warm_level runs the evk CRT (IMAD kernel) and two forward NTT passes first
+# (ntt_col + the pass-B ntt_pass_kernel).
 prof crt crt_tc_kernel 2
 prof crt_r2 crt_tc_kernel 3
-prof ntt_a ntt_pass_kernel 4
-prof mid_r1 ntt_mid_kernel 0
-prof intt_a ntt_pass_kernel 5
+prof ntt_a ntt_col_kernel 4
+prof mid_r1 ntt_blk_kernel 2
+prof intt_a ntt_col_kernel 5
 prof icrt bigint_tc_kernel 2
-prof mid_r2 ntt_mid_kernel 1
+prof mid_r2 ntt_blk_kernel 3
 prof finish bigint_tc_kernel 3
-python tools/ncu_summary.py $OUT/prof_*.ncu-rep --out $OUT/ncu_summary_X.md --traffic $OUT/traffic.json --config X
+python tools/ncu_summary.py $OUT/prof_*.ncu-rep --out $OUT/ncu_summary_X.md --traffic $OUT/traffic.json --config X || exit 1
 for f in $OUT/prof_*.ncu-rep; do python tools/ncu_keys.py $f; done > $OUT/ncu_keys_X.txt
 rm -f $OUT/prof_*.ncu-rep
