@@ -28,7 +28,8 @@
 // (kernels.hpp Finisher).
 //
 // Persistent warp-specialised CTA (one per SM, 512 TMEM columns):
-//   warp 4      TMA: B chunks (64 K-bytes x n_cols rows, 64-byte swizzle)
+//   warp 4      bulk copies of the B chunks (64 K-bytes x n_cols rows, stored
+//               chunk-major and pre-swizzled for the 64-byte UMMA layout)
 //   warp 5      MMA issue: 2 k-steps x 2 MMAs (N = n_cols / 2 each) per chunk
 //   warps 6-9   producers: cp.async of the t_j rows (6-stage private ring; the
 //               inverse NTT already scaled x_j by (P/p_j)^-1, context.cu
@@ -80,6 +81,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_addr(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(tc::smem_addr(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_addr(bar)),
                "r"(bytes)
@@ -101,7 +110,7 @@ __device__ __forceinline__ int seg_row(const BigTcSeg& s, int e, int B, int j) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    bigint_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap rmap0,
+    bigint_tc_kernel(const uint8_t* __restrict__ btab, const __grid_constant__ CUtensorMap rmap0,
                      const __grid_constant__ CUtensorMap rmap1, Params P) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t a_full[kSA], a_empty[kSA], b_full[kSB], b_empty[kSB];
@@ -162,16 +171,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto slot_hi = [&](int t) { return nslots == 3 ? (2 * t + 1) % 3 : 1; };
 
   if (warp == kTmaWarp) {
-    // ---- TMA: B chunks (table) -------------------------------------------
+    // ---- B chunks: one linear bulk copy each (the table is stored chunk-
+    // major and pre-swizzled, level_tables.cpp build_bigint) ---------------
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       for (int q = 0, c = 0; q < total; ++q) {
         const int s = q % kSB;
         tc::mbar_wait(&b_empty[s], ((q / kSB) & 1) ^ 1);
         mbar_expect_tx(&b_full[s], b_bytes);
-        const uint32_t dst = tc::smem_addr(sB + s * b_bytes);
-        tma_load_2d(dst, &tmap, c * kChunk, 0, &b_full[s]);
-        tma_load_2d(dst + NH * kChunk, &tmap, c * kChunk, NH, &b_full[s]);
+        bulk_load(tc::smem_addr(sB + s * b_bytes), btab + size_t(c) * b_bytes, b_bytes, &b_full[s]);
         if (++c == C) c = 0;
       }
     }
@@ -438,7 +445,7 @@ cudaError_t bigint_tc_setup_attributes() {
 cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, int B, int log_n,
                       const BigTcOut& o, const void* const* rmaps, cudaStream_t st) {
   const size_t n = size_t(1) << log_n;
-  if (!t.tmap || !rmaps || !rmaps[0] || !rmaps[1] || t.nseg < 1 || t.nseg > kMaxSeg || n < size_t(kRows) || t.n_cols % 32 ||
+  if (!t.btab || !rmaps || !rmaps[0] || !rmaps[1] || t.nseg < 1 || t.nseg > kMaxSeg || n < size_t(kRows) || t.n_cols % 32 ||
       t.n_cols > 480 || t.k_bytes % kChunk || bigint_tc_smem(t.n_cols) > size_t(kMaxDynSmem))
     return cudaErrorInvalidValue;
   if ((o.check_amb || o.force_exact) && !o.flags.count) return cudaErrorInvalidValue;
@@ -480,7 +487,7 @@ cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, in
     if (e != cudaSuccess) return e;
   }
   bigint_tc_kernel<<<grid, kThreads, bigint_tc_smem(t.n_cols), st>>>(
-      *static_cast<const CUtensorMap*>(t.tmap), *static_cast<const CUtensorMap*>(rmaps[0]),
+      t.btab, *static_cast<const CUtensorMap*>(rmaps[0]),
       *static_cast<const CUtensorMap*>(rmaps[1]), P);
   return cudaGetLastError();
 }

@@ -106,7 +106,6 @@ struct RegionDev {
 // A tensor-core iCRT / finisher table on the device, with its TMA map.
 struct BigTcDev {
   DevBuf btab;
-  alignas(64) CUtensorMap tmap;
   BigTcTable t;
   int out_bit = 0, out_bits = 0;
 };
@@ -325,9 +324,7 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
   }
 }
 
-// 2-D TMA map of a u8 table [rows][inner] with boxes of box_inner x box_rows
-// and 64-byte swizzle (bigint_tc.cu's B operand). The driver entry point is
-// resolved through the runtime (no libcuda link).
+// cuTensorMapEncodeTiled, resolved through the runtime (no libcuda link).
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -340,19 +337,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   return encode;
-}
-
-void make_tmap_u8(CUtensorMap* m, const void* g, uint64_t inner, uint64_t rows, uint32_t box_inner,
-                  uint32_t box_rows) {
-  const auto encode = tmap_encoder();
-  const cuuint64_t dims[2] = {inner, rows};
-  const cuuint64_t strides[1] = {inner};
-  const cuuint32_t box[2] = {box_inner, box_rows};
-  const cuuint32_t es[2] = {1, 1};
-  const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(g), dims, strides,
-                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaFail(HEMUL_E_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
 // 2-D TMA map of a u32 residue array [rows][n], boxes of 128 residues x 16
@@ -373,11 +357,8 @@ std::unique_ptr<BigTcDev> upload_bigint(const BigTcHost& h, cudaStream_t st) {
   if (h.n_cols > 480 || bigint_tc_smem(h.n_cols) > size_t(kMaxDynSmem)) return nullptr;
   auto d = std::make_unique<BigTcDev>();
   upload(d->btab, h.btab, st);
-  make_tmap_u8(&d->tmap, d->btab.ptr, uint64_t(h.k_bytes), uint64_t(h.n_cols), 64,
-               uint32_t(h.n_cols / 2));
   BigTcTable& t = d->t;
   t.btab = d->btab.as<uint8_t>();
-  t.tmap = &d->tmap;
   t.n_cols = h.n_cols;
   t.k_bytes = h.k_bytes;
   t.k_slot = h.k_slot;

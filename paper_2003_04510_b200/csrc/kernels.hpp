@@ -216,14 +216,12 @@ struct BigTcSeg {
   int np = 0;
   int slot0 = 0;  // set from the table
 };
-// Constant GEMM operand (level_tables.cpp build_bigint_tc): btab [n_cols][k_bytes]
-// u8, column m <-> 2^(8 (m + m0)) of the window; segment s's row j occupies
-// K bytes 4 (slot0[s] + j) .. +3, the k quotients bytes 4 k_slot + 2 s, +1.
-// tmap: host pointer to the CUtensorMap of btab (box 64 x n_cols / 2, 64-byte
-// swizzle), built by the context.
+// Constant GEMM operand (level_tables.cpp build_bigint): B[m][K] u8, column
+// m <-> 2^(8 (m + m0)) of the window; segment s's row j occupies K bytes
+// 4 (slot0[s] + j) .. +3, the k quotients bytes 4 k_slot + 2 s, +1. Stored
+// chunk-major and pre-swizzled: btab = [k_bytes / 64][n_cols][64].
 struct BigTcTable {
   const uint8_t* btab = nullptr;
-  const void* tmap = nullptr;
   int n_cols = 0;   // multiple of 32, <= 480 (16-column TMEM reads past the end)
   int k_bytes = 0;  // multiple of 64
   int k_slot = 0;

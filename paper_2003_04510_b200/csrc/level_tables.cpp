@@ -471,6 +471,18 @@ BigTcHost build_bigint(const std::vector<std::vector<Nat>>& segs, int T, int bas
     }
   }
   for (int m = 0; m < t.n_cols; ++m) t.btab[size_t(m) * t.k_bytes + 4 * t.k_slot + 6] = nat_byte(round, m + m0);
+  // device layout: chunk-major blocks of n_cols x 64 K-bytes, each already in
+  // the 64-byte-swizzled K-major order the UMMA descriptor reads (16-byte
+  // piece q of row m at piece q ^ ((m >> 1) & 3)), so one linear bulk copy per
+  // chunk fills a pipeline stage (bigint_tc.cu)
+  std::vector<uint8_t> dev(t.btab.size());
+  const int nchunks = t.k_bytes / 64;
+  for (int c = 0; c < nchunks; ++c)
+    for (int m = 0; m < t.n_cols; ++m)
+      for (int kb = 0; kb < 64; ++kb)
+        dev[(size_t(c) * t.n_cols + m) * 64 + ((((kb >> 4) ^ ((m >> 1) & 3)) << 4) | (kb & 15))] =
+            t.btab[size_t(m) * t.k_bytes + 64 * c + kb];
+  t.btab.swap(dev);
   return t;
 }
 

@@ -114,7 +114,7 @@ struct BigTcHost {
   int slot0[3] = {0, 0, 0}, np[3] = {0, 0, 0};
   // output window (relative to base8); rounding constants are a table row
   int out_bit = 0, out_bits = 0;
-  std::vector<uint8_t> btab;  // [n_cols][k_bytes]
+  std::vector<uint8_t> btab;  // [k_bytes / 64][n_cols][64] (64-byte swizzled)
 };
 // iCRT of a split region 1 (d = c0 + 2^h c1 mod 2^log_q, exact from bit 0).
 BigTcHost build_icrt_tc(const RegionHost& r1);
