@@ -31,12 +31,19 @@
 //   warp 4      bulk copies of the B chunks (64 K-bytes x n_cols rows, stored
 //               chunk-major and pre-swizzled for the 64-byte UMMA layout)
 //   warp 5      MMA issue: 2 k-steps x 2 MMAs (N = n_cols / 2 each) per chunk
-//   warps 6-9   producers: cp.async of the t_j rows (6-stage private ring; the
+//   warp 14     TMA of the t_j rows (16 rows x 128 coefficients per chunk; the
 //               inverse NTT already scaled x_j by (P/p_j)^-1, context.cu
-//               ntt_inv to_t), fixed-point sum_j umulhi(t_j, 2^55 / p_j) for k,
-//               byte planes written MN-major (128-byte swizzle); the last
-//               chunk of a tile carries the k bytes
+//               ntt_inv to_t)
+//   warps 6-13  producers, one chunk each in turn (chunk q -> warp q mod 8, A
+//               stage q mod 8): the chunk is read into registers (the raw
+//               stage returns to the TMA warp at once), byte planes written
+//               MN-major (128-byte swizzle), fixed-point sum_j umulhi(t_j,
+//               2^55 / p_j) kept per warp and tile; the last chunk of a tile
+//               carries the k bytes, from the eight warps' posted partial sums
 //   warps 0-3   epilogue: TMEM columns -> 32-bit digits -> output limbs
+// A warp spends about eight chunk periods on its chunk, so the producers are
+// eight chunks apart rather than eight warps on one chunk: the per-chunk
+// latency (loads, proxy fence, barrier round trips) is paid in parallel.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -49,26 +56,27 @@ namespace hemul_gpu {
 
 namespace {
 
+
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
 constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
 constexpr int kSlots = kChunk / 4;   // row slots (4-byte residues) per chunk
 constexpr int kEpiWarps = 4;
 constexpr int kTmaWarp = 4, kMmaWarp = 5, kProd0 = 6, kProdWarps = 8;
 constexpr int kRawWarp = kProd0 + kProdWarps;  // TMA of the t rows
-constexpr int kProdRows = kSlots / kProdWarps;  // row slots per producer warp and chunk
 constexpr int kThreads = 32 * (kRawWarp + 1);
-constexpr int kSA = 3;               // A (byte plane) stages
-constexpr int kSB = 6;               // B (table) stages
-constexpr int kSR = 6;               // raw t stages (TMA, kRawWarp)
-constexpr int kLag = kSR - 1;        // producer prefetch distance in chunks
+constexpr int kSA = kProdWarps;      // A (byte plane) stages: one per producer warp
+constexpr int kSR = 8;               // raw t stages (>= kProdWarps: see the producers)
+constexpr int kMaxSB = 4;            // B (table) stages, 2 .. 4 by shared memory
 constexpr int kABytes = kChunk * kRows;          // 8 KB
 constexpr int kRawBytes = kSlots * kRows * 4;    // 8 KB
 constexpr int kMaxSeg = 3;
+constexpr int kXWords = 2 * kProdWarps * kMaxSeg * kRows;  // posted k partial sums
 
 struct Params {
   BigTcSeg seg[kMaxSeg];
   int nseg, B, entries, log_n;
   int n_cols, k_bytes, k_slot, rows_total;
+  int nsb;  // B stages
   BigTcOut o;
   uint32_t s8, s16, s24;  // 2^8, 2^16, 2^24 (arguments: kept as IMAD.WIDE)
 };
@@ -94,9 +102,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void producer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kProdWarps * 32) : "memory");
-}
 
 // MN-major, 128-byte swizzle A tile (M = 128): K row kk, bytes m .. m + 3
 __device__ __forceinline__ uint32_t a_off(uint32_t kk, uint32_t m) {
@@ -113,8 +118,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     bigint_tc_kernel(const uint8_t* __restrict__ btab, const __grid_constant__ CUtensorMap rmap0,
                      const __grid_constant__ CUtensorMap rmap1, Params P) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t a_full[kSA], a_empty[kSA], b_full[kSB], b_empty[kSB];
+  __shared__ __align__(8) uint64_t a_full[kSA], a_empty[kSA], b_full[kMaxSB], b_empty[kMaxSB];
   __shared__ __align__(8) uint64_t t_full[2], blk_free[3], r_full[kSR], r_empty[kSR];
+  __shared__ __align__(8) uint64_t f_done[2], f_free[2];
   __shared__ uint32_t tmem_base;
   // 1024-byte aligned by pointer arithmetic on the shared array (an integer
   // round trip would lose the state space: generic LD/ST instead of LDS/STS)
@@ -122,12 +128,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t n = size_t(1) << P.log_n;
   const int N = P.n_cols, NH = N / 2;
+  const int nsb = P.nsb;
   const uint32_t b_bytes = uint32_t(N) * kChunk;
-  uint8_t* sB = smem;                                  // kSB x [N][64] (SW64 K-major)
-  uint8_t* sA = sB + kSB * b_bytes;                    // kSA x [64 K][128 M] (SW128 MN-major)
+  uint8_t* sB = smem;                                  // nsb x [N][64] (SW64 K-major)
+  uint8_t* sA = sB + nsb * b_bytes;                    // kSA x [64 K][128 M] (SW128 MN-major)
   uint8_t* sR = sA + kSA * kABytes;                    // kSR x [16 rows][128] u32
-  uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);  // [4][3][128]
-  uint32_t* mu_tab = xbuf + kProdWarps * kMaxSeg * kRows;                // [rows]
+  uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);  // [2][8][3][128]
+  uint32_t* mu_tab = xbuf + kXWords;                   // [rows]
   const int C = P.k_bytes / kChunk;                    // chunks per tile (last: k bytes)
   const int tiles_per_entry = static_cast<int>(n / kRows);
   const int tiles = P.entries * tiles_per_entry;
@@ -136,18 +143,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSA; ++s) {
-      tc::mbar_init(&a_full[s], kProdWarps * 32);
+      tc::mbar_init(&a_full[s], 32);
       tc::mbar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < kSB; ++s) {
+    for (int s = 0; s < nsb; ++s) {
       tc::mbar_init(&b_full[s], 1);
       tc::mbar_init(&b_empty[s], 1);
     }
     for (int s = 0; s < kSR; ++s) {
       tc::mbar_init(&r_full[s], 1);
-      tc::mbar_init(&r_empty[s], kProdWarps);
+      tc::mbar_init(&r_empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) tc::mbar_init(&t_full[a], 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&t_full[a], 1);
+      tc::mbar_init(&f_done[a], kProdWarps * 32);
+      tc::mbar_init(&f_free[a], 32);
+    }
     for (int b = 0; b < 3; ++b) tc::mbar_init(&blk_free[b], kEpiWarps * 32);
     tc::mbar_fence_init();
   }
@@ -174,12 +185,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- B chunks: one linear bulk copy each (the table is stored chunk-
     // major and pre-swizzled, level_tables.cpp build_bigint) ---------------
     if (lane == 0) {
-      for (int q = 0, c = 0; q < total; ++q) {
-        const int s = q % kSB;
-        tc::mbar_wait(&b_empty[s], ((q / kSB) & 1) ^ 1);
+      for (int q = 0, c = 0, s = 0, ph = 0; q < total; ++q) {
+        tc::mbar_wait(&b_empty[s], ph ^ 1);
         mbar_expect_tx(&b_full[s], b_bytes);
         bulk_load(tc::smem_addr(sB + s * b_bytes), btab + size_t(c) * b_bytes, b_bytes, &b_full[s]);
         if (++c == C) c = 0;
+        if (++s == nsb) s = 0, ph ^= 1;
       }
     }
   } else if (warp == kRawWarp) {
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = tc::idesc_u8(kRows, NH, 1, 0);
       int uses[3] = {0, 0, 0};
       uint32_t dlo = 0, dhi = 0;
-      for (int q = 0, c = 0, it = 0; q < total; ++q) {
+      for (int q = 0, c = 0, it = 0, sb = 0, phb = 0; q < total; ++q) {
         if (c == 0) {  // a new tile: its two TMEM blocks must be drained
           const int bl = slot_lo(it), bh = slot_hi(it);
 #pragma unroll
@@ -219,12 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           dlo = tmem + bl * NH;
           dhi = tmem + bh * NH;
         }
-        tc::mbar_wait(&b_full[q % kSB], (q / kSB) & 1);
-        tc::mbar_wait(&a_full[q % kSA], (q / kSA) & 1);
-        tc::fence_async_smem();
+        const int sa = q % kSA;
+        tc::mbar_wait(&b_full[sb], phb);
+        tc::mbar_wait(&a_full[sa], (q / kSA) & 1);  // the producer fenced its stores
         tc::fence_after();
-        const uint32_t a0 = tc::smem_addr(sA + (q % kSA) * kABytes);
-        const uint32_t b0 = tc::smem_addr(sB + (q % kSB) * b_bytes);
+        const uint32_t a0 = tc::smem_addr(sA + sa * kABytes);
+        const uint32_t b0 = tc::smem_addr(sB + sb * b_bytes);
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           const uint64_t ad = tc::smem_desc(a0 + ks * 4096, 8192, 1024, tc::kSw128);
@@ -233,8 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mma_u8(dhi, ad, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
                      idesc, acc);
         }
-        tc::mma_commit(&b_empty[q % kSB]);
-        tc::mma_commit(&a_empty[q % kSA]);
+        tc::mma_commit(&b_empty[sb]);
+        tc::mma_commit(&a_empty[sa]);
+        if (++sb == nsb) sb = 0, phb ^= 1;
         if (++c == C) {
           tc::mma_commit(&t_full[it & 1]);
           c = 0;
@@ -243,86 +255,122 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kProd0) {
-    // ---- producers ---------------------------------------------------------
+    // ---- producers, one warp per chunk (chunk q -> warp q mod kProdWarps) ----
+    // lane: coefficients 4 lane .. 4 lane + 3, all 16 row slots of the chunk.
+    // Each warp sums umulhi(t_j, 2^55 / p_j) over its chunks of a tile; at the
+    // tile's end it posts the partial sums (xbuf[tile & 1][warp]) and the
+    // owner of the k chunk adds them up. Barrier phases: a warp's A stage is
+    // its own; a warp is at most kProdWarps raw chunks ahead of its previous
+    // one, so with kSR >= kProdWarps it never waits on a raw stage two phases
+    // ahead; the posting of tile t waits until tile t - 2's k chunk has read
+    // the buffer, so f_done / f_free never run two phases ahead either.
     const int pw = warp - kProd0;
-    const int slot_lo = kProdRows * pw;  // this warp's row slots of every chunk
-    const int pt = threadIdx.x - 32 * kProd0;  // 0 .. 32 kProdWarps - 1
-    // fixed point sum_j t_j / p_j 2^23 of the 4 coefficients per segment:
-    // umulhi(t_j, floor(2^55 / p_j)) per row (each term < 2^23, low by < 1;
-    // <= 511 rows per segment keep the sum below 2^32)
     uint32_t F[kMaxSeg][4];
 #pragma unroll
-    for (int s = 0; s < kMaxSeg; ++s)
+    for (int sg = 0; sg < kMaxSeg; ++sg)
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) F[s][c4] = 0;
+      for (int c4 = 0; c4 < 4; ++c4) F[sg][c4] = 0;
     const int sl1 = P.seg[1].slot0, sl2 = P.seg[2].slot0;
     const int np0 = P.seg[0].np, np1 = P.seg[1].np, np2 = P.seg[2].np;
-    for (int q = 0, c = 0, qr = 0; q < total; ++q) {
-      const int sa = q % kSA;
-      tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
-      uint8_t* A = sA + sa * kABytes;
-      if (c != C - 1) {
+    // chunks of tile tl handled by this warp: c = (pw - tl C) mod kProdWarps, step kProdWarps
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int q0 = tl * C;
+      int c = pw - q0 % kProdWarps;
+      if (c < 0) c += kProdWarps;
+      for (; c < C - 1; c += kProdWarps) {
+        const int q = q0 + c;
+        const int sa = q % kSA;
+        tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
+        uint8_t* A = sA + sa * kABytes;
+        const int qr = tl * (C - 1) + c;
         const int r = qr % kSR;
         tc::mbar_wait_sleep<32>(&r_full[r], (qr / kSR) & 1);
-        const uint8_t* R = sR + r * kRawBytes + slot_lo * kRows * 4 + 16 * lane;
-        const int g0 = kSlots * c + slot_lo;
-        const int s = (g0 >= sl1) + (g0 >= sl2);  // one segment per chunk (warp-uniform)
-        const int j0 = g0 - (s == 2 ? sl2 : s == 1 ? sl1 : 0);
-        const int npn = s == 2 ? np2 : s == 1 ? np1 : np0;
+        const uint8_t* R = sR + r * kRawBytes + 16 * lane;
+        const int g0 = kSlots * c;
+        const int sg = (g0 >= sl1) + (g0 >= sl2);  // one segment per chunk
+        const int j0 = g0 - (sg == 2 ? sl2 : sg == 1 ? sl1 : 0);
+        const int npn = sg == 2 ? np2 : sg == 1 ? np1 : np0;
+        const int nrows = min(kSlots, npn - j0);  // padding rows have zero B rows
+        // read the whole chunk first so the raw stage goes back to the TMA
+        // warp at once (a warp spends ~kProdWarps chunk periods on its chunk)
+        uint4 x[kSlots];
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i)
+          x[i] = i < nrows ? *reinterpret_cast<const uint4*>(R + i * kRows * 4) : make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&r_empty[r]);
         uint32_t f[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < kProdRows; ++i) {
-          if (j0 + i < npn) {  // warp-uniform (padding rows have zero B rows)
-            // t_j of 4 coefficients (the inverse NTT folded (P/p_j)^-1 in)
-            const uint4 x = *reinterpret_cast<const uint4*>(R + i * kRows * 4);
-            const uint32_t t0 = x.x, t1 = x.y, t2 = x.z, t3 = x.w;
+        for (int i = 0; i < kSlots; ++i) {
+          if (i < nrows) {
             const uint32_t mu = mu_tab[g0 + i];
-            f[0] += __umulhi(t0, mu);
-            f[1] += __umulhi(t1, mu);
-            f[2] += __umulhi(t2, mu);
-            f[3] += __umulhi(t3, mu);
-            // byte planes of the 4 coefficients (K rows 4 slot + b)
-            const uint32_t lo01 = __byte_perm(t0, t1, 0x5140), lo23 = __byte_perm(t2, t3, 0x5140);
-            const uint32_t hi01 = __byte_perm(t0, t1, 0x7362), hi23 = __byte_perm(t2, t3, 0x7362);
-            const uint32_t kk = 4 * (slot_lo + i);
+            f[0] += __umulhi(x[i].x, mu);
+            f[1] += __umulhi(x[i].y, mu);
+            f[2] += __umulhi(x[i].z, mu);
+            f[3] += __umulhi(x[i].w, mu);
+            const uint32_t lo01 = __byte_perm(x[i].x, x[i].y, 0x5140), lo23 = __byte_perm(x[i].z, x[i].w, 0x5140);
+            const uint32_t hi01 = __byte_perm(x[i].x, x[i].y, 0x7362), hi23 = __byte_perm(x[i].z, x[i].w, 0x7362);
+            const uint32_t kk = 4 * i;
             *reinterpret_cast<uint32_t*>(A + a_off(kk, 4 * lane)) = __byte_perm(lo01, lo23, 0x5410);
             *reinterpret_cast<uint32_t*>(A + a_off(kk + 1, 4 * lane)) = __byte_perm(lo01, lo23, 0x7632);
             *reinterpret_cast<uint32_t*>(A + a_off(kk + 2, 4 * lane)) = __byte_perm(hi01, hi23, 0x5410);
             *reinterpret_cast<uint32_t*>(A + a_off(kk + 3, 4 * lane)) = __byte_perm(hi01, hi23, 0x7632);
           }
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&r_empty[r]);  // this warp's rows are read
-        ++qr;
 #pragma unroll
         for (int ss = 0; ss < kMaxSeg; ++ss)
-          if (ss == s)
+          if (ss == sg)
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) F[ss][c4] += f[c4];
-      } else {
-        // k chunk: k_s = round(sum_j t_j / p_j) per segment, bytes 2 s, 2 s + 1
+        tc::fence_async_smem();
+        tc::mbar_arrive(&a_full[sa]);
+      }
+      // post this tile's partial k sums (buffer tl & 1 is free once the k
+      // chunk of tile tl - 2 has read it)
+      const int xb = tl & 1;
+      if (tl >= 2) tc::mbar_wait_sleep<32>(&f_free[xb], ((tl >> 1) - 1) & 1);
 #pragma unroll
-        for (int s = 0; s < kMaxSeg; ++s)
+      for (int sg = 0; sg < kMaxSeg; ++sg)
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          xbuf[((xb * kProdWarps + pw) * kMaxSeg + sg) * kRows + 4 * lane + c4] = F[sg][c4];
+          F[sg][c4] = 0;
+        }
+      tc::mbar_arrive(&f_done[xb]);
+      if (c == C - 1) {
+        // k chunk: k_s = round(sum_j t_j / p_j) from every warp's partial sums
+        const int q = q0 + c;
+        const int sa = q % kSA;
+        tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
+        uint8_t* A = sA + sa * kABytes;
+        tc::mbar_wait_sleep<32>(&f_done[xb], (tl >> 1) & 1);
+        uint32_t kb[kMaxSeg][4];
+#pragma unroll
+        for (int sg = 0; sg < kMaxSeg; ++sg)
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
-            xbuf[(pw * kMaxSeg + s) * kRows + 4 * lane + c4] = F[s][c4];
-            F[s][c4] = 0;
-          }
-        producer_sync();
-        for (int s = 0; s < P.nseg && pt < kRows; ++s) {
-          uint32_t tot = 0;
+            uint32_t tot = 0;
 #pragma unroll
-          for (int w = 0; w < kProdWarps; ++w) tot += xbuf[(w * kMaxSeg + s) * kRows + pt];
-          const uint32_t k = (tot + (1u << 22)) >> 23;
-          A[a_off(2 * s, pt)] = static_cast<uint8_t>(k);
-          A[a_off(2 * s + 1, pt)] = static_cast<uint8_t>(k >> 8);
+            for (int w = 0; w < kProdWarps; ++w)
+              tot += xbuf[((xb * kProdWarps + w) * kMaxSeg + sg) * kRows + 4 * lane + c4];
+            kb[sg][c4] = (tot + (1u << 22)) >> 23;
+          }
+        tc::mbar_arrive(&f_free[xb]);
+#pragma unroll
+        for (int sg = 0; sg < kMaxSeg; ++sg) {
+          if (sg < P.nseg) {
+            const uint32_t lo = (kb[sg][0] & 0xff) | (kb[sg][1] & 0xff) << 8 |
+                                (kb[sg][2] & 0xff) << 16 | kb[sg][3] << 24;
+            const uint32_t hi = (kb[sg][0] >> 8) | (kb[sg][1] >> 8) << 8 |
+                                (kb[sg][2] >> 8) << 16 | (kb[sg][3] >> 8) << 24;
+            *reinterpret_cast<uint32_t*>(A + a_off(2 * sg, 4 * lane)) = lo;
+            *reinterpret_cast<uint32_t*>(A + a_off(2 * sg + 1, 4 * lane)) = hi;
+          }
         }
-        if (pt < kRows) A[a_off(6, pt)] = 1;  // constant row: the window's rounding constants
-        producer_sync();
+        *reinterpret_cast<uint32_t*>(A + a_off(6, 4 * lane)) = 0x01010101u;  // constant row
+        tc::fence_async_smem();
+        tc::mbar_arrive(&a_full[sa]);
       }
-      tc::fence_async_smem();
-      tc::mbar_arrive(&a_full[sa]);
-      if (++c == C) c = 0;
     }
   } else {
     // ---- epilogue: lane = coefficient i0 + 32 warp + lane -----------------------
@@ -432,10 +480,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 constexpr int kMaxRows = 1024;  // A rows (residues) per coefficient
 
-size_t bigint_tc_smem(int n_cols) {
-  return size_t(kSB) * n_cols * kChunk + size_t(kSA) * kABytes + size_t(kSR) * kRawBytes +
-         size_t(kProdWarps) * kMaxSeg * kRows * 4 + kMaxRows * 4 + 1024;
+namespace {
+size_t smem_for(int n_cols, int nsb) {
+  return size_t(nsb) * n_cols * kChunk + size_t(kSA) * kABytes + size_t(kSR) * kRawBytes +
+         size_t(kXWords) * 4 + kMaxRows * 4 + 1024;
 }
+// B stages: as many as fit (2 .. kMaxSB)
+int b_stages(int n_cols) {
+  int nsb = kMaxSB;
+  while (nsb > 2 && smem_for(n_cols, nsb) > size_t(kMaxDynSmem)) --nsb;
+  return nsb;
+}
+}  // namespace
+
+size_t bigint_tc_smem(int n_cols) { return smem_for(n_cols, b_stages(n_cols)); }
 
 cudaError_t bigint_tc_setup_attributes() {
   return cudaFuncSetAttribute(bigint_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -467,6 +525,7 @@ cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, in
   P.entries = entries;
   P.log_n = log_n;
   P.n_cols = t.n_cols;
+  P.nsb = b_stages(t.n_cols);
   P.k_bytes = t.k_bytes;
   P.k_slot = t.k_slot;
   P.rows_total = t.slot0[t.nseg - 1] + t.np[t.nseg - 1];  // real rows; padding up to k_slot
