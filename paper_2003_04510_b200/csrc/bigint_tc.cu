@@ -18,32 +18,37 @@
 // V_row = sum_e v_{row,e} 2^(8e),
 //   D[i][m] = sum_{row,b} a_{row,b}(i) * v_{row, m + m0 - b}      (u8 x u8 -> s32)
 //   V = sum_m D[i][m] 2^(8 (m + m0))
-// i.e. a GEMM of the coefficients' byte planes (A, M = 128 coefficients,
-// K = 4 bytes per row) against a constant table B[m][K] of shifted row bytes
-// (level_tables.cpp build_bigint_tc). D < K 2^16 < 2^27 is exact in s32; the
+// i.e. a GEMM of the coefficients' bytes (A, M = 128 coefficients, K = 4
+// bytes per row) against a constant table B[m][K] of shifted row bytes
+// (level_tables.cpp build_bigint). The A operand lives in TMEM (the .kind::i8
+// "TS" form): TMEM lane = coefficient, column = 4 K-bytes, so a residue t_j
+// stored as one 32-bit column IS its four K-bytes; no byte transposition and
+// no shared-memory traffic for A. D < K 2^16 < 2^27 is exact in s32; the
 // epilogue carries the columns into 32-bit digits and extracts the output
 // window. Columns below m0 (the finisher's bits under logQ - 125) are
 // dropped: the truncation error is < 2^(8 m0 + 19), far below the 64 guard
 // bits the ambiguity check inspects, exactly as in the IMAD finisher
 // (kernels.hpp Finisher).
 //
-// Persistent warp-specialised CTA (one per SM, 512 TMEM columns):
+// Persistent warp-specialised CTA (one per SM, 512 TMEM columns: 3 x N/2
+// accumulator columns, 2 x 16 A columns):
 //   warp 4      bulk copies of the B chunks (64 K-bytes x n_cols rows, stored
 //               chunk-major and pre-swizzled for the 64-byte UMMA layout)
-//   warp 5      MMA issue: 2 k-steps x 2 MMAs (N = n_cols / 2 each) per chunk
+//   warp 5      MMA issue: 2 k-steps x 2 MMAs (N = n_cols / 2 each) per chunk,
+//               A from TMEM
 //   warp 14     TMA of the t_j rows (16 rows x 128 coefficients per chunk; the
 //               inverse NTT already scaled x_j by (P/p_j)^-1, context.cu
 //               ntt_inv to_t)
-//   warps 6-13  producers, one chunk each in turn (chunk q -> warp q mod 8, A
-//               stage q mod 8): the chunk is read into registers (the raw
-//               stage returns to the TMA warp at once), byte planes written
-//               MN-major (128-byte swizzle), fixed-point sum_j umulhi(t_j,
-//               2^55 / p_j) kept per warp and tile; the last chunk of a tile
-//               carries the k bytes, from the eight warps' posted partial sums
+//   warps 6-13  producers, two quads of four warps (one per TMEM lane
+//               quadrant): quad q mod 2 takes chunk q into TMEM A stage q mod 2
+//               (16 LDS + one 16-column tcgen05.st per thread) and keeps the
+//               fixed-point sum_j umulhi(t_j, 2^55 / p_j) of its coefficient;
+//               the last chunk of a tile carries the k bytes, from both quads'
+//               posted partial sums
 //   warps 0-3   epilogue: TMEM columns -> 32-bit digits -> output limbs
-// A warp spends about eight chunk periods on its chunk, so the producers are
-// eight chunks apart rather than eight warps on one chunk: the per-chunk
-// latency (loads, proxy fence, barrier round trips) is paid in parallel.
+// Shared-memory traffic per chunk: the B chunk (written once, read once) and
+// the t rows (TMA write, one LDS pass): 56 KB instead of 80 KB with a
+// byte-plane A operand in shared memory.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -56,7 +61,6 @@ namespace hemul_gpu {
 
 namespace {
 
-
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
 constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
 constexpr int kSlots = kChunk / 4;   // row slots (4-byte residues) per chunk
@@ -64,13 +68,12 @@ constexpr int kEpiWarps = 4;
 constexpr int kTmaWarp = 4, kMmaWarp = 5, kProd0 = 6, kProdWarps = 8;
 constexpr int kRawWarp = kProd0 + kProdWarps;  // TMA of the t rows
 constexpr int kThreads = 32 * (kRawWarp + 1);
-constexpr int kSA = kProdWarps;      // A (byte plane) stages: one per producer warp
-constexpr int kSR = 8;               // raw t stages (>= kProdWarps: see the producers)
+constexpr int kSR = 8;               // raw t stages
 constexpr int kMaxSB = 4;            // B (table) stages, 2 .. 4 by shared memory
-constexpr int kABytes = kChunk * kRows;          // 8 KB
 constexpr int kRawBytes = kSlots * kRows * 4;    // 8 KB
 constexpr int kMaxSeg = 3;
-constexpr int kXWords = 2 * kProdWarps * kMaxSeg * kRows;  // posted k partial sums
+constexpr int kACol = 512 - 2 * kSlots;          // TMEM A stages: columns 480 .. 511
+constexpr int kXWords = 2 * 2 * kMaxSeg * kRows; // posted k partial sums [tile&1][quad][seg][i]
 
 struct Params {
   BigTcSeg seg[kMaxSeg];
@@ -102,10 +105,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-
-// MN-major, 128-byte swizzle A tile (M = 128): K row kk, bytes m .. m + 3
-__device__ __forceinline__ uint32_t a_off(uint32_t kk, uint32_t m) {
-  return (kk >> 3) * 1024 + (kk & 7) * 128 + ((((m >> 4) ^ kk) & 7) << 4) + (m & 15);
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t a, uint32_t b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b)
+               : "memory");
 }
 
 // row (in the segment's tensor map) of residue row j of entry e
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bigint_tc_kernel(const uint8_t* __restrict__ btab, const __grid_constant__ CUtensorMap rmap0,
                      const __grid_constant__ CUtensorMap rmap1, Params P) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t a_full[kSA], a_empty[kSA], b_full[kMaxSB], b_empty[kMaxSB];
+  __shared__ __align__(8) uint64_t a_full[2], a_empty[2], b_full[kMaxSB], b_empty[kMaxSB];
   __shared__ __align__(8) uint64_t t_full[2], blk_free[3], r_full[kSR], r_empty[kSR];
   __shared__ __align__(8) uint64_t f_done[2], f_free[2];
   __shared__ uint32_t tmem_base;
@@ -131,10 +133,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nsb = P.nsb;
   const uint32_t b_bytes = uint32_t(N) * kChunk;
   uint8_t* sB = smem;                                  // nsb x [N][64] (SW64 K-major)
-  uint8_t* sA = sB + nsb * b_bytes;                    // kSA x [64 K][128 M] (SW128 MN-major)
-  uint8_t* sR = sA + kSA * kABytes;                    // kSR x [16 rows][128] u32
-  uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);  // [2][8][3][128]
-  uint32_t* mu_tab = xbuf + kXWords;                   // [rows]
+  uint8_t* sR = sB + nsb * b_bytes;                    // kSR x [16 rows][128] u32
+  uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);
+  uint32_t* mu_tab = xbuf + kXWords;                   // [k_slot]
   const int C = P.k_bytes / kChunk;                    // chunks per tile (last: k bytes)
   const int tiles_per_entry = static_cast<int>(n / kRows);
   const int tiles = P.entries * tiles_per_entry;
@@ -142,9 +143,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total = my_tiles * C;                      // this CTA's chunk sequence
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSA; ++s) {
-      tc::mbar_init(&a_full[s], 32);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&a_full[s], kProdWarps / 2 * 32);
       tc::mbar_init(&a_empty[s], 1);
+      tc::mbar_init(&t_full[s], 1);
+      tc::mbar_init(&f_done[s], kProdWarps * 32);
+      tc::mbar_init(&f_free[s], kProdWarps / 2 * 32);
     }
     for (int s = 0; s < nsb; ++s) {
       tc::mbar_init(&b_full[s], 1);
@@ -152,21 +156,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kSR; ++s) {
       tc::mbar_init(&r_full[s], 1);
-      tc::mbar_init(&r_empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      tc::mbar_init(&t_full[a], 1);
-      tc::mbar_init(&f_done[a], kProdWarps * 32);
-      tc::mbar_init(&f_free[a], 32);
+      tc::mbar_init(&r_empty[s], kProdWarps / 2);
     }
     for (int b = 0; b < 3; ++b) tc::mbar_init(&blk_free[b], kEpiWarps * 32);
     tc::mbar_fence_init();
   }
-  // floor(2^55 / p) of every A row (the fixed-point k quotient)
-  for (int g = threadIdx.x; g < P.rows_total; g += kThreads) {
+  // floor(2^55 / p) of every A row slot (the fixed-point k quotient; 0 for
+  // padding slots, whose t values are whatever the TMA box held)
+  for (int g = threadIdx.x; g < P.k_slot; g += kThreads) {
     const int s = (g >= P.seg[1].slot0) + (g >= P.seg[2].slot0);
     const int j = g - P.seg[s].slot0;
-    mu_tab[g] = j < P.seg[s].np ? P.seg[s].primes[j].pad[0] : 0u;  // 0: padding row
+    mu_tab[g] = j < P.seg[s].np ? P.seg[s].primes[j].pad[0] : 0u;
   }
   if (warp == kTmaWarp) tc::tmem_alloc<512>(&tmem_base);
   tc::fence_before();
@@ -174,10 +174,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_after();
   const uint32_t tmem = tmem_base;
   // TMEM: the accumulator is two column blocks of NH (low / high columns).
-  // With 3 NH <= 512 the blocks rotate through three slots, tile t using
+  // With 3 NH <= 480 the blocks rotate through three slots, tile t using
   // slots (2t mod 3, 2t+1 mod 3): the MMAs of tile t+1 need only the low
   // block of tile t, which the epilogue releases half way through.
-  const int nslots = 3 * NH <= 512 ? 3 : 2;
+  const int nslots = 3 * NH <= kACol ? 3 : 2;
   auto slot_lo = [&](int t) { return nslots == 3 ? (2 * t) % 3 : 0; };
   auto slot_hi = [&](int t) { return nslots == 3 ? (2 * t + 1) % 3 : 1; };
 
@@ -215,9 +215,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    // ---- MMA issue -------------------------------------------------------
+    // ---- MMA issue (A: TMEM stage q mod 2, B: shared memory) --------------
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_u8(kRows, NH, 1, 0);
+      const uint32_t idesc = tc::idesc_u8(kRows, NH, 0, 0);
       int uses[3] = {0, 0, 0};
       uint32_t dlo = 0, dhi = 0;
       for (int q = 0, c = 0, it = 0, sb = 0, phb = 0; q < total; ++q) {
@@ -230,19 +230,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           dlo = tmem + bl * NH;
           dhi = tmem + bh * NH;
         }
-        const int sa = q % kSA;
+        const int sa = q & 1;
         tc::mbar_wait(&b_full[sb], phb);
-        tc::mbar_wait(&a_full[sa], (q / kSA) & 1);  // the producer fenced its stores
+        tc::mbar_wait(&a_full[sa], (q >> 1) & 1);
         tc::fence_after();
-        const uint32_t a0 = tc::smem_addr(sA + sa * kABytes);
         const uint32_t b0 = tc::smem_addr(sB + sb * b_bytes);
+        const uint32_t a0 = tmem + kACol + sa * kSlots;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          const uint64_t ad = tc::smem_desc(a0 + ks * 4096, 8192, 1024, tc::kSw128);
           const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
-          tc::mma_u8(dlo, ad, tc::smem_desc(b0 + ks * 32, 16, 512, tc::kSw64), idesc, acc);
-          tc::mma_u8(dhi, ad, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
-                     idesc, acc);
+          tc::mma_u8_ts(dlo, a0 + ks * 8, tc::smem_desc(b0 + ks * 32, 16, 512, tc::kSw64), idesc, acc);
+          tc::mma_u8_ts(dhi, a0 + ks * 8, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
+                        idesc, acc);
         }
         tc::mma_commit(&b_empty[sb]);
         tc::mma_commit(&a_empty[sa]);
@@ -255,121 +254,74 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kProd0) {
-    // ---- producers, one warp per chunk (chunk q -> warp q mod kProdWarps) ----
-    // lane: coefficients 4 lane .. 4 lane + 3, all 16 row slots of the chunk.
-    // Each warp sums umulhi(t_j, 2^55 / p_j) over its chunks of a tile; at the
-    // tile's end it posts the partial sums (xbuf[tile & 1][warp]) and the
-    // owner of the k chunk adds them up. Barrier phases: a warp's A stage is
-    // its own; a warp is at most kProdWarps raw chunks ahead of its previous
-    // one, so with kSR >= kProdWarps it never waits on a raw stage two phases
-    // ahead; the posting of tile t waits until tile t - 2's k chunk has read
-    // the buffer, so f_done / f_free never run two phases ahead either.
-    const int pw = warp - kProd0;
-    uint32_t F[kMaxSeg][4];
-#pragma unroll
-    for (int sg = 0; sg < kMaxSeg; ++sg)
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) F[sg][c4] = 0;
+    // ---- producers: quad (warp - kProd0) / 4 takes the chunks q with
+    // q mod 2 == quad into TMEM A stage quad; the warp writes the lanes of its
+    // quadrant (warp mod 4), one coefficient per thread. Barrier phases: a
+    // stage belongs to one quad; a quad's raw chunks are at most 3 apart
+    // (< kSR), and tile t's partial sums are posted only after tile t - 2's
+    // k chunk has read the buffer, so no wait can alias two phases ahead.
+    const int quad = (warp - kProd0) >> 2, lq = warp & 3;
+    const int ci = 32 * lq + lane;
+    const uint32_t a_st = tmem + kACol + quad * kSlots + (uint32_t(32 * lq) << 16);
     const int sl1 = P.seg[1].slot0, sl2 = P.seg[2].slot0;
-    const int np0 = P.seg[0].np, np1 = P.seg[1].np, np2 = P.seg[2].np;
-    // chunks of tile tl handled by this warp: c = (pw - tl C) mod kProdWarps, step kProdWarps
     for (int tl = 0; tl < my_tiles; ++tl) {
       const int q0 = tl * C;
-      int c = pw - q0 % kProdWarps;
-      if (c < 0) c += kProdWarps;
-      for (; c < C - 1; c += kProdWarps) {
+      int c = (quad - q0) & 1;  // (q0 + c) mod 2 == quad
+      uint32_t F0 = 0, F1 = 0, F2 = 0;
+      for (; c < C - 1; c += 2) {
         const int q = q0 + c;
-        const int sa = q % kSA;
-        tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
-        uint8_t* A = sA + sa * kABytes;
         const int qr = tl * (C - 1) + c;
         const int r = qr % kSR;
         tc::mbar_wait_sleep<32>(&r_full[r], (qr / kSR) & 1);
-        const uint8_t* R = sR + r * kRawBytes + 16 * lane;
+        const uint32_t* R = reinterpret_cast<const uint32_t*>(sR + r * kRawBytes) + ci;
         const int g0 = kSlots * c;
-        const int sg = (g0 >= sl1) + (g0 >= sl2);  // one segment per chunk
-        const int j0 = g0 - (sg == 2 ? sl2 : sg == 1 ? sl1 : 0);
-        const int npn = sg == 2 ? np2 : sg == 1 ? np1 : np0;
-        const int nrows = min(kSlots, npn - j0);  // padding rows have zero B rows
-        // read the whole chunk first so the raw stage goes back to the TMA
-        // warp at once (a warp spends ~kProdWarps chunk periods on its chunk)
-        uint4 x[kSlots];
+        uint32_t t[kSlots];
 #pragma unroll
-        for (int i = 0; i < kSlots; ++i)
-          x[i] = i < nrows ? *reinterpret_cast<const uint4*>(R + i * kRows * 4) : make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < kSlots; ++i) t[i] = R[i * kRows];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&r_empty[r]);
-        uint32_t f[4] = {0, 0, 0, 0};
+        uint32_t f = 0;
 #pragma unroll
-        for (int i = 0; i < kSlots; ++i) {
-          if (i < nrows) {
-            const uint32_t mu = mu_tab[g0 + i];
-            f[0] += __umulhi(x[i].x, mu);
-            f[1] += __umulhi(x[i].y, mu);
-            f[2] += __umulhi(x[i].z, mu);
-            f[3] += __umulhi(x[i].w, mu);
-            const uint32_t lo01 = __byte_perm(x[i].x, x[i].y, 0x5140), lo23 = __byte_perm(x[i].z, x[i].w, 0x5140);
-            const uint32_t hi01 = __byte_perm(x[i].x, x[i].y, 0x7362), hi23 = __byte_perm(x[i].z, x[i].w, 0x7362);
-            const uint32_t kk = 4 * i;
-            *reinterpret_cast<uint32_t*>(A + a_off(kk, 4 * lane)) = __byte_perm(lo01, lo23, 0x5410);
-            *reinterpret_cast<uint32_t*>(A + a_off(kk + 1, 4 * lane)) = __byte_perm(lo01, lo23, 0x7632);
-            *reinterpret_cast<uint32_t*>(A + a_off(kk + 2, 4 * lane)) = __byte_perm(hi01, hi23, 0x5410);
-            *reinterpret_cast<uint32_t*>(A + a_off(kk + 3, 4 * lane)) = __byte_perm(hi01, hi23, 0x7632);
-          }
-        }
-#pragma unroll
-        for (int ss = 0; ss < kMaxSeg; ++ss)
-          if (ss == sg)
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) F[ss][c4] += f[c4];
-        tc::fence_async_smem();
-        tc::mbar_arrive(&a_full[sa]);
+        for (int i = 0; i < kSlots; ++i) f += __umulhi(t[i], mu_tab[g0 + i]);
+        const int sg = (g0 >= sl1) + (g0 >= sl2);  // one segment per chunk
+        F0 += sg == 0 ? f : 0u;
+        F1 += sg == 1 ? f : 0u;
+        F2 += sg == 2 ? f : 0u;
+        tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
+        tc::fence_after();
+        tc::tmem_st16(a_st, t);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        tc::mbar_arrive(&a_full[quad]);
       }
       // post this tile's partial k sums (buffer tl & 1 is free once the k
       // chunk of tile tl - 2 has read it)
       const int xb = tl & 1;
+      uint32_t* X = xbuf + (xb * 2 + quad) * kMaxSeg * kRows + ci;
       if (tl >= 2) tc::mbar_wait_sleep<32>(&f_free[xb], ((tl >> 1) - 1) & 1);
-#pragma unroll
-      for (int sg = 0; sg < kMaxSeg; ++sg)
-#pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          xbuf[((xb * kProdWarps + pw) * kMaxSeg + sg) * kRows + 4 * lane + c4] = F[sg][c4];
-          F[sg][c4] = 0;
-        }
+      X[0] = F0;
+      X[kRows] = F1;
+      X[2 * kRows] = F2;
       tc::mbar_arrive(&f_done[xb]);
       if (c == C - 1) {
-        // k chunk: k_s = round(sum_j t_j / p_j) from every warp's partial sums
+        // k chunk: k_s = round(sum_j t_j / p_j) from both quads' partial sums
         const int q = q0 + c;
-        const int sa = q % kSA;
-        tc::mbar_wait_sleep<32>(&a_empty[sa], ((q / kSA) & 1) ^ 1);
-        uint8_t* A = sA + sa * kABytes;
-        tc::mbar_wait_sleep<32>(&f_done[xb], (tl >> 1) & 1);
-        uint32_t kb[kMaxSeg][4];
-#pragma unroll
-        for (int sg = 0; sg < kMaxSeg; ++sg)
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            uint32_t tot = 0;
-#pragma unroll
-            for (int w = 0; w < kProdWarps; ++w)
-              tot += xbuf[((xb * kProdWarps + w) * kMaxSeg + sg) * kRows + 4 * lane + c4];
-            kb[sg][c4] = (tot + (1u << 22)) >> 23;
-          }
-        tc::mbar_arrive(&f_free[xb]);
+        tc::mbar_wait(&f_done[xb], (tl >> 1) & 1);
+        const uint32_t* Y = xbuf + xb * 2 * kMaxSeg * kRows + ci;
+        uint32_t k[kMaxSeg];
 #pragma unroll
         for (int sg = 0; sg < kMaxSeg; ++sg) {
-          if (sg < P.nseg) {
-            const uint32_t lo = (kb[sg][0] & 0xff) | (kb[sg][1] & 0xff) << 8 |
-                                (kb[sg][2] & 0xff) << 16 | kb[sg][3] << 24;
-            const uint32_t hi = (kb[sg][0] >> 8) | (kb[sg][1] >> 8) << 8 |
-                                (kb[sg][2] >> 8) << 16 | (kb[sg][3] >> 8) << 24;
-            *reinterpret_cast<uint32_t*>(A + a_off(2 * sg, 4 * lane)) = lo;
-            *reinterpret_cast<uint32_t*>(A + a_off(2 * sg + 1, 4 * lane)) = hi;
-          }
+          const uint32_t tot = Y[sg * kRows] + Y[(kMaxSeg + sg) * kRows];
+          k[sg] = sg < P.nseg ? (tot + (1u << 22)) >> 23 : 0u;
         }
-        *reinterpret_cast<uint32_t*>(A + a_off(6, 4 * lane)) = 0x01010101u;  // constant row
-        tc::fence_async_smem();
-        tc::mbar_arrive(&a_full[sa]);
+        tc::mbar_arrive(&f_free[xb]);
+        tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
+        tc::fence_after();
+        // K bytes 2s, 2s+1 = k_s (< 2^16), byte 6 = 1 (the constant row)
+        tmem_st2(a_st, k[0] | k[1] << 16, k[2] | 1u << 16);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        tc::mbar_arrive(&a_full[quad]);
       }
     }
   } else {
@@ -482,8 +434,8 @@ constexpr int kMaxRows = 1024;  // A rows (residues) per coefficient
 
 namespace {
 size_t smem_for(int n_cols, int nsb) {
-  return size_t(nsb) * n_cols * kChunk + size_t(kSA) * kABytes + size_t(kSR) * kRawBytes +
-         size_t(kXWords) * 4 + kMaxRows * 4 + 1024;
+  return size_t(nsb) * n_cols * kChunk + size_t(kSR) * kRawBytes + size_t(kXWords) * 4 +
+         kMaxRows * 4 + 1024;
 }
 // B stages: as many as fit (2 .. kMaxSB)
 int b_stages(int n_cols) {
