@@ -231,8 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           dhi = tmem + bh * NH;
         }
         const int sa = q & 1;
-        tc::mbar_wait(&b_full[sb], phb);
-        tc::mbar_wait(&a_full[sa], (q >> 1) & 1);
+        tc::mbar_wait(&a_full[sa], (q >> 1) & 1);  // the producers saw b_full too
         tc::fence_after();
         const uint32_t b0 = tc::smem_addr(sB + sb * b_bytes);
         const uint32_t a0 = tmem + kACol + sa * kSlots;
@@ -288,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         F1 += sg == 1 ? f : 0u;
         F2 += sg == 2 ? f : 0u;
         tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
+        tc::mbar_wait_sleep<32>(&b_full[q % nsb], (q / nsb) & 1);
         tc::fence_after();
         tc::tmem_st16(a_st, t);
         tc::tmem_wait_st();
@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::mbar_arrive(&f_free[xb]);
         tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
+        tc::mbar_wait_sleep<32>(&b_full[q % nsb], (q / nsb) & 1);
         tc::fence_after();
         // K bytes 2s, 2s+1 = k_s (< 2^16), byte 6 = 1 (the constant row)
         tmem_st2(a_st, k[0] | k[1] << 16, k[2] | 1u << 16);

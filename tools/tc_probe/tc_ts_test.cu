@@ -191,6 +191,8 @@ __global__ void ring_rate(int chunks, int N, int mode, const uint8_t* __restrict
     tc::mbar_init(&bar[1], 1);
     for (int i = 0; i < 4; ++i) tc::mbar_init(&cbar[i], 1);
     tc::mbar_fence_init();
+    tc::mbar_arrive(&cbar[0]);
+    tc::mbar_arrive(&cbar[1]);
     done = 0;
   }
   if (threadIdx.x < 32) tc::tmem_alloc<512>(&tmem_base);
@@ -205,6 +207,11 @@ __global__ void ring_rate(int chunks, int N, int mode, const uint8_t* __restrict
     const uint32_t idesc = tc::idesc_u8(128, N, 1, 0);
     int sa_i = 0, sb_i = 0;
     for (int c = 0; c < chunks; ++c) {
+      if (mode & 8) {  // the finisher's per-chunk barrier waits (already complete)
+        tc::mbar_wait(&cbar[0], 0);
+        tc::mbar_wait(&cbar[1], 0);
+        tc::fence_after();
+      }
       const uint32_t ab = a0 + sa_i * 8192, bb = b0 + sb_i * b_bytes;
       const uint32_t d = tbase + ((c / 29) & 1) * N;
 #pragma unroll
@@ -215,8 +222,8 @@ __global__ void ring_rate(int chunks, int N, int mode, const uint8_t* __restrict
         tc::mma_u8(d, ad, bd0, idesc, (c % 29) | s);
         tc::mma_u8(d + N, ad, bd1, idesc, (c % 29) | s);
       }
-      tc::mma_commit(&cbar[c & 3]);
-      tc::mma_commit(&cbar[(c + 1) & 3]);
+      tc::mma_commit(&cbar[2 + (c & 1)]);
+      tc::mma_commit(&cbar[3 - (c & 1)]);
       sa_i = sa_i == 2 ? 0 : sa_i + 1;
       sb_i = sb_i == 5 ? 0 : sb_i + 1;
     }
@@ -355,7 +362,7 @@ int main() {
     uint8_t* g;
     CK(cudaMalloc(&g, 4096 * 8192));
     CK(cudaFuncSetAttribute(ring_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    for (int mode : {0, 4, 6})
+    for (int mode : {0, 8, 4, 12})
       for (int N : {160}) {
         const int chunks = 29 * 64;
         ring_rate<<<sms, 448, 220 * 1024>>>(58, N, mode, g, sink);
