@@ -65,9 +65,9 @@ constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
 constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
 constexpr int kSlots = kChunk / 4;   // row slots (4-byte residues) per chunk
 constexpr int kEpiWarps = 4;
-constexpr int kTmaWarp = 4, kMmaWarp = 5, kProd0 = 6, kProdWarps = 8;
-constexpr int kRawWarp = kProd0 + kProdWarps;  // TMA of the t rows
-constexpr int kThreads = 32 * (kRawWarp + 1);
+constexpr int kTmaWarp = 4, kRawWarp = 5, kProd0 = 6, kProdWarps = 8;
+constexpr int kMmaWarp = kProd0 + kProdWarps;  // highest warp id: first in issue arbitration
+constexpr int kThreads = 32 * (kMmaWarp + 1);
 constexpr int kSR = 8;               // raw t stages
 constexpr int kMaxSB = 4;            // B (table) stages, 2 .. 4 by shared memory
 constexpr int kRawBytes = kSlots * kRows * 4;    // 8 KB
