@@ -96,6 +96,10 @@ __device__ __forceinline__ uint32_t neg_inv32(uint32_t p) {
   return 0u - inv;
 }
 
+// LOGN > 0: the ring degree is a compile-time constant, so the epilogue's
+// stores to the prime rows j, j+1, ... (n residues apart) take immediate
+// offsets instead of a 64-bit address add each (LOGN = 0: any degree)
+template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 1)
     crt_tc_kernel(TcInputs in, int count, int B, int limbs, int log_n, CrtTcTable tab,
                   const DevPrime32* __restrict__ primes, int np, uint32_t* __restrict__ out,
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint2 eprimes[kMaxTilePrimes];  // {p, -p^-1 mod 2^32} of the tile's primes
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_addr(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t n = size_t(1) << log_n;
+  const size_t n = size_t(1) << (LOGN > 0 ? LOGN : log_n);
   const int kpad = tab.kpad;                  // K bytes the MMAs read (multiple of 32)
   const uint32_t kcols = round128(kpad);      // K bytes per smem row (atom columns)
   const int ct = blockIdx.x % tab.ncol_tiles;  // this CTA's column tile
@@ -244,12 +248,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tmem_wait_ld();
         uint32_t* op = o + size_t(4 * g) * n;
         const int jn = min((g + 1 < g1) ? 8 : 4, pcount - 4 * g);  // primes in this pair
+        if (jn == 8) {  // full pair: no per-prime predicate
 #pragma unroll
-        for (int q = 0; q < 8; ++q, op += n)
-          if (q < jn) {
+          for (int q = 0; q < 8; ++q) {
             const uint2 e = eprimes[4 * g + q];
-            *op = planes_mont(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], e.x, e.y);
+            op[q * n] = planes_mont(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], e.x, e.y);
           }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < jn) {
+              const uint2 e = eprimes[4 * g + q];
+              op[q * n] = planes_mont(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], e.x, e.y);
+            }
+        }
       }
       tc::fence_before();
       tc::mbar_arrive(&t_empty[acc]);
@@ -286,8 +298,15 @@ bool crt_tc_supported(const CrtTcTable& tab) {
 }
 
 cudaError_t crt_tc_setup_attributes() {
-  return cudaFuncSetAttribute(crt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kMaxDynSmem);
+  cudaError_t e = cudaFuncSetAttribute(crt_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kMaxDynSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(crt_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxDynSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(crt_tc_kernel<17>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxDynSmem);
+  return e;
 }
 
 cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs, int count,
@@ -327,8 +346,9 @@ cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs,
   if (smem > size_t(kMaxDynSmem)) return cudaErrorInvalidValue;
   const int per_ct = std::max(1, sms / tab.ncol_tiles);
   const int grid = per_ct * tab.ncol_tiles;
-  crt_tc_kernel<<<grid, kThreads, smem, st>>>(in, count, static_cast<int>(batch), limbs, log_n,
-                                              tab, primes, np, out, stages, nslots);
+  auto kern = log_n == 17 ? crt_tc_kernel<17> : log_n == 16 ? crt_tc_kernel<16> : crt_tc_kernel<0>;
+  kern<<<grid, kThreads, smem, st>>>(in, count, static_cast<int>(batch), limbs, log_n, tab, primes,
+                                     np, out, stages, nslots);
   return cudaGetLastError();
 }
 
