@@ -69,23 +69,17 @@ __device__ __forceinline__ uint32_t limb_bytes(int l, int limbs, int end_bit) {
 // (d0 + 2^8 d1 + 2^16 d2 + 2^24 d3) 2^-32 mod p, lazy in [0, 2p) (inside the
 // forward NTT's input domain [0, 4p), fields.cuh F32::ct), for plane sums
 // d_b < 2^26. The table weights carry the factor 2^32 (build_crt_tc), so this
-// is a mod p. z = d0 + ... < 2^51 is assembled in two 32-bit words with a
-// carry chain (ALU pipe), then one Montgomery step: m = zl (-p^-1) mod 2^32,
-// (z + m p) / 2^32 = zh + umulhi(m, p) + (zl != 0) < p + 2^19 + 1 < 2p.
+// is a mod p. z = d0 + ... < 2^51, then one Montgomery step: m = z (-p^-1)
+// mod 2^32, (z + m p) / 2^32 < 2^19 + p < 2p (z + m p < 2^63: no overflow).
 __device__ __forceinline__ uint32_t planes_mont(uint32_t d0, uint32_t d1, uint32_t d2,
                                                 uint32_t d3, uint32_t p, uint32_t pinv) {
-  uint32_t zl, zh;
-  asm("{\n\t.reg .u32 a1, a2, a3, h1, h2, h3;\n\t"
-      "shl.b32 a1, %2, 8;\n\tshr.u32 h1, %2, 24;\n\t"
-      "shl.b32 a2, %3, 16;\n\tshr.u32 h2, %3, 16;\n\t"
-      "shl.b32 a3, %4, 24;\n\tshr.u32 h3, %4, 8;\n\t"
-      "add.cc.u32 %0, %5, a1;\n\taddc.u32 %1, h1, h2;\n\t"
-      "add.cc.u32 %0, %0, a2;\n\taddc.u32 %1, %1, h3;\n\t"
-      "add.cc.u32 %0, %0, a3;\n\taddc.u32 %1, %1, 0;\n\t}"
-      : "=r"(zl), "=r"(zh)
-      : "r"(d1), "r"(d2), "r"(d3), "r"(d0));
-  const uint32_t m = zl * pinv;
-  return zh + __umulhi(m, p) + (zl != 0u);
+  // z = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3 < 2^51: three IMAD.WIDE
+  uint64_t z = static_cast<uint64_t>(d1) * 256u + d0;
+  z += static_cast<uint64_t>(d2) * 65536u;
+  z += static_cast<uint64_t>(d3) * 16777216u;
+  // Montgomery: m = -z / p mod 2^32, (z + m p) / 2^32 exactly (one IMAD.WIDE)
+  const uint32_t m = static_cast<uint32_t>(z) * pinv;
+  return static_cast<uint32_t>((z + static_cast<uint64_t>(m) * p) >> 32);
 }
 
 // -p^-1 mod 2^32 (p odd): Newton, 5 steps from inv = p (correct to 3 bits)
