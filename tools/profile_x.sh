@@ -14,13 +14,14 @@ prof() {  # class kernel-regex launch-skip
 # launch order per he_mul (30-bit basis, tensor-core engine): crt_tc r1,
 # ntt_col (fwd A), ntt_blk (mid r1), ntt_col (inv A), bigint_tc (iCRT), crt_tc
 # r2, ntt_col, ntt_blk (mid r2), ntt_col, bigint_tc (finisher), fix-up.
-# warm_level runs the evk CRT (IMAD kernel) and two forward NTT passes first
-# (ntt_col + the pass-B ntt_pass_kernel).
+# warm_level runs the evk CRT (IMAD kernel) and one forward ntt_col pass (+ the
+# pass-B ntt_pass_kernel) first, so ntt_col launch 1 + 4k is the forward r1
+# pass of he_mul k, 2 + 4k its inverse r1 pass (ntt_col_kernel<S, INV>).
 prof crt crt_tc_kernel 2
 prof crt_r2 crt_tc_kernel 3
-prof ntt_a ntt_col_kernel 4
+prof ntt_a ntt_col_kernel 5
 prof mid_r1 ntt_blk_kernel 2
-prof intt_a ntt_col_kernel 5
+prof intt_a ntt_col_kernel 6
 prof icrt bigint_tc_kernel 2
 prof mid_r2 ntt_blk_kernel 3
 prof finish bigint_tc_kernel 3
