@@ -72,6 +72,7 @@ constexpr int kSR = 8;               // raw t stages
 constexpr int kMaxSB = 4;            // B (table) stages, 2 .. 4 by shared memory
 constexpr int kRawBytes = kSlots * kRows * 4;    // 8 KB
 constexpr int kMaxSeg = 3;
+constexpr int kMaxRows = 1024;       // A rows (residues) per coefficient
 constexpr int kACol = 512 - 2 * kSlots;          // TMEM A stages: columns 480 .. 511
 constexpr int kXWords = 2 * 2 * kMaxSeg * kRows; // posted k partial sums [tile&1][quad][seg][i]
 
@@ -79,7 +80,8 @@ struct Params {
   BigTcSeg seg[kMaxSeg];
   int nseg, B, entries, log_n;
   int n_cols, k_bytes, k_slot, rows_total;
-  int nsb;  // B stages
+  int nsb;    // B stages
+  int lobuf;  // the epilogue copies each tile's low accumulator block to shared memory
   BigTcOut o;
   uint32_t s8, s16, s24;  // 2^8, 2^16, 2^24 (arguments: kept as IMAD.WIDE)
 };
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sR = sB + nsb * b_bytes;                    // kSR x [16 rows][128] u32
   uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);
   uint32_t* mu_tab = xbuf + kXWords;                   // [k_slot]
+  uint32_t* lobuf = P.lobuf ? mu_tab + kMaxRows : nullptr;  // [NH][128] (epilogue)
   const int C = P.k_bytes / kChunk;                    // chunks per tile (last: k bytes)
   const int tiles_per_entry = static_cast<int>(n / kRows);
   const int tiles = P.entries * tiles_per_entry;
@@ -363,9 +366,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int bl = slot_lo(it), bh = slot_hi(it);
       const uint32_t alo = lane_base + bl * NH, ahi = lane_base + bh * NH - NH;
       bool lo_held = true;
-      // 16 columns from col (multiple of 4); the low block is handed back to
-      // the MMA as soon as every column below NH has been read
+      uint32_t* lb = lobuf + 32 * warp + lane;  // this coefficient's column of lobuf
+      if (lobuf) {
+        // the next tile's MMAs need the low block: copy it out and hand it
+        // back before the (sequential) carry pass (each thread reads back
+        // only its own coefficient: no synchronisation)
+        for (int c0 = 0; c0 < NH; c0 += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(alo + c0, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int d = 0; d < 16; ++d) lb[(c0 + d) * kRows] = v[d];
+        }
+        tc::fence_before();
+        tc::mbar_arrive(&blk_free[bl]);
+        lo_held = false;
+      }
+      // 16 columns from col (multiple of 4); without lobuf the low block is
+      // handed back as soon as every column below NH has been read
       auto load16 = [&](int col, uint32_t (&v)[16]) {
+        if (lobuf) {
+          if (col + 16 <= NH) {
+#pragma unroll
+            for (int d = 0; d < 16; ++d) v[d] = lb[(col + d) * kRows];
+            return;
+          }
+          if (col < NH) {
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+              const int cc = col + 4 * d;
+              if (cc < NH) {
+#pragma unroll
+                for (int x = 0; x < 4; ++x) v[4 * d + x] = lb[(cc + x) * kRows];
+              } else {
+                tc::tmem_ld4(ahi + cc, *reinterpret_cast<uint32_t(*)[4]>(v + 4 * d));
+              }
+            }
+            tc::tmem_wait_ld();
+            return;
+          }
+          tc::tmem_ld16(ahi + col, v);
+          tc::tmem_wait_ld();
+          return;
+        }
         if (col + 16 <= NH) {
           tc::tmem_ld16(alo + col, v);
         } else if (col >= NH) {
@@ -431,22 +474,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-constexpr int kMaxRows = 1024;  // A rows (residues) per coefficient
 
 namespace {
-size_t smem_for(int n_cols, int nsb) {
+size_t smem_for(int n_cols, int nsb, bool lobuf) {
   return size_t(nsb) * n_cols * kChunk + size_t(kSR) * kRawBytes + size_t(kXWords) * 4 +
-         kMaxRows * 4 + 1024;
+         kMaxRows * 4 + (lobuf ? size_t(n_cols / 2) * kRows * 4 : 0) + 1024;
 }
-// B stages: as many as fit (2 .. kMaxSB)
+// the low-block copy when it fits next to >= 3 B stages; B stages: as many as fit
+bool use_lobuf(int n_cols) { return smem_for(n_cols, 3, true) <= size_t(kMaxDynSmem); }
 int b_stages(int n_cols) {
+  const bool lb = use_lobuf(n_cols);
   int nsb = kMaxSB;
-  while (nsb > 2 && smem_for(n_cols, nsb) > size_t(kMaxDynSmem)) --nsb;
+  while (nsb > 2 && smem_for(n_cols, nsb, lb) > size_t(kMaxDynSmem)) --nsb;
   return nsb;
 }
 }  // namespace
 
-size_t bigint_tc_smem(int n_cols) { return smem_for(n_cols, b_stages(n_cols)); }
+size_t bigint_tc_smem(int n_cols) {
+  return smem_for(n_cols, b_stages(n_cols), use_lobuf(n_cols));
+}
 
 cudaError_t bigint_tc_setup_attributes() {
   return cudaFuncSetAttribute(bigint_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -479,6 +525,7 @@ cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, in
   P.log_n = log_n;
   P.n_cols = t.n_cols;
   P.nsb = b_stages(t.n_cols);
+  P.lobuf = use_lobuf(t.n_cols) ? 1 : 0;
   P.k_bytes = t.k_bytes;
   P.k_slot = t.k_slot;
   P.rows_total = t.slot0[t.nseg - 1] + t.np[t.nseg - 1];  // real rows; padding up to k_slot
