@@ -138,7 +138,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sR = sB + nsb * b_bytes;                    // kSR x [16 rows][128] u32
   uint32_t* xbuf = reinterpret_cast<uint32_t*>(sR + kSR * kRawBytes);
   uint32_t* mu_tab = xbuf + kXWords;                   // [k_slot]
-  uint32_t* lobuf = P.lobuf ? mu_tab + kMaxRows : nullptr;  // [NH][128] (epilogue)
+  // epilogue copy of the low accumulator block: [128 coefficients][LB]
+  // words, LB = NH + 4 (mod 32): 16-byte accesses of 8 lanes hit 32 banks
+  const int LB = NH + (NH % 32 == 0 ? 4 : 20);
+  uint32_t* lobuf = P.lobuf ? mu_tab + kMaxRows : nullptr;
   const int C = P.k_bytes / kChunk;                    // chunks per tile (last: k bytes)
   const int tiles_per_entry = static_cast<int>(n / kRows);
   const int tiles = P.entries * tiles_per_entry;
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int bl = slot_lo(it), bh = slot_hi(it);
       const uint32_t alo = lane_base + bl * NH, ahi = lane_base + bh * NH - NH;
       bool lo_held = true;
-      uint32_t* lb = lobuf + 32 * warp + lane;  // this coefficient's column of lobuf
+      uint32_t* lb = lobuf + (32 * warp + lane) * LB;  // this coefficient's row of lobuf
       if (lobuf) {
         // the next tile's MMAs need the low block: copy it out and hand it
         // back before the (sequential) carry pass (each thread reads back
@@ -376,7 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tmem_ld16(alo + c0, v);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int d = 0; d < 16; ++d) lb[(c0 + d) * kRows] = v[d];
+          for (int d = 0; d < 16; d += 4)
+            *reinterpret_cast<uint4*>(lb + c0 + d) = make_uint4(v[d], v[d + 1], v[d + 2], v[d + 3]);
         }
         tc::fence_before();
         tc::mbar_arrive(&blk_free[bl]);
@@ -388,7 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lobuf) {
           if (col + 16 <= NH) {
 #pragma unroll
-            for (int d = 0; d < 16; ++d) v[d] = lb[(col + d) * kRows];
+            for (int d = 0; d < 16; d += 4) {
+              const uint4 x = *reinterpret_cast<const uint4*>(lb + col + d);
+              v[d] = x.x, v[d + 1] = x.y, v[d + 2] = x.z, v[d + 3] = x.w;
+            }
             return;
           }
           if (col < NH) {
@@ -396,8 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int d = 0; d < 4; ++d) {
               const int cc = col + 4 * d;
               if (cc < NH) {
-#pragma unroll
-                for (int x = 0; x < 4; ++x) v[4 * d + x] = lb[(cc + x) * kRows];
+                const uint4 x = *reinterpret_cast<const uint4*>(lb + cc);
+                v[4 * d] = x.x, v[4 * d + 1] = x.y, v[4 * d + 2] = x.z, v[4 * d + 3] = x.w;
               } else {
                 tc::tmem_ld4(ahi + cc, *reinterpret_cast<uint32_t(*)[4]>(v + 4 * d));
               }
@@ -478,7 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 namespace {
 size_t smem_for(int n_cols, int nsb, bool lobuf) {
   return size_t(nsb) * n_cols * kChunk + size_t(kSR) * kRawBytes + size_t(kXWords) * 4 +
-         kMaxRows * 4 + (lobuf ? size_t(n_cols / 2) * kRows * 4 : 0) + 1024;
+         kMaxRows * 4 +
+         (lobuf ? size_t(n_cols / 2 + (n_cols / 2 % 32 == 0 ? 4 : 20)) * kRows * 4 : 0) + 1024;
 }
 // the low-block copy when it fits next to >= 3 B stages; B stages: as many as fit
 bool use_lobuf(int n_cols) { return smem_for(n_cols, 3, true) <= size_t(kMaxDynSmem); }
