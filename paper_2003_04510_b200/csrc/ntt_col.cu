@@ -84,9 +84,12 @@ __device__ __forceinline__ int twiddle_slot(int t) {
   return (1 << L) + (within & ((1 << i) - 1)) * 32 + (within >> i);
 }
 
-// One warp transforms one padded column mc (see the layout notes above).
-template <int S, bool INV>
-__device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* stw,
+// One warp transforms NC padded columns mc, mc + cstride, ... (see the layout
+// notes above) together: every twiddle load serves NC butterflies, and the
+// NC independent columns give each warp NC-fold instruction-level
+// parallelism.
+template <int S, bool INV, int NC>
+__device__ __forceinline__ void column_transform(uint32_t* mc, int cstride, const uint32_t* stw,
                                                  const DevPrime32& pr, int lane) {
   using G = ColGeo<S>;
   constexpr int EPT = G::EPT, R = G::R, NSH = G::NSH;
@@ -95,11 +98,24 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
     w = stw[idx];
     wq = stw[(1 << S) + idx];
   };
-  uint32_t v[EPT];
+  uint32_t v[NC][EPT];
+  auto ld = [&](auto pos) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) v[c][r] = mc[c * cstride + padf(pos(r))];
+  };
+  auto st = [&](auto pos) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) mc[c * cstride + padf(pos(r))] = v[c][r];
+  };
+  auto posH = [&](int r) { return lane + 32 * r; };
+  auto posL = [&](int r) { return EPT * lane + r; };
   if (!INV) {
     // ---- layout H: y = lane + 32 r; levels 0 .. R-1 ----------------------
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(lane + 32 * r)];
+    ld(posH);
 #pragma unroll
     for (int L = 0; L < R; ++L) {
       const int half = EPT >> (L + 1);
@@ -108,15 +124,15 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
         uint32_t w, wq;
         tw((1 << L) + blk, w, wq);  // group y >> (S - L) = blk: uniform
 #pragma unroll
-        for (int rr = 0; rr < half; ++rr)
-          ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int rr = 0; rr < half; ++rr)
+            ct(v[c][blk * 2 * half + rr], v[c][blk * 2 * half + rr + half], w, wq, p2, negp);
       }
     }
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) mc[padf(lane + 32 * r)] = v[r];
+    st(posH);
     __syncwarp();
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(EPT * lane + r)];
+    ld(posL);
     // ---- lane levels R .. S-R-1 (layout L: y = EPT lane + r) -------------
 #pragma unroll
     for (int L = R; L < R + NSH; ++L) {
@@ -125,13 +141,15 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
       uint32_t w, wq;
       tw((1 << L) + (lane >> (S - L - R)), w, wq);
 #pragma unroll
-      for (int r = 0; r < EPT; ++r) {
-        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lb);
-        const uint32_t top = upper ? o : v[r], bot = upper ? v[r] : o;
-        const uint32_t u = csub32(top, p2);
-        const uint32_t t = shoup32(bot, w, wq, negp);
-        v[r] = upper ? u + p2 - t : u + t;
-      }
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[c][r], 1 << lb);
+          const uint32_t top = upper ? o : v[c][r], bot = upper ? v[c][r] : o;
+          const uint32_t u = csub32(top, p2);
+          const uint32_t t = shoup32(bot, w, wq, negp);
+          v[c][r] = upper ? u + p2 - t : u + t;
+        }
     }
     // ---- register levels S-R .. S-1 --------------------------------------
 #pragma unroll
@@ -142,16 +160,16 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
         uint32_t w, wq;
         tw((1 << L) + blk * 32 + lane, w, wq);  // permuted (twiddle_slot)
 #pragma unroll
-        for (int rr = 0; rr < half; ++rr)
-          ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int rr = 0; rr < half; ++rr)
+            ct(v[c][blk * 2 * half + rr], v[c][blk * 2 * half + rr + half], w, wq, p2, negp);
       }
     }
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) mc[padf(EPT * lane + r)] = v[r];
+    st(posL);
   } else {
     // ---- layout L: levels S-1 .. S-R in registers --------------------------
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(EPT * lane + r)];
+    ld(posL);
 #pragma unroll
     for (int i = R - 1; i >= 0; --i) {
       const int L = S - R + i, half = EPT >> (i + 1);
@@ -160,8 +178,10 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
         uint32_t w, wq;
         tw((1 << L) + blk * 32 + lane, w, wq);  // permuted (twiddle_slot)
 #pragma unroll
-        for (int rr = 0; rr < half; ++rr)
-          gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int rr = 0; rr < half; ++rr)
+            gs(v[c][blk * 2 * half + rr], v[c][blk * 2 * half + rr + half], w, wq, p2, negp);
       }
     }
     // ---- lane levels S-R-1 .. R ------------------------------------------
@@ -172,17 +192,17 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
       uint32_t w, wq;
       tw((1 << L) + (lane >> (S - L - R)), w, wq);
 #pragma unroll
-      for (int r = 0; r < EPT; ++r) {
-        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lb);
-        const uint32_t top = upper ? o : v[r], bot = upper ? v[r] : o;
-        v[r] = upper ? shoup32(top + p2 - bot, w, wq, negp) : csub32(top + bot, p2);
-      }
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[c][r], 1 << lb);
+          const uint32_t top = upper ? o : v[c][r], bot = upper ? v[c][r] : o;
+          v[c][r] = upper ? shoup32(top + p2 - bot, w, wq, negp) : csub32(top + bot, p2);
+        }
     }
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) mc[padf(EPT * lane + r)] = v[r];
+    st(posL);
     __syncwarp();
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) v[r] = mc[padf(lane + 32 * r)];
+    ld(posH);
     // ---- layout H: levels R-1 .. 1, then level 0 with n^-1 folded ---------
 #pragma unroll
     for (int L = R - 1; L >= 1; --L) {
@@ -192,24 +212,36 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, const uint32_t* s
         uint32_t w, wq;
         tw((1 << L) + blk, w, wq);
 #pragma unroll
-        for (int rr = 0; rr < half; ++rr)
-          gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int rr = 0; rr < half; ++rr)
+            gs(v[c][blk * 2 * half + rr], v[c][blk * 2 * half + rr + half], w, wq, p2, negp);
       }
     }
 #pragma unroll
-    for (int rr = 0; rr < EPT / 2; ++rr) {
-      // a' = (u+v) n^-1, b' = (u-v) itw[1] n^-1, canonical (F32::inv_level0)
-      const uint32_t u = v[rr], w2 = v[rr + EPT / 2];
-      v[rr] = csub32(shoup32(u + w2, pr.ninv, pr.ninv_q, negp), p);
-      v[rr + EPT / 2] = csub32(shoup32(u + p2 - w2, pr.w1n, pr.w1n_q, negp), p);
-    }
+    for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) mc[padf(lane + 32 * r)] = v[r];
+      for (int rr = 0; rr < EPT / 2; ++rr) {
+        // a' = (u+v) n^-1, b' = (u-v) itw[1] n^-1, canonical (F32::inv_level0)
+        const uint32_t u = v[c][rr], w2 = v[c][rr + EPT / 2];
+        v[c][rr] = csub32(shoup32(u + w2, pr.ninv, pr.ninv_q, negp), p);
+        v[c][rr + EPT / 2] = csub32(shoup32(u + p2 - w2, pr.w1n, pr.w1n_q, negp), p);
+      }
+    st(posH);
   }
 }
 
+// Columns per warp-transform: the forward pass runs two interleaved columns
+// (2.23 -> 2.12 ms per step at X, 3 CTAs/SM), the inverse pass one (two are
+// slower there: 2.35 -> 2.44 ms).
+template <bool INV>
+struct ColCfg {
+  static constexpr int NC = INV ? 1 : 2;
+  static constexpr int kMinBlocks = INV ? 5 : 3;
+};
+
 template <int S, bool INV>
-__global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
+__global__ void __launch_bounds__(kThreads, ColCfg<INV>::kMinBlocks) ntt_col_kernel(ColArgs a) {
   constexpr int CS = ColGeo<S>::CS;
   extern __shared__ uint32_t smem[];
   uint32_t* col = smem;                        // [kCols][CS]
@@ -251,7 +283,10 @@ __global__ void __launch_bounds__(kThreads, 5) ntt_col_kernel(ColArgs a) {
     }
   }
   __syncthreads();
-  for (int cw = warp; cw < kCols; cw += kWarps) column_transform<S, INV>(col + cw * CS, stw, pr, lane);
+  constexpr int NC = ColCfg<INV>::NC;
+  static_assert(kCols % (kWarps * NC) == 0, "columns per warp");
+  for (int cw = warp; cw < kCols; cw += kWarps * NC)
+    column_transform<S, INV, NC>(col + cw * CS, kWarps * CS, stw, pr, lane);
   __syncthreads();
   // ---- cooperative store ------------------------------------------------
   {
