@@ -233,11 +233,23 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, int cstride, cons
 
 // Columns per warp-transform: the forward pass runs two interleaved columns
 // (2.23 -> 2.12 ms per step at X, 3 CTAs/SM), the inverse pass one (two are
-// slower there: 2.35 -> 2.44 ms).
+// slower there: 2.35 -> 2.44 ms). The macros exist for tools/build_variant.sh
+// sweeps; last sweep at X (ms per step, inverse / forward): inverse NC=2 at
+// 3 / 4 CTAs 2.43 / 2.50, NC=1 at 4 / 5 / 6 CTAs 2.52 / 2.37 / 2.55; forward
+// at 2 / 3 / 4 CTAs 2.25 / 2.13 / 2.15.
+#ifndef HEMUL_COL_NC_INV
+#define HEMUL_COL_NC_INV 1
+#endif
+#ifndef HEMUL_COL_MINB_INV
+#define HEMUL_COL_MINB_INV 5
+#endif
+#ifndef HEMUL_COL_MINB_FWD
+#define HEMUL_COL_MINB_FWD 3
+#endif
 template <bool INV>
 struct ColCfg {
-  static constexpr int NC = INV ? 1 : 2;
-  static constexpr int kMinBlocks = INV ? 5 : 3;
+  static constexpr int NC = INV ? HEMUL_COL_NC_INV : 2;
+  static constexpr int kMinBlocks = INV ? HEMUL_COL_MINB_INV : HEMUL_COL_MINB_FWD;
 };
 
 template <int S, bool INV>
