@@ -65,6 +65,7 @@ struct RegionDev {
   int target_bits = 0;
   DevBuf primes, tw, itw, btab, hat, big_p, half_p;
   DevBuf primes_t;  // word 32: inverse NTT constants that output t_j (level_tables.hpp)
+  DevBuf primes_m, primes_tm;  // the same, compensating Montgomery products (ntt_blk.cu)
   struct Crt {
     int in_bits;
     CrtWeights w;
@@ -280,6 +281,8 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
   } else {
     upload(d.primes, h.dev32, st);
     upload(d.primes_t, h.dev32_t, st);
+    upload(d.primes_m, h.dev32_m, st);
+    upload(d.primes_tm, h.dev32_tm, st);
     upload(d.tw, h.tw32, st);
     upload(d.itw, h.itw32, st);
   }
@@ -482,13 +485,16 @@ void ntt_fwd(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t r
 
 // Inverse NTT; passes = 1 runs only the final pass (after a fused middle pass).
 // to_t (30-bit basis): the last level scales by n^-1 (P/p_j)^-1, giving the
-// tensor-core iCRT / finisher operand t_j instead of x_j.
+// tensor-core iCRT / finisher operand t_j instead of x_j. mont: the data are
+// Montgomery products x y 2^-32 (ntt_blk.cu middle pass); the last level
+// multiplies the 2^32 back in.
 template <class F>
 void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t rows, int stage,
-             int passes = 2, bool to_t = false) {
+             int passes = 2, bool to_t = false, bool mont = false) {
   const int total = ntt_num_passes(c->log_n);
   const typename F::Prime* pr =
-      to_t ? r.primes_t.as<const typename F::Prime>() : r.P<F>();
+      mont ? (to_t ? r.primes_tm : r.primes_m).as<const typename F::Prime>()
+           : to_t ? r.primes_t.as<const typename F::Prime>() : r.P<F>();
   for (int pass = total > passes ? total - passes : 0; pass < total; ++pass)
     run(c, stage, pass + 1 == total ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B, "iNTT", [&] {
       return ntt_inverse_pass<F>(pass, data, rows, r.np, c->log_n, r.ITW<F>(), pr, c->stream);
@@ -915,6 +921,9 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   bool tc_big = false;
   if constexpr (kSplit) tc_big = c->tensor_cores && bs.icrt_tc && bs.fin_tc;
   const bool mid = ntt_has_mid(log_n);
+  // the warp-per-block middle pass (30-bit basis) Montgomery-reduces its
+  // products (ntt_blk.cu); the following inverse pass compensates
+  const bool blk_mont = kSplit && mid && ntt_blk_supported(log_n);
   if (mid) {
     // forward pass A, then one fused pass: forward pass B + tensor product +
     // inverse pass B, then inverse pass A
@@ -926,7 +935,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
         return ntt_mid_tensor<F>(R1, R1 + r1w, R1 + 2 * r1w, R1 + 3 * r1w, B, r1.np, log_n,
                                  r1.TW<F>(), r1.ITW<F>(), p1, c->stream);
     });
-    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 1, tc_big);
+    ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 1, tc_big, blk_mont);
   } else {
     ntt_fwd<F>(c, r1, R1, kInSlots * B * r1.np, HEMUL_STAGE_NTT);
     // pointwise products are booked under iCRT like rns.cpp:364
@@ -1005,7 +1014,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       return ntt_mid_evk<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, r2.TW<F>(), r2.ITW<F>(), p2,
                             c->stream);
     });
-    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1, tc_big);
+    ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 1, tc_big, blk_mont);
   } else {
     ntt_fwd<F>(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT);
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_EVK, "evk product",

@@ -42,7 +42,7 @@ struct DevPrime32 {
   uint32_t inv, inv_q;    // (P / p)^-1 mod p
   uint32_t ninv, ninv_q;  // n^-1 mod p
   uint32_t w1n, w1n_q;    // itw[1] n^-1
-  uint32_t pad[2];
+  uint32_t pad[2];         // [0] floor(2^55 / p) (bigint_tc.cu), [1] p^-1 mod 2^32
   double inv_p_dbl;       // 1 / p
   double pad2;
 };

@@ -49,6 +49,14 @@ __device__ __forceinline__ uint32_t reduce64_32(uint64_t z, uint32_t p, uint32_t
   return csub32(r, 2 * p);  // [0, 4p) -> [0, 2p)
 }
 
+// Montgomery: z < p 2^32 -> z 2^-32 mod p in (0, 2p), pinv = p^-1 mod 2^32.
+// z - m p with m = zl pinv has a zero low word, so (z - m p) / 2^32 =
+// zh - mulhi(m, p), in (-p, p) because zh < p and m p < p 2^32.
+__device__ __forceinline__ uint32_t mont32(uint64_t z, uint32_t p, uint32_t pinv) {
+  const uint32_t zh = static_cast<uint32_t>(z >> 32), m = static_cast<uint32_t>(z) * pinv;
+  return zh + p - __umulhi(m, p);
+}
+
 struct F64 {
   using W = uint64_t;
   using Prime = DevPrime;
@@ -160,6 +168,28 @@ struct F32 {
     v[3] = R(P(y1, Y2) + P(Y1, y2));
     v[4] = R(P(x1, y2) + P(x2, y1));
     v[5] = R(P(x1, Y2) + P(X1, y2) + P(x2, Y1) + P(X2, y1));
+  }
+  // The same six sums Montgomery-reduced: v = (sum) 2^-32 mod p in [0, 2p)
+  // (every sum < 4 p^2 < p 2^32); the inverse pass multiplies 2^32 back in
+  // (level_tables.hpp dev32_m / dev32_tm).
+  static __device__ __forceinline__ void tensor_split_mont(W (&v)[8], const Prime& pr) {
+    const Mod m(pr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m);
+    auto P = [](W a, W b) { return static_cast<uint64_t>(a) * b; };
+    const uint32_t pinv = pr.pad[1];
+    auto R = [&](uint64_t z) { return mont32(z, pr.p, pinv); };
+    const W x1 = v[0], X1 = v[1], y1 = v[2], Y1 = v[3], x2 = v[4], X2 = v[5], y2 = v[6], Y2 = v[7];
+    v[0] = R(P(x1, x2));
+    v[1] = R(P(x1, X2) + P(X1, x2));
+    v[2] = R(P(y1, y2));
+    v[3] = R(P(y1, Y2) + P(Y1, y2));
+    v[4] = R(P(x1, y2) + P(x2, y1));
+    v[5] = R(P(x1, Y2) + P(X1, y2) + P(x2, Y1) + P(X2, y1));
+  }
+  // x y 2^-32 mod p in [0, 2p) for x in [0, p), y in [0, 4p) (x y < 4 p^2)
+  static __device__ __forceinline__ W mul_mont(W x, W y, const Prime& pr) {
+    return mont32(static_cast<uint64_t>(x) * y, pr.p, pr.pad[1]);
   }
 };
 

@@ -281,6 +281,9 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
       d.ninv_q = shoup_q32(ninv[j], p);
       d.inv_p_dbl = 1.0 / double(p);
       d.pad[0] = uint32_t((u128(1) << 55) / p);  // bigint_tc.cu: fixed-point k quotient
+      uint32_t pinv = uint32_t(p);                // p^-1 mod 2^32 (Newton, p odd)
+      for (int it = 0; it < 5; ++it) pinv *= 2u - uint32_t(p) * pinv;
+      d.pad[1] = pinv;                            // ntt_blk.cu: Montgomery products
     }
     r.tw32.resize(size_t(count) * n);
     r.itw32.resize(size_t(count) * n);
@@ -325,6 +328,21 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
       d.w1n = uint32_t(wt);
       d.w1n_q = shoup_q32(wt, p);
     }
+    // Montgomery-compensated copies: ninv, w1n times 2^32 mod p
+    auto mont = [&](const std::vector<DevPrime32>& src, std::vector<DevPrime32>& dst) {
+      dst = src;
+      for (int j = 0; j < count; ++j) {
+        const uint64_t p = r.primes[j], r32 = (uint64_t(1) << 32) % p;
+        DevPrime32& d = dst[j];
+        const uint64_t nm = mulmod(d.ninv, r32, p), wm = mulmod(d.w1n, r32, p);
+        d.ninv = uint32_t(nm);
+        d.ninv_q = shoup_q32(nm, p);
+        d.w1n = uint32_t(wm);
+        d.w1n_q = shoup_q32(wm, p);
+      }
+    };
+    mont(r.dev32, r.dev32_m);
+    mont(r.dev32_t, r.dev32_tm);
   }
 
   // CRT weights of 2^(25 m) mod p_j (kernels.hpp CrtWeights): w64 as two

@@ -38,6 +38,10 @@ struct RegionHost {
   // the last inverse-NTT level outputs t_j = x_j (P/p_j)^-1 directly (the
   // operand of the tensor-core iCRT / finisher, bigint_tc.cu)
   std::vector<DevPrime32> dev32_t;
+  // word 32: dev32 / dev32_t with ninv, w1n also multiplied by 2^32, for the
+  // inverse passes that follow the warp-per-block middle pass, whose
+  // evaluation-domain products are Montgomery-reduced (x y 2^-32, ntt_blk.cu)
+  std::vector<DevPrime32> dev32_m, dev32_tm;
   std::vector<Twiddle32> tw32, itw32;  // np * n each (word 32)
   // CRT weights per input width (see kernels.hpp CrtWeights)
   struct Crt {

@@ -15,6 +15,10 @@
 // ntt_col.cu run between __syncwarp exchanges through the warp's own padded
 // shared-memory slots. No CTA barrier at all: warps progress independently,
 // so the HBM traffic of one warp overlaps the arithmetic of the others.
+// The evaluation-domain products are Montgomery-reduced (3 instructions
+// instead of 7 for the 64 -> 32-bit reduction): they come out as x y 2^-32,
+// and the inverse pass A that follows uses n^-1 constants carrying 2^32
+// (level_tables.hpp dev32_m / dev32_tm; context.cu blk_mont).
 #include <cuda_runtime.h>
 
 #include "fields.cuh"
@@ -244,14 +248,14 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? 6 : 7) ntt_blk_k
       uint32_t x[8];
 #pragma unroll
       for (int o = 0; o < 8; ++o) x[o] = slots[o * BS + e];
-      F32::tensor_split(x, pr);
+      F32::tensor_split_mont(x, pr);
 #pragma unroll
       for (int o = 0; o < 6; ++o) slots[o * BS + e] = x[o];
     } else {
       const size_t ei = size_t(j) * n + (size_t(block) << S) + EPT * lane + r;
-      const uint32_t f = slots[e];
-      slots[e] = F32::mul(f, __ldg(a.evk[0] + ei), pr);
-      slots[BS + e] = F32::mul(f, __ldg(a.evk[1] + ei), pr);
+      const uint32_t f = F32::fwd_canon(slots[e], F32::Mod(pr));
+      slots[e] = F32::mul_mont(f, __ldg(a.evk[0] + ei), pr);
+      slots[BS + e] = F32::mul_mont(f, __ldg(a.evk[1] + ei), pr);
     }
   }
   // ---- inverse levels of every product ------------------------------------
