@@ -187,7 +187,7 @@ struct F32 {
     v[4] = R(P(x1, y2) + P(x2, y1));
     v[5] = R(P(x1, Y2) + P(X1, y2) + P(x2, Y1) + P(X2, y1));
   }
-  // x y 2^-32 mod p in [0, 2p) for x in [0, p), y in [0, 4p) (x y < 4 p^2)
+  // x y 2^-32 mod p in [0, 2p) for x y < 4 p^2 (one factor canonical, the other < 4p)
   static __device__ __forceinline__ W mul_mont(W x, W y, const Prime& pr) {
     return mont32(static_cast<uint64_t>(x) * y, pr.p, pr.pad[1]);
   }

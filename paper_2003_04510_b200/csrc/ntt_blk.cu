@@ -253,7 +253,9 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? 6 : 7) ntt_blk_k
       for (int o = 0; o < 6; ++o) slots[o * BS + e] = x[o];
     } else {
       const size_t ei = size_t(j) * n + (size_t(block) << S) + EPT * lane + r;
-      const uint32_t f = F32::fwd_canon(slots[e], F32::Mod(pr));
+      // f in [0, 4p); the evk forms are full forward transforms, canonical
+      // (kernels.hpp), so f evk < 4 p^2 < p 2^32
+      const uint32_t f = slots[e];
       slots[e] = F32::mul_mont(f, __ldg(a.evk[0] + ei), pr);
       slots[BS + e] = F32::mul_mont(f, __ldg(a.evk[1] + ei), pr);
     }
