@@ -202,9 +202,18 @@ __device__ __forceinline__ void inv(uint32_t (&v)[BlkGeo<S>::EPT], const BlkTw<S
 }
 
 // register caps that buy one or two more CTAs per SM without spills
-// (measured at X: split tensor 2.25 -> 2.22 ms at 6 CTAs, evk 1.78 -> 1.72 at 7)
+// (measured at X: split tensor 2.25 -> 2.22 ms at 6 CTAs, evk 1.78 -> 1.72 at 7;
+// with the Montgomery products the evk pass fits 8: 1.74 -> 1.71 ms; 9 or a
+// 5-CTA split tensor pass are slower)
+#ifndef HEMUL_BLK_MINB_R1
+#define HEMUL_BLK_MINB_R1 6
+#endif
+#ifndef HEMUL_BLK_MINB_R2
+#define HEMUL_BLK_MINB_R2 8
+#endif
 template <int S, int OP>
-__global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? 6 : 7) ntt_blk_kernel(BlkArgs a) {
+__global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R1 : HEMUL_BLK_MINB_R2)
+    ntt_blk_kernel(BlkArgs a) {
   using G = BlkGeo<S>;
   constexpr int EPT = G::EPT, BS = G::BS;
   constexpr int NIN = OP == kTensor2 ? 8 : 1, NOUT = OP == kTensor2 ? 6 : 2;
