@@ -28,7 +28,12 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kWarps = 4;  // blocks (warps) per CTA
+#ifndef HEMUL_BLK_WARPS
+#define HEMUL_BLK_WARPS 4
+#endif
+// blocks (warps) per CTA; 2 warps at 12 / 16 CTAs per SM and 8 warps at 3 / 4
+// time the same or slower (mid r1 2.15-2.25 ms, r2 1.70-1.74 ms per step at X)
+constexpr int kWarps = HEMUL_BLK_WARPS;
 constexpr int kTensor2 = 0, kEvk = 1;
 
 __device__ __forceinline__ int padf(int y) { return y + (y >> 5); }
