@@ -107,6 +107,46 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx *ctx, int c1_log_q, int c2_log_q, si
                               const uint64_t *evk_ax, const uint64_t *evk_bx, uint64_t evk_id,
                               uint64_t *out_ax, uint64_t *out_bx);
 
+/* Which kernels he_mul runs at level log_q (the basis and engine choice are
+ * per level: table shapes change with log_q). Fills info[HEMUL_INFO_*]. */
+enum { HEMUL_INFO_WORD = 0,     /* 32 (30-bit basis) or 64 (reference primes) */
+       HEMUL_INFO_NP1,          /* region-1 primes (per half product when split) */
+       HEMUL_INFO_NP2,          /* region-2 primes */
+       HEMUL_INFO_SPLIT_H,      /* region-1 operand split bit h (0: unsplit) */
+       HEMUL_INFO_CRT1_TC,      /* region-1 CRT on the int8 tensor cores */
+       HEMUL_INFO_CRT2_TC,      /* ModUp CRT on the tensor cores */
+       HEMUL_INFO_BIG_TC,       /* iCRT + finisher on the tensor cores (t_j form) */
+       HEMUL_INFO_FUSED_MID,    /* fused middle NTT pass with the products */
+       HEMUL_INFO_BLK_MONT,     /* Montgomery-reduced warp-per-block middle pass */
+       HEMUL_INFO_COUNT };
+hemul_status hemul_gpu_engine_info(hemul_gpu_ctx *ctx, int log_q, int info[HEMUL_INFO_COUNT]);
+
+/* Test hook: run he_mul on `batch` pairs up to a stage checkpoint and copy
+ * that stage's device buffer to dst (host or device, cap bytes); *written =
+ * bytes copied. Lets the residue-level tests check the hot-path kernels of
+ * the 30-bit basis stage by stage against the restated oracle (the stage
+ * entry points below use the reference's w64 primes). Layouts (W = 4-byte
+ * residues in the 30-bit basis, 8 in w64; rows prime-major, n residues):
+ *   CRT1  region-1 operands after the CRT: 8 slots (w64: 4) of batch x np1
+ *         rows; slots x1 X1 y1 Y1 x2 X2 y2 Y2 = low / high halves (split at
+ *         h) of ax1 bx1 ax2 bx2 (w64: ax1 bx1 ax2 bx2); residues in [0, 2p)
+ *   PROD1 the products after the inverse NTT: 6 slots (w64: 3) of batch x
+ *         np1 rows, x1x2, x1X2+X1x2, y1y2, y1Y2+Y1y2, x1y2+x2y1,
+ *         x1Y2+X1y2+x2Y1+X2y1 (w64: d2, d0, d1); residues x_j, or t_j =
+ *         x_j (P/p_j)^-1 when HEMUL_INFO_BIG_TC
+ *   D2    d2 = ax1 ax2 mod 2^log_q, batch BigPolys (n x ceil(log_q/64))
+ *   CRT2  d2 in the region-2 primes: batch x np2 rows, [0, 2p)
+ *   PROD2 the evk products after the inverse NTT: 2 x batch x np2 rows
+ *         (d2 evk.ax, then d2 evk.bx), x_j or t_j as PROD1 */
+enum { HEMUL_TRACE_CRT1 = 1, HEMUL_TRACE_PROD1, HEMUL_TRACE_D2, HEMUL_TRACE_CRT2,
+       HEMUL_TRACE_PROD2 };
+hemul_status hemul_gpu_he_mul_trace(hemul_gpu_ctx *ctx, int log_q, size_t batch,
+                                    const uint64_t *c1_ax, const uint64_t *c1_bx,
+                                    const uint64_t *c2_ax, const uint64_t *c2_bx,
+                                    const uint64_t *evk_ax, const uint64_t *evk_bx,
+                                    uint64_t evk_id, int checkpoint, void *dst, size_t cap,
+                                    size_t *written);
+
 /* Scheme::rescale (heaan.cpp:328-337) on a batch: n x ceil(log_q/64) ->
  * n x ceil((log_q - log_p)/64). */
 hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, const uint64_t *ax,
@@ -149,9 +189,10 @@ hemul_status hemul_gpu_imad_peak(hemul_gpu_ctx *ctx, double *ops_per_s);
  * 30-bit basis' CRT / iCRT / finisher GEMMs (HEMUL_OPT_TENSOR_CORES). */
 hemul_status hemul_gpu_tc_peak(hemul_gpu_ctx *ctx, double *ops_per_s);
 
-/* Region tables of level log_q: region 1 (products mod q) or 2 (key
- * switching) in the reference's w64 basis, as the stage entry points use
- * them; region -1 / -2: the basis he_mul runs in (HEMUL_OPT_BASIS). Writes
+/* Prime set of level log_q: region 1 (products mod q) or 2 (key switching)
+ * by the reference's w64 rule (params.cpp:76-115, heaan.cpp:132-143) —
+ * host arithmetic only, no tables are built or uploaded; region -1 / -2: the
+ * basis he_mul runs in (HEMUL_OPT_BASIS; builds that level's tables). Writes
  * np and up to cap primes. */
 hemul_status hemul_gpu_level_info(hemul_gpu_ctx *ctx, int log_q, int region, int *np,
                                   uint64_t *primes, int cap);

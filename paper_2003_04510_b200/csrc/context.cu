@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <list>
@@ -34,8 +35,14 @@ namespace {
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
-  ~DevBuf() {
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
     if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
   }
   template <typename T>
   T* as() const {
@@ -126,6 +133,7 @@ struct Level {
   Basis basis[2];  // [0]: w64 reference primes, [1]: 30-bit basis
   bool has_evk = false;
   int evk_word = 0;  // basis of the cached evk forms
+  bool no_basis32 = false;  // the 30-bit basis cannot cover this level
   uint64_t evk_id = 0;
   DevBuf evk_a;  // 2 x np2 x n NTT forms (ax then bx)
 };
@@ -446,10 +454,19 @@ Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
 // primes when the 30-bit basis cannot cover the level (fields.cuh).
 int mul_word(hemul_gpu_ctx* c, Level& lv) {
   if (c->basis == 64) return 64;
+  if (lv.no_basis32) return 64;
   try {
     get_basis(c, lv, 32);
     return 32;
-  } catch (const std::runtime_error&) {
+  } catch (const BasisUnavailable&) {  // too few 30-bit primes; CUDA errors propagate
+    Basis& b = lv.basis[1];
+    b.r1.reset();
+    b.r2.reset();
+    b.icrt_tc.reset();
+    b.fin_tc.reset();
+    b.fin_btab.reset();
+    b.has_fin = false;
+    lv.no_basis32 = true;
     return 64;
   }
 }
@@ -505,7 +522,7 @@ void ntt_inv(hemul_gpu_ctx* c, const RegionDev& r, typename F::W* data, size_t r
 const uint64_t* stage_in(hemul_gpu_ctx* c, const uint64_t* p, size_t words, uint64_t* scratch) {
   if (is_device(c, p)) return p;
   run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D",
-      [&] { return cudaMemcpyAsync(scratch, p, words * 8, cudaMemcpyHostToDevice, c->stream); });
+      [&] { return cudaMemcpyAsync(scratch, p, words * 8, cudaMemcpyDefault, c->stream); });
   return scratch;
 }
 
@@ -566,15 +583,25 @@ OutPair out_pair(hemul_gpu_ctx* c, uint64_t* oa, uint64_t* ob, size_t words, Dev
 void copy_out(hemul_gpu_ctx* c, const OutPair& o, uint64_t* oa, uint64_t* ob, size_t words) {
   if (o.device) return;
   run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
-      [&] { return cudaMemcpyAsync(oa, o.a, words * 8, cudaMemcpyDeviceToHost, c->stream); });
+      [&] { return cudaMemcpyAsync(oa, o.a, words * 8, cudaMemcpyDefault, c->stream); });
   run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
-      [&] { return cudaMemcpyAsync(ob, o.b, words * 8, cudaMemcpyDeviceToHost, c->stream); });
+      [&] { return cudaMemcpyAsync(ob, o.b, words * 8, cudaMemcpyDefault, c->stream); });
   check(cudaStreamSynchronize(c->stream), "D2H");
 }
 
+// Stage checkpoint of he_mul_device (hemul_gpu_he_mul_trace): the run stops
+// after checkpoint `stop` and copies that stage's device buffer to dst.
+struct Trace {
+  int stop = 0;
+  void* dst = nullptr;
+  size_t cap = 0;
+  size_t written = 0;
+};
+
 template <class F>
 void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
-                   const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx);
+                   const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx,
+                   Trace* tr = nullptr);
 void he_mul_any(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                 const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx);
 void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
@@ -700,9 +727,17 @@ hemul_status hemul_gpu_level_info(hemul_gpu_ctx* c, int log_q, int region, int* 
                                   uint64_t* primes, int cap) {
   if (!c || (region != 1 && region != 2 && region != -1 && region != -2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
+    if (log_q <= 0 || log_q > c->log_q_max) throw std::invalid_argument("log_q out of range");
+    if (region > 0) {  // the reference's rule, host arithmetic only (no tables)
+      const std::vector<uint64_t> ps =
+          reference_primes(region, log_q, c->log_q_max, c->log_n, nullptr);
+      if (np) *np = static_cast<int>(ps.size());
+      for (int j = 0; j < int(ps.size()) && j < cap && primes; ++j) primes[j] = ps[j];
+      return HEMUL_OK;
+    }
     Level& lv = get_level(c, log_q);
-    const Basis& b = get_basis(c, lv, region > 0 ? 64 : mul_word(c, lv));
-    const RegionDev& r = region == 1 || region == -1 ? *b.r1 : *b.r2;
+    const Basis& b = get_basis(c, lv, mul_word(c, lv));
+    const RegionDev& r = region == -1 ? *b.r1 : *b.r2;
     if (np) *np = r.np;
     for (int j = 0; j < r.np && j < cap && primes; ++j) primes[j] = r.host_primes[j];
     return HEMUL_OK;
@@ -830,6 +865,71 @@ hemul_status hemul_gpu_he_mul(hemul_gpu_ctx* c, int c1_log_q, int c2_log_q, size
   });
 }
 
+hemul_status hemul_gpu_engine_info(hemul_gpu_ctx* c, int log_q, int info[HEMUL_INFO_COUNT]) {
+  if (!c || !info) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    Level& lv = get_level(c, log_q);
+    const int word = mul_word(c, lv);
+    const Basis& bs = get_basis(c, lv, word);
+    const RegionDev& r1 = *bs.r1;
+    const RegionDev& r2 = *bs.r2;
+    const bool tc = word == 32 && c->tensor_cores;
+    const int h = r1.split_h;
+    const bool mid = ntt_has_mid(c->log_n);
+    info[HEMUL_INFO_WORD] = word;
+    info[HEMUL_INFO_NP1] = r1.np;
+    info[HEMUL_INFO_NP2] = r2.np;
+    info[HEMUL_INFO_SPLIT_H] = h;
+    info[HEMUL_INFO_CRT1_TC] = tc && r1.tc_table(0, h) && r1.tc_table(h, log_q - h);
+    info[HEMUL_INFO_CRT2_TC] = tc && r2.tc_table(0, log_q);
+    info[HEMUL_INFO_BIG_TC] = tc && bs.icrt_tc && bs.fin_tc;
+    info[HEMUL_INFO_FUSED_MID] = mid;
+    info[HEMUL_INFO_BLK_MONT] = word == 32 && mid && ntt_blk_supported(c->log_n);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_he_mul_trace(hemul_gpu_ctx* c, int log_q, size_t batch,
+                                    const uint64_t* c1_ax, const uint64_t* c1_bx,
+                                    const uint64_t* c2_ax, const uint64_t* c2_bx,
+                                    const uint64_t* evk_ax, const uint64_t* evk_bx,
+                                    uint64_t evk_id, int checkpoint, void* dst, size_t cap,
+                                    size_t* written) {
+  if (!c || !dst || batch == 0 || checkpoint < HEMUL_TRACE_CRT1 || checkpoint > HEMUL_TRACE_PROD2)
+    return HEMUL_E_ARG;
+  if (log_q - c->log_p < c->log_p) return fail(c, HEMUL_E_DEPTH, "multiplicative depth exhausted");
+  if (!c1_ax || !c1_bx || !c2_ax || !c2_bx) return fail(c, HEMUL_E_ARG, "null buffer");
+  return guarded(c, [&]() -> hemul_status {
+    Level& lv = get_level(c, log_q);
+    const int word = mul_word(c, lv);
+    if (evk_ax && evk_bx &&
+        (!lv.has_evk || evk_id == 0 || lv.evk_id != evk_id || lv.evk_word != word))
+      set_evk_forms(c, lv, evk_ax, evk_bx, evk_id);
+    if (!lv.has_evk || lv.evk_word != word)
+      return fail(c, HEMUL_E_NO_EVK, "evaluation key not set for this level");
+    const size_t poly_w = size_t(c->n) * limbs_of(log_q);
+    const size_t out_w = size_t(c->n) * limbs_of(log_q - c->log_p);
+    ensure(c->in, 4 * batch * poly_w * 8);
+    const uint64_t* src[4] = {c1_ax, c1_bx, c2_ax, c2_bx};
+    const uint64_t* in[4];
+    for (int t = 0; t < 4; ++t)
+      in[t] = stage_in(c, src[t], batch * poly_w, c->in.as<uint64_t>() + t * batch * poly_w);
+    ensure(c->outb, 2 * batch * out_w * 8);
+    Trace tr;
+    tr.stop = checkpoint;
+    tr.dst = dst;
+    tr.cap = cap;
+    ++c->call_id;
+    uint64_t* oa = c->outb.as<uint64_t>();
+    if (word == 64)
+      he_mul_device<F64>(c, lv, log_q, batch, in, oa, oa + batch * out_w, &tr);
+    else
+      he_mul_device<F32>(c, lv, log_q, batch, in, oa, oa + batch * out_w, &tr);
+    if (written) *written = tr.written;
+    return HEMUL_OK;
+  });
+}
+
 hemul_status hemul_gpu_rescale(hemul_gpu_ctx* c, int log_q, size_t batch, const uint64_t* ax,
                                const uint64_t* bx, uint64_t* out_ax, uint64_t* out_bx) {
   if (!c) return HEMUL_E_ARG;
@@ -862,9 +962,19 @@ namespace {
 
 // One batched HE Mul on device buffers, every launch on c->stream, in the
 // prime basis of field F (fields.cuh).
+// True when the trace stops here (after copying `bytes` of `src` out).
+bool trace_at(hemul_gpu_ctx* c, Trace* tr, int point, const void* src, size_t bytes) {
+  if (!tr || tr->stop != point) return false;
+  if (bytes > tr->cap) throw std::invalid_argument("trace buffer too small");
+  check(cudaMemcpyAsync(tr->dst, src, bytes, cudaMemcpyDefault, c->stream), "trace copy");
+  check(cudaStreamSynchronize(c->stream), "trace copy");
+  tr->written = bytes;
+  return true;
+}
+
 template <class F>
 void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
-                   const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx) {
+                   const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx, Trace* tr) {
   using W = typename F::W;
   const size_t n = size_t(c->n);
   const int log_n = c->log_n;
@@ -916,6 +1026,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       return crt_forward_multi<F>(in, 4, L, B, log_n, *w1, p1, r1.np, R1, c->stream);
     });
   }
+  if (trace_at(c, tr, HEMUL_TRACE_CRT1, R1, kInSlots * r1w * sizeof(W))) return;
   // int8 tensor-core iCRT + finisher (30-bit split basis): the inverse NTTs
   // feeding them output t_j directly
   bool tc_big = false;
@@ -948,6 +1059,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
     });
     ntt_inv<F>(c, r1, R1, kOutSlots * B * r1.np, HEMUL_STAGE_INTT, 2, tc_big);
   }
+  if (trace_at(c, tr, HEMUL_TRACE_PROD1, R1, kOutSlots * r1w * sizeof(W))) return;
   // d2 = ax1 ax2 mod q in binary (ModUp input); d0 / d1 stay in RNS form
   // and are reconstructed inside the finisher
   ensure(c->dpoly, B * poly_w * 8);
@@ -984,6 +1096,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                      kSplit ? R1 + r1w : nullptr);
     });
   }
+  if (trace_at(c, tr, HEMUL_TRACE_D2, d2, B * poly_w * 8)) return;
   const W* D1 = R1 + (kSplit ? 4 : 2) * r1w;  // d1 (c0)
   const W* D0 = R1 + (kSplit ? 2 : 1) * r1w;  // d0 (c0)
   // ---- region 2: ModUp (CRT of d2), evk product, ModDown ------------------
@@ -1006,6 +1119,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       return crt_forward<F>(d2, L, B, log_n, *r2.weights(log_q), p2, r2.np, KA, c->stream);
     });
   }
+  if (trace_at(c, tr, HEMUL_TRACE_CRT2, KA, r2w * sizeof(W))) return;
   const W* EA = lv.evk_a.as<W>();
   const W* EB = EA + size_t(r2.np) * n;
   if (mid) {
@@ -1021,6 +1135,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
         [&] { return evk_product<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, p2, c->stream); });
     ntt_inv<F>(c, r2, KA, 2 * B * r2.np, HEMUL_STAGE_INTT, 2, tc_big);
   }
+  if (trace_at(c, tr, HEMUL_TRACE_PROD2, KA, 2 * r2w * sizeof(W))) return;
   // ---- finisher: out = R_logp(d + R_logQ(ks)) for ax (ks_a, d1) and bx
   // (ks_b, d0), exact iCRTs of both regions fused with ModDown + rescale
   IcrtFlags flags;
@@ -1083,12 +1198,31 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   ++c->launches;  // the (normally empty) exact fix-up kernel
 }
 
+// Row-indexed launches put rows on gridDim.y (<= 65535): a batch is run in
+// sub-batches whose largest row count (region-1 operand slots x np1, or the
+// 2 np2 region-2 rows) fits.
+constexpr size_t kMaxGridY = 65535;
+
+size_t max_sub_batch(const Basis& bs, int word) {
+  const size_t per = std::max<size_t>(size_t(word == 64 ? 4 : 8) * bs.r1->np, 2 * size_t(bs.r2->np));
+  return std::max<size_t>(1, kMaxGridY / per);
+}
+
 void he_mul_any(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
                 const uint64_t* const in[4], uint64_t* out_ax, uint64_t* out_bx) {
-  if (lv.evk_word == 64)
-    he_mul_device<F64>(c, lv, log_q, batch, in, out_ax, out_bx);
-  else
-    he_mul_device<F32>(c, lv, log_q, batch, in, out_ax, out_bx);
+  const int word = lv.evk_word;
+  const size_t sub = max_sub_batch(get_basis(c, lv, word), word);
+  const size_t poly_w = size_t(c->n) * limbs_of(log_q);
+  const size_t out_w = size_t(c->n) * limbs_of(log_q - c->log_p);
+  for (size_t b0 = 0; b0 < batch; b0 += sub) {
+    const size_t bc = std::min(sub, batch - b0);
+    const uint64_t* part[4];
+    for (int t = 0; t < 4; ++t) part[t] = in[t] + b0 * poly_w;
+    if (word == 64)
+      he_mul_device<F64>(c, lv, log_q, bc, part, out_ax + b0 * out_w, out_bx + b0 * out_w);
+    else
+      he_mul_device<F32>(c, lv, log_q, bc, part, out_ax + b0 * out_w, out_bx + b0 * out_w);
+  }
 }
 
 // Host buffers: the batch runs in chunks through double-buffered device
@@ -1120,7 +1254,7 @@ void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
         uint64_t* d = in_slot[s] + t * chunk * poly_w;
         run_on(c, c->h2d, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D", [&] {
           return cudaMemcpyAsync(d, src[t] + b0 * poly_w, bc * poly_w * 8,
-                                 cudaMemcpyHostToDevice, c->h2d);
+                                 cudaMemcpyDefault, c->h2d);
         });
         in[t] = d;
       }
@@ -1136,11 +1270,11 @@ void he_mul_pipelined(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
     if (!dev_out) {
       check(cudaStreamWaitEvent(c->d2h, c->ev_comp[s], 0), "wait");
       run_on(c, c->d2h, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(out_ax + b0 * out_w, oa, bc * out_w * 8, cudaMemcpyDeviceToHost,
+        return cudaMemcpyAsync(out_ax + b0 * out_w, oa, bc * out_w * 8, cudaMemcpyDefault,
                                c->d2h);
       });
       run_on(c, c->d2h, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(out_bx + b0 * out_w, ob, bc * out_w * 8, cudaMemcpyDeviceToHost,
+        return cudaMemcpyAsync(out_bx + b0 * out_w, ob, bc * out_w * 8, cudaMemcpyDefault,
                                c->d2h);
       });
       check(cudaEventRecord(c->ev_d2h[s], c->d2h), "event");
@@ -1186,13 +1320,18 @@ hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* da
       d = c->r1.as<uint64_t>();
       stage_in(c, data, words, d);
     }
-    if (inverse)
-      ntt_inv<F64>(c, r, d, rows, HEMUL_STAGE_INTT);
-    else
-      ntt_fwd<F64>(c, r, d, rows, HEMUL_STAGE_NTT);
+    // row r uses prime r % np: chunks are whole multiples of np
+    const size_t step = std::max<size_t>(1, kMaxGridY / size_t(r.np)) * size_t(r.np);
+    for (size_t r0 = 0; r0 < rows; r0 += step) {
+      const size_t rc = std::min(step, rows - r0);
+      if (inverse)
+        ntt_inv<F64>(c, r, d + r0 * c->n, rc, HEMUL_STAGE_INTT);
+      else
+        ntt_fwd<F64>(c, r, d + r0 * c->n, rc, HEMUL_STAGE_NTT);
+    }
     if (!dev)
       run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDeviceToHost, c->stream);
+        return cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDefault, c->stream);
       });
     check(cudaStreamSynchronize(c->stream), "ntt");
     return HEMUL_OK;
@@ -1220,11 +1359,17 @@ hemul_status hemul_gpu_crt(hemul_gpu_ctx* c, int log_q, int region, int in_bits,
       dst = c->r1.as<uint64_t>();
     }
     run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT", [&] {
-      return crt_forward<F64>(src, L, batch, c->log_n, *w, r.P<F64>(), r.np, dst, c->stream);
+      for (size_t b0 = 0; b0 < batch; b0 += kMaxGridY) {  // batch on gridDim.y
+        const size_t bc = std::min(kMaxGridY, batch - b0);
+        const cudaError_t e = crt_forward<F64>(src + b0 * n * L, L, bc, c->log_n, *w, r.P<F64>(),
+                                               r.np, dst + b0 * r.np * n, c->stream);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
     });
     if (!dev)
       run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(rns, dst, words * 8, cudaMemcpyDeviceToHost, c->stream);
+        return cudaMemcpyAsync(rns, dst, words * 8, cudaMemcpyDefault, c->stream);
       });
     check(cudaStreamSynchronize(c->stream), "crt");
     return HEMUL_OK;
@@ -1249,7 +1394,7 @@ hemul_status hemul_gpu_pointwise(hemul_gpu_ctx* c, int log_q, int region, size_t
     });
     if (!dev)
       run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDeviceToHost, c->stream);
+        return cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDefault, c->stream);
       });
     check(cudaStreamSynchronize(c->stream), "pointwise");
     return HEMUL_OK;
@@ -1281,12 +1426,18 @@ hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batc
     flags.count = c->flagbuf.as<unsigned>();
     flags.ids = flags.count + 1;
     run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT", [&] {
-      return icrt<F64>(src, batch, c->log_n, r.P<F64>(), r.np, r.icrt, dst, c->stream, &flags);
+      for (size_t b0 = 0; b0 < batch; b0 += kMaxGridY) {  // batch on gridDim.y
+        const size_t bc = std::min(kMaxGridY, batch - b0);
+        const cudaError_t e = icrt<F64>(src + b0 * r.np * n, bc, c->log_n, r.P<F64>(), r.np,
+                                        r.icrt, dst + b0 * n * TL, c->stream, &flags);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
     });
     ++c->launches;  // the fix-up kernel
     if (!dev)
       run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(poly, dst, batch * n * TL * 8, cudaMemcpyDeviceToHost, c->stream);
+        return cudaMemcpyAsync(poly, dst, batch * n * TL * 8, cudaMemcpyDefault, c->stream);
       });
     check(cudaStreamSynchronize(c->stream), "icrt");
     return HEMUL_OK;

@@ -187,11 +187,27 @@ void generate_primes30(int count, int log_n, std::vector<uint64_t>& primes,
   roots.clear();
   for (uint64_t c = top - (top - 1) % two_n; int(primes.size()) < count; c -= two_n) {
     if (c <= floor_ || c < two_n)
-      throw std::runtime_error("30-bit prime range exhausted for this ring degree");
+      throw BasisUnavailable("30-bit prime range exhausted for this ring degree");
     if (!is_prime(c)) continue;
     primes.push_back(c);
     roots.push_back(min_root(c, two_n));
   }
+}
+
+std::vector<uint64_t> reference_primes(int region, int log_q, int log_q_max, int log_n,
+                                       int* p_limbs) {
+  const int bound = region == 1 ? 2 * log_q + log_n + 1 : log_q + 2 * log_q_max + log_n + 1;
+  int count = region == 1 ? prime_count(2 * log_q, log_n) : prime_count(log_q + 2 * log_q_max, log_n);
+  std::vector<uint64_t> primes, roots;
+  Nat P;
+  for (;; ++count) {
+    generate_primes(count, log_n, primes, roots);
+    P.assign(1, 1);
+    for (uint64_t p : primes) nat_mul_word(P, p);
+    if (nat_bits(P) > bound) break;
+  }
+  if (p_limbs) *p_limbs = (nat_bits(P) + 63) / 64;
+  return primes;
 }
 
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
@@ -379,7 +395,11 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
       fields = {{0, h}, {h, log_q - h}};
     else if (region == 2)
       fields = {{0, log_q}};
-    for (auto [b0, nb] : fields) r.crt_tc.push_back(build_crt_tc(r.primes, b0, nb));
+    // the split halves run in one launch (crt_forward_tc), which needs one
+    // K padding and column tiling for both: build with the larger kpad
+    int kpad = 0;
+    for (auto [b0, nb] : fields) kpad = std::max(kpad, build_crt_tc_kpad(b0, nb));
+    for (auto [b0, nb] : fields) r.crt_tc.push_back(build_crt_tc(r.primes, b0, nb, kpad));
   }
 
   // iCRT operands mod 2^T in A-row order: w64 H_j, H_j 2^30 (the two 30-bit
@@ -416,7 +436,14 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   return r;
 }
 
-RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, int bits) {
+int build_crt_tc_kpad(int bit0, int bits) {
+  const int byte0 = bit0 / 8, nbytes = (bits + 7) / 8;
+  const int d = byte0 - 8 * (byte0 / 8);
+  return (d + nbytes + 31) / 32 * 32;
+}
+
+RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, int bits,
+                               int kpad_min) {
   RegionHost::CrtTc t;
   const int np = static_cast<int>(primes.size());
   t.bit0 = bit0;
@@ -424,7 +451,7 @@ RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, in
   const int byte0 = bit0 / 8, nbytes = (bits + 7) / 8;
   t.limb0 = byte0 / 8;
   const int d = byte0 - 8 * t.limb0;
-  t.kpad = (d + nbytes + 31) / 32 * 32;
+  t.kpad = std::max(build_crt_tc_kpad(bit0, bits), kpad_min);
   t.end_bit = bit0 + bits;
   // shared memory of crt_tc.cu: col_tile x K + 2 stages x 128 x K (K rounded
   // to 128-byte atom columns) + 1 KB alignment, within kMaxDynSmem (224 KB)

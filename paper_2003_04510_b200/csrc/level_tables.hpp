@@ -2,6 +2,7 @@
 // Scheme::Level, proj/core/src/heaan.cpp:104-112,119-150).
 #pragma once
 #include <cstdint>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -17,10 +18,23 @@ void generate_primes(int count, int log_n, std::vector<uint64_t>& primes,
                      std::vector<uint64_t>& roots);
 // The B200 basis (fields.cuh F32): the same rule below 2^30.
 constexpr int kPrime30Bits = 30;
+// Thrown (only) when the 30-bit basis cannot cover a ring degree / level;
+// the context then computes in the w64 basis. Every other failure (CUDA,
+// allocation, upload) propagates.
+struct BasisUnavailable : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 void generate_primes30(int count, int log_n, std::vector<uint64_t>& primes,
                        std::vector<uint64_t>& roots);
 // iCRT headroom every he_mul region keeps (icrt.cu: fp64 quotient argument)
 constexpr int kMinSlackBits = 4;
+
+// The reference's prime set of one region at modulus log_q (w64 rule with the
+// grow-until-bound loop of heaan.cpp:132-143), host arithmetic only: no
+// twiddle or CRT tables are built. p_limbs = 64-bit limbs of P = prod p_j
+// (the PLimbs of the reference's iCRT, params.cpp:215-239).
+std::vector<uint64_t> reference_primes(int region, int log_q, int log_q_max, int log_n,
+                                       int* p_limbs);
 
 struct RegionHost {
   int region = 0;
@@ -87,7 +101,11 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
 // Tensor-core CRT table of field [bit0, bit0 + bits) (bit0 % 8 == 0) for the
 // region's primes: column tiling chosen so that the weight tile and two
 // 128-coefficient A stages fit in shared memory (crt_tc.cu).
-RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, int bits);
+// kpad_min: pad K at least this far (fields converted in one launch share
+// one K padding and column tiling).
+int build_crt_tc_kpad(int bit0, int bits);
+RegionHost::CrtTc build_crt_tc(const std::vector<uint64_t>& primes, int bit0, int bits,
+                               int kpad_min = 0);
 // Split point of the 30-bit basis' region 1: ceil(log_q / 2) rounded up to a
 // byte (the tensor-core CRT reads whole bytes), or ceil(log_q / 2) when that
 // leaves no high half.

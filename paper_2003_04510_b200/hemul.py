@@ -91,7 +91,17 @@ _SIGS = {
     "hemul_gpu_imad_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "hemul_gpu_tc_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "hemul_gpu_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "hemul_gpu_engine_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_int)]),
+    "hemul_gpu_he_mul_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t,
+                                              _u64p, _u64p, _u64p, _u64p, _u64p, _u64p,
+                                              ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p,
+                                              ctypes.c_size_t,
+                                              ctypes.POINTER(ctypes.c_size_t)]),
 }
+ENGINE_INFO = ("word", "np1", "np2", "split_h", "crt1_tc", "crt2_tc", "big_tc", "fused_mid",
+               "blk_mont")  # HEMUL_INFO_* in include/hemul_gpu.h
+TRACE_POINTS = {"crt1": 1, "prod1": 2, "d2": 3, "crt2": 4, "prod2": 5}  # HEMUL_TRACE_*
 HEMUL_OPT_FORCE_EXACT = 1
 HEMUL_OPT_BASIS = 2
 HEMUL_OPT_TENSOR_CORES = 3
@@ -187,6 +197,10 @@ class Context:
         if st != HEMUL_OK:
             raise HemulGpuError(st, "hemul_gpu_create failed (no usable CUDA device?)")
         self._h = h
+        # evk identity (see _evk_identity); automatic ids live above 2^62 so
+        # they never meet explicit caller ids
+        self._evk_last: tuple[Any, Any, int] | None = None
+        self._evk_seq = 1 << 62
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -221,17 +235,36 @@ class Context:
         return self.params.n
 
     # -- Scheme-level API ------------------------------------------------
-    def warm_level(self, log_q: int, evk: tuple[Any, Any] | None = None, evk_id: int = 1) -> None:
+    def _evk_identity(self, evk: tuple[Any, Any] | None, evk_id: int | None) -> int:
+        """The id the C side keys its cached evk forms by. The reference keys
+        them by the EvalKey's address (heaan.cpp:152); here by the identity of
+        the two arrays: the same objects as last time keep their id (the
+        context holds them, so the identity cannot be recycled), anything else
+        gets a fresh one. An explicit evk_id overrides (0 = always rebuild)."""
+        if evk is None:
+            return 0
+        if evk_id is not None:
+            return int(evk_id)
+        last = self._evk_last
+        if last is not None and last[0] is evk[0] and last[1] is evk[1]:
+            return last[2]
+        self._evk_seq += 1
+        self._evk_last = (evk[0], evk[1], self._evk_seq)
+        return self._evk_seq
+
+    def warm_level(self, log_q: int, evk: tuple[Any, Any] | None = None,
+                   evk_id: int | None = None) -> None:
         """Scheme::warm_level (heaan.hpp:100): tables, and evk forms if given."""
         if evk is None:
             self._check(self._lib.hemul_gpu_set_level(self._h, log_q))
         else:
             ea, eb = evk
-            self._check(self._lib.hemul_gpu_set_evk(self._h, log_q, _ptr(ea), _ptr(eb), evk_id))
+            self._check(self._lib.hemul_gpu_set_evk(self._h, log_q, _ptr(ea), _ptr(eb),
+                                                    self._evk_identity(evk, evk_id)))
 
     def he_mul(self, c1: tuple[Any, Any], c2: tuple[Any, Any], log_q: int,
                c2_log_q: int | None = None, evk: tuple[Any, Any] | None = None,
-               evk_id: int = 1, out: tuple[Any, Any] | None = None):
+               evk_id: int | None = None, out: tuple[Any, Any] | None = None):
         """Scheme::he_mul (heaan.cpp:339-410) on (ax, bx) pairs. Inputs have
         shape (n, limbs) or (batch, n, limbs); returns (ax, bx) at modulus
         log_q - log_p."""
@@ -256,7 +289,7 @@ class Context:
         eb = _ptr(evk[1]) if evk is not None else None
         self._check(self._lib.hemul_gpu_he_mul(
             self._h, log_q, c2_log_q, batch, _ptr(c1[0]), _ptr(c1[1]), _ptr(c2[0]), _ptr(c2[1]),
-            ea, eb, evk_id if evk is not None else 0, _ptr(out[0]), _ptr(out[1])))
+            ea, eb, self._evk_identity(evk, evk_id), _ptr(out[0]), _ptr(out[1])))
         return out
 
     def rescale(self, c: tuple[Any, Any], log_q: int):
@@ -268,6 +301,40 @@ class Context:
         out = (_like(c[0], shape), _like(c[0], shape))
         self._check(self._lib.hemul_gpu_rescale(self._h, log_q, batch, _ptr(c[0]), _ptr(c[1]),
                                                 _ptr(out[0]), _ptr(out[1])))
+        return out
+
+    def engine_info(self, log_q: int) -> dict[str, int]:
+        """Basis and kernels he_mul uses at level log_q (hemul_gpu_engine_info)."""
+        buf = (ctypes.c_int * len(ENGINE_INFO))()
+        self._check(self._lib.hemul_gpu_engine_info(self._h, log_q, buf))
+        return dict(zip(ENGINE_INFO, list(buf)))
+
+    def he_mul_trace(self, c1: tuple[Any, Any], c2: tuple[Any, Any], log_q: int, point: str,
+                     evk: tuple[Any, Any] | None = None, evk_id: int | None = None) -> np.ndarray:
+        """Test hook: he_mul stopped at a stage checkpoint (crt1, prod1, d2,
+        crt2, prod2; include/hemul_gpu.h HEMUL_TRACE_*); returns that stage's
+        buffer (uint32 residues in the 30-bit basis, uint64 otherwise)."""
+        info = self.engine_info(log_q)
+        p = self.params
+        per = self.n * limbs(log_q)
+        batch = _size(c1[0]) // per
+        w = 4 if info["word"] == 32 else 8
+        rows = {"crt1": (8 if w == 4 else 4) * batch * info["np1"],
+                "prod1": (6 if w == 4 else 3) * batch * info["np1"],
+                "crt2": batch * info["np2"], "prod2": 2 * batch * info["np2"]}
+        if point == "d2":
+            out = np.zeros((batch, self.n, limbs(log_q)), np.uint64)
+        else:
+            out = np.zeros((rows[point], self.n), np.uint32 if w == 4 else np.uint64)
+        ea = _ptr(evk[0]) if evk is not None else None
+        eb = _ptr(evk[1]) if evk is not None else None
+        wrote = ctypes.c_size_t()
+        self._check(self._lib.hemul_gpu_he_mul_trace(
+            self._h, log_q, batch, _ptr(c1[0]), _ptr(c1[1]), _ptr(c2[0]), _ptr(c2[1]), ea, eb,
+            self._evk_identity(evk, evk_id), TRACE_POINTS[point], out.ctypes.data, out.nbytes,
+            ctypes.byref(wrote)))
+        assert wrote.value == out.nbytes, (wrote.value, out.nbytes)
+        del p
         return out
 
     # -- stage API (ntt.hpp / rns.hpp) -------------------------------------

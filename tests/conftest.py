@@ -30,9 +30,17 @@ def restated():
 
 
 @pytest.fixture(scope="session")
-def reference():
+def reference(request):
+    """The reference library itself (oracle/_ref, built from /root/reference by
+    oracle/Makefile; prebuilt .so travels to the GPU box). Missing it is a
+    failure, never a skip: the paper-scale parity tests depend on it."""
     from oracle_lib import REFERENCE_SO, Reference
 
+    if not REFERENCE_SO.exists() and Path("/root/reference").exists():
+        import subprocess
+
+        subprocess.run(["make", "-C", str(ROOT / "oracle"), "ref"], capture_output=True)
     if not REFERENCE_SO.exists():
-        pytest.skip("oracle/_ref/libhemul_ref.so not built (needs /root/reference at build time)")
+        pytest.fail("oracle/_ref/libhemul_ref.so not built: run `python -c 'import "
+                    "__graft_entry__ as g; g.build()'` where /root/reference exists")
     return Reference()

@@ -1,7 +1,7 @@
 """Regenerate tests/golden/* from the reference itself (oracle/_ref).
 
 Run here (where /root/reference exists and oracle/_ref was built):
-    python tests/golden/gen_golden.py [--big]
+    python tests/golden/gen_golden.py [--big] [--only NAME]
 
 Writes
   digests.json   ciphertext_digest of run_he_mul_bench(seed=7, reps=1)
@@ -27,6 +27,7 @@ CONFIGS = {
     "S": (30, 4, 13),
     "logN13_logQ300": (30, 10, 13),
     "logN14_logQ300": (30, 10, 0),
+    "logN15_logQ600": (30, 20, 0),
     "M": (30, 40, 0),
     "X": (30, 80, 0),
 }
@@ -34,11 +35,12 @@ CONFIGS = {
 
 def main() -> None:
     big = "--big" in sys.argv
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     ref = Reference()
     out = HERE / "digests.json"
     data = json.loads(out.read_text()) if out.exists() else {}
     for name, cfg in CONFIGS.items():
-        if name in ("M", "X") and not big:
+        if (name in ("M", "X") and not big) or (only and name != only):
             continue
         t = time.time()
         dig, ms = ref.run_bench(*cfg, seed=7, reps=1)
@@ -48,6 +50,8 @@ def main() -> None:
                       "ref_stage_ms_1thread": ms}
         print(name, f"{dig:016x}", f"{time.time() - t:.1f}s", flush=True)
         out.write_text(json.dumps(data, indent=1, sort_keys=True) + "\n")
+    if only:
+        return
     # S inputs / outputs
     cfg = CONFIGS["S"]
     inp = ref.bench_inputs(*cfg, seed=7)

@@ -217,7 +217,7 @@ def test_basis_switch_and_counts():
 
 @pytest.mark.slow
 @pytest.mark.parametrize("basis", BASES)
-@pytest.mark.parametrize("name", ["logN14_logQ300", "M", "X"])
+@pytest.mark.parametrize("name", ["logN14_logQ300", "logN15_logQ600", "M", "X"])
 def test_bench_protocol_digest_paper_scale(name, basis, reference):
     """Digest of he_mul on the reference's own seed-7 keys and ciphertexts
     equals the reference's."""
@@ -228,3 +228,100 @@ def test_bench_protocol_digest_paper_scale(name, basis, reference):
     q = inp["log_q_max"]
     oa, ob = ctx.he_mul(inp["c1"], inp["c2"], q, evk=inp["evk"])
     assert f"{_digest(q - cfg[0], oa, ob):016x}" == d["digest"]
+
+
+# ---- paper-scale parity below the fresh modulus ------------------------------
+# Levels of the M and X ladders (heaan.cpp:339-410 at log_q < log_Q): the
+# region tables, the split point and the iCRT / finisher byte windows all
+# change with log_q. Random ciphertexts (SURVEY §8(d) throughput inputs) and
+# one random evk per config; the reference's own he_mul (oracle/_ref, all host
+# threads) computes each expected output once, shared by the three engines.
+PAPER_LADDERS = {"X": ((30, 80, 0), [2400, 1800, 1200, 60]),
+                 "M": ((30, 40, 0), [1200, 630, 60])}
+_REF_CACHE: dict = {}
+
+
+def _paper_case(name, log_q, reference):
+    key = (name, log_q)
+    if key not in _REF_CACHE:
+        import os
+
+        cfg, _ = PAPER_LADDERS[name]
+        log_n, n, qmax = reference.make_params(*cfg)
+        rng = np.random.default_rng(1000 + log_q)
+        if (name, "evk") not in _REF_CACHE:
+            erng = np.random.default_rng(7)
+            _REF_CACHE[(name, "evk")] = (random_poly(erng, n, 2 * qmax),
+                                         random_poly(erng, n, 2 * qmax))
+        evk = _REF_CACHE[(name, "evk")]
+        c1 = (random_poly(rng, n, log_q), random_poly(rng, n, log_q))
+        c2 = (random_poly(rng, n, log_q), random_poly(rng, n, log_q))
+        st, wa, wb = reference.he_mul(*cfg, log_q, c1, c2, evk, threads=os.cpu_count() or 1)
+        assert st == 0, reference.err()
+        _REF_CACHE[key] = (c1, c2, evk, wa, wb)
+    return _REF_CACHE[key]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("basis", BASES)
+@pytest.mark.parametrize("name", ["M", "X"])
+def test_paper_scale_ladder_levels_vs_reference(name, basis, reference):
+    cfg, levels = PAPER_LADDERS[name]
+    ctx = _ctx(cfg, basis)
+    for log_q in levels:
+        c1, c2, evk, wa, wb = _paper_case(name, log_q, reference)
+        oa, ob = ctx.he_mul(c1, c2, log_q, evk=evk)
+        assert np.array_equal(oa, wa), (name, log_q, basis)
+        assert np.array_equal(ob, wb), (name, log_q, basis)
+    ctx.close()
+
+
+# ---- evk identity and batch limits --------------------------------
+
+def test_two_evks_at_one_level_in_one_context(restated):
+    """The cached evk forms are keyed by the key's identity (heaan.cpp:152):
+    a different evk at an already-warm level must not reuse the old forms."""
+    cfg = (30, 4, 10)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    q = p.log_q_max
+    rng = np.random.default_rng(31)
+    evks = [(random_poly(rng, p.n, 2 * q), random_poly(rng, p.n, 2 * q)) for _ in range(2)]
+    c1 = (random_poly(rng, p.n, q), random_poly(rng, p.n, q))
+    c2 = (random_poly(rng, p.n, q), random_poly(rng, p.n, q))
+    for evk in (evks[0], evks[1], evks[0], evks[1]):
+        st, wa, wb = restated.he_mul(p.log_n, p.log_p, q, q, c1, c2, evk)
+        oa, ob = ctx.he_mul(c1, c2, q, evk=evk)
+        assert np.array_equal(oa, wa) and np.array_equal(ob, wb)
+    # an equal-content copy is a different key object: rebuilt, same result
+    copy = (evks[1][0].copy(), evks[1][1].copy())
+    oa2, ob2 = ctx.he_mul(c1, c2, q, evk=copy)
+    assert np.array_equal(oa2, oa) and np.array_equal(ob2, ob)
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+def test_batch_beyond_grid_row_limit(device):
+    """More rows than gridDim.y allows (65535) in one launch: the context runs
+    the batch in sub-batches (context.cu row limits)."""
+    torch = pytest.importorskip("torch")
+    cfg = (30, 4, 10)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    q = p.log_q_max
+    info = ctx.engine_info(q)
+    rows_per_pair = max(8 * info["np1"], 2 * info["np2"])
+    B = 65535 // rows_per_pair + 37
+    rng = np.random.default_rng(5)
+    evk = (random_poly(rng, p.n, 2 * q), random_poly(rng, p.n, 2 * q))
+    base = [[random_poly(rng, p.n, q) for _ in range(4)] for _ in range(3)]
+    singles = [ctx.he_mul((b[0], b[1]), (b[2], b[3]), q, evk=evk) for b in base]
+    polys = [np.stack([base[i % 3][t] for i in range(B)]) for t in range(4)]
+    if device:
+        polys = [torch.from_numpy(x).cuda() for x in polys]
+    oa, ob = ctx.he_mul((polys[0], polys[1]), (polys[2], polys[3]), q, evk=evk)
+    if device:
+        ctx.synchronize()
+        oa, ob = oa.cpu().numpy(), ob.cpu().numpy()
+    assert oa.shape[0] == B
+    for i in (0, 1, 2, B // 2, B - 1):
+        assert np.array_equal(oa[i], singles[i % 3][0]) and np.array_equal(ob[i], singles[i % 3][1])
