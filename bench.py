@@ -307,6 +307,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--latency-reps", type=int, default=5)
+    ap.add_argument("--chain", type=int, default=8,
+                    help="device-resident chain length for the `chain` key (0 = skip)")
     ap.add_argument("--basis", type=int, default=32, choices=[32, 64],
                     help="RNS basis of he_mul (HEMUL_OPT_BASIS); results are identical")
     ap.add_argument("--engine", default="tc", choices=["tc", "imad"],
@@ -445,6 +447,47 @@ def main() -> None:
     if not torch.equal(ho[0], out[0].cpu()):
         raise RuntimeError("e2e output differs from the device-resident output")
 
+    # ---- device-resident chain: B accumulators times K
+    # fresh ciphertexts down K levels (mod_down on the device), one upload of
+    # every operand and one download of the result inside the timed region;
+    # every level's tables and evk forms warmed by an untimed first pass
+    K = args.chain
+    chain = None
+    if K > 0:
+        ctx.set_level_cache(K + 1)
+        hf = [tuple(rand_poly(B, q).cpu().pin_memory() for _ in range(2)) for _ in range(K)]
+        ha = (nph(hc1[0]), nph(hc1[1]))
+        hres = tuple(torch.empty((B, n, limbs(q - K * p.log_p)), dtype=torch.uint64).pin_memory()
+                     for _ in range(2))
+
+        def run_chain():
+            # pinned sources, queued on the copy stream: operand k+1 crosses
+            # PCIe while HE Mul k runs
+            acc = ctx.upload(ha, q, asynchronous=True)
+            fresh = [ctx.upload((nph(f[0]), nph(f[1])), q, asynchronous=True) for f in hf]
+            for f in fresh:
+                f = ctx.mod_down_dev(f, acc.log_q) if f.log_q > acc.log_q else f
+                acc = ctx.he_mul_dev(acc, f, evk=evk, evk_id=1)
+            acc.download(out=(nph(hres[0]), nph(hres[1])))  # into pinned host buffers
+            return acc.log_q
+
+        run_chain()
+        torch.cuda.synchronize()
+        barrier()
+        c0, c1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        final_q = run_chain()
+        c1e.record(stream)
+        torch.cuda.synchronize()
+        chain_ms = max_over_ranks(c0.elapsed_time(c1e), device="cuda")
+        chain = {"value": world * B * K / (chain_ms / 1000.0), "unit": "HE Mul/s",
+                 "chain_len": K, "batch_per_gpu": B, "ms": chain_ms,
+                 "levels": f"{q} -> {final_q}",
+                 "h2d_bytes": (K + 1) * 2 * B * n * L * 8,
+                 "d2h_bytes": 2 * B * n * limbs(final_q) * 8,
+                 "note": "one H2D of every operand and one D2H of the result per chain "
+                         "(hemul_gpu_ct_* handles); level LRU sized to the chain"}
+
     # ---- result digests gathered to rank 0 (after timing) ------------------
     o0 = out[0][0].cpu().numpy(), out[1][0].cpu().numpy()
     dig = ciphertext_digest(q - p.log_p, o0[0], o0[1])
@@ -529,6 +572,7 @@ def main() -> None:
             "e2e": {"value": e2e_value, "unit": "HE Mul/s",
                     "h2d_bytes_per_step": 4 * B * n * L * 8,
                     "d2h_bytes_per_step": 2 * B * n * Lo * 8},
+            "chain": chain,
             "roofline": roof,
             "kernels": per_class,
             "engine": "int8 tensor cores (tcgen05)" if tensor else "IMAD.WIDE integer pipe",

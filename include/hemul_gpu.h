@@ -147,6 +147,46 @@ hemul_status hemul_gpu_he_mul_trace(hemul_gpu_ctx *ctx, int log_q, size_t batch,
                                     uint64_t evk_id, int checkpoint, void *dst, size_t cap,
                                     size_t *written);
 
+/* ---- device-resident ciphertexts (HE Mul chains without host copies) -----
+ * The reference's Ciphertext is a host value (heaan.hpp:38-42); a chain such
+ * as the multiplication ladder (test_heaan.cpp:143-167) copies every operand
+ * and result across PCIe when driven through hemul_gpu_he_mul with host
+ * buffers. A handle keeps a batch of ciphertexts {ax, bx, log_q} in device
+ * memory (stream-ordered pool); the operations below queue kernels on the
+ * context stream and return without waiting; only create (from host memory)
+ * and download synchronise. Results are new handles; the caller destroys
+ * every handle it receives (hemul_gpu_ct_destroy, ordered on ctx's stream;
+ * ctx = NULL frees synchronously). */
+typedef struct hemul_gpu_ct hemul_gpu_ct;
+/* batch ciphertexts at modulus log_q from BigPoly buffers (host or device;
+ * NULL = zero polynomials). flags = 0: returns after the copy (the sources
+ * may be reused at once). HEMUL_CT_ASYNC: the copy is queued on the
+ * context's copy stream and overlaps kernels already queued; later work on
+ * the handle waits for it; pinned sources must stay unchanged until the next
+ * synchronising call (download / hemul_gpu_synchronize). */
+enum { HEMUL_CT_ASYNC = 1 };
+hemul_status hemul_gpu_ct_create(hemul_gpu_ctx *ctx, int log_q, size_t batch,
+                                 const uint64_t *ax, const uint64_t *bx, int flags,
+                                 hemul_gpu_ct **out);
+void hemul_gpu_ct_destroy(hemul_gpu_ctx *ctx, hemul_gpu_ct *ct);
+hemul_status hemul_gpu_ct_info(const hemul_gpu_ct *ct, int *log_q, size_t *batch);
+/* device addresses of the ax / bx batches (n x ceil(log_q/64) words each per
+ * ciphertext), e.g. to wrap them in framework tensors */
+hemul_status hemul_gpu_ct_device_ptrs(const hemul_gpu_ct *ct, uint64_t **ax, uint64_t **bx);
+hemul_status hemul_gpu_ct_download(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, uint64_t *ax,
+                                   uint64_t *bx);
+/* Scheme::he_mul (heaan.cpp:339-410) on two handles of equal batch; same
+ * checks and errors as hemul_gpu_he_mul; *out at log_q - log_p. */
+hemul_status hemul_gpu_ct_he_mul(hemul_gpu_ctx *ctx, const hemul_gpu_ct *c1,
+                                 const hemul_gpu_ct *c2, const uint64_t *evk_ax,
+                                 const uint64_t *evk_bx, uint64_t evk_id, hemul_gpu_ct **out);
+/* Scheme::rescale (heaan.cpp:328-337) */
+hemul_status hemul_gpu_ct_rescale(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, hemul_gpu_ct **out);
+/* poly_mod_down (poly.cpp:117-127) of both polynomials to new_log_q <= log_q:
+ * the ladder's modulus alignment (test_heaan.cpp:154-160) */
+hemul_status hemul_gpu_ct_mod_down(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, int new_log_q,
+                                   hemul_gpu_ct **out);
+
 /* Scheme::rescale (heaan.cpp:328-337) on a batch: n x ceil(log_q/64) ->
  * n x ceil((log_q - log_p)/64). */
 hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, const uint64_t *ax,
@@ -166,7 +206,12 @@ hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, cons
  * base conversions run as exact u8 x u8 -> s32 GEMMs on the tcgen05 tensor
  * cores; 0 selects the IMAD.WIDE integer-pipe kernels. Results are
  * bit-identical either way. */
-enum { HEMUL_OPT_FORCE_EXACT = 1, HEMUL_OPT_BASIS = 2, HEMUL_OPT_TENSOR_CORES = 3 };
+enum { HEMUL_OPT_FORCE_EXACT = 1, HEMUL_OPT_BASIS = 2, HEMUL_OPT_TENSOR_CORES = 3,
+       HEMUL_OPT_LEVEL_CACHE = 4 };
+/* HEMUL_OPT_LEVEL_CACHE: capacity of the level LRU (default 2, the
+ * reference's Scheme::level, heaan.cpp:119-150). A device-resident chain
+ * walks one level per HE Mul; with a larger cache (about 1 GB per level at
+ * N=2^17) a repeated chain keeps every level's tables and evk forms. */
 hemul_status hemul_gpu_set_option(hemul_gpu_ctx *ctx, int option, int value);
 
 /* Device timing. When enabled every launch is bracketed by CUDA events on the

@@ -187,6 +187,7 @@ struct hemul_gpu_ctx {
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
   int basis = 32;       // HEMUL_OPT_BASIS: he_mul prime basis (32 or 64)
   int tensor_cores = 1;  // HEMUL_OPT_TENSOR_CORES: int8 tcgen05 base conversions
+  int level_cache = 2;   // HEMUL_OPT_LEVEL_CACHE: LRU capacity (heaan.cpp:119-150: 2)
 
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
@@ -400,7 +401,7 @@ Level& get_level(hemul_gpu_ctx* c, int log_q) {
   auto lv = std::make_unique<Level>();
   lv->log_q = log_q;
   c->cache.push_front(std::move(lv));
-  while (c->cache.size() > 2) c->cache.pop_back();
+  while (c->cache.size() > size_t(c->level_cache)) c->cache.pop_back();
   return *c->cache.front();
 }
 
@@ -652,6 +653,13 @@ hemul_status hemul_gpu_create(int device, int log_p, int depth, int log_n_overri
         cudaEventCreateWithFlags(&c->ev_comp[s], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventDisableTiming) != cudaSuccess)
       return HEMUL_E_CUDA;
+  // keep freed stream-ordered memory (device ciphertext handles) in the pool
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
   if (ntt_setup_attributes() != cudaSuccess || crt_setup_attributes() != cudaSuccess ||
       crt_tc_setup_attributes() != cudaSuccess || bigint_tc_setup_attributes() != cudaSuccess ||
       icrt_setup_attributes() != cudaSuccess)
@@ -752,6 +760,11 @@ hemul_status hemul_gpu_set_option(hemul_gpu_ctx* c, int option, int value) {
       return HEMUL_OK;
     case HEMUL_OPT_TENSOR_CORES:
       c->tensor_cores = value != 0;
+      return HEMUL_OK;
+    case HEMUL_OPT_LEVEL_CACHE:
+      if (value < 1 || value > 1024) return fail(c, HEMUL_E_ARG, "level cache capacity out of range");
+      c->level_cache = value;
+      while (c->cache.size() > size_t(c->level_cache)) c->cache.pop_back();
       return HEMUL_OK;
     case HEMUL_OPT_BASIS:
       if (value != 32 && value != 64) return fail(c, HEMUL_E_ARG, "basis must be 32 or 64");
@@ -926,6 +939,213 @@ hemul_status hemul_gpu_he_mul_trace(hemul_gpu_ctx* c, int log_q, size_t batch,
     else
       he_mul_device<F32>(c, lv, log_q, batch, in, oa, oa + batch * out_w, &tr);
     if (written) *written = tr.written;
+    return HEMUL_OK;
+  });
+}
+
+}  // extern "C"
+
+// A device-resident ciphertext batch. Its memory comes from the device's
+// stream-ordered pool (cudaMallocAsync on the context stream), so creating
+// and dropping intermediates inside a chain never synchronises the device.
+struct hemul_gpu_ct {
+  int device = 0;
+  int log_q = 0;
+  size_t batch = 0;
+  size_t words = 0;  // per polynomial of the batch: n x ceil(log_q / 64)
+  uint64_t* mem = nullptr;  // [ax batch | bx batch]
+  cudaEvent_t ready = nullptr;  // asynchronous upload still in flight (HEMUL_CT_ASYNC)
+  uint64_t* ax() const { return mem; }
+  uint64_t* bx() const { return mem + batch * words; }
+};
+
+namespace {
+
+struct CtDeleter {
+  cudaStream_t st;
+  void operator()(hemul_gpu_ct* t) const {
+    if (t && t->mem) cudaFreeAsync(t->mem, st);
+    if (t && t->ready) cudaEventDestroy(t->ready);
+    delete t;
+  }
+};
+using CtPtr = std::unique_ptr<hemul_gpu_ct, CtDeleter>;
+
+CtPtr new_ct(hemul_gpu_ctx* c, int log_q, size_t batch) {
+  if (log_q <= 0 || log_q > c->log_q_max) throw std::invalid_argument("log_q out of range");
+  if (batch == 0) throw std::invalid_argument("empty ciphertext batch");
+  CtPtr t(new hemul_gpu_ct, CtDeleter{c->stream});
+  t->device = c->device;
+  t->log_q = log_q;
+  t->batch = batch;
+  t->words = size_t(c->n) * limbs_of(log_q);
+  check(cudaMallocAsync(reinterpret_cast<void**>(&t->mem), 2 * batch * t->words * 8, c->stream),
+        "ciphertext allocation");
+  return t;
+}
+
+// Validates a handle and orders the context stream after its upload.
+void check_ct(const hemul_gpu_ctx* c, const hemul_gpu_ct* t) {
+  if (!t) throw std::invalid_argument("null ciphertext handle");
+  if (t->device != c->device) throw std::invalid_argument("ciphertext on another device");
+  if (t->words != size_t(c->n) * limbs_of(t->log_q))
+    throw std::invalid_argument("ciphertext of another ring degree");
+  if (t->ready) check(cudaStreamWaitEvent(c->stream, t->ready, 0), "wait");
+}
+
+}  // namespace
+
+extern "C" {
+
+hemul_status hemul_gpu_ct_create(hemul_gpu_ctx* c, int log_q, size_t batch, const uint64_t* ax,
+                                 const uint64_t* bx, int flags, hemul_gpu_ct** out) {
+  if (!c || !out || (flags & ~HEMUL_CT_ASYNC)) return HEMUL_E_ARG;
+  *out = nullptr;
+  return guarded(c, [&] {
+    auto t = new_ct(c, log_q, batch);
+    const size_t bytes = batch * t->words * 8;
+    const bool async = flags & HEMUL_CT_ASYNC;
+    // async: the copies run on the copy stream (overlapping kernels already
+    // queued on the context stream), which waits for the allocation; the
+    // context stream then waits for the copies
+    cudaStream_t st = async ? c->h2d : c->stream;
+    cudaEvent_t ev = nullptr;
+    if (async) {
+      check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      check(cudaEventRecord(ev, c->stream), "event");
+      check(cudaStreamWaitEvent(c->h2d, ev, 0), "wait");
+    }
+    for (int s = 0; s < 2; ++s) {
+      const uint64_t* src = s ? bx : ax;
+      uint64_t* dst = s ? t->bx() : t->ax();
+      if (src)
+        run_on(c, st, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D", [&] {
+          return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+        });
+      else
+        check(cudaMemsetAsync(dst, 0, bytes, st), "ciphertext zero");
+    }
+    if (async) {
+      // the first operation that reads the handle waits for this event
+      check(cudaEventRecord(ev, c->h2d), "event");
+      t->ready = ev;
+    } else {
+      // host sources may be reused by the caller as soon as this returns
+      check(cudaStreamSynchronize(c->stream), "ciphertext upload");
+    }
+    *out = t.release();
+    return HEMUL_OK;
+  });
+}
+
+void hemul_gpu_ct_destroy(hemul_gpu_ctx* c, hemul_gpu_ct* t) {
+  if (!t) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(t->device);
+  if (c && c->device == t->device) {
+    if (t->ready) cudaStreamWaitEvent(c->stream, t->ready, 0);  // an upload still in flight
+    cudaFreeAsync(t->mem, c->stream);  // after the work queued on the context stream
+  } else {
+    cudaDeviceSynchronize();
+    cudaFree(t->mem);
+  }
+  if (t->ready) cudaEventDestroy(t->ready);
+  delete t;
+  cudaSetDevice(cur);
+}
+
+hemul_status hemul_gpu_ct_info(const hemul_gpu_ct* t, int* log_q, size_t* batch) {
+  if (!t) return HEMUL_E_ARG;
+  if (log_q) *log_q = t->log_q;
+  if (batch) *batch = t->batch;
+  return HEMUL_OK;
+}
+
+hemul_status hemul_gpu_ct_device_ptrs(const hemul_gpu_ct* t, uint64_t** ax, uint64_t** bx) {
+  if (!t) return HEMUL_E_ARG;
+  if (ax) *ax = t->ax();
+  if (bx) *bx = t->bx();
+  return HEMUL_OK;
+}
+
+hemul_status hemul_gpu_ct_download(hemul_gpu_ctx* c, const hemul_gpu_ct* t, uint64_t* ax,
+                                   uint64_t* bx) {
+  if (!c || !t || !ax || !bx) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    check_ct(c, t);
+    const size_t bytes = t->batch * t->words * 8;
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
+        [&] { return cudaMemcpyAsync(ax, t->ax(), bytes, cudaMemcpyDefault, c->stream); });
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
+        [&] { return cudaMemcpyAsync(bx, t->bx(), bytes, cudaMemcpyDefault, c->stream); });
+    check(cudaStreamSynchronize(c->stream), "ciphertext download");
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_ct_he_mul(hemul_gpu_ctx* c, const hemul_gpu_ct* c1, const hemul_gpu_ct* c2,
+                                 const uint64_t* evk_ax, const uint64_t* evk_bx, uint64_t evk_id,
+                                 hemul_gpu_ct** out) {
+  if (!c || !c1 || !c2 || !out) return HEMUL_E_ARG;
+  *out = nullptr;
+  if (c1->log_q != c2->log_q)
+    return fail(c, HEMUL_E_MODULUS_MISMATCH, "ciphertext modulus mismatch");
+  const int log_q = c1->log_q;
+  if (log_q - c->log_p < c->log_p)
+    return fail(c, HEMUL_E_DEPTH, "multiplicative depth exhausted");
+  if (c1->batch != c2->batch) return fail(c, HEMUL_E_ARG, "ciphertext batches differ");
+  return guarded(c, [&]() -> hemul_status {
+    check_ct(c, c1);
+    check_ct(c, c2);
+    Level& lv = get_level(c, log_q);
+    const int word = mul_word(c, lv);
+    if (evk_ax && evk_bx &&
+        (!lv.has_evk || evk_id == 0 || lv.evk_id != evk_id || lv.evk_word != word))
+      set_evk_forms(c, lv, evk_ax, evk_bx, evk_id);
+    if (!lv.has_evk || lv.evk_word != word)
+      return fail(c, HEMUL_E_NO_EVK, "evaluation key not set for this level");
+    auto r = new_ct(c, log_q - c->log_p, c1->batch);
+    ++c->call_id;
+    const uint64_t* in[4] = {c1->ax(), c1->bx(), c2->ax(), c2->bx()};
+    he_mul_any(c, lv, log_q, c1->batch, in, r->ax(), r->bx());
+    *out = r.release();  // asynchronous: ordered on the context stream
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_ct_rescale(hemul_gpu_ctx* c, const hemul_gpu_ct* t, hemul_gpu_ct** out) {
+  if (!c || !t || !out) return HEMUL_E_ARG;
+  *out = nullptr;
+  if (t->log_q - c->log_p < c->log_p)
+    return fail(c, HEMUL_E_DEPTH, "modulus exhausted; cannot rescale");
+  return guarded(c, [&] {
+    check_ct(c, t);
+    auto r = new_ct(c, t->log_q - c->log_p, t->batch);
+    for (int s = 0; s < 2; ++s)
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "rescale", [&] {
+        return shift_right(s ? t->bx() : t->ax(), s ? r->bx() : r->ax(), t->batch, c->log_n,
+                           t->log_q, c->log_p, c->stream);
+      });
+    *out = r.release();
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_ct_mod_down(hemul_gpu_ctx* c, const hemul_gpu_ct* t, int new_log_q,
+                                   hemul_gpu_ct** out) {
+  if (!c || !t || !out) return HEMUL_E_ARG;
+  *out = nullptr;
+  if (new_log_q <= 0 || new_log_q > t->log_q) return fail(c, HEMUL_E_ARG, "new_log_q out of range");
+  return guarded(c, [&] {
+    check_ct(c, t);
+    auto r = new_ct(c, new_log_q, t->batch);
+    for (int s = 0; s < 2; ++s)
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "mod_down", [&] {
+        return mod_down(s ? t->bx() : t->ax(), s ? r->bx() : r->ax(), t->batch, c->log_n,
+                        t->log_q, new_log_q, c->stream);
+      });
+    *out = r.release();
     return HEMUL_OK;
   });
 }

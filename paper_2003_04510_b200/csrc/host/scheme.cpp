@@ -325,6 +325,87 @@ Ciphertext Scheme::he_mul(const Ciphertext& c1, const Ciphertext& c2, const Eval
   return out;
 }
 
+// ---- device-resident ciphertexts ---------------------------------------------
+
+DeviceCiphertext::DeviceCiphertext(hemul_gpu_ctx* ctx, hemul_gpu_ct* h, int q, int slots)
+    : log_q(q), n_slots(slots), ctx_(ctx), h_(h) {}
+
+DeviceCiphertext::~DeviceCiphertext() { hemul_gpu_ct_destroy(ctx_, h_); }
+
+DeviceCiphertext::DeviceCiphertext(DeviceCiphertext&& o) noexcept
+    : log_q(o.log_q), n_slots(o.n_slots), ctx_(o.ctx_), h_(o.h_) {
+  o.h_ = nullptr;
+}
+
+DeviceCiphertext& DeviceCiphertext::operator=(DeviceCiphertext&& o) noexcept {
+  if (this != &o) {
+    hemul_gpu_ct_destroy(ctx_, h_);
+    log_q = o.log_q;
+    n_slots = o.n_slots;
+    ctx_ = o.ctx_;
+    h_ = o.h_;
+    o.h_ = nullptr;
+  }
+  return *this;
+}
+
+DeviceCiphertext Scheme::upload(const Ciphertext& c) const {
+  hemul_gpu_ctx* g = gpu();
+  if (c.ax.log_q != c.log_q || c.bx.log_q != c.log_q || c.ax.n != params_.n)
+    throw std::invalid_argument("ciphertext polynomials do not match its modulus");
+  hemul_gpu_ct* h = nullptr;
+  const hemul_status st =
+      hemul_gpu_ct_create(g, c.log_q, 1, c.ax.data.data(), c.bx.data.data(), 0, &h);
+  if (st != HEMUL_OK) throw_status(g, st);
+  return DeviceCiphertext(g, h, c.log_q, c.n_slots);
+}
+
+Ciphertext Scheme::download(const DeviceCiphertext& c) const {
+  hemul_gpu_ctx* g = gpu();
+  if (c.empty()) throw std::invalid_argument("empty device ciphertext");
+  Ciphertext r;
+  r.ax = make_poly(params_.n, c.log_q, params_.word);
+  r.bx = make_poly(params_.n, c.log_q, params_.word);
+  const hemul_status st = hemul_gpu_ct_download(g, c.h_, r.ax.data.data(), r.bx.data.data());
+  if (st != HEMUL_OK) throw_status(g, st);
+  r.log_q = c.log_q;
+  r.n_slots = c.n_slots;
+  return r;
+}
+
+DeviceCiphertext Scheme::he_mul(const DeviceCiphertext& c1, const DeviceCiphertext& c2,
+                                const EvalKey& evk) {
+  if (c1.log_q != c2.log_q) throw std::invalid_argument("ciphertext modulus mismatch");
+  if (c1.log_q - params_.log_p < params_.log_p)
+    throw std::runtime_error("multiplicative depth exhausted");
+  hemul_gpu_ctx* g = gpu();
+  hemul_gpu_ct* h = nullptr;
+  const hemul_status st = hemul_gpu_ct_he_mul(g, c1.h_, c2.h_, evk.ax.data.data(),
+                                              evk.bx.data.data(),
+                                              reinterpret_cast<uintptr_t>(&evk), &h);
+  if (st != HEMUL_OK) throw_status(g, st);
+  evk_src_ = &evk;
+  return DeviceCiphertext(g, h, c1.log_q - params_.log_p, std::max(c1.n_slots, c2.n_slots));
+}
+
+DeviceCiphertext Scheme::rescale(const DeviceCiphertext& c) const {
+  if (c.log_q - params_.log_p < params_.log_p)
+    throw std::runtime_error("modulus exhausted; cannot rescale");
+  hemul_gpu_ctx* g = gpu();
+  hemul_gpu_ct* h = nullptr;
+  const hemul_status st = hemul_gpu_ct_rescale(g, c.h_, &h);
+  if (st != HEMUL_OK) throw_status(g, st);
+  return DeviceCiphertext(g, h, c.log_q - params_.log_p, c.n_slots);
+}
+
+DeviceCiphertext Scheme::mod_down(const DeviceCiphertext& c, int new_log_q) const {
+  hemul_gpu_ctx* g = gpu();
+  hemul_gpu_ct* h = nullptr;
+  const hemul_status st = hemul_gpu_ct_mod_down(g, c.h_, new_log_q, &h);
+  if (st != HEMUL_OK) throw_status(g, st);
+  return DeviceCiphertext(g, h, new_log_q, c.n_slots);
+}
+
 // The reference algorithm's operation counts for one he_mul (rns.cpp:345-355,
 // 370, 385-391; ntt.cpp:168-173, 191-196; call counts heaan.cpp:372-402).
 void Scheme::count_he_mul(int log_q) {

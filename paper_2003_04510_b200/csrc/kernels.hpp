@@ -282,6 +282,10 @@ cudaError_t evk_product(const typename F::W* f, const typename F::W* ea, const t
 // d: n x ceil(log_q/64), out: n x ceil((log_q-log_p)/64); batch of each.
 cudaError_t keyswitch_epilogue(const uint64_t* ks, const uint64_t* d, uint64_t* out, size_t batch,
                                int log_n, int log_q, int log_Q, int log_p, cudaStream_t st);
+// poly_mod_down (poly.cpp:117-127) on a poly batch: n x ceil(log_q/64) ->
+// n x ceil(new_log_q/64), top limb masked.
+cudaError_t mod_down(const uint64_t* a, uint64_t* out, size_t batch, int log_n, int log_q,
+                     int new_log_q, cudaStream_t st);
 // Scheme::rescale on one poly batch (poly_shift_right, poly.cpp:98-115).
 cudaError_t shift_right(const uint64_t* a, uint64_t* out, size_t batch, int log_n, int log_q,
                         int bits, cudaStream_t st);

@@ -157,6 +157,19 @@ __global__ void shift_right_kernel(const uint64_t* __restrict__ a, uint64_t* __r
   }
 }
 
+// poly_mod_down (poly.cpp:117-127): the low ceil(new_log_q / 64) limbs of
+// each coefficient, top limb masked; one thread per output word.
+__global__ void mod_down_kernel(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
+                                size_t words, int L, int Lo, uint64_t top_mask) {
+  for (size_t o = blockIdx.x * size_t(blockDim.x) + threadIdx.x; o < words;
+       o += size_t(gridDim.x) * blockDim.x) {
+    const size_t i = o / Lo;
+    const int k = static_cast<int>(o - i * Lo);
+    const uint64_t v = a[i * L + k];
+    out[o] = k == Lo - 1 ? v & top_mask : v;
+  }
+}
+
 unsigned grid_for(size_t total, int threads) {
   size_t blocks = (total + threads - 1) / threads;
   const size_t cap = 148 * 64;
@@ -216,6 +229,17 @@ cudaError_t keyswitch_epilogue(const uint64_t* ks, const uint64_t* d, uint64_t* 
   const size_t total = batch << log_n;
   keyswitch_epilogue_kernel<<<grid_for(total, 128), 128, 0, st>>>(ks, d, out, total, log_q,
                                                                    log_Q, log_p);
+  return cudaGetLastError();
+}
+
+cudaError_t mod_down(const uint64_t* a, uint64_t* out, size_t batch, int log_n, int log_q,
+                     int new_log_q, cudaStream_t st) {
+  if (new_log_q <= 0 || new_log_q > log_q) return cudaErrorInvalidValue;
+  const int L = (log_q + 63) / 64, Lo = (new_log_q + 63) / 64;
+  const size_t words = (batch << log_n) * size_t(Lo);
+  const int rest = new_log_q - 64 * (Lo - 1);
+  const uint64_t top = rest == 64 ? ~uint64_t(0) : (uint64_t(1) << rest) - 1;
+  mod_down_kernel<<<grid_for(words, 256), 256, 0, st>>>(a, out, words, L, Lo, top);
   return cudaGetLastError();
 }
 

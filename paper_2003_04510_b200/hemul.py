@@ -99,6 +99,24 @@ _SIGS = {
                                               ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t)]),
 }
+_SIGS.update({
+    "hemul_gpu_ct_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, _u64p,
+                                           _u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "hemul_gpu_ct_destroy": (None, [ctypes.c_void_p, ctypes.c_void_p]),
+    "hemul_gpu_ct_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
+                                         ctypes.POINTER(ctypes.c_size_t)]),
+    "hemul_gpu_ct_device_ptrs": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
+                                                ctypes.POINTER(ctypes.c_void_p)]),
+    "hemul_gpu_ct_download": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _u64p, _u64p]),
+    "hemul_gpu_ct_he_mul": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           _u64p, _u64p, ctypes.c_uint64,
+                                           ctypes.POINTER(ctypes.c_void_p)]),
+    "hemul_gpu_ct_rescale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.POINTER(ctypes.c_void_p)]),
+    "hemul_gpu_ct_mod_down": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_void_p)]),
+})
+HEMUL_OPT_LEVEL_CACHE = 4
 ENGINE_INFO = ("word", "np1", "np2", "split_h", "crt1_tc", "crt2_tc", "big_tc", "fused_mid",
                "blk_mont")  # HEMUL_INFO_* in include/hemul_gpu.h
 TRACE_POINTS = {"crt1": 1, "prod1": 2, "d2": 3, "crt2": 4, "prod2": 5}  # HEMUL_TRACE_*
@@ -123,6 +141,56 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     if path is None:
         _lib = lib
     return lib
+
+
+class DeviceCiphertext:
+    """A batch of ciphertexts resident in device memory (hemul_gpu_ct): the
+    operands of a device-resident HE Mul chain. Operations on it queue work
+    on the context stream; ``download`` returns host arrays."""
+
+    def __init__(self, ctx: "Context", handle: ctypes.c_void_p):
+        self._ctx = ctx
+        self._h = handle
+        q = ctypes.c_int()
+        b = ctypes.c_size_t()
+        ctx._check(ctx._lib.hemul_gpu_ct_info(handle, ctypes.byref(q), ctypes.byref(b)))
+        self.log_q = q.value
+        self.batch = b.value
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        n, L = self._ctx.n, limbs(self.log_q)
+        return (self.batch, n, L) if self.batch > 1 else (n, L)
+
+    def download(self, out: tuple[Any, Any] | None = None) -> tuple[Any, Any]:
+        """(ax, bx) to host arrays (or into `out`: pinned host buffers make the
+        copy run at full PCIe speed; device tensors work too)."""
+        if out is None:
+            out = (np.empty(self.shape, np.uint64), np.empty(self.shape, np.uint64))
+        n_words = self.batch * self._ctx.n * limbs(self.log_q)
+        if _size(out[0]) != n_words or _size(out[1]) != n_words:
+            raise ValueError("download buffers do not match the ciphertext batch")
+        self._ctx._check(self._ctx._lib.hemul_gpu_ct_download(self._ctx._h, self._h,
+                                                              _ptr(out[0]), _ptr(out[1])))
+        return out
+
+    def device_ptrs(self) -> tuple[int, int]:
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        self._ctx._check(self._ctx._lib.hemul_gpu_ct_device_ptrs(self._h, ctypes.byref(a),
+                                                                 ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            ctx = self._ctx
+            ctx._lib.hemul_gpu_ct_destroy(ctx._h if ctx._h else None, self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass(frozen=True)
@@ -302,6 +370,47 @@ class Context:
         self._check(self._lib.hemul_gpu_rescale(self._h, log_q, batch, _ptr(c[0]), _ptr(c[1]),
                                                 _ptr(out[0]), _ptr(out[1])))
         return out
+
+    # -- device-resident chains (hemul_gpu_ct_*) -----------------------------
+    def upload(self, c: tuple[Any, Any], log_q: int, asynchronous: bool = False) -> DeviceCiphertext:
+        """Ciphertext(s) (ax, bx) of shape (n, limbs) or (batch, n, limbs) into
+        device memory. asynchronous=True queues the copy on the copy stream
+        (HEMUL_CT_ASYNC): the sources must stay alive and unchanged until the
+        next download / synchronize."""
+        per = self.n * limbs(log_q)
+        batch = _size(c[0]) // per
+        if batch * per != _size(c[0]) or _size(c[1]) != _size(c[0]):
+            raise ValueError("ciphertext buffers are not batch x n x limbs")
+        h = ctypes.c_void_p()
+        self._check(self._lib.hemul_gpu_ct_create(self._h, log_q, batch, _ptr(c[0]), _ptr(c[1]),
+                                                  int(asynchronous), ctypes.byref(h)))
+        return DeviceCiphertext(self, h)
+
+    def he_mul_dev(self, c1: DeviceCiphertext, c2: DeviceCiphertext,
+                   evk: tuple[Any, Any] | None = None,
+                   evk_id: int | None = None) -> DeviceCiphertext:
+        """Scheme::he_mul on device-resident operands; the result stays on the device."""
+        h = ctypes.c_void_p()
+        ea = _ptr(evk[0]) if evk is not None else None
+        eb = _ptr(evk[1]) if evk is not None else None
+        self._check(self._lib.hemul_gpu_ct_he_mul(self._h, c1._h, c2._h, ea, eb,
+                                                  self._evk_identity(evk, evk_id), ctypes.byref(h)))
+        return DeviceCiphertext(self, h)
+
+    def rescale_dev(self, c: DeviceCiphertext) -> DeviceCiphertext:
+        h = ctypes.c_void_p()
+        self._check(self._lib.hemul_gpu_ct_rescale(self._h, c._h, ctypes.byref(h)))
+        return DeviceCiphertext(self, h)
+
+    def mod_down_dev(self, c: DeviceCiphertext, new_log_q: int) -> DeviceCiphertext:
+        """poly_mod_down (poly.cpp:117-127) of both polynomials."""
+        h = ctypes.c_void_p()
+        self._check(self._lib.hemul_gpu_ct_mod_down(self._h, c._h, new_log_q, ctypes.byref(h)))
+        return DeviceCiphertext(self, h)
+
+    def set_level_cache(self, capacity: int) -> None:
+        """Level LRU capacity (default 2 like Scheme::level, heaan.cpp:119-150)."""
+        self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_LEVEL_CACHE, capacity))
 
     def engine_info(self, log_q: int) -> dict[str, int]:
         """Basis and kernels he_mul uses at level log_q (hemul_gpu_engine_info)."""

@@ -9,6 +9,9 @@
 //   dropin_check ladder <log_p> <depth> <log_n> <seed>                (GPU)
 //       test_heaan.cpp:143-167: he_mul down the modulus chain, decrypting
 //       and decoding after each step; prints "max_err <e>"; exit 1 on > 1e-3
+//   dropin_check ladder_dev <log_p> <depth> <log_n> <seed>            (GPU)
+//       the ladder on DeviceCiphertext (upload / he_mul / mod_down /
+//       download); each step bit-identical to the host-API step
 //   dropin_check errors                                                (GPU)
 //       test_heaan.cpp:169-182: modulus mismatch / exhausted depth throw
 #include <cmath>
@@ -102,6 +105,41 @@ int cmd_ladder(int log_p, int depth, int log_n, uint64_t seed) {
   return worst < 1e-3 && acc.log_q == p.log_q_max - (depth - 2) * p.log_p ? 0 : 1;
 }
 
+// The same ladder with the accumulator resident on the GPU (Scheme::upload /
+// he_mul / mod_down on DeviceCiphertext): every step must equal the host-API
+// step bit for bit, and only the fresh operands cross PCIe.
+int cmd_ladder_dev(int log_p, int depth, int log_n, uint64_t seed) {
+  const Params p = make_params(log_p, depth, WordSize::w64, log_n);
+  Scheme sch(p);
+  Rng rng(seed);
+  const KeySet keys = sch.keygen(rng);
+  Message want = random_message(8, rng);
+  Ciphertext acc = sch.encrypt(sch.encode(want), keys.pk, rng);
+  DeviceCiphertext dacc = sch.upload(acc);
+  double worst = 0;
+  int mismatches = 0;
+  for (int step = 0; step < depth - 2; ++step) {
+    const Message m = random_message(8, rng);
+    Ciphertext c = sch.encrypt(sch.encode(m), keys.pk, rng);
+    DeviceCiphertext dc = sch.upload(c);
+    if (dc.log_q > dacc.log_q) dc = sch.mod_down(dc, dacc.log_q);
+    if (c.log_q > acc.log_q) {
+      c.ax = poly_mod_down(c.ax, acc.log_q);
+      c.bx = poly_mod_down(c.bx, acc.log_q);
+      c.log_q = acc.log_q;
+    }
+    acc = sch.he_mul(acc, c, keys.evk);
+    dacc = sch.he_mul(dacc, dc, keys.evk);
+    const Ciphertext got = sch.download(dacc);
+    if (got.log_q != acc.log_q || !poly_equal(got.ax, acc.ax) || !poly_equal(got.bx, acc.bx))
+      ++mismatches;
+    for (size_t i = 0; i < want.slots.size(); ++i) want.slots[i] *= m.slots[i];
+    worst = std::max(worst, max_err(sch.decode(sch.decrypt(got, keys.sk)), want));
+  }
+  std::printf("max_err %.3e final_log_q %d mismatches %d\n", worst, dacc.log_q, mismatches);
+  return worst < 1e-3 && mismatches == 0 ? 0 : 1;
+}
+
 int cmd_errors() {
   const Params p = make_params(30, 4, WordSize::w64, 10);
   Scheme sch(p);
@@ -140,6 +178,8 @@ int main(int argc, char** argv) {
       return cmd_bench(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10), arg(6));
     if (cmd == "ladder" && argc == 6)
       return cmd_ladder(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10));
+    if (cmd == "ladder_dev" && argc == 6)
+      return cmd_ladder_dev(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10));
     if (cmd == "errors") return cmd_errors();
     std::fprintf(stderr, "usage: see the header of tests/cpp/dropin_check.cpp\n");
     return 2;

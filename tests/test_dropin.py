@@ -71,3 +71,14 @@ def test_ladder_decrypts():
 def test_error_kinds():
     res = _run("errors")
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [(30, 6, 11), (30, 10, 13)])
+def test_ladder_device_resident(cfg):
+    """Scheme::upload / he_mul / mod_down / download on DeviceCiphertext: the
+    ladder (test_heaan.cpp:143-167) with the accumulator kept in HBM equals the
+    host-API ladder bit for bit at every step and decrypts correctly."""
+    res = _run("ladder_dev", *cfg, 7)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "mismatches 0" in res.stdout

@@ -138,3 +138,28 @@ def test_engine_info_levels_at_paper_scale():
         assert info["word"] == 32
         assert info["crt1_tc"] and info["crt2_tc"] and info["big_tc"], (log_q, info)
     ctx.close()
+
+
+@pytest.mark.slow
+def test_every_level_of_the_logQ2400_ladder(restated):
+    """he_mul at all 79 levels of logQ = 2400 (N = 4096) in both engines of the
+    30-bit basis against the C restatement: every split point / byte-window
+    shape the X ladder produces."""
+    cfg = (30, 80, 12)
+    ctxs = {tc: _ctx(cfg, tc) for tc in (True, False)}
+    p = ctxs[True].params
+    rng = np.random.default_rng(2400)
+    evk = (random_poly(rng, p.n, 2 * p.log_q_max), random_poly(rng, p.n, 2 * p.log_q_max))
+    for log_q in range(p.log_q_max, 2 * p.log_p - 1, -p.log_p):
+        c1 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
+        c2 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
+        st, wa, wb = restated.he_mul(p.log_n, p.log_p, p.log_q_max, log_q, c1, c2, evk)
+        assert st == 0
+        for tc, ctx in ctxs.items():
+            if tc:
+                info = ctx.engine_info(log_q)
+                assert info["crt1_tc"] and info["crt2_tc"] and info["big_tc"], (log_q, info)
+            oa, ob = ctx.he_mul(c1, c2, log_q, evk=evk)
+            assert np.array_equal(oa, wa) and np.array_equal(ob, wb), (log_q, tc)
+    for ctx in ctxs.values():
+        ctx.close()

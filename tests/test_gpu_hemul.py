@@ -325,3 +325,95 @@ def test_batch_beyond_grid_row_limit(device):
     assert oa.shape[0] == B
     for i in (0, 1, 2, B // 2, B - 1):
         assert np.array_equal(oa[i], singles[i % 3][0]) and np.array_equal(ob[i], singles[i % 3][1])
+
+
+# ---- device-resident chains -----------------------------
+
+def _mod_down_np(a, log_q, new_log_q):
+    """poly_mod_down (poly.cpp:117-127) on a host BigPoly."""
+    L = (new_log_q + 63) // 64
+    out = np.ascontiguousarray(a[..., :L]).copy()
+    if new_log_q % 64:
+        out[..., -1] &= np.uint64((1 << (new_log_q % 64)) - 1)
+    return out
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("basis", ["32tc", "64"])
+def test_device_chain_paper_scale_vs_reference(basis, reference):
+    """A 4-step HE Mul chain at N=2^17 / logQ=2400 with every operand resident
+    in HBM (upload once, mod_down on the device, download once) equals the
+    reference's he_mul applied step by step."""
+    import os
+
+    cfg = (30, 80, 0)
+    key = ("chain", cfg)
+    if key not in _REF_CACHE:
+        log_n, n, qmax = reference.make_params(*cfg)
+        rng = np.random.default_rng(4242)
+        evk = (random_poly(rng, n, 2 * qmax), random_poly(rng, n, 2 * qmax))
+        acc = (random_poly(rng, n, qmax), random_poly(rng, n, qmax))
+        fresh = [(random_poly(rng, n, qmax), random_poly(rng, n, qmax)) for _ in range(4)]
+        want, q = [], qmax
+        cur = acc
+        for c in fresh:
+            cd = (_mod_down_np(c[0], qmax, q), _mod_down_np(c[1], qmax, q))
+            st, wa, wb = reference.he_mul(*cfg, q, cur, cd, evk, threads=os.cpu_count() or 1)
+            assert st == 0, reference.err()
+            cur = (wa, wb)
+            q -= cfg[0]
+            want.append(cur)
+        _REF_CACHE[key] = (evk, acc, fresh, want)
+    evk, acc, fresh, want = _REF_CACHE[key]
+    ctx = _ctx(cfg, basis)
+    ctx.set_level_cache(4)
+    qmax = ctx.params.log_q_max
+    dacc = ctx.upload(acc, qmax)
+    dfresh = [ctx.upload(c, qmax) for c in fresh]
+    outs = []
+    for k, dc in enumerate(dfresh):
+        if dc.log_q > dacc.log_q:
+            dc = ctx.mod_down_dev(dc, dacc.log_q)
+        dacc = ctx.he_mul_dev(dacc, dc, evk=evk)
+        outs.append(dacc)
+    for k, (o, w) in enumerate(zip(outs, want)):
+        ga, gb = o.download()
+        assert o.log_q == qmax - (k + 1) * 30
+        assert np.array_equal(ga, w[0]) and np.array_equal(gb, w[1]), k
+
+
+def test_device_handles_small_chain(restated):
+    """Handles: upload / he_mul_dev / rescale_dev / mod_down_dev / download
+    against the C restatement and the host-buffer path."""
+    cfg = (30, 6, 11)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    q = p.log_q_max
+    rng = np.random.default_rng(11)
+    evk = (random_poly(rng, p.n, 2 * q), random_poly(rng, p.n, 2 * q))
+    c1 = (random_poly(rng, p.n, q), random_poly(rng, p.n, q))
+    c2 = (random_poly(rng, p.n, q), random_poly(rng, p.n, q))
+    d1, d2 = ctx.upload(c1, q), ctx.upload(c2, q, asynchronous=True)
+    assert np.array_equal(d1.download()[0], c1[0])
+    r = ctx.he_mul_dev(d1, d2, evk=evk)
+    st, wa, wb = restated.he_mul(p.log_n, p.log_p, q, q, c1, c2, evk)
+    ga, gb = r.download()
+    assert r.log_q == q - 30 and np.array_equal(ga, wa) and np.array_equal(gb, wb)
+    rs = ctx.rescale_dev(r)
+    ha, hb = ctx.rescale((wa, wb), q - 30)
+    sa, sb = rs.download()
+    assert np.array_equal(sa, ha) and np.array_equal(sb, hb)
+    md = ctx.mod_down_dev(d1, q - 61)
+    ma, mb = md.download()
+    assert np.array_equal(ma, _mod_down_np(c1[0], q, q - 61))
+    assert np.array_equal(mb, _mod_down_np(c1[1], q, q - 61))
+    with pytest.raises(ValueError, match="ciphertext modulus mismatch"):
+        ctx.he_mul_dev(r, d1, evk=evk)
+    # batched handles
+    B = 3
+    cb1 = [np.stack([random_poly(rng, p.n, q) for _ in range(B)]) for _ in range(2)]
+    cb2 = [np.stack([random_poly(rng, p.n, q) for _ in range(B)]) for _ in range(2)]
+    rb = ctx.he_mul_dev(ctx.upload(tuple(cb1), q), ctx.upload(tuple(cb2), q), evk=evk)
+    ba, bb = rb.download()
+    ha, hb = ctx.he_mul(tuple(cb1), tuple(cb2), q, evk=evk)
+    assert np.array_equal(ba, ha) and np.array_equal(bb, hb)
