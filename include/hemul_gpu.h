@@ -260,6 +260,31 @@ hemul_status hemul_gpu_pointwise(hemul_gpu_ctx *ctx, int log_q, int region, size
 hemul_status hemul_gpu_icrt(hemul_gpu_ctx *ctx, int log_q, int region, size_t batch,
                             const uint64_t *rns, uint64_t *poly);
 
+/* ---- explicit prime sets (the reference's lower-level API) ----------------
+ * crt_forward / rns_pointwise_mul / icrt_reordered / ntt_forward /
+ * ntt_inverse (rns.hpp:62-85, ntt.hpp:34-39) take a caller's PrimeSet and
+ * tables rather than a level. A prime-set object holds the device tables of
+ * w64 primes p_j < 2^62, p_j = 1 mod 2n with primitive 2n-th roots r_j
+ * (generate_primes / make_*_tables, params.cpp:89-239) for ring degree
+ * 2^log_n (1..17; roots = NULL: no NTT tables, any odd p < 2^62, for
+ * CRT / pointwise / iCRT only): CRT weights for inputs of in_bits (0: no CRT), iCRT to
+ * 2^target_bits (0: no iCRT). The calls run the stage kernels on the
+ * context's device and stream, synchronously; layouts as the stage entry
+ * points above (any n; rings below 32 coefficients are padded internally). */
+typedef struct hemul_gpu_rns hemul_gpu_rns;
+hemul_status hemul_gpu_rns_create(hemul_gpu_ctx *ctx, int log_n, const uint64_t *primes,
+                                  const uint64_t *roots, int np, int in_bits, int target_bits,
+                                  hemul_gpu_rns **out);
+void hemul_gpu_rns_destroy(hemul_gpu_rns *rns);
+hemul_status hemul_gpu_rns_ntt(hemul_gpu_ctx *ctx, const hemul_gpu_rns *rns, uint64_t *data,
+                               size_t rows, int inverse);
+hemul_status hemul_gpu_rns_crt(hemul_gpu_ctx *ctx, const hemul_gpu_rns *rns, size_t batch,
+                               const uint64_t *poly, uint64_t *out);
+hemul_status hemul_gpu_rns_pointwise(hemul_gpu_ctx *ctx, const hemul_gpu_rns *rns, size_t batch,
+                                     const uint64_t *a, const uint64_t *b, uint64_t *out);
+hemul_status hemul_gpu_rns_icrt(hemul_gpu_ctx *ctx, const hemul_gpu_rns *rns, size_t batch,
+                                const uint64_t *data, uint64_t *poly);
+
 /* Number of kernels this library launched since the context was created
  * (the bench reports it as gpu_launches). */
 uint64_t hemul_gpu_launch_count(const hemul_gpu_ctx *ctx);

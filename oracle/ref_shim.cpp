@@ -91,7 +91,78 @@ PmContext ctx_of(const RegionTables& t) {
 
 }  // namespace
 
+namespace {
+
+// FNV-1a over every field of the lower-level tables of one prime set
+// (params.hpp: PrimeSet, CrtTables, NttTables, IcrtTables); the same routine
+// is in tests/cpp/dropin_check.cpp and oracle/ref_shim.cpp.
+struct TableHash {
+  uint64_t h = 1469598103934665603ull;
+  void word(uint64_t v) {
+    for (int k = 0; k < 8; ++k) h = (h ^ ((v >> (8 * k)) & 0xff)) * 1099511628211ull;
+  }
+  void words(const std::vector<uint64_t>& v) {
+    word(v.size());
+    for (uint64_t x : v) word(x);
+  }
+  void pairs(const std::vector<ShoupPair>& v) {
+    word(v.size());
+    for (const ShoupPair& s : v) {
+      word(s.value);
+      word(s.quotient);
+    }
+  }
+};
+
+uint64_t table_digest(int np, int log_n, int log_q, bool w32) {
+  const WordSize w = w32 ? WordSize::w32 : WordSize::w64;
+  const PrimeSet ps = generate_primes(np, log_n, w);
+  const CrtTables ct = make_crt_tables(ps, log_q);
+  const NttTables nt = make_ntt_tables(ps, log_n);
+  const IcrtTables it = make_icrt_tables(ps, bigint_pow2(log_q, w), w);
+  TableHash t;
+  t.word(ps.two_n);
+  t.words(ps.primes);
+  t.words(ps.roots);
+  t.pairs(ps.pair_one);
+  t.pairs(ps.pair_beta);
+  t.pairs(ps.pair_beta2);
+  t.words(ps.product);
+  t.word(ct.np);
+  t.word(ct.q_limbs);
+  t.pairs(ct.pow_beta);
+  t.word(nt.log_n);
+  t.word(nt.n);
+  t.pairs(nt.tw);
+  t.pairs(nt.itw);
+  t.pairs(nt.n_inv);
+  t.word(it.np);
+  t.word(it.p_limbs);
+  t.pairs(it.inv_p);
+  t.words(it.p_div_p);
+  t.words(it.p_div_p_t);
+  t.words(it.big_p);
+  t.words(it.half_p);
+  t.words(it.neg_p_mod);
+  for (const auto& m : it.p_multiples) t.words(m);
+  t.words(it.target);
+  t.word(it.target_pow2);
+  t.word(it.target_log2);
+  t.word(it.accum_words);
+  return t.h;
+}
+
+}  // namespace
+
 extern "C" {
+
+uint64_t ref_table_digest(int np, int log_n, int log_q, int w32) {
+  try {
+    return table_digest(np, log_n, log_q, w32 != 0);
+  } catch (const std::exception& e) {
+    return (void)fail(e, 1), 0;
+  }
+}
 
 const char* ref_last_error() { return g_err.c_str(); }
 
@@ -269,6 +340,41 @@ int ref_time_he_mul(int log_p, int depth, int log_n_override, uint64_t seed, int
       ms_out[r] = std::chrono::duration<double, std::milli>(t1 - t0).count();
     }
     if (digest) *digest = ciphertext_digest(out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
+// Scheme::counters after one he_mul on the bench-protocol inputs (seed):
+// out[5 * 4] = {mul, adc, modmul, addsub} per stage (counters.hpp:13-31).
+// four_products / periodic select SchemeOptions (periodic: period 4).
+int ref_counters(int log_p, int depth, int log_n_override, uint64_t seed, int four_products,
+                 int periodic, uint64_t* out) {
+  try {
+    const Params p = make_params(log_p, depth, WordSize::w64, log_n_override);
+    Scheme scheme(p);
+    scheme.options().four_products = four_products != 0;
+    if (periodic) {
+      scheme.options().strategy.kind = AccumKind::periodic_mod;
+      scheme.options().strategy.period = 4;
+    }
+    Rng rng(seed);
+    const KeySet keys = scheme.keygen(rng);
+    Message m;
+    m.slots.assign(std::min(8, p.n / 2), {0.5, -0.25});
+    const Ciphertext c1 = scheme.encrypt(scheme.encode(m), keys.pk, rng);
+    const Ciphertext c2 = scheme.encrypt(scheme.encode(m), keys.pk, rng);
+    scheme.warm_level(p.log_q_max, &keys.evk);
+    scheme.counters.reset();
+    scheme.he_mul(c1, c2, keys.evk);
+    for (int s = 0; s < 5; ++s) {
+      const OpCounts& c = scheme.counters.stage[s];
+      out[4 * s + 0] = c.mul;
+      out[4 * s + 1] = c.adc;
+      out[4 * s + 2] = c.modmul;
+      out[4 * s + 3] = c.addsub;
+    }
     return 0;
   } catch (const std::exception& e) {
     return fail(e, 1);

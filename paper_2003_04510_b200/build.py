@@ -82,11 +82,12 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
     if jobs or not out.exists():
         _run([NVCC, *ARCH, "-shared", "-o", str(out), *map(str, objs), "-lcudart", "-lpthread"])
     # the C++ drop-in check (tests/cpp): reference-API code linked against us
-    check_src = ROOT / "tests" / "cpp" / "dropin_check.cpp"
-    check_bin = LIB / "dropin_check"
-    if check_src.exists() and _stale(check_bin, [check_src, out] + headers):
-        _run([CXX, *CXX_FLAGS, str(check_src), "-o", str(check_bin), f"-L{LIB}", "-lhemul_gpu",
-              "-Wl,-rpath,$ORIGIN"])
+    for name in ("dropin_check", "stage_check"):
+        check_src = ROOT / "tests" / "cpp" / f"{name}.cpp"
+        check_bin = LIB / name
+        if check_src.exists() and _stale(check_bin, [check_src, out] + headers):
+            _run([CXX, *CXX_FLAGS, str(check_src), "-o", str(check_bin), f"-L{LIB}",
+                  "-lhemul_gpu", "-Wl,-rpath,$ORIGIN"])
     if verbose:
         print(f"built {out}")
     return out

@@ -1525,35 +1525,186 @@ uint64_t hemul_ciphertext_digest(int log_q, size_t words, const uint64_t* ax,
 
 // ---- stage entry points ------------------------------------------------------
 
+}  // extern "C"
+
+// ---- stage kernels on one region's device tables -----------------------------
+// Shared by the level/region entry points (reference primes of a level) and
+// the explicit-prime-set objects (hemul_gpu_rns_*, the lower-level C++ API).
+// Every pointer may be host or device memory.
+
+struct hemul_gpu_rns {
+  int device = 0;
+  int log_n = 0;
+  int in_bits = 0;
+  bool has_ntt = false;
+  RegionDev r;
+};
+
+namespace {
+
+void stage_ntt(hemul_gpu_ctx* c, const RegionDev& r, int log_n, uint64_t* data, size_t rows,
+               int inverse) {
+  const size_t n = size_t(1) << log_n;
+  const size_t words = rows * n;
+  const bool dev = is_device(c, data);
+  uint64_t* d = data;
+  if (!dev) {
+    ensure(c->r1, words * 8);
+    d = c->r1.as<uint64_t>();
+    stage_in(c, data, words, d);
+  }
+  // row r uses prime r % np: chunks are whole multiples of np (gridDim.y)
+  const size_t step = std::max<size_t>(1, kMaxGridY / size_t(r.np)) * size_t(r.np);
+  for (size_t r0 = 0; r0 < rows; r0 += step) {
+    const size_t rc = std::min(step, rows - r0);
+    const int total = ntt_num_passes(log_n);
+    for (int pass = 0; pass < total; ++pass)
+      run(c, inverse ? HEMUL_STAGE_INTT : HEMUL_STAGE_NTT,
+          inverse ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_NTT_A, inverse ? "iNTT" : "NTT", [&] {
+            return inverse ? ntt_inverse_pass<F64>(pass, d + r0 * n, rc, r.np, log_n, r.ITW<F64>(),
+                                                   r.P<F64>(), c->stream)
+                           : ntt_forward_pass<F64>(pass, d + r0 * n, rc, r.np, log_n, r.TW<F64>(),
+                                                   r.P<F64>(), c->stream);
+          });
+  }
+  if (!dev)
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+      return cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDefault, c->stream);
+    });
+  check(cudaStreamSynchronize(c->stream), "ntt");
+}
+
+// The GEMM-tiled CRT / iCRT kernels take 32-coefficient tiles: smaller rings
+// run on a zero-padded copy with n = 32 (both maps act per coefficient).
+constexpr int kMinTileLogN = 5;
+
+void stage_crt(hemul_gpu_ctx* c, const RegionDev& r, int log_n, int in_bits, size_t batch,
+               const uint64_t* poly, uint64_t* rns) {
+  const CrtWeights* w = r.weights(in_bits);
+  if (!w) throw std::invalid_argument("no CRT table for this input width");
+  const int L = limbs_of(in_bits);
+  const int ln = std::max(log_n, kMinTileLogN);
+  const size_t n = size_t(1) << log_n, nt = size_t(1) << ln;
+  ensure(c->in, batch * nt * L * 8);
+  const uint64_t* src;
+  if (ln != log_n) {
+    uint64_t* pad = c->in.as<uint64_t>();
+    check(cudaMemsetAsync(pad, 0, batch * nt * L * 8, c->stream), "pad");
+    check(cudaMemcpy2DAsync(pad, nt * L * 8, poly, n * L * 8, n * L * 8, batch, cudaMemcpyDefault,
+                            c->stream), "pad");
+    src = pad;
+  } else {
+    src = stage_in(c, poly, batch * n * L, c->in.as<uint64_t>());
+  }
+  const size_t words = batch * r.np * nt;
+  const bool dev = ln == log_n && is_device(c, rns);
+  uint64_t* dst = rns;
+  if (!dev) {
+    ensure(c->r1, words * 8);
+    dst = c->r1.as<uint64_t>();
+  }
+  run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT", [&] {
+    for (size_t b0 = 0; b0 < batch; b0 += kMaxGridY) {  // batch on gridDim.y
+      const size_t bc = std::min(kMaxGridY, batch - b0);
+      const cudaError_t e = crt_forward<F64>(src + b0 * nt * L, L, bc, ln, *w, r.P<F64>(), r.np,
+                                             dst + b0 * r.np * nt, c->stream);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  });
+  if (!dev)
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+      return cudaMemcpy2DAsync(rns, n * 8, dst, nt * 8, n * 8, batch * r.np, cudaMemcpyDefault,
+                               c->stream);
+    });
+  check(cudaStreamSynchronize(c->stream), "crt");
+}
+
+void stage_pointwise(hemul_gpu_ctx* c, const RegionDev& r, int log_n, size_t batch,
+                     const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  const size_t words = batch * r.np * (size_t(1) << log_n);
+  ensure(c->r1, 3 * words * 8);
+  const uint64_t* da = stage_in(c, a, words, c->r1.as<uint64_t>());
+  const uint64_t* db = stage_in(c, b, words, c->r1.as<uint64_t>() + words);
+  const bool dev = is_device(c, out);
+  uint64_t* d = dev ? out : c->r1.as<uint64_t>() + 2 * words;
+  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "pointwise", [&] {
+    return pointwise(da, db, d, batch, r.np, log_n, r.primes.as<DevPrime>(), c->stream);
+  });
+  if (!dev)
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+      return cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDefault, c->stream);
+    });
+  check(cudaStreamSynchronize(c->stream), "pointwise");
+}
+
+void stage_icrt(hemul_gpu_ctx* c, const RegionDev& r, int log_n, size_t batch, const uint64_t* rns,
+                uint64_t* poly) {
+  const int ln = std::max(log_n, kMinTileLogN);
+  const size_t n = size_t(1) << log_n, nt = size_t(1) << ln;
+  const size_t words = batch * r.np * nt;
+  const int TL = limbs_of(r.target_bits);
+  ensure(c->r1, words * 8);
+  const uint64_t* src;
+  if (ln != log_n) {
+    uint64_t* pad = c->r1.as<uint64_t>();
+    check(cudaMemsetAsync(pad, 0, words * 8, c->stream), "pad");
+    check(cudaMemcpy2DAsync(pad, nt * 8, rns, n * 8, n * 8, batch * r.np, cudaMemcpyDefault,
+                            c->stream), "pad");
+    src = pad;
+  } else {
+    src = stage_in(c, rns, words, c->r1.as<uint64_t>());
+  }
+  const bool dev = ln == log_n && is_device(c, poly);
+  uint64_t* dst = poly;
+  if (!dev) {
+    ensure(c->ks, batch * nt * TL * 8);
+    dst = c->ks.as<uint64_t>();
+  }
+  // arbitrary residues: the exact fix-up handles |v| >= P/4
+  IcrtFlags flags;
+  flags.capacity = static_cast<unsigned>(std::min(batch, kMaxGridY) * nt);
+  ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
+  flags.count = c->flagbuf.as<unsigned>();
+  flags.ids = flags.count + 1;
+  run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT", [&] {
+    for (size_t b0 = 0; b0 < batch; b0 += kMaxGridY) {  // batch on gridDim.y
+      const size_t bc = std::min(kMaxGridY, batch - b0);
+      const cudaError_t e = icrt<F64>(src + b0 * r.np * nt, bc, ln, r.P<F64>(), r.np, r.icrt,
+                                      dst + b0 * nt * TL, c->stream, &flags);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  });
+  ++c->launches;  // the fix-up kernel
+  if (!dev)
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+      return cudaMemcpy2DAsync(poly, n * TL * 8, dst, nt * TL * 8, n * TL * 8, batch,
+                               cudaMemcpyDefault, c->stream);
+    });
+  check(cudaStreamSynchronize(c->stream), "icrt");
+}
+
+const RegionDev& stage_region(hemul_gpu_ctx* c, int log_q, int region) {
+  Level& lv = get_level(c, log_q);
+  const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
+  return region == 1 ? *bs.r1 : *bs.r2;
+}
+
+void check_rns(const hemul_gpu_ctx* c, const hemul_gpu_rns* t) {
+  if (!t) throw std::invalid_argument("null prime-set handle");
+  if (t->device != c->device) throw std::invalid_argument("prime set on another device");
+}
+
+}  // namespace
+
+extern "C" {
+
 hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* data, size_t rows,
                            int inverse) {
   if (!c || !data || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
-    Level& lv = get_level(c, log_q);
-    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
-    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
-    const size_t words = rows * size_t(c->n);
-    const bool dev = is_device(c, data);
-    uint64_t* d = data;
-    if (!dev) {
-      ensure(c->r1, words * 8);
-      d = c->r1.as<uint64_t>();
-      stage_in(c, data, words, d);
-    }
-    // row r uses prime r % np: chunks are whole multiples of np
-    const size_t step = std::max<size_t>(1, kMaxGridY / size_t(r.np)) * size_t(r.np);
-    for (size_t r0 = 0; r0 < rows; r0 += step) {
-      const size_t rc = std::min(step, rows - r0);
-      if (inverse)
-        ntt_inv<F64>(c, r, d + r0 * c->n, rc, HEMUL_STAGE_INTT);
-      else
-        ntt_fwd<F64>(c, r, d + r0 * c->n, rc, HEMUL_STAGE_NTT);
-    }
-    if (!dev)
-      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(data, d, words * 8, cudaMemcpyDefault, c->stream);
-      });
-    check(cudaStreamSynchronize(c->stream), "ntt");
+    stage_ntt(c, stage_region(c, log_q, region), c->log_n, data, rows, inverse);
     return HEMUL_OK;
   });
 }
@@ -1562,36 +1713,9 @@ hemul_status hemul_gpu_crt(hemul_gpu_ctx* c, int log_q, int region, int in_bits,
                            const uint64_t* poly, uint64_t* rns) {
   if (!c || !poly || !rns || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&]() -> hemul_status {
-    Level& lv = get_level(c, log_q);
-    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
-    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
-    const CrtWeights* w = r.weights(in_bits);
-    if (!w) return fail(c, HEMUL_E_ARG, "no CRT table for this input width");
-    const size_t n = size_t(c->n);
-    const int L = limbs_of(in_bits);
-    ensure(c->in, batch * n * L * 8);
-    const uint64_t* src = stage_in(c, poly, batch * n * L, c->in.as<uint64_t>());
-    const bool dev = is_device(c, rns);
-    uint64_t* dst = rns;
-    const size_t words = batch * r.np * n;
-    if (!dev) {
-      ensure(c->r1, words * 8);
-      dst = c->r1.as<uint64_t>();
-    }
-    run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT", [&] {
-      for (size_t b0 = 0; b0 < batch; b0 += kMaxGridY) {  // batch on gridDim.y
-        const size_t bc = std::min(kMaxGridY, batch - b0);
-        const cudaError_t e = crt_forward<F64>(src + b0 * n * L, L, bc, c->log_n, *w, r.P<F64>(),
-                                               r.np, dst + b0 * r.np * n, c->stream);
-        if (e != cudaSuccess) return e;
-      }
-      return cudaSuccess;
-    });
-    if (!dev)
-      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(rns, dst, words * 8, cudaMemcpyDefault, c->stream);
-      });
-    check(cudaStreamSynchronize(c->stream), "crt");
+    const RegionDev& r = stage_region(c, log_q, region);
+    if (!r.weights(in_bits)) return fail(c, HEMUL_E_ARG, "no CRT table for this input width");
+    stage_crt(c, r, c->log_n, in_bits, batch, poly, rns);
     return HEMUL_OK;
   });
 }
@@ -1600,23 +1724,7 @@ hemul_status hemul_gpu_pointwise(hemul_gpu_ctx* c, int log_q, int region, size_t
                                  const uint64_t* a, const uint64_t* b, uint64_t* out) {
   if (!c || !a || !b || !out || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
-    Level& lv = get_level(c, log_q);
-    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
-    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
-    const size_t words = batch * r.np * size_t(c->n);
-    ensure(c->r1, 3 * words * 8);
-    const uint64_t* da = stage_in(c, a, words, c->r1.as<uint64_t>());
-    const uint64_t* db = stage_in(c, b, words, c->r1.as<uint64_t>() + words);
-    const bool dev = is_device(c, out);
-    uint64_t* d = dev ? out : c->r1.as<uint64_t>() + 2 * words;
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_TENSOR, "pointwise", [&] {
-      return pointwise(da, db, d, batch, r.np, c->log_n, r.primes.as<DevPrime>(), c->stream);
-    });
-    if (!dev)
-      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(out, d, words * 8, cudaMemcpyDefault, c->stream);
-      });
-    check(cudaStreamSynchronize(c->stream), "pointwise");
+    stage_pointwise(c, stage_region(c, log_q, region), c->log_n, batch, a, b, out);
     return HEMUL_OK;
   });
 }
@@ -1625,41 +1733,89 @@ hemul_status hemul_gpu_icrt(hemul_gpu_ctx* c, int log_q, int region, size_t batc
                             const uint64_t* rns, uint64_t* poly) {
   if (!c || !rns || !poly || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
-    Level& lv = get_level(c, log_q);
-    const Basis& bs = get_basis(c, lv, 64);  // stage entry points: reference primes
-    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
-    const size_t n = size_t(c->n);
-    const size_t words = batch * r.np * n;
-    const int TL = limbs_of(r.target_bits);
-    ensure(c->r1, words * 8);
-    const uint64_t* src = stage_in(c, rns, words, c->r1.as<uint64_t>());
-    const bool dev = is_device(c, poly);
-    uint64_t* dst = poly;
-    if (!dev) {
-      ensure(c->ks, batch * n * TL * 8);
-      dst = c->ks.as<uint64_t>();
-    }
-    // arbitrary residues: enable the exact fix-up for |v| >= P/4
-    IcrtFlags flags;
-    flags.capacity = static_cast<unsigned>(batch * n);
-    ensure(c->flagbuf, (size_t(flags.capacity) + 1) * sizeof(unsigned));
-    flags.count = c->flagbuf.as<unsigned>();
-    flags.ids = flags.count + 1;
-    run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT", [&] {
-      for (size_t b0 = 0; b0 < batch; b0 += kMaxGridY) {  // batch on gridDim.y
-        const size_t bc = std::min(kMaxGridY, batch - b0);
-        const cudaError_t e = icrt<F64>(src + b0 * r.np * n, bc, c->log_n, r.P<F64>(), r.np,
-                                        r.icrt, dst + b0 * n * TL, c->stream, &flags);
-        if (e != cudaSuccess) return e;
-      }
-      return cudaSuccess;
-    });
-    ++c->launches;  // the fix-up kernel
-    if (!dev)
-      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
-        return cudaMemcpyAsync(poly, dst, batch * n * TL * 8, cudaMemcpyDefault, c->stream);
-      });
-    check(cudaStreamSynchronize(c->stream), "icrt");
+    stage_icrt(c, stage_region(c, log_q, region), c->log_n, batch, rns, poly);
+    return HEMUL_OK;
+  });
+}
+
+// ---- explicit prime sets (the reference's lower-level API) -------------------
+
+hemul_status hemul_gpu_rns_create(hemul_gpu_ctx* c, int log_n, const uint64_t* primes,
+                                  const uint64_t* roots, int np, int in_bits, int target_bits,
+                                  hemul_gpu_rns** out) {
+  if (!c || !out || !primes || np <= 0) return HEMUL_E_ARG;
+  *out = nullptr;
+  if (log_n < 1 || log_n > 17) return fail(c, HEMUL_E_ARG, "log_n out of range (1..17)");
+  if (in_bits < 0 || target_bits < 0) return fail(c, HEMUL_E_ARG, "negative bit width");
+  return guarded(c, [&] {
+    const std::vector<uint64_t> ps(primes, primes + np);
+    const std::vector<uint64_t> rs = roots ? std::vector<uint64_t>(roots, roots + np)
+                                           : std::vector<uint64_t>{};
+    std::vector<int> crt_bits;
+    if (in_bits > 0) crt_bits.push_back(in_bits);
+    const RegionHost h = build_explicit_region(ps, rs, log_n, target_bits > 0 ? target_bits : 64,
+                                               crt_bits, host_threads());
+    auto t = std::make_unique<hemul_gpu_rns>();
+    t->device = c->device;
+    t->log_n = log_n;
+    t->in_bits = in_bits;
+    t->has_ntt = roots != nullptr;
+    fill_region(t->r, h, c->stream);
+    if (target_bits == 0) t->r.target_bits = 0;
+    check(cudaStreamSynchronize(c->stream), "prime-set upload");
+    *out = t.release();
+    return HEMUL_OK;
+  });
+}
+
+void hemul_gpu_rns_destroy(hemul_gpu_rns* t) {
+  if (!t) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(t->device);
+  delete t;
+  cudaSetDevice(cur);
+}
+
+hemul_status hemul_gpu_rns_ntt(hemul_gpu_ctx* c, const hemul_gpu_rns* t, uint64_t* data,
+                               size_t rows, int inverse) {
+  if (!c || !data) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    check_rns(c, t);
+    if (!t->has_ntt) return fail(c, HEMUL_E_ARG, "prime set built without roots (no NTT tables)");
+    stage_ntt(c, t->r, t->log_n, data, rows, inverse);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_rns_crt(hemul_gpu_ctx* c, const hemul_gpu_rns* t, size_t batch,
+                               const uint64_t* poly, uint64_t* rns) {
+  if (!c || !poly || !rns) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    check_rns(c, t);
+    if (t->in_bits <= 0) return fail(c, HEMUL_E_ARG, "prime set built without CRT tables");
+    stage_crt(c, t->r, t->log_n, t->in_bits, batch, poly, rns);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_rns_pointwise(hemul_gpu_ctx* c, const hemul_gpu_rns* t, size_t batch,
+                                     const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  if (!c || !a || !b || !out) return HEMUL_E_ARG;
+  return guarded(c, [&] {
+    check_rns(c, t);
+    stage_pointwise(c, t->r, t->log_n, batch, a, b, out);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_rns_icrt(hemul_gpu_ctx* c, const hemul_gpu_rns* t, size_t batch,
+                                const uint64_t* rns, uint64_t* poly) {
+  if (!c || !rns || !poly) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    check_rns(c, t);
+    if (t->r.target_bits <= 0) return fail(c, HEMUL_E_ARG, "prime set built without iCRT tables");
+    stage_icrt(c, t->r, t->log_n, batch, rns, poly);
     return HEMUL_OK;
   });
 }

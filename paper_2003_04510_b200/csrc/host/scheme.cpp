@@ -423,11 +423,16 @@ void Scheme::count_he_mul(int log_q) {
   }
   const uint64_t n = static_cast<uint64_t>(params_.n), logn = static_cast<uint64_t>(params_.log_n);
   const uint64_t L = static_cast<uint64_t>((log_q + 63) / 64);
+  // reductions per CRT cell: one 3-word reduction, or one per period
+  // (rns.cpp:350-353)
+  const uint64_t red = opts_.strategy.kind == AccumKind::three_word_adc
+                           ? 1
+                           : (L + opts_.strategy.period - 1) / opts_.strategy.period;
   auto crt = [&](uint64_t nprime, uint64_t calls) {
     auto& c = counters[Stage::crt];
     c.mul += calls * n * nprime * L;
     c.adc += calls * n * nprime * L;
-    c.modmul += calls * n * nprime;
+    c.modmul += calls * n * nprime * red;
   };
   auto ntt = [&](uint64_t nprime, uint64_t calls) {
     auto& c = counters[Stage::ntt];

@@ -210,6 +210,11 @@ std::vector<uint64_t> reference_primes(int region, int log_q, int log_q_max, int
   return primes;
 }
 
+namespace {
+void build_tables(RegionHost& r, const Nat& P, const std::vector<int>& crt_bits, int threads,
+                  int log_q);
+}  // namespace
+
 RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
                         const std::vector<int>& crt_bits, int threads, int word, int split_h) {
   RegionHost r;
@@ -251,7 +256,49 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   r.slack_bits = (nat_bits(P) - 1) - 1 - vbits;
   if (r.slack_bits < kMinSlackBits)
     throw std::runtime_error("prime set leaves less than 4 bits of iCRT headroom");
+  build_tables(r, P, crt_bits, threads, log_q);
+  return r;
+}
 
+RegionHost build_explicit_region(const std::vector<uint64_t>& primes,
+                                 const std::vector<uint64_t>& roots, int log_n, int target_bits,
+                                 const std::vector<int>& crt_bits, int threads) {
+  // roots empty: a CRT / pointwise / iCRT-only set (no NTT of this degree;
+  // the twiddle slots are filled with 1)
+  if (primes.empty() || (!roots.empty() && primes.size() != roots.size()))
+    throw std::invalid_argument("prime set and roots differ in size");
+  const uint64_t two_n = uint64_t(2) << log_n;
+  for (size_t j = 0; j < primes.size(); ++j) {
+    const uint64_t p = primes[j];
+    if (p < 3 || p >= (uint64_t(1) << 62) || (p & 1) == 0)
+      throw std::invalid_argument("primes must be odd and below 2^62");
+    if (roots.empty()) continue;
+    if ((p - 1) % two_n != 0) throw std::invalid_argument("primes must be 1 mod 2n");
+    if (powmod(roots[j], two_n / 2, p) != p - 1)
+      throw std::invalid_argument("root is not a primitive 2n-th root of unity");
+  }
+  RegionHost r;
+  r.region = 0;
+  r.log_n = log_n;
+  r.word = 64;
+  r.split_h = 0;
+  r.primes = primes;
+  r.roots = roots.empty() ? std::vector<uint64_t>(primes.size(), 1) : roots;
+  r.np = static_cast<int>(primes.size());
+  r.target_bits = target_bits;
+  Nat P(1, 1);
+  for (uint64_t p : primes) nat_mul_word(P, p);
+  r.slack_bits = 0;  // arbitrary residues: the iCRT runs with the exact fix-up
+  build_tables(r, P, crt_bits, threads, 0);
+  return r;
+}
+
+namespace {
+
+void build_tables(RegionHost& r, const Nat& P, const std::vector<int>& crt_bits, int threads,
+                  int log_q) {
+  const int count = r.np, log_n = r.log_n, n = 1 << log_n, word = r.word, h = r.split_h,
+            region = r.region;
   // per-prime constants
   std::vector<Nat> hat(count);
   std::vector<uint64_t> inv(count), ninv(count);
@@ -433,8 +480,9 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   for (int k = 0; k < r.p_limbs && k < int(P.size()); ++k) r.big_p[k] = P[k];
   for (int k = 0; k < r.p_limbs; ++k)
     r.half_p[k] = (r.big_p[k] >> 1) | (k + 1 < r.p_limbs ? r.big_p[k + 1] << 63 : 0);
-  return r;
 }
+
+}  // namespace
 
 int build_crt_tc_kpad(int bit0, int bits) {
   const int byte0 = bit0 / 8, nbytes = (bits + 7) / 8;

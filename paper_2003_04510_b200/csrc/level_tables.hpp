@@ -98,6 +98,15 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
                         const std::vector<int>& crt_bits, int threads, int word = 64,
                         int split_h = 0);
 
+// Tables of an explicit w64 prime set (the reference's lower-level API:
+// generate_primes / make_crt_tables / make_ntt_tables / make_icrt_tables,
+// params.cpp:89-239): twiddles from the given roots, CRT weights per input
+// width, iCRT to 2^target_bits. No headroom requirement: the stage iCRT runs
+// with the exact fix-up for arbitrary residues.
+RegionHost build_explicit_region(const std::vector<uint64_t>& primes,
+                                 const std::vector<uint64_t>& roots, int log_n, int target_bits,
+                                 const std::vector<int>& crt_bits, int threads);
+
 // Tensor-core CRT table of field [bit0, bit0 + bits) (bit0 % 8 == 0) for the
 // region's primes: column tiling chosen so that the weight tile and two
 // 128-coefficient A stages fit in shared memory (crt_tc.cu).

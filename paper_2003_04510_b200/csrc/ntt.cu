@@ -682,10 +682,58 @@ int ntt_num_passes(int log_n) {
   return s2 == 0 ? 1 : 2;
 }
 
+// Rings below the tiled kernels' smallest pass (n < 8: the SPEC's N = 4
+// known answer, test_ntt.cpp:59-93): one thread per row runs the reference's
+// radix-2 loops (ntt.cpp:11-57) with canonical Shoup products.
+template <class F>
+__global__ void ntt_small_kernel(typename F::W* data, size_t rows, int np, int log_n,
+                                 const typename F::Tw* tw, const typename F::Prime* primes,
+                                 bool inv) {
+  using W = typename F::W;
+  const size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const int n = 1 << log_n;
+  const typename F::Prime& pr = primes[r % np];
+  const W p = pr.p;
+  const typename F::Tw* t = tw + size_t(r % np) * n;
+  W* a = data + r * n;
+  auto mulw = [&](W x, const typename F::Tw& w) { return shoup_mul(x, w.w, w.wq, p); };
+  if (!inv) {
+    for (int m = 1, h = n / 2; m < n; m *= 2, h /= 2)
+      for (int i = 0; i < m; ++i)
+        for (int j = 2 * i * h; j < 2 * i * h + h; ++j) {
+          const W u = a[j], v = mulw(a[j + h], t[m + i]);
+          a[j] = add_mod(u, v, p);
+          a[j + h] = sub_mod(u, v, p);
+        }
+  } else {
+    for (int m = n / 2, h = 1; m >= 1; m /= 2, h *= 2)
+      for (int i = 0; i < m; ++i)
+        for (int j = 2 * i * h; j < 2 * i * h + h; ++j) {
+          const W u = a[j], v = a[j + h];
+          a[j] = add_mod(u, v, p);
+          a[j + h] = mulw(sub_mod(u, v, p), t[m + i]);
+        }
+    for (int i = 0; i < n; ++i) a[i] = shoup_mul(a[i], pr.ninv, pr.ninv_q, p);
+  }
+}
+
+template <class F>
+cudaError_t ntt_small(typename F::W* data, size_t rows, int np, int log_n,
+                      const typename F::Tw* tw, const typename F::Prime* primes, bool inv,
+                      cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  ntt_small_kernel<F><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+      data, rows, np, log_n, tw, primes, inv);
+  return cudaGetLastError();
+}
+
 template <class F>
 cudaError_t ntt_forward_pass(int pass, typename F::W* data, size_t rows, int np, int log_n,
                              const typename F::Tw* tw, const typename F::Prime* primes,
                              cudaStream_t st) {
+  if constexpr (sizeof(typename F::W) == 8)
+    if (log_n < 3) return ntt_small<F>(data, rows, np, log_n, tw, primes, false, st);
   int s1, s2;
   split_levels(log_n, s1, s2);
   if (pass == 0)
@@ -697,6 +745,8 @@ template <class F>
 cudaError_t ntt_inverse_pass(int pass, typename F::W* data, size_t rows, int np, int log_n,
                              const typename F::Tw* itw, const typename F::Prime* primes,
                              cudaStream_t st) {
+  if constexpr (sizeof(typename F::W) == 8)
+    if (log_n < 3) return ntt_small<F>(data, rows, np, log_n, itw, primes, true, st);
   int s1, s2;
   split_levels(log_n, s1, s2);
   if (pass == 0 && s2 > 0)

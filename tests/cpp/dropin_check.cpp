@@ -12,6 +12,10 @@
 //   dropin_check ladder_dev <log_p> <depth> <log_n> <seed>            (GPU)
 //       the ladder on DeviceCiphertext (upload / he_mul / mod_down /
 //       download); each step bit-identical to the host-API step
+//   dropin_check counters <log_p> <depth> <log_n> <seed> <four> <periodic> (GPU)
+//       Scheme::counters of one he_mul (compared with the reference's)
+//   dropin_check tables <np> <log_n> <log_q> <w32>                    (CPU only)
+//       digest of generate_primes / make_{crt,ntt,icrt}_tables (params.hpp)
 //   dropin_check errors                                                (GPU)
 //       test_heaan.cpp:169-182: modulus mismatch / exhausted depth throw
 #include <cmath>
@@ -20,6 +24,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "hemul/bench.hpp"
 #include "hemul/heaan.hpp"
@@ -140,6 +145,35 @@ int cmd_ladder_dev(int log_p, int depth, int log_n, uint64_t seed) {
   return worst < 1e-3 && mismatches == 0 ? 0 : 1;
 }
 
+// Scheme::counters after one he_mul (same protocol as oracle/ref_shim.cpp
+// ref_counters): 20 numbers {mul, adc, modmul, addsub} x 5 stages.
+int cmd_counters(int log_p, int depth, int log_n, uint64_t seed, int four, int periodic) {
+  const Params p = make_params(log_p, depth, WordSize::w64, log_n);
+  Scheme sch(p);
+  sch.options().four_products = four != 0;
+  if (periodic) {
+    sch.options().strategy.kind = AccumKind::periodic_mod;
+    sch.options().strategy.period = 4;
+  }
+  Rng rng(seed);
+  const KeySet keys = sch.keygen(rng);
+  Message m;
+  m.slots.assign(std::min(8, p.n / 2), {0.5, -0.25});
+  const Ciphertext c1 = sch.encrypt(sch.encode(m), keys.pk, rng);
+  const Ciphertext c2 = sch.encrypt(sch.encode(m), keys.pk, rng);
+  sch.warm_level(p.log_q_max, &keys.evk);
+  sch.counters.reset();
+  sch.he_mul(c1, c2, keys.evk);
+  std::printf("counters");
+  for (int s = 0; s < 5; ++s) {
+    const OpCounts& c = sch.counters.stage[s];
+    std::printf(" %llu %llu %llu %llu", (unsigned long long)c.mul, (unsigned long long)c.adc,
+                (unsigned long long)c.modmul, (unsigned long long)c.addsub);
+  }
+  std::printf("\n");
+  return 0;
+}
+
 int cmd_errors() {
   const Params p = make_params(30, 4, WordSize::w64, 10);
   Scheme sch(p);
@@ -166,6 +200,66 @@ int cmd_errors() {
   return fails;
 }
 
+
+// FNV-1a over every field of the lower-level tables of one prime set
+// (params.hpp: PrimeSet, CrtTables, NttTables, IcrtTables); the same routine
+// is in tests/cpp/dropin_check.cpp and oracle/ref_shim.cpp.
+struct TableHash {
+  uint64_t h = 1469598103934665603ull;
+  void word(uint64_t v) {
+    for (int k = 0; k < 8; ++k) h = (h ^ ((v >> (8 * k)) & 0xff)) * 1099511628211ull;
+  }
+  void words(const std::vector<uint64_t>& v) {
+    word(v.size());
+    for (uint64_t x : v) word(x);
+  }
+  void pairs(const std::vector<ShoupPair>& v) {
+    word(v.size());
+    for (const ShoupPair& s : v) {
+      word(s.value);
+      word(s.quotient);
+    }
+  }
+};
+
+uint64_t table_digest(int np, int log_n, int log_q, bool w32) {
+  const WordSize w = w32 ? WordSize::w32 : WordSize::w64;
+  const PrimeSet ps = generate_primes(np, log_n, w);
+  const CrtTables ct = make_crt_tables(ps, log_q);
+  const NttTables nt = make_ntt_tables(ps, log_n);
+  const IcrtTables it = make_icrt_tables(ps, bigint_pow2(log_q, w), w);
+  TableHash t;
+  t.word(ps.two_n);
+  t.words(ps.primes);
+  t.words(ps.roots);
+  t.pairs(ps.pair_one);
+  t.pairs(ps.pair_beta);
+  t.pairs(ps.pair_beta2);
+  t.words(ps.product);
+  t.word(ct.np);
+  t.word(ct.q_limbs);
+  t.pairs(ct.pow_beta);
+  t.word(nt.log_n);
+  t.word(nt.n);
+  t.pairs(nt.tw);
+  t.pairs(nt.itw);
+  t.pairs(nt.n_inv);
+  t.word(it.np);
+  t.word(it.p_limbs);
+  t.pairs(it.inv_p);
+  t.words(it.p_div_p);
+  t.words(it.p_div_p_t);
+  t.words(it.big_p);
+  t.words(it.half_p);
+  t.words(it.neg_p_mod);
+  for (const auto& m : it.p_multiples) t.words(m);
+  t.words(it.target);
+  t.word(it.target_pow2);
+  t.word(it.target_log2);
+  t.word(it.accum_words);
+  return t.h;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -180,6 +274,14 @@ int main(int argc, char** argv) {
       return cmd_ladder(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10));
     if (cmd == "ladder_dev" && argc == 6)
       return cmd_ladder_dev(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10));
+    if (cmd == "counters" && argc == 8)
+      return cmd_counters(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10), arg(6),
+                          arg(7));
+    if (cmd == "tables" && argc == 6) {
+      std::printf("table_digest %016llx\n",
+                  static_cast<unsigned long long>(table_digest(arg(2), arg(3), arg(4), arg(5))));
+      return 0;
+    }
     if (cmd == "errors") return cmd_errors();
     std::fprintf(stderr, "usage: see the header of tests/cpp/dropin_check.cpp\n");
     return 2;

@@ -134,6 +134,16 @@ class Reference:
         L.ref_pointwise.argtypes = [_i, _i, _i, _i, _p, _p, _p]
         L.ref_shift_right.argtypes = [_i, _i, _i, _p, _p]
         L.ref_time_he_mul.argtypes = [_i, _i, _i, _u64, _i, _i, _i, _p, _p]
+        L.ref_counters.argtypes = [_i, _i, _i, _u64, _i, _i, _p]
+
+    def counters(self, log_p, depth, log_n_override, seed=7, four_products=False,
+                 periodic=False):
+        """Scheme::counters after one he_mul: 5 stages x {mul, adc, modmul, addsub}."""
+        out = np.zeros(20, np.uint64)
+        st = self.lib.ref_counters(log_p, depth, log_n_override, seed, int(four_products),
+                                   int(periodic), _ptr(out))
+        assert st == 0, self.err()
+        return [int(v) for v in out]
 
     def err(self):
         return self.lib.ref_last_error().decode()

@@ -82,3 +82,57 @@ def test_ladder_device_resident(cfg):
     res = _run("ladder_dev", *cfg, 7)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "mismatches 0" in res.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("four,periodic", [(0, 0), (1, 0), (0, 1)])
+@pytest.mark.parametrize("cfg", [(30, 4, 10), (30, 6, 12)])
+def test_scheme_counters_match_reference(cfg, four, periodic, reference):
+    """Scheme::counters after one he_mul equals the reference's runtime
+    counters (counters.hpp:13-31, test_costmodel.cpp:34-70) for every option
+    that changes them."""
+    res = _run("counters", *cfg, 7, four, periodic)
+    assert res.returncode == 0, res.stdout + res.stderr
+    ours = [int(v) for v in res.stdout.split("counters", 1)[1].split()]
+    assert ours == reference.counters(*cfg, seed=7, four_products=bool(four),
+                                      periodic=bool(periodic))
+
+
+@pytest.mark.gpu
+def test_lower_level_api_restated_reference_tests():
+    """tests/cpp/stage_check.cpp: the reference's test_ntt / test_rns /
+    test_polymul cases restated against the drop-in lower-level headers
+    (rns.hpp, ntt.hpp, polymul.hpp, params.hpp, word.hpp), on the GPU."""
+    exe = ROOT / "paper_2003_04510_b200" / "lib" / "stage_check"
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr
+    assert "failures 0" in res.stdout
+
+
+def test_stage_check_fails_loudly_without_gpu():
+    """No CPU fallback: without a device every stage call throws."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    exe = ROOT / "paper_2003_04510_b200" / "lib" / "stage_check"
+    res = subprocess.run([str(exe), "--quick"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 1
+    assert "no usable CUDA device" in res.stdout
+
+
+@pytest.mark.parametrize("np_,log_n,log_q,w32", [(5, 6, 150, 0), (7, 8, 300, 1), (3, 2, 60, 0),
+                                                 (42, 12, 1200, 0), (84, 13, 2400, 0)])
+def test_lower_level_tables_equal_reference(np_, log_n, log_q, w32, reference):
+    """generate_primes / make_crt_tables / make_ntt_tables / make_icrt_tables
+    (params.hpp) build the reference's tables field for field
+    (params.cpp:89-239), both word sizes: digest over every field."""
+    import ctypes
+
+    res = _run("tables", np_, log_n, log_q, w32)
+    assert res.returncode == 0, res.stderr
+    ours = res.stdout.split()[1]
+    fn = reference.lib.ref_table_digest
+    fn.restype = ctypes.c_uint64
+    fn.argtypes = [ctypes.c_int] * 4
+    assert ours == f"{fn(np_, log_n, log_q, w32):016x}"
