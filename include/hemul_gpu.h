@@ -187,6 +187,15 @@ hemul_status hemul_gpu_ct_rescale(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, he
 hemul_status hemul_gpu_ct_mod_down(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, int new_log_q,
                                    hemul_gpu_ct **out);
 
+/* Scheme::mul_by_ternary (heaan.cpp:234-256): out_b = a_b * t mod (X^n + 1,
+ * 2^log_q) for batch BigPolys a_b (n x ceil(log_q/64)) and one ternary
+ * polynomial t (n int32 in {-1, 0, 1}, typically sparse: the secret key or
+ * the encryption randomness). The key generation, encryption and decryption
+ * products of the drop-in Scheme run here; the RNG stays on the host so the
+ * keys follow the reference's transcript (rng.hpp). */
+hemul_status hemul_gpu_mul_by_ternary(hemul_gpu_ctx *ctx, int log_q, size_t batch,
+                                      const uint64_t *a, const int32_t *t, uint64_t *out);
+
 /* Scheme::rescale (heaan.cpp:328-337) on a batch: n x ceil(log_q/64) ->
  * n x ceil((log_q - log_p)/64). */
 hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, const uint64_t *ax,

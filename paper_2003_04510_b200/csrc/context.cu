@@ -184,6 +184,7 @@ struct hemul_gpu_ctx {
   std::vector<cudaEvent_t> event_pool;
   // scratch
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
+  DevBuf tern_a, tern_b, tern_nz;  // mul_by_ternary scratch
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
   int basis = 32;       // HEMUL_OPT_BASIS: he_mul prime basis (32 or 64)
   int tensor_cores = 1;  // HEMUL_OPT_TENSOR_CORES: int8 tcgen05 base conversions
@@ -1146,6 +1147,52 @@ hemul_status hemul_gpu_ct_mod_down(hemul_gpu_ctx* c, const hemul_gpu_ct* t, int 
                         t->log_q, new_log_q, c->stream);
       });
     *out = r.release();
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_mul_by_ternary(hemul_gpu_ctx* c, int log_q, size_t batch,
+                                      const uint64_t* a, const int32_t* t, uint64_t* out) {
+  if (!c || !a || !t || !out || batch == 0) return HEMUL_E_ARG;
+  if (log_q <= 0 || log_q > 4 * c->log_q_max) return fail(c, HEMUL_E_ARG, "log_q out of range");
+  return guarded(c, [&]() -> hemul_status {
+    const int n = c->n, L = limbs_of(log_q);
+    // the nonzero coefficients of the ternary polynomial, host side (the
+    // caller's vector); nz = 2 i + (t_i < 0)
+    std::vector<int> nz;
+    for (int i = 0; i < n; ++i) {
+      if (t[i] != 0 && t[i] != 1 && t[i] != -1)
+        return fail(c, HEMUL_E_ARG, "ternary coefficients must be -1, 0 or 1");
+      if (t[i]) nz.push_back(2 * i + (t[i] < 0));
+    }
+    const size_t words = size_t(n) * L;
+    ensure(c->tern_a, 2 * words * 8);
+    ensure(c->tern_b, words * 8);
+    ensure(c->tern_nz, (nz.size() + 1) * sizeof(int));
+    uint64_t* aT = c->tern_a.as<uint64_t>();
+    uint64_t* stage = aT + words;
+    uint64_t* rT = c->tern_b.as<uint64_t>();
+    if (!nz.empty())
+      check(cudaMemcpyAsync(c->tern_nz.ptr, nz.data(), nz.size() * sizeof(int),
+                            cudaMemcpyHostToDevice, c->stream), "ternary upload");
+    for (size_t b = 0; b < batch; ++b) {
+      const uint64_t* src = stage_in(c, a + b * words, words, stage);
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "transpose",
+          [&] { return word_transpose(src, aT, n, L, c->stream); });
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "mul_by_ternary", [&] {
+        return mul_by_ternary(aT, c->tern_nz.as<int>(), static_cast<int>(nz.size()), rT,
+                              c->log_n, log_q, c->stream);
+      });
+      const bool dev = is_device(c, out + b * words);
+      uint64_t* dst = dev ? out + b * words : stage;
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "transpose",
+          [&] { return word_transpose(rT, dst, L, n, c->stream); });
+      if (!dev)
+        run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+          return cudaMemcpyAsync(out + b * words, dst, words * 8, cudaMemcpyDefault, c->stream);
+        });
+    }
+    check(cudaStreamSynchronize(c->stream), "mul_by_ternary");
     return HEMUL_OK;
   });
 }

@@ -23,24 +23,6 @@ uint64_t word_mask(WordSize w) {
   return log_beta(w) == 64 ? ~uint64_t{0} : (uint64_t{1} << log_beta(w)) - 1;
 }
 
-uint64_t top_mask_of(const BigPoly& a) {
-  const int rest = a.log_q - (a.limbs - 1) * log_beta(a.word);
-  return rest == log_beta(a.word) ? word_mask(a.word) : (uint64_t{1} << rest) - 1;
-}
-
-// dst += sign * src (one coefficient, mod 2^log_q)
-void coeff_accumulate(uint64_t* dst, const uint64_t* src, int limbs, int lb, uint64_t wm,
-                      uint64_t tm, bool negative) {
-  unsigned __int128 carry = negative ? 1 : 0;  // two's complement: dst + ~src + 1
-  for (int k = 0; k < limbs; ++k) {
-    const uint64_t s = negative ? (~src[k] & wm) : src[k];
-    const unsigned __int128 t = (unsigned __int128)dst[k] + s + carry;
-    dst[k] = static_cast<uint64_t>(t) & wm;
-    carry = t >> lb;
-  }
-  dst[limbs - 1] &= tm;
-}
-
 // a[idx] += v for a small signed v, mod 2^log_q (heaan.cpp:53-71)
 void add_signed(BigPoly& a, int idx, int64_t v) {
   if (v == 0) return;
@@ -191,23 +173,20 @@ Message Scheme::decode(const Plaintext& t) const {
 
 // ---- ternary products and keys (heaan.cpp:234-315) ---------------------------
 
+// On the GPU (hemul_gpu_mul_by_ternary: one thread per output coefficient
+// over the limb-major polynomial, exact carries); the ternary vector and
+// everything drawn from the RNG stay host-side.
 BigPoly Scheme::mul_by_ternary(const BigPoly& a, const std::vector<int>& t) const {
-  const int n = a.n;
-  BigPoly r = make_poly(n, a.log_q, a.word);
-  const int lb = log_beta(a.word);
-  const uint64_t wm = word_mask(a.word), tm = top_mask_of(a);
-  for (int i = 0; i < n; ++i) {
-    if (t[static_cast<size_t>(i)] == 0) continue;
-    for (int j = 0; j < n; ++j) {
-      int dst = i + j;
-      bool negative = t[static_cast<size_t>(i)] < 0;
-      if (dst >= n) {  // X^n = -1
-        dst -= n;
-        negative = !negative;
-      }
-      coeff_accumulate(r.coeff(dst), a.coeff(j), a.limbs, lb, wm, tm, negative);
-    }
-  }
+  if (static_cast<int>(t.size()) != a.n) throw std::invalid_argument("ternary size mismatch");
+  if (a.word != WordSize::w64 || a.n != params_.n)
+    throw std::invalid_argument("mul_by_ternary: 64-bit words at the scheme's ring degree");
+  hemul_gpu_ctx* g = gpu();
+  BigPoly r = make_poly(a.n, a.log_q, a.word);
+  static_assert(sizeof(int) == sizeof(int32_t), "int32 ternary vector");
+  const hemul_status st = hemul_gpu_mul_by_ternary(g, a.log_q, 1, a.data.data(),
+                                                   reinterpret_cast<const int32_t*>(t.data()),
+                                                   r.data.data());
+  if (st != HEMUL_OK) throw_status(g, st);
   return r;
 }
 

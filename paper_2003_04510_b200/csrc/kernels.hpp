@@ -282,6 +282,12 @@ cudaError_t evk_product(const typename F::W* f, const typename F::W* ea, const t
 // d: n x ceil(log_q/64), out: n x ceil((log_q-log_p)/64); batch of each.
 cudaError_t keyswitch_epilogue(const uint64_t* ks, const uint64_t* d, uint64_t* out, size_t batch,
                                int log_n, int log_q, int log_Q, int log_p, cudaStream_t st);
+// rows x cols words -> cols x rows (BigPoly coefficient-major <-> limb-major)
+cudaError_t word_transpose(const uint64_t* in, uint64_t* out, int rows, int cols, cudaStream_t st);
+// Scheme::mul_by_ternary (heaan.cpp:234-256) on limb-major polys (L x n):
+// nz[j] = 2 i_j + (s_j < 0) lists the nonzero ternary coefficients.
+cudaError_t mul_by_ternary(const uint64_t* aT, const int* nz, int nnz, uint64_t* rT, int log_n,
+                           int log_q, cudaStream_t st);
 // poly_mod_down (poly.cpp:117-127) on a poly batch: n x ceil(log_q/64) ->
 // n x ceil(new_log_q/64), top limb masked.
 cudaError_t mod_down(const uint64_t* a, uint64_t* out, size_t batch, int log_n, int log_q,

@@ -221,7 +221,6 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   r.region = region;
   r.log_n = log_n;
   r.word = word;
-  const int n = 1 << log_n;
   const int h = region == 1 ? split_h : 0;
   r.split_h = h;
   // Largest |v| the iCRT must recover: region 1 carries d1 = A1 B2 + A2 B1,

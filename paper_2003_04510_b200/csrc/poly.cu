@@ -170,6 +170,57 @@ __global__ void mod_down_kernel(const uint64_t* __restrict__ a, uint64_t* __rest
   }
 }
 
+// BigPoly (rows x cols words, row-major) -> cols x rows, 32 x 32 tiles
+// through shared memory (both sides coalesced).
+__global__ void word_transpose_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                      int rows, int cols) {
+  __shared__ uint64_t tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int r = r0 + y, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[y][threadIdx.x] = in[size_t(r) * cols + c];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int c = c0 + y, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[size_t(c) * rows + r] = tile[threadIdx.x][y];
+  }
+}
+
+// Scheme::mul_by_ternary (heaan.cpp:234-256) on limb-major operands: out =
+// sum_j s_j X^(i_j) a mod (X^n + 1, 2^log_q) for a sparse ternary s given
+// as nz[j] = 2 i_j + (s_j < 0). One thread per output coefficient d walks
+// the limbs low to high; per limb the positive and negative terms
+// a[(d - i_j) mod n] (negated once more on the X^n = -1 wrap) are summed in
+// 128 bits and the signed difference plus the incoming carry gives the limb
+// and the next carry — exact for any nonzero count below 2^62.
+__global__ void ternary_mul_kernel(const uint64_t* __restrict__ aT, const int* __restrict__ nz,
+                                   int nnz, uint64_t* __restrict__ rT, int n, int L,
+                                   uint64_t top_mask) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  __int128 carry = 0;
+  for (int k = 0; k < L; ++k) {
+    const uint64_t* col = aT + size_t(k) * n;
+    unsigned __int128 pos = 0, neg = 0;
+    for (int j = 0; j < nnz; ++j) {
+      const int e = __ldg(nz + j);
+      int src = d - (e >> 1);
+      const int wrap = src < 0;
+      src += wrap ? n : 0;
+      const uint64_t v = col[src];
+      const uint64_t m = 0 - uint64_t((e & 1) ^ wrap);  // all ones: a negative term
+      pos += v & ~m;
+      neg += v & m;
+    }
+    const __int128 val = static_cast<__int128>(pos) - static_cast<__int128>(neg) + carry;
+    uint64_t w = static_cast<uint64_t>(val);
+    if (k == L - 1) w &= top_mask;
+    rT[size_t(k) * n + d] = w;
+    carry = val >> 64;
+  }
+}
+
 unsigned grid_for(size_t total, int threads) {
   size_t blocks = (total + threads - 1) / threads;
   const size_t cap = 148 * 64;
@@ -248,6 +299,22 @@ cudaError_t shift_right(const uint64_t* a, uint64_t* out, size_t batch, int log_
   if ((log_q + 63) / 64 > kMaxLimbs) return cudaErrorInvalidValue;
   const size_t total = batch << log_n;
   shift_right_kernel<<<grid_for(total, 128), 128, 0, st>>>(a, out, total, log_q, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t word_transpose(const uint64_t* in, uint64_t* out, int rows, int cols,
+                           cudaStream_t st) {
+  const dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  word_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t mul_by_ternary(const uint64_t* aT, const int* nz, int nnz, uint64_t* rT, int log_n,
+                           int log_q, cudaStream_t st) {
+  const int n = 1 << log_n, L = (log_q + 63) / 64;
+  const int rest = log_q - 64 * (L - 1);
+  const uint64_t top = rest == 64 ? ~uint64_t(0) : (uint64_t(1) << rest) - 1;
+  ternary_mul_kernel<<<(n + 127) / 128, 128, 0, st>>>(aT, nz, nnz, rT, n, L, top);
   return cudaGetLastError();
 }
 

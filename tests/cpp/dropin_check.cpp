@@ -1,9 +1,10 @@
 // Drop-in check: code written against the reference's C++ API (namespace
 // hemul, include/hemul/*.hpp) compiled against libhemul_gpu.so.
 //
-//   dropin_check keys  <log_p> <depth> <log_n> <seed> <out_prefix>   (CPU only)
+//   dropin_check keys  <log_p> <depth> <log_n> <seed> <out_prefix>   (GPU)
 //       bench-protocol keygen/encode/encrypt (bench.cpp:60-67); writes
-//       c1ax c1bx c2ax c2bx evkax evkbx as raw little-endian u64 files
+//       c1ax c1bx c2ax c2bx evkax evkbx as raw little-endian u64 files;
+//       the ternary products run on the GPU; prints the stage times
 //   dropin_check bench <log_p> <depth> <log_n> <seed> <reps>          (GPU)
 //       run_he_mul_bench; prints "digest <hex>" and the table
 //   dropin_check ladder <log_p> <depth> <log_n> <seed>                (GPU)
@@ -18,6 +19,7 @@
 //       digest of generate_primes / make_{crt,ntt,icrt}_tables (params.hpp)
 //   dropin_check errors                                                (GPU)
 //       test_heaan.cpp:169-182: modulus mismatch / exhausted depth throw
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -60,13 +62,25 @@ void write_poly(const std::string& path, const BigPoly& p) {
 int cmd_keys(int log_p, int depth, int log_n, uint64_t seed, const std::string& out) {
   const Params p = make_params(log_p, depth, WordSize::w64, log_n);
   Scheme sch(p);
+  sch.gpu();  // context creation outside the timings below
   Rng rng(seed);
   const int ns = std::min(64, p.n / 2);
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   const KeySet keys = sch.keygen(rng);
+  const auto t1k = clk::now();
   const Plaintext t1 = sch.encode(random_message(ns, rng));
   const Plaintext t2 = sch.encode(random_message(ns, rng));
+  const auto t2e = clk::now();
   const Ciphertext c1 = sch.encrypt(t1, keys.pk, rng);
   const Ciphertext c2 = sch.encrypt(t2, keys.pk, rng);
+  const auto t3 = clk::now();
+  const Plaintext back = sch.decrypt(c1, keys.sk);
+  const auto t4 = clk::now();
+  (void)back;
+  auto sec = [](clk::duration d) { return std::chrono::duration<double>(d).count(); };
+  std::printf("keygen_s %.4f encode_s %.4f encrypt2_s %.4f decrypt_s %.4f\n", sec(t1k - t0),
+              sec(t2e - t1k), sec(t3 - t2e), sec(t4 - t3));
   write_poly(out + "c1ax", c1.ax);
   write_poly(out + "c1bx", c1.bx);
   write_poly(out + "c2ax", c2.ax);

@@ -29,10 +29,21 @@ def _run(*args, timeout=600):
                           timeout=timeout)
 
 
-@pytest.mark.parametrize("cfg", [(30, 4, 13), (30, 10, 0), (30, 6, 11)])
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [(30, 4, 13), (30, 10, 0), (30, 6, 11),
+                                 pytest.param((30, 80, 0), marks=pytest.mark.slow)])
 def test_host_keys_and_ciphertexts_match_reference(cfg, tmp_path, reference):
+    """keygen / encode / encrypt with the ternary products on the GPU
+    (hemul_gpu_mul_by_ternary, heaan.cpp:234-315): keys and ciphertexts are
+    byte-identical to the reference's seed-7 transcript; at X (N=2^17,
+    logQ=2400) keygen + two encryptions take under a second (the reference:
+    ~15 s single-threaded)."""
     res = _run("keys", *cfg, 7, str(tmp_path) + "/")
     assert res.returncode == 0, res.stderr
+    tok = res.stdout.split()
+    t = dict(zip(tok[0::2], map(float, tok[1::2])))
+    if cfg == (30, 80, 0):
+        assert t["keygen_s"] + t["encrypt2_s"] < 1.0, t
     want = reference.bench_inputs(*cfg, seed=7)
     for name, arr in (("c1ax", want["c1"][0]), ("c1bx", want["c1"][1]), ("c2ax", want["c2"][0]),
                       ("c2bx", want["c2"][1]), ("evkax", want["evk"][0]),
@@ -41,6 +52,7 @@ def test_host_keys_and_ciphertexts_match_reference(cfg, tmp_path, reference):
         assert np.array_equal(got, arr), name
 
 
+@pytest.mark.gpu
 def test_host_keys_match_committed_fixture(tmp_path):
     """Same check without the reference build: the S fixture's inputs."""
     g = np.load(GOLDEN / "s_bench.npz")
