@@ -56,7 +56,8 @@ typedef enum {
                                     "modulus exhausted; cannot rescale" heaan.cpp:329-330 */
   HEMUL_E_CUDA = 4,              /* CUDA runtime / launch failure, or no device */
   HEMUL_E_OOM = 5,               /* device allocation failed */
-  HEMUL_E_NO_EVK = 6             /* he_mul before set_evk at this level */
+  HEMUL_E_NO_EVK = 6,            /* he_mul before set_evk at this level */
+  HEMUL_E_IO = 7                 /* IoError: unreadable / corrupt / truncated file (io.cpp) */
 } hemul_status;
 
 /* Stage buckets, same order as hemul::Stage (counters.hpp:13). */
@@ -175,6 +176,14 @@ hemul_status hemul_gpu_ct_info(const hemul_gpu_ct *ct, int *log_q, size_t *batch
 hemul_status hemul_gpu_ct_device_ptrs(const hemul_gpu_ct *ct, uint64_t **ax, uint64_t **bx);
 hemul_status hemul_gpu_ct_download(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, uint64_t *ax,
                                    uint64_t *bx);
+/* HEA1 ciphertext files (io.cpp:101-141) straight to / from HBM through a
+ * pinned double buffer (the file read / write of chunk k overlaps the PCIe
+ * copy of chunk k+1): load_ciphertext + upload, download + save_ciphertext.
+ * 64-bit words at the context's ring degree; batch-1 handles. */
+hemul_status hemul_gpu_ct_load(hemul_gpu_ctx *ctx, const char *path, hemul_gpu_ct **out,
+                               int *n_slots);
+hemul_status hemul_gpu_ct_save(hemul_gpu_ctx *ctx, const hemul_gpu_ct *ct, int n_slots,
+                               const char *path);
 /* Scheme::he_mul (heaan.cpp:339-410) on two handles of equal batch; same
  * checks and errors as hemul_gpu_he_mul; *out at log_q - log_p. */
 hemul_status hemul_gpu_ct_he_mul(hemul_gpu_ctx *ctx, const hemul_gpu_ct *c1,

@@ -19,6 +19,7 @@
 
 #include "hemul/bench.hpp"
 #include "hemul/heaan.hpp"
+#include "hemul/io.hpp"
 #include "hemul/ntt.hpp"
 #include "hemul/params.hpp"
 #include "hemul/poly.hpp"
@@ -155,6 +156,16 @@ uint64_t table_digest(int np, int log_n, int log_q, bool w32) {
 }  // namespace
 
 extern "C" {
+
+// save_params (io.cpp:54-70) of make_params(log_p, depth, w64, log_n_override)
+int ref_save_params(const char* path, int log_p, int depth, int log_n_override) {
+  try {
+    save_params(path, make_params(log_p, depth, WordSize::w64, log_n_override));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
 
 uint64_t ref_table_digest(int np, int log_n, int log_q, int w32) {
   try {

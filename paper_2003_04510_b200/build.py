@@ -88,6 +88,11 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> Path:
         if check_src.exists() and _stale(check_bin, [check_src, out] + headers):
             _run([CXX, *CXX_FLAGS, str(check_src), "-o", str(check_bin), f"-L{LIB}",
                   "-lhemul_gpu", "-Wl,-rpath,$ORIGIN"])
+    cli_src = CSRC / "cli" / "hemul.cpp"
+    cli_bin = LIB / "hemul"
+    if cli_src.exists() and _stale(cli_bin, [cli_src, out] + headers):
+        _run([CXX, *CXX_FLAGS, str(cli_src), "-o", str(cli_bin), f"-L{LIB}", "-lhemul_gpu",
+              "-Wl,-rpath,$ORIGIN"])
     if verbose:
         print(f"built {out}")
     return out

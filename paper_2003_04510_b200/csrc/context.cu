@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <list>
@@ -185,6 +186,8 @@ struct hemul_gpu_ctx {
   // scratch
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
   DevBuf tern_a, tern_b, tern_nz;  // mul_by_ternary scratch
+  void* pinned[2] = {nullptr, nullptr};  // file streaming (hemul_gpu_ct_load / _save)
+  cudaEvent_t ev_pin[2] = {nullptr, nullptr};
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
   int basis = 32;       // HEMUL_OPT_BASIS: he_mul prime basis (32 or 64)
   int tensor_cores = 1;  // HEMUL_OPT_TENSOR_CORES: int8 tcgen05 base conversions
@@ -686,6 +689,10 @@ void hemul_gpu_destroy(hemul_gpu_ctx* c) {
     cudaEventDestroy(c->ev_comp[s]);
     cudaEventDestroy(c->ev_d2h[s]);
   }
+  for (int s = 0; s < 2; ++s) {
+    if (c->pinned[s]) cudaFreeHost(c->pinned[s]);
+    if (c->ev_pin[s]) cudaEventDestroy(c->ev_pin[s]);
+  }
   cudaStreamDestroy(c->h2d);
   cudaStreamDestroy(c->d2h);
   cudaStreamDestroy(c->own_stream);
@@ -1081,6 +1088,107 @@ hemul_status hemul_gpu_ct_download(hemul_gpu_ctx* c, const hemul_gpu_ct* t, uint
     run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
         [&] { return cudaMemcpyAsync(bx, t->bx(), bytes, cudaMemcpyDefault, c->stream); });
     check(cudaStreamSynchronize(c->stream), "ciphertext download");
+    return HEMUL_OK;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Pinned double buffer for file <-> device streaming.
+constexpr size_t kPinChunk = size_t(32) << 20;
+
+void ensure_pinned(hemul_gpu_ctx* c) {
+  for (int s = 0; s < 2; ++s) {
+    if (!c->pinned[s]) check(cudaHostAlloc(&c->pinned[s], kPinChunk, cudaHostAllocDefault), "pinned");
+    if (!c->ev_pin[s]) check(cudaEventCreateWithFlags(&c->ev_pin[s], cudaEventDisableTiming), "event");
+  }
+}
+
+struct File {
+  FILE* f = nullptr;
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+hemul_status hemul_gpu_ct_load(hemul_gpu_ctx* c, const char* path, hemul_gpu_ct** out,
+                               int* n_slots) {
+  if (!c || !path || !out) return HEMUL_E_ARG;
+  *out = nullptr;
+  return guarded(c, [&]() -> hemul_status {
+    File file;
+    file.f = std::fopen(path, "rb");
+    if (!file.f) return fail(c, HEMUL_E_IO, std::string("cannot open: ") + path);
+    uint32_t h[5];
+    if (std::fread(h, 4, 5, file.f) != 5 || std::memcmp(h, "HEA1", 4) != 0)
+      return fail(c, HEMUL_E_IO, std::string("bad magic: ") + path);
+    if (h[1] != 64) return fail(c, HEMUL_E_ARG, "device ciphertexts use 64-bit words");
+    if (h[2] != uint32_t(c->n)) return fail(c, HEMUL_E_ARG, "ciphertext ring degree differs");
+    const int log_q = static_cast<int>(h[3]);
+    if (log_q <= 0) return fail(c, HEMUL_E_IO, "bad header fields");
+    auto t = new_ct(c, log_q, 1);
+    ensure_pinned(c);
+    // read chunk k into pinned buffer k % 2 while chunk k-1 is copied
+    char* dst = reinterpret_cast<char*>(t->mem);
+    size_t left = 2 * t->words * 8, off = 0;
+    for (int k = 0; left > 0; ++k) {
+      const int s = k & 1;
+      const size_t sz = std::min(left, kPinChunk);
+      check(cudaEventSynchronize(c->ev_pin[s]), "pinned reuse");
+      if (std::fread(c->pinned[s], 1, sz, file.f) != sz)
+        return fail(c, HEMUL_E_IO, "truncated polynomial data");
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D", [&] {
+        return cudaMemcpyAsync(dst + off, c->pinned[s], sz, cudaMemcpyHostToDevice, c->stream);
+      });
+      check(cudaEventRecord(c->ev_pin[s], c->stream), "event");
+      off += sz;
+      left -= sz;
+    }
+    check(cudaStreamSynchronize(c->stream), "ciphertext load");
+    if (n_slots) *n_slots = static_cast<int>(h[4]);
+    *out = t.release();
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_ct_save(hemul_gpu_ctx* c, const hemul_gpu_ct* t, int n_slots,
+                               const char* path) {
+  if (!c || !t || !path || t->batch != 1) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    check_ct(c, t);
+    File file;
+    file.f = std::fopen(path, "wb");
+    if (!file.f) return fail(c, HEMUL_E_IO, std::string("cannot open for writing: ") + path);
+    const uint32_t h[5] = {0, 64, uint32_t(c->n), uint32_t(t->log_q), uint32_t(n_slots)};
+    std::fwrite("HEA1", 1, 4, file.f);
+    std::fwrite(h + 1, 4, 4, file.f);
+    ensure_pinned(c);
+    // copy chunk k + 1 while chunk k is written
+    const char* src = reinterpret_cast<const char*>(t->mem);
+    const size_t total = 2 * t->words * 8;
+    const size_t chunks = (total + kPinChunk - 1) / kPinChunk;
+    auto issue = [&](size_t k) {
+      const size_t off = k * kPinChunk, sz = std::min(kPinChunk, total - off);
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H", [&] {
+        return cudaMemcpyAsync(c->pinned[k & 1], src + off, sz, cudaMemcpyDeviceToHost, c->stream);
+      });
+      check(cudaEventRecord(c->ev_pin[k & 1], c->stream), "event");
+    };
+    issue(0);
+    for (size_t k = 0; k < chunks; ++k) {
+      if (k + 1 < chunks) issue(k + 1);
+      check(cudaEventSynchronize(c->ev_pin[k & 1]), "ciphertext save");
+      const size_t sz = std::min(kPinChunk, total - k * kPinChunk);
+      if (std::fwrite(c->pinned[k & 1], 1, sz, file.f) != sz)
+        return fail(c, HEMUL_E_IO, std::string("write failed: ") + path);
+    }
+    if (std::fflush(file.f) != 0) return fail(c, HEMUL_E_IO, std::string("write failed: ") + path);
     return HEMUL_OK;
   });
 }

@@ -13,15 +13,12 @@
 #include <string>
 
 #include "hemul/heaan.hpp"
+#include "hemul/io.hpp"
 #include "hemul_gpu.h"
 
 namespace hemul {
 
 namespace {
-
-uint64_t word_mask(WordSize w) {
-  return log_beta(w) == 64 ? ~uint64_t{0} : (uint64_t{1} << log_beta(w)) - 1;
-}
 
 // a[idx] += v for a small signed v, mod 2^log_q (heaan.cpp:53-71)
 void add_signed(BigPoly& a, int idx, int64_t v) {
@@ -75,6 +72,8 @@ bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 [[noreturn]] void throw_status(hemul_gpu_ctx* g, hemul_status st) {
   const std::string msg = g ? hemul_gpu_last_error(g) : "no GPU context";
   switch (st) {
+    case HEMUL_E_IO:
+      throw IoError(msg);
     case HEMUL_E_MODULUS_MISMATCH:
     case HEMUL_E_ARG:
       throw std::invalid_argument(msg);
@@ -383,6 +382,24 @@ DeviceCiphertext Scheme::mod_down(const DeviceCiphertext& c, int new_log_q) cons
   const hemul_status st = hemul_gpu_ct_mod_down(g, c.h_, new_log_q, &h);
   if (st != HEMUL_OK) throw_status(g, st);
   return DeviceCiphertext(g, h, new_log_q, c.n_slots);
+}
+
+DeviceCiphertext Scheme::load_device(const std::string& path) const {
+  hemul_gpu_ctx* g = gpu();
+  hemul_gpu_ct* h = nullptr;
+  int slots = 0;
+  const hemul_status st = hemul_gpu_ct_load(g, path.c_str(), &h, &slots);
+  if (st != HEMUL_OK) throw_status(g, st);
+  int log_q = 0;
+  hemul_gpu_ct_info(h, &log_q, nullptr);
+  return DeviceCiphertext(g, h, log_q, slots);
+}
+
+void Scheme::save_device(const DeviceCiphertext& c, const std::string& path) const {
+  hemul_gpu_ctx* g = gpu();
+  if (c.empty()) throw std::invalid_argument("empty device ciphertext");
+  const hemul_status st = hemul_gpu_ct_save(g, c.h_, c.n_slots, path.c_str());
+  if (st != HEMUL_OK) throw_status(g, st);
 }
 
 // The reference algorithm's operation counts for one he_mul (rns.cpp:345-355,

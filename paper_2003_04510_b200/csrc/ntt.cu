@@ -297,8 +297,8 @@ __device__ __forceinline__ void block_group(typename F::W* sb, int grp, int sp0,
             w[(1 << i) - 1 + blk] = t.w;
             wq[(1 << i) - 1 + blk] = t.wq;
           }
-#pragma unroll
     const int sbase = swz<W>(e0);
+#pragma unroll
     for (int op = 0; op < NOPS; ++op) {
       W x[8];
       W* base = sb + op * OPS;  // OPS is a multiple of 256: slots swizzle alike

@@ -39,6 +39,7 @@ HEMUL_E_DEPTH = 3
 HEMUL_E_CUDA = 4
 HEMUL_E_OOM = 5
 HEMUL_E_NO_EVK = 6
+HEMUL_E_IO = 7
 
 STAGES = ("crt", "ntt", "intt", "icrt", "extra")  # counters.hpp:13
 KERNEL_CLASSES = ("crt", "ntt_a", "ntt_b", "intt_b", "intt_a", "tensor", "evk", "icrt",
@@ -115,6 +116,15 @@ _SIGS.update({
                                             ctypes.POINTER(ctypes.c_void_p)]),
     "hemul_gpu_ct_mod_down": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_void_p)]),
+})
+_SIGS.update({
+    "hemul_gpu_ct_load": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p,
+                                         ctypes.POINTER(ctypes.c_void_p),
+                                         ctypes.POINTER(ctypes.c_int)]),
+    "hemul_gpu_ct_save": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                         ctypes.c_char_p]),
+    "hemul_gpu_mul_by_ternary": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t,
+                                                _u64p, ctypes.c_void_p, _u64p]),
 })
 HEMUL_OPT_LEVEL_CACHE = 4
 ENGINE_INFO = ("word", "np1", "np2", "split_h", "crt1_tc", "crt2_tc", "big_tc", "fused_mid",
@@ -407,6 +417,28 @@ class Context:
         h = ctypes.c_void_p()
         self._check(self._lib.hemul_gpu_ct_mod_down(self._h, c._h, new_log_q, ctypes.byref(h)))
         return DeviceCiphertext(self, h)
+
+    def load_dev(self, path: str) -> tuple[DeviceCiphertext, int]:
+        """HEA1 ciphertext file (io.cpp:101-141) straight into HBM; returns
+        (handle, n_slots)."""
+        h = ctypes.c_void_p()
+        slots = ctypes.c_int()
+        self._check(self._lib.hemul_gpu_ct_load(self._h, str(path).encode(), ctypes.byref(h),
+                                                ctypes.byref(slots)))
+        return DeviceCiphertext(self, h), slots.value
+
+    def save_dev(self, c: DeviceCiphertext, path: str, n_slots: int = 0) -> None:
+        self._check(self._lib.hemul_gpu_ct_save(self._h, c._h, n_slots, str(path).encode()))
+
+    def mul_by_ternary(self, a: np.ndarray, t: np.ndarray, log_q: int) -> np.ndarray:
+        """Scheme::mul_by_ternary (heaan.cpp:234-256) on the GPU."""
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        t = np.ascontiguousarray(t, dtype=np.int32)
+        out = np.empty_like(a)
+        batch = a.size // (self.n * limbs(log_q))
+        self._check(self._lib.hemul_gpu_mul_by_ternary(self._h, log_q, batch, a.ctypes.data,
+                                                       t.ctypes.data, out.ctypes.data))
+        return out
 
     def set_level_cache(self, capacity: int) -> None:
         """Level LRU capacity (default 2 like Scheme::level, heaan.cpp:119-150)."""

@@ -15,6 +15,8 @@
 //       download); each step bit-identical to the host-API step
 //   dropin_check counters <log_p> <depth> <log_n> <seed> <four> <periodic> (GPU)
 //       Scheme::counters of one he_mul (compared with the reference's)
+//   dropin_check params <log_p> <depth> <log_n> <path>                 (CPU only)
+//       save_params (io.hpp)
 //   dropin_check tables <np> <log_n> <log_q> <w32>                    (CPU only)
 //       digest of generate_primes / make_{crt,ntt,icrt}_tables (params.hpp)
 //   dropin_check errors                                                (GPU)
@@ -30,6 +32,7 @@
 
 #include "hemul/bench.hpp"
 #include "hemul/heaan.hpp"
+#include "hemul/io.hpp"
 
 using namespace hemul;
 
@@ -291,6 +294,10 @@ int main(int argc, char** argv) {
     if (cmd == "counters" && argc == 8)
       return cmd_counters(arg(2), arg(3), arg(4), std::strtoull(argv[5], nullptr, 10), arg(6),
                           arg(7));
+    if (cmd == "params" && argc == 6) {
+      save_params(argv[5], make_params(arg(2), arg(3), WordSize::w64, arg(4)));
+      return 0;
+    }
     if (cmd == "tables" && argc == 6) {
       std::printf("table_digest %016llx\n",
                   static_cast<unsigned long long>(table_digest(arg(2), arg(3), arg(4), arg(5))));
