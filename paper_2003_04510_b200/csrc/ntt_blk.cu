@@ -21,6 +21,8 @@
 // (level_tables.hpp dev32_m / dev32_tm; context.cu blk_mont).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "fields.cuh"
 #include "kernels.hpp"
 
@@ -54,7 +56,8 @@ struct BlkGeo {
   static constexpr int R = S - 5;
   static constexpr int NSH = S - 2 * R;
   static constexpr int NH = EPT - 1;  // twiddles of R register levels
-  static constexpr int BS = (1 << S) + (1 << (S - 5));  // padded slot (words)
+  // padded slot (words); S = 8 also holds the f1pad exchange (< 284)
+  static constexpr int BS = S == 8 ? 288 : (1 << S) + (1 << (S - 5));
 };
 
 __device__ __forceinline__ Twiddle32 ldtw(const Twiddle32* p) {
@@ -206,6 +209,169 @@ __device__ __forceinline__ void inv(uint32_t (&v)[BlkGeo<S>::EPT], const BlkTw<S
   }
 }
 
+// ---- S = 8 without shuffle levels ----------------------------------------
+// The generic form above runs levels R .. S-R-1 (two of them at S = 8) as
+// shuffle levels: every lane computes the whole butterfly (a duplicated
+// Shoup product) plus a shuffle and three selects. At S = 8 the 8 levels are
+// split instead into
+//   layout H: y = lane + 32 r              levels 0-2 (r = y7 y6 y5)
+//   -- shared exchange (pad f1(y) = y + 4 (y >> 5): H stores and M loads
+//      are both bank-conflict free) --
+//   layout M: y = (lane & 3) + 4 r + 32 (lane >> 2)   levels 3-5 (r = y4 y3 y2)
+//   -- two register <-> lane bit swaps: lane bit 1 (y1) <-> r bit 2 (y4),
+//      lane bit 0 (y0) <-> r bit 1 (y3); one shuffle per register pair --
+//   layout L': lane = y >> 3, r = (y1, y0, y2)   levels 6-7
+// and L' is the parked layout L (y = 8 lane + rL) with the registers renamed
+// (rL = 4 b0 + 2 b2 + b1 for r = b2 b1 b0). Same butterflies, same lazy
+// ranges, same outputs; the inverse runs the mirror image.
+__device__ __forceinline__ int f1pad(int y) { return y + 4 * (y >> 5); }
+__device__ __forceinline__ constexpr int rl_of(int r) {  // L' register -> L index
+  return 4 * (r & 1) + 2 * ((r >> 2) & 1) + ((r >> 1) & 1);
+}
+
+struct BlkTw8 {
+  uint32_t hw[7], hq[7];   // H levels 0-2: (gbase << L) + blk (uniform)
+  uint32_t mw[7], mq[7];   // M levels 3-5: (gbase << L) + (lane >> 2) 2^(L-3) + blk
+  uint32_t w6[2], q6[2];   // level 6: (gbase << 6) + 2 lane + b0
+  uint32_t w7[4], q7[4];   // level 7: (gbase << 7) + 4 lane + 2 b0 + b2
+  __device__ __forceinline__ void load(const Twiddle32* t, uint32_t gbase, int lane) {
+#pragma unroll
+    for (int L = 0; L < 3; ++L)
+#pragma unroll
+      for (int b = 0; b < (1 << L); ++b) {
+        const Twiddle32 x = ldtw(t + (size_t(gbase) << L) + b);
+        hw[(1 << L) - 1 + b] = x.w;
+        hq[(1 << L) - 1 + b] = x.wq;
+      }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int b = 0; b < (1 << k); ++b) {
+        const int L = 3 + k;
+        const Twiddle32 x = ldtw(t + (size_t(gbase) << L) + (size_t(lane >> 2) << k) + b);
+        mw[(1 << k) - 1 + b] = x.w;
+        mq[(1 << k) - 1 + b] = x.wq;
+      }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const Twiddle32 x = ldtw(t + (size_t(gbase) << 6) + 2 * lane + b);
+      w6[b] = x.w;
+      q6[b] = x.wq;
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {  // b = 2 b0 + b2
+      const Twiddle32 x = ldtw(t + (size_t(gbase) << 7) + 4 * lane + b);
+      w7[b] = x.w;
+      q7[b] = x.wq;
+    }
+  }
+};
+
+// exchange register bit RB with lane bit LB (see the S = 8 notes)
+template <int RB>
+__device__ __forceinline__ void swap_bit(uint32_t (&v)[8], int lane, int lb) {
+  const bool c = (lane >> lb) & 1;
+#pragma unroll
+  for (int r0 = 0; r0 < 8; ++r0) {
+    if (r0 & (1 << RB)) continue;
+    const int r1 = r0 | (1 << RB);
+    const uint32_t send = c ? v[r0] : v[r1];
+    const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1 << lb);
+    v[r0] = c ? recv : v[r0];
+    v[r1] = c ? v[r1] : recv;
+  }
+}
+
+// register level over pairs (r, r + 2^K) of an 8-array; TW(blk) = group twiddle
+template <int K, bool INV, typename TwF>
+__device__ __forceinline__ void reg_level8(uint32_t (&v)[8], const TwF& tw, uint32_t p2,
+                                           uint32_t negp) {
+  constexpr int half = 1 << K;
+#pragma unroll
+  for (int blk = 0; blk < 8 / (2 * half); ++blk) {
+    uint32_t w, wq;
+    tw(blk, w, wq);
+#pragma unroll
+    for (int rr = 0; rr < half; ++rr) {
+      if constexpr (INV)
+        gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+      else
+        ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+    }
+  }
+}
+
+// levels 6 / 7 in layout L': level 6 pairs bit 2 (twiddle by b0), level 7
+// pairs bit 1 (twiddle by b0, b2)
+template <bool INV>
+__device__ __forceinline__ void level6(uint32_t (&v)[8], const BlkTw8& T, uint32_t p2,
+                                       uint32_t negp) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if constexpr (INV)
+      gs(v[r], v[r + 4], T.w6[r & 1], T.q6[r & 1], p2, negp);
+    else
+      ct(v[r], v[r + 4], T.w6[r & 1], T.q6[r & 1], p2, negp);
+  }
+}
+template <bool INV>
+__device__ __forceinline__ void level7(uint32_t (&v)[8], const BlkTw8& T, uint32_t p2,
+                                       uint32_t negp) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    if (r & 2) continue;
+    const int b = 2 * (r & 1) + (r >> 2);
+    if constexpr (INV)
+      gs(v[r], v[r + 2], T.w7[b], T.q7[b], p2, negp);
+    else
+      ct(v[r], v[r + 2], T.w7[b], T.q7[b], p2, negp);
+  }
+}
+
+// forward levels: v in layout H on entry, L' on exit (slot = scratch)
+__device__ __forceinline__ void fwd8(uint32_t (&v)[8], const BlkTw8& T, uint32_t* slot, int lane,
+                                     uint32_t p2, uint32_t negp) {
+  reg_level8<2, false>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.hw[0]; q = T.hq[0]; }, p2, negp);
+  reg_level8<1, false>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.hw[1 + b]; q = T.hq[1 + b]; }, p2, negp);
+  reg_level8<0, false>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.hw[3 + b]; q = T.hq[3 + b]; }, p2, negp);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) slot[f1pad(lane + 32 * r)] = v[r];
+  __syncwarp();
+  const int mbase = f1pad((lane & 3) + 32 * (lane >> 2));
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = slot[mbase + 4 * r];
+  __syncwarp();
+  reg_level8<2, false>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.mw[0]; q = T.mq[0]; }, p2, negp);
+  reg_level8<1, false>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.mw[1 + b]; q = T.mq[1 + b]; }, p2, negp);
+  reg_level8<0, false>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.mw[3 + b]; q = T.mq[3 + b]; }, p2, negp);
+  swap_bit<2>(v, lane, 1);
+  swap_bit<1>(v, lane, 0);
+  level6<false>(v, T, p2, negp);
+  level7<false>(v, T, p2, negp);
+}
+
+// inverse levels: layout L' on entry, layout H on exit
+__device__ __forceinline__ void inv8(uint32_t (&v)[8], const BlkTw8& T, uint32_t* slot, int lane,
+                                     uint32_t p2, uint32_t negp) {
+  level7<true>(v, T, p2, negp);
+  level6<true>(v, T, p2, negp);
+  swap_bit<1>(v, lane, 0);
+  swap_bit<2>(v, lane, 1);
+  reg_level8<0, true>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.mw[3 + b]; q = T.mq[3 + b]; }, p2, negp);
+  reg_level8<1, true>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.mw[1 + b]; q = T.mq[1 + b]; }, p2, negp);
+  reg_level8<2, true>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.mw[0]; q = T.mq[0]; }, p2, negp);
+  const int mbase = f1pad((lane & 3) + 32 * (lane >> 2));
+#pragma unroll
+  for (int r = 0; r < 8; ++r) slot[mbase + 4 * r] = v[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = slot[f1pad(lane + 32 * r)];
+  __syncwarp();
+  reg_level8<0, true>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.hw[3 + b]; q = T.hq[3 + b]; }, p2, negp);
+  reg_level8<1, true>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.hw[1 + b]; q = T.hq[1 + b]; }, p2, negp);
+  reg_level8<2, true>(v, [&](int b, uint32_t& w, uint32_t& q) { w = T.hw[0]; q = T.hq[0]; }, p2, negp);
+}
+
 // register caps that buy one or two more CTAs per SM without spills
 // (measured at X: split tensor 2.25 -> 2.22 ms at 6 CTAs, evk 1.78 -> 1.72 at 7;
 // with the Montgomery products the evk pass fits 8: 1.74 -> 1.71 ms; 9 or a
@@ -234,7 +400,10 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
   const int block = blockIdx.x * kWarps + warp;
   const uint32_t gbase = (1u << a.s1) + block;
   const size_t off = (size_t(bt) * a.np + j) * n + (size_t(block) << S) + lane;
-  BlkTw<S> T;
+  // S = 8: no shuffle levels (fwd8 / inv8); registers are renamed (rl_of)
+  constexpr bool k8 = S == 8;
+  auto rl = [](int r) { return k8 ? rl_of(r) : r; };
+  std::conditional_t<k8, BlkTw8, BlkTw<S>> T;
   T.load(a.tw + size_t(j) * n, gbase, lane);
   // ---- forward levels of every operand; results parked in layout L. The
   // next operand's rows are loaded while this one is transformed. ----------
@@ -250,9 +419,12 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
 #pragma unroll
       for (int r = 0; r < EPT; ++r) nx[r] = a.in[o + 1][off + 32 * r];
     }
-    fwd<S>(v, T, slots + o * BS, lane, p2, negp);
+    if constexpr (k8)
+      fwd8(v, T, slots + o * BS, lane, p2, negp);
+    else
+      fwd<S>(v, T, slots + o * BS, lane, p2, negp);
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) slots[o * BS + padf(EPT * lane + r)] = v[r];
+    for (int r = 0; r < EPT; ++r) slots[o * BS + padf(EPT * lane + rl(r))] = v[r];
   }
   // ---- products at this lane's own positions (no exchange needed) -------
 #pragma unroll
@@ -280,8 +452,11 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
   for (int o = 0; o < NOUT; ++o) {
     uint32_t v[EPT];
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) v[r] = slots[o * BS + padf(EPT * lane + r)];
-    inv<S>(v, T, slots + o * BS, lane, p2, negp);
+    for (int r = 0; r < EPT; ++r) v[r] = slots[o * BS + padf(EPT * lane + rl(r))];
+    if constexpr (k8)
+      inv8(v, T, slots + o * BS, lane, p2, negp);
+    else
+      inv<S>(v, T, slots + o * BS, lane, p2, negp);
 #pragma unroll
     for (int r = 0; r < EPT; ++r) a.out[o][off + 32 * r] = v[r];
   }

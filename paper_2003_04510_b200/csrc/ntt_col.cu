@@ -45,10 +45,19 @@ struct ColGeo {
   static constexpr int R = S - 5;                 // log2(EPT)
   static_assert(EPT >= 4, "16-byte cooperative load: >= 4 residues per thread");
   static constexpr int NSH = S - 2 * R;           // shuffle levels
-  // column stride: >= f(2^S) and = 2 (mod 32)
-  static constexpr int CS = ((1 << S) + (1 << (S - 5)) + 29) / 32 * 32 + 2;
+  // half-warp form (S >= 8): 16 lanes per column, HE = 2^S / 16 residues
+  // per lane, RH = log2(HE) levels in each of the two register layouts
+  static constexpr bool kHalf = S >= 8;
+  static constexpr int HE = (1 << S) / 16;
+  static constexpr int RH = S - 4;
+  // padded position of row y: one pad word per 2^PS rows
+  static constexpr int PS = kHalf ? S - 4 : 5;
+  // column stride: > f(2^S - 1) and = 2 (mod 32)
+  static constexpr int CS = ((1 << S) + (1 << (S - PS)) + 29) / 32 * 32 + 2;
 };
 
+template <int S>
+__device__ __forceinline__ int padc(int y) { return y + (y >> ColGeo<S>::PS); }
 __device__ __forceinline__ int padf(int y) { return y + (y >> 5); }
 
 struct ColArgs {
@@ -79,9 +88,17 @@ __device__ __forceinline__ void gs(uint32_t& a, uint32_t& b, uint32_t w, uint32_
 // are bank-conflict free; w and wq live in separate arrays.
 template <int S>
 __device__ __forceinline__ int twiddle_slot(int t) {
-  if (t < 32) return t;
-  const int L = 31 - __clz(t), i = L - 5, within = t - (1 << L);
-  return (1 << L) + (within & ((1 << i) - 1)) * 32 + (within >> i);
+  if constexpr (ColGeo<S>::kHalf) {
+    // half-warp form: layout-L levels L >= RH are read by half-lane h at
+    // t = 2^L + h 2^i + blk (i = L - 4) -> stored at 2^L + blk 16 + h
+    if (t < (1 << ColGeo<S>::RH)) return t;
+    const int L = 31 - __clz(t), i = L - 4, within = t - (1 << L);
+    return (1 << L) + (within & ((1 << i) - 1)) * 16 + (within >> i);
+  } else {
+    if (t < 32) return t;
+    const int L = 31 - __clz(t), i = L - 5, within = t - (1 << L);
+    return (1 << L) + (within & ((1 << i) - 1)) * 32 + (within >> i);
+  }
 }
 
 // One warp transforms NC padded columns mc, mc + cstride, ... (see the layout
@@ -231,6 +248,139 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, int cstride, cons
   }
 }
 
+// Half-warp form of the column transform (S >= 8): the 16 lanes h of a
+// half-warp own one column, HE = 2^S / 16 residues each, and the two halves
+// of a warp take columns c and c + 8 (the column stride is 2 mod 32, so the
+// halves sit 16 banks apart). Two register layouts cover all S levels with
+// one shared-memory exchange and no shuffle levels:
+//   layout H: y = h + 16 r  -> levels 0 .. RH-1 (the top RH bits of y are r;
+//             twiddles uniform across the warp),
+//   layout L: y = HE h + r  -> levels RH .. S-1 (the low 4 bits of y are r's
+//             low bits; twiddle t = 2^L + h 2^i + blk read lane-minor).
+// The butterflies are those of column_transform (same pairs, same lazy
+// ranges), so the outputs are identical; per residue it drops the shuffle
+// level (a shuffle, three selects and a duplicated Shoup product per lane).
+// Inverse of twiddle_slot for the half-warp form: the table entry at slot s.
+template <int S>
+__device__ __forceinline__ int twiddle_entry(int s) {
+  static_assert(ColGeo<S>::kHalf, "half-warp form");
+  if (s < (1 << ColGeo<S>::RH)) return s;
+  const int L = 31 - __clz(s), i = L - 4, within = s - (1 << L);
+  return (1 << L) + ((within & 15) << i) + (within >> 4);
+}
+
+// One register level of the half-warp form with compile-time level L:
+// butterflies (r, r + half) in groups of 2 half registers, group twiddle at
+// shared slot TW(blk) (templated so that nvcc unrolls every level fully; a
+// runtime-indexed register array would turn into predicated moves).
+template <int HE, int LOG_HALF, bool INV, typename TwF>
+__device__ __forceinline__ void half_level(uint32_t (&v)[HE], const TwF& tw, uint32_t p2,
+                                           uint32_t negp) {
+  constexpr int half = 1 << LOG_HALF, groups = HE / (2 * half);
+#pragma unroll
+  for (int blk = 0; blk < groups; ++blk) {
+    uint32_t w, wq;
+    tw(blk, w, wq);
+#pragma unroll
+    for (int rr = 0; rr < half; ++rr) {
+      if constexpr (INV)
+        gs(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+      else
+        ct(v[blk * 2 * half + rr], v[blk * 2 * half + rr + half], w, wq, p2, negp);
+    }
+  }
+}
+
+template <int S, bool INV, int L, typename ReadTw>
+__device__ __forceinline__ void half_level_at(uint32_t (&v)[ColGeo<S>::HE], const ReadTw& rd, int h,
+                                              uint32_t p2, uint32_t negp) {
+  constexpr int HE = ColGeo<S>::HE, RH = ColGeo<S>::RH;
+  if constexpr (L < RH) {  // layout H: r holds the top bits, twiddle uniform
+    half_level<HE, RH - 1 - L, INV>(
+        v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + blk, w, wq); }, p2, negp);
+  } else {  // layout L: lane-minor twiddle slots (twiddle_slot)
+    half_level<HE, S - 1 - L, INV>(
+        v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + blk * 16 + h, w, wq); }, p2,
+        negp);
+  }
+}
+
+template <int S, bool INV, int L0, int L1, typename ReadTw>
+__device__ __forceinline__ void half_levels(uint32_t (&v)[ColGeo<S>::HE], const ReadTw& rd, int h,
+                                            uint32_t p2, uint32_t negp) {
+  // forward: L0, L0+1, ..., L1-1; inverse: L1-1, ..., L0
+  if constexpr (L0 < L1) {
+    if constexpr (!INV) {
+      half_level_at<S, INV, L0>(v, rd, h, p2, negp);
+      half_levels<S, INV, L0 + 1, L1>(v, rd, h, p2, negp);
+    } else {
+      half_level_at<S, INV, L1 - 1>(v, rd, h, p2, negp);
+      half_levels<S, INV, L0, L1 - 1>(v, rd, h, p2, negp);
+    }
+  }
+}
+
+// Half-warp form of the column transform (S >= 8): the 16 lanes h of a
+// half-warp own one column, HE = 2^S / 16 residues each, and the two halves
+// of a warp take columns c and c + 8 (the column stride is 2 mod 32, so the
+// halves sit 16 banks apart). Two register layouts cover all S levels with
+// one shared-memory exchange and no shuffle levels:
+//   layout H: y = h + 16 r  -> levels 0 .. RH-1 (the top RH bits of y are r;
+//             twiddles uniform across the warp),
+//   layout L: y = HE h + r  -> levels RH .. S-1 (the low 4 bits of y are r's
+//             low bits; twiddle t = 2^L + h 2^i + blk read lane-minor).
+// The butterflies are those of column_transform (same pairs, same lazy
+// ranges), so the outputs are identical; per residue it drops the shuffle
+// level (a shuffle, three selects and a duplicated Shoup product per lane).
+template <int S, bool INV>
+__device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32_t* stw,
+                                                      const DevPrime32& pr, int h) {
+  using G = ColGeo<S>;
+  constexpr int HE = G::HE, RH = G::RH;
+  static_assert(S - RH <= RH, "layout L must hold the remaining levels");
+  const uint32_t p = pr.p, p2 = 2 * p, negp = 0u - p;
+  const auto rd = [&](int idx, uint32_t& w, uint32_t& wq) {  // one LDS.64 per pair
+    const uint2 x = reinterpret_cast<const uint2*>(stw)[idx];
+    w = x.x;
+    wq = x.y;
+  };
+  uint32_t v[HE];
+  auto ld = [&](auto pos) {
+#pragma unroll
+    for (int r = 0; r < HE; ++r) v[r] = mc[padc<S>(pos(r))];
+  };
+  auto st = [&](auto pos) {
+#pragma unroll
+    for (int r = 0; r < HE; ++r) mc[padc<S>(pos(r))] = v[r];
+  };
+  auto posH = [&](int r) { return h + 16 * r; };
+  auto posL = [&](int r) { return HE * h + r; };
+  if (!INV) {
+    ld(posH);
+    half_levels<S, false, 0, RH>(v, rd, h, p2, negp);
+    st(posH);
+    __syncwarp();
+    ld(posL);
+    half_levels<S, false, RH, S>(v, rd, h, p2, negp);
+    st(posL);
+  } else {
+    ld(posL);
+    half_levels<S, true, RH, S>(v, rd, h, p2, negp);
+    st(posL);
+    __syncwarp();
+    ld(posH);
+    half_levels<S, true, 1, RH>(v, rd, h, p2, negp);
+#pragma unroll
+    for (int rr = 0; rr < HE / 2; ++rr) {
+      // level 0 with n^-1 folded (F32::inv_level0)
+      const uint32_t u = v[rr], w2 = v[rr + HE / 2];
+      v[rr] = csub32(shoup32(u + w2, pr.ninv, pr.ninv_q, negp), p);
+      v[rr + HE / 2] = csub32(shoup32(u + p2 - w2, pr.w1n, pr.w1n_q, negp), p);
+    }
+    st(posH);
+  }
+}
+
 // Columns per warp-transform: the forward pass runs two interleaved columns
 // (2.23 -> 2.12 ms per step at X, 3 CTAs/SM), the inverse pass one (two are
 // slower there: 2.35 -> 2.44 ms). The macros exist for tools/build_variant.sh
@@ -246,14 +396,18 @@ __device__ __forceinline__ void column_transform(uint32_t* mc, int cstride, cons
 #ifndef HEMUL_COL_MINB_FWD
 #define HEMUL_COL_MINB_FWD 3
 #endif
-template <bool INV>
+#ifndef HEMUL_COL_MINB_HALF
+#define HEMUL_COL_MINB_HALF 4
+#endif
+template <int S, bool INV>
 struct ColCfg {
   static constexpr int NC = INV ? HEMUL_COL_NC_INV : 2;
-  static constexpr int kMinBlocks = INV ? HEMUL_COL_MINB_INV : HEMUL_COL_MINB_FWD;
+  static constexpr int kMinBlocks =
+      ColGeo<S>::kHalf ? HEMUL_COL_MINB_HALF : (INV ? HEMUL_COL_MINB_INV : HEMUL_COL_MINB_FWD);
 };
 
 template <int S, bool INV>
-__global__ void __launch_bounds__(kThreads, ColCfg<INV>::kMinBlocks) ntt_col_kernel(ColArgs a) {
+__global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_kernel(ColArgs a) {
   constexpr int CS = ColGeo<S>::CS;
   extern __shared__ uint32_t smem[];
   uint32_t* col = smem;                        // [kCols][CS]
@@ -281,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, ColCfg<INV>::kMinBlocks) ntt_col_ker
 #pragma unroll
     for (int r = 0; r < (1 << S) / RS; ++r) {
       const uint4 q = src[r * step];
-      const int fy = padf(y0 + RS * r);
+      const int fy = padc<S>(y0 + RS * r);
       col[x4 * CS + fy] = q.x;
       col[(x4 + 1) * CS + fy] = q.y;
       col[(x4 + 2) * CS + fy] = q.z;
@@ -289,16 +443,28 @@ __global__ void __launch_bounds__(kThreads, ColCfg<INV>::kMinBlocks) ntt_col_ker
     }
     const uint32_t* t2 = reinterpret_cast<const uint32_t*>(a.tw + size_t(j) * n);
     for (int i = tid; i < 1 << S; i += kThreads) {
-      const int pos = twiddle_slot<S>(i);
-      stw[pos] = t2[2 * i];
-      stw[(1 << S) + pos] = t2[2 * i + 1];
+      if constexpr (ColGeo<S>::kHalf) {
+        // (w, wq) pairs interleaved; walk the slots (consecutive shared
+        // words per warp) and gather the table entry each slot holds
+        reinterpret_cast<uint2*>(stw)[i] =
+            reinterpret_cast<const uint2*>(t2)[twiddle_entry<S>(i)];
+      } else {
+        const int pos = twiddle_slot<S>(i);
+        stw[pos] = t2[2 * i];
+        stw[(1 << S) + pos] = t2[2 * i + 1];
+      }
     }
   }
   __syncthreads();
-  constexpr int NC = ColCfg<INV>::NC;
-  static_assert(kCols % (kWarps * NC) == 0, "columns per warp");
-  for (int cw = warp; cw < kCols; cw += kWarps * NC)
-    column_transform<S, INV, NC>(col + cw * CS, kWarps * CS, stw, pr, lane);
+  if constexpr (ColGeo<S>::kHalf) {
+    static_assert(kCols == 2 * kWarps, "one column per half-warp");
+    column_transform_half<S, INV>(col + (warp + kWarps * (lane >> 4)) * CS, stw, pr, lane & 15);
+  } else {
+    constexpr int NC = ColCfg<S, INV>::NC;
+    static_assert(kCols % (kWarps * NC) == 0, "columns per warp");
+    for (int cw = warp; cw < kCols; cw += kWarps * NC)
+      column_transform<S, INV, NC>(col + cw * CS, kWarps * CS, stw, pr, lane);
+  }
   __syncthreads();
   // ---- cooperative store ------------------------------------------------
   {
@@ -308,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, ColCfg<INV>::kMinBlocks) ntt_col_ker
     const size_t step = size_t(RS) * tlast / 4;
 #pragma unroll
     for (int r = 0; r < (1 << S) / RS; ++r) {
-      const int fy = padf(y0 + RS * r);
+      const int fy = padc<S>(y0 + RS * r);
       dst[r * step] = make_uint4(col[x4 * CS + fy], col[(x4 + 1) * CS + fy],
                                  col[(x4 + 2) * CS + fy], col[(x4 + 3) * CS + fy]);
     }

@@ -36,6 +36,10 @@ LADDERS = [
     ((30, 80, 12), [2400, 1800, 1230, 600, 300, 90, 60]),
     ((30, 40, 12), [1200, 870, 450, 60]),
     ((30, 20, 13), [600, 330, 60]),
+    # paper ring degrees (small log_q): the half-warp column pass and the
+    # S = 8 middle pass run only at log N >= 15
+    ((30, 4, 16), [120, 60]),
+    ((30, 4, 17), [120]),
 ]
 
 
@@ -97,7 +101,8 @@ def _check_rows(got, want_slots, primes, t_form):
 
 @pytest.mark.parametrize("tc", [True, False], ids=["tc", "imad"])
 @pytest.mark.parametrize("cfg,levels", LADDERS, ids=["X_logQ@N4096", "M_logQ@N4096",
-                                                     "logQ600@N8192"])
+                                                     "logQ600@N8192", "logQ120@N65536",
+                                                     "logQ120@N131072"])
 def test_stage_checkpoints_along_the_ladder(cfg, levels, tc, restated):
     ctx = _ctx(cfg, tc)
     p = ctx.params
