@@ -25,9 +25,12 @@ Printed JSON (rank 0, one line):
             on this device in this run (tcgen05 probe; or IMAD.WIDE products
             vs the IMAD probe with --engine imad). `kernels` lists every class.
   cpu_baseline  the reference CPU he_mul (oracle/_ref, compiled from the
-            reference sources) on this host's cores, 1 HE Mul sample
---impl reference times that same reference CPU implementation as the whole
-arm (all host threads), on the same config and metric.
+            reference sources) in its fastest variant (NTT radix 16) on this
+            host: 1 HE Mul on all cores (value) + 1 on one thread (latency
+            comparison), CPU model and clock; --cpu-full adds the full
+            protocol (3 reps x radix 2/16 x 1/all threads)
+--impl reference times that same reference CPU implementation (fastest
+variant, all host threads) as the whole arm, on the same config and metric.
 """
 from __future__ import annotations
 
@@ -35,6 +38,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -250,7 +254,29 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # reference CPU arm / baseline
 # --------------------------------------------------------------------------
-def reference_cpu(cfg, reps: int, threads: int, seed: int = 1):
+# The reference's fastest NTT variant on this host (SURVEY.md §8(d):
+# radix 2^4 beats the default radix 2 by 11-27 %, profiles/r01_cpu_ref_threads.json);
+# both the cpu_baseline leg and the reference arm use it.
+FASTEST_RADIX_LOG = 4
+
+
+def cpu_info() -> dict:
+    """CPU model, logical cores and the current clock (median of /proc/cpuinfo)."""
+    model, mhz = platform.processor(), []
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+            elif line.startswith("cpu MHz"):
+                mhz.append(float(line.split(":", 1)[1]))
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count() or 1,
+            "cpu_mhz": statistics.median(mhz) if mhz else None}
+
+
+def reference_cpu(cfg, reps: int, threads: int, seed: int = 1,
+                  radix_log: int = FASTEST_RADIX_LOG):
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import REFERENCE_SO, Reference
 
@@ -258,15 +284,74 @@ def reference_cpu(cfg, reps: int, threads: int, seed: int = 1):
         return None, "oracle/_ref/libhemul_ref.so missing (build it where /root/reference exists)"
     ref = Reference()
     t0 = time.time()
-    ms, dig = ref.time_he_mul(*cfg, seed=seed, reps=reps, threads=threads, radix_log=1)
+    ms, dig = ref.time_he_mul(*cfg, seed=seed, reps=reps, threads=threads, radix_log=radix_log)
     return {"ms": ms, "digest": f"{dig:016x}", "wall_s": time.time() - t0}, None
+
+
+def reference_cpu_full(cfg, reps: int = 3) -> dict:
+    """SURVEY.md §8(d) CPU protocol: `reps` HE Muls at radix 2 (the reference
+    default, tools/hemul.cpp:141) and radix 16, on 1 thread and on all threads."""
+    nproc = os.cpu_count() or 1
+    rows = []
+    for threads in (1, nproc):
+        for radix_log in (1, 4):
+            res, why = reference_cpu(cfg, reps=reps, threads=threads, radix_log=radix_log)
+            if res is None:
+                return {"unavailable": why}
+            rows.append({"threads": threads, "radix": 1 << radix_log, "ms": res["ms"],
+                         "ms_median": statistics.median(res["ms"]), "digest": res["digest"]})
+            print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+    single = min((r for r in rows if r["threads"] == 1), key=lambda r: r["ms_median"])
+    return {**cpu_info(), "reps": reps, "results": rows,
+            "fastest_single_thread_ms": single["ms_median"],
+            "fastest_single_thread_radix": single["radix"]}
+
+
+STAGE_MAP = {
+    "crt": "crt_forward of region 1 (8 half-inputs) and region 2 (ModUp of d2)",
+    "ntt": "forward pass A + the fused middle passes (forward tails, the pointwise "
+           "tensor / evk products the reference books under iCRT, inverse heads)",
+    "intt": "inverse pass A (emits t_j = x (P/p_j)^-1)",
+    "icrt": "iCRT of d2 + the fused finisher (ModDown, d0/d1 add, rescale: the "
+            "reference's Extra work)",
+    "extra": "0: poly_add/sub/shift are fused into the finisher (icrt)",
+}
+
+
+def poly_source(n: int, seed: int, device: str = "cuda"):
+    """rand_poly(batch, bits): uniform BigPolys (batch, n, limbs) mod 2^bits
+    from one seeded device generator."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def rand_poly(batch, bits):
+        t = torch.randint(-(2**63), 2**63 - 1, (batch, n, limbs(bits)), generator=g,
+                          device=device, dtype=torch.int64)
+        if bits % 64:
+            t[..., -1] &= (1 << (bits % 64)) - 1
+        return t.view(torch.uint64)
+
+    return rand_poly
+
+
+def make_inputs(n: int, q: int, B: int, seed: int, device: str = "cuda"):
+    """The bench's synthetic inputs (rank r uses seed 1000 + r): B ciphertext
+    pairs mod 2^q and an evk mod 2^(2q), uniform limbs, top limb masked."""
+    rand_poly = poly_source(n, seed, device)
+    c1 = (rand_poly(B, q), rand_poly(B, q))
+    c2 = (rand_poly(B, q), rand_poly(B, q))
+    evk = (rand_poly(1, 2 * q)[0].contiguous(), rand_poly(1, 2 * q)[0].contiguous())
+    return c1, c2, evk
 
 
 def run_reference_arm(args, cfg, rank: int) -> None:
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    # one step = one full HE Mul; warm-up steps run untimed
+    # one step = one full HE Mul (fastest variant, all host threads); warm-up
+    # steps run untimed
     res, why = reference_cpu(cfg, reps=args.warmup + args.steps, threads=threads)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": why}))
@@ -278,16 +363,18 @@ def run_reference_arm(args, cfg, rank: int) -> None:
 
     p = make_params(*cfg)
     sample = (f"{args.steps} timed + {args.warmup} warm-up reference Scheme::he_mul calls "
-              f"(N=2^{p.log_n}, logQ={p.log_q_max}), random inputs, level warmed outside timing")
+              f"(N=2^{p.log_n}, logQ={p.log_q_max}, NTT radix {1 << FASTEST_RADIX_LOG}, the "
+              f"fastest variant), random inputs, level warmed outside timing")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "HE Mul/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "latency_us": ms * 1000.0, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{args.config}: HE Mul N=2^{p.log_n} logQ={p.log_q_max}",
-                   "batch_per_gpu": 1, "threads": threads},
+                   "batch_per_gpu": 1, "threads": threads,
+                   "radix": 1 << FASTEST_RADIX_LOG},
         "cpu_baseline": {"value": value, "unit": "HE Mul/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, **cpu_info()},
         "e2e": {"value": value, "unit": "HE Mul/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "digest": res["digest"],
@@ -306,7 +393,15 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=0, help="HE Muls per GPU per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also run the full CPU protocol (3 reps, radix 2/16, 1/all threads; "
+                         "several minutes at X) into cpu_baseline.full")
     ap.add_argument("--latency-reps", type=int, default=5)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: the same code path without "
+                         "NCCL, e.g. for two ranks sharing one GPU in tests)")
+    ap.add_argument("--one-device", action="store_true",
+                    help="every rank on cuda:0 (exercises the multi-rank path on one GPU)")
     ap.add_argument("--chain", type=int, default=8,
                     help="device-resident chain length for the `chain` key (0 = skip)")
     ap.add_argument("--basis", type=int, default=32, choices=[32, 64],
@@ -331,9 +426,14 @@ def main() -> None:
     from paper_2003_04510_b200.dist import gather_to_rank0, max_over_ranks
     from paper_2003_04510_b200.hemul import Context, ciphertext_digest, make_params
 
+    if args.one_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     p = make_params(*cfg)
     ctx = Context(p, device=local)
     # a dedicated (non-legacy) stream shared by torch and the library, so the
@@ -349,19 +449,7 @@ def main() -> None:
 
     # synthetic random ciphertexts and keys (SURVEY §8(d) throughput inputs),
     # generated on the device, resident before timing; per-rank seeds
-    g = torch.Generator(device="cuda")
-    g.manual_seed(1000 + rank)
-
-    def rand_poly(batch, bits):
-        t = torch.randint(-(2**63), 2**63 - 1, (batch, n, limbs(bits)), generator=g,
-                          device="cuda", dtype=torch.int64)
-        if bits % 64:
-            t[..., -1] &= (1 << (bits % 64)) - 1
-        return t.view(torch.uint64)
-
-    c1 = (rand_poly(B, q), rand_poly(B, q))
-    c2 = (rand_poly(B, q), rand_poly(B, q))
-    evk = (rand_poly(1, 2 * q)[0].contiguous(), rand_poly(1, 2 * q)[0].contiguous())
+    c1, c2, evk = make_inputs(n, q, B, seed=1000 + rank)
     out = (torch.empty((B, n, Lo), dtype=torch.uint64, device="cuda"),
            torch.empty((B, n, Lo), dtype=torch.uint64, device="cuda"))
     t0 = time.time()
@@ -455,6 +543,7 @@ def main() -> None:
     chain = None
     if K > 0:
         ctx.set_level_cache(K + 1)
+        rand_poly = poly_source(n, seed=2000 + rank)
         hf = [tuple(rand_poly(B, q).cpu().pin_memory() for _ in range(2)) for _ in range(K)]
         ha = (nph(hc1[0]), nph(hc1[1]))
         hres = tuple(torch.empty((B, n, limbs(q - K * p.log_p)), dtype=torch.uint64).pin_memory()
@@ -546,14 +635,25 @@ def main() -> None:
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
+            # bounded sample (~25 s of CPU work at X): one HE Mul of the
+            # reference's fastest variant on all host threads (the value) and
+            # one on a single thread (the latency comparison)
             threads = os.cpu_count() or 1
             res, why = reference_cpu(cfg, reps=1, threads=threads)
+            one, _ = reference_cpu(cfg, reps=1, threads=1) if res is not None else (None, None)
             if res is not None:
                 v = 1000.0 / res["ms"][0]
                 cpu = {"value": v, "unit": "HE Mul/s", "cores": threads, "kind": "reference",
-                       "sample": f"1 reference Scheme::he_mul (N=2^{p.log_n}, logQ={q}) on "
-                                 f"{threads} threads, random inputs, level warmed outside timing",
-                       "latency_ms": res["ms"][0]}
+                       "sample": f"1 reference Scheme::he_mul (N=2^{p.log_n}, logQ={q}, NTT radix "
+                                 f"{1 << FASTEST_RADIX_LOG}) on {threads} threads and 1 on one "
+                                 f"thread, random inputs, level warmed outside timing",
+                       "latency_ms": res["ms"][0],
+                       "single_thread_latency_ms": one["ms"][0] if one else None,
+                       "radix": 1 << FASTEST_RADIX_LOG, **cpu_info()}
+                if one:
+                    cpu["gpu_latency_speedup_vs_single_thread"] = one["ms"][0] * 1000.0 / latency_us
+                if args.cpu_full:
+                    cpu["full"] = reference_cpu_full(cfg)
             else:
                 cpu = {"value": None, "unavailable": why}
         line = {
@@ -567,6 +667,8 @@ def main() -> None:
                                    f"{' per half product' if word == 32 else ''}, np2={np2}",
                        "batch_per_gpu": B, "global_batch": B * world,
                        "parallelism": f"ciphertext-sharded x{world}, evk replicated",
+                       "dist_backend": args.dist_backend if world > 1 else None,
+                       "seeds": f"rank r: inputs seed 1000 + r (bench.make_inputs)",
                        "l2": f"inputs {4 * B * n * L * 8 / 2**20:.0f} MiB per step > 126 MiB L2"},
             "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": "HE Mul/s",
@@ -579,6 +681,9 @@ def main() -> None:
             "peaks": {"tensor_int8_tops": tc_peak / 1e12, "imad_wide_tops": imad_peak / 1e12,
                       "hbm_gbs": hbm_peak},
             "stage_ms_one_call": stage_ms,
+            # our buckets vs the reference's StageTimers (counters.hpp, rns.cpp:364,
+            # bench.cpp:81-84: pointwise booked under iCRT, add/sub/shift under Extra)
+            "stage_map": STAGE_MAP,
             "level_setup_s": level_s,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

@@ -266,6 +266,21 @@ hemul_status hemul_gpu_level_info(hemul_gpu_ctx *ctx, int log_q, int region, int
  * rows of n residues; row r is transformed mod prime (r % np) of the region. */
 hemul_status hemul_gpu_ntt(hemul_gpu_ctx *ctx, int log_q, int region, uint64_t *data, size_t rows,
                            int inverse);
+/* ntt_forward / ntt_inverse (ntt.cpp:59-137, 153-197) in the B200 30-bit
+ * basis of a level (hemul_gpu_level_info region -1 / -2 lists its primes):
+ * rows of n u32 residues, row r mod prime r % np over the basis' first np
+ * primes (np = 0: all of them), the column / block kernels of the he_mul
+ * path (pass A ntt_col.cu + pass B), outputs in the lazy ranges of the
+ * 30-bit field ([0, 4p) forward, [0, p) inverse). For the C2 NTT sweep and
+ * residue-level tests. */
+hemul_status hemul_gpu_ntt32(hemul_gpu_ctx *ctx, int log_q, int region, int np, uint32_t *data,
+                             size_t rows, int inverse);
+/* make_ntt_tables (params.cpp:151-180) of the level's 30-bit basis, built on
+ * the device: prime j's forward and inverse twiddles as n (w, wq) u32 pairs
+ * each, tw[rev(i)] = psi_j^i, itw[rev(i)] = psi_j^-i, wq = floor(w 2^32 / p_j)
+ * (either output may be NULL). Introspection for tests. */
+hemul_status hemul_gpu_level_twiddles32(hemul_gpu_ctx *ctx, int log_q, int region, int j,
+                                        uint32_t *tw, uint32_t *itw);
 /* crt_forward (rns.cpp:331-358): batch polys of n x ceil(in_bits/64) limbs ->
  * batch x np x n residues. */
 hemul_status hemul_gpu_crt(hemul_gpu_ctx *ctx, int log_q, int region, int in_bits, size_t batch,

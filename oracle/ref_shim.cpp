@@ -422,6 +422,40 @@ int ref_prepare(int region, int log_q, int log_q_max, int log_n, int in_bits,
 }
 
 // Forward (inverse=0) or inverse NTT in place over np x n prime-major rows.
+// bench_ntt.cpp:10-27 protocol widened to the C2 sweep:
+// generate_primes(np, log_n, w64), residues Rng(3).below(p_j), `reps` timed
+// ntt_forward / ntt_inverse calls on a fresh copy each (copy untimed), on
+// `threads` threads (ThreadPool) at NTT radix 2^radix_log.
+int ref_time_ntt(int log_n, int np, int threads, int radix_log, int reps, int inverse,
+                 double* ms_out) {
+  try {
+    const PrimeSet ps = generate_primes(np, log_n, WordSize::w64);
+    const NttTables nt = make_ntt_tables(ps, log_n);
+    const int n = 1 << log_n;
+    Rng rng(3);
+    RnsMatrix m = make_rns(np, n, Layout::prime_major);
+    for (int j = 0; j < np; ++j)
+      for (int i = 0; i < n; ++i) m.at(j, i) = rng.below(ps.primes[j]);
+    std::unique_ptr<ThreadPool> pool;
+    if (threads > 1) pool = std::make_unique<ThreadPool>(threads);
+    NttOptions opt;
+    opt.radix_log = radix_log > 0 ? radix_log : 1;
+    for (int r = 0; r < reps; ++r) {
+      RnsMatrix copy = m;
+      const auto t0 = std::chrono::steady_clock::now();
+      if (inverse)
+        ntt_inverse(copy, ps, nt, opt, pool.get());
+      else
+        ntt_forward(copy, ps, nt, opt, pool.get());
+      const auto t1 = std::chrono::steady_clock::now();
+      ms_out[r] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
 int ref_ntt(int region, int log_q, int log_q_max, int log_n, uint64_t* data,
             int inverse) {
   try {

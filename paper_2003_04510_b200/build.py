@@ -32,7 +32,7 @@ CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I", str(ROOT / "include"),
              "-I", str(CSRC)]
 
-CU_SOURCES = ["ntt.cu", "ntt_col.cu", "ntt_blk.cu", "crt.cu", "crt_tc.cu", "bigint_tc.cu", "icrt.cu", "poly.cu", "probe.cu", "context.cu"]
+CU_SOURCES = ["ntt.cu", "ntt_col.cu", "ntt_blk.cu", "crt.cu", "crt_tc.cu", "bigint_tc.cu", "icrt.cu", "poly.cu", "probe.cu", "tables.cu", "context.cu"]
 CPP_SOURCES = ["level_tables.cpp"]
 
 

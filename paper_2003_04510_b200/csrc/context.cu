@@ -296,8 +296,25 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
     upload(d.primes_t, h.dev32_t, st);
     upload(d.primes_m, h.dev32_m, st);
     upload(d.primes_tm, h.dev32_tm, st);
-    upload(d.tw, h.tw32, st);
-    upload(d.itw, h.itw32, st);
+    // twiddles on the device (tables.cu): primes, psi_j, psi_j^-1 in, np x n
+    // Shoup pairs per direction out
+    const size_t n = size_t(1) << h.log_n, bytes = size_t(h.np) * n * sizeof(Twiddle32);
+    if (!d.tw.ensure(bytes + 16) || !d.itw.ensure(bytes + 16))
+      throw CudaFail(HEMUL_E_OOM, "device allocation failed");
+    std::vector<uint32_t> pr(3 * size_t(h.np));
+    for (int j = 0; j < h.np; ++j) {
+      const uint64_t p = h.primes[j];
+      pr[j] = uint32_t(p);
+      pr[h.np + j] = uint32_t(h.roots[j]);
+      pr[2 * h.np + j] = uint32_t(h.roots_inv[j]);
+    }
+    DevBuf tmp;
+    upload(tmp, pr, st);
+    const uint32_t* t = tmp.as<uint32_t>();
+    check(build_twiddles32(t, t + h.np, t + 2 * h.np, h.np, h.log_n, d.tw.as<Twiddle32>(),
+                           d.itw.as<Twiddle32>(), st),
+          "twiddle tables");
+    check(cudaStreamSynchronize(st), "twiddle tables");  // tmp is freed on return
   }
   upload(d.btab, h.btab, st);
   d.icrt.btab = d.btab.as<uint32_t>();
@@ -1860,6 +1877,70 @@ hemul_status hemul_gpu_ntt(hemul_gpu_ctx* c, int log_q, int region, uint64_t* da
   if (!c || !data || (region != 1 && region != 2)) return HEMUL_E_ARG;
   return guarded(c, [&] {
     stage_ntt(c, stage_region(c, log_q, region), c->log_n, data, rows, inverse);
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_ntt32(hemul_gpu_ctx* c, int log_q, int region, int np, uint32_t* data,
+                             size_t rows, int inverse) {
+  if (!c || !data || (region != 1 && region != 2) || np < 0) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    Level& lv = get_level(c, log_q);
+    const Basis& bs = get_basis(c, lv, 32);
+    const RegionDev& r = region == 1 ? *bs.r1 : *bs.r2;
+    if (r.word != 32) return fail(c, HEMUL_E_ARG, "level has no 30-bit basis");
+    if (np > r.np) return fail(c, HEMUL_E_ARG, "more primes than the level's basis holds");
+    const int npu = np ? np : r.np;  // rows use the first npu primes
+    const size_t n = size_t(1) << c->log_n, words = rows * n;
+    uint32_t* d = data;
+    const bool dev = is_device(c, data);
+    if (!dev) {
+      ensure(c->r1, words * 4);
+      d = c->r1.as<uint32_t>();
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_H2D, "H2D",
+          [&] { return cudaMemcpyAsync(d, data, words * 4, cudaMemcpyDefault, c->stream); });
+    }
+    // row r uses prime r % npu; chunks are whole multiples of npu (gridDim.y)
+    const size_t step = std::max<size_t>(1, kMaxGridY / size_t(npu)) * size_t(npu);
+    const int total = ntt_num_passes(c->log_n);
+    for (size_t r0 = 0; r0 < rows; r0 += step) {
+      const size_t rc = std::min(step, rows - r0);
+      for (int pass = 0; pass < total; ++pass) {
+        const bool a = inverse ? pass + 1 == total : pass == 0;
+        run(c, inverse ? HEMUL_STAGE_INTT : HEMUL_STAGE_NTT,
+            inverse ? (a ? HEMUL_KCLASS_INTT_A : HEMUL_KCLASS_INTT_B)
+                    : (a ? HEMUL_KCLASS_NTT_A : HEMUL_KCLASS_NTT_B),
+            inverse ? "iNTT" : "NTT", [&] {
+              return inverse ? ntt_inverse_pass<F32>(pass, d + r0 * n, rc, npu, c->log_n,
+                                                     r.ITW<F32>(), r.P<F32>(), c->stream)
+                             : ntt_forward_pass<F32>(pass, d + r0 * n, rc, npu, c->log_n,
+                                                     r.TW<F32>(), r.P<F32>(), c->stream);
+            });
+      }
+    }
+    if (!dev)
+      run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_D2H, "D2H",
+          [&] { return cudaMemcpyAsync(data, d, words * 4, cudaMemcpyDefault, c->stream); });
+    check(cudaStreamSynchronize(c->stream), "ntt32");
+    return HEMUL_OK;
+  });
+}
+
+hemul_status hemul_gpu_level_twiddles32(hemul_gpu_ctx* c, int log_q, int region, int j,
+                                        uint32_t* tw, uint32_t* itw) {
+  if (!c || (region != 1 && region != 2) || j < 0) return HEMUL_E_ARG;
+  return guarded(c, [&]() -> hemul_status {
+    Level& lv = get_level(c, log_q);
+    const RegionDev& r = region == 1 ? *get_basis(c, lv, 32).r1 : *get_basis(c, lv, 32).r2;
+    if (r.word != 32 || j >= r.np) return fail(c, HEMUL_E_ARG, "no such 30-bit basis prime");
+    const size_t n = size_t(1) << c->log_n, off = size_t(j) * n;
+    if (tw)
+      check(cudaMemcpyAsync(tw, r.tw.as<Twiddle32>() + off, n * sizeof(Twiddle32),
+                            cudaMemcpyDefault, c->stream), "twiddles");
+    if (itw)
+      check(cudaMemcpyAsync(itw, r.itw.as<Twiddle32>() + off, n * sizeof(Twiddle32),
+                            cudaMemcpyDefault, c->stream), "twiddles");
+    check(cudaStreamSynchronize(c->stream), "twiddles");
     return HEMUL_OK;
   });
 }

@@ -35,6 +35,11 @@ cudaError_t ntt_inverse_pass(int pass, typename F::W* data, size_t rows, int np,
 // 30-bit basis pass A (strided levels [0, S), ntt_col.cu): one warp per
 // column, shuffles for the lane levels; used by ntt_forward_pass /
 // ntt_inverse_pass when supported (S = 6..9, >= 16 columns).
+// tables.cu: the 30-bit basis' twiddle tables (make_ntt_tables,
+// params.cpp:151-180) on the device; roots_inv = psi_j^-1
+cudaError_t build_twiddles32(const uint32_t* primes, const uint32_t* roots,
+                             const uint32_t* roots_inv, int np, int log_n, Twiddle32* tw,
+                             Twiddle32* itw, cudaStream_t st);
 bool ntt_col_supported(int log_n, int S);
 cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
                          const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st);

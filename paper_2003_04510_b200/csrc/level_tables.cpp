@@ -347,36 +347,36 @@ void build_tables(RegionHost& r, const Nat& P, const std::vector<int>& crt_bits,
       for (int it = 0; it < 5; ++it) pinv *= 2u - uint32_t(p) * pinv;
       d.pad[1] = pinv;                            // ntt_blk.cu: Montgomery products
     }
-    r.tw32.resize(size_t(count) * n);
-    r.itw32.resize(size_t(count) * n);
+    // the twiddle tables of the 30-bit basis are built on the device
+    // (tables.cu build_twiddles32, from primes and roots); only the
+    // per-prime constant w1n = itw[1] n^-1 is needed here
+    r.roots_inv.resize(count);
+    for (int j = 0; j < count; ++j) {
+      const uint64_t p = r.primes[j];
+      r.roots_inv[j] = powmod(r.roots[j], p - 2, p);
+      const uint64_t itw1 = n > 1 ? powmod(r.roots_inv[j], uint64_t(n) / 2, p) : 1;
+      const uint64_t w1n = n > 1 ? mulmod(itw1, ninv[j], p) : ninv[j];
+      r.dev32[j].w1n = uint32_t(w1n);
+      r.dev32[j].w1n_q = shoup_q32(w1n, p);
+    }
   }
 
   // twiddles: tw[j*n + i] = psi^rev(i), itw = psi^-rev(i) (params.cpp:151-180)
-  parallel_for(count, threads, [&](int j) {
+  if (word == 64) parallel_for(count, threads, [&](int j) {
     const uint64_t p = r.primes[j], psi = r.roots[j];
     const uint64_t psi_inv = powmod(psi, p - 2, p);
     uint64_t pw = 1, ipw = 1, itw1 = 1;
     for (int i = 0; i < n; ++i) {
       const uint32_t k = bit_reverse(uint32_t(i), log_n);
       if (k == 1) itw1 = ipw;
-      if (word == 64) {
-        r.tw[size_t(j) * n + k] = Twiddle{pw, shoup_q(pw, p)};
-        r.itw[size_t(j) * n + k] = Twiddle{ipw, shoup_q(ipw, p)};
-      } else {
-        r.tw32[size_t(j) * n + k] = Twiddle32{uint32_t(pw), shoup_q32(pw, p)};
-        r.itw32[size_t(j) * n + k] = Twiddle32{uint32_t(ipw), shoup_q32(ipw, p)};
-      }
+      r.tw[size_t(j) * n + k] = Twiddle{pw, shoup_q(pw, p)};
+      r.itw[size_t(j) * n + k] = Twiddle{ipw, shoup_q(ipw, p)};
       pw = mulmod(pw, psi, p);
       ipw = mulmod(ipw, psi_inv, p);
     }
     const uint64_t w1n = n > 1 ? mulmod(itw1, ninv[j], p) : ninv[j];
-    if (word == 64) {
-      r.dev[j].w1n = w1n;
-      r.dev[j].w1n_q = shoup_q(w1n, p);
-    } else {
-      r.dev32[j].w1n = uint32_t(w1n);
-      r.dev32[j].w1n_q = shoup_q32(w1n, p);
-    }
+    r.dev[j].w1n = w1n;
+    r.dev[j].w1n_q = shoup_q(w1n, p);
   });
 
   if (word == 32) {

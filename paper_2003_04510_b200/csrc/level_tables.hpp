@@ -56,7 +56,9 @@ struct RegionHost {
   // inverse passes that follow the warp-per-block middle pass, whose
   // evaluation-domain products are Montgomery-reduced (x y 2^-32, ntt_blk.cu)
   std::vector<DevPrime32> dev32_m, dev32_tm;
-  std::vector<Twiddle32> tw32, itw32;  // np * n each (word 32)
+  // word 32: no host twiddle tables; the device builds them from primes,
+  // roots and roots_inv = psi_j^-1 (tables.cu build_twiddles32)
+  std::vector<uint64_t> roots_inv;
   // CRT weights per input width (see kernels.hpp CrtWeights)
   struct Crt {
     int in_bits = 0, chunks = 0, ld = 0;

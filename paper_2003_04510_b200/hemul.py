@@ -72,6 +72,10 @@ _SIGS = {
                                          _u64p, _u64p, _u64p]),
     "hemul_gpu_enable_stage_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "hemul_gpu_stage_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]),
+    "hemul_gpu_level_twiddles32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "hemul_gpu_ntt32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]),
     "hemul_gpu_level_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_int), _u64p, ctypes.c_int]),
     "hemul_gpu_ntt": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u64p,
@@ -237,11 +241,12 @@ def limbs(bits: int) -> int:
     return (bits + 63) // 64
 
 
-def _ptr(a: Any) -> int:
-    """Raw address of a numpy array or torch tensor (contiguous, uint64)."""
+def _ptr(a: Any, dtype: Any = np.uint64) -> int:
+    """Raw address of a numpy array or torch tensor (contiguous, uint64 or
+    the given numpy dtype)."""
     if isinstance(a, np.ndarray):
-        if a.dtype != np.uint64 or not a.flags["C_CONTIGUOUS"]:
-            raise ValueError("expected a C-contiguous uint64 numpy array")
+        if a.dtype != dtype or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"expected a C-contiguous {np.dtype(dtype).name} numpy array")
         return a.ctypes.data
     if hasattr(a, "data_ptr"):
         if not a.is_contiguous():
@@ -279,6 +284,12 @@ class Context:
         # they never meet explicit caller ids
         self._evk_last: tuple[Any, Any, int] | None = None
         self._evk_seq = 1 << 62
+        # stream ordering with torch: until set_stream() names a stream, calls
+        # that receive torch CUDA tensors run on torch's current stream (so
+        # the producer of the inputs and the consumer of the outputs are
+        # ordered with the library's kernels without a host sync)
+        self._stream_explicit = False
+        self._cur_stream: int | None = None
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -298,6 +309,19 @@ class Context:
         self.close()
 
     # -- plumbing --------------------------------------------------------
+    def _follow_torch(self, *bufs: Any) -> None:
+        if self._stream_explicit:
+            return
+        for b in bufs:
+            if b is not None and getattr(b, "is_cuda", False):
+                import torch
+
+                s = torch.cuda.current_stream(b.device).cuda_stream
+                if s != self._cur_stream:
+                    self._check(self._lib.hemul_gpu_set_stream(self._h, s))
+                    self._cur_stream = s
+                return
+
     def _check(self, st: int) -> None:
         if st == HEMUL_OK:
             return
@@ -333,6 +357,7 @@ class Context:
     def warm_level(self, log_q: int, evk: tuple[Any, Any] | None = None,
                    evk_id: int | None = None) -> None:
         """Scheme::warm_level (heaan.hpp:100): tables, and evk forms if given."""
+        self._follow_torch(*(evk or ()))
         if evk is None:
             self._check(self._lib.hemul_gpu_set_level(self._h, log_q))
         else:
@@ -346,6 +371,7 @@ class Context:
         """Scheme::he_mul (heaan.cpp:339-410) on (ax, bx) pairs. Inputs have
         shape (n, limbs) or (batch, n, limbs); returns (ax, bx) at modulus
         log_q - log_p."""
+        self._follow_torch(c1[0], c2[0], *(evk or ()), *(out or ()))
         c2_log_q = log_q if c2_log_q is None else c2_log_q
         p = self.params
         if log_q != c2_log_q:
@@ -372,6 +398,7 @@ class Context:
 
     def rescale(self, c: tuple[Any, Any], log_q: int):
         """Scheme::rescale (heaan.cpp:328-337)."""
+        self._follow_torch(c[0])
         p = self.params
         L, Lo = limbs(log_q), limbs(log_q - p.log_p)
         batch = _size(c[0]) // (self.n * L)
@@ -387,6 +414,7 @@ class Context:
         device memory. asynchronous=True queues the copy on the copy stream
         (HEMUL_CT_ASYNC): the sources must stay alive and unchanged until the
         next download / synchronize."""
+        self._follow_torch(c[0])
         per = self.n * limbs(log_q)
         batch = _size(c[0]) // per
         if batch * per != _size(c[0]) or _size(c[1]) != _size(c[0]):
@@ -400,6 +428,7 @@ class Context:
                    evk: tuple[Any, Any] | None = None,
                    evk_id: int | None = None) -> DeviceCiphertext:
         """Scheme::he_mul on device-resident operands; the result stays on the device."""
+        self._follow_torch(*(evk or ()))
         h = ctypes.c_void_p()
         ea = _ptr(evk[0]) if evk is not None else None
         eb = _ptr(evk[1]) if evk is not None else None
@@ -455,6 +484,7 @@ class Context:
         """Test hook: he_mul stopped at a stage checkpoint (crt1, prod1, d2,
         crt2, prod2; include/hemul_gpu.h HEMUL_TRACE_*); returns that stage's
         buffer (uint32 residues in the 30-bit basis, uint64 otherwise)."""
+        self._follow_torch(c1[0], c2[0], *(evk or ()))
         info = self.engine_info(log_q)
         p = self.params
         per = self.n * limbs(log_q)
@@ -488,12 +518,31 @@ class Context:
                                                    buf.ctypes.data, np_.value))
         return buf
 
+    def level_twiddles32(self, log_q: int, region: int, j: int) -> tuple[np.ndarray, np.ndarray]:
+        """(tw, itw) of prime j of the level's 30-bit basis: (n, 2) u32 (w, wq)."""
+        tw = np.zeros((self.n, 2), np.uint32)
+        itw = np.zeros((self.n, 2), np.uint32)
+        self._check(self._lib.hemul_gpu_level_twiddles32(self._h, log_q, region, j,
+                                                         tw.ctypes.data, itw.ctypes.data))
+        return tw, itw
+
+    def ntt32(self, data: Any, log_q: int, region: int, inverse: bool = False,
+              nprimes: int = 0) -> None:
+        """The 30-bit basis NTT of the he_mul path, in place over u32 rows
+        (row r mod level_primes(log_q, -region)[r % nprimes]; 0 = all)."""
+        self._follow_torch(data)
+        rows = _size(data) // self.n
+        self._check(self._lib.hemul_gpu_ntt32(self._h, log_q, region, nprimes,
+                                              _ptr(data, np.uint32), rows, int(inverse)))
+
     def ntt(self, data: Any, log_q: int, region: int, inverse: bool = False) -> None:
         """In place over rows of n residues (row r uses prime r % np)."""
+        self._follow_torch(data)
         rows = _size(data) // self.n
         self._check(self._lib.hemul_gpu_ntt(self._h, log_q, region, _ptr(data), rows, int(inverse)))
 
     def crt(self, poly: Any, log_q: int, region: int, in_bits: int):
+        self._follow_torch(poly)
         batch = _size(poly) // (self.n * limbs(in_bits))
         np_ = len(self.level_primes(log_q, region))
         out = _like(poly, (batch, np_, self.n) if batch > 1 else (np_, self.n))
@@ -502,6 +551,7 @@ class Context:
         return out
 
     def pointwise(self, a: Any, b: Any, log_q: int, region: int):
+        self._follow_torch(a, b)
         np_ = len(self.level_primes(log_q, region))
         batch = _size(a) // (np_ * self.n)
         out = _like(a, tuple(a.shape))
@@ -510,6 +560,7 @@ class Context:
         return out
 
     def icrt(self, rns: Any, log_q: int, region: int):
+        self._follow_torch(rns)
         p = self.params
         np_ = len(self.level_primes(log_q, region))
         batch = _size(rns) // (np_ * self.n)
@@ -563,8 +614,12 @@ class Context:
         return word, len(p1), len(p2)
 
     def set_stream(self, stream: int | None) -> None:
-        """Launch on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        """Launch on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+        None: the context's own stream, and calls with torch CUDA tensors
+        follow torch's current stream again."""
         self._check(self._lib.hemul_gpu_set_stream(self._h, stream))
+        self._stream_explicit = stream is not None
+        self._cur_stream = stream
 
     def imad_peak(self) -> float:
         """Measured IMAD.WIDE.U32 ops/s of this device."""

@@ -134,6 +134,7 @@ class Reference:
         L.ref_pointwise.argtypes = [_i, _i, _i, _i, _p, _p, _p]
         L.ref_shift_right.argtypes = [_i, _i, _i, _p, _p]
         L.ref_time_he_mul.argtypes = [_i, _i, _i, _u64, _i, _i, _i, _p, _p]
+        L.ref_time_ntt.argtypes = [_i, _i, _i, _i, _i, _i, _p]
         L.ref_counters.argtypes = [_i, _i, _i, _u64, _i, _i, _p]
 
     def counters(self, log_p, depth, log_n_override, seed=7, four_products=False,
@@ -196,6 +197,15 @@ class Reference:
 
     def digest(self, log_q, n, ax, bx):
         return int(self.lib.ref_digest(log_q, n, _ptr(ax), _ptr(bx)))
+
+    def time_ntt(self, log_n, np_, threads=1, radix_log=4, reps=1, inverse=False):
+        """Wall ms of `reps` reference ntt_forward / ntt_inverse calls over np_
+        rows of 2^log_n (bench_ntt.cpp protocol)."""
+        ms = np.zeros(reps, np.float64)
+        st = self.lib.ref_time_ntt(log_n, np_, threads, radix_log, reps, int(inverse),
+                                   ms.ctypes.data)
+        assert st == 0, self.err()
+        return ms.tolist()
 
     def time_he_mul(self, log_p, depth, log_n_override=0, seed=1, reps=1, threads=1,
                     radix_log=1):

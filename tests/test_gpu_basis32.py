@@ -168,3 +168,67 @@ def test_every_level_of_the_logQ2400_ladder(restated):
             assert np.array_equal(oa, wa) and np.array_equal(ob, wb), (log_q, tc)
     for ctx in ctxs.values():
         ctx.close()
+
+
+@pytest.mark.parametrize("log_n", [12, 15, 16, 17])
+def test_ntt32_rows_vs_restated(log_n, restated):
+    """hemul_gpu_ntt32: the 30-bit column kernels (ntt_col.cu: warp form at
+    S = 7, half-warp form at S >= 8) + pass B, residue for residue against the
+    C restatement's ntt_forward / ntt_inverse (ntt.cpp:59-137, 153-197) with
+    the same primes and min-root rule; lazy GPU outputs compared mod p, and
+    the inverse of the GPU forward output returns the input exactly."""
+    import torch
+
+    ctx = _ctx((30, 10, log_n), True)
+    q = ctx.params.log_q_max
+    primes = ctx.level_primes(q, -2)
+    npr = min(5, len(primes))
+    ps = primes[:npr]
+    n = 1 << log_n
+    rng = np.random.default_rng(log_n)
+    x = (rng.integers(0, 2**62, size=(2 * npr, n), dtype=np.uint64)
+         % np.tile(ps, 2).astype(np.uint64)[:, None])
+    roots = [mm.root_2n(int(p), n) for p in ps]
+    P = np.tile(ps, 2).astype(np.uint64)[:, None]
+    dev = torch.from_numpy(x.astype(np.int32)).cuda()
+    ctx.ntt32(dev, q, 2, nprimes=npr)
+    fwd = dev.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert int(fwd.max()) < 4 * int(P.max())
+    want = restated.ntt(x, ps, roots, log_n)
+    assert np.array_equal(fwd % P, want % P)
+    ctx.ntt32(dev, q, 2, inverse=True, nprimes=npr)
+    back = dev.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(back, x)
+    want_inv = restated.ntt(x, ps, roots, log_n, inverse=True)
+    dev = torch.from_numpy(x.astype(np.int32)).cuda()
+    ctx.ntt32(dev, q, 2, inverse=True, nprimes=npr)
+    assert np.array_equal(dev.cpu().numpy().view(np.uint32).astype(np.uint64) % P, want_inv % P)
+    ctx.close()
+
+
+@pytest.mark.parametrize("log_n", [12, 17])
+def test_device_twiddles_match_rule(log_n):
+    """The 30-bit basis twiddle tables built on the device (tables.cu) equal
+    make_ntt_tables' rule (params.cpp:151-180): tw[rev(i)] = psi^i,
+    itw[rev(i)] = psi^-i, psi the smallest-c primitive 2n-th root, Shoup
+    quotient floor(w 2^32 / p) — for the first, a middle and the last prime
+    of both regions."""
+    ctx = _ctx((30, 80, log_n), True)
+    q = ctx.params.log_q_max
+    n = 1 << log_n
+    rev = np.array([int(format(i, f"0{log_n}b")[::-1], 2) for i in range(n)])
+    for region in (1, 2):
+        primes = ctx.level_primes(q, -region)
+        for j in sorted({0, len(primes) // 2, len(primes) - 1}):
+            p = int(primes[j])
+            psi = mm.root_2n(p, n)
+            for tab, base in zip(ctx.level_twiddles32(q, region, j), (psi, pow(psi, p - 2, p))):
+                w = np.ones(n, np.uint64)
+                for i in range(1, n):
+                    w[i] = w[i - 1] * base % p
+                want_w = np.zeros(n, np.uint64)
+                want_w[rev] = w
+                want_q = (want_w << np.uint64(32)) // np.uint64(p)
+                assert np.array_equal(tab[:, 0].astype(np.uint64), want_w), (region, j)
+                assert np.array_equal(tab[:, 1].astype(np.uint64), want_q), (region, j)
+    ctx.close()
