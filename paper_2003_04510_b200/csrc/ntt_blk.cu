@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
   using G = BlkGeo<S>;
   constexpr int EPT = G::EPT, BS = G::BS;
   constexpr int NIN = OP == kTensor2 ? 8 : 1, NOUT = OP == kTensor2 ? 6 : 2;
-  constexpr int NSLOT = NIN > NOUT ? NIN : NOUT;
+  constexpr int NSLOT = (S == 8 && OP == kEvk) ? 1 : (NIN > NOUT ? NIN : NOUT);
   extern __shared__ uint32_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* slots = smem + warp * NSLOT * BS;
@@ -405,6 +405,33 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
   auto rl = [](int r) { return k8 ? rl_of(r) : r; };
   std::conditional_t<k8, BlkTw8, BlkTw<S>> T;
   T.load(a.tw + size_t(j) * n, gbase, lane);
+  if constexpr (k8 && OP == kEvk) {
+    // key-switch product at S = 8 entirely in registers: forward levels of
+    // F (layout L' on exit), F evk_a and F evk_b at the lane's own positions
+    // y = 8 lane + rl(r), then the inverse levels of each product from L';
+    // one scratch slot per warp (the H <-> M exchange)
+    uint32_t v[EPT], pb[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) v[r] = a.in[0][off + 32 * r];
+    fwd8(v, T, slots, lane, p2, negp);
+    const size_t eb0 = size_t(j) * n + (size_t(block) << S) + EPT * lane;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      // f in [0, 4p); the evk forms are full forward transforms, canonical
+      // (kernels.hpp), so f evk < 4 p^2 < p 2^32
+      const uint32_t f = v[r];
+      v[r] = F32::mul_mont(f, __ldg(a.evk[0] + eb0 + rl(r)), pr);
+      pb[r] = F32::mul_mont(f, __ldg(a.evk[1] + eb0 + rl(r)), pr);
+    }
+    T.load(a.itw + size_t(j) * n, gbase, lane);
+    inv8(v, T, slots, lane, p2, negp);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) a.out[0][off + 32 * r] = v[r];
+    inv8(pb, T, slots, lane, p2, negp);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) a.out[1][off + 32 * r] = pb[r];
+    return;
+  }
   // ---- forward levels of every operand; results parked in layout L. The
   // next operand's rows are loaded while this one is transformed. ----------
   uint32_t nx[EPT];
@@ -464,7 +491,7 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
 
 template <int S, int OP>
 cudaError_t launch_blk(const BlkArgs& a, size_t rows, cudaStream_t st) {
-  constexpr int NSLOT = OP == kTensor2 ? 8 : 2;
+  constexpr int NSLOT = OP == kTensor2 ? 8 : (S == 8 ? 1 : 2);
   const size_t smem = size_t(kWarps) * NSLOT * BlkGeo<S>::BS * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(ntt_blk_kernel<S, OP>,

@@ -263,6 +263,9 @@ def _like(a: Any, shape: tuple[int, ...]):
     return torch.empty(shape, dtype=torch.uint64, device=a.device)
 
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (driver_types.h)
+
+
 def _size(a: Any) -> int:
     return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
 
@@ -316,7 +319,9 @@ class Context:
             if b is not None and getattr(b, "is_cuda", False):
                 import torch
 
-                s = torch.cuda.current_stream(b.device).cuda_stream
+                # torch's default stream reports handle 0, which the C side
+                # reads as "the context's own stream": pass cudaStreamLegacy
+                s = torch.cuda.current_stream(b.device).cuda_stream or _CUDA_STREAM_LEGACY
                 if s != self._cur_stream:
                     self._check(self._lib.hemul_gpu_set_stream(self._h, s))
                     self._cur_stream = s

@@ -417,3 +417,35 @@ def test_device_handles_small_chain(restated):
     ba, bb = rb.download()
     ha, hb = ctx.he_mul(tuple(cb1), tuple(cb2), q, evk=evk)
     assert np.array_equal(ba, ha) and np.array_equal(bb, hb)
+
+
+def test_torch_tensors_follow_torch_stream(restated):
+    """A Context without an explicit stream runs calls on torch CUDA tensors
+    on torch's current stream (the default stream maps to cudaStreamLegacy):
+    inputs produced by torch kernels just before the call and outputs read by
+    torch right after are ordered without a host sync."""
+    import torch
+
+    cfg = (30, 4, 13)
+    ctx = _ctx(cfg)
+    p = ctx.params
+    q = p.log_q_max
+    for seed in range(3):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(seed)
+
+        def rnd(bits):
+            t = torch.randint(-(2**63), 2**63 - 1, (p.n, (bits + 63) // 64), generator=g,
+                              device="cuda", dtype=torch.int64)
+            if bits % 64:
+                t[:, -1] &= (1 << (bits % 64)) - 1
+            return t.view(torch.uint64)
+
+        c1, c2, evk = (rnd(q), rnd(q)), (rnd(q), rnd(q)), (rnd(2 * q), rnd(2 * q))
+        oa, ob = ctx.he_mul(c1, c2, q, evk=evk, evk_id=0)  # no synchronize in between
+        ga, gb = oa.cpu().numpy(), ob.cpu().numpy()
+        h = lambda t: t.cpu().numpy()  # noqa: E731
+        st, wa, wb = restated.he_mul(p.log_n, p.log_p, q, q, (h(c1[0]), h(c1[1])),
+                                     (h(c2[0]), h(c2[1])), (h(evk[0]), h(evk[1])))
+        assert st == 0 and np.array_equal(ga, wa) and np.array_equal(gb, wb), seed
+    ctx.close()
