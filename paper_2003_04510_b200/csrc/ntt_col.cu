@@ -1,5 +1,6 @@
 // Strided NTT pass A (levels [0, S) on 2^S-point columns) for the 30-bit
-// basis, one warp per column (sm_100a).
+// basis (sm_100a): a half-warp per column at S >= 8 (the he_mul path at
+// log N >= 15), a warp per column at S = 7.
 //
 // Reference: ntt_forward / ntt_inverse (proj/core/src/ntt.cpp:59-137,
 // 153-197); pass structure as in ntt.cu (pass A = the first forward levels /
@@ -9,23 +10,26 @@
 //
 // Layout. A CTA loads 16 adjacent columns (16 consecutive residues of every
 // one of the 2^S rows: coalesced 64-byte segments) into shared memory, column
-// x at x * CS + f(y), f(y) = y + y / 32, CS = 2 (mod 32): the cooperative
-// load / store, and both register layouts below, are bank-conflict free. Each
-// warp then transforms its column alone (only __syncwarp), with EPT = 2^S / 32
-// residues per lane:
-//   layout H: lane l holds y = l + 32 r (r < EPT): the top R = log2(EPT) bits
-//             of y live in registers -> levels 0 .. R-1 in registers, their
-//             twiddles uniform across the warp (broadcast reads);
-//   layout L: lane l holds y = EPT l + r: the low R bits in registers ->
-//             levels S-R .. S-1 in registers;
-//   levels R .. S-R-1 pair lanes: one __shfl_xor per residue and level.
-// The forward pass runs H, shuffles, L; the inverse the mirror image.
-// Compared with the radix-8 CTA-wide kernel this drops the 3 CTA barriers
-// and most index arithmetic: every shared address is a per-thread base plus
-// a compile-time offset. 256-thread CTAs (each warp takes two of the 16
-// columns in turn), 5 per SM: the pass is bound by how much HBM traffic is in
-// flight, and more independent CTAs keep more of it going (2 x 512 threads:
-// 2.84 / 3.17 ms per step forward / inverse at X, 5 x 256: 2.30 / 2.49).
+// x at x * CS + f(y) (f pads one word per 32 or 2^(S-4) rows, CS = 2 mod 32):
+// the cooperative load / store and the register layouts below are
+// bank-conflict free (checked exhaustively).
+// S >= 8 (column_transform_half): the two halves of a warp take columns c and
+// c + 8, 2^S / 16 residues per lane, two register layouts and one shared
+// exchange cover all S levels (layout H: y = h + 16 r, layout L: y = HE h + r).
+// S = 7 (column_transform): a warp per column, layouts H / L plus one
+// shuffle level between them. No CTA barrier inside the transform.
+//
+// Measured at X (ms per step forward / inverse; tools/run_variants.sh with
+// the HEMUL_COL_* macros below): the half-warp form 2.02 / 2.33 (the warp
+// form with its shuffle level 2.14 / 2.38). Its HBM phase alone
+// (HEMUL_COL_EXP=1) takes 1.48 / 1.62, the transform alone (EXP=2) 1.50 /
+// 1.67: the one-tile CTAs overlap the two only in part. Not adopted, all
+// slower: 32-column tiles (128-byte row segments; HBM phase alone 1.28 /
+// 1.39 = 0.91 of HBM, full pass 2.09 / 2.42 at 2 CTAs per SM); a persistent
+// cp.async double-buffered CTA (3.0 / 3.4: 2 CTAs per SM, 41 % issue); a
+// warp-specialised persistent CTA (16 transform + 8 copy warps, named
+// barriers, 2 or 3 buffers: 2.49 / 2.74) — the transform needs ~32 resident
+// warps per SM, which at 64 registers is the whole register file.
 #include <cuda_runtime.h>
 
 #include "fields.cuh"
@@ -35,9 +39,13 @@ namespace hemul_gpu {
 
 namespace {
 
-constexpr int kCols = 16;     // columns per CTA (64-byte row segments)
-constexpr int kWarps = 8;     // each warp transforms kCols / kWarps columns in turn
+#ifndef HEMUL_COL_COLS
+#define HEMUL_COL_COLS 16
+#endif
+constexpr int kCols = HEMUL_COL_COLS;  // columns per CTA (4 kCols-byte row segments)
+constexpr int kWarps = kCols / 2;      // half-warp form: one column per half-warp
 constexpr int kThreads = 32 * kWarps;
+constexpr int kTpr = kCols / 4;        // threads per row segment (16-byte vectors)
 
 template <int S>
 struct ColGeo {
@@ -52,8 +60,11 @@ struct ColGeo {
   static constexpr int RH = S - 4;
   // padded position of row y: one pad word per 2^PS rows
   static constexpr int PS = kHalf ? S - 4 : 5;
-  // column stride: > f(2^S - 1) and = 2 (mod 32)
-  static constexpr int CS = ((1 << S) + (1 << (S - PS)) + 29) / 32 * 32 + 2;
+  // column stride: > f(2^S - 1) and = 2 (mod 32) for 16-column tiles, 1 (mod
+  // 32) for 32-column tiles (the cooperative copies then cover 8 columns x 4
+  // rows per warp; the half-warp columns c, c + 16 sit 16 banks apart)
+  static constexpr int CM = (kHalf && kCols == 32) ? 1 : 2;
+  static constexpr int CS = ((1 << S) + (1 << (S - PS)) + 32 - CM - 1) / 32 * 32 + CM;
 };
 
 template <int S>
@@ -397,7 +408,7 @@ __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32
 #define HEMUL_COL_MINB_FWD 3
 #endif
 #ifndef HEMUL_COL_MINB_HALF
-#define HEMUL_COL_MINB_HALF 4
+#define HEMUL_COL_MINB_HALF (64 / kCols)
 #endif
 template <int S, bool INV>
 struct ColCfg {
@@ -428,13 +439,16 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
   // ---- cooperative load: 16-byte vectors, thread -> (columns 4 (tid % 4)
   // .. +3, rows tid / 4 + 128 r) ------------------------------------------------
   {
-    constexpr int RS = kThreads / 4;  // rows per sweep
-    const int x4 = 4 * (tid & 3), y0 = tid >> 2;
+    constexpr int RS = kThreads / kTpr;  // rows per sweep
+    const int x4 = 4 * (tid % kTpr), y0 = tid / kTpr;
     const uint4* src = reinterpret_cast<const uint4*>(rowp + size_t(y0) * tlast + x4);
     const size_t step = size_t(RS) * tlast / 4;
+#ifndef HEMUL_COL_EXP
+#define HEMUL_COL_EXP 0  // experiments: 1 = no transform, 2 = no HBM traffic
+#endif
 #pragma unroll
     for (int r = 0; r < (1 << S) / RS; ++r) {
-      const uint4 q = src[r * step];
+      const uint4 q = HEMUL_COL_EXP == 2 ? make_uint4(tid, r, 1, 2) : src[r * step];
       const int fy = padc<S>(y0 + RS * r);
       col[x4 * CS + fy] = q.x;
       col[(x4 + 1) * CS + fy] = q.y;
@@ -456,7 +470,8 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
     }
   }
   __syncthreads();
-  if constexpr (ColGeo<S>::kHalf) {
+  if constexpr (HEMUL_COL_EXP == 1) {
+  } else if constexpr (ColGeo<S>::kHalf) {
     static_assert(kCols == 2 * kWarps, "one column per half-warp");
     column_transform_half<S, INV>(col + (warp + kWarps * (lane >> 4)) * CS, stw, pr, lane & 15);
   } else {
@@ -467,9 +482,9 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
   }
   __syncthreads();
   // ---- cooperative store ------------------------------------------------
-  {
-    constexpr int RS = kThreads / 4;
-    const int x4 = 4 * (tid & 3), y0 = tid >> 2;
+  if (HEMUL_COL_EXP != 2 || a.np < 0) {
+    constexpr int RS = kThreads / kTpr;
+    const int x4 = 4 * (tid % kTpr), y0 = tid / kTpr;
     uint4* dst = reinterpret_cast<uint4*>(rowp + size_t(y0) * tlast + x4);
     const size_t step = size_t(RS) * tlast / 4;
 #pragma unroll
@@ -484,6 +499,15 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
 template <int S, bool INV>
 cudaError_t launch_col(const ColArgs& a, size_t rows, cudaStream_t st) {
   const size_t smem = (size_t(kCols) * ColGeo<S>::CS + (size_t(2) << S)) * 4;
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      const cudaError_t e = cudaFuncSetAttribute(
+          ntt_col_kernel<S, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+  }
   const int cols = 1 << (a.log_n - S);
   dim3 grid(static_cast<unsigned>(cols / kCols), static_cast<unsigned>(rows));
   ntt_col_kernel<S, INV><<<grid, kThreads, smem, st>>>(a);
@@ -496,7 +520,7 @@ cudaError_t launch_col(const ColArgs& a, size_t rows, cudaStream_t st) {
 // [0, S) (not the last pass) or inverse levels [S-1, 0] with n^-1 (the last
 // pass); S = the pass-A level count of ntt.cu (7..9), n / 2^S >= 16 columns.
 bool ntt_col_supported(int log_n, int S) {
-  return S >= 7 && S <= 9 && log_n - S >= 4;
+  return S >= 7 && S <= 9 && (1 << (log_n - S)) >= kCols;
 }
 
 cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
