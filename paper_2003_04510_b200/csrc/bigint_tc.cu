@@ -222,11 +222,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ---- MMA issue (A: TMEM stage q mod 2, B: shared memory) --------------
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_u8(kRows, NH, 0, 0);
+    // The whole warp walks the chunk sequence (its barrier waits are warp-
+    // uniform) and one elected lane issues; the B descriptors are the stage-0
+    // descriptor plus a 16-byte-unit offset (shared addresses < 256 KB keep
+    // the 14-bit start field from carrying), so a chunk costs a handful of
+    // uniform adds instead of four descriptor builds. (With a lane-0 branch
+    // and per-MMA descriptors the MMA warp spent ~110 instructions per chunk,
+    // as long as the four MMAs themselves take.)
+    const uint32_t idesc = tc::idesc_u8(kRows, NH, 0, 0);
+    const uint64_t bdesc0 = tc::smem_desc(tc::smem_addr(sB), 16, 512, tc::kSw64);
+    const uint32_t b_step = b_bytes >> 4, hi_off = uint32_t(NH * kChunk) >> 4;
+    const bool leader = tc::elect_one();
+    {
       int uses[3] = {0, 0, 0};
       uint32_t dlo = 0, dhi = 0;
-      for (int q = 0, c = 0, it = 0, sb = 0, phb = 0; q < total; ++q) {
+      for (int q = 0, c = 0, it = 0, sb = 0; q < total; ++q) {
         if (c == 0) {  // a new tile: its two TMEM blocks must be drained
           const int bl = slot_lo(it), bh = slot_hi(it);
 #pragma unroll
@@ -239,23 +249,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sa = q & 1;
         tc::mbar_wait(&a_full[sa], (q >> 1) & 1);  // the producers saw b_full too
         tc::fence_after();
-        const uint32_t b0 = tc::smem_addr(sB + sb * b_bytes);
+        const uint64_t bd = bdesc0 + uint64_t(uint32_t(sb) * b_step);
         const uint32_t a0 = tmem + kACol + sa * kSlots;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
-          tc::mma_u8_ts(dlo, a0 + ks * 8, tc::smem_desc(b0 + ks * 32, 16, 512, tc::kSw64), idesc, acc);
-          tc::mma_u8_ts(dhi, a0 + ks * 8, tc::smem_desc(b0 + NH * kChunk + ks * 32, 16, 512, tc::kSw64),
-                        idesc, acc);
+        if (leader) {
+          const uint32_t acc0 = c > 0 ? 1u : 0u;
+          tc::mma_u8_ts(dlo, a0, bd, idesc, acc0);
+          tc::mma_u8_ts(dhi, a0, bd + hi_off, idesc, acc0);
+          tc::mma_u8_ts(dlo, a0 + 8, bd + 2, idesc, 1u);
+          tc::mma_u8_ts(dhi, a0 + 8, bd + hi_off + 2, idesc, 1u);
+          tc::mma_commit(&b_empty[sb]);
+          tc::mma_commit(&a_empty[sa]);
         }
-        tc::mma_commit(&b_empty[sb]);
-        tc::mma_commit(&a_empty[sa]);
-        if (++sb == nsb) sb = 0, phb ^= 1;
+        if (++sb == nsb) sb = 0;
         if (++c == C) {
-          tc::mma_commit(&t_full[it & 1]);
+          if (leader) tc::mma_commit(&t_full[it & 1]);
           c = 0;
           ++it;
         }
+        __syncwarp();
       }
     }
   } else if (warp >= kProd0) {
