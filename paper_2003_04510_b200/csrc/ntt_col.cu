@@ -47,6 +47,8 @@ constexpr int kWarps = kCols / 2;      // half-warp form: one column per half-wa
 constexpr int kThreads = 32 * kWarps;
 constexpr int kTpr = kCols / 4;        // threads per row segment (16-byte vectors)
 
+// (every form reads only its own members: silence nvcc's unused-member note)
+#pragma nv_diag_suppress 177
 template <int S>
 struct ColGeo {
   static constexpr int EPT = (1 << S) / 32;
@@ -66,6 +68,7 @@ struct ColGeo {
   static constexpr int CM = (kHalf && kCols == 32) ? 1 : 2;
   static constexpr int CS = ((1 << S) + (1 << (S - PS)) + 32 - CM - 1) / 32 * 32 + CM;
 };
+#pragma nv_diag_default 177
 
 template <int S>
 __device__ __forceinline__ int padc(int y) { return y + (y >> ColGeo<S>::PS); }
@@ -410,12 +413,14 @@ __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32
 #ifndef HEMUL_COL_MINB_HALF
 #define HEMUL_COL_MINB_HALF (64 / kCols)
 #endif
+#pragma nv_diag_suppress 177
 template <int S, bool INV>
 struct ColCfg {
   static constexpr int NC = INV ? HEMUL_COL_NC_INV : 2;
   static constexpr int kMinBlocks =
       ColGeo<S>::kHalf ? HEMUL_COL_MINB_HALF : (INV ? HEMUL_COL_MINB_INV : HEMUL_COL_MINB_FWD);
 };
+#pragma nv_diag_default 177
 
 template <int S, bool INV>
 __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_kernel(ColArgs a) {
