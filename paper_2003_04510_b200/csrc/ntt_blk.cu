@@ -50,6 +50,7 @@ struct BlkArgs {
   int np, log_n, s1, rows_per_prime;
 };
 
+#pragma nv_diag_suppress 177
 template <int S>
 struct BlkGeo {
   static constexpr int EPT = (1 << S) / 32;
@@ -59,6 +60,7 @@ struct BlkGeo {
   // padded slot (words); S = 8 also holds the f1pad exchange (< 284)
   static constexpr int BS = S == 8 ? 288 : (1 << S) + (1 << (S - 5));
 };
+#pragma nv_diag_default 177
 
 __device__ __forceinline__ Twiddle32 ldtw(const Twiddle32* p) {
   const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
@@ -430,8 +432,7 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
     inv8(pb, T, slots, lane, p2, negp);
 #pragma unroll
     for (int r = 0; r < EPT; ++r) a.out[1][off + 32 * r] = pb[r];
-    return;
-  }
+  } else {
   // ---- forward levels of every operand; results parked in layout L. The
   // next operand's rows are loaded while this one is transformed. ----------
   uint32_t nx[EPT];
@@ -487,6 +488,7 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
 #pragma unroll
     for (int r = 0; r < EPT; ++r) a.out[o][off + 32 * r] = v[r];
   }
+  }  // generic path
 }
 
 template <int S, int OP>
