@@ -443,6 +443,8 @@ def main() -> None:
     ctx.set_stream(stream.cuda_stream)
     ctx.set_basis(args.basis)
     ctx.set_tensor_cores(args.engine == "tc")
+    if os.environ.get("HEMUL_BENCH_TRANSPOSED"):
+        ctx.set_transposed(os.environ["HEMUL_BENCH_TRANSPOSED"] == "1")
     q = p.log_q_max
     L, Lo, Le = limbs(q), limbs(q - p.log_p), limbs(2 * q)
     n = p.n

@@ -119,6 +119,10 @@ enum { HEMUL_INFO_WORD = 0,     /* 32 (30-bit basis) or 64 (reference primes) */
        HEMUL_INFO_BIG_TC,       /* iCRT + finisher on the tensor cores (t_j form) */
        HEMUL_INFO_FUSED_MID,    /* fused middle NTT pass with the products */
        HEMUL_INFO_BLK_MONT,     /* Montgomery-reduced warp-per-block middle pass */
+       HEMUL_INFO_T_PASS_A,     /* > 0: CRT outputs and t rows are column-major with
+                                   this pass-A level count S (HEMUL_OPT_TRANSPOSED):
+                                   position x 2^S + y holds coefficient y n / 2^S + x
+                                   (he_mul_trace checkpoints crt1, prod1, crt2, prod2) */
        HEMUL_INFO_COUNT };
 hemul_status hemul_gpu_engine_info(hemul_gpu_ctx *ctx, int log_q, int info[HEMUL_INFO_COUNT]);
 
@@ -225,7 +229,12 @@ hemul_status hemul_gpu_rescale(hemul_gpu_ctx *ctx, int log_q, size_t batch, cons
  * cores; 0 selects the IMAD.WIDE integer-pipe kernels. Results are
  * bit-identical either way. */
 enum { HEMUL_OPT_FORCE_EXACT = 1, HEMUL_OPT_BASIS = 2, HEMUL_OPT_TENSOR_CORES = 3,
-       HEMUL_OPT_LEVEL_CACHE = 4 };
+       HEMUL_OPT_LEVEL_CACHE = 4, HEMUL_OPT_TRANSPOSED = 5 };
+/* HEMUL_OPT_TRANSPOSED: in the tensor-core engine at log N >= 15 the RNS rows
+ * around NTT pass A use the column-major layout (CRT writes it, the forward
+ * column pass reads it without a staging barrier, the inverse column pass
+ * writes it without a store phase, the iCRT / finisher read it). Results are
+ * identical either way. Default 1. */
 /* HEMUL_OPT_LEVEL_CACHE: capacity of the level LRU (default 2, the
  * reference's Scheme::level, heaan.cpp:119-150). A device-resident chain
  * walks one level per HE Mul; with a larger cache (about 1 GB per level at

@@ -372,7 +372,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = 0; it < my_tiles; ++it) {
       const int tile = blockIdx.x + it * gridDim.x;
       const int e = tile / tiles_per_entry;
-      const size_t i = size_t(tile - e * tiles_per_entry) * kRows + 32 * warp + lane;
+      // position of this lane's residues in the t rows -> its coefficient
+      const size_t ipos = size_t(tile - e * tiles_per_entry) * kRows + 32 * warp + lane;
+      const size_t i = o.tS ? ((ipos & ((size_t(1) << o.tS) - 1)) << (P.log_n - o.tS)) |
+                                  (ipos >> o.tS)
+                            : ipos;
       const int eb = e % P.B;
       uint64_t* dst = (e < P.B ? o.out0 : o.out1) + (size_t(eb) * n + i) * L;
       tc::mbar_wait_sleep<128>(&t_full[it & 1], (it >> 1) & 1);

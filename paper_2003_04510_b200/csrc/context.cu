@@ -185,12 +185,14 @@ struct hemul_gpu_ctx {
   std::vector<cudaEvent_t> event_pool;
   // scratch
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
+  DevBuf r1b, r2b;  // out-of-place NTT pass-A buffers of the transposed layout
   DevBuf tern_a, tern_b, tern_nz;  // mul_by_ternary scratch
   void* pinned[2] = {nullptr, nullptr};  // file streaming (hemul_gpu_ct_load / _save)
   cudaEvent_t ev_pin[2] = {nullptr, nullptr};
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
   int basis = 32;       // HEMUL_OPT_BASIS: he_mul prime basis (32 or 64)
   int tensor_cores = 1;  // HEMUL_OPT_TENSOR_CORES: int8 tcgen05 base conversions
+  int transposed = 1;    // HEMUL_OPT_TRANSPOSED: column-major RNS rows around pass A
   int level_cache = 2;   // HEMUL_OPT_LEVEL_CACHE: LRU capacity (heaan.cpp:119-150: 2)
 
   cudaEvent_t take_event() {
@@ -786,6 +788,9 @@ hemul_status hemul_gpu_set_option(hemul_gpu_ctx* c, int option, int value) {
     case HEMUL_OPT_TENSOR_CORES:
       c->tensor_cores = value != 0;
       return HEMUL_OK;
+    case HEMUL_OPT_TRANSPOSED:
+      c->transposed = value != 0;
+      return HEMUL_OK;
     case HEMUL_OPT_LEVEL_CACHE:
       if (value < 1 || value > 1024) return fail(c, HEMUL_E_ARG, "level cache capacity out of range");
       c->level_cache = value;
@@ -923,6 +928,13 @@ hemul_status hemul_gpu_engine_info(hemul_gpu_ctx* c, int log_q, int info[HEMUL_I
     info[HEMUL_INFO_BIG_TC] = tc && bs.icrt_tc && bs.fin_tc;
     info[HEMUL_INFO_FUSED_MID] = mid;
     info[HEMUL_INFO_BLK_MONT] = word == 32 && mid && ntt_blk_supported(c->log_n);
+    const int tS = ntt_pass_a_levels(c->log_n);
+    info[HEMUL_INFO_T_PASS_A] =
+        (tc && c->transposed && info[HEMUL_INFO_BIG_TC] && info[HEMUL_INFO_BLK_MONT] &&
+         info[HEMUL_INFO_CRT1_TC] && info[HEMUL_INFO_CRT2_TC] &&
+         ntt_col_transposed_supported(c->log_n, tS))
+            ? tS
+            : 0;
     return HEMUL_OK;
   });
 }
@@ -1390,6 +1402,22 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   ensure(c->r1, kInSlots * r1w * sizeof(W));
   W* R1 = c->r1.as<W>();
   const CrtWeights* w1 = r1.weights(kSplit ? h : log_q);
+  // int8 tensor-core iCRT + finisher (30-bit split basis): the inverse NTTs
+  // feeding them output t_j directly
+  bool tc_big = false;
+  if constexpr (kSplit) tc_big = c->tensor_cores && bs.icrt_tc && bs.fin_tc;
+  const bool mid = ntt_has_mid(log_n);
+  // the warp-per-block middle pass (30-bit basis) Montgomery-reduces its
+  // products (ntt_blk.cu); the following inverse pass compensates
+  const bool blk_mont = kSplit && mid && ntt_blk_supported(log_n);
+  // transposed pass-A layout (ntt_col.cu TR forms): both tensor-core CRTs
+  // write column-major rows, forward pass A reads them and writes natural
+  // rows into a second buffer, the middle pass runs there, inverse pass A
+  // writes column-major t rows back for the tensor-core iCRT / finisher
+  const int tS = ntt_pass_a_levels(log_n);
+  const bool trn = kSplit && c->transposed && c->tensor_cores && tc_big && blk_mont &&
+                   ntt_col_transposed_supported(log_n, tS) && r1.tc_table(0, h) &&
+                   r1.tc_table(h, log_q - h) && r2.tc_table(0, log_q);
   if constexpr (kSplit) {
     const uint64_t* polys[8];
     int bit0[8], bits[8];
@@ -1404,7 +1432,8 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       CrtTcTable tabs[8];
       for (int t = 0; t < 8; ++t) tabs[t] = (t & 1) ? *thi : *tlo;
       run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1 (tensor cores)", [&] {
-        return crt_forward_tc(polys, tabs, 8, L, B, log_n, p1, r1.np, R1, c->stream);
+        return crt_forward_tc(polys, tabs, 8, L, B, log_n, p1, r1.np, R1, c->stream,
+                              trn ? tS : 0);
       });
     } else {
       run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r1", [&] {
@@ -1419,15 +1448,25 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
     });
   }
   if (trace_at(c, tr, HEMUL_TRACE_CRT1, R1, kInSlots * r1w * sizeof(W))) return;
-  // int8 tensor-core iCRT + finisher (30-bit split basis): the inverse NTTs
-  // feeding them output t_j directly
-  bool tc_big = false;
-  if constexpr (kSplit) tc_big = c->tensor_cores && bs.icrt_tc && bs.fin_tc;
-  const bool mid = ntt_has_mid(log_n);
-  // the warp-per-block middle pass (30-bit basis) Montgomery-reduces its
-  // products (ntt_blk.cu); the following inverse pass compensates
-  const bool blk_mont = kSplit && mid && ntt_blk_supported(log_n);
-  if (mid) {
+  if (trn) {
+    if constexpr (kSplit) {
+      const int S = tS;
+      ensure(c->r1b, kInSlots * r1w * sizeof(W));
+      W* R1b = c->r1b.as<W>();
+      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_NTT_A, "NTT pass A (transposed in)", [&] {
+        return ntt_col_pass_transposed(false, R1, R1b, kInSlots * B * r1.np, r1.np, log_n, S,
+                                       r1.TW<F>(), p1, c->stream);
+      });
+      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R1, "NTT mid r1", [&] {
+        return ntt_mid_tensor_split(R1b, B, r1.np, log_n, r1.TW<F>(), r1.ITW<F>(), p1, c->stream);
+      });
+      run(c, HEMUL_STAGE_INTT, HEMUL_KCLASS_INTT_A, "iNTT pass A (transposed out)", [&] {
+        return ntt_col_pass_transposed(true, R1b, R1, kOutSlots * B * r1.np, r1.np, log_n, S,
+                                       r1.ITW<F>(), r1.primes_tm.as<const DevPrime32>(),
+                                       c->stream);
+      });
+    }
+  } else if (mid) {
     // forward pass A, then one fused pass: forward pass B + tensor product +
     // inverse pass B, then inverse pass A
     ntt_fwd<F>(c, r1, R1, kInSlots * B * r1.np, HEMUL_STAGE_NTT, 1);
@@ -1475,6 +1514,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       o.out_limbs = L;
       o.out_bit = T.out_bit;
       o.out_bits = T.out_bits;
+      o.tS = trn ? tS : 0;
       run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_ICRT, "iCRT r1 (tensor cores)", [&] {
         return bigint_tc(T.t, segs, static_cast<int>(B), static_cast<int>(B), log_n, o, rmaps,
                          c->stream);
@@ -1501,7 +1541,8 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
     if (const CrtTcTable* t2 = c->tensor_cores ? r2.tc_table(0, log_q) : nullptr) {
       const uint64_t* d2c = d2;
       run(c, HEMUL_STAGE_CRT, HEMUL_KCLASS_CRT, "CRT r2 (tensor cores)", [&] {
-        return crt_forward_tc(&d2c, t2, 1, L, B, log_n, p2, r2.np, KA, c->stream);
+        return crt_forward_tc(&d2c, t2, 1, L, B, log_n, p2, r2.np, KA, c->stream,
+                              trn ? tS : 0);
       });
       r2_done = true;
     }
@@ -1514,7 +1555,26 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
   if (trace_at(c, tr, HEMUL_TRACE_CRT2, KA, r2w * sizeof(W))) return;
   const W* EA = lv.evk_a.as<W>();
   const W* EB = EA + size_t(r2.np) * n;
-  if (mid) {
+  if (trn) {
+    if constexpr (kSplit) {
+      const int S = tS;
+      ensure(c->r2b, 2 * r2w * sizeof(W));
+      W* Y0 = c->r2b.as<W>();
+      W* Y1 = Y0 + r2w;
+      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_NTT_A, "NTT pass A r2 (transposed in)", [&] {
+        return ntt_col_pass_transposed(false, KA, Y0, B * r2.np, r2.np, log_n, S, r2.TW<F>(),
+                                       p2, c->stream);
+      });
+      run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R2, "NTT mid r2", [&] {
+        return ntt_mid_evk<F>(Y0, EA, EB, Y0, Y1, B, r2.np, log_n, r2.TW<F>(), r2.ITW<F>(), p2,
+                              c->stream);
+      });
+      run(c, HEMUL_STAGE_INTT, HEMUL_KCLASS_INTT_A, "iNTT pass A r2 (transposed out)", [&] {
+        return ntt_col_pass_transposed(true, Y0, KA, 2 * B * r2.np, r2.np, log_n, S, r2.ITW<F>(),
+                                       r2.primes_tm.as<const DevPrime32>(), c->stream);
+      });
+    }
+  } else if (mid) {
     ntt_fwd<F>(c, r2, KA, B * r2.np, HEMUL_STAGE_NTT, 1);
     run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R2, "NTT mid r2", [&] {
       return ntt_mid_evk<F>(KA, EA, EB, KA, KB, B, r2.np, log_n, r2.TW<F>(), r2.ITW<F>(), p2,
@@ -1569,12 +1629,14 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       o.check_amb = 1;
       o.force_exact = c->force_exact;
       o.flags = flags;
+      o.tS = trn ? tS : 0;
       run(c, HEMUL_STAGE_ICRT, HEMUL_KCLASS_FINISH, "finisher (tensor cores)", [&] {
         cudaError_t e = bigint_tc(T.t, segs, static_cast<int>(2 * B), static_cast<int>(B), log_n, o,
                                   rmaps, c->stream);
         if (e != cudaSuccess) return e;
         Finisher ft = fin;
         ft.t_inputs = 1;
+        ft.tS = trn ? tS : 0;
         return finish_fixup<F32>(KA, D1, D0, B, log_n, p2, r2.np, p1, r1.np, ft, r2.icrt,
                                  r1.icrt, out_ax, out_bx, flags, c->stream);
       });

@@ -82,6 +82,8 @@ __device__ __forceinline__ uint32_t planes_mont(uint32_t d0, uint32_t d1, uint32
   return static_cast<uint32_t>((z + static_cast<uint64_t>(m) * p) >> 32);
 }
 
+#define LOGN_OR(x) (LOGN > 0 ? LOGN : (x))
+
 // -p^-1 mod 2^32 (p odd): Newton, 5 steps from inv = p (correct to 3 bits)
 __device__ __forceinline__ uint32_t neg_inv32(uint32_t p) {
   uint32_t inv = p;
@@ -97,7 +99,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 1)
     crt_tc_kernel(TcInputs in, int count, int B, int limbs, int log_n, CrtTcTable tab,
                   const DevPrime32* __restrict__ primes, int np, uint32_t* __restrict__ out,
-                  int stages, int nslots) {
+                  int stages, int nslots, int tS) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t a_full[kMaxStages], a_empty[kMaxStages], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_base;
@@ -173,7 +175,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int pt = threadIdx.x - 32 * (kMmaWarp + 1);
       tc::mbar_wait_sleep<32>(&a_empty[s], ((it / stages) & 1) ^ 1);
       uint8_t* dstA = sA + s * a_bytes;
-      const uint64_t* base = in.p[t] + (size_t(b) * n + i0) * limbs;
+      // output positions i0 .. i0+127; their coefficients: the same (natural
+      // layout, tS = 0) or, in the column-major layout of NTT pass A (tS = S:
+      // position x 2^S + y holds coefficient y n / 2^S + x), one column's
+      // coefficients n / 2^S apart
+      const size_t cb = tS ? ((i0 & ((size_t(1) << tS) - 1)) << (LOGN_OR(log_n) - tS)) | (i0 >> tS)
+                           : i0;
+      const size_t rs = tS ? size_t(1) << (LOGN_OR(log_n) - tS) : 1;
+      const uint64_t* base = in.p[t] + (size_t(b) * n + cb) * limbs;
       const int chunks = kpad / 16;  // 16-byte chunks per row
       const int l0 = in.limb0[t], eb = in.end_bit[t];
       const bool al16 = in.aligned16[t] != 0;
@@ -181,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // 8 lanes cover 128 contiguous bytes of a row; moving 16 rows down
       // moves 2048 bytes in the swizzled tile (no index division)
       const int pw = pt >> 5, r0 = 4 * pw + (lane >> 3);
-      const uint64_t* rowp = base + size_t(r0) * limbs;
+      const uint64_t* rowp = base + size_t(r0) * rs * limbs;
+      const size_t rstride = 16 * rs * limbs;  // 16 rows down
       const uint32_t sa0 = tc::smem_addr(dstA);
       for (int c = lane & 7; c < chunks; c += 8) {
         const int l = l0 + 2 * c;
@@ -192,14 +202,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t* g = sz ? rowp + l : rowp;
 #pragma unroll
           for (int i = 0; i < kRows / 16; ++i)
-            tc::cp_async16z(dst + 2048 * i, g + size_t(16 * i) * limbs, sz);
+            tc::cp_async16z(dst + 2048 * i, g + i * rstride, sz);
         } else {
           const uint64_t* g0 = b0 ? rowp + l : rowp;
           const uint64_t* g1 = b1 ? rowp + l + 1 : rowp;
 #pragma unroll
           for (int i = 0; i < kRows / 16; ++i) {
-            tc::cp_async8z(dst + 2048 * i, g0 + size_t(16 * i) * limbs, b0);
-            tc::cp_async8z(dst + 2048 * i + 8, g1 + size_t(16 * i) * limbs, b1);
+            tc::cp_async8z(dst + 2048 * i, g0 + i * rstride, b0);
+            tc::cp_async8z(dst + 2048 * i + 8, g1 + i * rstride, b1);
           }
         }
       }
@@ -305,9 +315,10 @@ cudaError_t crt_tc_setup_attributes() {
 
 cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs, int count,
                            int limbs, size_t batch, int log_n, const DevPrime32* primes, int np,
-                           uint32_t* out, cudaStream_t st) {
+                           uint32_t* out, cudaStream_t st, int transposed_S) {
   const size_t n = size_t(1) << log_n;
   if (count < 1 || count > kMaxCrtInputs || n < size_t(kRows)) return cudaErrorInvalidValue;
+  if (transposed_S && (transposed_S < 7 || transposed_S >= log_n)) return cudaErrorInvalidValue;
   TcInputs in{};
   CrtTcTable tab = tabs[0];
   int nslots = 0;
@@ -342,7 +353,7 @@ cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs,
   const int grid = per_ct * tab.ncol_tiles;
   auto kern = log_n == 17 ? crt_tc_kernel<17> : log_n == 16 ? crt_tc_kernel<16> : crt_tc_kernel<0>;
   kern<<<grid, kThreads, smem, st>>>(in, count, static_cast<int>(batch), limbs, log_n, tab, primes,
-                                     np, out, stages, nslots);
+                                     np, out, stages, nslots, transposed_S);
   return cudaGetLastError();
 }
 

@@ -420,15 +420,18 @@ __global__ void finish_fixup_kernel(const typename F::W* __restrict__ ks,
     const size_t id = flags.ids[fi];
     const int bb = static_cast<int>(id / n);
     const size_t i = id % n;
+    // residue position of coefficient i (column-major rows: x 2^tS + y for
+    // i = y n / 2^tS + x)
+    const size_t ip = f.tS ? ((i & ((n >> f.tS) - 1)) << f.tS) | (i >> (log_n - f.tS)) : i;
     const bool is_bx = bb >= B;
     const int b = is_bx ? bb - B : bb;
     uint64_t x2[kFixMaxLimbs], x1[kFixMaxLimbs];
-    exact_centered<F>(ks + size_t(bb) * np2 * n, n, i, p2, np2, t2, T2, x2, f.t_inputs);
+    exact_centered<F>(ks + size_t(bb) * np2 * n, n, ip, p2, np2, t2, T2, x2, f.t_inputs);
     const typename F::W* d1p = (is_bx ? d_bx : d_ax) + size_t(b) * np1 * n;
-    exact_centered<F>(d1p, n, i, p1, np1, t1, f.log_q, x1, f.t_inputs);
+    exact_centered<F>(d1p, n, ip, p1, np1, t1, f.log_q, x1, f.t_inputs);
     if (f.hi_off) {  // split: x1 = c0 + 2^h c1 mod 2^logq
       uint64_t x1h[kFixMaxLimbs];
-      exact_centered<F>(d1p + f.hi_off, n, i, p1, np1, t1, f.log_q, x1h, f.t_inputs);
+      exact_centered<F>(d1p + f.hi_off, n, ip, p1, np1, t1, f.log_q, x1h, f.t_inputs);
       for (int k = 0; k < l1; ++k) add_shifted(x1, l1, f.split_h + 64 * k, x1h[k]);
       if (f.log_q % 64) x1[l1 - 1] &= (uint64_t(1) << (f.log_q % 64)) - 1;
     }

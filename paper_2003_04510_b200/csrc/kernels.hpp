@@ -23,6 +23,7 @@ cudaError_t ntt_setup_attributes();
 // [s1, logN) on blocks; inverse pass 0 = levels [s1, logN), pass 1 = levels
 // [0, s1) + n^-1. Outputs of a full transform are canonical.
 int ntt_num_passes(int log_n);
+int ntt_pass_a_levels(int log_n);  // S of pass A (split_levels s1)
 template <class F>
 cudaError_t ntt_forward_pass(int pass, typename F::W* data, size_t rows, int np, int log_n,
                              const typename F::Tw* tw, const typename F::Prime* primes,
@@ -41,6 +42,13 @@ cudaError_t build_twiddles32(const uint32_t* primes, const uint32_t* roots,
                              const uint32_t* roots_inv, int np, int log_n, Twiddle32* tw,
                              Twiddle32* itw, cudaStream_t st);
 bool ntt_col_supported(int log_n, int S);
+// Transposed forms of the column pass (S = 8, 9; out of place): forward reads
+// rows in the column-major layout (column x of a row at [x 2^S, (x+1) 2^S))
+// and writes the natural layout; inverse reads natural and writes transposed.
+bool ntt_col_transposed_supported(int log_n, int S);
+cudaError_t ntt_col_pass_transposed(bool inv, const uint32_t* in, uint32_t* out, size_t rows,
+                                    int np, int log_n, int S, const Twiddle32* tw,
+                                    const DevPrime32* primes, cudaStream_t st);
 cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
                          const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st);
 
@@ -134,7 +142,7 @@ bool crt_tc_supported(const CrtTcTable& tab);
 // at out + t * batch * np * n as canonical residues (crt_forward_multi).
 cudaError_t crt_forward_tc(const uint64_t* const* polys, const CrtTcTable* tabs, int count,
                            int limbs, size_t batch, int log_n, const DevPrime32* primes, int np,
-                           uint32_t* out, cudaStream_t st);
+                           uint32_t* out, cudaStream_t st, int transposed_S = 0);
 
 // ---- iCRT (icrt.cu) --------------------------------------------------------
 // B table for the exact reconstruction mod 2^T: (R np + 1) rows x m_pad
@@ -196,6 +204,7 @@ struct Finisher {
   int split_h = 0;
   size_t hi_off = 0;
   int t_inputs = 0;  // residues are t_j already (tensor-core path, bigint_tc.cu)
+  int tS = 0;        // residue rows column-major (BigTcOut::tS); flag ids per coefficient
 };
 cudaError_t finisher_setup_attributes();
 // ks: 2B x np2 x n (B ax-batches then B bx-batches), d_ax / d_bx: B x np1 x n
@@ -243,6 +252,10 @@ struct BigTcOut {
   uint64_t* out1 = nullptr;
   int out_limbs = 0, out_bit = 0, out_bits = 0;
   int check_amb = 0, force_exact = 0;
+  // tS > 0: the t rows are in NTT pass A's column-major layout (position
+  // x 2^tS + y holds coefficient y n / 2^tS + x); outputs and flag ids are
+  // per coefficient either way
+  int tS = 0;
   IcrtFlags flags;
 };
 cudaError_t bigint_tc_setup_attributes();

@@ -676,6 +676,12 @@ cudaError_t ntt_mid_evk(typename F::W* Fin, const typename F::W* ea, const typen
   return launch_mid_any<F, OP_EVK>(a, s2, batch * np, st);
 }
 
+int ntt_pass_a_levels(int log_n) {
+  int s1, s2;
+  split_levels(log_n, s1, s2);
+  return s1;
+}
+
 int ntt_num_passes(int log_n) {
   int s1, s2;
   split_levels(log_n, s1, s2);

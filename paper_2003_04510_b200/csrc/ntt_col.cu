@@ -76,6 +76,7 @@ __device__ __forceinline__ int padf(int y) { return y + (y >> 5); }
 
 struct ColArgs {
   uint32_t* data;
+  uint32_t* out;  // == data except in the transposed forms (out of place)
   const Twiddle32* tw;
   const DevPrime32* primes;
   int np, log_n, rows_per_prime;
@@ -305,13 +306,19 @@ __device__ __forceinline__ void half_level(uint32_t (&v)[HE], const TwF& tw, uin
   }
 }
 
-template <int S, bool INV, int L, typename ReadTw>
+// GTW: rd reads the global table in its natural order (t = 2^L + h 2^i + blk
+// at layout-L levels) instead of the shared twiddle_slot order
+template <int S, bool INV, int L, bool GTW, typename ReadTw>
 __device__ __forceinline__ void half_level_at(uint32_t (&v)[ColGeo<S>::HE], const ReadTw& rd, int h,
                                               uint32_t p2, uint32_t negp) {
   constexpr int HE = ColGeo<S>::HE, RH = ColGeo<S>::RH;
   if constexpr (L < RH) {  // layout H: r holds the top bits, twiddle uniform
     half_level<HE, RH - 1 - L, INV>(
         v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + blk, w, wq); }, p2, negp);
+  } else if constexpr (GTW) {
+    half_level<HE, S - 1 - L, INV>(
+        v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + (h << (L - 4)) + blk, w, wq); },
+        p2, negp);
   } else {  // layout L: lane-minor twiddle slots (twiddle_slot)
     half_level<HE, S - 1 - L, INV>(
         v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + blk * 16 + h, w, wq); }, p2,
@@ -319,17 +326,17 @@ __device__ __forceinline__ void half_level_at(uint32_t (&v)[ColGeo<S>::HE], cons
   }
 }
 
-template <int S, bool INV, int L0, int L1, typename ReadTw>
+template <int S, bool INV, int L0, int L1, bool GTW = false, typename ReadTw>
 __device__ __forceinline__ void half_levels(uint32_t (&v)[ColGeo<S>::HE], const ReadTw& rd, int h,
                                             uint32_t p2, uint32_t negp) {
   // forward: L0, L0+1, ..., L1-1; inverse: L1-1, ..., L0
   if constexpr (L0 < L1) {
     if constexpr (!INV) {
-      half_level_at<S, INV, L0>(v, rd, h, p2, negp);
-      half_levels<S, INV, L0 + 1, L1>(v, rd, h, p2, negp);
+      half_level_at<S, INV, L0, GTW>(v, rd, h, p2, negp);
+      half_levels<S, INV, L0 + 1, L1, GTW>(v, rd, h, p2, negp);
     } else {
-      half_level_at<S, INV, L1 - 1>(v, rd, h, p2, negp);
-      half_levels<S, INV, L0, L1 - 1>(v, rd, h, p2, negp);
+      half_level_at<S, INV, L1 - 1, GTW>(v, rd, h, p2, negp);
+      half_levels<S, INV, L0, L1 - 1, GTW>(v, rd, h, p2, negp);
     }
   }
 }
@@ -346,15 +353,28 @@ __device__ __forceinline__ void half_levels(uint32_t (&v)[ColGeo<S>::HE], const 
 // The butterflies are those of column_transform (same pairs, same lazy
 // ranges), so the outputs are identical; per residue it drops the shuffle
 // level (a shuffle, three selects and a duplicated Shoup product per lane).
-template <int S, bool INV>
+// IO = kIoShared: input and output in the shared column (the cooperative
+// copies move the tile); kIoGlobalIn (forward): the column is read straight
+// from a transposed ("column-major") global row, gcol[y], and the twiddles
+// from the global table, so the transform needs no CTA barrier before it;
+// kIoGlobalOut (inverse): the result is written straight to a transposed
+// global row. In the transposed layout column x of a row occupies
+// [x 2^S, (x+1) 2^S): a half-warp's 16 lanes at one register touch 64
+// contiguous bytes.
+enum { kIoShared = 0, kIoGlobalIn = 1, kIoGlobalOut = 2 };
+template <int S, bool INV, int IO = kIoShared>
 __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32_t* stw,
-                                                      const DevPrime32& pr, int h) {
+                                                      const DevPrime32& pr, int h,
+                                                      uint32_t* gcol = nullptr,
+                                                      const Twiddle32* gtw = nullptr) {
   using G = ColGeo<S>;
   constexpr int HE = G::HE, RH = G::RH;
   static_assert(S - RH <= RH, "layout L must hold the remaining levels");
+  constexpr bool kGTw = false;  // twiddles from shared memory in every form
   const uint32_t p = pr.p, p2 = 2 * p, negp = 0u - p;
-  const auto rd = [&](int idx, uint32_t& w, uint32_t& wq) {  // one LDS.64 per pair
-    const uint2 x = reinterpret_cast<const uint2*>(stw)[idx];
+  const auto rd = [&](int idx, uint32_t& w, uint32_t& wq) {  // one LDS.64 / LDG.64 per pair
+    const uint2 x = kGTw ? __ldg(reinterpret_cast<const uint2*>(gtw) + idx)
+                         : reinterpret_cast<const uint2*>(stw)[idx];
     w = x.x;
     wq = x.y;
   };
@@ -370,12 +390,20 @@ __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32
   auto posH = [&](int r) { return h + 16 * r; };
   auto posL = [&](int r) { return HE * h + r; };
   if (!INV) {
-    ld(posH);
-    half_levels<S, false, 0, RH>(v, rd, h, p2, negp);
+    if constexpr (IO == kIoGlobalIn) {
+      // the column's loads go out first; the barrier only waits for the
+      // CTA's twiddle fill (the loads stay in flight through it)
+#pragma unroll
+      for (int r = 0; r < HE; ++r) v[r] = gcol[posH(r)];
+      __syncthreads();
+    } else {
+      ld(posH);
+    }
+    half_levels<S, false, 0, RH, kGTw>(v, rd, h, p2, negp);
     st(posH);
     __syncwarp();
     ld(posL);
-    half_levels<S, false, RH, S>(v, rd, h, p2, negp);
+    half_levels<S, false, RH, S, kGTw>(v, rd, h, p2, negp);
     st(posL);
   } else {
     ld(posL);
@@ -391,7 +419,12 @@ __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32
       v[rr] = csub32(shoup32(u + w2, pr.ninv, pr.ninv_q, negp), p);
       v[rr + HE / 2] = csub32(shoup32(u + p2 - w2, pr.w1n, pr.w1n_q, negp), p);
     }
-    st(posH);
+    if constexpr (IO == kIoGlobalOut) {
+#pragma unroll
+      for (int r = 0; r < HE; ++r) gcol[posH(r)] = v[r];
+    } else {
+      st(posH);
+    }
   }
 }
 
@@ -422,9 +455,13 @@ struct ColCfg {
 };
 #pragma nv_diag_default 177
 
-template <int S, bool INV>
+// TR = 1 (forward, S >= 8): input rows in the transposed layout (column x at
+// [x 2^S, (x+1) 2^S), crt_tc.cu writes them so), output natural, out of place;
+// TR = 2 (inverse): input natural, output transposed (bigint_tc.cu reads it).
+template <int S, bool INV, int TR = 0>
 __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_kernel(ColArgs a) {
   constexpr int CS = ColGeo<S>::CS;
+  static_assert(TR == 0 || (ColGeo<S>::kHalf && (TR == 1) == !INV), "transposed forms");
   extern __shared__ uint32_t smem[];
   uint32_t* col = smem;                        // [kCols][CS]
   uint32_t* stw = smem + kCols * CS;           // w[2^S] then wq[2^S] (twiddle_slot order)
@@ -441,6 +478,11 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
   const size_t n = size_t(1) << a.log_n;
   const int tlast = 1 << (a.log_n - S);
   uint32_t* rowp = a.data + size_t(row) * n + size_t(blockIdx.x) * kCols;
+  uint32_t* orowp = a.out + size_t(row) * n + size_t(blockIdx.x) * kCols;
+  // transposed row of this half-warp's column (TR != 0)
+  const int mycol = warp + kWarps * (lane >> 4);
+  uint32_t* gcol = (TR == 1 ? a.data : a.out) + size_t(row) * n +
+                   (size_t(blockIdx.x) * kCols + mycol) * (size_t(1) << S);
   // ---- cooperative load: 16-byte vectors, thread -> (columns 4 (tid % 4)
   // .. +3, rows tid / 4 + 128 r) ------------------------------------------------
   {
@@ -452,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
 #define HEMUL_COL_EXP 0  // experiments: 1 = no transform, 2 = no HBM traffic
 #endif
 #pragma unroll
-    for (int r = 0; r < (1 << S) / RS; ++r) {
+    for (int r = 0; r < (TR == 1 ? 0 : (1 << S) / RS); ++r) {  // TR 1: the transform loads
       const uint4 q = HEMUL_COL_EXP == 2 ? make_uint4(tid, r, 1, 2) : src[r * step];
       const int fy = padc<S>(y0 + RS * r);
       col[x4 * CS + fy] = q.x;
@@ -474,11 +516,16 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
       }
     }
   }
-  __syncthreads();
+  if constexpr (TR != 1) __syncthreads();
   if constexpr (HEMUL_COL_EXP == 1) {
+  } else if constexpr (TR == 1) {
+    column_transform_half<S, INV, kIoGlobalIn>(col + mycol * CS, stw, pr, lane & 15, gcol);
+  } else if constexpr (TR == 2) {
+    column_transform_half<S, INV, kIoGlobalOut>(col + mycol * CS, stw, pr, lane & 15, gcol);
+    return;  // written straight to the transposed row: no store phase
   } else if constexpr (ColGeo<S>::kHalf) {
     static_assert(kCols == 2 * kWarps, "one column per half-warp");
-    column_transform_half<S, INV>(col + (warp + kWarps * (lane >> 4)) * CS, stw, pr, lane & 15);
+    column_transform_half<S, INV>(col + mycol * CS, stw, pr, lane & 15);
   } else {
     constexpr int NC = ColCfg<S, INV>::NC;
     static_assert(kCols % (kWarps * NC) == 0, "columns per warp");
@@ -490,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
   if (HEMUL_COL_EXP != 2 || a.np < 0) {
     constexpr int RS = kThreads / kTpr;
     const int x4 = 4 * (tid % kTpr), y0 = tid / kTpr;
-    uint4* dst = reinterpret_cast<uint4*>(rowp + size_t(y0) * tlast + x4);
+    uint4* dst = reinterpret_cast<uint4*>(orowp + size_t(y0) * tlast + x4);
     const size_t step = size_t(RS) * tlast / 4;
 #pragma unroll
     for (int r = 0; r < (1 << S) / RS; ++r) {
@@ -501,21 +548,21 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
   }
 }
 
-template <int S, bool INV>
+template <int S, bool INV, int TR = 0>
 cudaError_t launch_col(const ColArgs& a, size_t rows, cudaStream_t st) {
   const size_t smem = (size_t(kCols) * ColGeo<S>::CS + (size_t(2) << S)) * 4;
   if (smem > 48 * 1024) {
     static bool attr = false;
     if (!attr) {
       const cudaError_t e = cudaFuncSetAttribute(
-          ntt_col_kernel<S, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+          ntt_col_kernel<S, INV, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       attr = true;
     }
   }
   const int cols = 1 << (a.log_n - S);
   dim3 grid(static_cast<unsigned>(cols / kCols), static_cast<unsigned>(rows));
-  ntt_col_kernel<S, INV><<<grid, kThreads, smem, st>>>(a);
+  ntt_col_kernel<S, INV, TR><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -528,11 +575,29 @@ bool ntt_col_supported(int log_n, int S) {
   return S >= 7 && S <= 9 && (1 << (log_n - S)) >= kCols;
 }
 
+cudaError_t ntt_col_pass_transposed(bool inv, const uint32_t* in, uint32_t* out, size_t rows,
+                                    int np, int log_n, int S, const Twiddle32* tw,
+                                    const DevPrime32* primes, cudaStream_t st) {
+  if (!ntt_col_transposed_supported(log_n, S) || in == out) return cudaErrorInvalidValue;
+  const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
+  const ColArgs a{const_cast<uint32_t*>(in), out, tw, primes, np, log_n, rpp};
+  switch (S * 2 + (inv ? 1 : 0)) {
+    case 16: return launch_col<8, false, 1>(a, rows, st);
+    case 17: return launch_col<8, true, 2>(a, rows, st);
+    case 18: return launch_col<9, false, 1>(a, rows, st);
+    default: return launch_col<9, true, 2>(a, rows, st);
+  }
+}
+
+bool ntt_col_transposed_supported(int log_n, int S) {
+  return ntt_col_supported(log_n, S) && (S == 8 || S == 9);
+}
+
 cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
                          const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st) {
   if (!ntt_col_supported(log_n, S)) return cudaErrorInvalidValue;
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
-  const ColArgs a{data, tw, primes, np, log_n, rpp};
+  const ColArgs a{data, data, tw, primes, np, log_n, rpp};
   switch (S * 2 + (inv ? 1 : 0)) {
     case 14: return launch_col<7, false>(a, rows, st);
     case 15: return launch_col<7, true>(a, rows, st);

@@ -132,11 +132,12 @@ _SIGS.update({
 })
 HEMUL_OPT_LEVEL_CACHE = 4
 ENGINE_INFO = ("word", "np1", "np2", "split_h", "crt1_tc", "crt2_tc", "big_tc", "fused_mid",
-               "blk_mont")  # HEMUL_INFO_* in include/hemul_gpu.h
+               "blk_mont", "t_pass_a")  # HEMUL_INFO_* in include/hemul_gpu.h
 TRACE_POINTS = {"crt1": 1, "prod1": 2, "d2": 3, "crt2": 4, "prod2": 5}  # HEMUL_TRACE_*
 HEMUL_OPT_FORCE_EXACT = 1
 HEMUL_OPT_BASIS = 2
 HEMUL_OPT_TENSOR_CORES = 3
+HEMUL_OPT_TRANSPOSED = 5
 
 
 def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
@@ -610,6 +611,11 @@ class Context:
         GEMMs on the tcgen05 tensor cores (default) or on the IMAD.WIDE
         integer pipe. Bit-identical results."""
         self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_TENSOR_CORES, int(on)))
+
+    def set_transposed(self, on: bool = True) -> None:
+        """Tensor-core engine, log N >= 15: column-major RNS rows around NTT
+        pass A (HEMUL_OPT_TRANSPOSED). Bit-identical results."""
+        self._check(self._lib.hemul_gpu_set_option(self._h, HEMUL_OPT_TRANSPOSED, int(on)))
 
     def mul_basis(self, log_q: int) -> tuple[int, int, int]:
         """(word, np1, np2) of the basis he_mul uses at level log_q."""

@@ -43,13 +43,24 @@ LADDERS = [
 ]
 
 
-def _ctx(cfg, tc):
+def _ctx(cfg, tc, transposed=None):
     from paper_2003_04510_b200.hemul import Context, make_params
 
     ctx = Context(make_params(*cfg))
     ctx.set_basis(32)
     ctx.set_tensor_cores(tc)
+    if transposed is not None:
+        ctx.set_transposed(transposed)
     return ctx
+
+
+def _natural(rows, log_n, S):
+    """Column-major RNS rows (HEMUL_INFO_T_PASS_A = S: position x 2^S + y holds
+    coefficient y n / 2^S + x) back in coefficient order."""
+    if not S:
+        return rows
+    r = rows.reshape(rows.shape[0], 1 << (log_n - S), 1 << S)
+    return np.ascontiguousarray(r.transpose(0, 2, 1)).reshape(rows.shape[0], 1 << log_n)
 
 
 def _expected(ctx, info, log_q, c1, c2, evk):
@@ -99,12 +110,15 @@ def _check_rows(got, want_slots, primes, t_form):
         assert bad.size == 0, f"slot {s}: {len(bad)} residues differ, first (prime, coeff) {bad[0]}"
 
 
-@pytest.mark.parametrize("tc", [True, False], ids=["tc", "imad"])
+@pytest.mark.parametrize("tc,trn", [(True, True), (True, False), (False, False)],
+                         ids=["tc", "tc-natural", "imad"])
 @pytest.mark.parametrize("cfg,levels", LADDERS, ids=["X_logQ@N4096", "M_logQ@N4096",
                                                      "logQ600@N8192", "logQ120@N65536",
                                                      "logQ120@N131072"])
-def test_stage_checkpoints_along_the_ladder(cfg, levels, tc, restated):
-    ctx = _ctx(cfg, tc)
+def test_stage_checkpoints_along_the_ladder(cfg, levels, tc, trn, restated):
+    if not trn and tc and cfg[2] < 15:
+        pytest.skip("the layouts differ only at log N >= 15")
+    ctx = _ctx(cfg, tc, trn)
     p = ctx.params
     rng = np.random.default_rng(cfg[1] + 7 * tc)
     evk = (random_poly(rng, p.n, 2 * p.log_q_max), random_poly(rng, p.n, 2 * p.log_q_max))
@@ -120,8 +134,12 @@ def test_stage_checkpoints_along_the_ladder(cfg, levels, tc, restated):
         c2 = (random_poly(rng, p.n, log_q), random_poly(rng, p.n, log_q))
         want = _expected(ctx, info, log_q, c1, c2, evk)
         t_form = bool(info["big_tc"])
+        S = info["t_pass_a"]
+        assert bool(S) == (tc and trn and cfg[2] >= 15), info
         tr = {k: ctx.he_mul_trace(c1, c2, log_q, k, evk=evk)
               for k in ("crt1", "prod1", "d2", "crt2", "prod2")}
+        for k in ("crt1", "prod1", "crt2", "prod2"):
+            tr[k] = _natural(tr[k], p.log_n, S)
         _check_rows(tr["crt1"], want["crt1"], want["p1"], False)
         _check_rows(tr["prod1"], want["prod1"], want["p1"], t_form)
         assert np.array_equal(tr["d2"].reshape(p.n, -1), want["d2"]), log_q
