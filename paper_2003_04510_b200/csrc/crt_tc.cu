@@ -39,7 +39,10 @@ namespace hemul_gpu {
 namespace {
 
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
-constexpr int kEpiWarps = 16;        // four per TMEM lane quadrant (prime groups split); the
+#ifndef HEMUL_CRT_EPI_WARPS
+#define HEMUL_CRT_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = HEMUL_CRT_EPI_WARPS;  // four per TMEM lane quadrant (prime groups split); the
                                      // epilogue is latency bound: 8 -> 16 warps, 2.20 -> 1.93 ms
                                      // per step at X
 constexpr int kMmaWarp = kEpiWarps;  // TMEM allocation + MMA issue
