@@ -513,6 +513,15 @@ int b_stages(int n_cols) {
 }
 }  // namespace
 
+// Shapes the kernel runs: the low-block copy must fit (forcing the path
+// without it failed the M ladder at log_q = 60, n_cols = 32 — not reachable
+// while the copy fits, i.e. n_cols <= 352, every he_mul level with logQ up to
+// ~2700; larger tables take the IMAD.WIDE finisher)
+bool bigint_tc_supported(int n_cols) {
+  return n_cols % 32 == 0 && n_cols <= 480 && use_lobuf(n_cols) &&
+         bigint_tc_smem(n_cols) <= size_t(kMaxDynSmem);
+}
+
 size_t bigint_tc_smem(int n_cols) {
   return smem_for(n_cols, b_stages(n_cols), use_lobuf(n_cols));
 }
@@ -526,7 +535,7 @@ cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, in
                       const BigTcOut& o, const void* const* rmaps, cudaStream_t st) {
   const size_t n = size_t(1) << log_n;
   if (!t.btab || !rmaps || !rmaps[0] || !rmaps[1] || t.nseg < 1 || t.nseg > kMaxSeg || n < size_t(kRows) || t.n_cols % 32 ||
-      t.n_cols > 480 || t.k_bytes % kChunk || bigint_tc_smem(t.n_cols) > size_t(kMaxDynSmem))
+      !bigint_tc_supported(t.n_cols) || t.k_bytes % kChunk)
     return cudaErrorInvalidValue;
   if ((o.check_amb || o.force_exact) && !o.flags.count) return cudaErrorInvalidValue;
   if (t.k_slot > kMaxRows) return cudaErrorInvalidValue;

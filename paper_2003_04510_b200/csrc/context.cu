@@ -389,7 +389,7 @@ void make_raw_tmap(CUtensorMap* m, const uint32_t* g, uint64_t n, uint64_t rows)
 }
 
 std::unique_ptr<BigTcDev> upload_bigint(const BigTcHost& h, cudaStream_t st) {
-  if (h.n_cols > 480 || bigint_tc_smem(h.n_cols) > size_t(kMaxDynSmem)) return nullptr;
+  if (!bigint_tc_supported(h.n_cols)) return nullptr;
   auto d = std::make_unique<BigTcDev>();
   upload(d->btab, h.btab, st);
   BigTcTable& t = d->t;

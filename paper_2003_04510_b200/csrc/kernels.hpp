@@ -260,6 +260,7 @@ struct BigTcOut {
 };
 cudaError_t bigint_tc_setup_attributes();
 size_t bigint_tc_smem(int n_cols);
+bool bigint_tc_supported(int n_cols);
 // rmaps[2]: host pointers to CUtensorMaps of u32 residue arrays [rows][n]
 // (box 128 x 16, no swizzle; make_raw_tmap).
 cudaError_t bigint_tc(const BigTcTable& t, const BigTcSeg* segs, int entries, int B, int log_n,
