@@ -19,6 +19,9 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 # he_mul engines: prime basis (HEMUL_OPT_BASIS) x base-conversion engine
 # (HEMUL_OPT_TENSOR_CORES, 30-bit basis only); results must not depend on them
 BASES = ["32tc", "32imad", "64"]
+# + the tensor-core engine with natural-order pass-A rows (HEMUL_OPT_TRANSPOSED
+# off; the default lays them out column-major at log N >= 15)
+BASES_PAPER = BASES + ["32tc-natural"]
 
 
 def _word(basis) -> int:
@@ -30,7 +33,8 @@ def _ctx(cfg, basis="32tc"):
 
     ctx = Context(make_params(*cfg))
     ctx.set_basis(_word(basis))
-    ctx.set_tensor_cores(str(basis).endswith("tc"))
+    ctx.set_tensor_cores("tc" in str(basis))
+    ctx.set_transposed(not str(basis).endswith("natural"))
     return ctx
 
 
@@ -216,7 +220,7 @@ def test_basis_switch_and_counts():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("basis", BASES)
+@pytest.mark.parametrize("basis", BASES_PAPER)
 @pytest.mark.parametrize("name", ["logN14_logQ300", "logN15_logQ600", "M", "X"])
 def test_bench_protocol_digest_paper_scale(name, basis, reference):
     """Digest of he_mul on the reference's own seed-7 keys and ciphertexts
