@@ -21,6 +21,7 @@
 #include <list>
 #include <memory>
 #include <stdexcept>
+#include <utility>
 #include <string>
 #include <thread>
 #include <vector>
@@ -74,6 +75,7 @@ struct RegionDev {
   DevBuf primes, tw, itw, btab, hat, big_p, half_p;
   DevBuf primes_t;  // word 32: inverse NTT constants that output t_j (level_tables.hpp)
   DevBuf primes_m, primes_tm;  // the same, compensating Montgomery products (ntt_blk.cu)
+  DevBuf twc, itwc;  // tw / itw in the column pass's shared-slot order (column-major pass A)
   struct Crt {
     int in_bits;
     CrtWeights w;
@@ -316,6 +318,16 @@ void fill_region(RegionDev& d, const RegionHost& h, cudaStream_t st) {
     check(build_twiddles32(t, t + h.np, t + 2 * h.np, h.np, h.log_n, d.tw.as<Twiddle32>(),
                            d.itw.as<Twiddle32>(), st),
           "twiddle tables");
+    const int S = ntt_pass_a_levels(h.log_n);
+    if (ntt_col_transposed_supported(h.log_n, S)) {
+      for (auto [src, dst] : {std::pair{&d.tw, &d.twc}, std::pair{&d.itw, &d.itwc}}) {
+        if (!dst->ensure((size_t(h.np) << S) * sizeof(Twiddle32) + 16))
+          throw CudaFail(HEMUL_E_OOM, "device allocation failed");
+        check(ntt_col_slot_twiddles(src->as<Twiddle32>(), h.np, h.log_n, S, dst->as<Twiddle32>(),
+                                    st),
+              "slot twiddles");
+      }
+    }
     check(cudaStreamSynchronize(st), "twiddle tables");  // tmp is freed on return
   }
   upload(d.btab, h.btab, st);
@@ -1455,14 +1467,14 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       W* R1b = c->r1b.as<W>();
       run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_NTT_A, "NTT pass A (transposed in)", [&] {
         return ntt_col_pass_transposed(false, R1, R1b, kInSlots * B * r1.np, r1.np, log_n, S,
-                                       r1.TW<F>(), p1, c->stream);
+                                       r1.TW<F>(), r1.twc.as<const Twiddle32>(), p1, c->stream);
       });
       run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R1, "NTT mid r1", [&] {
         return ntt_mid_tensor_split(R1b, B, r1.np, log_n, r1.TW<F>(), r1.ITW<F>(), p1, c->stream);
       });
       run(c, HEMUL_STAGE_INTT, HEMUL_KCLASS_INTT_A, "iNTT pass A (transposed out)", [&] {
         return ntt_col_pass_transposed(true, R1b, R1, kOutSlots * B * r1.np, r1.np, log_n, S,
-                                       r1.ITW<F>(), r1.primes_tm.as<const DevPrime32>(),
+                                       r1.ITW<F>(), r1.itwc.as<const Twiddle32>(), r1.primes_tm.as<const DevPrime32>(),
                                        c->stream);
       });
     }
@@ -1563,7 +1575,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       W* Y1 = Y0 + r2w;
       run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_NTT_A, "NTT pass A r2 (transposed in)", [&] {
         return ntt_col_pass_transposed(false, KA, Y0, B * r2.np, r2.np, log_n, S, r2.TW<F>(),
-                                       p2, c->stream);
+                                       r2.twc.as<const Twiddle32>(), p2, c->stream);
       });
       run(c, HEMUL_STAGE_NTT, HEMUL_KCLASS_MID_R2, "NTT mid r2", [&] {
         return ntt_mid_evk<F>(Y0, EA, EB, Y0, Y1, B, r2.np, log_n, r2.TW<F>(), r2.ITW<F>(), p2,
@@ -1571,7 +1583,7 @@ void he_mul_device(hemul_gpu_ctx* c, Level& lv, int log_q, size_t batch,
       });
       run(c, HEMUL_STAGE_INTT, HEMUL_KCLASS_INTT_A, "iNTT pass A r2 (transposed out)", [&] {
         return ntt_col_pass_transposed(true, Y0, KA, 2 * B * r2.np, r2.np, log_n, S, r2.ITW<F>(),
-                                       r2.primes_tm.as<const DevPrime32>(), c->stream);
+                                       r2.itwc.as<const Twiddle32>(), r2.primes_tm.as<const DevPrime32>(), c->stream);
       });
     }
   } else if (mid) {

@@ -46,9 +46,14 @@ bool ntt_col_supported(int log_n, int S);
 // rows in the column-major layout (column x of a row at [x 2^S, (x+1) 2^S))
 // and writes the natural layout; inverse reads natural and writes transposed.
 bool ntt_col_transposed_supported(int log_n, int S);
+// twc (forward): the forward twiddles in the kernel's shared-slot order, per
+// prime 2^S pairs (ntt_col_slot_twiddles, built once per level)
 cudaError_t ntt_col_pass_transposed(bool inv, const uint32_t* in, uint32_t* out, size_t rows,
                                     int np, int log_n, int S, const Twiddle32* tw,
-                                    const DevPrime32* primes, cudaStream_t st);
+                                    const Twiddle32* twc, const DevPrime32* primes,
+                                    cudaStream_t st);
+cudaError_t ntt_col_slot_twiddles(const Twiddle32* tw, int np, int log_n, int S, Twiddle32* out,
+                                  cudaStream_t st);
 cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_n, int S,
                          const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st);
 

@@ -78,6 +78,7 @@ struct ColArgs {
   uint32_t* data;
   uint32_t* out;  // == data except in the transposed forms (out of place)
   const Twiddle32* tw;
+  const uint2* twc;  // TR != 0: per prime 2^S (w, wq) pairs in shared-slot order
   const DevPrime32* primes;
   int np, log_n, rows_per_prime;
 };
@@ -306,19 +307,13 @@ __device__ __forceinline__ void half_level(uint32_t (&v)[HE], const TwF& tw, uin
   }
 }
 
-// GTW: rd reads the global table in its natural order (t = 2^L + h 2^i + blk
-// at layout-L levels) instead of the shared twiddle_slot order
-template <int S, bool INV, int L, bool GTW, typename ReadTw>
+template <int S, bool INV, int L, typename ReadTw>
 __device__ __forceinline__ void half_level_at(uint32_t (&v)[ColGeo<S>::HE], const ReadTw& rd, int h,
                                               uint32_t p2, uint32_t negp) {
   constexpr int HE = ColGeo<S>::HE, RH = ColGeo<S>::RH;
   if constexpr (L < RH) {  // layout H: r holds the top bits, twiddle uniform
     half_level<HE, RH - 1 - L, INV>(
         v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + blk, w, wq); }, p2, negp);
-  } else if constexpr (GTW) {
-    half_level<HE, S - 1 - L, INV>(
-        v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + (h << (L - 4)) + blk, w, wq); },
-        p2, negp);
   } else {  // layout L: lane-minor twiddle slots (twiddle_slot)
     half_level<HE, S - 1 - L, INV>(
         v, [&](int blk, uint32_t& w, uint32_t& wq) { rd((1 << L) + blk * 16 + h, w, wq); }, p2,
@@ -326,17 +321,17 @@ __device__ __forceinline__ void half_level_at(uint32_t (&v)[ColGeo<S>::HE], cons
   }
 }
 
-template <int S, bool INV, int L0, int L1, bool GTW = false, typename ReadTw>
+template <int S, bool INV, int L0, int L1, typename ReadTw>
 __device__ __forceinline__ void half_levels(uint32_t (&v)[ColGeo<S>::HE], const ReadTw& rd, int h,
                                             uint32_t p2, uint32_t negp) {
   // forward: L0, L0+1, ..., L1-1; inverse: L1-1, ..., L0
   if constexpr (L0 < L1) {
     if constexpr (!INV) {
-      half_level_at<S, INV, L0, GTW>(v, rd, h, p2, negp);
-      half_levels<S, INV, L0 + 1, L1, GTW>(v, rd, h, p2, negp);
+      half_level_at<S, INV, L0>(v, rd, h, p2, negp);
+      half_levels<S, INV, L0 + 1, L1>(v, rd, h, p2, negp);
     } else {
-      half_level_at<S, INV, L1 - 1, GTW>(v, rd, h, p2, negp);
-      half_levels<S, INV, L0, L1 - 1, GTW>(v, rd, h, p2, negp);
+      half_level_at<S, INV, L1 - 1>(v, rd, h, p2, negp);
+      half_levels<S, INV, L0, L1 - 1>(v, rd, h, p2, negp);
     }
   }
 }
@@ -355,26 +350,26 @@ __device__ __forceinline__ void half_levels(uint32_t (&v)[ColGeo<S>::HE], const 
 // level (a shuffle, three selects and a duplicated Shoup product per lane).
 // IO = kIoShared: input and output in the shared column (the cooperative
 // copies move the tile); kIoGlobalIn (forward): the column is read straight
-// from a transposed ("column-major") global row, gcol[y], and the twiddles
-// from the global table, so the transform needs no CTA barrier before it;
+// from a transposed ("column-major") global row, gcol[y], and the CTA's
+// twiddle copy (a straight uint4 copy of the prime's table in shared-slot
+// order, built at level setup by ntt_col_slot_twiddles) is waited on after
+// those loads are issued, so the barrier hides behind the column's HBM
+// latency instead of preceding it (pass A forward -5..7% on B200);
 // kIoGlobalOut (inverse): the result is written straight to a transposed
 // global row. In the transposed layout column x of a row occupies
 // [x 2^S, (x+1) 2^S): a half-warp's 16 lanes at one register touch 64
-// contiguous bytes.
+// contiguous bytes, and a layout-L twiddle read is 16 consecutive pairs.
 enum { kIoShared = 0, kIoGlobalIn = 1, kIoGlobalOut = 2 };
 template <int S, bool INV, int IO = kIoShared>
 __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32_t* stw,
                                                       const DevPrime32& pr, int h,
-                                                      uint32_t* gcol = nullptr,
-                                                      const Twiddle32* gtw = nullptr) {
+                                                      uint32_t* gcol = nullptr) {
   using G = ColGeo<S>;
   constexpr int HE = G::HE, RH = G::RH;
   static_assert(S - RH <= RH, "layout L must hold the remaining levels");
-  constexpr bool kGTw = false;  // twiddles from shared memory in every form
   const uint32_t p = pr.p, p2 = 2 * p, negp = 0u - p;
-  const auto rd = [&](int idx, uint32_t& w, uint32_t& wq) {  // one LDS.64 / LDG.64 per pair
-    const uint2 x = kGTw ? __ldg(reinterpret_cast<const uint2*>(gtw) + idx)
-                         : reinterpret_cast<const uint2*>(stw)[idx];
+  const auto rd = [&](int idx, uint32_t& w, uint32_t& wq) {  // one LDS.64 per pair
+    const uint2 x = reinterpret_cast<const uint2*>(stw)[idx];
     w = x.x;
     wq = x.y;
   };
@@ -391,19 +386,17 @@ __device__ __forceinline__ void column_transform_half(uint32_t* mc, const uint32
   auto posL = [&](int r) { return HE * h + r; };
   if (!INV) {
     if constexpr (IO == kIoGlobalIn) {
-      // the column's loads go out first; the barrier only waits for the
-      // CTA's twiddle fill (the loads stay in flight through it)
 #pragma unroll
       for (int r = 0; r < HE; ++r) v[r] = gcol[posH(r)];
-      __syncthreads();
+      __syncthreads();  // the CTA's twiddle copy, overlapped with the loads above
     } else {
       ld(posH);
     }
-    half_levels<S, false, 0, RH, kGTw>(v, rd, h, p2, negp);
+    half_levels<S, false, 0, RH>(v, rd, h, p2, negp);
     st(posH);
     __syncwarp();
     ld(posL);
-    half_levels<S, false, RH, S, kGTw>(v, rd, h, p2, negp);
+    half_levels<S, false, RH, S>(v, rd, h, p2, negp);
     st(posL);
   } else {
     ld(posL);
@@ -503,7 +496,12 @@ __global__ void __launch_bounds__(kThreads, ColCfg<S, INV>::kMinBlocks) ntt_col_
       col[(x4 + 3) * CS + fy] = q.w;
     }
     const uint32_t* t2 = reinterpret_cast<const uint32_t*>(a.tw + size_t(j) * n);
-    for (int i = tid; i < 1 << S; i += kThreads) {
+    if constexpr (TR != 0) {  // slot-ordered table: a straight copy (TR 1: waited on in the transform)
+      static_assert((kCols * CS) % 4 == 0, "16-byte aligned twiddle slots");
+      const uint4* s4 = reinterpret_cast<const uint4*>(a.twc + (size_t(j) << S));
+      for (int i = tid; i < (1 << S) / 2; i += kThreads) reinterpret_cast<uint4*>(stw)[i] = s4[i];
+    }
+    for (int i = tid; i < (TR != 0 ? 0 : 1 << S); i += kThreads) {
       if constexpr (ColGeo<S>::kHalf) {
         // (w, wq) pairs interleaved; walk the slots (consecutive shared
         // words per warp) and gather the table entry each slot holds
@@ -575,12 +573,36 @@ bool ntt_col_supported(int log_n, int S) {
   return S >= 7 && S <= 9 && (1 << (log_n - S)) >= kCols;
 }
 
+namespace {
+template <int S>
+__global__ void slot_twiddles_kernel(const Twiddle32* __restrict__ tw, int log_n, int np,
+                                     Twiddle32* __restrict__ out) {
+  const int j = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (1 << S); i += gridDim.x * blockDim.x)
+    out[(size_t(j) << S) + i] = tw[(size_t(j) << log_n) + twiddle_entry<S>(i)];
+}
+}  // namespace
+
+cudaError_t ntt_col_slot_twiddles(const Twiddle32* tw, int np, int log_n, int S, Twiddle32* out,
+                                  cudaStream_t st) {
+  if (!ntt_col_transposed_supported(log_n, S) || np < 1) return cudaErrorInvalidValue;
+  const dim3 grid(2, static_cast<unsigned>(np));
+  if (S == 8)
+    slot_twiddles_kernel<8><<<grid, 256, 0, st>>>(tw, log_n, np, out);
+  else
+    slot_twiddles_kernel<9><<<grid, 256, 0, st>>>(tw, log_n, np, out);
+  return cudaGetLastError();
+}
+
 cudaError_t ntt_col_pass_transposed(bool inv, const uint32_t* in, uint32_t* out, size_t rows,
                                     int np, int log_n, int S, const Twiddle32* tw,
-                                    const DevPrime32* primes, cudaStream_t st) {
-  if (!ntt_col_transposed_supported(log_n, S) || in == out) return cudaErrorInvalidValue;
+                                    const Twiddle32* twc, const DevPrime32* primes,
+                                    cudaStream_t st) {
+  if (!ntt_col_transposed_supported(log_n, S) || in == out || !twc)
+    return cudaErrorInvalidValue;
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
-  const ColArgs a{const_cast<uint32_t*>(in), out, tw, primes, np, log_n, rpp};
+  const ColArgs a{const_cast<uint32_t*>(in), out, tw, reinterpret_cast<const uint2*>(twc), primes,
+                  np, log_n, rpp};
   switch (S * 2 + (inv ? 1 : 0)) {
     case 16: return launch_col<8, false, 1>(a, rows, st);
     case 17: return launch_col<8, true, 2>(a, rows, st);
@@ -597,7 +619,7 @@ cudaError_t ntt_col_pass(bool inv, uint32_t* data, size_t rows, int np, int log_
                          const Twiddle32* tw, const DevPrime32* primes, cudaStream_t st) {
   if (!ntt_col_supported(log_n, S)) return cudaErrorInvalidValue;
   const int rpp = rows % np ? 0 : static_cast<int>(rows / np);
-  const ColArgs a{data, data, tw, primes, np, log_n, rpp};
+  const ColArgs a{data, data, tw, nullptr, primes, np, log_n, rpp};
   switch (S * 2 + (inv ? 1 : 0)) {
     case 14: return launch_col<7, false>(a, rows, st);
     case 15: return launch_col<7, true>(a, rows, st);
