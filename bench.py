@@ -404,6 +404,9 @@ def main() -> None:
                     help="every rank on cuda:0 (exercises the multi-rank path on one GPU)")
     ap.add_argument("--chain", type=int, default=8,
                     help="device-resident chain length for the `chain` key (0 = skip)")
+    ap.add_argument("--levels", default="0.5,0.25",
+                    help="fractions of log Q at which to time device-resident batches for the "
+                         "`lower_levels` key (empty = skip)")
     ap.add_argument("--basis", type=int, default=32, choices=[32, 64],
                     help="RNS basis of he_mul (HEMUL_OPT_BASIS); results are identical")
     ap.add_argument("--engine", default="tc", choices=["tc", "imad"],
@@ -579,6 +582,37 @@ def main() -> None:
                  "note": "one H2D of every operand and one D2H of the result per chain "
                          "(hemul_gpu_ct_* handles); level LRU sized to the chain"}
 
+    # ---- throughput below the fresh modulus: device-resident batches at a few
+    # lower levels (region 2 of the 30-bit basis shrinks with the level: the
+    # key is taken mod 2^(log_q + log_Q)); same batch, same key
+    lower = []
+    if args.levels:
+        ctx.set_level_cache(2)
+        for frac in (float(x) for x in args.levels.split(",")):
+            lq = max(2 * p.log_p, int(q * frac) // p.log_p * p.log_p)
+            lc1, lc2, _ = make_inputs(n, lq, B, seed=3000 + rank)
+            lo = tuple(torch.empty((B, n, limbs(lq - p.log_p)), dtype=torch.uint64,
+                                   device="cuda") for _ in range(2))
+            ctx.warm_level(lq, evk, evk_id=1)
+
+            def lstep():
+                ctx.he_mul(lc1, lc2, lq, evk=evk, evk_id=1, out=lo)
+
+            lstep()
+            torch.cuda.synchronize()
+            barrier()
+            l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0.record(stream)
+            lsteps = max(1, min(args.steps, 5))
+            for _ in range(lsteps):
+                lstep()
+            l1.record(stream)
+            torch.cuda.synchronize()
+            lms = max_over_ranks(l0.elapsed_time(l1), device="cuda") / lsteps
+            _, lnp1, lnp2 = ctx.mul_basis(lq)
+            lower.append({"log_q": lq, "value": world * B / (lms / 1000.0), "unit": "HE Mul/s",
+                          "ms_per_step": lms, "np1": lnp1, "np2": lnp2})
+
     # ---- result digests gathered to rank 0 (after timing) ------------------
     o0 = out[0][0].cpu().numpy(), out[1][0].cpu().numpy()
     dig = ciphertext_digest(q - p.log_p, o0[0], o0[1])
@@ -677,6 +711,7 @@ def main() -> None:
                     "h2d_bytes_per_step": 4 * B * n * L * 8,
                     "d2h_bytes_per_step": 2 * B * n * Lo * 8},
             "chain": chain,
+            "lower_levels": lower,
             "roofline": roof,
             "kernels": per_class,
             "engine": "int8 tensor cores (tcgen05)" if tensor else "IMAD.WIDE integer pipe",

@@ -189,6 +189,7 @@ struct hemul_gpu_ctx {
   DevBuf in, r1, dpoly, r2, ks, outb, rescale_buf, flagbuf;
   DevBuf r1b, r2b;  // out-of-place NTT pass-A buffers of the transposed layout
   DevBuf tern_a, tern_b, tern_nz;  // mul_by_ternary scratch
+  DevBuf evk_tmp;  // the key reduced mod 2^(log_q + log_Q) (30-bit basis, evk_forms)
   void* pinned[2] = {nullptr, nullptr};  // file streaming (hemul_gpu_ct_load / _save)
   cudaEvent_t ev_pin[2] = {nullptr, nullptr};
   int force_exact = 0;  // HEMUL_OPT_FORCE_EXACT (tests the exact fix-up path)
@@ -443,6 +444,8 @@ Level& get_level(hemul_gpu_ctx* c, int log_q) {
 // Regions 1 and 2 of a level in basis `word` (64 or 32), plus the finisher
 // table when he_mul can run at this level. Throws std::runtime_error when
 // the 30-bit basis has too few primes for the ring degree.
+int evk_bits(const hemul_gpu_ctx* c, int log_q, int word);
+
 Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
   Basis& b = lv.basis[word == 64 ? 0 : 1];
   if (b.r1) return b;
@@ -451,8 +454,8 @@ Basis& get_basis(hemul_gpu_ctx* c, Level& lv, int word) {
   // the 30-bit basis splits region-1 operands in halves (h = ceil(log_q / 2))
   const int split_h = word == 32 ? split_point(log_q) : 0;
   RegionHost h1 = build_region(1, log_q, c->log_q_max, c->log_n, {log_q}, th, word, split_h);
-  RegionHost h2 =
-      build_region(2, log_q, c->log_q_max, c->log_n, {log_q, 2 * c->log_q_max}, th, word);
+  RegionHost h2 = build_region(2, log_q, c->log_q_max, c->log_n,
+                               {log_q, evk_bits(c, log_q, word)}, th, word);
   auto r1 = std::make_unique<RegionDev>();
   auto r2 = std::make_unique<RegionDev>();
   fill_region(*r1, h1, c->stream);
@@ -523,6 +526,13 @@ void ensure(DevBuf& b, size_t bytes) {
 
 int limbs_of(int bits) { return (bits + 63) / 64; }
 
+// Bits of the evk coefficients the region-2 CRT takes: the reference's full
+// 2 log_Q (w64 basis) or the key reduced mod 2^(log_q + log_Q) (30-bit basis,
+// see evk_forms and build_region).
+int evk_bits(const hemul_gpu_ctx* c, int log_q, int word) {
+  return word == 64 ? 2 * c->log_q_max : log_q + c->log_q_max;
+}
+
 // Forward NTT of `rows` rows, one launch per memory pass (only the first
 // `passes` of them when a fused middle pass follows).
 template <class F>
@@ -562,19 +572,34 @@ const uint64_t* stage_in(hemul_gpu_ctx* c, const uint64_t* p, size_t words, uint
   return scratch;
 }
 
-// Scheme::level's evk transforms (heaan.cpp:152-167): CRT of the 2 log_Q-bit
-// key polys into the region-2 primes of the he_mul basis + forward NTT,
-// kept on the device.
+// Scheme::level's evk transforms (heaan.cpp:152-167): CRT of the key polys
+// into the region-2 primes of the he_mul basis + forward NTT, kept on the
+// device. The 30-bit basis first reduces the 2 log_Q-bit key mod
+// 2^(log_q + log_Q) (poly_mod_down on the device): the key-switch product is
+// only used mod qQ, so the result is unchanged and region 2 needs
+// 2 log_q + log_Q + log_n bits instead of log_q + 2 log_Q + log_n.
 template <class F>
 void evk_forms(hemul_gpu_ctx* c, Level& lv, const RegionDev& r2, const uint64_t* a,
                const uint64_t* b) {
   using W = typename F::W;
   const size_t n = size_t(c->n);
   ensure(lv.evk_a, 2 * size_t(r2.np) * n * sizeof(W));  // [evk_ax form | evk_bx form]
-  const CrtWeights* w = r2.weights(2 * c->log_q_max);
+  const int bits = evk_bits(c, lv.log_q, sizeof(W) == 8 ? 64 : 32);
+  const CrtWeights* w = r2.weights(bits);
   W* fa = lv.evk_a.as<W>();
   W* fb = fa + size_t(r2.np) * n;
-  const int Le = limbs_of(2 * c->log_q_max);
+  const int Le = limbs_of(bits);
+  if (bits < 2 * c->log_q_max) {
+    ensure(c->evk_tmp, 2 * n * Le * 8);
+    uint64_t* ra = c->evk_tmp.as<uint64_t>();
+    uint64_t* rb = ra + n * Le;
+    run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_EPILOGUE, "evk mod_down", [&] {
+      const cudaError_t e = mod_down(a, ra, 1, c->log_n, 2 * c->log_q_max, bits, c->stream);
+      return e != cudaSuccess ? e : mod_down(b, rb, 1, c->log_n, 2 * c->log_q_max, bits, c->stream);
+    });
+    a = ra;
+    b = rb;
+  }
   run(c, HEMUL_STAGE_EXTRA, HEMUL_KCLASS_CRT, "evk CRT", [&] {
     return crt_forward<F>(a, Le, 1, c->log_n, *w, r2.P<F>(), r2.np, fa, c->stream);
   });

@@ -225,8 +225,13 @@ RegionHost build_region(int region, int log_q, int log_q_max, int log_n,
   r.split_h = h;
   // Largest |v| the iCRT must recover: region 1 carries d1 = A1 B2 + A2 B1,
   // |v| < 2 n q^2 (split: the high product sums four h-bit x h-bit
-  // products, |v| < 4 n 2^(2h)); region 2 carries d2 * evk, |v| < n q Q^2.
-  const int vbits = region == 2 ? log_q + 2 * log_q_max + log_n
+  // products, |v| < 4 n 2^(2h)); region 2 carries d2 * evk, |v| < n q Q^2
+  // with the reference's full 2 log Q-bit key (w64 basis, heaan.cpp:139-143).
+  // The 30-bit basis reduces the key mod 2^(log q + log Q) before its CRT
+  // (the product is only needed mod qQ, a power of two), so |v| < n q^2 Q
+  // and region 2 shrinks with the level.
+  const int vbits = region == 2 ? (word == 64 ? log_q + 2 * log_q_max + log_n
+                                              : 2 * log_q + log_q_max + log_n)
                                 : (h ? 2 * h + log_n + 2 : 2 * log_q + log_n + 1);
   Nat P;
   int count;

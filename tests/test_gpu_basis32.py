@@ -89,8 +89,10 @@ def _expected(ctx, info, log_q, c1, c2, evk):
     crt2 = mm.residues(d2, p2)
     plan2 = mm.NttPlan(p2, n)
     fd2 = plan2.fwd(crt2)
-    prod2 = [plan2.inv(fd2 * plan2.fwd(mm.residues(mm.poly_ints(e), p2)) % plan2.P)
-             for e in evk]
+    # the 30-bit basis takes the key mod 2^(log_q + log_Q) (context.cu evk_forms)
+    kmask = (1 << (log_q + ctx.params.log_q_max)) - 1
+    prod2 = [plan2.inv(fd2 * plan2.fwd(mm.residues([x & kmask for x in mm.poly_ints(e)], p2))
+                       % plan2.P) for e in evk]
     return {"p1": p1, "p2": p2, "crt1": crt1, "prod1": prod1, "d2": mm.ints_poly(d2, log_q),
             "crt2": crt2, "prod2": prod2}
 

@@ -5,6 +5,7 @@ test_cli.cpp:141-170 (digest identity)."""
 from __future__ import annotations
 
 import json
+import math
 from pathlib import Path
 
 import numpy as np
@@ -217,6 +218,29 @@ def test_basis_switch_and_counts():
         outs.append(ctx.he_mul((g["c1ax"], g["c1bx"]), (g["c2ax"], g["c2bx"]), q, evk=evk))
     for oa, ob in outs:
         assert np.array_equal(oa, g["outax"]) and np.array_equal(ob, g["outbx"])
+
+
+def test_region2_shrinks_with_level():
+    """The 30-bit basis takes the evk mod 2^(log_q + log_Q) before its CRT
+    (context.cu evk_forms), so region 2 covers |d2 evk| < n q^2 Q plus the
+    iCRT headroom and shrinks with the level; the w64 basis keeps the
+    reference's rule (log_q + 2 log_Q + log_n, heaan.cpp:139-143)."""
+    ctx = _ctx((30, 4, 13), 32)
+    log_qm, log_n = ctx.params.log_q_max, ctx.params.log_n
+    prev = None
+    for q in (log_qm, log_qm - 30, log_qm - 60):
+        p2 = [int(x) for x in ctx.level_primes(q, -2)]
+        bits = math.prod(p2).bit_length()
+        vbits = 2 * q + log_qm + log_n
+        assert bits - 2 - vbits >= 4                              # iCRT headroom
+        assert math.prod(p2[:-1]).bit_length() - 2 - vbits < 4   # and no more primes
+        if prev is not None:
+            assert len(p2) < prev
+        prev = len(p2)
+    ctx.set_basis(64)
+    q = log_qm - 60
+    p2 = [int(x) for x in ctx.level_primes(q, -2)]
+    assert math.prod(p2).bit_length() > q + 2 * log_qm + log_n
 
 
 @pytest.mark.slow
