@@ -63,6 +63,7 @@ namespace {
 
 #ifndef HEMUL_BIG_ABL
 #define HEMUL_BIG_ABL 0  // ablation experiments (tools/run_variants.sh); 0 in production
+// (1: B chunks loaded once, 2: A stages never written, 3: MMAs not waiting for the A hand-off)
 #endif
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
 constexpr int kChunk = 64;           // K bytes per pipeline chunk (2 MMA k-steps)
@@ -258,7 +259,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           dhi = tmem + bh * NH;
         }
         const int sa = q & 1;
+#if HEMUL_BIG_ABL == 3  // ablation: MMAs decoupled from the A hand-off (wrong results)
+        tc::mbar_wait(&b_full[sb], (q / nsb) & 1);
+#else
         tc::mbar_wait(&a_full[sa], (q >> 1) & 1);  // the producers saw b_full too
+#endif
         tc::fence_after();
         const uint64_t bd = bdesc0 + uint64_t(uint32_t(sb) * b_step);
         const uint32_t a0 = tmem + kACol + sa * kSlots;
@@ -314,8 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         F0 += sg == 0 ? f : 0u;
         F1 += sg == 1 ? f : 0u;
         F2 += sg == 2 ? f : 0u;
+#if HEMUL_BIG_ABL != 3
         tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
         tc::mbar_wait_sleep<32>(&b_full[q % nsb], (q / nsb) & 1);
+#endif
         tc::fence_after();
 #if HEMUL_BIG_ABL != 2  // ablation 2: A stages never written (wrong results)
         tc::tmem_st16(a_st, t);
@@ -345,8 +352,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           k[sg] = sg < P.nseg ? (tot + (1u << 22)) >> 23 : 0u;
         }
         tc::mbar_arrive(&f_free[xb]);
+#if HEMUL_BIG_ABL != 3
         tc::mbar_wait_sleep<32>(&a_empty[quad], ((q >> 1) & 1) ^ 1);
         tc::mbar_wait_sleep<32>(&b_full[q % nsb], (q / nsb) & 1);
+#endif
         tc::fence_after();
         // K bytes 2s, 2s+1 = k_s (< 2^16), byte 6 = 1 (the constant row)
         tmem_st2(a_st, k[0] | k[1] << 16, k[2] | 1u << 16);
