@@ -24,6 +24,7 @@
 #include <type_traits>
 
 #include "fields.cuh"
+#include "igemm.cuh"
 #include "kernels.hpp"
 
 namespace hemul_gpu {
@@ -384,6 +385,14 @@ __device__ __forceinline__ void inv8(uint32_t (&v)[8], const BlkTw8& T, uint32_t
 #ifndef HEMUL_BLK_MINB_R2
 #define HEMUL_BLK_MINB_R2 8
 #endif
+// S = 8 key-switch pass: the lane's evk words are copied to shared memory by
+// cp.async when the warp starts, so their L2 latency hides behind the forward
+// levels of F instead of stalling the products (the pass's top stall was
+// long_scoreboard)
+#ifndef HEMUL_BLK_EVK_PREFETCH
+#define HEMUL_BLK_EVK_PREFETCH 1
+#endif
+constexpr int kEvkStage = HEMUL_BLK_EVK_PREFETCH ? 2 * 256 : 0;  // words per warp (S = 8)
 template <int S, int OP>
 __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R1 : HEMUL_BLK_MINB_R2)
     ntt_blk_kernel(BlkArgs a) {
@@ -393,7 +402,8 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
   constexpr int NSLOT = (S == 8 && OP == kEvk) ? 1 : (NIN > NOUT ? NIN : NOUT);
   extern __shared__ uint32_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* slots = smem + warp * NSLOT * BS;
+  constexpr int EVS = (S == 8 && OP == kEvk) ? kEvkStage : 0;
+  uint32_t* slots = smem + warp * (NSLOT * BS + EVS);
   const int j = blockIdx.y / a.rows_per_prime;
   const int bt = blockIdx.y - j * a.rows_per_prime;
   const DevPrime32& pr = a.primes[j];
@@ -413,17 +423,47 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
     // y = 8 lane + rl(r), then the inverse levels of each product from L';
     // one scratch slot per warp (the H <-> M exchange)
     uint32_t v[EPT], pb[EPT];
+    const size_t eb0 = size_t(j) * n + (size_t(block) << S) + EPT * lane;
+    uint32_t* ev = slots + NSLOT * BS + EPT * lane;  // [2][256] (HEMUL_BLK_EVK_PREFETCH)
+    if constexpr (EVS > 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        cp_async16(ev + 256 * h, a.evk[h] + eb0);
+        cp_async16(ev + 256 * h + 4, a.evk[h] + eb0 + 4);
+      }
+      cp_async_commit();
+    }
 #pragma unroll
     for (int r = 0; r < EPT; ++r) v[r] = a.in[0][off + 32 * r];
     fwd8(v, T, slots, lane, p2, negp);
-    const size_t eb0 = size_t(j) * n + (size_t(block) << S) + EPT * lane;
+    if constexpr (EVS > 0) cp_async_wait<0>();  // this lane's own words: no barrier
+    // f in [0, 4p); the evk forms are full forward transforms, canonical
+    // (kernels.hpp), so f evk < 4 p^2 < p 2^32
+    if constexpr (EVS > 0) {
+      // the lane's 8 words of each key row as two 16-byte loads (2-way bank
+      // conflicts instead of 8-way scalar ones), evk_b first so that F is
+      // overwritten last
+      uint32_t e[EPT];
+      auto ld8 = [&](const uint32_t* src) {
+        const uint4 x0 = *reinterpret_cast<const uint4*>(src);
+        const uint4 x1 = *reinterpret_cast<const uint4*>(src + 4);
+        e[0] = x0.x, e[1] = x0.y, e[2] = x0.z, e[3] = x0.w;
+        e[4] = x1.x, e[5] = x1.y, e[6] = x1.z, e[7] = x1.w;
+      };
+      static_assert(EPT == 8, "S = 8");
+      ld8(ev + 256);
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      // f in [0, 4p); the evk forms are full forward transforms, canonical
-      // (kernels.hpp), so f evk < 4 p^2 < p 2^32
-      const uint32_t f = v[r];
-      v[r] = F32::mul_mont(f, __ldg(a.evk[0] + eb0 + rl(r)), pr);
-      pb[r] = F32::mul_mont(f, __ldg(a.evk[1] + eb0 + rl(r)), pr);
+      for (int r = 0; r < EPT; ++r) pb[r] = F32::mul_mont(v[r], e[rl(r)], pr);
+      ld8(ev);
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) v[r] = F32::mul_mont(v[r], e[rl(r)], pr);
+    } else {
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const uint32_t f = v[r];
+        v[r] = F32::mul_mont(f, __ldg(a.evk[0] + eb0 + rl(r)), pr);
+        pb[r] = F32::mul_mont(f, __ldg(a.evk[1] + eb0 + rl(r)), pr);
+      }
     }
     T.load(a.itw + size_t(j) * n, gbase, lane);
     inv8(v, T, slots, lane, p2, negp);
@@ -494,7 +534,8 @@ __global__ void __launch_bounds__(32 * kWarps, OP == kTensor2 ? HEMUL_BLK_MINB_R
 template <int S, int OP>
 cudaError_t launch_blk(const BlkArgs& a, size_t rows, cudaStream_t st) {
   constexpr int NSLOT = OP == kTensor2 ? 8 : (S == 8 ? 1 : 2);
-  const size_t smem = size_t(kWarps) * NSLOT * BlkGeo<S>::BS * 4;
+  constexpr int EVS = (S == 8 && OP == kEvk) ? kEvkStage : 0;
+  const size_t smem = size_t(kWarps) * (NSLOT * BlkGeo<S>::BS + EVS) * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(ntt_blk_kernel<S, OP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
