@@ -64,7 +64,8 @@ namespace {
 #ifndef HEMUL_BIG_ABL
 #define HEMUL_BIG_ABL 0  // ablation experiments (tools/run_variants.sh); 0 in production
 // (1: B chunks loaded once, 2: A stages never written,
-// 4: epilogue without the carry pass and the stores, 5: carry pass without the limb stores)
+// 4: epilogue without the carry pass and the stores, 5: carry pass without the limb stores,
+// 6: the high block's TMEM reads without the carry pass)
 // (1: B chunks loaded once, 2: A stages never written, 3: MMAs not waiting for the A hand-off)
 #endif
 constexpr int kRows = 128;           // coefficients per tile (TMEM lanes)
@@ -475,6 +476,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           lo_held = false;
         }
       };
+#if HEMUL_BIG_ABL == 6  // ablation: the high block's TMEM reads only (wrong results)
+      {
+        uint32_t acc = 0;
+        for (int col = NH; col < N; col += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(ahi + col, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int d = 0; d < 16; ++d) acc ^= v[d];
+        }
+        dst[0] = acc;
+        tc::fence_before();
+        if (lo_held) tc::mbar_arrive(&blk_free[bl]);
+        tc::mbar_arrive(&blk_free[bh]);
+        continue;
+      }
+#endif
 #if HEMUL_BIG_ABL == 4  // ablation: no carry pass / output (wrong results)
       if (lo_held) {
         uint32_t v[16];
